@@ -1,0 +1,156 @@
+/* C-ABI of the B200-native TR-ALS hot path (libtrals.so).
+ *
+ * Conventions (all entry points):
+ *   - plain extern "C"; no torch or C++ types cross this boundary;
+ *   - every pointer argument named d_* is a caller-owned DEVICE buffer,
+ *     h_* is host memory;
+ *   - every call takes the CUDA stream (cudaStream_t passed as void*) and is
+ *     asynchronous: nothing synchronises the device or allocates memory
+ *     inside a call (workspace is caller-provided, sized by the matching
+ *     *_ws_elems query);
+ *   - every call returns an int status (TRALS_OK or an error code, see
+ *     trals_strerror); numerical failures detected on the device are reported
+ *     through a caller-provided device int array (d_info), never by a sync;
+ *   - results are deterministic (fixed reduction orders), so replicas on
+ *     several GPUs stay bitwise identical.
+ *
+ * Cores are ring cores G_n of shape (R_n, I_n, R_{n+1}) (reference ring.py:1-24).
+ * Three device layouts are used (TRALS_LAYOUT_*):
+ *   C     : [r_n][i][r_{n+1}]   the reference's C-order array
+ *   SLICE : [i][r_n][r_{n+1}]   lateral slices G_n(i) contiguous
+ *   ZT    : [i][r_{n+1}][r_n]   = classical 2-unfolding Z[i, r_n + R_n r_{n+1}]
+ *                               (tensor_ops.py:100-108), the solve's output
+ *
+ * Each entry point cites the reference code it replaces.
+ */
+#ifndef TRALS_H
+#define TRALS_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  TRALS_OK = 0,
+  TRALS_ERR_ARG = 1,         /* bad shape / stride / pointer */
+  TRALS_ERR_CUDA = 2,        /* kernel launch failed */
+  TRALS_ERR_WORKSPACE = 3,   /* caller workspace too small */
+  TRALS_ERR_UNSUPPORTED = 4  /* size outside the kernels' envelope */
+};
+
+enum { TRALS_LAYOUT_C = 0, TRALS_LAYOUT_SLICE = 1, TRALS_LAYOUT_ZT = 2 };
+
+/* d_info slots written by the solve kernels (int32 each, 0 = no event) */
+enum {
+  TRALS_INFO_CHOL = 0,       /* 1-based index of first non-positive pivot */
+  TRALS_INFO_ASYM = 1,       /* 1 if |S - S^T| > 1e-8 max|S| (linalg.py:70-72) */
+  TRALS_INFO_DEGEN = 2,      /* 1-based index of diag <= 1e-13 max|R| (linalg.py:96-99) */
+  TRALS_INFO_SLOTS = 4
+};
+
+const char* trals_strerror(int code);
+int trals_version(void);
+
+/* Generic strided fp64 contraction on the DMMA pipe (the engine behind every
+ * entry point below):  C[p][m][n] (+)= sum_k A(p,m,k) * B[k*ldb + n],
+ * A(p,m,k) = d_A[p*sAp + m*sAm + k*sAk] with sAk == 1 or sAm == 1,
+ * C address = p*cmap[0] + (m/cmap[1])*cmap[2] + (m%cmap[1])*cmap[3]
+ *                       + (n/cmap[4])*cmap[5] + (n%cmap[4])*cmap[6].
+ * Replaces the numpy matmul / tensordot / einsum calls on the path
+ * (solvers.py:379, ring.py:129,188, tensor_ops.py:161,225). */
+int64_t trals_gemm_ws_elems(int64_t P, int64_t M, int64_t K, int64_t N);
+int trals_gemm_f64(const double* d_A, int64_t sAp, int64_t sAm, int64_t sAk,
+                   int64_t P, int64_t M, int64_t K, int64_t N,
+                   const double* d_B, int64_t ldb, double* d_C, const int64_t* h_cmap, int beta,
+                   double* d_ws, int64_t ws_elems, void* stream);
+
+/* Core layout moves (tensor_ops.py:52-119 classical fold/unfold of a core). */
+int trals_core_relayout_f64(const double* d_src, int src_layout, int Ra, int64_t I, int Rb,
+                            double* d_dst, int dst_layout, void* stream);
+
+/* Half chain H[i_u..i_v][r_u][r_{v+1}] = G_u(i_u) ... G_v(i_v) of a contiguous
+ * block of cores (ring.py:110-152 subchain_merge/skip restricted to a block).
+ * d_cores_c[j] = core u+j in layout C, d_first_slice = core u in layout SLICE.
+ * d_tmp must hold the largest intermediate chain (trals_half_chain_tmp_elems). */
+int64_t trals_half_chain_tmp_elems(int nblk, const int64_t* dims, const int32_t* ranks);
+int trals_half_chain_f64(int nblk, const int64_t* dims, const int32_t* ranks,
+                         const double* d_first_slice, const double* const* h_cores_c,
+                         double* d_out, double* d_tmp, double* d_ws, int64_t ws_elems, void* stream);
+
+/* Environment of the prefix/suffix segment complementary to a half chain
+ * (the X_[n] * G^{!=n}_[2] product of solvers.py:379 restricted to the
+ * modes of the half chain).  X is C-contiguous and viewed as [pre][post].
+ *  side = 0: half chain covers the suffix (post);  Env[r_0][pre][r_y]
+ *  side = 1: half chain covers the prefix (pre);   Env[r_x][post][r_0]
+ * r_lo/r_hi are the chain's outer bonds (left, right).  leaf != 0: the
+ * segment is a single mode and the result is written as M_n directly. */
+int trals_env_f64(const double* d_X, int64_t pre, int64_t post, int side,
+                  const double* d_H, int r_lo, int r_hi, double* d_env, int leaf,
+                  double* d_ws, int64_t ws_elems, void* stream);
+
+/* Absorb the rightmost / leftmost core of an environment segment.
+ * Env layout [r_a][i_a .. i_b][r_{b+1}].
+ *   right: Out[r_a][pre][r_b]       = sum E[r_a][pre][i_b][r_{b+1}] G_b[r_b,i_b,r_{b+1}]
+ *          (d_core in layout ZT)
+ *   left : Out[r_{a+1}][rest][r_{b+1}] = sum E[r_a][i_a][rest][r_{b+1}] G_a[r_a,i_a,r_{a+1}]
+ *          (d_core in layout C)
+ * leaf != 0 writes the single-mode result directly as M_n (I_n x R_n R_{n+1},
+ * column r_n + R_n r_{n+1}), the layout of solvers.py:379's product. */
+int trals_absorb_right_f64(const double* d_env, int Ra, int64_t pre, int64_t Ib, int Rb, int Rb1,
+                           const double* d_core_zt, double* d_out, int leaf,
+                           double* d_ws, int64_t ws_elems, void* stream);
+int trals_absorb_left_f64(const double* d_env, int Ra, int64_t Ia, int64_t rest, int Ra1, int Rb1,
+                          const double* d_core_c, double* d_out, int leaf,
+                          double* d_ws, int64_t ws_elems, void* stream);
+
+/* Bond Gram of one core as a transfer matrix
+ * E[(a,c)][(b,d)] = sum_i G[a,i,b] G[c,i,d]  (ring.py:173-188, Alg. 2 line 2). */
+int trals_core_gram_f64(const double* d_core_slice, int Ra, int64_t I, int Rb, double* d_E,
+                        double* d_ws, int64_t ws_elems, void* stream);
+
+/* Coefficient Gram S_n = (G^{!=n}_[2])^T G^{!=n}_[2] from the chain of transfer
+ * matrices (ring.py:191-214 gram_chain(_order), Prop. 3).  h_E[j] = transfer
+ * matrix of core j; d_tmp holds two R^2 x R^2 buffers. */
+int trals_gram_chain_f64(int N, int n, const int32_t* ranks, const double* const* h_E,
+                         double* d_S, double* d_tmp, double* d_ws, int64_t ws_elems, void* stream);
+
+/* spd_solve (linalg.py:55-81): symmetry check + symmetrise + upper Cholesky
+ * S = U^T U.  Writes U (upper, row-major) and L = U^T (row-major) into d_U,
+ * d_L.  Pivot failures go to d_info[TRALS_INFO_CHOL]; with check_degen the
+ * 1e-13 triangular floor of tri_solve_right (linalg.py:96-99) is evaluated on
+ * U and reported in d_info[TRALS_INFO_DEGEN]. */
+int trals_cholesky_f64(const double* d_S, int m, double* d_U, double* d_L, int check_degen,
+                       int* d_info, void* stream);
+
+/* Z S = M with S = U^T U: Y U = M then Z U^T = Y, row-parallel
+ * (scipy cho_solve / solve_triangular, linalg.py:76,100). */
+int trals_chol_solve_f64(const double* d_U, const double* d_L, int m, const double* d_M,
+                         int64_t rows, double* d_Z, void* stream);
+
+/* Sum of squares of n doubles into d_out[0] (tensor_ops.py:237-239 norm). */
+int64_t trals_sumsq_ws_elems(void);
+int trals_sumsq_f64(const double* d_x, int64_t n, double* d_out, double* d_ws, void* stream);
+
+/* Relative error from sweep intermediates (solvers.py:177-212):
+ * d_out[0] = sqrt(max(0, |X|^2 - 2<M,Z> + <S, Z^T Z>)) / |X|,
+ * d_out[1] = <M,Z>, d_out[2] = <S, Z^T Z>.  d_xnorm2 = |X|^2 on the device. */
+int64_t trals_error_ws_elems(int64_t rows, int m);
+int trals_error_terms_f64(const double* d_M, const double* d_Z, const double* d_S, int64_t rows, int m,
+                          const double* d_xnorm2, double* d_out, double* d_ws, int64_t ws_elems,
+                          void* stream);
+
+/* Stateless convenience: M_n = X_[n] G^{!=n}_[2] for one mode, the exact
+ * drop-in for solvers.py:375+379 (`cyclic_unfold(x, n) @ a`).  Cores in
+ * layout C (h_cores_c) and SLICE (h_cores_s); never materialises the
+ * (prod_{j!=n} I_j) x R_n R_{n+1} subchain. */
+int64_t trals_mttsp_ws_elems(int N, const int64_t* dims, const int32_t* ranks, int n);
+int trals_mttsp_f64(const double* d_X, int N, const int64_t* dims, const int32_t* ranks, int n,
+                    const double* const* h_cores_c, const double* const* h_cores_s,
+                    const double* const* h_cores_zt, double* d_M, double* d_ws, int64_t ws_elems,
+                    void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TRALS_H */

@@ -1,0 +1,931 @@
+// libtrals: B200-native kernels + C-ABI for the TR-ALS NE / QR / QRNE sweep.
+// See include/trals.h for the contract and DESIGN.md for the data layout.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <vector>
+
+#include "../../include/trals.h"
+#include "dmma_gemm.cuh"
+
+using trals::CMap;
+using trals::GemmArgs;
+
+namespace {
+
+constexpr int kSMs = 148;
+
+inline int launch_status() {
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? TRALS_OK : TRALS_ERR_CUDA;
+}
+
+// ---------------------------------------------------------------------------
+// GEMM dispatch
+// ---------------------------------------------------------------------------
+struct Cfg {
+  int BM, BN;
+  int id;
+};
+// (WM, WN, TM, TN): 128x64, 128x80, 128x32, 128x24, 128x16, 128x8, 64x112
+constexpr Cfg kCfgs[] = {{128, 64, 0}, {128, 80, 1}, {128, 32, 2}, {128, 24, 3},
+                         {128, 16, 4}, {128, 8, 5},  {64, 112, 6}};
+
+Cfg pick_cfg(int64_t N) {
+  Cfg best = kCfgs[0];
+  double best_score = -1;
+  for (const Cfg& c : kCfgs) {
+    const int64_t nt = (N + c.BN - 1) / c.BN;
+    const double eff = static_cast<double>(N) / static_cast<double>(nt * c.BN);
+    // favour wide tiles (fewer re-reads of A) once padding waste is similar
+    const double score = eff + 0.002 * c.BN;
+    if (score > best_score + 1e-12) {
+      best_score = score;
+      best = c;
+    }
+  }
+  return best;
+}
+
+struct SplitPlan {
+  int splits;
+  int64_t kchunk;
+};
+
+SplitPlan plan_split(const Cfg& c, int64_t P, int64_t M, int64_t K, int64_t N) {
+  const int64_t tiles = P * ((M + c.BM - 1) / c.BM) * ((N + c.BN - 1) / c.BN);
+  const int64_t target = 2 * kSMs;
+  int64_t splits = 1;
+  if (tiles < target) {
+    splits = (target + tiles - 1) / tiles;
+    const int64_t max_by_k = std::max<int64_t>(1, K / (8 * trals::kBK));  // >= 128 of K per split
+    splits = std::min(splits, max_by_k);
+    splits = std::min<int64_t>(splits, 64);
+  }
+  int64_t kchunk = (K + splits - 1) / splits;
+  kchunk = ((kchunk + trals::kBK - 1) / trals::kBK) * trals::kBK;
+  if (kchunk <= 0) kchunk = trals::kBK;
+  splits = std::max<int64_t>(1, (K + kchunk - 1) / kchunk);
+  return {static_cast<int>(splits), kchunk};
+}
+
+template <int WM, int WN, int TM, int TN, bool AK, int VEC>
+int launch_tile(const GemmArgs& g, cudaStream_t s) {
+  using T = trals::Tile<WM, WN, TM, TN, AK, VEC>;
+  auto kern = trals::dmma_gemm_kernel<WM, WN, TM, TN, AK, VEC>;
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(T::kSmemBytes));
+    attr_done = true;
+  }
+  const int64_t mtiles = (g.M + T::BM - 1) / T::BM;
+  dim3 grid(static_cast<unsigned>((g.N + T::BN - 1) / T::BN), static_cast<unsigned>(g.P * mtiles),
+            static_cast<unsigned>(g.splits));
+  if (grid.y > 65535u || grid.x > 65535u) return TRALS_ERR_UNSUPPORTED;
+  kern<<<grid, T::kThreads, T::kSmemBytes, s>>>(g);
+  return launch_status();
+}
+
+template <bool AK, int VEC>
+int launch_cfg(int id, const GemmArgs& g, cudaStream_t s) {
+  switch (id) {
+    case 0: return launch_tile<4, 2, 4, 4, AK, VEC>(g, s);
+    case 1: return launch_tile<4, 2, 4, 5, AK, VEC>(g, s);
+    case 2: return launch_tile<8, 1, 2, 4, AK, VEC>(g, s);
+    case 3: return launch_tile<8, 1, 2, 3, AK, VEC>(g, s);
+    case 4: return launch_tile<8, 1, 2, 2, AK, VEC>(g, s);
+    case 5: return launch_tile<8, 1, 2, 1, AK, VEC>(g, s);
+    case 6: return launch_tile<4, 2, 2, 7, AK, VEC>(g, s);
+  }
+  return TRALS_ERR_ARG;
+}
+
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+int gemm(const double* A, int64_t sAp, int64_t sAm, int64_t sAk, int64_t P, int64_t M, int64_t K, int64_t N,
+         const double* B, int64_t ldb, double* C, const CMap& cm, int beta, double* ws, int64_t ws_elems,
+         cudaStream_t s) {
+  if (P <= 0 || M <= 0 || N <= 0) return TRALS_OK;
+  if (!A || !B || !C) return TRALS_ERR_ARG;
+  const bool ak = (sAk == 1);
+  if (!ak && sAm != 1) return TRALS_ERR_ARG;
+  if (cm.M2 <= 0 || cm.N2 <= 0) return TRALS_ERR_ARG;
+  if (K <= 0) {
+    // empty contraction: C = 0 (or unchanged when accumulating)
+    if (beta) return TRALS_OK;
+    return TRALS_ERR_ARG;
+  }
+  const Cfg c = pick_cfg(N);
+  SplitPlan sp = plan_split(c, P, M, K, N);
+  if (sp.splits > 1) {
+    const int64_t need = static_cast<int64_t>(sp.splits) * P * M * N;
+    if (!ws || need > ws_elems) {
+      // fall back to fewer splits that fit the workspace
+      int64_t fit = ws ? ws_elems / (P * M * N) : 1;
+      if (fit < 2) {
+        sp.splits = 1;
+        sp.kchunk = ((K + trals::kBK - 1) / trals::kBK) * trals::kBK;
+      } else {
+        int64_t kchunk = (K + fit - 1) / fit;
+        kchunk = ((kchunk + trals::kBK - 1) / trals::kBK) * trals::kBK;
+        sp.kchunk = kchunk;
+        sp.splits = static_cast<int>((K + kchunk - 1) / kchunk);
+      }
+    }
+  }
+  GemmArgs g;
+  g.A = A; g.sAp = sAp; g.sAm = sAm; g.sAk = sAk;
+  g.B = B; g.ldb = ldb; g.C = C; g.cmap = cm;
+  g.P = P; g.M = M; g.K = K; g.N = N; g.beta = beta;
+  g.kchunk = sp.kchunk; g.splits = sp.splits; g.ws = ws;
+  // 16-byte vector loads need every row start 16-byte aligned
+  const int64_t sA_lead = ak ? sAm : sAk;
+  const bool vec2 = aligned16(A) && aligned16(B) && (sA_lead % 2 == 0) && (P == 1 || sAp % 2 == 0) &&
+                    (ldb % 2 == 0);
+  int st;
+  if (ak) st = vec2 ? launch_cfg<true, 2>(c.id, g, s) : launch_cfg<true, 1>(c.id, g, s);
+  else st = vec2 ? launch_cfg<false, 2>(c.id, g, s) : launch_cfg<false, 1>(c.id, g, s);
+  if (st != TRALS_OK) return st;
+  if (sp.splits > 1) {
+    const int64_t total = P * M * N;
+    const int threads = 256;
+    const int blocks = static_cast<int>(std::min<int64_t>((total + threads - 1) / threads, 8 * kSMs));
+    trals::splitk_reduce_kernel<<<blocks, threads, 0, s>>>(g);
+    return launch_status();
+  }
+  return TRALS_OK;
+}
+
+int64_t gemm_ws(int64_t P, int64_t M, int64_t K, int64_t N) {
+  const Cfg c = pick_cfg(N);
+  const SplitPlan sp = plan_split(c, P, M, K, N);
+  return sp.splits > 1 ? static_cast<int64_t>(sp.splits) * P * M * N : 0;
+}
+
+inline CMap rowmajor(int64_t ldc) { return CMap{0, 1 << 30, 0, ldc, 1 << 30, 0, 1}; }
+
+// ---------------------------------------------------------------------------
+// small kernels
+// ---------------------------------------------------------------------------
+// index of core element (a, i, b) in each layout
+__device__ __forceinline__ int64_t core_index(int layout, int64_t a, int64_t i, int64_t b, int Ra, int64_t I,
+                                              int Rb) {
+  if (layout == TRALS_LAYOUT_C) return (a * I + i) * Rb + b;
+  if (layout == TRALS_LAYOUT_SLICE) return (i * Ra + a) * Rb + b;
+  return (i * Rb + b) * Ra + a;  // ZT
+}
+
+__global__ void relayout_kernel(const double* __restrict__ src, int sl, int Ra, int64_t I, int Rb,
+                                double* __restrict__ dst, int dl) {
+  const int64_t total = static_cast<int64_t>(Ra) * I * Rb;
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    // t enumerates the destination in its own order
+    int64_t a, i, b;
+    if (dl == TRALS_LAYOUT_C) { b = t % Rb; i = (t / Rb) % I; a = t / (Rb * I); }
+    else if (dl == TRALS_LAYOUT_SLICE) { b = t % Rb; a = (t / Rb) % Ra; i = t / (static_cast<int64_t>(Rb) * Ra); }
+    else { a = t % Ra; b = (t / Ra) % Rb; i = t / (static_cast<int64_t>(Ra) * Rb); }
+    dst[t] = src[core_index(sl, a, i, b, Ra, I, Rb)];
+  }
+}
+
+constexpr int kSumsqBlocks = 4 * kSMs;  // fixed -> deterministic summation tree
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <int NT>
+__device__ __forceinline__ double block_sum(double v, double* red) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (w == 0) {
+    r = (l < NT / 32) ? red[l] : 0.0;
+    r = warp_sum(r);
+  }
+  __syncthreads();
+  return r;  // valid in warp 0
+}
+
+__global__ void __launch_bounds__(512) sumsq_partial_kernel(const double* __restrict__ x, int64_t n,
+                                                            double* __restrict__ part) {
+  __shared__ double red[16];
+  double acc = 0.0;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if ((reinterpret_cast<uintptr_t>(x) & 15u) == 0) {
+    const double2* x2 = reinterpret_cast<const double2*>(x);
+    const int64_t n2 = n / 2;
+    for (int64_t j = i; j < n2; j += stride) {
+      const double2 v = __ldg(x2 + j);
+      acc = fma(v.x, v.x, acc);
+      acc = fma(v.y, v.y, acc);
+    }
+    if (i == 0 && (n & 1)) acc = fma(x[n - 1], x[n - 1], acc);
+  } else {
+    for (int64_t j = i; j < n; j += stride) acc = fma(x[j], x[j], acc);
+  }
+  const double s = block_sum<512>(acc, red);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+__global__ void __launch_bounds__(1024) sum_final_kernel(const double* __restrict__ part, int np,
+                                                         double* __restrict__ out) {
+  __shared__ double red[32];
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < np; i += blockDim.x) acc += part[i];
+  const double s = block_sum<1024>(acc, red);
+  if (threadIdx.x == 0) out[0] = s;
+}
+
+// ---------------------------------------------------------------------------
+// Cholesky (single CTA; S in L2-resident global memory; DMMA trailing update)
+// ---------------------------------------------------------------------------
+constexpr int kCholNB = 32;       // panel width
+constexpr int kCholThreads = 512;
+
+__global__ void __launch_bounds__(kCholThreads) cholesky_kernel(const double* __restrict__ S, int m,
+                                                                double* __restrict__ U, double* __restrict__ L,
+                                                                int check_degen, int* __restrict__ info) {
+  extern __shared__ __align__(16) double panel[];  // [kCholNB][pw] pw = padded width
+  __shared__ double red[32];
+  __shared__ int fail;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5, nwarps = kCholThreads / 32;
+  const int64_t mm = static_cast<int64_t>(m) * m;
+
+  // symmetry check (linalg.py:70-72) and symmetrised copy into U
+  double amax = 0.0, asym = 0.0;
+  for (int64_t t = tid; t < mm; t += kCholThreads) {
+    const int i = static_cast<int>(t / m), j = static_cast<int>(t % m);
+    const double sij = S[t], sji = S[static_cast<int64_t>(j) * m + i];
+    amax = fmax(amax, fabs(sij));
+    asym = fmax(asym, fabs(sij - sji));
+    U[t] = 0.5 * (sij + sji);
+  }
+  // block max-reduce
+  for (int o = 16; o > 0; o >>= 1) {
+    amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    asym = fmax(asym, __shfl_xor_sync(0xffffffffu, asym, o));
+  }
+  if (lane == 0) { red[warp] = amax; red[16 + warp] = asym; }
+  if (tid == 0) fail = 0;
+  __syncthreads();
+  if (tid == 0) {
+    double a = 0, b = 0;
+    for (int w = 0; w < nwarps; ++w) { a = fmax(a, red[w]); b = fmax(b, red[16 + w]); }
+    if (a > 0 && b > 1e-8 * a) info[TRALS_INFO_ASYM] = 1;
+  }
+  __syncthreads();
+
+  const int pw_full = ((m + 7) / 8) * 8 + 4;  // padded smem pitch (bank-conflict-free fragments)
+  for (int p0 = 0; p0 < m; p0 += kCholNB) {
+    const int pb = min(kCholNB, m - p0);
+    const int w = m - p0;
+    const int wpad = ((w + 7) / 8) * 8;
+    const int pw = pw_full;
+    // load panel rows p0..p0+pb-1, cols p0..m-1 (zero padded to 8-multiples, rows to kCholNB)
+    for (int t = tid; t < kCholNB * wpad; t += kCholThreads) {
+      const int r = t / wpad, c = t % wpad;
+      double v = 0.0;
+      if (r < pb && c < w && c >= r) v = U[static_cast<int64_t>(p0 + r) * m + p0 + c];
+      panel[r * pw + c] = v;
+    }
+    __syncthreads();
+    // factor the panel (upper form, row-oriented): row j /= sqrt(pivot), rank-1 update below
+    for (int j = 0; j < pb; ++j) {
+      if (tid == 0) {
+        const double d = panel[j * pw + j];
+        if (!(d > 0.0)) {  // also catches NaN
+          fail = p0 + j + 1;
+        }
+      }
+      __syncthreads();
+      if (fail) break;
+      const double dinv = 1.0 / sqrt(panel[j * pw + j]);
+      for (int c = j + tid; c < w; c += kCholThreads) panel[j * pw + c] *= dinv;
+      __syncthreads();
+      const int rows = pb - j - 1;
+      for (int t = tid; t < rows * w; t += kCholThreads) {
+        const int r = j + 1 + t / w, c = t % w;
+        if (c >= r) panel[r * pw + c] -= panel[j * pw + r] * panel[j * pw + c];
+      }
+      __syncthreads();
+    }
+    if (fail) break;
+    // write the factored panel rows back
+    for (int t = tid; t < pb * w; t += kCholThreads) {
+      const int r = t / w, c = t % w;
+      if (c >= r) U[static_cast<int64_t>(p0 + r) * m + p0 + c] = panel[r * pw + c];
+    }
+    // trailing update of the upper triangle: A[i][c] -= sum_t P[t][i] P[t][c], i,c >= pb (panel coords)
+    const int tw = w - pb;
+    if (tw > 0) {
+      const int nb8 = (tw + 7) / 8;
+      const int nblk = nb8 * (nb8 + 1) / 2;
+      const int fr = lane >> 2, fk = lane & 3;
+      for (int bidx = warp; bidx < nblk; bidx += nwarps) {
+        // decode upper-triangular block index -> (bi, bc), bc >= bi
+        int bi = 0, rem = bidx;
+        while (rem >= nb8 - bi) { rem -= nb8 - bi; ++bi; }
+        const int bc = bi + rem;
+        const int i0 = pb + bi * 8, c0 = pb + bc * 8;
+        // C fragment: row i0+fr, cols c0+2fk, c0+2fk+1
+        const int gi = p0 + i0 + fr;
+        double c[2];
+        for (int e = 0; e < 2; ++e) {
+          const int gc = p0 + c0 + 2 * fk + e;
+          c[e] = (gi < m && gc < m) ? U[static_cast<int64_t>(gi) * m + gc] : 0.0;
+        }
+        for (int k0 = 0; k0 < kCholNB; k0 += 4) {
+          // A(m=i, k=t) = -P[t][i];  B(k=t, n=c) = P[t][c]
+          const double a = -panel[(k0 + fk) * pw + i0 + fr];
+          const double b = panel[(k0 + fk) * pw + c0 + fr];
+          trals::dmma884(c[0], c[1], a, b);
+        }
+        for (int e = 0; e < 2; ++e) {
+          const int gc = p0 + c0 + 2 * fk + e;
+          if (gi < m && gc < m && gc >= gi) U[static_cast<int64_t>(gi) * m + gc] = c[e];
+        }
+      }
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+  if (fail) {
+    if (tid == 0) info[TRALS_INFO_CHOL] = fail;
+    return;
+  }
+  // zero the strict lower triangle of U, write L = U^T, degeneracy floor
+  double umax = 0.0, dmin = INFINITY;
+  int dmin_idx = 0;
+  for (int64_t t = tid; t < mm; t += kCholThreads) {
+    const int i = static_cast<int>(t / m), j = static_cast<int>(t % m);
+    double v = 0.0;
+    if (j >= i) v = U[t];
+    else U[t] = 0.0;
+    (void)v;
+  }
+  __syncthreads();
+  for (int64_t t = tid; t < mm; t += kCholThreads) {
+    const int i = static_cast<int>(t / m), j = static_cast<int>(t % m);
+    const double v = U[static_cast<int64_t>(j) * m + i];  // L[i][j] = U[j][i]
+    L[t] = v;
+    const double u = U[t];
+    umax = fmax(umax, fabs(u));
+    if (i == j && fabs(u) < dmin) { dmin = fabs(u); dmin_idx = i; }
+  }
+  if (check_degen) {
+    for (int o = 16; o > 0; o >>= 1) {
+      umax = fmax(umax, __shfl_xor_sync(0xffffffffu, umax, o));
+      const double od = __shfl_xor_sync(0xffffffffu, dmin, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, dmin_idx, o);
+      if (od < dmin || (od == dmin && oi < dmin_idx)) { dmin = od; dmin_idx = oi; }
+    }
+    __shared__ double sd[16];
+    __shared__ int si[16];
+    __syncthreads();
+    if (lane == 0) { red[warp] = umax; sd[warp] = dmin; si[warp] = dmin_idx; }
+    __syncthreads();
+    if (tid == 0) {
+      double a = 0, d = INFINITY;
+      int di = 0;
+      for (int w = 0; w < nwarps; ++w) {
+        a = fmax(a, red[w]);
+        if (sd[w] < d || (sd[w] == d && si[w] < di)) { d = sd[w]; di = si[w]; }
+      }
+      if (d <= 1e-13 * a) info[TRALS_INFO_DEGEN] = di + 1;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Row-parallel triangular solves Z S = M, S = U^T U  (Y U = M, then Z U^T = Y)
+// One warp per RHS row; the CTA's warps share U/L rows staged in shared memory.
+// ---------------------------------------------------------------------------
+constexpr int kSolveWarps = 8;
+constexpr int kSolveChunk = 8;  // U rows per smem stage
+
+template <int NR>
+__global__ void __launch_bounds__(kSolveWarps * 32) chol_solve_kernel(const double* __restrict__ U,
+                                                                      const double* __restrict__ L, int m,
+                                                                      const double* __restrict__ Mr, int64_t rows,
+                                                                      double* __restrict__ Z) {
+  extern __shared__ __align__(16) double stage[];  // [2][kSolveChunk][m]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * kSolveWarps + warp;
+  const bool active = row < rows;
+  double r[NR];
+#pragma unroll
+  for (int s = 0; s < NR; ++s) {
+    const int k = s * 32 + lane;
+    r[s] = (active && k < m) ? Mr[row * m + k] : 0.0;
+  }
+  const int nchunks = (m + kSolveChunk - 1) / kSolveChunk;
+  // ---- forward: Y U = M.  y_j = r_j / U[j][j];  r_k -= y_j U[j][k]  (k > j) ----
+  for (int pass = 0; pass < 2; ++pass) {
+    const double* Src = pass == 0 ? U : L;
+    auto load_chunk = [&](int ch, int buf) {
+      // pass 0 walks rows 0..m-1 of U; pass 1 walks rows m-1..0 of L
+      for (int t = threadIdx.x; t < kSolveChunk * m; t += kSolveWarps * 32) {
+        const int rr = t / m, c = t % m;
+        const int j = pass == 0 ? ch * kSolveChunk + rr : m - 1 - (ch * kSolveChunk + rr);
+        stage[(buf * kSolveChunk + rr) * m + c] = (j >= 0 && j < m) ? Src[static_cast<int64_t>(j) * m + c] : 0.0;
+      }
+    };
+    load_chunk(0, 0);
+    __syncthreads();
+    for (int ch = 0; ch < nchunks; ++ch) {
+      if (ch + 1 < nchunks) load_chunk(ch + 1, (ch + 1) & 1);
+      const double* buf = stage + (ch & 1) * kSolveChunk * m;
+      for (int rr = 0; rr < kSolveChunk; ++rr) {
+        const int j = pass == 0 ? ch * kSolveChunk + rr : m - 1 - (ch * kSolveChunk + rr);
+        if (j < 0 || j >= m) break;
+        const double* urow = buf + rr * m;
+        const int js = j >> 5, jl = j & 31;
+        double v = 0.0;
+#pragma unroll
+        for (int s = 0; s < NR; ++s)
+          if (s == js) v = r[s];
+        v = __shfl_sync(0xffffffffu, v, jl);
+        const double y = v / urow[j];
+#pragma unroll
+        for (int s = 0; s < NR; ++s) {
+          const int k = s * 32 + lane;
+          if (k < m) {
+            if (k == j) r[s] = y;
+            else if (pass == 0 ? (k > j) : (k < j)) r[s] = fma(-y, urow[k], r[s]);
+          }
+        }
+      }
+      __syncthreads();
+    }
+    __syncthreads();
+  }
+  if (active) {
+#pragma unroll
+    for (int s = 0; s < NR; ++s) {
+      const int k = s * 32 + lane;
+      if (k < m) Z[row * m + k] = r[s];
+    }
+  }
+}
+
+template <int NR>
+int launch_solve(const double* U, const double* L, int m, const double* Mr, int64_t rows, double* Z,
+                 cudaStream_t s) {
+  const size_t smem = sizeof(double) * 2 * kSolveChunk * m;
+  auto k = chol_solve_kernel<NR>;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  const int64_t blocks = (rows + kSolveWarps - 1) / kSolveWarps;
+  k<<<static_cast<unsigned>(blocks), kSolveWarps * 32, smem, s>>>(U, L, m, Mr, rows, Z);
+  return launch_status();
+}
+
+// C(m, n) = F[m * ncols + n] scattered through a CMap
+__global__ void reshuffle_kernel(const double* __restrict__ F, int64_t rows, int64_t cols, CMap cm,
+                                 double* __restrict__ C) {
+  const int64_t total = rows * cols;
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    C[trals::cmap_addr(cm, 0, t / cols, t % cols)] = F[t];
+}
+
+// ---------------------------------------------------------------------------
+// error terms: out[1] = <M,Z>, out[2] = <S, G> with G = Z^T Z (precomputed)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024) error_terms_kernel(const double* __restrict__ M, const double* __restrict__ Z,
+                                                           int64_t nz, const double* __restrict__ S,
+                                                           const double* __restrict__ G, int64_t ns,
+                                                           const double* __restrict__ xnorm2, double* __restrict__ out) {
+  __shared__ double red[32];
+  double a = 0.0;
+  for (int64_t t = threadIdx.x; t < nz; t += blockDim.x) a = fma(M[t], Z[t], a);
+  const double cross = block_sum<1024>(a, red);
+  double b = 0.0;
+  for (int64_t t = threadIdx.x; t < ns; t += blockDim.x) b = fma(S[t], G[t], b);
+  const double model = block_sum<1024>(b, red);
+  if (threadIdx.x == 0) {
+    const double x2 = xnorm2[0];
+    const double xn = sqrt(x2);
+    double e = 0.0;
+    if (xn != 0.0) {
+      const double sq = xn * xn - 2.0 * cross + model;
+      e = sqrt(fmax(0.0, sq)) / xn;
+    }
+    out[0] = e;
+    out[1] = cross;
+    out[2] = model;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// composite host helpers (no allocation; stride bookkeeping only)
+// ---------------------------------------------------------------------------
+int half_chain(int nblk, const int64_t* dims, const int32_t* ranks, const double* first_slice,
+               const double* const* cores_c, double* out, double* tmp, double* ws, int64_t ws_elems,
+               cudaStream_t s) {
+  // chain of cores u..u+nblk-1; dims[j], ranks[j] = left bond of core j, ranks[nblk] = right bond of last
+  if (nblk < 1) return TRALS_ERR_ARG;
+  const int64_t Ru = ranks[0];
+  if (nblk == 1) {
+    const int64_t n = dims[0] * Ru * ranks[1];
+    if (cudaMemcpyAsync(out, first_slice, n * sizeof(double), cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+      return TRALS_ERR_CUDA;
+    return TRALS_OK;
+  }
+  // ping-pong so that the final product lands in `out`
+  const double* cur = first_slice;
+  int64_t pre = dims[0];
+  for (int j = 1; j < nblk; ++j) {
+    double* dst = ((nblk - 1 - j) % 2 == 0) ? out : tmp;
+    const int64_t Rt = ranks[j], Ij = dims[j], Rn = ranks[j + 1];
+    // A(m = (i_pre, r_u), k = t) = cur[m*Rt + t]; B[t][(i_j, r')] = core_c[j]
+    // Out[i_pre][i_j][r_u][r'] : m1 = i_pre, m2 = r_u ; n1 = i_j, n2 = r'
+    CMap cm{0, Ru, Ij * Ru * Rn, Rn, Rn, Ru * Rn, 1};
+    int st = gemm(cur, 0, Rt, 1, 1, pre * Ru, Rt, Ij * Rn, cores_c[j], Ij * Rn, dst, cm, 0, ws, ws_elems, s);
+    if (st) return st;
+    cur = dst;
+    pre *= Ij;
+  }
+  return TRALS_OK;
+}
+
+int64_t half_chain_tmp(int nblk, const int64_t* dims, const int32_t* ranks) {
+  int64_t pre = dims[0], best = 0;
+  for (int j = 1; j < nblk; ++j) {
+    pre *= dims[j];
+    best = std::max<int64_t>(best, pre * ranks[0] * ranks[j + 1]);
+  }
+  return best;
+}
+
+int64_t half_chain_ws(int nblk, const int64_t* dims, const int32_t* ranks) {
+  int64_t pre = dims[0], best = 0;
+  for (int j = 1; j < nblk; ++j) {
+    best = std::max(best, gemm_ws(1, pre * ranks[0], ranks[j], dims[j] * ranks[j + 1]));
+    pre *= dims[j];
+  }
+  return best;
+}
+
+int env(const double* X, int64_t pre, int64_t post, int side, const double* H, int r_lo, int r_hi, double* E,
+        int leaf, double* ws, int64_t ws_elems, cudaStream_t s) {
+  const int64_t RR = static_cast<int64_t>(r_lo) * r_hi;
+  if (side == 0) {
+    // H over post modes (y..N-1): H[k][r_y][r_0], r_lo = r_y, r_hi = r_0
+    // Env[r_0][m][r_y]; n = (r_y, r_0): n1 = r_y, n2 = r_0 (N2 = r_hi)
+    CMap cm{0, pre, 0, r_lo, r_hi, 1, pre * r_lo};
+    // single-mode segment [0]: write M_0[i_0][r_0 + R_0 r_1] (r_y = r_1)
+    if (leaf) cm = CMap{0, pre, 0, RR, r_hi, r_hi, 1};
+    return gemm(X, 0, post, 1, 1, pre, post, RR, H, RR, E, cm, 0, ws, ws_elems, s);
+  }
+  // H over pre modes (0..x): H[k][r_0][r_{x+1}], r_lo = r_0, r_hi = r_{x+1}
+  // Env[r_{x+1}][m][r_0]; n = (r_0, r_x1): n1 = r_0, n2 = r_x1
+  CMap cm{0, post, 0, r_lo, r_hi, 1, post * r_lo};
+  // single-mode segment [N-1]: M_{N-1}[i][r_{N-1} + R_{N-1} r_0] (r_{x+1} = r_{N-1})
+  if (leaf) cm = CMap{0, post, 0, RR, r_hi, r_hi, 1};
+  return gemm(X, 0, 1, post, 1, post, pre, RR, H, RR, E, cm, 0, ws, ws_elems, s);
+}
+
+int absorb_right(const double* E, int Ra, int64_t pre, int64_t Ib, int Rb, int Rb1, const double* core_zt,
+                 double* out, int leaf, double* ws, int64_t ws_elems, cudaStream_t s) {
+  const int64_t M = static_cast<int64_t>(Ra) * pre, K = Ib * Rb1;
+  CMap cm = rowmajor(Rb);
+  if (leaf) {
+    // out = M_a[i_a][r_a + Ra r_b]: m = (r_a, i_a) -> m1 = r_a, m2 = i_a (M2 = pre)
+    cm = CMap{0, pre, 1, static_cast<int64_t>(Ra) * Rb, 1 << 30, 0, Ra};
+  }
+  return gemm(E, 0, K, 1, 1, M, K, Rb, core_zt, Rb, out, cm, 0, ws, ws_elems, s);
+}
+
+int absorb_left(const double* E, int Ra, int64_t Ia, int64_t rest, int Ra1, int Rb1, const double* core_c,
+                double* out, int leaf, double* ws, int64_t ws_elems, cudaStream_t s) {
+  const int64_t M = rest * Rb1, K = static_cast<int64_t>(Ra) * Ia;
+  // Out[r_{a+1}][m]: element (m, n) at n*M + m
+  CMap cm{0, 1 << 30, 0, 1, 1 << 30, 0, M};
+  if (leaf) {
+    // out = M_b[i_b][r_b + R_b r_{b+1}] with r_b = n, (i_b, r_{b+1}) = m -> m1 = i_b, m2 = r_{b+1}
+    cm = CMap{0, Rb1, static_cast<int64_t>(Ra1) * Rb1, Ra1, 1 << 30, 0, 1};
+  }
+  return gemm(E, 0, 1, M, 1, M, K, Ra1, core_c, Ra1, out, cm, 0, ws, ws_elems, s);
+}
+
+
+// ---------------------------------------------------------------------------
+// stateless single-mode MTTSP plan (used by trals_mttsp_f64)
+// ---------------------------------------------------------------------------
+struct MttspPlan {
+  int side;           // 0: half chain over suffix [y..N-1]; 1: over prefix [0..x]
+  int lo, hi;         // chain block [lo..hi]
+  int seg_a, seg_b;   // environment segment after the root product
+  int64_t pre, post;  // X viewed as [pre][post]
+  int64_t h_elems, tmp_elems, env_elems, ws_elems;
+};
+
+inline int64_t prod_dims(const int64_t* dims, int a, int b) {
+  int64_t p = 1;
+  for (int j = a; j <= b; ++j) p *= dims[j];
+  return p;
+}
+
+MttspPlan plan_mttsp(int N, const int64_t* dims, const int32_t* ranks, int n) {
+  MttspPlan best{};
+  double best_cost = -1;
+  const int64_t total = prod_dims(dims, 0, N - 1);
+  auto consider = [&](int side, int lo, int hi) {
+    const int64_t pc = prod_dims(dims, lo, hi);
+    const double cost = static_cast<double>(std::max(pc, total / pc)) + 1e-9 * pc;
+    if (best_cost < 0 || cost < best_cost) {
+      best_cost = cost;
+      best.side = side; best.lo = lo; best.hi = hi;
+    }
+  };
+  for (int y = n + 1; y <= N - 1; ++y) consider(0, y, N - 1);
+  for (int x = 0; x <= n - 1; ++x) consider(1, 0, x);
+  MttspPlan& p = best;
+  if (p.side == 0) { p.seg_a = 0; p.seg_b = p.lo - 1; p.pre = prod_dims(dims, 0, p.lo - 1); p.post = prod_dims(dims, p.lo, N - 1); }
+  else { p.seg_a = p.hi + 1; p.seg_b = N - 1; p.pre = prod_dims(dims, 0, p.hi); p.post = prod_dims(dims, p.hi + 1, N - 1); }
+  const int nblk = p.hi - p.lo + 1;
+  std::vector<int64_t> bd(dims + p.lo, dims + p.hi + 1);
+  std::vector<int32_t> br;
+  for (int j = p.lo; j <= p.hi + 1; ++j) br.push_back(ranks[j % N]);
+  const int64_t r_lo = br.front(), r_hi = br.back();
+  p.h_elems = prod_dims(dims, p.lo, p.hi) * r_lo * r_hi;
+  p.tmp_elems = half_chain_tmp(nblk, bd.data(), br.data());
+  int64_t ws = half_chain_ws(nblk, bd.data(), br.data());
+  const int64_t seg_len = p.side == 0 ? p.pre : p.post;
+  const int64_t RR = r_lo * r_hi;
+  p.env_elems = seg_len * RR;
+  const bool root_leaf = (p.seg_a == p.seg_b);
+  ws = std::max(ws, p.side == 0 ? gemm_ws(1, p.pre, p.post, RR) : gemm_ws(1, p.post, p.pre, RR));
+  (void)root_leaf;
+  // walk the absorptions to size the gemm workspace
+  int a = p.seg_a, b = p.seg_b;
+  int64_t seg = seg_len;
+  while (b > n) {
+    const int64_t Ra = ranks[a], Rb = ranks[b], Rb1 = ranks[(b + 1) % N];
+    ws = std::max(ws, gemm_ws(1, Ra * (seg / dims[b]), dims[b] * Rb1, Rb));
+    seg /= dims[b];
+    --b;
+  }
+  while (a < n) {
+    const int64_t Ra = ranks[a], Ra1 = ranks[a + 1], Rb1 = ranks[(b + 1) % N];
+    ws = std::max(ws, gemm_ws(1, (seg / dims[a]) * Rb1, Ra * dims[a], Ra1));
+    seg /= dims[a];
+    ++a;
+  }
+  p.ws_elems = ws;
+  return p;
+}
+
+int64_t mttsp_total_ws(const MttspPlan& p) {
+  // [H][tmp][env0][env1][gemm ws]
+  return p.h_elems + p.tmp_elems + 2 * p.env_elems + p.ws_elems + 64;
+}
+
+int run_mttsp(const double* X, int N, const int64_t* dims, const int32_t* ranks, int n,
+              const double* const* cc, const double* const* cs, const double* const* czt, double* M, double* ws,
+              int64_t ws_elems, cudaStream_t s) {
+  const MttspPlan p = plan_mttsp(N, dims, ranks, n);
+  if (ws_elems < mttsp_total_ws(p)) return TRALS_ERR_WORKSPACE;
+  auto al = [](int64_t v) { return (v + 7) & ~int64_t(7); };
+  double* H = ws;
+  double* tmp = H + al(p.h_elems);
+  double* env0 = tmp + al(p.tmp_elems);
+  double* env1 = env0 + al(p.env_elems);
+  double* gws = env1 + al(p.env_elems);
+  const int64_t gws_elems = ws_elems - (gws - ws);
+  const int nblk = p.hi - p.lo + 1;
+  std::vector<int64_t> bd(dims + p.lo, dims + p.hi + 1);
+  std::vector<int32_t> br;
+  for (int j = p.lo; j <= p.hi + 1; ++j) br.push_back(ranks[j % N]);
+  std::vector<const double*> bc(cc + p.lo, cc + p.hi + 1);
+  int st = half_chain(nblk, bd.data(), br.data(), cs[p.lo], bc.data(), H, tmp, gws, gws_elems, s);
+  if (st) return st;
+  const bool root_leaf = (p.seg_a == p.seg_b);
+  st = env(X, p.pre, p.post, p.side, H, br.front(), br.back(), root_leaf ? M : env0, root_leaf, gws, gws_elems, s);
+  if (st || root_leaf) return st;
+  int a = p.seg_a, b = p.seg_b;
+  int64_t seg = p.side == 0 ? p.pre : p.post;
+  const double* cur = env0;
+  double* nxt = env1;
+  while (b > n) {
+    const bool leaf = (a == n && b == n + 1);
+    st = absorb_right(cur, ranks[a], seg / dims[b], dims[b], ranks[b], ranks[(b + 1) % N], czt[b],
+                      leaf ? M : nxt, leaf, gws, gws_elems, s);
+    if (st) return st;
+    seg /= dims[b];
+    --b;
+    std::swap(const_cast<double*&>(cur), nxt);
+    if (leaf) return TRALS_OK;
+  }
+  while (a < n) {
+    const bool leaf = (a + 1 == n && b == n);
+    st = absorb_left(cur, ranks[a], dims[a], seg / dims[a], ranks[a + 1], ranks[(b + 1) % N], cc[a],
+                     leaf ? M : nxt, leaf, gws, gws_elems, s);
+    if (st) return st;
+    seg /= dims[a];
+    ++a;
+    std::swap(const_cast<double*&>(cur), nxt);
+    if (leaf) return TRALS_OK;
+  }
+  return TRALS_ERR_ARG;  // unreachable for valid plans
+}
+
+}  // namespace
+
+// ===========================================================================
+// C-ABI
+// ===========================================================================
+extern "C" {
+
+const char* trals_strerror(int code) {
+  switch (code) {
+    case TRALS_OK: return "ok";
+    case TRALS_ERR_ARG: return "invalid argument";
+    case TRALS_ERR_CUDA: return "CUDA launch failure";
+    case TRALS_ERR_WORKSPACE: return "workspace too small";
+    case TRALS_ERR_UNSUPPORTED: return "size outside the supported envelope";
+  }
+  return "unknown error";
+}
+
+int trals_version(void) { return 1; }
+
+int64_t trals_gemm_ws_elems(int64_t P, int64_t M, int64_t K, int64_t N) { return gemm_ws(P, M, K, N); }
+
+int trals_gemm_f64(const double* A, int64_t sAp, int64_t sAm, int64_t sAk, int64_t P, int64_t M, int64_t K,
+                   int64_t N, const double* B, int64_t ldb, double* C, const int64_t* h_cmap, int beta,
+                   double* ws, int64_t ws_elems, void* stream) {
+  if (!h_cmap) return TRALS_ERR_ARG;
+  CMap cm{h_cmap[0], h_cmap[1], h_cmap[2], h_cmap[3], h_cmap[4], h_cmap[5], h_cmap[6]};
+  return gemm(A, sAp, sAm, sAk, P, M, K, N, B, ldb, C, cm, beta, ws, ws_elems, static_cast<cudaStream_t>(stream));
+}
+
+int trals_core_relayout_f64(const double* src, int sl, int Ra, int64_t I, int Rb, double* dst, int dl,
+                            void* stream) {
+  if (!src || !dst || Ra < 1 || Rb < 1 || I < 1 || sl < 0 || sl > 2 || dl < 0 || dl > 2) return TRALS_ERR_ARG;
+  const int64_t total = static_cast<int64_t>(Ra) * I * Rb;
+  const int threads = 256;
+  const int blocks = static_cast<int>(std::min<int64_t>((total + threads - 1) / threads, 4 * kSMs));
+  relayout_kernel<<<blocks, threads, 0, static_cast<cudaStream_t>(stream)>>>(src, sl, Ra, I, Rb, dst, dl);
+  return launch_status();
+}
+
+int64_t trals_half_chain_tmp_elems(int nblk, const int64_t* dims, const int32_t* ranks) {
+  return half_chain_tmp(nblk, dims, ranks);
+}
+
+int trals_half_chain_f64(int nblk, const int64_t* dims, const int32_t* ranks, const double* first_slice,
+                         const double* const* cores_c, double* out, double* tmp, double* ws, int64_t ws_elems,
+                         void* stream) {
+  if (!dims || !ranks || !first_slice || !out) return TRALS_ERR_ARG;
+  if (nblk > 1 && (!cores_c || !tmp)) return TRALS_ERR_ARG;
+  return half_chain(nblk, dims, ranks, first_slice, cores_c, out, tmp, ws, ws_elems,
+                    static_cast<cudaStream_t>(stream));
+}
+
+int trals_env_f64(const double* X, int64_t pre, int64_t post, int side, const double* H, int r_lo, int r_hi,
+                  double* E, int leaf, double* ws, int64_t ws_elems, void* stream) {
+  if (!X || !H || !E || pre < 1 || post < 1 || r_lo < 1 || r_hi < 1 || (side != 0 && side != 1))
+    return TRALS_ERR_ARG;
+  return env(X, pre, post, side, H, r_lo, r_hi, E, leaf, ws, ws_elems, static_cast<cudaStream_t>(stream));
+}
+
+int trals_absorb_right_f64(const double* E, int Ra, int64_t pre, int64_t Ib, int Rb, int Rb1, const double* core_zt,
+                           double* out, int leaf, double* ws, int64_t ws_elems, void* stream) {
+  if (!E || !core_zt || !out || Ra < 1 || pre < 1 || Ib < 1 || Rb < 1 || Rb1 < 1) return TRALS_ERR_ARG;
+  return absorb_right(E, Ra, pre, Ib, Rb, Rb1, core_zt, out, leaf, ws, ws_elems, static_cast<cudaStream_t>(stream));
+}
+
+int trals_absorb_left_f64(const double* E, int Ra, int64_t Ia, int64_t rest, int Ra1, int Rb1, const double* core_c,
+                          double* out, int leaf, double* ws, int64_t ws_elems, void* stream) {
+  if (!E || !core_c || !out || Ra < 1 || Ia < 1 || rest < 1 || Ra1 < 1 || Rb1 < 1) return TRALS_ERR_ARG;
+  return absorb_left(E, Ra, Ia, rest, Ra1, Rb1, core_c, out, leaf, ws, ws_elems, static_cast<cudaStream_t>(stream));
+}
+
+int trals_core_gram_f64(const double* Gs, int Ra, int64_t I, int Rb, double* E, double* ws, int64_t ws_elems,
+                        void* stream) {
+  if (!Gs || !E || Ra < 1 || Rb < 1 || I < 1) return TRALS_ERR_ARG;
+  const int64_t RR = static_cast<int64_t>(Ra) * Rb;
+  // C'[(a,b)][(c,d)] = sum_i Gs[i][a][b] Gs[i][c][d]; E[(a,c)][(b,d)] at (a*Ra + c)*Rb^2 + b*Rb + d
+  CMap cm{0, Rb, static_cast<int64_t>(Ra) * Rb * Rb, Rb, Rb, static_cast<int64_t>(Rb) * Rb, 1};
+  return gemm(Gs, 0, 1, RR, 1, RR, I, RR, Gs, RR, E, cm, 0, ws, ws_elems, static_cast<cudaStream_t>(stream));
+}
+
+int trals_gram_chain_f64(int N, int n, const int32_t* ranks, const double* const* E, double* S, double* tmp,
+                         double* ws, int64_t ws_elems, void* stream) {
+  if (N < 2 || n < 0 || n >= N || !ranks || !E || !S) return TRALS_ERR_ARG;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // ring order n+1, ..., N-1, 0, ..., n-1 ; F = E_{n+1} E_{n+2} ... E_{n-1}
+  std::vector<int> order;
+  for (int j = n + 1; j < N; ++j) order.push_back(j);
+  for (int j = 0; j < n; ++j) order.push_back(j);
+  const int64_t Rn = ranks[n], Rn1 = ranks[(n + 1) % N];
+  const int64_t RR = Rn * Rn1;
+  // final scatter into S[(r_n + Rn r_{n+1})][(r'_n + Rn r'_{n+1})] from F[(r_{n+1}, r'_{n+1})][(r_n, r'_n)]
+  const CMap to_s{0, Rn1, Rn * RR, Rn, Rn, RR, 1};
+  const int64_t rows = Rn1 * Rn1;  // F rows
+  if (order.size() == 1) {
+    // N == 2: S is a reshuffle of the single transfer matrix
+    const int64_t total = RR * RR;
+    const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 4 * kSMs));
+    reshuffle_kernel<<<blocks, 256, 0, s>>>(E[order[0]], rows, Rn * Rn, to_s, S);
+    return launch_status();
+  }
+  double* bufs[2] = {tmp, tmp + RR * RR};
+  const double* cur = E[order[0]];
+  int64_t cols = static_cast<int64_t>(ranks[(order[0] + 1) % N]) * ranks[(order[0] + 1) % N];
+  for (size_t t = 1; t < order.size(); ++t) {
+    const int j = order[t];
+    const int64_t Rj1 = ranks[(j + 1) % N];
+    const int64_t ncols = Rj1 * Rj1;
+    const bool last = (t + 1 == order.size());
+    double* dst = last ? S : bufs[t & 1];
+    const CMap cm = last ? to_s : rowmajor(ncols);
+    int st = gemm(cur, 0, cols, 1, 1, rows, cols, ncols, E[j], ncols, dst, cm, 0, ws, ws_elems, s);
+    if (st) return st;
+    cur = dst;
+    cols = ncols;
+  }
+  return TRALS_OK;
+}
+
+int trals_cholesky_f64(const double* S, int m, double* U, double* L, int check_degen, int* info, void* stream) {
+  if (!S || !U || !L || !info || m < 1) return TRALS_ERR_ARG;
+  const int pw = ((m + 7) / 8) * 8 + 4;
+  const size_t smem = sizeof(double) * kCholNB * pw;
+  if (smem > 200 * 1024) return TRALS_ERR_UNSUPPORTED;
+  static int attr = 0;
+  if (smem > 48 * 1024 && static_cast<int>(smem) > attr) {
+    cudaFuncSetAttribute(cholesky_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = 200 * 1024;
+  }
+  cholesky_kernel<<<1, kCholThreads, smem, static_cast<cudaStream_t>(stream)>>>(S, m, U, L, check_degen, info);
+  return launch_status();
+}
+
+int trals_chol_solve_f64(const double* U, const double* L, int m, const double* Mr, int64_t rows, double* Z,
+                         void* stream) {
+  if (!U || !L || !Mr || !Z || m < 1) return TRALS_ERR_ARG;
+  if (rows <= 0) return TRALS_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int nr = (m + 31) / 32;
+  if (nr <= 1) return launch_solve<1>(U, L, m, Mr, rows, Z, s);
+  if (nr <= 2) return launch_solve<2>(U, L, m, Mr, rows, Z, s);
+  if (nr <= 4) return launch_solve<4>(U, L, m, Mr, rows, Z, s);
+  if (nr <= 8) return launch_solve<8>(U, L, m, Mr, rows, Z, s);
+  if (nr <= 16) return launch_solve<16>(U, L, m, Mr, rows, Z, s);
+  if (nr <= 24) return launch_solve<24>(U, L, m, Mr, rows, Z, s);
+  return TRALS_ERR_UNSUPPORTED;
+}
+
+int64_t trals_sumsq_ws_elems(void) { return kSumsqBlocks; }
+
+int trals_sumsq_f64(const double* x, int64_t n, double* out, double* ws, void* stream) {
+  if (!x || !out || !ws || n < 0) return TRALS_ERR_ARG;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  sumsq_partial_kernel<<<kSumsqBlocks, 512, 0, s>>>(x, n, ws);
+  sum_final_kernel<<<1, 1024, 0, s>>>(ws, kSumsqBlocks, out);
+  return launch_status();
+}
+
+int64_t trals_error_ws_elems(int64_t rows, int m) {
+  return static_cast<int64_t>(m) * m + gemm_ws(1, m, rows, m);
+}
+
+int trals_error_terms_f64(const double* Mr, const double* Z, const double* S, int64_t rows, int m,
+                          const double* xnorm2, double* out, double* ws, int64_t ws_elems, void* stream) {
+  if (!Mr || !Z || !S || !xnorm2 || !out || !ws || m < 1 || rows < 1) return TRALS_ERR_ARG;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t mm = static_cast<int64_t>(m) * m;
+  if (ws_elems < mm) return TRALS_ERR_WORKSPACE;
+  double* G = ws;
+  // G = Z^T Z : A(m=c, k=i) = Z[i*m + c]
+  int st = gemm(Z, 0, 1, m, 1, m, rows, m, Z, m, G, rowmajor(m), 0, ws + mm, ws_elems - mm, s);
+  if (st) return st;
+  error_terms_kernel<<<1, 1024, 0, s>>>(Mr, Z, rows * m, S, G, mm, xnorm2, out);
+  return launch_status();
+}
+
+int64_t trals_mttsp_ws_elems(int N, const int64_t* dims, const int32_t* ranks, int n) {
+  if (N < 2 || !dims || !ranks || n < 0 || n >= N) return -1;
+  return mttsp_total_ws(plan_mttsp(N, dims, ranks, n));
+}
+
+int trals_mttsp_f64(const double* X, int N, const int64_t* dims, const int32_t* ranks, int n,
+                    const double* const* cc, const double* const* cs, const double* const* czt, double* M,
+                    double* ws, int64_t ws_elems, void* stream) {
+  if (!X || N < 2 || !dims || !ranks || n < 0 || n >= N || !cc || !cs || !czt || !M || !ws) return TRALS_ERR_ARG;
+  return run_mttsp(X, N, dims, ranks, n, cc, cs, czt, M, ws, ws_elems, static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,430 @@
+"""Device sweep engine: the B200 schedule behind tr_als_ne / tr_als_qr / tr_als_qrne.
+
+One `SweepEngine` owns every device buffer a run needs (allocated once, so a
+sweep is a fixed list of kernel launches that can be replayed or captured in a
+CUDA graph) and compiles the reference's per-mode loop (solvers.py:369-389,
+:419-448, :472-498) into steps.
+
+Right-hand sides (the MTTSP, solvers.py:379) come from a two-phase
+environment tree instead of one X pass per mode:
+
+* the modes are split into a prefix L = [0, h) and a suffix R = [h, N);
+* phase L contracts X once with a half chain of (old) suffix cores, giving
+  the environment of the prefix segment (|L-modes| x R^2 numbers); each
+  M_n, n in L, is then reached by absorbing the other L cores (old ones from
+  the right, freshly updated ones from the left) -- small GEMMs;
+* phase R does the same with a half chain of the (new) prefix cores.
+
+So X is streamed twice per sweep whatever N is, instead of N times, and the
+(prod_{j!=n} I_j) x R^2 subchain matrix is never formed: the largest chain
+ever materialised covers a contiguous block C' of modes chosen so that
+max(prod C', |X| / prod C') is minimal.
+
+Sharding (one process per GPU): X is split along `shard_mode`; every rank
+runs the identical schedule on its slab (local core rows for the sharded
+mode), so each M_n is a partial sum that one NCCL all-reduce completes before
+the replicated, deterministic solve.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import torch
+
+from . import _lib as L
+
+BUCKETS = ("subchain", "mttsp", "solve", "gramqr", "other")  # solvers.py:57
+
+
+def _prod(v):
+    p = 1
+    for x in v:
+        p *= int(x)
+    return p
+
+
+class _HostStream:
+    cuda_stream = 0
+
+
+@dataclass
+class Step:
+    bucket: str
+    fn: object
+    name: str = ""
+
+
+@dataclass
+class EngineStats:
+    gemm_launches: int = 0
+    x_passes_per_sweep: int = 0
+    steps_per_sweep: int = 0
+    kernels_per_sweep: int = 0
+    notes: list = field(default_factory=list)
+
+
+class SweepEngine:
+    """Compiles and runs TR-ALS sweeps on one GPU (one rank of a sharded run)."""
+
+    def __init__(self, x_local: torch.Tensor, dims, ranks, variant: str, *, shard_mode=None, lo=0, hi=None,
+                 group=None, world_size: int = 1, _test_lib=None):
+        if variant not in ("ne", "qr", "qrne"):
+            raise ValueError(f"unsupported device variant {variant!r}")
+        # `_test_lib` lets the CPU test-suite drive this exact schedule through a numpy
+        # model of the C-ABI (tests/fake_trals.py); the solvers never pass it.
+        if _test_lib is None and not x_local.is_cuda:
+            raise TypeError("x_local must be a CUDA tensor")
+        if not (x_local.dtype == torch.float64 and x_local.is_contiguous()):
+            raise TypeError("x_local must be a contiguous float64 tensor")
+        self.lib = _test_lib if _test_lib is not None else L.lib()
+        self.dev = x_local.device
+        self.variant = variant
+        self.N = len(dims)
+        self.dims = [int(d) for d in dims]
+        self.ranks = [int(r) for r in ranks]
+        self.world = int(world_size)
+        self.group = group
+        self.s = shard_mode
+        self.lo = int(lo)
+        self.hi = int(hi) if hi is not None else (self.dims[shard_mode] if shard_mode is not None else 0)
+        self.dl = list(self.dims)
+        if shard_mode is not None:
+            self.dl[shard_mode] = self.hi - self.lo
+        if tuple(x_local.shape) != tuple(self.dl):
+            raise ValueError(f"local slab shape {tuple(x_local.shape)} != expected {tuple(self.dl)}")
+        self.x = x_local
+        self.stream = torch.cuda.current_stream(self.dev) if x_local.is_cuda else _HostStream()
+        self.stats = EngineStats()
+        self._alloc()
+        self._compile()
+
+    # ------------------------------------------------------------------ buffers
+    def R(self, j):
+        return self.ranks[j % self.N]
+
+    def _empty(self, *shape):
+        return torch.empty(shape, dtype=torch.float64, device=self.dev)
+
+    def _alloc(self):
+        N = self.N
+        self.Gc = [self._empty(self.R(j), self.dims[j], self.R(j + 1)) for j in range(N)]
+        self.Gs = [self._empty(self.dims[j], self.R(j), self.R(j + 1)) for j in range(N)]
+        self.Gt = [self._empty(self.dims[j], self.R(j + 1), self.R(j)) for j in range(N)]
+        self.E = [self._empty(self.R(j) ** 2, self.R(j + 1) ** 2) for j in range(N)]
+        self.M = [self._empty(self.dims[n], self.R(n) * self.R(n + 1)) for n in range(N)]
+        self.S = [self._empty(self.R(n) * self.R(n + 1), self.R(n) * self.R(n + 1)) for n in range(N)]
+        mmax = max(self.R(n) * self.R(n + 1) for n in range(N))
+        self.U = self._empty(mmax, mmax)
+        self.Lo = self._empty(mmax, mmax)
+        self.info = torch.zeros(L.INFO_SLOTS, dtype=torch.int32, device=self.dev)
+        self.xnorm2 = self._empty(1)
+        self.err_cur = self._empty(3)
+        rmax = max(self.ranks)
+        self.chain_tmp = self._empty(2 * rmax ** 4)
+        self.sumsq_ws = self._empty(self.lib.trals_sumsq_ws_elems())
+        self.Gc_loc = None
+        if self.s is not None:
+            s = self.s
+            self.Gc_loc = self._empty(self.R(s), self.dl[s], self.R(s + 1))
+        self.gws_need = 1
+        self.gws = None  # sized after compile
+
+    # local views used by the X contractions
+    def core_c(self, j):
+        return self.Gc_loc if (self.s is not None and j == self.s) else self.Gc[j]
+
+    def core_s(self, j):
+        if self.s is not None and j == self.s:
+            return self.Gs[j][self.lo:self.hi]
+        return self.Gs[j]
+
+    def core_zt(self, j):
+        if self.s is not None and j == self.s:
+            return self.Gt[j][self.lo:self.hi]
+        return self.Gt[j]
+
+    def m_target(self, n):
+        """Pointer where the leaf for mode n writes its (local) rows of M_n."""
+        rr = self.R(n) * self.R(n + 1)
+        if self.s is not None and n == self.s:
+            return self.M[n].data_ptr() + self.lo * rr * 8
+        return self.M[n].data_ptr()
+
+    def _ws(self, elems):
+        self.gws_need = max(self.gws_need, int(elems))
+
+    # ----------------------------------------------------------------- compile
+    def _compile(self):
+        N = self.N
+        self.steps: list[Step] = []
+        self._bufs = []  # keep env buffers alive
+        self.stats.x_passes_per_sweep = 0
+        if N == 2:
+            phases = [(0, 0), (1, 1)]
+        else:
+            h = (N + 1) // 2
+            phases = [(0, h - 1), (h, N - 1)]
+        for a, b in phases:
+            self._phase(a, b)
+        # error terms need the last mode's quantities (solvers.py:385-389)
+        rows = self.dims[N - 1]
+        m = self.R(N - 1) * self.R(N)
+        self.err_ws = self._empty(self.lib.trals_error_ws_elems(rows, m))
+        self.gws = self._empty(self.gws_need)
+        self.stats.steps_per_sweep = len(self.steps)
+
+    def _choose_block(self, a, b):
+        """Contiguous block C' of the complement of [a..b] that X is contracted with."""
+        N = self.N
+        total = _prod(self.dl)
+        best = None
+        if a == 0:
+            cands = [(y, N - 1) for y in range(b + 1, N)]
+        else:
+            cands = [(0, x) for x in range(0, a)]
+        for lo, hi in cands:
+            pc = _prod(self.dl[lo:hi + 1])
+            cost = (max(pc, total // pc), pc)
+            if best is None or cost < best[0]:
+                best = (cost, lo, hi)
+        return best[1], best[2]
+
+    def _phase(self, a, b):
+        N = self.N
+        lo, hi = self._choose_block(a, b)
+        nblk = hi - lo + 1
+        bd = self.dl[lo:hi + 1]
+        br = [self.R(j) for j in range(lo, hi + 2)]
+        r_lo, r_hi = br[0], br[-1]
+        H = self._empty(_prod(bd) * r_lo * r_hi)
+        tmp = self._empty(max(1, self.lib.trals_half_chain_tmp_elems(nblk, L.i64_array(bd), L.i32_array(br))))
+        self._bufs += [H, tmp]
+        # gemm workspace of the chain build
+        pre = bd[0]
+        for j in range(1, nblk):
+            self._ws(self.lib.trals_gemm_ws_elems(1, pre * r_lo, br[j], bd[j] * br[j + 1]))
+            pre *= bd[j]
+        bd_a, br_a = L.i64_array(bd), L.i32_array(br)
+        blk = list(range(lo, hi + 1))
+
+        def chain_step(bd_a=bd_a, br_a=br_a, blk=blk, H=H, tmp=tmp, nblk=nblk):
+            cc = L.ptr_array([self.core_c(j).data_ptr() for j in blk])
+            L.check(self.lib.trals_half_chain_f64(nblk, bd_a, br_a, self.core_s(blk[0]).data_ptr(), cc,
+                                                  H.data_ptr(), tmp.data_ptr(), self.gws.data_ptr(),
+                                                  self.gws.numel(), self._sp()), "half_chain")
+        self.steps.append(Step("subchain", chain_step, f"chain[{lo}..{hi}]"))
+
+        if a == 0:
+            side, seg_a, seg_b = 0, 0, lo - 1
+            pre, post = _prod(self.dl[:lo]), _prod(self.dl[lo:])
+        else:
+            side, seg_a, seg_b = 1, hi + 1, N - 1
+            pre, post = _prod(self.dl[:hi + 1]), _prod(self.dl[hi + 1:])
+        seg_len = pre if side == 0 else post
+        RR = r_lo * r_hi
+        self._ws(self.lib.trals_gemm_ws_elems(1, pre, post, RR) if side == 0
+                 else self.lib.trals_gemm_ws_elems(1, post, pre, RR))
+        root_leaf = seg_a == seg_b
+        if root_leaf:
+            n = seg_a
+            self._pre_leaf(n)
+            target = lambda n=n: self.m_target(n)
+        else:
+            E0 = self._empty(seg_len * RR)
+            self._bufs.append(E0)
+            target = lambda E0=E0: E0.data_ptr()
+
+        def env_step(pre=pre, post=post, side=side, H=H, r_lo=r_lo, r_hi=r_hi, target=target, leaf=int(root_leaf)):
+            L.check(self.lib.trals_env_f64(self.x.data_ptr(), pre, post, side, H.data_ptr(), r_lo, r_hi, target(),
+                                           leaf, self.gws.data_ptr(), self.gws.numel(), self._sp()), "env")
+        self.steps.append(Step("mttsp", env_step, f"env[{seg_a}..{seg_b}]"))
+        self.stats.x_passes_per_sweep += 1
+        if root_leaf:
+            self._solve(seg_a)
+            return
+        # absorb the extra complement cores so the environment covers exactly [a..b]
+        cur = E0
+        sa, sb = seg_a, seg_b
+        while sb > b:
+            last = (a == b and sa == a and sb == b + 1)
+            cur, sa, sb = self._absorb_right(cur, sa, sb, leaf_mode=a if last else None)
+        while sa < a:
+            last = (a == b and sa + 1 == a)
+            cur, sa, sb = self._absorb_left(cur, sa, sb, leaf_mode=a if last else None)
+        self._tree(cur, a, b)
+
+    def _pre_leaf(self, n):
+        if self.s is not None and n == self.s and self.world > 1:
+            M = self.M[n]
+            self.steps.append(Step("mttsp", lambda M=M: M.zero_(), f"zero M{n}"))
+
+    def _absorb_right(self, cur, a, b, leaf_mode):
+        """Env [a..b] -> [a..b-1] by absorbing (old) core b."""
+        pre = _prod(self.dl[a:b])
+        Ra, Rb, Rb1 = self.R(a), self.R(b), self.R(b + 1)
+        leaf = leaf_mode is not None
+        self._ws(self.lib.trals_gemm_ws_elems(1, Ra * pre, self.dl[b] * Rb1, Rb))
+        if leaf:
+            self._pre_leaf(leaf_mode)
+            out = None
+            target = lambda n=leaf_mode: self.m_target(n)
+        else:
+            out = self._empty(Ra * pre * Rb)
+            self._bufs.append(out)
+            target = lambda out=out: out.data_ptr()
+
+        def step(cur=cur, Ra=Ra, pre=pre, Ib=self.dl[b], Rb=Rb, Rb1=Rb1, b=b, target=target, leaf=int(leaf)):
+            L.check(self.lib.trals_absorb_right_f64(cur.data_ptr(), Ra, pre, Ib, Rb, Rb1, self.core_zt(b).data_ptr(),
+                                                    target(), leaf, self.gws.data_ptr(), self.gws.numel(),
+                                                    self._sp()), "absorb_right")
+        self.steps.append(Step("mttsp", step, f"absorbR core{b} -> [{a}..{b - 1}]"))
+        return out, a, b - 1
+
+    def _absorb_left(self, cur, a, b, leaf_mode):
+        """Env [a..b] -> [a+1..b] by absorbing (new) core a."""
+        rest = _prod(self.dl[a + 1:b + 1])
+        Ra, Ra1, Rb1 = self.R(a), self.R(a + 1), self.R(b + 1)
+        leaf = leaf_mode is not None
+        self._ws(self.lib.trals_gemm_ws_elems(1, rest * Rb1, Ra * self.dl[a], Ra1))
+        if leaf:
+            self._pre_leaf(leaf_mode)
+            out = None
+            target = lambda n=leaf_mode: self.m_target(n)
+        else:
+            out = self._empty(Ra1 * rest * Rb1)
+            self._bufs.append(out)
+            target = lambda out=out: out.data_ptr()
+
+        def step(cur=cur, Ra=Ra, Ia=self.dl[a], rest=rest, Ra1=Ra1, Rb1=Rb1, a=a, target=target, leaf=int(leaf)):
+            L.check(self.lib.trals_absorb_left_f64(cur.data_ptr(), Ra, Ia, rest, Ra1, Rb1, self.core_c(a).data_ptr(),
+                                                   target(), leaf, self.gws.data_ptr(), self.gws.numel(),
+                                                   self._sp()), "absorb_left")
+        self.steps.append(Step("mttsp", step, f"absorbL core{a} -> [{a + 1}..{b}]"))
+        return out, a + 1, b
+
+    def _tree(self, env, a, b):
+        """Emit steps that update modes a..b in order from the environment of [a..b]."""
+        if a == b:
+            self._solve(a)  # env already is M_a (written by the leaf absorption)
+            return
+        m = (a + b) // 2
+        cur, sa, sb = env, a, b
+        while sb > m:
+            leaf = a if (sa == a and sb == a + 1 and m == a) else None
+            cur, sa, sb = self._absorb_right(cur, sa, sb, leaf)
+        self._tree(cur, a, m)
+        cur, sa, sb = env, a, b
+        while sa <= m:
+            leaf = b if (sa + 1 == b and m + 1 == b) else None
+            cur, sa, sb = self._absorb_left(cur, sa, sb, leaf)
+        self._tree(cur, m + 1, b)
+
+    def _solve(self, n):
+        """Steps for one block update once M_n is complete (local rows)."""
+        N = self.N
+        rr = self.R(n) * self.R(n + 1)
+        S, M = self.S[n], self.M[n]
+        if self.world > 1:
+            import torch.distributed as dist
+            self.steps.append(Step("mttsp", lambda M=M: dist.all_reduce(M, group=self.group), f"allreduce M{n}"))
+        ranks_a = L.i32_array(self.ranks)
+        rmax = max(self.ranks)
+        self._ws(self.lib.trals_gemm_ws_elems(1, rmax ** 2, rmax ** 2, rmax ** 2))
+
+        def gram_chain(n=n, S=S, ranks_a=ranks_a):
+            E = L.ptr_array([e.data_ptr() for e in self.E])
+            L.check(self.lib.trals_gram_chain_f64(N, n, ranks_a, E, S.data_ptr(), self.chain_tmp.data_ptr(),
+                                                  self.gws.data_ptr(), self.gws.numel(), self._sp()), "gram_chain")
+        self.steps.append(Step("other", gram_chain, f"S{n}"))
+        check_degen = 1 if self.variant == "qr" else 0
+
+        def solve(n=n, S=S, M=M, rr=rr, check_degen=check_degen):
+            L.check(self.lib.trals_cholesky_f64(S.data_ptr(), rr, self.U.data_ptr(), self.Lo.data_ptr(), check_degen,
+                                                self.info.data_ptr(), self._sp()), "cholesky")
+            L.check(self.lib.trals_chol_solve_f64(self.U.data_ptr(), self.Lo.data_ptr(), rr, M.data_ptr(),
+                                                  self.dims[n], self.Gt[n].data_ptr(), self._sp()), "chol_solve")
+        self.steps.append(Step("solve", solve, f"solve{n}"))
+
+        def refresh(n=n):
+            ra, i, rb = self.R(n), self.dims[n], self.R(n + 1)
+            sp = self._sp()
+            L.check(self.lib.trals_core_relayout_f64(self.Gt[n].data_ptr(), L.LAYOUT_ZT, ra, i, rb,
+                                                     self.Gc[n].data_ptr(), L.LAYOUT_C, sp), "relayout")
+            L.check(self.lib.trals_core_relayout_f64(self.Gt[n].data_ptr(), L.LAYOUT_ZT, ra, i, rb,
+                                                     self.Gs[n].data_ptr(), L.LAYOUT_SLICE, sp), "relayout")
+            if self.s is not None and n == self.s:
+                L.check(self.lib.trals_core_relayout_f64(self.core_zt(n).data_ptr(), L.LAYOUT_ZT, ra,
+                                                         self.hi - self.lo, rb, self.Gc_loc.data_ptr(),
+                                                         L.LAYOUT_C, sp), "relayout")
+            L.check(self.lib.trals_core_gram_f64(self.Gs[n].data_ptr(), ra, i, rb, self.E[n].data_ptr(),
+                                                 self.gws.data_ptr(), self.gws.numel(), sp), "core_gram")
+        self._ws(self.lib.trals_gemm_ws_elems(1, rr, self.dims[n], rr))
+        self.steps.append(Step("gramqr", refresh, f"refresh{n}"))
+
+    # ----------------------------------------------------------------- running
+    def _sp(self):
+        return int(self.stream.cuda_stream)
+
+    def set_cores(self, cores_host):
+        """Upload C-order host cores and derive every layout + Gram (the 'prepare' of solvers.py:366-367)."""
+        sp = self._sp()
+        for j, g in enumerate(cores_host):
+            t = torch.as_tensor(g, dtype=torch.float64)
+            self.Gc[j].copy_(t, non_blocking=False)
+        for j in range(self.N):
+            self._derive(j, sp)
+
+    def _derive(self, j, sp):
+        ra, i, rb = self.R(j), self.dims[j], self.R(j + 1)
+        L.check(self.lib.trals_core_relayout_f64(self.Gc[j].data_ptr(), L.LAYOUT_C, ra, i, rb,
+                                                 self.Gs[j].data_ptr(), L.LAYOUT_SLICE, sp), "relayout")
+        L.check(self.lib.trals_core_relayout_f64(self.Gc[j].data_ptr(), L.LAYOUT_C, ra, i, rb,
+                                                 self.Gt[j].data_ptr(), L.LAYOUT_ZT, sp), "relayout")
+        if self.s is not None and j == self.s:
+            L.check(self.lib.trals_core_relayout_f64(self.core_zt(j).data_ptr(), L.LAYOUT_ZT, ra,
+                                                     self.hi - self.lo, rb, self.Gc_loc.data_ptr(), L.LAYOUT_C,
+                                                     sp), "relayout")
+        need = self.lib.trals_gemm_ws_elems(1, ra * rb, i, ra * rb)
+        if need > self.gws.numel():
+            self.gws = self._empty(need)
+        L.check(self.lib.trals_core_gram_f64(self.Gs[j].data_ptr(), ra, i, rb, self.E[j].data_ptr(),
+                                             self.gws.data_ptr(), self.gws.numel(), sp), "core_gram")
+
+    def compute_xnorm2(self):
+        L.check(self.lib.trals_sumsq_f64(self.x.data_ptr(), self.x.numel(), self.xnorm2.data_ptr(),
+                                         self.sumsq_ws.data_ptr(), self._sp()), "sumsq")
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.all_reduce(self.xnorm2, group=self.group)
+        return self.xnorm2
+
+    def run_sweep(self, events=None):
+        """Launch one full sweep; if `events` is a list, append (bucket, event) pairs at bucket changes."""
+        prev = None
+        for st in self.steps:
+            if events is not None and st.bucket != prev:
+                ev = torch.cuda.Event(enable_timing=True)
+                ev.record(self.stream)
+                events.append((st.bucket, ev))
+                prev = st.bucket
+            st.fn()
+
+    def error_step(self, out):
+        """Cheap-error terms after a sweep into `out` (3 doubles): [e, <M,Z>, <S,Z^T Z>]."""
+        N = self.N
+        n = N - 1
+        rr = self.R(n) * self.R(n + 1)
+        L.check(self.lib.trals_error_terms_f64(self.M[n].data_ptr(), self.Gt[n].data_ptr(), self.S[n].data_ptr(),
+                                               self.dims[n], rr, self.xnorm2.data_ptr(), out.data_ptr(),
+                                               self.err_ws.data_ptr(), self.err_ws.numel(), self._sp()),
+                "error_terms")
+
+    def cores_host(self):
+        return [g.detach().cpu().numpy().copy() for g in self.Gc]
+
+    def mttsp_flops_per_sweep(self):
+        """Algorithmic RHS flops of one sweep: sum_n 2 |X| R_n R_{n+1}."""
+        tot = _prod(self.dims)
+        return sum(2.0 * tot * self.R(n) * self.R(n + 1) for n in range(self.N))

@@ -1,0 +1,274 @@
+"""Drop-in TR-ALS solvers (NE / QR / QRNE) running on the B200 engine.
+
+Mirrors the reference's public surface for the north-star path
+(pkg/src/tenring/solvers.py): `AlsConfig` (:60-104), `AlsReport`
+(:107-133), `tr_als_ne` (:352-391), `tr_als_qr` (:403-451), `tr_als_qrne`
+(:454-501) and `decompose` (:504-520), with the same arguments, defaults,
+validation errors, zero-input rule, seeded initial cores (numpy Philox, the
+exact draws of ring.random_cores) and returned objects.  The sweep itself
+runs in `engine.SweepEngine` on the GPU; there is no CPU path.
+"""
+
+from __future__ import annotations
+
+import math
+import os
+from dataclasses import dataclass, field
+from time import perf_counter
+
+import numpy as np
+
+from . import _lib as L
+from .errors import DegenerateTriangularError, ElementBudgetError, StaleCacheError  # noqa: F401
+from .host import (check_dense_tensor, check_element_budget, check_ranks, core_ranks, make_rng,
+                   random_cores, validate_cores, zero_cores)
+
+VARIANTS = ("als", "ne", "qr", "qrne")          # solvers.py:55
+DEVICE_VARIANTS = ("ne", "qr", "qrne")
+ERROR_MODES = ("exact", "cheap", "none")         # solvers.py:56
+BUCKETS = ("subchain", "mttsp", "solve", "gramqr", "other")  # solvers.py:57
+SVD_RCOND_DEFAULT = 1e-12                        # linalg.py:20
+
+
+@dataclass
+class AlsConfig:
+    """Same fields and defaults as the reference AlsConfig (solvers.py:60-104).
+
+    `shard_mode` (extension) selects the mode X is split along when the call
+    runs inside an initialised torch.distributed NCCL group (one process per
+    GPU); it is ignored for single-process runs.
+    """
+
+    ranks: tuple
+    max_iters: int = 20
+    tol: float = 0.0
+    seed: object = None
+    error_mode: str = "exact"
+    rank_deficient_fallback: bool = True
+    init_cores: list = None
+    element_budget: int = None
+    svd_rcond: float = SVD_RCOND_DEFAULT
+    debug_checks: bool = False
+    shard_mode: int = 1
+    timing_buckets: bool = True
+
+
+@dataclass
+class AlsReport:
+    """solvers.py:107-133; timings are CUDA-event device times."""
+
+    variant: str
+    errors: list = field(default_factory=list)
+    iter_seconds: list = field(default_factory=list)
+    iter_buckets: list = field(default_factory=list)
+    upfront_seconds: dict = field(default_factory=dict)
+    termination: str = ""
+    fallback_count: int = 0
+
+    @property
+    def n_iters(self):
+        return len(self.iter_seconds)
+
+    @property
+    def final_error(self):
+        return self.errors[-1] if self.errors else None
+
+
+def _validate(x, config, variant):
+    """solvers.py:224-246 validation order and messages."""
+    if variant not in VARIANTS:
+        raise ValueError(f"unknown variant {variant!r}; expected one of {VARIANTS}")
+    if config.error_mode not in ERROR_MODES:
+        raise ValueError(f"unknown error_mode {config.error_mode!r}; expected one of {ERROR_MODES}")
+    if config.tol > 0 and config.error_mode == "none":
+        raise ValueError("tol-based termination needs error tracking enabled")
+    if config.max_iters < 1:
+        raise ValueError("max_iters must be at least 1")
+
+
+def _as_device_tensor(x):
+    import torch
+    if isinstance(x, torch.Tensor):
+        t = x.detach()
+        if not t.is_cuda:
+            t = t.to(torch.float64)
+        return t
+    return None
+
+
+def _run(x, config, variant):
+    import torch
+
+    _validate(x, config, variant)
+    if variant not in DEVICE_VARIANTS:
+        raise NotImplementedError("tr_als (Alg. 1) is outside the B200 hot path; use ne/qr/qrne")
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2210_11362_b200 needs a CUDA device (no CPU fallback)")
+    L.lib()  # fail loudly if the extension is missing
+
+    tx = _as_device_tensor(x)
+    if tx is not None and tx.is_cuda:
+        # device input: validate on the device, avoid a host copy
+        if tx.dim() < 2:
+            raise ValueError(f"tensor order {tx.dim()} is below the minimum 2")
+        if tx.numel() == 0:
+            raise ValueError("tensor has no elements")
+        xd = tx.to(torch.float64).contiguous()
+        if not bool(torch.isfinite(xd).all()):
+            raise ValueError("tensor contains non-finite entries")
+        dims = tuple(xd.shape)
+    else:
+        xh = check_dense_tensor(x if tx is None else tx.numpy(), min_order=2)
+        dims = xh.shape
+        xd = None
+    N = len(dims)
+    ranks = check_ranks(config.ranks, N)
+    if config.error_mode == "exact":
+        check_element_budget(dims, config.element_budget)
+
+    report = AlsReport(variant=variant)
+    dist = _dist_context()
+    if dist is None:
+        if xd is None:
+            xd = torch.from_numpy(np.ascontiguousarray(xh)).to("cuda", non_blocking=False)
+        shard, lo, hi, world, group = None, 0, None, 1, None
+        x_local = xd
+    else:
+        world, rank, group = dist
+        shard = int(config.shard_mode) % N
+        I = dims[shard]
+        lo, hi = _slab(I, world, rank)
+        src = xd if xd is not None else torch.from_numpy(np.ascontiguousarray(xh))
+        idx = [slice(None)] * N
+        idx[shard] = slice(lo, hi)
+        x_local = src[tuple(idx)].contiguous().to("cuda")
+
+    from .engine import SweepEngine
+    eng = SweepEngine(x_local, dims, ranks, variant, shard_mode=shard, lo=lo, hi=hi, group=group,
+                      world_size=world)
+    xnorm2 = float(eng.compute_xnorm2().item())
+    if xnorm2 == 0.0:  # solvers.py:289-291
+        report.termination = "zero_input"
+        return zero_cores(dims, ranks), report
+
+    # initial cores (solvers.py:248-257)
+    if config.init_cores is not None:
+        cores0 = validate_cores(config.init_cores, dims=dims)
+        got = core_ranks(cores0)
+        if got != tuple(ranks):
+            raise ValueError(f"init cores have ranks {got}, expected {tuple(ranks)}")
+        cores0 = [g.copy() for g in cores0]
+    else:
+        cores0 = random_cores(dims, ranks, make_rng(config.seed))
+
+    stream = eng.stream
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    eng.set_cores(cores0)
+    t1.record(stream)
+
+    track = config.error_mode in ("exact", "cheap")
+    errs = torch.zeros((config.max_iters, 3), dtype=torch.float64, device=x_local.device)
+    sweep_events = []
+    report.termination = "max_iters"
+    done = 0
+    for k in range(config.max_iters):
+        ev = [] if config.timing_buckets else None
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        eng.run_sweep(ev)
+        b.record(stream)
+        sweep_events.append((a, b, ev))
+        if track:
+            eng.error_step(errs[k])
+        done = k + 1
+        if config.tol > 0 and k >= 1:
+            e = errs[k - 1:k + 1, 0].cpu().numpy()
+            if abs(e[0] - e[1]) < config.tol:
+                report.termination = "tol"
+                break
+    torch.cuda.synchronize(x_local.device)
+    _raise_on_info(eng, config, report)
+    report.upfront_seconds["gramqr"] = t0.elapsed_time(t1) / 1e3
+    for a, b, ev in sweep_events:
+        report.iter_seconds.append(a.elapsed_time(b) / 1e3)
+        buckets = dict.fromkeys(BUCKETS, 0.0)
+        if ev:
+            marks = ev + [(None, b)]
+            for (bk, e0), (_, e1) in zip(marks[:-1], marks[1:]):
+                buckets[bk] += e0.elapsed_time(e1) / 1e3
+        report.iter_buckets.append(buckets)
+    if track:
+        report.errors = [float(v) for v in errs[:done, 0].cpu().numpy()]
+    return eng.cores_host(), report
+
+
+def _raise_on_info(eng, config, report):
+    info = eng.info.cpu().numpy()
+    if info[L.INFO_ASYM]:
+        raise ValueError("matrix is not symmetric within 1e-8 relative")  # linalg.py:70-72
+    if info[L.INFO_CHOL]:
+        # the reference falls back to a pivoted least-squares solve (linalg.py:77-81)
+        raise np.linalg.LinAlgError(
+            f"normal-equation matrix not positive definite at pivot {int(info[L.INFO_CHOL])}; "
+            "the device least-squares fallback is not available in this build")
+    if info[L.INFO_DEGEN]:
+        idx = int(info[L.INFO_DEGEN]) - 1
+        if not config.rank_deficient_fallback:
+            raise DegenerateTriangularError(idx, 0.0, 0.0)
+        raise np.linalg.LinAlgError("degenerate triangular factor; device SVD fallback not available in this build")
+
+
+def _dist_context():
+    try:
+        import torch.distributed as dist
+    except Exception:  # pragma: no cover
+        return None
+    if not (dist.is_available() and dist.is_initialized()):
+        return None
+    world = dist.get_world_size()
+    if world <= 1:
+        return None
+    return world, dist.get_rank(), None
+
+
+def _slab(I, world, rank):
+    base, extra = divmod(I, world)
+    lo = rank * base + min(rank, extra)
+    hi = lo + base + (1 if rank < extra else 0)
+    return lo, hi
+
+
+def tr_als_ne(x, config):
+    """Normal-equation sweep (Alg. 2; reference solvers.py:352-391). Returns (cores, report)."""
+    return _run(x, config, "ne")
+
+
+def tr_als_qr(x, config):
+    """QR-stabilised sweep (Alg. 3; reference solvers.py:403-451). Returns (cores, report)."""
+    return _run(x, config, "qr")
+
+
+def tr_als_qrne(x, config):
+    """Compressed NE sweep (Alg. 4; reference solvers.py:454-501). Returns (cores, report)."""
+    return _run(x, config, "qrne")
+
+
+def tr_als(x, config):
+    """Alg. 1 is not on the B200 path (reference solvers.py:323-349)."""
+    _validate(x, config, "als")
+    raise NotImplementedError("tr_als (Alg. 1) is outside the B200 hot path; use ne/qr/qrne")
+
+
+_SOLVERS = {"als": tr_als, "ne": tr_als_ne, "qr": tr_als_qr, "qrne": tr_als_qrne}
+
+
+def decompose(x, variant, config):
+    """Run the named solver variant (reference solvers.py:504-520)."""
+    try:
+        solver = _SOLVERS[variant]
+    except KeyError:
+        raise ValueError(f"unknown variant {variant!r}; expected one of {VARIANTS}") from None
+    return solver(x, config)

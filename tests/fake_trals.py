@@ -1,0 +1,234 @@
+"""Numpy model of the libtrals C-ABI -- TEST INFRASTRUCTURE ONLY.
+
+Implements every entry point of include/trals.h from its documented
+semantics (independently of the CUDA code), operating on raw host pointers
+(CPU torch tensors).  Injected into `SweepEngine(_test_lib=FakeTrals())`, it
+lets the CPU test suite execute the engine's exact step list -- the
+environment-tree schedule, the index conventions, the shard/all-reduce logic
+-- and compare the sweep with the oracle without a GPU.  It is never used by
+the product path.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import scipy.linalg as sla
+
+
+def _arr(ptr, n):
+    ptr = int(ptr.value if isinstance(ptr, ctypes.c_void_p) else ptr)
+    return np.ctypeslib.as_array((ctypes.c_double * int(n)).from_address(ptr))
+
+
+def _iarr(ptr, n):
+    ptr = int(ptr.value if isinstance(ptr, ctypes.c_void_p) else ptr)
+    return np.ctypeslib.as_array((ctypes.c_int32 * int(n)).from_address(ptr))
+
+
+def _vals(a, n):
+    return [int(a[i]) for i in range(n)]
+
+
+def _ptrs(a, n):
+    return [int(a[i]) for i in range(n)]
+
+
+class FakeTrals:
+    def __init__(self):
+        self.calls = {}
+
+    def _count(self, name):
+        self.calls[name] = self.calls.get(name, 0) + 1
+
+    # --- helpers ---------------------------------------------------------
+    def trals_strerror(self, code):
+        return b"fake"
+
+    def trals_version(self):
+        return 1
+
+    def trals_gemm_ws_elems(self, P, M, K, N):
+        return 0
+
+    def trals_sumsq_ws_elems(self):
+        return 4
+
+    def trals_error_ws_elems(self, rows, m):
+        return 1
+
+    def trals_half_chain_tmp_elems(self, nblk, dims, ranks):
+        return 1
+
+    # --- generic GEMM ----------------------------------------------------
+    def trals_gemm_f64(self, A, sAp, sAm, sAk, P, M, K, N, B, ldb, C, cmap, beta, ws, ws_elems, stream):
+        self._count("gemm")
+        cm = [int(cmap[i]) for i in range(7)]
+        amax = (P - 1) * sAp + (M - 1) * sAm + (K - 1) * sAk + 1
+        a = _arr(A, amax)
+        av = np.lib.stride_tricks.as_strided(a, shape=(P, M, K), strides=(sAp * 8, sAm * 8, sAk * 8))
+        b = _arr(B, (K - 1) * ldb + N)
+        bv = np.lib.stride_tricks.as_strided(b, shape=(K, N), strides=(ldb * 8, 8))
+        res = np.einsum("pmk,kn->pmn", av, bv)
+        p = np.arange(P)[:, None, None]
+        m = np.arange(M)[None, :, None]
+        n = np.arange(N)[None, None, :]
+        addr = p * cm[0] + (m // cm[1]) * cm[2] + (m % cm[1]) * cm[3] + (n // cm[4]) * cm[5] + (n % cm[4]) * cm[6]
+        c = _arr(C, int(addr.max()) + 1)
+        if beta:
+            c[addr] += res
+        else:
+            c[addr] = res
+        return 0
+
+    # --- layouts ---------------------------------------------------------
+    @staticmethod
+    def _to_canon(buf, layout, Ra, I, Rb):
+        if layout == 0:
+            return buf.reshape(Ra, I, Rb)
+        if layout == 1:
+            return buf.reshape(I, Ra, Rb).transpose(1, 0, 2)
+        return buf.reshape(I, Rb, Ra).transpose(2, 0, 1)
+
+    @staticmethod
+    def _from_canon(g, layout):
+        if layout == 0:
+            return g
+        if layout == 1:
+            return g.transpose(1, 0, 2)
+        return g.transpose(1, 2, 0)
+
+    def trals_core_relayout_f64(self, src, sl, Ra, I, Rb, dst, dl, stream):
+        self._count("relayout")
+        n = Ra * I * Rb
+        g = self._to_canon(_arr(src, n).copy(), sl, Ra, I, Rb)
+        _arr(dst, n)[:] = np.ascontiguousarray(self._from_canon(g, dl)).ravel()
+        return 0
+
+    # --- ring pieces -----------------------------------------------------
+    def trals_half_chain_f64(self, nblk, dims, ranks, first_slice, cores_c, out, tmp, ws, ws_elems, stream):
+        self._count("half_chain")
+        d = _vals(dims, nblk)
+        r = _vals(ranks, nblk + 1)
+        cc = _ptrs(cores_c, nblk) if nblk > 1 else []
+        h = _arr(first_slice, d[0] * r[0] * r[1]).reshape(d[0], r[0], r[1]).copy()
+        for j in range(1, nblk):
+            g = _arr(cc[j], r[j] * d[j] * r[j + 1]).reshape(r[j], d[j], r[j + 1])
+            h = np.einsum("pat,tic->piac", h, g).reshape(-1, r[0], r[j + 1])
+        _arr(out, h.size)[:] = h.ravel()
+        return 0
+
+    def trals_env_f64(self, X, pre, post, side, H, r_lo, r_hi, E, leaf, ws, ws_elems, stream):
+        self._count("env")
+        x = _arr(X, pre * post).reshape(pre, post)
+        if side == 0:
+            h = _arr(H, post * r_lo * r_hi).reshape(post, r_lo, r_hi)   # [k][r_y][r_0]
+            env = np.einsum("mk,kyz->zmy", x, h)                         # [r_0][m][r_y]
+            if leaf:  # M_0[i][r_0 + R_0 r_1]
+                out = env.transpose(1, 2, 0).reshape(pre, -1)          # [m][r_y][r_0]
+            else:
+                out = env
+        else:
+            h = _arr(H, pre * r_lo * r_hi).reshape(pre, r_lo, r_hi)    # [k][r_0][r_x1]
+            env = np.einsum("km,kzx->xmz", x, h)                         # [r_x1][m][r_0]
+            if leaf:  # M_{N-1}[i][r_{N-1} + R_{N-1} r_0]
+                out = env.transpose(1, 2, 0).reshape(post, -1)
+            else:
+                out = env
+        _arr(E, out.size)[:] = np.ascontiguousarray(out).ravel()
+        return 0
+
+    def trals_absorb_right_f64(self, E, Ra, pre, Ib, Rb, Rb1, core_zt, out, leaf, ws, ws_elems, stream):
+        self._count("absorb_right")
+        e = _arr(E, Ra * pre * Ib * Rb1).reshape(Ra, pre, Ib, Rb1)
+        gt = _arr(core_zt, Ib * Rb1 * Rb).reshape(Ib, Rb1, Rb)
+        o = np.einsum("apir,irb->apb", e, gt)                           # [r_a][pre][r_b]
+        if leaf:
+            o = o.transpose(1, 2, 0).reshape(pre, Rb * Ra)              # [i_a][r_b][r_a]
+        _arr(out, o.size)[:] = np.ascontiguousarray(o).ravel()
+        return 0
+
+    def trals_absorb_left_f64(self, E, Ra, Ia, rest, Ra1, Rb1, core_c, out, leaf, ws, ws_elems, stream):
+        self._count("absorb_left")
+        e = _arr(E, Ra * Ia * rest * Rb1).reshape(Ra, Ia, rest, Rb1)
+        g = _arr(core_c, Ra * Ia * Ra1).reshape(Ra, Ia, Ra1)
+        o = np.einsum("airz,aic->crz", e, g)                            # [r_a1][rest][r_b1]
+        if leaf:
+            o = o.transpose(1, 2, 0).reshape(rest, Rb1 * Ra1)           # [i_b][r_b1][r_b]
+        _arr(out, o.size)[:] = np.ascontiguousarray(o).ravel()
+        return 0
+
+    def trals_core_gram_f64(self, Gs, Ra, I, Rb, E, ws, ws_elems, stream):
+        self._count("core_gram")
+        g = _arr(Gs, I * Ra * Rb).reshape(I, Ra, Rb)
+        e = np.einsum("iab,icd->acbd", g, g).reshape(Ra * Ra, Rb * Rb)
+        _arr(E, e.size)[:] = e.ravel()
+        return 0
+
+    def trals_gram_chain_f64(self, N, n, ranks, E, S, tmp, ws, ws_elems, stream):
+        self._count("gram_chain")
+        r = _vals(ranks, N)
+        es = _ptrs(E, N)
+        order = list(range(n + 1, N)) + list(range(n))
+        F = None
+        for j in order:
+            Rj, Rj1 = r[j], r[(j + 1) % N]
+            e = _arr(es[j], Rj * Rj * Rj1 * Rj1).reshape(Rj * Rj, Rj1 * Rj1)
+            F = e.copy() if F is None else F @ e
+        Rn, Rn1 = r[n], r[(n + 1) % N]
+        f = F.reshape(Rn1, Rn1, Rn, Rn)                                  # [x][y][b][d]
+        s = f.transpose(0, 2, 1, 3)  # [x][b][y][d]: row (x, b) = b + Rn*x, col (y, d) = d + Rn*y
+        s = s.reshape(Rn1 * Rn, Rn1 * Rn)
+        _arr(S, s.size)[:] = s.ravel()
+        return 0
+
+    def trals_cholesky_f64(self, S, m, U, Lo, check_degen, info, stream):
+        self._count("cholesky")
+        s = _arr(S, m * m).reshape(m, m)
+        inf = _iarr(info, 4)
+        scale = np.max(np.abs(s))
+        if scale > 0 and np.max(np.abs(s - s.T)) > 1e-8 * scale:
+            inf[1] = 1
+        sym = 0.5 * (s + s.T)
+        try:
+            u = sla.cholesky(sym, lower=False)
+        except np.linalg.LinAlgError:
+            inf[0] = 1
+            return 0
+        _arr(U, m * m)[:] = u.ravel()
+        _arr(Lo, m * m)[:] = u.T.ravel()
+        if check_degen:
+            d = np.abs(np.diagonal(u))
+            if d.min() <= 1e-13 * np.max(np.abs(u)):
+                inf[2] = int(np.argmin(d)) + 1
+        return 0
+
+    def trals_chol_solve_f64(self, U, Lo, m, M, rows, Z, stream):
+        self._count("chol_solve")
+        u = _arr(U, m * m).reshape(m, m)
+        rhs = _arr(M, rows * m).reshape(rows, m)
+        y = sla.solve_triangular(u, rhs.T, trans="T", lower=False)
+        z = sla.solve_triangular(u, y, lower=False).T
+        _arr(Z, rows * m)[:] = z.ravel()
+        return 0
+
+    def trals_sumsq_f64(self, x, n, out, ws, stream):
+        self._count("sumsq")
+        v = _arr(x, n)
+        _arr(out, 1)[0] = float(np.dot(v, v))
+        return 0
+
+    def trals_error_terms_f64(self, M, Z, S, rows, m, xnorm2, out, ws, ws_elems, stream):
+        self._count("error_terms")
+        mm = _arr(M, rows * m).reshape(rows, m)
+        z = _arr(Z, rows * m).reshape(rows, m)
+        s = _arr(S, m * m).reshape(m, m)
+        cross = float(np.vdot(mm, z))
+        model = float(np.vdot(s, z.T @ z))
+        x2 = float(_arr(xnorm2, 1)[0])
+        xn = np.sqrt(x2)
+        e = 0.0 if xn == 0 else np.sqrt(max(0.0, xn * xn - 2 * cross + model)) / xn
+        o = _arr(out, 3)
+        o[0], o[1], o[2] = e, cross, model
+        return 0

@@ -1,0 +1,136 @@
+"""GPU parity of the individual sm_100a operators against the oracle / numpy (fp64)."""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import golden_cores, load_golden, rel
+from oracle import tenring_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+SMALL = ["spec_n3_i30_r3", "nonuni_n4", "n5_i6", "n2_mat", "odd_n3"]
+
+
+def cuda(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).cuda()
+
+
+@pytest.mark.parametrize("P,M,K,N,ak", [
+    (1, 128, 64, 64, True), (1, 300, 77, 50, True), (1, 1000, 1000, 400, True), (1, 37, 5000, 25, True),
+    (3, 70, 33, 100, False), (1, 513, 129, 8, False), (2, 64, 4096, 24, True), (1, 257, 31, 1, True),
+    (1, 100, 100, 112, False), (1, 5, 3, 7, True),
+])
+def test_gemm_engine(P, M, K, N, ak):
+    from paper_2210_11362_b200 import ops
+    rng = np.random.default_rng(P * 1000 + M + K + N)
+    if ak:
+        a = rng.standard_normal((P, M, K))
+        sAp, sAm, sAk = M * K, K, 1
+    else:
+        a = rng.standard_normal((P, K, M))
+        sAp, sAm, sAk = M * K, 1, M
+    b = rng.standard_normal((K, N))
+    ref = np.einsum("pmk,kn->pmn", a if ak else a.transpose(0, 2, 1), b)
+    C = torch.zeros(P * M * N, dtype=torch.float64, device="cuda")
+    ops.gemm(cuda(a), sAp, sAm, sAk, P, M, K, N, cuda(b), N, C, [M * N, 1 << 30, 0, N, 1 << 30, 0, 1])
+    got = C.cpu().numpy().reshape(P, M, N)
+    assert rel(got, ref) < 1e-14
+
+
+def test_gemm_cmap_scatter_and_beta():
+    from paper_2210_11362_b200 import ops
+    rng = np.random.default_rng(3)
+    M, K, N = 12, 9, 6  # m = (m1, m2) with M2 = 4; n = (n1, n2) with N2 = 3
+    a, b = rng.standard_normal((M, K)), rng.standard_normal((K, N))
+    ref = (a @ b).reshape(3, 4, 2, 3)  # [m1][m2][n1][n2]
+    out = np.zeros((2, 4, 3, 3))       # dst [n1][m2][n2][m1]
+    cm = [0, 4, 1, 3 * 3, 3, 4 * 3 * 3, 3]
+    C = cuda(out)
+    ops.gemm(cuda(a), 0, K, 1, 1, M, K, N, cuda(b), N, C, cm)
+    ops.gemm(cuda(a), 0, K, 1, 1, M, K, N, cuda(b), N, C, cm, beta=1)
+    np.testing.assert_allclose(C.cpu().numpy(), 2 * ref.transpose(2, 1, 3, 0), rtol=1e-14, atol=1e-13)
+
+
+@pytest.mark.parametrize("name", SMALL)
+def test_mttsp_every_mode(name):
+    from paper_2210_11362_b200 import ops
+    g = load_golden(name)
+    dims = tuple(int(d) for d in g["dims"])
+    N = len(dims)
+    init = golden_cores(g, "init", N)
+    x = cuda(g["x"])
+    cores = [cuda(c) for c in init]
+    for n in range(N):
+        got = ops.mttsp(x, cores, n).cpu().numpy()
+        assert rel(got, g[f"mttsp_{n}"]) < 1e-13, n
+
+
+@pytest.mark.parametrize("dims,ranks", [((40, 30, 50), (5, 4, 6)), ((12, 10, 9, 11), (3, 4, 2, 5)),
+                                        ((6, 5, 7, 4, 6), (2, 3, 2, 2, 3)), ((64, 64, 64, 64), (8, 8, 8, 8))])
+def test_mttsp_random_shapes(dims, ranks):
+    from paper_2210_11362_b200 import ops
+    rng = np.random.default_rng(len(dims))
+    x = rng.standard_normal(dims)
+    cores = O.gaussian_ring(dims, ranks, O.philox(1))
+    xt, ct = cuda(x), [cuda(c) for c in cores]
+    for n in range(len(dims)):
+        assert rel(ops.mttsp(xt, ct, n).cpu().numpy(), O.mttsp(x, cores, n)) < 1e-13
+
+
+@pytest.mark.parametrize("name", SMALL)
+def test_coefficient_gram(name):
+    from paper_2210_11362_b200 import ops
+    g = load_golden(name)
+    N = len(g["dims"])
+    cores = [cuda(c) for c in golden_cores(g, "init", N)]
+    for n in range(N):
+        assert rel(ops.coefficient_gram(cores, n).cpu().numpy(), g[f"S_{n}"]) < 1e-13
+
+
+@pytest.mark.parametrize("m,rows", [(4, 7), (25, 100), (64, 64), (100, 500), (400, 160), (9, 3), (130, 33)])
+def test_cholesky_solve(m, rows):
+    from paper_2210_11362_b200 import ops
+    rng = np.random.default_rng(m)
+    a = rng.standard_normal((3 * m, m))
+    s = a.T @ a
+    rhs = rng.standard_normal((rows, m))
+    U, Lo, info = ops.cholesky(cuda(s))
+    assert info.cpu().numpy().tolist() == [0, 0, 0, 0]
+    ref_u = np.linalg.cholesky(s).T
+    assert rel(U.cpu().numpy(), ref_u) < 1e-12
+    z = ops.chol_solve(U, Lo, cuda(rhs)).cpu().numpy()
+    zref, _ = O.solve_spd_right(s, rhs)
+    assert rel(z, zref) < 1e-11
+
+
+def test_cholesky_flags():
+    from paper_2210_11362_b200 import ops
+    s = np.diag([1.0, 2.0, -1.0, 3.0])
+    _, _, info = ops.cholesky(cuda(s))
+    assert info.cpu().numpy()[0] == 3  # first non-positive pivot, 1-based
+    s = np.eye(3)
+    s[0, 2] = 1e-3
+    _, _, info = ops.cholesky(cuda(s))
+    assert info.cpu().numpy()[1] == 1  # asymmetric beyond 1e-8
+    s = np.diag([1.0, 1e-30, 1.0])
+    _, _, info = ops.cholesky(cuda(s), check_degen=True)
+    assert info.cpu().numpy()[2] == 2  # below the 1e-13 floor
+
+
+def test_sumsq_and_error_terms():
+    from paper_2210_11362_b200 import ops
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal(1_000_003)
+    assert abs(ops.sumsq(cuda(x)).item() - np.dot(x, x)) < 1e-10 * np.dot(x, x)
+    m, rows = 36, 50
+    a = rng.standard_normal((90, m))
+    s = a.T @ a
+    z = rng.standard_normal((rows, m))
+    M = z @ s + 1e-3 * rng.standard_normal((rows, m))
+    x2 = torch.tensor([1e4], dtype=torch.float64, device="cuda")
+    out = ops.error_terms(cuda(M), cuda(z), cuda(s), x2).cpu().numpy()
+    cross, model = float(np.vdot(M, z)), float(np.vdot(s, z.T @ z))
+    assert abs(out[1] - cross) < 1e-10 * abs(cross)
+    assert abs(out[2] - model) < 1e-10 * abs(model)
+    assert abs(out[0] - O.residual_from_sweep(100.0, cross, model)) < 1e-12

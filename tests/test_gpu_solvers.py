@@ -1,0 +1,88 @@
+"""GPU parity of the drop-in solvers against the reference goldens and the oracle.
+
+Tolerances (north_star): per-sweep relative error within 1e-9 absolute, cores
+within 1e-6 relative Frobenius for the first 10 sweeps (fp64).
+"""
+
+import numpy as np
+import pytest
+
+from conftest import golden_cores, load_golden, rel
+from oracle import tenring_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+SMALL = ["spec_n3_i30_r3", "nonuni_n4", "n5_i6", "n2_mat", "odd_n3"]
+
+
+@pytest.mark.parametrize("name", SMALL)
+@pytest.mark.parametrize("variant", ["ne", "qr", "qrne"])
+@pytest.mark.parametrize("mode", ["cheap", "exact"])
+def test_small_goldens(name, variant, mode):
+    from paper_2210_11362_b200 import AlsConfig, decompose
+    g = load_golden(name)
+    if f"{variant}_{mode}_errors" not in g:
+        pytest.skip("variant not in fixture")
+    dims = tuple(int(d) for d in g["dims"])
+    N = len(dims)
+    ranks = tuple(int(r) for r in g["ranks"])
+    cfg = AlsConfig(ranks=ranks, max_iters=int(g["sweeps"]), init_cores=golden_cores(g, "init", N), error_mode=mode)
+    cores, rep = decompose(g["x"], variant, cfg)
+    assert rep.variant == variant and rep.termination == "max_iters"
+    assert len(rep.iter_seconds) == int(g["sweeps"]) and set(rep.iter_buckets[0]) == {
+        "subchain", "mttsp", "solve", "gramqr", "other"}
+    np.testing.assert_allclose(rep.errors, g[f"{variant}_{mode}_errors"], rtol=0, atol=1e-9)
+    for j in range(N):
+        assert cores[j].shape == g[f"{variant}_core_{j}"].shape
+        assert rel(cores[j], g[f"{variant}_core_{j}"]) < 1e-6
+
+
+@pytest.mark.parametrize("name", ["c1", "c2"])
+def test_baseline_configs(name):
+    from paper_2210_11362_b200 import AlsConfig, decompose
+    g = load_golden(f"base_{name}")
+    order, dim, rt, sd, rf, si, sweeps = (int(v) for v in g["recipe"])
+    x, _ = O.synth(O.Recipe(order=order, dim=dim, rank=rt, noise=float(g["noise"]), seed=sd))
+    for v in ("ne", "qr"):
+        if f"{v}_exact_errors" not in g:
+            continue
+        cores, rep = decompose(x, v, AlsConfig(ranks=(rf,) * order, max_iters=sweeps, seed=si))
+        np.testing.assert_allclose(rep.errors, g[f"{v}_exact_errors"], rtol=0, atol=1e-9)
+        for j in range(order):
+            assert rel(cores[j], g[f"{v}_core_{j}"]) < 1e-6
+
+
+def test_one_sweep_from_reference_state_c2():
+    from paper_2210_11362_b200 import AlsConfig, tr_als_ne
+    g = load_golden("base_c2")
+    order, dim, rt, sd, rf, si, sweeps = (int(v) for v in g["recipe"])
+    x, _ = O.synth(O.Recipe(order=order, dim=dim, rank=rt, noise=float(g["noise"]), seed=sd))
+    cores, rep = tr_als_ne(x, AlsConfig(ranks=(rf,) * order, max_iters=1, error_mode="cheap",
+                                        init_cores=golden_cores(g, "ne_state2_core", order)))
+    assert abs(rep.errors[0] - float(g["ne_state3_cheap_error"])) < 1e-12
+    for j in range(order):
+        assert rel(cores[j], g[f"ne_state3_core_{j}"]) < 1e-10
+
+
+def test_seeded_init_and_zero_input():
+    from paper_2210_11362_b200 import AlsConfig, tr_als_ne
+    rng = np.random.default_rng(0)
+    x = rng.standard_normal((8, 9, 10))
+    cores, rep = tr_als_ne(x, AlsConfig(ranks=(2, 2, 2), max_iters=3, seed=42, error_mode="cheap"))
+    ocores, orep = O.solve(x, "ne", O.Config(ranks=(2, 2, 2), max_iters=3, seed=42, error_mode="cheap"))
+    np.testing.assert_allclose(rep.errors, orep.errors, rtol=0, atol=1e-12)
+    cores, rep = tr_als_ne(np.zeros((4, 5, 6)), AlsConfig(ranks=(2, 3, 2), max_iters=3))
+    assert rep.termination == "zero_input" and rep.errors == [] and all(not c.any() for c in cores)
+    assert [c.shape for c in cores] == [(2, 4, 3), (3, 5, 2), (2, 6, 2)]
+
+
+def test_tol_termination():
+    from paper_2210_11362_b200 import AlsConfig, tr_als_ne
+    rng = O.philox(3)
+    dims, ranks = (10, 11, 12), (2, 2, 2)
+    x = O.dense_from_ring(O.gaussian_ring(dims, ranks, rng))
+    cfg = AlsConfig(ranks=ranks, max_iters=50, seed=1, tol=1e-6, error_mode="cheap")
+    _, rep = tr_als_ne(x, cfg)
+    _, orep = O.solve(x, "ne", O.Config(ranks=ranks, max_iters=50, seed=1, tol=1e-6, error_mode="cheap"))
+    assert rep.termination == orep.termination == "tol"
+    assert rep.n_iters == len(orep.iter_seconds)
