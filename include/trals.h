@@ -51,6 +51,8 @@ enum {
 
 const char* trals_strerror(int code);
 int trals_version(void);
+/* Number of kernels this library has launched in the process (instrumentation). */
+long long trals_launch_count(void);
 
 /* Generic strided fp64 contraction on the DMMA pipe (the engine behind every
  * entry point below):  C[p][m][n] (+)= sum_k A(p,m,k) * B[k*ldb + n],
@@ -128,7 +130,8 @@ int trals_cholesky_f64(const double* d_S, int m, double* d_U, double* d_L, int c
 int trals_chol_solve_f64(const double* d_U, const double* d_L, int m, const double* d_M,
                          int64_t rows, double* d_Z, void* stream);
 
-/* Sum of squares of n doubles into d_out[0] (tensor_ops.py:237-239 norm). */
+/* Sum of squares of n doubles into d_out[0] (tensor_ops.py:237-239 norm) and the
+ * number of non-finite entries into d_out[1] (validation.py:53-54). */
 int64_t trals_sumsq_ws_elems(void);
 int trals_sumsq_f64(const double* d_x, int64_t n, double* d_out, double* d_ws, void* stream);
 

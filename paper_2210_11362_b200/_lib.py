@@ -24,6 +24,7 @@ _lib = None
 _SIGNATURES = {
     "trals_strerror": (ctypes.c_char_p, [c_int]),
     "trals_version": (c_int, []),
+    "trals_launch_count": (ctypes.c_longlong, []),
     "trals_gemm_ws_elems": (c_int64, [c_int64, c_int64, c_int64, c_int64]),
     "trals_gemm_f64": (c_int, [_dp, c_int64, c_int64, c_int64, c_int64, c_int64, c_int64, c_int64,
                                _dp, c_int64, _dp, POINTER(c_int64), c_int, _dp, c_int64, c_void_p]),

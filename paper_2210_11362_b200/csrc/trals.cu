@@ -17,7 +17,10 @@ namespace {
 
 constexpr int kSMs = 148;
 
+long long g_launches = 0;  // kernels launched through this library (reported by trals_launch_count)
+
 inline int launch_status() {
+  ++g_launches;
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? TRALS_OK : TRALS_ERR_CUDA;
 }
@@ -214,10 +217,11 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
   return r;  // valid in warp 0
 }
 
+// partial sums of squares and of non-finite entries (the check of validation.py:53-54)
 __global__ void __launch_bounds__(512) sumsq_partial_kernel(const double* __restrict__ x, int64_t n,
                                                             double* __restrict__ part) {
   __shared__ double red[16];
-  double acc = 0.0;
+  double acc = 0.0, bad = 0.0;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if ((reinterpret_cast<uintptr_t>(x) & 15u) == 0) {
@@ -227,22 +231,40 @@ __global__ void __launch_bounds__(512) sumsq_partial_kernel(const double* __rest
       const double2 v = __ldg(x2 + j);
       acc = fma(v.x, v.x, acc);
       acc = fma(v.y, v.y, acc);
+      bad += (isfinite(v.x) ? 0.0 : 1.0) + (isfinite(v.y) ? 0.0 : 1.0);
     }
-    if (i == 0 && (n & 1)) acc = fma(x[n - 1], x[n - 1], acc);
+    if (i == 0 && (n & 1)) {
+      acc = fma(x[n - 1], x[n - 1], acc);
+      bad += isfinite(x[n - 1]) ? 0.0 : 1.0;
+    }
   } else {
-    for (int64_t j = i; j < n; j += stride) acc = fma(x[j], x[j], acc);
+    for (int64_t j = i; j < n; j += stride) {
+      acc = fma(x[j], x[j], acc);
+      bad += isfinite(x[j]) ? 0.0 : 1.0;
+    }
   }
   const double s = block_sum<512>(acc, red);
-  if (threadIdx.x == 0) part[blockIdx.x] = s;
+  const double b = block_sum<512>(bad, red);
+  if (threadIdx.x == 0) {
+    part[blockIdx.x] = s;
+    part[gridDim.x + blockIdx.x] = b;
+  }
 }
 
 __global__ void __launch_bounds__(1024) sum_final_kernel(const double* __restrict__ part, int np,
                                                          double* __restrict__ out) {
   __shared__ double red[32];
-  double acc = 0.0;
-  for (int i = threadIdx.x; i < np; i += blockDim.x) acc += part[i];
+  double acc = 0.0, bad = 0.0;
+  for (int i = threadIdx.x; i < np; i += blockDim.x) {
+    acc += part[i];
+    bad += part[np + i];
+  }
   const double s = block_sum<1024>(acc, red);
-  if (threadIdx.x == 0) out[0] = s;
+  const double b = block_sum<1024>(bad, red);
+  if (threadIdx.x == 0) {
+    out[0] = s;
+    out[1] = b;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -760,6 +782,8 @@ const char* trals_strerror(int code) {
 
 int trals_version(void) { return 1; }
 
+long long trals_launch_count(void) { return g_launches; }
+
 int64_t trals_gemm_ws_elems(int64_t P, int64_t M, int64_t K, int64_t N) { return gemm_ws(P, M, K, N); }
 
 int trals_gemm_f64(const double* A, int64_t sAp, int64_t sAm, int64_t sAk, int64_t P, int64_t M, int64_t K,
@@ -888,12 +912,13 @@ int trals_chol_solve_f64(const double* U, const double* L, int m, const double* 
   return TRALS_ERR_UNSUPPORTED;
 }
 
-int64_t trals_sumsq_ws_elems(void) { return kSumsqBlocks; }
+int64_t trals_sumsq_ws_elems(void) { return 2 * kSumsqBlocks; }
 
 int trals_sumsq_f64(const double* x, int64_t n, double* out, double* ws, void* stream) {
   if (!x || !out || !ws || n < 0) return TRALS_ERR_ARG;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   sumsq_partial_kernel<<<kSumsqBlocks, 512, 0, s>>>(x, n, ws);
+  ++g_launches;
   sum_final_kernel<<<1, 1024, 0, s>>>(ws, kSumsqBlocks, out);
   return launch_status();
 }

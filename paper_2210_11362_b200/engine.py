@@ -119,7 +119,7 @@ class SweepEngine:
         self.U = self._empty(mmax, mmax)
         self.Lo = self._empty(mmax, mmax)
         self.info = torch.zeros(L.INFO_SLOTS, dtype=torch.int32, device=self.dev)
-        self.xnorm2 = self._empty(1)
+        self.xnorm2 = self._empty(2)  # [|X|^2, #non-finite]
         self.err_cur = self._empty(3)
         rmax = max(self.ranks)
         self.chain_tmp = self._empty(2 * rmax ** 4)
@@ -160,6 +160,7 @@ class SweepEngine:
         N = self.N
         self.steps: list[Step] = []
         self._bufs = []  # keep env buffers alive
+        self._env_flops = []
         self.stats.x_passes_per_sweep = 0
         if N == 2:
             phases = [(0, 0), (1, 1)]
@@ -241,6 +242,7 @@ class SweepEngine:
                                            leaf, self.gws.data_ptr(), self.gws.numel(), self._sp()), "env")
         self.steps.append(Step("mttsp", env_step, f"env[{seg_a}..{seg_b}]"))
         self.stats.x_passes_per_sweep += 1
+        self._env_flops.append(2.0 * pre * post * RR)
         if root_leaf:
             self._solve(seg_a)
             return
@@ -393,6 +395,7 @@ class SweepEngine:
                                              self.gws.data_ptr(), self.gws.numel(), sp), "core_gram")
 
     def compute_xnorm2(self):
+        """Device [|X|^2, #non-finite entries] (all-reduced over ranks)."""
         L.check(self.lib.trals_sumsq_f64(self.x.data_ptr(), self.x.numel(), self.xnorm2.data_ptr(),
                                          self.sumsq_ws.data_ptr(), self._sp()), "sumsq")
         if self.world > 1:
@@ -400,8 +403,17 @@ class SweepEngine:
             dist.all_reduce(self.xnorm2, group=self.group)
         return self.xnorm2
 
-    def run_sweep(self, events=None):
-        """Launch one full sweep; if `events` is a list, append (bucket, event) pairs at bucket changes."""
+    def env_flops(self):
+        """Flops of each X-streaming environment product (2*M*K*N), in step order."""
+        return list(self._env_flops)
+
+    def run_sweep(self, events=None, env_events=None):
+        """Launch one full sweep.
+
+        events: list -> (bucket, event) pairs appended at bucket changes.
+        env_events: list -> (start, end) event pairs around every X-streaming
+        environment product (the dominant kernel, for the roofline).
+        """
         prev = None
         for st in self.steps:
             if events is not None and st.bucket != prev:
@@ -409,7 +421,15 @@ class SweepEngine:
                 ev.record(self.stream)
                 events.append((st.bucket, ev))
                 prev = st.bucket
-            st.fn()
+            if env_events is not None and st.name.startswith("env"):
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(self.stream)
+                st.fn()
+                e1.record(self.stream)
+                env_events.append((e0, e1))
+            else:
+                st.fn()
 
     def error_step(self, out):
         """Cheap-error terms after a sweep into `out` (3 doubles): [e, <M,Z>, <S,Z^T Z>]."""

@@ -134,7 +134,7 @@ def chol_solve(U: torch.Tensor, Lo: torch.Tensor, M: torch.Tensor) -> torch.Tens
 
 def sumsq(x: torch.Tensor) -> torch.Tensor:
     _require_cuda(x)
-    out = torch.empty(1, dtype=torch.float64, device=x.device)
+    out = torch.empty(2, dtype=torch.float64, device=x.device)
     w = ws(L.lib().trals_sumsq_ws_elems(), x.device)
     L.check(L.lib().trals_sumsq_f64(x.data_ptr(), x.numel(), out.data_ptr(), w.data_ptr(), _stream()),
             "trals_sumsq_f64")

@@ -20,7 +20,7 @@ import numpy as np
 
 from . import _lib as L
 from .errors import DegenerateTriangularError, ElementBudgetError, StaleCacheError  # noqa: F401
-from .host import (check_dense_tensor, check_element_budget, check_ranks, core_ranks, make_rng,
+from .host import (check_element_budget, check_ranks, core_ranks, make_rng,
                    random_cores, validate_cores, zero_cores)
 
 VARIANTS = ("als", "ne", "qr", "qrne")          # solvers.py:55
@@ -34,9 +34,11 @@ SVD_RCOND_DEFAULT = 1e-12                        # linalg.py:20
 class AlsConfig:
     """Same fields and defaults as the reference AlsConfig (solvers.py:60-104).
 
-    `shard_mode` (extension) selects the mode X is split along when the call
-    runs inside an initialised torch.distributed NCCL group (one process per
-    GPU); it is ignored for single-process runs.
+    `shard_mode` (extension, 0-based) selects the mode X is split along when
+    the call runs inside an initialised torch.distributed NCCL group (one
+    process per GPU); it is ignored for single-process runs.  The default 0 is
+    BASELINE's "mode 1" in the paper's 1-based numbering; with it every rank's
+    slab is a contiguous block of X.
     """
 
     ranks: tuple
@@ -49,7 +51,7 @@ class AlsConfig:
     element_budget: int = None
     svd_rcond: float = SVD_RCOND_DEFAULT
     debug_checks: bool = False
-    shard_mode: int = 1
+    shard_mode: int = 0
     timing_buckets: bool = True
 
 
@@ -86,14 +88,23 @@ def _validate(x, config, variant):
         raise ValueError("max_iters must be at least 1")
 
 
-def _as_device_tensor(x):
+def _host_or_device_tensor(x):
+    """Coerce the input like check_dense_tensor (validation.py:43-55) without a host pass over the data.
+
+    Returns a float64 torch tensor (host or device, possibly a view); the finite
+    check runs later on the device (sumsq kernel)."""
     import torch
     if isinstance(x, torch.Tensor):
         t = x.detach()
-        if not t.is_cuda:
+        if t.dtype != torch.float64:
             t = t.to(torch.float64)
-        return t
-    return None
+    else:
+        t = torch.from_numpy(np.asarray(x, dtype=np.float64))
+    if t.dim() < 2:
+        raise ValueError(f"tensor order {t.dim()} is below the minimum 2")
+    if t.numel() == 0:
+        raise ValueError("tensor has no elements")
+    return t
 
 
 def _run(x, config, variant):
@@ -102,51 +113,41 @@ def _run(x, config, variant):
     _validate(x, config, variant)
     if variant not in DEVICE_VARIANTS:
         raise NotImplementedError("tr_als (Alg. 1) is outside the B200 hot path; use ne/qr/qrne")
-    if not torch.cuda.is_available():
-        raise RuntimeError("paper_2210_11362_b200 needs a CUDA device (no CPU fallback)")
-    L.lib()  # fail loudly if the extension is missing
-
-    tx = _as_device_tensor(x)
-    if tx is not None and tx.is_cuda:
-        # device input: validate on the device, avoid a host copy
-        if tx.dim() < 2:
-            raise ValueError(f"tensor order {tx.dim()} is below the minimum 2")
-        if tx.numel() == 0:
-            raise ValueError("tensor has no elements")
-        xd = tx.to(torch.float64).contiguous()
-        if not bool(torch.isfinite(xd).all()):
-            raise ValueError("tensor contains non-finite entries")
-        dims = tuple(xd.shape)
-    else:
-        xh = check_dense_tensor(x if tx is None else tx.numpy(), min_order=2)
-        dims = xh.shape
-        xd = None
+    t = _host_or_device_tensor(x)
+    dims = tuple(int(d) for d in t.shape)
     N = len(dims)
     ranks = check_ranks(config.ranks, N)
     if config.error_mode == "exact":
         check_element_budget(dims, config.element_budget)
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2210_11362_b200 needs a CUDA device (no CPU fallback)")
+    L.lib()  # fail loudly if the extension is missing
 
     report = AlsReport(variant=variant)
     dist = _dist_context()
+    dev = torch.device("cuda", torch.cuda.current_device())
     if dist is None:
-        if xd is None:
-            xd = torch.from_numpy(np.ascontiguousarray(xh)).to("cuda", non_blocking=False)
         shard, lo, hi, world, group = None, 0, None, 1, None
-        x_local = xd
+        src = t
     else:
         world, rank, group = dist
         shard = int(config.shard_mode) % N
-        I = dims[shard]
-        lo, hi = _slab(I, world, rank)
-        src = xd if xd is not None else torch.from_numpy(np.ascontiguousarray(xh))
-        idx = [slice(None)] * N
-        idx[shard] = slice(lo, hi)
-        x_local = src[tuple(idx)].contiguous().to("cuda")
+        lo, hi = _slab(dims[shard], world, rank)
+        src = t.narrow(shard, lo, hi - lo)
+    if src.is_cuda and src.device == dev:
+        x_local = src.contiguous()
+    else:
+        if not src.is_contiguous():
+            src = src.contiguous()
+        x_local = src.to(dev, non_blocking=bool(src.is_pinned()))
 
     from .engine import SweepEngine
     eng = SweepEngine(x_local, dims, ranks, variant, shard_mode=shard, lo=lo, hi=hi, group=group,
                       world_size=world)
-    xnorm2 = float(eng.compute_xnorm2().item())
+    xn = eng.compute_xnorm2().cpu().numpy()
+    if xn[1] > 0:
+        raise ValueError("tensor contains non-finite entries")  # validation.py:53-54
+    xnorm2 = float(xn[0])
     if xnorm2 == 0.0:  # solvers.py:289-291
         report.termination = "zero_input"
         return zero_cores(dims, ranks), report

@@ -216,7 +216,9 @@ class FakeTrals:
     def trals_sumsq_f64(self, x, n, out, ws, stream):
         self._count("sumsq")
         v = _arr(x, n)
-        _arr(out, 1)[0] = float(np.dot(v, v))
+        o = _arr(out, 2)
+        o[0] = float(np.dot(v, v))
+        o[1] = float(np.count_nonzero(~np.isfinite(v)))
         return 0
 
     def trals_error_terms_f64(self, M, Z, S, rows, m, xnorm2, out, ws, ws_elems, stream):

@@ -122,7 +122,10 @@ def test_sumsq_and_error_terms():
     from paper_2210_11362_b200 import ops
     rng = np.random.default_rng(5)
     x = rng.standard_normal(1_000_003)
-    assert abs(ops.sumsq(cuda(x)).item() - np.dot(x, x)) < 1e-10 * np.dot(x, x)
+    out = ops.sumsq(cuda(x)).cpu().numpy()
+    assert abs(out[0] - np.dot(x, x)) < 1e-10 * np.dot(x, x) and out[1] == 0
+    x[[5, 77, 1_000_002]] = [np.nan, np.inf, -np.inf]
+    assert ops.sumsq(cuda(x)).cpu().numpy()[1] == 3
     m, rows = 36, 50
     a = rng.standard_normal((90, m))
     s = a.T @ a
