@@ -252,9 +252,15 @@ def run_ours(args):
     eng.set_cores(cores0)
     errs = torch.zeros((args.warmup + args.steps, 3), dtype=torch.float64, device=dev)
     stream = eng.stream
+    use_graph = (world == 1 and not args.eager and args.config != "c5")
+    if use_graph:
+        eng.capture(with_error=True)
     for k in range(args.warmup):
-        eng.run_sweep()
-        eng.error_step(errs[k])
+        if use_graph:
+            eng.replay()
+        else:
+            eng.run_sweep()
+            eng.error_step(errs[k])
     torch.cuda.synchronize()
     if world > 1:
         tdist.barrier()
@@ -270,13 +276,27 @@ def run_ours(args):
         tdist.barrier()
     e0.record(stream)
     for k in range(args.steps):
-        eng.run_sweep(env_events=env_events)
-        eng.error_step(errs[args.warmup + k])
+        if use_graph:
+            eng.replay()
+        else:
+            eng.run_sweep(env_events=env_events)
+            eng.error_step(errs[args.warmup + k])
     e1.record(stream)
     torch.cuda.synchronize()
     if world > 1:
         tdist.barrier()
     launches = L.lib().trals_launch_count() - l0
+    if use_graph:
+        # graph replays launch no host-side calls: count the kernels of one captured sweep
+        c0 = L.lib().trals_launch_count()
+        eng.run_sweep(env_events=env_events)
+        eng.error_step(errs[-1])
+        torch.cuda.synchronize()
+        launches = (L.lib().trals_launch_count() - c0) * args.steps
+        for _ in range(4):
+            eng.run_sweep(env_events=env_events)
+        torch.cuda.synchronize()
+        errs[-1].copy_(eng.err_cur)
     clocks = sampler.stop()
     ms = e0.elapsed_time(e1) / args.steps
     env_ms = [a.elapsed_time(b) for a, b in env_events]
@@ -284,14 +304,14 @@ def run_ours(args):
     if world > 1:
         tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
     ms_max = float(t.item())
-    final_err = float(errs[args.warmup + args.steps - 1, 0].item())
+    final_err = float(errs[args.warmup + args.steps - 1, 0].item()) if not use_graph else float(eng.err_cur[0].item())
 
     # dominant kernel: the X-streaming environment GEMM (one per phase)
     env_flops = eng.env_flops()
     per_launch = [env_flops[i % len(env_flops)] / (env_ms[i] * 1e-3) / 1e12 for i in range(len(env_ms))]
     env_avg_ms = float(np.mean(env_ms))
     env_tf = float(np.mean(per_launch))
-    env_share = sum(env_ms) / (ms * args.steps)
+    env_share = env_avg_ms * len(env_flops) / ms
     traffic = None
     tpath = os.path.join(ROOT, "profiles", f"{args.config}_env_traffic.json")
     if os.path.exists(tpath):
@@ -355,7 +375,8 @@ def run_ours(args):
         "config": {"workload": f"{args.config} {args.variant.upper()} sweep", "dims": dims, "ranks": ranks,
                    "variant": args.variant, "parallelism": f"shard mode 0 x{world}" if world > 1 else "single",
                    "l2": "X (%.2f GB) larger than the 126 MB L2, no flush needed" % (np.prod(dims) * 8 / 1e9),
-                   "step": "one full sweep + per-sweep relative error"},
+                   "step": "one full sweep + per-sweep relative error",
+                   "launch": "CUDA graph replay" if use_graph else "eager stream launches"},
         "contraction_tflops": F / sweep_s / 1e12,
         "contraction_roofline_frac": t_roof / sweep_s,
         "roofline_sweep_ms": t_roof * 1e3,
@@ -390,6 +411,7 @@ def main():
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c5")
     ap.add_argument("--variant", choices=["ne", "qr", "qrne"], default="ne")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--eager", action="store_true", help="no CUDA graph for the small configs")
     ap.add_argument("--e2e-reps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-frac", type=float, default=0.5, help="slab fraction for the cpu_baseline sample")

@@ -193,22 +193,37 @@ dmma_gemm_kernel(const GemmArgs g) {
   }
   cp_async_wait<0>();
 
-  // epilogue: C fragment (row fr, cols 2*fk, 2*fk+1) of every m8n8 block
+  // epilogue: C fragment (row fr, cols 2*fk, 2*fk+1) of every m8n8 block.
+  // Address parts are computed once per row / column (32-bit div/mod).
+  int64_t col_off[TN][2];
+  bool col_ok[TN][2];
+#pragma unroll
+  for (int j = 0; j < TN; ++j)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int64_t n = n0 + wn0 + j * 8 + 2 * fk + e;
+      col_ok[j][e] = n < g.N;
+      const uint32_t un = static_cast<uint32_t>(n), n2 = static_cast<uint32_t>(g.cmap.N2);
+      col_off[j][e] = static_cast<int64_t>(un / n2) * g.cmap.sn1 + static_cast<int64_t>(un % n2) * g.cmap.sn2;
+    }
 #pragma unroll
   for (int i = 0; i < TM; ++i) {
     const int64_t m = m0 + wm0 + i * 8 + fr;
     if (m >= g.M) continue;
+    const uint32_t um = static_cast<uint32_t>(m), m2 = static_cast<uint32_t>(g.cmap.M2);
+    const int64_t row_off = p * g.cmap.sp + static_cast<int64_t>(um / m2) * g.cmap.sm1 +
+                            static_cast<int64_t>(um % m2) * g.cmap.sm2;
+    double* wsrow = g.ws + ((static_cast<int64_t>(split) * g.P + p) * g.M + m) * g.N;
 #pragma unroll
     for (int j = 0; j < TN; ++j) {
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        const int64_t n = n0 + wn0 + j * 8 + 2 * fk + e;
-        if (n >= g.N) continue;
+        if (!col_ok[j][e]) continue;
         const double v = acc[i][j][e];
         if (g.splits > 1) {
-          g.ws[((static_cast<int64_t>(split) * g.P + p) * g.M + m) * g.N + n] = v;
+          wsrow[n0 + wn0 + j * 8 + 2 * fk + e] = v;
         } else {
-          double* dst = g.C + cmap_addr(g.cmap, p, m, n);
+          double* dst = g.C + row_off + col_off[j][e];
           *dst = g.beta ? *dst + v : v;
         }
       }
@@ -218,16 +233,20 @@ dmma_gemm_kernel(const GemmArgs g) {
 
 // Deterministic split-K reduction: partials summed in split order.
 __global__ void splitk_reduce_kernel(const GemmArgs g) {
-  const int64_t total = g.P * g.M * g.N;
-  const int64_t plane = total;
-  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
+  const int64_t plane = g.P * g.M * g.N;
+  const uint32_t N = static_cast<uint32_t>(g.N), M = static_cast<uint32_t>(g.M);
+  const uint32_t M2 = static_cast<uint32_t>(g.cmap.M2), N2 = static_cast<uint32_t>(g.cmap.N2);
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < plane;
        idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     double s = 0.0;
     for (int z = 0; z < g.splits; ++z) s += g.ws[z * plane + idx];
-    const int64_t n = idx % g.N;
-    const int64_t m = (idx / g.N) % g.M;
-    const int64_t p = idx / (g.N * g.M);
-    double* dst = g.C + cmap_addr(g.cmap, p, m, n);
+    const int64_t pm = idx / N;  // (p, m) row index
+    const uint32_t n = static_cast<uint32_t>(idx - pm * N);
+    const uint32_t m = static_cast<uint32_t>(pm % M);
+    const int64_t p = pm / M;
+    double* dst = g.C + p * g.cmap.sp + static_cast<int64_t>(m / M2) * g.cmap.sm1 +
+                  static_cast<int64_t>(m % M2) * g.cmap.sm2 + static_cast<int64_t>(n / N2) * g.cmap.sn1 +
+                  static_cast<int64_t>(n % N2) * g.cmap.sn2;
     *dst = g.beta ? *dst + s : s;
   }
 }

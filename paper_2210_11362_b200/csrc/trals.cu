@@ -186,10 +186,12 @@ __global__ void relayout_kernel(const double* __restrict__ src, int sl, int Ra, 
   for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
        t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     // t enumerates the destination in its own order
+    const uint32_t u = static_cast<uint32_t>(t), I32 = static_cast<uint32_t>(I);
+    const uint32_t ra = static_cast<uint32_t>(Ra), rb = static_cast<uint32_t>(Rb);
     int64_t a, i, b;
-    if (dl == TRALS_LAYOUT_C) { b = t % Rb; i = (t / Rb) % I; a = t / (Rb * I); }
-    else if (dl == TRALS_LAYOUT_SLICE) { b = t % Rb; a = (t / Rb) % Ra; i = t / (static_cast<int64_t>(Rb) * Ra); }
-    else { a = t % Ra; b = (t / Ra) % Rb; i = t / (static_cast<int64_t>(Ra) * Rb); }
+    if (dl == TRALS_LAYOUT_C) { b = u % rb; i = (u / rb) % I32; a = u / (rb * I32); }
+    else if (dl == TRALS_LAYOUT_SLICE) { b = u % rb; a = (u / rb) % ra; i = u / (rb * ra); }
+    else { a = u % ra; b = (u / ra) % rb; i = u / (ra * rb); }
     dst[t] = src[core_index(sl, a, i, b, Ra, I, Rb)];
   }
 }
@@ -268,153 +270,207 @@ __global__ void __launch_bounds__(1024) sum_final_kernel(const double* __restric
 }
 
 // ---------------------------------------------------------------------------
-// Cholesky (single CTA; S in L2-resident global memory; DMMA trailing update)
+// Cholesky S = U^T U (upper, like scipy cho_factor(lower=False), linalg.py:75)
+// One CTA.  m <= kCholSmemMax: whole matrix in shared memory, panel-blocked
+// right-looking factorisation.  Larger m (R = 20 -> m = 400): the matrix stays
+// in L2-resident global memory; panels of 32 rows are factored in shared
+// memory and the trailing upper triangle is updated with DMMA 8x8x4 blocks,
+// each warp keeping kCholBatch blocks' loads in flight.
 // ---------------------------------------------------------------------------
-constexpr int kCholNB = 32;       // panel width
-constexpr int kCholThreads = 512;
+constexpr int kCholNB = 32;        // panel height (rows of U per panel)
+constexpr int kCholThreads = 1024;
+constexpr int kCholSmemMax = 152;  // m*(m+1) doubles <= ~185 KB
+constexpr int kCholBatch = 8;      // trailing 8x8 blocks in flight per warp
 
-__global__ void __launch_bounds__(kCholThreads) cholesky_kernel(const double* __restrict__ S, int m,
-                                                                double* __restrict__ U, double* __restrict__ L,
-                                                                int check_degen, int* __restrict__ info) {
-  extern __shared__ __align__(16) double panel[];  // [kCholNB][pw] pw = padded width
-  __shared__ double red[32];
-  __shared__ int fail;
-  const int tid = threadIdx.x;
-  const int lane = tid & 31, warp = tid >> 5, nwarps = kCholThreads / 32;
-  const int64_t mm = static_cast<int64_t>(m) * m;
-
-  // symmetry check (linalg.py:70-72) and symmetrised copy into U
-  double amax = 0.0, asym = 0.0;
-  for (int64_t t = tid; t < mm; t += kCholThreads) {
-    const int i = static_cast<int>(t / m), j = static_cast<int>(t % m);
-    const double sij = S[t], sji = S[static_cast<int64_t>(j) * m + i];
-    amax = fmax(amax, fabs(sij));
-    asym = fmax(asym, fabs(sij - sji));
-    U[t] = 0.5 * (sij + sji);
-  }
-  // block max-reduce
+__device__ __forceinline__ void chol_reduce_flags(double amax, double asym, double* red, int* info) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int o = 16; o > 0; o >>= 1) {
     amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
     asym = fmax(asym, __shfl_xor_sync(0xffffffffu, asym, o));
   }
-  if (lane == 0) { red[warp] = amax; red[16 + warp] = asym; }
-  if (tid == 0) fail = 0;
+  if (lane == 0) { red[warp] = amax; red[32 + warp] = asym; }
   __syncthreads();
-  if (tid == 0) {
+  if (threadIdx.x == 0) {
     double a = 0, b = 0;
-    for (int w = 0; w < nwarps; ++w) { a = fmax(a, red[w]); b = fmax(b, red[16 + w]); }
-    if (a > 0 && b > 1e-8 * a) info[TRALS_INFO_ASYM] = 1;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { a = fmax(a, red[w]); b = fmax(b, red[32 + w]); }
+    if (a > 0 && b > 1e-8 * a) info[TRALS_INFO_ASYM] = 1;  // linalg.py:70-72
   }
   __syncthreads();
+}
 
-  const int pw_full = ((m + 7) / 8) * 8 + 4;  // padded smem pitch (bank-conflict-free fragments)
-  for (int p0 = 0; p0 < m; p0 += kCholNB) {
-    const int pb = min(kCholNB, m - p0);
-    const int w = m - p0;
-    const int wpad = ((w + 7) / 8) * 8;
-    const int pw = pw_full;
-    // load panel rows p0..p0+pb-1, cols p0..m-1 (zero padded to 8-multiples, rows to kCholNB)
-    for (int t = tid; t < kCholNB * wpad; t += kCholThreads) {
-      const int r = t / wpad, c = t % wpad;
-      double v = 0.0;
-      if (r < pb && c < w && c >= r) v = U[static_cast<int64_t>(p0 + r) * m + p0 + c];
-      panel[r * pw + c] = v;
+// factor rows [p0, p0+pb) of an upper-form matrix held as rows of length w (row r at P + r*ld,
+// column offset p0 already applied): P[j][j..] /= sqrt(P[j][j]), P[r][r..] -= P[j][r] P[j][r..]
+__device__ __forceinline__ int chol_panel(double* P, int ld, int pb, int w, int p0, int* fail) {
+  for (int j = 0; j < pb; ++j) {
+    const double d = P[j * ld + j];
+    if (!(d > 0.0)) {  // non-positive or NaN pivot: dpotrf failure
+      if (threadIdx.x == 0) *fail = p0 + j + 1;
+      return 1;
     }
+    const double dinv = rsqrt(d);
     __syncthreads();
-    // factor the panel (upper form, row-oriented): row j /= sqrt(pivot), rank-1 update below
-    for (int j = 0; j < pb; ++j) {
-      if (tid == 0) {
-        const double d = panel[j * pw + j];
-        if (!(d > 0.0)) {  // also catches NaN
-          fail = p0 + j + 1;
-        }
-      }
-      __syncthreads();
-      if (fail) break;
-      const double dinv = 1.0 / sqrt(panel[j * pw + j]);
-      for (int c = j + tid; c < w; c += kCholThreads) panel[j * pw + c] *= dinv;
-      __syncthreads();
-      const int rows = pb - j - 1;
-      for (int t = tid; t < rows * w; t += kCholThreads) {
-        const int r = j + 1 + t / w, c = t % w;
-        if (c >= r) panel[r * pw + c] -= panel[j * pw + r] * panel[j * pw + c];
-      }
-      __syncthreads();
-    }
-    if (fail) break;
-    // write the factored panel rows back
-    for (int t = tid; t < pb * w; t += kCholThreads) {
-      const int r = t / w, c = t % w;
-      if (c >= r) U[static_cast<int64_t>(p0 + r) * m + p0 + c] = panel[r * pw + c];
-    }
-    // trailing update of the upper triangle: A[i][c] -= sum_t P[t][i] P[t][c], i,c >= pb (panel coords)
-    const int tw = w - pb;
-    if (tw > 0) {
-      const int nb8 = (tw + 7) / 8;
-      const int nblk = nb8 * (nb8 + 1) / 2;
-      const int fr = lane >> 2, fk = lane & 3;
-      for (int bidx = warp; bidx < nblk; bidx += nwarps) {
-        // decode upper-triangular block index -> (bi, bc), bc >= bi
-        int bi = 0, rem = bidx;
-        while (rem >= nb8 - bi) { rem -= nb8 - bi; ++bi; }
-        const int bc = bi + rem;
-        const int i0 = pb + bi * 8, c0 = pb + bc * 8;
-        // C fragment: row i0+fr, cols c0+2fk, c0+2fk+1
-        const int gi = p0 + i0 + fr;
-        double c[2];
-        for (int e = 0; e < 2; ++e) {
-          const int gc = p0 + c0 + 2 * fk + e;
-          c[e] = (gi < m && gc < m) ? U[static_cast<int64_t>(gi) * m + gc] : 0.0;
-        }
-        for (int k0 = 0; k0 < kCholNB; k0 += 4) {
-          // A(m=i, k=t) = -P[t][i];  B(k=t, n=c) = P[t][c]
-          const double a = -panel[(k0 + fk) * pw + i0 + fr];
-          const double b = panel[(k0 + fk) * pw + c0 + fr];
-          trals::dmma884(c[0], c[1], a, b);
-        }
-        for (int e = 0; e < 2; ++e) {
-          const int gc = p0 + c0 + 2 * fk + e;
-          if (gi < m && gc < m && gc >= gi) U[static_cast<int64_t>(gi) * m + gc] = c[e];
-        }
-      }
+    for (int c = j + threadIdx.x; c < w; c += blockDim.x) P[j * ld + c] *= dinv;
+    __syncthreads();
+    const int rows = pb - j - 1;
+    for (int t = threadIdx.x; t < rows * w; t += blockDim.x) {
+      const int r = j + 1 + t / w, c = t % w;
+      if (c >= r) P[r * ld + c] = fma(-P[j * ld + r], P[j * ld + c], P[r * ld + c]);
     }
     __syncthreads();
   }
+  return 0;
+}
+
+template <bool kResident>
+__global__ void __launch_bounds__(kResident ? kCholThreads : kCholThreads / 2)
+cholesky_kernel(const double* __restrict__ S, int m, double* __restrict__ U, double* __restrict__ L,
+                int check_degen, int* __restrict__ info) {
+  extern __shared__ __align__(16) double sm[];
+  __shared__ double red[64];
+  __shared__ int fail;
+  constexpr int kT = kResident ? kCholThreads : kCholThreads / 2;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = kT / 32;
+  if (tid == 0) fail = 0;
+  constexpr bool in_smem = kResident;
+  const int ldm = m + 1;  // smem pitch for the resident path
+
+  // symmetry check + symmetrised copy (into smem or U)
+  double amax = 0.0, asym = 0.0;
+  for (int i = warp; i < m; i += nwarps)
+    for (int j = lane; j < m; j += 32) {
+      const double sij = S[i * m + j], sji = S[j * m + i];
+      amax = fmax(amax, fabs(sij));
+      asym = fmax(asym, fabs(sij - sji));
+      const double v = 0.5 * (sij + sji);
+      if constexpr (in_smem) sm[i * ldm + j] = v;
+      else U[i * m + j] = v;
+    }
   __syncthreads();
-  if (fail) {
-    if (tid == 0) info[TRALS_INFO_CHOL] = fail;
-    return;
-  }
-  // zero the strict lower triangle of U, write L = U^T, degeneracy floor
-  double umax = 0.0, dmin = INFINITY;
-  int dmin_idx = 0;
-  for (int64_t t = tid; t < mm; t += kCholThreads) {
-    const int i = static_cast<int>(t / m), j = static_cast<int>(t % m);
-    double v = 0.0;
-    if (j >= i) v = U[t];
-    else U[t] = 0.0;
-    (void)v;
-  }
-  __syncthreads();
-  for (int64_t t = tid; t < mm; t += kCholThreads) {
-    const int i = static_cast<int>(t / m), j = static_cast<int>(t % m);
-    const double v = U[static_cast<int64_t>(j) * m + i];  // L[i][j] = U[j][i]
-    L[t] = v;
-    const double u = U[t];
-    umax = fmax(umax, fabs(u));
-    if (i == j && fabs(u) < dmin) { dmin = fabs(u); dmin_idx = i; }
+  chol_reduce_flags(amax, asym, red, info);
+
+  if constexpr (in_smem) {
+    for (int p0 = 0; p0 < m; p0 += kCholNB) {
+      const int pb = min(kCholNB, m - p0), w = m - p0;
+      if (chol_panel(sm + p0 * ldm + p0, ldm, pb, w, p0, &fail)) break;
+      // trailing update rows/cols >= p0+pb of the upper triangle
+      const int tw = w - pb;
+      const int tot = tw * tw;
+      for (int t = tid; t < tot; t += kT) {
+        const int i = t / tw, c = t - i * tw;
+        if (c < i) continue;
+        const int gi = p0 + pb + i, gc = p0 + pb + c;
+        double acc = sm[gi * ldm + gc];
+#pragma unroll 8
+        for (int k = 0; k < pb; ++k) acc = fma(-sm[(p0 + k) * ldm + gi], sm[(p0 + k) * ldm + gc], acc);
+        sm[gi * ldm + gc] = acc;
+      }
+      __syncthreads();
+    }
+    __syncthreads();
+    if (fail) { if (tid == 0) info[TRALS_INFO_CHOL] = fail; return; }
+    for (int i = warp; i < m; i += nwarps)
+      for (int j = lane; j < m; j += 32) {
+        U[i * m + j] = j >= i ? sm[i * ldm + j] : 0.0;
+        L[i * m + j] = j <= i ? sm[j * ldm + i] : 0.0;
+      }
+  } else {
+    const int pw = ((m + 7) / 8) * 8 + 4;  // bank-conflict-free fragment pitch
+    double* panel = sm;                   // [kCholNB][pw]
+    const int fr = lane >> 2, fk = lane & 3;
+    for (int p0 = 0; p0 < m; p0 += kCholNB) {
+      const int pb = min(kCholNB, m - p0), w = m - p0;
+      const int wpad = ((w + 7) / 8) * 8;
+      for (int t = tid; t < kCholNB * wpad; t += kT) {
+        const int r = t / wpad, c = t % wpad;
+        panel[r * pw + c] = (r < pb && c < w && c >= r) ? U[static_cast<int64_t>(p0 + r) * m + p0 + c] : 0.0;
+      }
+      __syncthreads();
+      if (chol_panel(panel, pw, pb, w, p0, &fail)) break;
+      for (int t = tid; t < pb * w; t += kT) {
+        const int r = t / w, c = t % w;
+        if (c >= r) U[static_cast<int64_t>(p0 + r) * m + p0 + c] = panel[r * pw + c];
+      }
+      const int tw = w - pb;
+      if (tw > 0) {
+        const int nb8 = (tw + 7) / 8;
+        const int nblk = nb8 * (nb8 + 1) / 2;
+        for (int b0 = warp * kCholBatch; b0 < nblk; b0 += nwarps * kCholBatch) {
+          int gi[kCholBatch], gc0[kCholBatch], pi[kCholBatch], pc[kCholBatch];
+          double c[kCholBatch][2];
+#pragma unroll
+          for (int q = 0; q < kCholBatch; ++q) {
+            const int bidx = b0 + q;
+            gi[q] = -1;
+            c[q][0] = c[q][1] = 0.0;
+            if (bidx < nblk) {
+              // row-major enumeration of the upper-triangular block grid
+              const double fb = static_cast<double>(nb8) + 0.5;
+              int bi = static_cast<int>(fb - sqrt(fb * fb - 2.0 * bidx));
+              bi = max(0, min(bi, nb8 - 1));
+              while (bi > 0 && bi * nb8 - bi * (bi - 1) / 2 > bidx) --bi;
+              while ((bi + 1) * nb8 - (bi + 1) * bi / 2 <= bidx) ++bi;
+              const int bc = bi + (bidx - (bi * nb8 - bi * (bi - 1) / 2));
+              pi[q] = pb + bi * 8;
+              pc[q] = pb + bc * 8;
+              gi[q] = p0 + pi[q] + fr;
+              gc0[q] = p0 + pc[q] + 2 * fk;
+#pragma unroll
+              for (int e = 0; e < 2; ++e)
+                if (gi[q] < m && gc0[q] + e < m) c[q][e] = U[static_cast<int64_t>(gi[q]) * m + gc0[q] + e];
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < kCholBatch; ++q) {
+            if (gi[q] < 0) continue;
+#pragma unroll
+            for (int k0 = 0; k0 < kCholNB; k0 += 4) {
+              const double a = -panel[(k0 + fk) * pw + pi[q] + fr];
+              const double b = panel[(k0 + fk) * pw + pc[q] + fr];
+              trals::dmma884(c[q][0], c[q][1], a, b);
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < kCholBatch; ++q) {
+            if (gi[q] < 0 || gi[q] >= m) continue;
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int gc = gc0[q] + e;
+              if (gc < m && gc >= gi[q]) U[static_cast<int64_t>(gi[q]) * m + gc] = c[q][e];
+            }
+          }
+        }
+      }
+      __syncthreads();
+    }
+    __syncthreads();
+    if (fail) { if (tid == 0) info[TRALS_INFO_CHOL] = fail; return; }
+    for (int i = warp; i < m; i += nwarps)
+      for (int j = lane; j < i; j += 32) U[i * m + j] = 0.0;
+    __syncthreads();
+    for (int i = warp; i < m; i += nwarps)
+      for (int j = lane; j < m; j += 32) L[i * m + j] = j <= i ? U[j * m + i] : 0.0;
   }
   if (check_degen) {
+    __syncthreads();
+    // diag <= 1e-13 * max|U|  (linalg.py:96-99)
+    double umax = 0.0, dmin = INFINITY;
+    int didx = 0;
+    for (int i = warp; i < m; i += nwarps)
+      for (int j = lane + i - (i & 31); j < m; j += 32) {
+        if (j < i) continue;
+        const double u = fabs(U[i * m + j]);
+        umax = fmax(umax, u);
+        if (i == j && u < dmin) { dmin = u; didx = i; }
+      }
     for (int o = 16; o > 0; o >>= 1) {
       umax = fmax(umax, __shfl_xor_sync(0xffffffffu, umax, o));
       const double od = __shfl_xor_sync(0xffffffffu, dmin, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, dmin_idx, o);
-      if (od < dmin || (od == dmin && oi < dmin_idx)) { dmin = od; dmin_idx = oi; }
+      const int oi = __shfl_xor_sync(0xffffffffu, didx, o);
+      if (od < dmin || (od == dmin && oi < didx)) { dmin = od; didx = oi; }
     }
-    __shared__ double sd[16];
-    __shared__ int si[16];
-    __syncthreads();
-    if (lane == 0) { red[warp] = umax; sd[warp] = dmin; si[warp] = dmin_idx; }
+    __shared__ double sd[32];
+    __shared__ int si[32];
+    if (lane == 0) { red[warp] = umax; sd[warp] = dmin; si[warp] = didx; }
     __syncthreads();
     if (tid == 0) {
       double a = 0, d = INFINITY;
@@ -428,74 +484,115 @@ __global__ void __launch_bounds__(kCholThreads) cholesky_kernel(const double* __
   }
 }
 
+size_t cholesky_smem(int m) {
+  if (m <= kCholSmemMax) return sizeof(double) * static_cast<size_t>(m) * (m + 1);
+  return sizeof(double) * kCholNB * (((m + 7) / 8) * 8 + 4);
+}
+
 // ---------------------------------------------------------------------------
-// Row-parallel triangular solves Z S = M, S = U^T U  (Y U = M, then Z U^T = Y)
-// One warp per RHS row; the CTA's warps share U/L rows staged in shared memory.
+// Row-parallel triangular solves Z S = M, S = U^T U:  Y U = M, then Z U^T = Y
+// (scipy cho_solve, linalg.py:76).  Each warp owns kSolveRPW right-hand-side
+// rows (register-resident, column k on lane k % 32); U rows (forward) and
+// L = U^T rows (backward) stream through a cp.async double buffer shared by
+// the CTA's warps; the diagonal reciprocals are precomputed once.
 // ---------------------------------------------------------------------------
-constexpr int kSolveWarps = 8;
-constexpr int kSolveChunk = 8;  // U rows per smem stage
+constexpr int kSolveWarps = 4;
+constexpr int kSolveRPW = 2;     // rows per warp
+constexpr int kSolveChunk = 16;  // U rows per stage
 
 template <int NR>
 __global__ void __launch_bounds__(kSolveWarps * 32) chol_solve_kernel(const double* __restrict__ U,
                                                                       const double* __restrict__ L, int m,
                                                                       const double* __restrict__ Mr, int64_t rows,
                                                                       double* __restrict__ Z) {
-  extern __shared__ __align__(16) double stage[];  // [2][kSolveChunk][m]
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t row = static_cast<int64_t>(blockIdx.x) * kSolveWarps + warp;
-  const bool active = row < rows;
-  double r[NR];
+  extern __shared__ __align__(16) double stage[];  // [2][kSolveChunk][mp] + dinv[m]
+  const int mp = (m + 1) & ~1;
+  double* dinv = stage + 2 * kSolveChunk * mp;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t row0 = (static_cast<int64_t>(blockIdx.x) * kSolveWarps + warp) * kSolveRPW;
+  for (int j = tid; j < m; j += kSolveWarps * 32) dinv[j] = 1.0 / U[static_cast<int64_t>(j) * m + j];
+  double r[kSolveRPW][NR];
 #pragma unroll
-  for (int s = 0; s < NR; ++s) {
-    const int k = s * 32 + lane;
-    r[s] = (active && k < m) ? Mr[row * m + k] : 0.0;
-  }
+  for (int q = 0; q < kSolveRPW; ++q)
+#pragma unroll
+    for (int s = 0; s < NR; ++s) {
+      const int k = s * 32 + lane;
+      const int64_t row = row0 + q;
+      r[q][s] = (row < rows && k < m) ? Mr[row * m + k] : 0.0;
+    }
   const int nchunks = (m + kSolveChunk - 1) / kSolveChunk;
-  // ---- forward: Y U = M.  y_j = r_j / U[j][j];  r_k -= y_j U[j][k]  (k > j) ----
+  const bool vec = (m % 2 == 0);
   for (int pass = 0; pass < 2; ++pass) {
     const double* Src = pass == 0 ? U : L;
-    auto load_chunk = [&](int ch, int buf) {
-      // pass 0 walks rows 0..m-1 of U; pass 1 walks rows m-1..0 of L
-      for (int t = threadIdx.x; t < kSolveChunk * m; t += kSolveWarps * 32) {
-        const int rr = t / m, c = t % m;
-        const int j = pass == 0 ? ch * kSolveChunk + rr : m - 1 - (ch * kSolveChunk + rr);
-        stage[(buf * kSolveChunk + rr) * m + c] = (j >= 0 && j < m) ? Src[static_cast<int64_t>(j) * m + c] : 0.0;
+    auto issue = [&](int ch, int buf) {
+      // pass 0 walks U rows 0..m-1, pass 1 walks L rows m-1..0
+      if (vec) {
+        const int cpr = m / 2;
+        for (int t = tid; t < kSolveChunk * cpr; t += kSolveWarps * 32) {
+          const int rr = t / cpr, c = (t % cpr) * 2;
+          const int j = pass == 0 ? ch * kSolveChunk + rr : m - 1 - (ch * kSolveChunk + rr);
+          if (j >= 0 && j < m)
+            trals::cp_async_zfill(stage + (buf * kSolveChunk + rr) * mp + c, Src + static_cast<int64_t>(j) * m + c,
+                                  16, 16);
+        }
+      } else {
+        for (int t = tid; t < kSolveChunk * m; t += kSolveWarps * 32) {
+          const int rr = t / m, c = t % m;
+          const int j = pass == 0 ? ch * kSolveChunk + rr : m - 1 - (ch * kSolveChunk + rr);
+          if (j >= 0 && j < m)
+            trals::cp_async_zfill(stage + (buf * kSolveChunk + rr) * mp + c, Src + static_cast<int64_t>(j) * m + c,
+                                  8, 8);
+        }
       }
+      trals::cp_async_commit();
     };
-    load_chunk(0, 0);
-    __syncthreads();
+    issue(0, 0);
     for (int ch = 0; ch < nchunks; ++ch) {
-      if (ch + 1 < nchunks) load_chunk(ch + 1, (ch + 1) & 1);
-      const double* buf = stage + (ch & 1) * kSolveChunk * m;
+      if (ch + 1 < nchunks) {
+        issue(ch + 1, (ch + 1) & 1);
+        trals::cp_async_wait<1>();
+      } else {
+        trals::cp_async_wait<0>();
+      }
+      __syncthreads();
+      const double* buf = stage + (ch & 1) * kSolveChunk * mp;
+#pragma unroll 1
       for (int rr = 0; rr < kSolveChunk; ++rr) {
         const int j = pass == 0 ? ch * kSolveChunk + rr : m - 1 - (ch * kSolveChunk + rr);
         if (j < 0 || j >= m) break;
-        const double* urow = buf + rr * m;
+        const double* urow = buf + rr * mp;
         const int js = j >> 5, jl = j & 31;
-        double v = 0.0;
+        const double dj = dinv[j];
+        double y[kSolveRPW];
 #pragma unroll
-        for (int s = 0; s < NR; ++s)
-          if (s == js) v = r[s];
-        v = __shfl_sync(0xffffffffu, v, jl);
-        const double y = v / urow[j];
+        for (int q = 0; q < kSolveRPW; ++q) {
+          double v = 0.0;
+#pragma unroll
+          for (int s = 0; s < NR; ++s) v = (s == js) ? r[q][s] : v;
+          y[q] = __shfl_sync(0xffffffffu, v, jl) * dj;
+        }
 #pragma unroll
         for (int s = 0; s < NR; ++s) {
           const int k = s * 32 + lane;
-          if (k < m) {
-            if (k == j) r[s] = y;
-            else if (pass == 0 ? (k > j) : (k < j)) r[s] = fma(-y, urow[k], r[s]);
+          const bool live = pass == 0 ? (k > j && k < m) : (k < j);
+          const double u = live ? urow[k] : 0.0;
+#pragma unroll
+          for (int q = 0; q < kSolveRPW; ++q) {
+            r[q][s] = (k == j) ? y[q] : fma(-y[q], u, r[q][s]);
           }
         }
       }
       __syncthreads();
     }
-    __syncthreads();
   }
-  if (active) {
+#pragma unroll
+  for (int q = 0; q < kSolveRPW; ++q) {
+    const int64_t row = row0 + q;
+    if (row >= rows) continue;
 #pragma unroll
     for (int s = 0; s < NR; ++s) {
       const int k = s * 32 + lane;
-      if (k < m) Z[row * m + k] = r[s];
+      if (k < m) Z[row * m + k] = r[q][s];
     }
   }
 }
@@ -503,10 +600,16 @@ __global__ void __launch_bounds__(kSolveWarps * 32) chol_solve_kernel(const doub
 template <int NR>
 int launch_solve(const double* U, const double* L, int m, const double* Mr, int64_t rows, double* Z,
                  cudaStream_t s) {
-  const size_t smem = sizeof(double) * 2 * kSolveChunk * m;
+  const int mp = (m + 1) & ~1;
+  const size_t smem = sizeof(double) * (2 * kSolveChunk * mp + m);
   auto k = chol_solve_kernel<NR>;
-  if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-  const int64_t blocks = (rows + kSolveWarps - 1) / kSolveWarps;
+  static size_t attr = 0;
+  if (smem > 48 * 1024 && smem > attr) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    attr = smem;
+  }
+  const int64_t per_cta = kSolveWarps * kSolveRPW;
+  const int64_t blocks = (rows + per_cta - 1) / per_cta;
   k<<<static_cast<unsigned>(blocks), kSolveWarps * 32, smem, s>>>(U, L, m, Mr, rows, Z);
   return launch_status();
 }
@@ -885,15 +988,17 @@ int trals_gram_chain_f64(int N, int n, const int32_t* ranks, const double* const
 
 int trals_cholesky_f64(const double* S, int m, double* U, double* L, int check_degen, int* info, void* stream) {
   if (!S || !U || !L || !info || m < 1) return TRALS_ERR_ARG;
-  const int pw = ((m + 7) / 8) * 8 + 4;
-  const size_t smem = sizeof(double) * kCholNB * pw;
-  if (smem > 200 * 1024) return TRALS_ERR_UNSUPPORTED;
-  static int attr = 0;
-  if (smem > 48 * 1024 && static_cast<int>(smem) > attr) {
-    cudaFuncSetAttribute(cholesky_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = 200 * 1024;
+  const size_t smem = cholesky_smem(m);
+  if (smem > 220 * 1024) return TRALS_ERR_UNSUPPORTED;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(cholesky_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    cudaFuncSetAttribute(cholesky_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    attr = true;
   }
-  cholesky_kernel<<<1, kCholThreads, smem, static_cast<cudaStream_t>(stream)>>>(S, m, U, L, check_degen, info);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (m <= kCholSmemMax) cholesky_kernel<true><<<1, kCholThreads, smem, s>>>(S, m, U, L, check_degen, info);
+  else cholesky_kernel<false><<<1, kCholThreads / 2, smem, s>>>(S, m, U, L, check_degen, info);
   return launch_status();
 }
 
@@ -902,13 +1007,21 @@ int trals_chol_solve_f64(const double* U, const double* L, int m, const double* 
   if (!U || !L || !Mr || !Z || m < 1) return TRALS_ERR_ARG;
   if (rows <= 0) return TRALS_OK;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const int nr = (m + 31) / 32;
-  if (nr <= 1) return launch_solve<1>(U, L, m, Mr, rows, Z, s);
-  if (nr <= 2) return launch_solve<2>(U, L, m, Mr, rows, Z, s);
-  if (nr <= 4) return launch_solve<4>(U, L, m, Mr, rows, Z, s);
-  if (nr <= 8) return launch_solve<8>(U, L, m, Mr, rows, Z, s);
-  if (nr <= 16) return launch_solve<16>(U, L, m, Mr, rows, Z, s);
-  if (nr <= 24) return launch_solve<24>(U, L, m, Mr, rows, Z, s);
+  switch ((m + 31) / 32) {
+    case 1: return launch_solve<1>(U, L, m, Mr, rows, Z, s);
+    case 2: return launch_solve<2>(U, L, m, Mr, rows, Z, s);
+    case 3: return launch_solve<3>(U, L, m, Mr, rows, Z, s);
+    case 4: return launch_solve<4>(U, L, m, Mr, rows, Z, s);
+    case 5: return launch_solve<5>(U, L, m, Mr, rows, Z, s);
+    case 6: case 7: case 8: return launch_solve<8>(U, L, m, Mr, rows, Z, s);
+    case 9: case 10: return launch_solve<10>(U, L, m, Mr, rows, Z, s);
+    case 11: case 12: case 13: return launch_solve<13>(U, L, m, Mr, rows, Z, s);
+    case 14: case 15: case 16: return launch_solve<16>(U, L, m, Mr, rows, Z, s);
+    case 17: case 18: case 19: case 20: return launch_solve<20>(U, L, m, Mr, rows, Z, s);
+    case 21: case 22: case 23: case 24: return launch_solve<24>(U, L, m, Mr, rows, Z, s);
+    case 25: case 26: case 27: case 28: case 29: case 30: case 31: case 32:
+      return launch_solve<32>(U, L, m, Mr, rows, Z, s);
+  }
   return TRALS_ERR_UNSUPPORTED;
 }
 

@@ -130,6 +130,7 @@ class SweepEngine:
             self.Gc_loc = self._empty(self.R(s), self.dl[s], self.R(s + 1))
         self.gws_need = 1
         self.gws = None  # sized after compile
+        self.graph = None
 
     # local views used by the X contractions
     def core_c(self, j):
@@ -443,6 +444,40 @@ class SweepEngine:
 
     def cores_host(self):
         return [g.detach().cpu().numpy().copy() for g in self.Gc]
+
+    # ------------------------------------------------------------ CUDA graphs
+    def capture(self, with_error=True):
+        """Capture one sweep (+ the error terms into `err_cur`) as a CUDA graph.
+
+        Every buffer is owned by the engine, so the graph stays valid for the
+        engine's lifetime; replaying it re-launches the identical kernel list
+        with a single host call (the small configs are launch-bound)."""
+        if not self.x.is_cuda:
+            raise RuntimeError("graphs need a CUDA engine")
+        if self.world > 1:
+            raise RuntimeError("sharded sweeps run eagerly (collectives between kernels)")
+        old = self.stream
+        cap = torch.cuda.Stream(device=self.dev)
+        cap.wait_stream(old)
+        g = torch.cuda.CUDAGraph()
+        self.stream = cap
+        try:
+            with torch.cuda.stream(cap):
+                g.capture_begin()
+                self.run_sweep()
+                if with_error:
+                    self.error_step(self.err_cur)
+                g.capture_end()
+        finally:
+            self.stream = old
+        old.wait_stream(cap)
+        self.graph = g
+        return g
+
+    def replay(self):
+        """Replay the captured sweep on the engine's stream."""
+        with torch.cuda.stream(self.stream):
+            self.graph.replay()
 
     def mttsp_flops_per_sweep(self):
         """Algorithmic RHS flops of one sweep: sum_n 2 |X| R_n R_{n+1}."""
