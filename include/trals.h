@@ -119,16 +119,22 @@ int trals_gram_chain_f64(int N, int n, const int32_t* ranks, const double* const
 
 /* spd_solve (linalg.py:55-81): symmetry check + symmetrise + upper Cholesky
  * S = U^T U.  Writes U (upper, row-major) and L = U^T (row-major) into d_U,
- * d_L.  Pivot failures go to d_info[TRALS_INFO_CHOL]; with check_degen the
- * 1e-13 triangular floor of tri_solve_right (linalg.py:96-99) is evaluated on
- * U and reported in d_info[TRALS_INFO_DEGEN]. */
-int trals_cholesky_f64(const double* d_S, int m, double* d_U, double* d_L, int check_degen,
+ * d_L.  m <= 152: one CTA, matrix resident in shared memory; larger m: blocked
+ * (64-row panels, diagonal blocks factored+inverted in shared memory, panel and
+ * trailing updates as DMMA GEMMs), with the diagonal-block inverses kept in
+ * d_aux (trals_cholesky_aux_elems) for the solve.  Pivot failures go to
+ * d_info[TRALS_INFO_CHOL]; with check_degen the 1e-13 triangular floor of
+ * tri_solve_right (linalg.py:96-99) is evaluated on U -> d_info[TRALS_INFO_DEGEN]. */
+int64_t trals_cholesky_aux_elems(int m);
+int trals_cholesky_f64(const double* d_S, int m, double* d_U, double* d_L, double* d_aux, int check_degen,
                        int* d_info, void* stream);
 
 /* Z S = M with S = U^T U: Y U = M then Z U^T = Y, row-parallel
- * (scipy cho_solve / solve_triangular, linalg.py:76,100). */
-int trals_chol_solve_f64(const double* d_U, const double* d_L, int m, const double* d_M,
-                         int64_t rows, double* d_Z, void* stream);
+ * (scipy cho_solve / solve_triangular, linalg.py:76,100).  d_aux as written by
+ * trals_cholesky_f64; d_ws holds trals_chol_solve_ws_elems doubles. */
+int64_t trals_chol_solve_ws_elems(int64_t rows, int m);
+int trals_chol_solve_f64(const double* d_U, const double* d_L, const double* d_aux, int m, const double* d_M,
+                         int64_t rows, double* d_Z, double* d_ws, int64_t ws_elems, void* stream);
 
 /* Sum of squares of n doubles into d_out[0] (tensor_ops.py:237-239 norm) and the
  * number of non-finite entries into d_out[1] (validation.py:53-54). */

@@ -42,7 +42,8 @@ struct GemmArgs {
   double* C;
   CMap cmap;
   int64_t P, M, K, N;
-  int beta;           // 0: C = acc, 1: C += acc
+  int beta;           // 0: C = alpha*acc, 1: C += alpha*acc
+  double alpha;
   int64_t kchunk;     // K range per split (multiple of kBK)
   int splits;         // > 1: write raw partials to ws[split][p][m][n]
   double* ws;
@@ -219,7 +220,7 @@ dmma_gemm_kernel(const GemmArgs g) {
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         if (!col_ok[j][e]) continue;
-        const double v = acc[i][j][e];
+        const double v = g.splits > 1 ? acc[i][j][e] : g.alpha * acc[i][j][e];
         if (g.splits > 1) {
           wsrow[n0 + wn0 + j * 8 + 2 * fk + e] = v;
         } else {
@@ -240,6 +241,7 @@ __global__ void splitk_reduce_kernel(const GemmArgs g) {
        idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     double s = 0.0;
     for (int z = 0; z < g.splits; ++z) s += g.ws[z * plane + idx];
+    s *= g.alpha;
     const int64_t pm = idx / N;  // (p, m) row index
     const uint32_t n = static_cast<uint32_t>(idx - pm * N);
     const uint32_t m = static_cast<uint32_t>(pm % M);

@@ -109,7 +109,7 @@ inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 
 
 int gemm(const double* A, int64_t sAp, int64_t sAm, int64_t sAk, int64_t P, int64_t M, int64_t K, int64_t N,
          const double* B, int64_t ldb, double* C, const CMap& cm, int beta, double* ws, int64_t ws_elems,
-         cudaStream_t s) {
+         cudaStream_t s, double alpha = 1.0) {
   if (P <= 0 || M <= 0 || N <= 0) return TRALS_OK;
   if (!A || !B || !C) return TRALS_ERR_ARG;
   const bool ak = (sAk == 1);
@@ -141,7 +141,7 @@ int gemm(const double* A, int64_t sAp, int64_t sAm, int64_t sAk, int64_t P, int6
   GemmArgs g;
   g.A = A; g.sAp = sAp; g.sAm = sAm; g.sAk = sAk;
   g.B = B; g.ldb = ldb; g.C = C; g.cmap = cm;
-  g.P = P; g.M = M; g.K = K; g.N = N; g.beta = beta;
+  g.P = P; g.M = M; g.K = K; g.N = N; g.beta = beta; g.alpha = alpha;
   g.kchunk = sp.kchunk; g.splits = sp.splits; g.ws = ws;
   // 16-byte vector loads need every row start 16-byte aligned
   const int64_t sA_lead = ak ? sAm : sAk;
@@ -614,6 +614,227 @@ int launch_solve(const double* U, const double* L, int m, const double* Mr, int6
   return launch_status();
 }
 
+// ---------------------------------------------------------------------------
+// Blocked Cholesky + triangular solves for m > kCholSmemMax (R = 20: m = 400).
+// Right-looking with 64-row panels: a one-CTA kernel factors the 64x64
+// diagonal block in shared memory and inverts it; the panel row block and the
+// trailing update are DMMA GEMMs over the whole GPU (the inverse turns the
+// panel TRSM into a GEMM).  The same diagonal inverses drive the blocked
+// forward/backward substitution of the solve.
+// ---------------------------------------------------------------------------
+constexpr int kBlkNB = 64;
+
+__global__ void __launch_bounds__(1024) chol_sym_kernel(const double* __restrict__ S, int m,
+                                                        double* __restrict__ U, int* __restrict__ info) {
+  __shared__ double red[64];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  double amax = 0.0, asym = 0.0;
+  for (int i = warp; i < m; i += nwarps)
+    for (int j = lane; j < m; j += 32) {
+      const double sij = S[i * m + j], sji = S[j * m + i];
+      amax = fmax(amax, fabs(sij));
+      asym = fmax(asym, fabs(sij - sji));
+      U[i * m + j] = 0.5 * (sij + sji);
+    }
+  chol_reduce_flags(amax, asym, red, info);
+}
+
+// factor the pb x pb diagonal block at (p0, p0) of U in place; W = block^{-1}, WT = W^T (ld kBlkNB)
+__global__ void __launch_bounds__(256) chol_diag_kernel(double* __restrict__ U, int m, int p0, int pb,
+                                                        double* __restrict__ W, double* __restrict__ WT,
+                                                        int* __restrict__ info) {
+  extern __shared__ __align__(16) double dsm[];
+  double (*a)[kBlkNB + 1] = reinterpret_cast<double (*)[kBlkNB + 1]>(dsm);
+  double (*w)[kBlkNB + 1] = reinterpret_cast<double (*)[kBlkNB + 1]>(dsm + kBlkNB * (kBlkNB + 1));
+  __shared__ int failed;
+  const int tid = threadIdx.x;
+  if (tid == 0) failed = info[TRALS_INFO_CHOL];
+  for (int t = tid; t < pb * pb; t += blockDim.x) {
+    const int r = t / pb, c = t - r * pb;
+    a[r][c] = c >= r ? U[(p0 + r) * m + p0 + c] : 0.0;
+  }
+  __syncthreads();
+  if (failed) return;
+  for (int j = 0; j < pb; ++j) {
+    const double d = a[j][j];
+    if (!(d > 0.0)) {
+      if (tid == 0) info[TRALS_INFO_CHOL] = p0 + j + 1;
+      return;  // uniform: every thread read the same pivot
+    }
+    const double dinv = rsqrt(d);
+    __syncthreads();
+    for (int c = j + tid; c < pb; c += blockDim.x) a[j][c] *= dinv;
+    __syncthreads();
+    const int rows = pb - j - 1;
+    for (int t = tid; t < rows * rows; t += blockDim.x) {
+      const int r = j + 1 + t / rows, c = j + 1 + t % rows;
+      if (c >= r) a[r][c] = fma(-a[j][r], a[j][c], a[r][c]);
+    }
+    __syncthreads();
+  }
+  for (int t = tid; t < pb * pb; t += blockDim.x) {
+    const int r = t / pb, c = t - r * pb;
+    if (c >= r) U[(p0 + r) * m + p0 + c] = a[r][c];
+  }
+  // W = a^{-1} (upper): row k from the bottom, W[k][j] = (d_kj - sum_{t=k+1..j} a[k][t] W[t][j]) / a[k][k]
+  for (int k = pb - 1; k >= 0; --k) {
+    for (int j = tid; j < pb; j += blockDim.x) {
+      double v = 0.0;
+      if (j >= k) {
+        v = (j == k) ? 1.0 : 0.0;
+        for (int t = k + 1; t <= j; ++t) v = fma(-a[k][t], w[t][j], v);
+        v /= a[k][k];
+      }
+      w[k][j] = v;
+    }
+    __syncthreads();
+  }
+  for (int t = tid; t < kBlkNB * kBlkNB; t += blockDim.x) {
+    const int r = t / kBlkNB, c = t - r * kBlkNB;
+    const bool in = r < pb && c < pb;
+    W[t] = in ? w[r][c] : 0.0;
+    WT[t] = in ? w[c][r] : 0.0;
+  }
+}
+
+// zero the strict lower triangle of U and write L = U^T
+__global__ void chol_finalize_kernel(double* __restrict__ U, double* __restrict__ L, int m) {
+  __shared__ double tile[32][33];
+  const int bi = blockIdx.y * 32, bj = blockIdx.x * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+  for (int r = ty; r < 32; r += 8) {
+    const int i = bi + r, j = bj + tx;
+    double v = 0.0;
+    if (i < m && j < m) {
+      v = j >= i ? U[i * m + j] : 0.0;
+    }
+    tile[r][tx] = v;
+  }
+  __syncthreads();
+  for (int r = ty; r < 32; r += 8) {
+    const int i = bi + r, j = bj + tx;
+    if (i < m && j < m && j < i) U[i * m + j] = 0.0;
+    const int li = bj + r, lj = bi + tx;  // L[li][lj] = U[lj][li]
+    if (li < m && lj < m) L[li * m + lj] = tile[tx][r];
+  }
+}
+
+__global__ void __launch_bounds__(1024) degen_kernel(const double* __restrict__ U, int m, int* __restrict__ info) {
+  __shared__ double red[32], sd[32];
+  __shared__ int si[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  double umax = 0.0, dmin = INFINITY;
+  int didx = 0;
+  for (int i = warp; i < m; i += nwarps)
+    for (int j = lane; j < m; j += 32) {
+      if (j < i) continue;
+      const double u = fabs(U[i * m + j]);
+      umax = fmax(umax, u);
+      if (i == j && u < dmin) { dmin = u; didx = i; }
+    }
+  for (int o = 16; o > 0; o >>= 1) {
+    umax = fmax(umax, __shfl_xor_sync(0xffffffffu, umax, o));
+    const double od = __shfl_xor_sync(0xffffffffu, dmin, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, didx, o);
+    if (od < dmin || (od == dmin && oi < didx)) { dmin = od; didx = oi; }
+  }
+  if (lane == 0) { red[warp] = umax; sd[warp] = dmin; si[warp] = didx; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0, d = INFINITY;
+    int di = 0;
+    for (int w = 0; w < nwarps; ++w) {
+      a = fmax(a, red[w]);
+      if (sd[w] < d || (sd[w] == d && si[w] < di)) { d = sd[w]; di = si[w]; }
+    }
+    if (d <= 1e-13 * a) info[TRALS_INFO_DEGEN] = di + 1;  // linalg.py:96-99
+  }
+}
+
+int64_t blocked_aux_elems(int m) {
+  const int nblk = (m + kBlkNB - 1) / kBlkNB;
+  return static_cast<int64_t>(nblk) * 2 * kBlkNB * kBlkNB;
+}
+
+int blocked_cholesky(const double* S, int m, double* U, double* L, double* aux, int check_degen, int* info,
+                     cudaStream_t s) {
+  chol_sym_kernel<<<1, 1024, 0, s>>>(S, m, U, info);
+  if (int st = launch_status()) return st;
+  const CMap rm = rowmajor(m);
+  for (int p0 = 0, b = 0; p0 < m; p0 += kBlkNB, ++b) {
+    const int pb = std::min(kBlkNB, m - p0);
+    const int rest = m - p0 - pb;
+    double* W = aux + static_cast<int64_t>(b) * 2 * kBlkNB * kBlkNB;
+    double* WT = W + kBlkNB * kBlkNB;
+    constexpr size_t kDiagSmem = sizeof(double) * 2 * kBlkNB * (kBlkNB + 1);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(chol_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kDiagSmem);
+      attr = true;
+    }
+    chol_diag_kernel<<<1, 256, kDiagSmem, s>>>(U, m, p0, pb, W, WT, info);
+    if (int st = launch_status()) return st;
+    if (rest == 0) continue;
+    double* U12 = U + static_cast<int64_t>(p0) * m + p0 + pb;
+    // U12 <- W^T A12 (in place: one M tile, each CTA rewrites exactly the columns it read)
+    int st = gemm(WT, 0, kBlkNB, 1, 1, pb, pb, rest, U12, m, U12, rm, 0, nullptr, 0, s);
+    if (st) return st;
+    // A22 -= U12^T U12
+    double* A22 = U + static_cast<int64_t>(p0 + pb) * m + p0 + pb;
+    st = gemm(U12, 0, 1, m, 1, rest, pb, rest, U12, m, A22, rm, 1, nullptr, 0, s, -1.0);
+    if (st) return st;
+  }
+  dim3 grid((m + 31) / 32, (m + 31) / 32);
+  chol_finalize_kernel<<<grid, dim3(32, 8), 0, s>>>(U, L, m);
+  if (int st = launch_status()) return st;
+  if (check_degen) {
+    degen_kernel<<<1, 1024, 0, s>>>(U, m, info);
+    return launch_status();
+  }
+  return TRALS_OK;
+}
+
+int64_t blocked_solve_ws(int64_t rows, int m) { return rows * m; }
+
+// Z S = M, S = U^T U:  Y U = M (forward), Z U^T = Y (backward), 64-column blocks
+int blocked_solve(const double* U, const double* L, const double* aux, int m, const double* Mr, int64_t rows,
+                  double* Z, double* ws, cudaStream_t s) {
+  const CMap rm = rowmajor(m);
+  double* R = ws;   // running right-hand side
+  double* Y = Z;    // forward result lives in Z's storage, then overwritten block by block
+  const int nblk = (m + kBlkNB - 1) / kBlkNB;
+  // forward: R = M; Y_b = (R_b - Y_{<b} U_{<b,b}) W_b
+  if (cudaMemcpyAsync(R, Mr, sizeof(double) * rows * m, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+    return TRALS_ERR_CUDA;
+  for (int b = 0; b < nblk; ++b) {
+    const int j0 = b * kBlkNB, pb = std::min(kBlkNB, m - j0);
+    const double* W = aux + static_cast<int64_t>(b) * 2 * kBlkNB * kBlkNB;
+    if (j0 > 0) {
+      int st = gemm(Y, 0, m, 1, 1, rows, j0, pb, U + j0, m, R + j0, rm, 1, nullptr, 0, s, -1.0);
+      if (st) return st;
+    }
+    int st = gemm(R + j0, 0, m, 1, 1, rows, pb, pb, W, kBlkNB, Y + j0, rm, 0, nullptr, 0, s);
+    if (st) return st;
+  }
+  // backward: R = Y; Z_b = (R_b - Z_{>b} L_{>b,b}) W_b^T, last block first (Z overwrites Y in place:
+  // block b of Y is consumed into R before block b of Z is written)
+  if (cudaMemcpyAsync(R, Y, sizeof(double) * rows * m, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+    return TRALS_ERR_CUDA;
+  for (int b = nblk - 1; b >= 0; --b) {
+    const int j0 = b * kBlkNB, pb = std::min(kBlkNB, m - j0);
+    const int j1 = j0 + pb;
+    const double* WT = aux + static_cast<int64_t>(b) * 2 * kBlkNB * kBlkNB + kBlkNB * kBlkNB;
+    if (j1 < m) {
+      int st = gemm(Z + j1, 0, m, 1, 1, rows, m - j1, pb, L + static_cast<int64_t>(j1) * m + j0, m, R + j0, rm, 1,
+                    nullptr, 0, s, -1.0);
+      if (st) return st;
+    }
+    int st = gemm(R + j0, 0, m, 1, 1, rows, pb, pb, WT, kBlkNB, Z + j0, rm, 0, nullptr, 0, s);
+    if (st) return st;
+  }
+  return TRALS_OK;
+}
+
 // C(m, n) = F[m * ncols + n] scattered through a CMap
 __global__ void reshuffle_kernel(const double* __restrict__ F, int64_t rows, int64_t cols, CMap cm,
                                  double* __restrict__ C) {
@@ -986,41 +1207,43 @@ int trals_gram_chain_f64(int N, int n, const int32_t* ranks, const double* const
   return TRALS_OK;
 }
 
-int trals_cholesky_f64(const double* S, int m, double* U, double* L, int check_degen, int* info, void* stream) {
+int64_t trals_cholesky_aux_elems(int m) { return m > kCholSmemMax ? blocked_aux_elems(m) : 0; }
+
+int trals_cholesky_f64(const double* S, int m, double* U, double* L, double* aux, int check_degen, int* info,
+                       void* stream) {
   if (!S || !U || !L || !info || m < 1) return TRALS_ERR_ARG;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (m > kCholSmemMax) {
+    if (!aux) return TRALS_ERR_WORKSPACE;
+    return blocked_cholesky(S, m, U, L, aux, check_degen, info, s);
+  }
   const size_t smem = cholesky_smem(m);
-  if (smem > 220 * 1024) return TRALS_ERR_UNSUPPORTED;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(cholesky_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    cudaFuncSetAttribute(cholesky_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     attr = true;
   }
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (m <= kCholSmemMax) cholesky_kernel<true><<<1, kCholThreads, smem, s>>>(S, m, U, L, check_degen, info);
-  else cholesky_kernel<false><<<1, kCholThreads / 2, smem, s>>>(S, m, U, L, check_degen, info);
+  cholesky_kernel<true><<<1, kCholThreads, smem, s>>>(S, m, U, L, check_degen, info);
   return launch_status();
 }
 
-int trals_chol_solve_f64(const double* U, const double* L, int m, const double* Mr, int64_t rows, double* Z,
-                         void* stream) {
+int64_t trals_chol_solve_ws_elems(int64_t rows, int m) { return m > kCholSmemMax ? blocked_solve_ws(rows, m) : 0; }
+
+int trals_chol_solve_f64(const double* U, const double* L, const double* aux, int m, const double* Mr, int64_t rows,
+                         double* Z, double* ws, int64_t ws_elems, void* stream) {
   if (!U || !L || !Mr || !Z || m < 1) return TRALS_ERR_ARG;
   if (rows <= 0) return TRALS_OK;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (m > kCholSmemMax) {
+    if (!aux || !ws || ws_elems < blocked_solve_ws(rows, m)) return TRALS_ERR_WORKSPACE;
+    return blocked_solve(U, L, aux, m, Mr, rows, Z, ws, s);
+  }
   switch ((m + 31) / 32) {
     case 1: return launch_solve<1>(U, L, m, Mr, rows, Z, s);
     case 2: return launch_solve<2>(U, L, m, Mr, rows, Z, s);
     case 3: return launch_solve<3>(U, L, m, Mr, rows, Z, s);
     case 4: return launch_solve<4>(U, L, m, Mr, rows, Z, s);
     case 5: return launch_solve<5>(U, L, m, Mr, rows, Z, s);
-    case 6: case 7: case 8: return launch_solve<8>(U, L, m, Mr, rows, Z, s);
-    case 9: case 10: return launch_solve<10>(U, L, m, Mr, rows, Z, s);
-    case 11: case 12: case 13: return launch_solve<13>(U, L, m, Mr, rows, Z, s);
-    case 14: case 15: case 16: return launch_solve<16>(U, L, m, Mr, rows, Z, s);
-    case 17: case 18: case 19: case 20: return launch_solve<20>(U, L, m, Mr, rows, Z, s);
-    case 21: case 22: case 23: case 24: return launch_solve<24>(U, L, m, Mr, rows, Z, s);
-    case 25: case 26: case 27: case 28: case 29: case 30: case 31: case 32:
-      return launch_solve<32>(U, L, m, Mr, rows, Z, s);
   }
   return TRALS_ERR_UNSUPPORTED;
 }

@@ -118,6 +118,10 @@ class SweepEngine:
         mmax = max(self.R(n) * self.R(n + 1) for n in range(N))
         self.U = self._empty(mmax, mmax)
         self.Lo = self._empty(mmax, mmax)
+        self.chol_aux = self._empty(max(1, max(self.lib.trals_cholesky_aux_elems(self.R(n) * self.R(n + 1))
+                                              for n in range(N))))
+        self.solve_ws = self._empty(max(1, max(self.lib.trals_chol_solve_ws_elems(self.dims[n], self.R(n) * self.R(n + 1))
+                                              for n in range(N))))
         self.info = torch.zeros(L.INFO_SLOTS, dtype=torch.int32, device=self.dev)
         self.xnorm2 = self._empty(2)  # [|X|^2, #non-finite]
         self.err_cur = self._empty(3)
@@ -344,10 +348,13 @@ class SweepEngine:
         check_degen = 1 if self.variant == "qr" else 0
 
         def solve(n=n, S=S, M=M, rr=rr, check_degen=check_degen):
-            L.check(self.lib.trals_cholesky_f64(S.data_ptr(), rr, self.U.data_ptr(), self.Lo.data_ptr(), check_degen,
-                                                self.info.data_ptr(), self._sp()), "cholesky")
-            L.check(self.lib.trals_chol_solve_f64(self.U.data_ptr(), self.Lo.data_ptr(), rr, M.data_ptr(),
-                                                  self.dims[n], self.Gt[n].data_ptr(), self._sp()), "chol_solve")
+            L.check(self.lib.trals_cholesky_f64(S.data_ptr(), rr, self.U.data_ptr(), self.Lo.data_ptr(),
+                                                self.chol_aux.data_ptr(), check_degen, self.info.data_ptr(),
+                                                self._sp()), "cholesky")
+            L.check(self.lib.trals_chol_solve_f64(self.U.data_ptr(), self.Lo.data_ptr(), self.chol_aux.data_ptr(), rr,
+                                                  M.data_ptr(), self.dims[n], self.Gt[n].data_ptr(),
+                                                  self.solve_ws.data_ptr(), self.solve_ws.numel(), self._sp()),
+                    "chol_solve")
         self.steps.append(Step("solve", solve, f"solve{n}"))
 
         def refresh(n=n):

@@ -110,25 +110,38 @@ def coefficient_gram(cores_c, n: int) -> torch.Tensor:
     return S
 
 
-def cholesky(S: torch.Tensor, check_degen: bool = False):
-    """Upper Cholesky S = U^T U with the reference's checks; returns (U, L, info)."""
+class CholFactor:
+    """Device Cholesky factor: U (upper), L = U^T, diagonal-block inverses (aux), info flags."""
+
+    def __init__(self, U, Lo, aux, info):
+        self.U, self.L, self.aux, self.info = U, Lo, aux, info
+
+    def __iter__(self):  # (U, L, info) unpacking
+        return iter((self.U, self.L, self.info))
+
+
+def cholesky(S: torch.Tensor, check_degen: bool = False) -> CholFactor:
+    """Upper Cholesky S = U^T U with the reference's checks (linalg.py:55-81)."""
     _require_cuda(S)
     m = int(S.shape[0])
     U = torch.empty_like(S)
     Lo = torch.empty_like(S)
+    aux = ws(L.lib().trals_cholesky_aux_elems(m), S.device)
     info = torch.zeros(L.INFO_SLOTS, dtype=torch.int32, device=S.device)
-    L.check(L.lib().trals_cholesky_f64(S.data_ptr(), m, U.data_ptr(), Lo.data_ptr(), int(check_degen),
-                                       info.data_ptr(), _stream()), "trals_cholesky_f64")
-    return U, Lo, info
+    L.check(L.lib().trals_cholesky_f64(S.data_ptr(), m, U.data_ptr(), Lo.data_ptr(), aux.data_ptr(),
+                                       int(check_degen), info.data_ptr(), _stream()), "trals_cholesky_f64")
+    return CholFactor(U, Lo, aux, info)
 
 
-def chol_solve(U: torch.Tensor, Lo: torch.Tensor, M: torch.Tensor) -> torch.Tensor:
-    """Z with Z (U^T U) = M, row-parallel triangular solves."""
-    _require_cuda(U, Lo, M)
-    m = int(U.shape[0])
+def chol_solve(f: CholFactor, M: torch.Tensor) -> torch.Tensor:
+    """Z with Z (U^T U) = M (cho_solve, linalg.py:76)."""
+    _require_cuda(f.U, f.L, M)
+    m = int(f.U.shape[0])
+    rows = int(M.shape[0])
     Z = torch.empty_like(M)
-    L.check(L.lib().trals_chol_solve_f64(U.data_ptr(), Lo.data_ptr(), m, M.data_ptr(), int(M.shape[0]),
-                                         Z.data_ptr(), _stream()), "trals_chol_solve_f64")
+    w = ws(L.lib().trals_chol_solve_ws_elems(rows, m), M.device)
+    L.check(L.lib().trals_chol_solve_f64(f.U.data_ptr(), f.L.data_ptr(), f.aux.data_ptr(), m, M.data_ptr(), rows,
+                                         Z.data_ptr(), w.data_ptr(), w.numel(), _stream()), "trals_chol_solve_f64")
     return Z
 
 

@@ -183,7 +183,13 @@ class FakeTrals:
         _arr(S, s.size)[:] = s.ravel()
         return 0
 
-    def trals_cholesky_f64(self, S, m, U, Lo, check_degen, info, stream):
+    def trals_cholesky_aux_elems(self, m):
+        return 1
+
+    def trals_chol_solve_ws_elems(self, rows, m):
+        return 1
+
+    def trals_cholesky_f64(self, S, m, U, Lo, aux, check_degen, info, stream):
         self._count("cholesky")
         s = _arr(S, m * m).reshape(m, m)
         inf = _iarr(info, 4)
@@ -204,7 +210,7 @@ class FakeTrals:
                 inf[2] = int(np.argmin(d)) + 1
         return 0
 
-    def trals_chol_solve_f64(self, U, Lo, m, M, rows, Z, stream):
+    def trals_chol_solve_f64(self, U, Lo, aux, m, M, rows, Z, ws, ws_elems, stream):
         self._count("chol_solve")
         u = _arr(U, m * m).reshape(m, m)
         rhs = _arr(M, rows * m).reshape(rows, m)

@@ -88,33 +88,38 @@ def test_coefficient_gram(name):
         assert rel(ops.coefficient_gram(cores, n).cpu().numpy(), g[f"S_{n}"]) < 1e-13
 
 
-@pytest.mark.parametrize("m,rows", [(4, 7), (25, 100), (64, 64), (100, 500), (400, 160), (9, 3), (130, 33)])
+@pytest.mark.parametrize("m,rows", [(4, 7), (25, 100), (64, 64), (100, 500), (400, 160), (9, 3), (130, 33),
+                                    (152, 20), (153, 41), (200, 7), (257, 300), (625, 64)])
 def test_cholesky_solve(m, rows):
     from paper_2210_11362_b200 import ops
     rng = np.random.default_rng(m)
     a = rng.standard_normal((3 * m, m))
     s = a.T @ a
     rhs = rng.standard_normal((rows, m))
-    U, Lo, info = ops.cholesky(cuda(s))
-    assert info.cpu().numpy().tolist() == [0, 0, 0, 0]
+    f = ops.cholesky(cuda(s))
+    assert f.info.cpu().numpy().tolist() == [0, 0, 0, 0]
     ref_u = np.linalg.cholesky(s).T
-    assert rel(U.cpu().numpy(), ref_u) < 1e-12
-    z = ops.chol_solve(U, Lo, cuda(rhs)).cpu().numpy()
+    assert rel(f.U.cpu().numpy(), ref_u) < 1e-12
+    assert rel(f.L.cpu().numpy(), ref_u.T) < 1e-12
+    z = ops.chol_solve(f, cuda(rhs)).cpu().numpy()
     zref, _ = O.solve_spd_right(s, rhs)
     assert rel(z, zref) < 1e-11
 
 
-def test_cholesky_flags():
+@pytest.mark.parametrize("m", [4, 300])
+def test_cholesky_flags(m):
     from paper_2210_11362_b200 import ops
-    s = np.diag([1.0, 2.0, -1.0, 3.0])
-    _, _, info = ops.cholesky(cuda(s))
+    d = np.ones(m)
+    d[2] = -1.0
+    _, _, info = ops.cholesky(cuda(np.diag(d)))
     assert info.cpu().numpy()[0] == 3  # first non-positive pivot, 1-based
-    s = np.eye(3)
+    s = np.eye(m)
     s[0, 2] = 1e-3
     _, _, info = ops.cholesky(cuda(s))
     assert info.cpu().numpy()[1] == 1  # asymmetric beyond 1e-8
-    s = np.diag([1.0, 1e-30, 1.0])
-    _, _, info = ops.cholesky(cuda(s), check_degen=True)
+    d = np.ones(m)
+    d[1] = 1e-30
+    _, _, info = ops.cholesky(cuda(np.diag(d)), check_degen=True)
     assert info.cpu().numpy()[2] == 2  # below the 1e-13 floor
 
 
