@@ -117,23 +117,29 @@ int trals_core_gram_f64(const double* d_core_slice, int Ra, int64_t I, int Rb, d
 int trals_gram_chain_f64(int N, int n, const int32_t* ranks, const double* const* h_E,
                          double* d_S, double* d_tmp, double* d_ws, int64_t ws_elems, void* stream);
 
-/* spd_solve (linalg.py:55-81): symmetry check + symmetrise + upper Cholesky
- * S = U^T U.  Writes U (upper, row-major) and L = U^T (row-major) into d_U,
- * d_L.  m <= 152: one CTA, matrix resident in shared memory; larger m: blocked
- * (64-row panels, diagonal blocks factored+inverted in shared memory, panel and
- * trailing updates as DMMA GEMMs), with the diagonal-block inverses kept in
- * d_aux (trals_cholesky_aux_elems) for the solve.  Pivot failures go to
- * d_info[TRALS_INFO_CHOL]; with check_degen the 1e-13 triangular floor of
- * tri_solve_right (linalg.py:96-99) is evaluated on U -> d_info[TRALS_INFO_DEGEN]. */
+/* spd_solve (linalg.py:55-81), factor step: symmetry check (1e-8 relative,
+ * -> d_info[TRALS_INFO_ASYM]), symmetrise, upper Cholesky S = U^T U
+ * (-> d_U, row-major).  Failing pivot (1-based) -> d_info[TRALS_INFO_CHOL];
+ * with check_degen the 1e-13 floor of tri_solve_right (linalg.py:96-99) is
+ * evaluated on diag(U) -> d_info[TRALS_INFO_DEGEN].
+ *   m <= 112: one CTA, [S | I] resident in shared memory, Gauss-Jordan
+ *             elimination yields U and V = U^{-T} together; d_F = U^{-1},
+ *             d_aux = V;
+ *   m  > 112: blocked (64-row panels: diagonal block + its inverse in one
+ *             CTA, panel and trailing updates as DMMA GEMMs); d_F = U^T,
+ *             d_aux = diagonal-block inverses + GEMM workspace.
+ * d_aux holds trals_cholesky_aux_elems(m) doubles. */
 int64_t trals_cholesky_aux_elems(int m);
-int trals_cholesky_f64(const double* d_S, int m, double* d_U, double* d_L, double* d_aux, int check_degen,
+int trals_cholesky_f64(const double* d_S, int m, double* d_U, double* d_F, double* d_aux, int check_degen,
                        int* d_info, void* stream);
 
-/* Z S = M with S = U^T U: Y U = M then Z U^T = Y, row-parallel
- * (scipy cho_solve / solve_triangular, linalg.py:76,100).  d_aux as written by
- * trals_cholesky_f64; d_ws holds trals_chol_solve_ws_elems doubles. */
+/* spd_solve, solve step (scipy cho_solve, linalg.py:76): Z with Z S = M for the
+ * factor written by trals_cholesky_f64.  m <= 112: Z = (M U^{-1}) U^{-T}, two
+ * DMMA GEMMs; m > 112: blocked forward/backward substitution (Y U = M,
+ * Z U^T = Y) with the diagonal-block inverses.  d_ws holds
+ * trals_chol_solve_ws_elems(rows, m) doubles. */
 int64_t trals_chol_solve_ws_elems(int64_t rows, int m);
-int trals_chol_solve_f64(const double* d_U, const double* d_L, const double* d_aux, int m, const double* d_M,
+int trals_chol_solve_f64(const double* d_U, const double* d_F, const double* d_aux, int m, const double* d_M,
                          int64_t rows, double* d_Z, double* d_ws, int64_t ws_elems, void* stream);
 
 /* Sum of squares of n doubles into d_out[0] (tensor_ops.py:237-239 norm) and the

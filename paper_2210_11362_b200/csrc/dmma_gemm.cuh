@@ -92,7 +92,7 @@ struct Tile {
 };
 
 template <int WM, int WN, int TM, int TN, bool AK, int VEC>
-__global__ void __launch_bounds__(WM * WN * 32)
+__global__ void __launch_bounds__(WM * WN * 32, 2)
 dmma_gemm_kernel(const GemmArgs g) {
   using T = Tile<WM, WN, TM, TN, AK, VEC>;
   extern __shared__ __align__(16) double smem[];
@@ -196,35 +196,34 @@ dmma_gemm_kernel(const GemmArgs g) {
 
   // epilogue: C fragment (row fr, cols 2*fk, 2*fk+1) of every m8n8 block.
   // Address parts are computed once per row / column (32-bit div/mod).
-  int64_t col_off[TN][2];
-  bool col_ok[TN][2];
-#pragma unroll
-  for (int j = 0; j < TN; ++j)
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const int64_t n = n0 + wn0 + j * 8 + 2 * fk + e;
-      col_ok[j][e] = n < g.N;
-      const uint32_t un = static_cast<uint32_t>(n), n2 = static_cast<uint32_t>(g.cmap.N2);
-      col_off[j][e] = static_cast<int64_t>(un / n2) * g.cmap.sn1 + static_cast<int64_t>(un % n2) * g.cmap.sn2;
-    }
+  int64_t row_off[TM];
 #pragma unroll
   for (int i = 0; i < TM; ++i) {
     const int64_t m = m0 + wm0 + i * 8 + fr;
-    if (m >= g.M) continue;
     const uint32_t um = static_cast<uint32_t>(m), m2 = static_cast<uint32_t>(g.cmap.M2);
-    const int64_t row_off = p * g.cmap.sp + static_cast<int64_t>(um / m2) * g.cmap.sm1 +
-                            static_cast<int64_t>(um % m2) * g.cmap.sm2;
-    double* wsrow = g.ws + ((static_cast<int64_t>(split) * g.P + p) * g.M + m) * g.N;
+    row_off[i] = m < g.M ? (g.splits > 1 ? ((static_cast<int64_t>(split) * g.P + p) * g.M + m) * g.N
+                                         : p * g.cmap.sp + static_cast<int64_t>(um / m2) * g.cmap.sm1 +
+                                               static_cast<int64_t>(um % m2) * g.cmap.sm2)
+                         : int64_t(-1);
+  }
 #pragma unroll
-    for (int j = 0; j < TN; ++j) {
+  for (int j = 0; j < TN; ++j) {
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        if (!col_ok[j][e]) continue;
-        const double v = g.splits > 1 ? acc[i][j][e] : g.alpha * acc[i][j][e];
+    for (int e = 0; e < 2; ++e) {
+      const int64_t n = n0 + wn0 + j * 8 + 2 * fk + e;
+      if (n >= g.N) continue;
+      const uint32_t un = static_cast<uint32_t>(n), n2 = static_cast<uint32_t>(g.cmap.N2);
+      const int64_t col = g.splits > 1 ? n
+                                       : static_cast<int64_t>(un / n2) * g.cmap.sn1 +
+                                             static_cast<int64_t>(un % n2) * g.cmap.sn2;
+#pragma unroll
+      for (int i = 0; i < TM; ++i) {
+        if (row_off[i] < 0) continue;
         if (g.splits > 1) {
-          wsrow[n0 + wn0 + j * 8 + 2 * fk + e] = v;
+          g.ws[row_off[i] + col] = acc[i][j][e];
         } else {
-          double* dst = g.C + row_off + col_off[j][e];
+          double* dst = g.C + row_off[i] + col;
+          const double v = g.alpha * acc[i][j][e];
           *dst = g.beta ? *dst + v : v;
         }
       }

@@ -271,17 +271,8 @@ __global__ void __launch_bounds__(1024) sum_final_kernel(const double* __restric
 
 // ---------------------------------------------------------------------------
 // Cholesky S = U^T U (upper, like scipy cho_factor(lower=False), linalg.py:75)
-// One CTA.  m <= kCholSmemMax: whole matrix in shared memory, panel-blocked
-// right-looking factorisation.  Larger m (R = 20 -> m = 400): the matrix stays
-// in L2-resident global memory; panels of 32 rows are factored in shared
-// memory and the trailing upper triangle is updated with DMMA 8x8x4 blocks,
-// each warp keeping kCholBatch blocks' loads in flight.
+// and Z = M S^{-1} (cho_solve, linalg.py:76)
 // ---------------------------------------------------------------------------
-constexpr int kCholNB = 32;        // panel height (rows of U per panel)
-constexpr int kCholThreads = 1024;
-constexpr int kCholSmemMax = 152;  // m*(m+1) doubles <= ~185 KB
-constexpr int kCholBatch = 8;      // trailing 8x8 blocks in flight per warp
-
 __device__ __forceinline__ void chol_reduce_flags(double amax, double asym, double* red, int* info) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int o = 16; o > 0; o >>= 1) {
@@ -298,324 +289,97 @@ __device__ __forceinline__ void chol_reduce_flags(double amax, double asym, doub
   __syncthreads();
 }
 
-// factor rows [p0, p0+pb) of an upper-form matrix held as rows of length w (row r at P + r*ld,
-// column offset p0 already applied): P[j][j..] /= sqrt(P[j][j]), P[r][r..] -= P[j][r] P[j][r..]
-__device__ __forceinline__ int chol_panel(double* P, int ld, int pb, int w, int p0, int* fail) {
-  for (int j = 0; j < pb; ++j) {
-    const double d = P[j * ld + j];
-    if (!(d > 0.0)) {  // non-positive or NaN pivot: dpotrf failure
-      if (threadIdx.x == 0) *fail = p0 + j + 1;
-      return 1;
-    }
+// In-place upper Cholesky of an n x n SPD block held in shared memory rows
+// a[r*ld + c], with an n-column identity block appended at column `aug`:
+// the right-looking row operations that turn A into U turn I into
+// V = U^{-T} (Gauss-Jordan on [A | I]), so the factor and its inverse come
+// out of one pass.  Only the upper triangle of the A part is maintained.
+// Returns the 1-based failing pivot (0 on success); uniform across the CTA.
+__device__ int chol_aug_smem(double* a, int ld, int n, int aug) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  for (int j = 0; j < n; ++j) {
+    const double d = a[j * ld + j];
+    if (!(d > 0.0)) return j + 1;  // dpotrf failure (also NaN)
     const double dinv = rsqrt(d);
+    __syncthreads();  // everyone has read the pivot before row j changes
+    for (int c = j + tid; c < n; c += blockDim.x) a[j * ld + c] *= dinv;
+    for (int c = tid; c <= j; c += blockDim.x) a[j * ld + aug + c] *= dinv;
     __syncthreads();
-    for (int c = j + threadIdx.x; c < w; c += blockDim.x) P[j * ld + c] *= dinv;
-    __syncthreads();
-    const int rows = pb - j - 1;
-    for (int t = threadIdx.x; t < rows * w; t += blockDim.x) {
-      const int r = j + 1 + t / w, c = t % w;
-      if (c >= r) P[r * ld + c] = fma(-P[j * ld + r], P[j * ld + c], P[r * ld + c]);
+    for (int r = j + 1 + warp; r < n; r += nwarps) {
+      const double mult = a[j * ld + r];
+      double* ar = a + r * ld;
+      const double* aj = a + j * ld;
+      for (int c = r + lane; c < n; c += 32) ar[c] = fma(-mult, aj[c], ar[c]);
+      for (int c = lane; c <= j; c += 32) ar[aug + c] = fma(-mult, aj[aug + c], ar[aug + c]);
     }
     __syncthreads();
   }
   return 0;
 }
 
-template <bool kResident>
-__global__ void __launch_bounds__(kResident ? kCholThreads : kCholThreads / 2)
-cholesky_kernel(const double* __restrict__ S, int m, double* __restrict__ U, double* __restrict__ L,
-                int check_degen, int* __restrict__ info) {
-  extern __shared__ __align__(16) double sm[];
-  __shared__ double red[64];
-  __shared__ int fail;
-  constexpr int kT = kResident ? kCholThreads : kCholThreads / 2;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = kT / 32;
-  if (tid == 0) fail = 0;
-  constexpr bool in_smem = kResident;
-  const int ldm = m + 1;  // smem pitch for the resident path
+// Resident factor + inverse for m <= kInvMax: U (upper), W = U^{-1} (upper), V = U^{-T} (lower).
+constexpr int kInvMax = 112;
 
-  // symmetry check + symmetrised copy (into smem or U)
+__global__ void __launch_bounds__(512) chol_inv_kernel(const double* __restrict__ S, int m, double* __restrict__ U,
+                                                       double* __restrict__ W, double* __restrict__ V,
+                                                       int check_degen, int* __restrict__ info) {
+  extern __shared__ __align__(16) double a[];
+  __shared__ double red[64];
+  const int ld = 2 * m + 1;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   double amax = 0.0, asym = 0.0;
-  for (int i = warp; i < m; i += nwarps)
+  for (int i = warp; i < m; i += nwarps) {
     for (int j = lane; j < m; j += 32) {
       const double sij = S[i * m + j], sji = S[j * m + i];
       amax = fmax(amax, fabs(sij));
       asym = fmax(asym, fabs(sij - sji));
-      const double v = 0.5 * (sij + sji);
-      if constexpr (in_smem) sm[i * ldm + j] = v;
-      else U[i * m + j] = v;
+      a[i * ld + j] = 0.5 * (sij + sji);
+      a[i * ld + m + j] = (i == j) ? 1.0 : 0.0;
     }
+  }
   __syncthreads();
   chol_reduce_flags(amax, asym, red, info);
-
-  if constexpr (in_smem) {
-    for (int p0 = 0; p0 < m; p0 += kCholNB) {
-      const int pb = min(kCholNB, m - p0), w = m - p0;
-      if (chol_panel(sm + p0 * ldm + p0, ldm, pb, w, p0, &fail)) break;
-      // trailing update rows/cols >= p0+pb of the upper triangle
-      const int tw = w - pb;
-      const int tot = tw * tw;
-      for (int t = tid; t < tot; t += kT) {
-        const int i = t / tw, c = t - i * tw;
-        if (c < i) continue;
-        const int gi = p0 + pb + i, gc = p0 + pb + c;
-        double acc = sm[gi * ldm + gc];
-#pragma unroll 8
-        for (int k = 0; k < pb; ++k) acc = fma(-sm[(p0 + k) * ldm + gi], sm[(p0 + k) * ldm + gc], acc);
-        sm[gi * ldm + gc] = acc;
-      }
-      __syncthreads();
-    }
-    __syncthreads();
-    if (fail) { if (tid == 0) info[TRALS_INFO_CHOL] = fail; return; }
-    for (int i = warp; i < m; i += nwarps)
-      for (int j = lane; j < m; j += 32) {
-        U[i * m + j] = j >= i ? sm[i * ldm + j] : 0.0;
-        L[i * m + j] = j <= i ? sm[j * ldm + i] : 0.0;
-      }
-  } else {
-    const int pw = ((m + 7) / 8) * 8 + 4;  // bank-conflict-free fragment pitch
-    double* panel = sm;                   // [kCholNB][pw]
-    const int fr = lane >> 2, fk = lane & 3;
-    for (int p0 = 0; p0 < m; p0 += kCholNB) {
-      const int pb = min(kCholNB, m - p0), w = m - p0;
-      const int wpad = ((w + 7) / 8) * 8;
-      for (int t = tid; t < kCholNB * wpad; t += kT) {
-        const int r = t / wpad, c = t % wpad;
-        panel[r * pw + c] = (r < pb && c < w && c >= r) ? U[static_cast<int64_t>(p0 + r) * m + p0 + c] : 0.0;
-      }
-      __syncthreads();
-      if (chol_panel(panel, pw, pb, w, p0, &fail)) break;
-      for (int t = tid; t < pb * w; t += kT) {
-        const int r = t / w, c = t % w;
-        if (c >= r) U[static_cast<int64_t>(p0 + r) * m + p0 + c] = panel[r * pw + c];
-      }
-      const int tw = w - pb;
-      if (tw > 0) {
-        const int nb8 = (tw + 7) / 8;
-        const int nblk = nb8 * (nb8 + 1) / 2;
-        for (int b0 = warp * kCholBatch; b0 < nblk; b0 += nwarps * kCholBatch) {
-          int gi[kCholBatch], gc0[kCholBatch], pi[kCholBatch], pc[kCholBatch];
-          double c[kCholBatch][2];
-#pragma unroll
-          for (int q = 0; q < kCholBatch; ++q) {
-            const int bidx = b0 + q;
-            gi[q] = -1;
-            c[q][0] = c[q][1] = 0.0;
-            if (bidx < nblk) {
-              // row-major enumeration of the upper-triangular block grid
-              const double fb = static_cast<double>(nb8) + 0.5;
-              int bi = static_cast<int>(fb - sqrt(fb * fb - 2.0 * bidx));
-              bi = max(0, min(bi, nb8 - 1));
-              while (bi > 0 && bi * nb8 - bi * (bi - 1) / 2 > bidx) --bi;
-              while ((bi + 1) * nb8 - (bi + 1) * bi / 2 <= bidx) ++bi;
-              const int bc = bi + (bidx - (bi * nb8 - bi * (bi - 1) / 2));
-              pi[q] = pb + bi * 8;
-              pc[q] = pb + bc * 8;
-              gi[q] = p0 + pi[q] + fr;
-              gc0[q] = p0 + pc[q] + 2 * fk;
-#pragma unroll
-              for (int e = 0; e < 2; ++e)
-                if (gi[q] < m && gc0[q] + e < m) c[q][e] = U[static_cast<int64_t>(gi[q]) * m + gc0[q] + e];
-            }
-          }
-#pragma unroll
-          for (int q = 0; q < kCholBatch; ++q) {
-            if (gi[q] < 0) continue;
-#pragma unroll
-            for (int k0 = 0; k0 < kCholNB; k0 += 4) {
-              const double a = -panel[(k0 + fk) * pw + pi[q] + fr];
-              const double b = panel[(k0 + fk) * pw + pc[q] + fr];
-              trals::dmma884(c[q][0], c[q][1], a, b);
-            }
-          }
-#pragma unroll
-          for (int q = 0; q < kCholBatch; ++q) {
-            if (gi[q] < 0 || gi[q] >= m) continue;
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const int gc = gc0[q] + e;
-              if (gc < m && gc >= gi[q]) U[static_cast<int64_t>(gi[q]) * m + gc] = c[q][e];
-            }
-          }
-        }
-      }
-      __syncthreads();
-    }
-    __syncthreads();
-    if (fail) { if (tid == 0) info[TRALS_INFO_CHOL] = fail; return; }
-    for (int i = warp; i < m; i += nwarps)
-      for (int j = lane; j < i; j += 32) U[i * m + j] = 0.0;
-    __syncthreads();
-    for (int i = warp; i < m; i += nwarps)
-      for (int j = lane; j < m; j += 32) L[i * m + j] = j <= i ? U[j * m + i] : 0.0;
+  const int fail = chol_aug_smem(a, ld, m, m);
+  if (fail) {
+    if (tid == 0) info[TRALS_INFO_CHOL] = fail;
+    return;
   }
-  if (check_degen) {
-    __syncthreads();
-    // diag <= 1e-13 * max|U|  (linalg.py:96-99)
-    double umax = 0.0, dmin = INFINITY;
-    int didx = 0;
-    for (int i = warp; i < m; i += nwarps)
-      for (int j = lane + i - (i & 31); j < m; j += 32) {
-        if (j < i) continue;
-        const double u = fabs(U[i * m + j]);
-        umax = fmax(umax, u);
-        if (i == j && u < dmin) { dmin = u; didx = i; }
-      }
-    for (int o = 16; o > 0; o >>= 1) {
-      umax = fmax(umax, __shfl_xor_sync(0xffffffffu, umax, o));
-      const double od = __shfl_xor_sync(0xffffffffu, dmin, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, didx, o);
-      if (od < dmin || (od == dmin && oi < didx)) { dmin = od; didx = oi; }
+  double umax = 0.0, dmin = INFINITY;
+  int didx = 0;
+  for (int i = warp; i < m; i += nwarps)
+    for (int j = lane; j < m; j += 32) {
+      const double u = j >= i ? a[i * ld + j] : 0.0;
+      U[i * m + j] = u;
+      V[i * m + j] = j <= i ? a[i * ld + m + j] : 0.0;
+      W[i * m + j] = j >= i ? a[j * ld + m + i] : 0.0;
+      umax = fmax(umax, fabs(u));
+      if (i == j && fabs(u) < dmin) { dmin = fabs(u); didx = i; }
     }
-    __shared__ double sd[32];
-    __shared__ int si[32];
-    if (lane == 0) { red[warp] = umax; sd[warp] = dmin; si[warp] = didx; }
-    __syncthreads();
-    if (tid == 0) {
-      double a = 0, d = INFINITY;
-      int di = 0;
-      for (int w = 0; w < nwarps; ++w) {
-        a = fmax(a, red[w]);
-        if (sd[w] < d || (sd[w] == d && si[w] < di)) { d = sd[w]; di = si[w]; }
-      }
-      if (d <= 1e-13 * a) info[TRALS_INFO_DEGEN] = di + 1;
-    }
+  if (!check_degen) return;
+  for (int o = 16; o > 0; o >>= 1) {
+    umax = fmax(umax, __shfl_xor_sync(0xffffffffu, umax, o));
+    const double od = __shfl_xor_sync(0xffffffffu, dmin, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, didx, o);
+    if (od < dmin || (od == dmin && oi < didx)) { dmin = od; didx = oi; }
   }
-}
-
-size_t cholesky_smem(int m) {
-  if (m <= kCholSmemMax) return sizeof(double) * static_cast<size_t>(m) * (m + 1);
-  return sizeof(double) * kCholNB * (((m + 7) / 8) * 8 + 4);
+  __shared__ double sd[32];
+  __shared__ int si[32];
+  __syncthreads();
+  if (lane == 0) { red[warp] = umax; sd[warp] = dmin; si[warp] = didx; }
+  __syncthreads();
+  if (tid == 0) {
+    double mx = 0, dm = INFINITY;
+    int di = 0;
+    for (int w = 0; w < nwarps; ++w) {
+      mx = fmax(mx, red[w]);
+      if (sd[w] < dm || (sd[w] == dm && si[w] < di)) { dm = sd[w]; di = si[w]; }
+    }
+    if (dm <= 1e-13 * mx) info[TRALS_INFO_DEGEN] = di + 1;  // linalg.py:96-99
+  }
 }
 
 // ---------------------------------------------------------------------------
-// Row-parallel triangular solves Z S = M, S = U^T U:  Y U = M, then Z U^T = Y
-// (scipy cho_solve, linalg.py:76).  Each warp owns kSolveRPW right-hand-side
-// rows (register-resident, column k on lane k % 32); U rows (forward) and
-// L = U^T rows (backward) stream through a cp.async double buffer shared by
-// the CTA's warps; the diagonal reciprocals are precomputed once.
-// ---------------------------------------------------------------------------
-constexpr int kSolveWarps = 4;
-constexpr int kSolveRPW = 2;     // rows per warp
-constexpr int kSolveChunk = 16;  // U rows per stage
-
-template <int NR>
-__global__ void __launch_bounds__(kSolveWarps * 32) chol_solve_kernel(const double* __restrict__ U,
-                                                                      const double* __restrict__ L, int m,
-                                                                      const double* __restrict__ Mr, int64_t rows,
-                                                                      double* __restrict__ Z) {
-  extern __shared__ __align__(16) double stage[];  // [2][kSolveChunk][mp] + dinv[m]
-  const int mp = (m + 1) & ~1;
-  double* dinv = stage + 2 * kSolveChunk * mp;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t row0 = (static_cast<int64_t>(blockIdx.x) * kSolveWarps + warp) * kSolveRPW;
-  for (int j = tid; j < m; j += kSolveWarps * 32) dinv[j] = 1.0 / U[static_cast<int64_t>(j) * m + j];
-  double r[kSolveRPW][NR];
-#pragma unroll
-  for (int q = 0; q < kSolveRPW; ++q)
-#pragma unroll
-    for (int s = 0; s < NR; ++s) {
-      const int k = s * 32 + lane;
-      const int64_t row = row0 + q;
-      r[q][s] = (row < rows && k < m) ? Mr[row * m + k] : 0.0;
-    }
-  const int nchunks = (m + kSolveChunk - 1) / kSolveChunk;
-  const bool vec = (m % 2 == 0);
-  for (int pass = 0; pass < 2; ++pass) {
-    const double* Src = pass == 0 ? U : L;
-    auto issue = [&](int ch, int buf) {
-      // pass 0 walks U rows 0..m-1, pass 1 walks L rows m-1..0
-      if (vec) {
-        const int cpr = m / 2;
-        for (int t = tid; t < kSolveChunk * cpr; t += kSolveWarps * 32) {
-          const int rr = t / cpr, c = (t % cpr) * 2;
-          const int j = pass == 0 ? ch * kSolveChunk + rr : m - 1 - (ch * kSolveChunk + rr);
-          if (j >= 0 && j < m)
-            trals::cp_async_zfill(stage + (buf * kSolveChunk + rr) * mp + c, Src + static_cast<int64_t>(j) * m + c,
-                                  16, 16);
-        }
-      } else {
-        for (int t = tid; t < kSolveChunk * m; t += kSolveWarps * 32) {
-          const int rr = t / m, c = t % m;
-          const int j = pass == 0 ? ch * kSolveChunk + rr : m - 1 - (ch * kSolveChunk + rr);
-          if (j >= 0 && j < m)
-            trals::cp_async_zfill(stage + (buf * kSolveChunk + rr) * mp + c, Src + static_cast<int64_t>(j) * m + c,
-                                  8, 8);
-        }
-      }
-      trals::cp_async_commit();
-    };
-    issue(0, 0);
-    for (int ch = 0; ch < nchunks; ++ch) {
-      if (ch + 1 < nchunks) {
-        issue(ch + 1, (ch + 1) & 1);
-        trals::cp_async_wait<1>();
-      } else {
-        trals::cp_async_wait<0>();
-      }
-      __syncthreads();
-      const double* buf = stage + (ch & 1) * kSolveChunk * mp;
-#pragma unroll 1
-      for (int rr = 0; rr < kSolveChunk; ++rr) {
-        const int j = pass == 0 ? ch * kSolveChunk + rr : m - 1 - (ch * kSolveChunk + rr);
-        if (j < 0 || j >= m) break;
-        const double* urow = buf + rr * mp;
-        const int js = j >> 5, jl = j & 31;
-        const double dj = dinv[j];
-        double y[kSolveRPW];
-#pragma unroll
-        for (int q = 0; q < kSolveRPW; ++q) {
-          double v = 0.0;
-#pragma unroll
-          for (int s = 0; s < NR; ++s) v = (s == js) ? r[q][s] : v;
-          y[q] = __shfl_sync(0xffffffffu, v, jl) * dj;
-        }
-#pragma unroll
-        for (int s = 0; s < NR; ++s) {
-          const int k = s * 32 + lane;
-          const bool live = pass == 0 ? (k > j && k < m) : (k < j);
-          const double u = live ? urow[k] : 0.0;
-#pragma unroll
-          for (int q = 0; q < kSolveRPW; ++q) {
-            r[q][s] = (k == j) ? y[q] : fma(-y[q], u, r[q][s]);
-          }
-        }
-      }
-      __syncthreads();
-    }
-  }
-#pragma unroll
-  for (int q = 0; q < kSolveRPW; ++q) {
-    const int64_t row = row0 + q;
-    if (row >= rows) continue;
-#pragma unroll
-    for (int s = 0; s < NR; ++s) {
-      const int k = s * 32 + lane;
-      if (k < m) Z[row * m + k] = r[q][s];
-    }
-  }
-}
-
-template <int NR>
-int launch_solve(const double* U, const double* L, int m, const double* Mr, int64_t rows, double* Z,
-                 cudaStream_t s) {
-  const int mp = (m + 1) & ~1;
-  const size_t smem = sizeof(double) * (2 * kSolveChunk * mp + m);
-  auto k = chol_solve_kernel<NR>;
-  static size_t attr = 0;
-  if (smem > 48 * 1024 && smem > attr) {
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    attr = smem;
-  }
-  const int64_t per_cta = kSolveWarps * kSolveRPW;
-  const int64_t blocks = (rows + per_cta - 1) / per_cta;
-  k<<<static_cast<unsigned>(blocks), kSolveWarps * 32, smem, s>>>(U, L, m, Mr, rows, Z);
-  return launch_status();
-}
-
-// ---------------------------------------------------------------------------
-// Blocked Cholesky + triangular solves for m > kCholSmemMax (R = 20: m = 400).
+// Blocked Cholesky + triangular solves for m > kInvMax (R = 20: m = 400).
 // Right-looking with 64-row panels: a one-CTA kernel factors the 64x64
 // diagonal block in shared memory and inverts it; the panel row block and the
 // trailing update are DMMA GEMMs over the whole GPU (the inverse turns the
@@ -643,58 +407,33 @@ __global__ void __launch_bounds__(1024) chol_sym_kernel(const double* __restrict
 __global__ void __launch_bounds__(256) chol_diag_kernel(double* __restrict__ U, int m, int p0, int pb,
                                                         double* __restrict__ W, double* __restrict__ WT,
                                                         int* __restrict__ info) {
-  extern __shared__ __align__(16) double dsm[];
-  double (*a)[kBlkNB + 1] = reinterpret_cast<double (*)[kBlkNB + 1]>(dsm);
-  double (*w)[kBlkNB + 1] = reinterpret_cast<double (*)[kBlkNB + 1]>(dsm + kBlkNB * (kBlkNB + 1));
+  extern __shared__ __align__(16) double a[];  // [pb][2*kBlkNB + 1]
+  constexpr int ld = 2 * kBlkNB + 1;
   __shared__ int failed;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   if (tid == 0) failed = info[TRALS_INFO_CHOL];
-  for (int t = tid; t < pb * pb; t += blockDim.x) {
-    const int r = t / pb, c = t - r * pb;
-    a[r][c] = c >= r ? U[(p0 + r) * m + p0 + c] : 0.0;
-  }
+  for (int r = warp; r < pb; r += nwarps)
+    for (int c = lane; c < pb; c += 32) {
+      a[r * ld + c] = c >= r ? U[(p0 + r) * m + p0 + c] : 0.0;
+      a[r * ld + kBlkNB + c] = (r == c) ? 1.0 : 0.0;
+    }
   __syncthreads();
   if (failed) return;
-  for (int j = 0; j < pb; ++j) {
-    const double d = a[j][j];
-    if (!(d > 0.0)) {
-      if (tid == 0) info[TRALS_INFO_CHOL] = p0 + j + 1;
-      return;  // uniform: every thread read the same pivot
+  const int f = chol_aug_smem(a, ld, pb, kBlkNB);
+  if (f) {
+    if (tid == 0) info[TRALS_INFO_CHOL] = p0 + f;
+    return;
+  }
+  for (int r = warp; r < pb; r += nwarps)
+    for (int c = lane; c < pb; c += 32)
+      if (c >= r) U[(p0 + r) * m + p0 + c] = a[r * ld + c];
+  // V = U_bb^{-T} (lower) sits in the augmented half: W = V^T, WT = V
+  for (int r = warp; r < kBlkNB; r += nwarps)
+    for (int c = lane; c < kBlkNB; c += 32) {
+      const bool in = r < pb && c < pb;
+      WT[r * kBlkNB + c] = (in && c <= r) ? a[r * ld + kBlkNB + c] : 0.0;
+      W[r * kBlkNB + c] = (in && c >= r) ? a[c * ld + kBlkNB + r] : 0.0;
     }
-    const double dinv = rsqrt(d);
-    __syncthreads();
-    for (int c = j + tid; c < pb; c += blockDim.x) a[j][c] *= dinv;
-    __syncthreads();
-    const int rows = pb - j - 1;
-    for (int t = tid; t < rows * rows; t += blockDim.x) {
-      const int r = j + 1 + t / rows, c = j + 1 + t % rows;
-      if (c >= r) a[r][c] = fma(-a[j][r], a[j][c], a[r][c]);
-    }
-    __syncthreads();
-  }
-  for (int t = tid; t < pb * pb; t += blockDim.x) {
-    const int r = t / pb, c = t - r * pb;
-    if (c >= r) U[(p0 + r) * m + p0 + c] = a[r][c];
-  }
-  // W = a^{-1} (upper): row k from the bottom, W[k][j] = (d_kj - sum_{t=k+1..j} a[k][t] W[t][j]) / a[k][k]
-  for (int k = pb - 1; k >= 0; --k) {
-    for (int j = tid; j < pb; j += blockDim.x) {
-      double v = 0.0;
-      if (j >= k) {
-        v = (j == k) ? 1.0 : 0.0;
-        for (int t = k + 1; t <= j; ++t) v = fma(-a[k][t], w[t][j], v);
-        v /= a[k][k];
-      }
-      w[k][j] = v;
-    }
-    __syncthreads();
-  }
-  for (int t = tid; t < kBlkNB * kBlkNB; t += blockDim.x) {
-    const int r = t / kBlkNB, c = t - r * kBlkNB;
-    const bool in = r < pb && c < pb;
-    W[t] = in ? w[r][c] : 0.0;
-    WT[t] = in ? w[c][r] : 0.0;
-  }
 }
 
 // zero the strict lower triangle of U and write L = U^T
@@ -756,8 +495,8 @@ int64_t blocked_aux_elems(int m) {
   return static_cast<int64_t>(nblk) * 2 * kBlkNB * kBlkNB;
 }
 
-int blocked_cholesky(const double* S, int m, double* U, double* L, double* aux, int check_degen, int* info,
-                     cudaStream_t s) {
+int blocked_cholesky(const double* S, int m, double* U, double* L, double* aux, double* gws, int64_t gws_elems,
+                     int check_degen, int* info, cudaStream_t s) {
   chol_sym_kernel<<<1, 1024, 0, s>>>(S, m, U, info);
   if (int st = launch_status()) return st;
   const CMap rm = rowmajor(m);
@@ -766,7 +505,7 @@ int blocked_cholesky(const double* S, int m, double* U, double* L, double* aux, 
     const int rest = m - p0 - pb;
     double* W = aux + static_cast<int64_t>(b) * 2 * kBlkNB * kBlkNB;
     double* WT = W + kBlkNB * kBlkNB;
-    constexpr size_t kDiagSmem = sizeof(double) * 2 * kBlkNB * (kBlkNB + 1);
+    constexpr size_t kDiagSmem = sizeof(double) * kBlkNB * (2 * kBlkNB + 1);
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(chol_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kDiagSmem);
@@ -777,11 +516,11 @@ int blocked_cholesky(const double* S, int m, double* U, double* L, double* aux, 
     if (rest == 0) continue;
     double* U12 = U + static_cast<int64_t>(p0) * m + p0 + pb;
     // U12 <- W^T A12 (in place: one M tile, each CTA rewrites exactly the columns it read)
-    int st = gemm(WT, 0, kBlkNB, 1, 1, pb, pb, rest, U12, m, U12, rm, 0, nullptr, 0, s);
+    int st = gemm(WT, 0, kBlkNB, 1, 1, pb, pb, rest, U12, m, U12, rm, 0, nullptr, 0, s);  // no split: in place
     if (st) return st;
     // A22 -= U12^T U12
     double* A22 = U + static_cast<int64_t>(p0 + pb) * m + p0 + pb;
-    st = gemm(U12, 0, 1, m, 1, rest, pb, rest, U12, m, A22, rm, 1, nullptr, 0, s, -1.0);
+    st = gemm(U12, 0, 1, m, 1, rest, pb, rest, U12, m, A22, rm, 1, gws, gws_elems, s, -1.0);
     if (st) return st;
   }
   dim3 grid((m + 31) / 32, (m + 31) / 32);
@@ -794,11 +533,10 @@ int blocked_cholesky(const double* S, int m, double* U, double* L, double* aux, 
   return TRALS_OK;
 }
 
-int64_t blocked_solve_ws(int64_t rows, int m) { return rows * m; }
 
 // Z S = M, S = U^T U:  Y U = M (forward), Z U^T = Y (backward), 64-column blocks
 int blocked_solve(const double* U, const double* L, const double* aux, int m, const double* Mr, int64_t rows,
-                  double* Z, double* ws, cudaStream_t s) {
+                  double* Z, double* ws, double* gws, int64_t gws_elems, cudaStream_t s) {
   const CMap rm = rowmajor(m);
   double* R = ws;   // running right-hand side
   double* Y = Z;    // forward result lives in Z's storage, then overwritten block by block
@@ -810,10 +548,10 @@ int blocked_solve(const double* U, const double* L, const double* aux, int m, co
     const int j0 = b * kBlkNB, pb = std::min(kBlkNB, m - j0);
     const double* W = aux + static_cast<int64_t>(b) * 2 * kBlkNB * kBlkNB;
     if (j0 > 0) {
-      int st = gemm(Y, 0, m, 1, 1, rows, j0, pb, U + j0, m, R + j0, rm, 1, nullptr, 0, s, -1.0);
+      int st = gemm(Y, 0, m, 1, 1, rows, j0, pb, U + j0, m, R + j0, rm, 1, gws, gws_elems, s, -1.0);
       if (st) return st;
     }
-    int st = gemm(R + j0, 0, m, 1, 1, rows, pb, pb, W, kBlkNB, Y + j0, rm, 0, nullptr, 0, s);
+    int st = gemm(R + j0, 0, m, 1, 1, rows, pb, pb, W, kBlkNB, Y + j0, rm, 0, gws, gws_elems, s);
     if (st) return st;
   }
   // backward: R = Y; Z_b = (R_b - Z_{>b} L_{>b,b}) W_b^T, last block first (Z overwrites Y in place:
@@ -826,10 +564,10 @@ int blocked_solve(const double* U, const double* L, const double* aux, int m, co
     const double* WT = aux + static_cast<int64_t>(b) * 2 * kBlkNB * kBlkNB + kBlkNB * kBlkNB;
     if (j1 < m) {
       int st = gemm(Z + j1, 0, m, 1, 1, rows, m - j1, pb, L + static_cast<int64_t>(j1) * m + j0, m, R + j0, rm, 1,
-                    nullptr, 0, s, -1.0);
+                    gws, gws_elems, s, -1.0);
       if (st) return st;
     }
-    int st = gemm(R + j0, 0, m, 1, 1, rows, pb, pb, WT, kBlkNB, Z + j0, rm, 0, nullptr, 0, s);
+    int st = gemm(R + j0, 0, m, 1, 1, rows, pb, pb, WT, kBlkNB, Z + j0, rm, 0, gws, gws_elems, s);
     if (st) return st;
   }
   return TRALS_OK;
@@ -1207,45 +945,48 @@ int trals_gram_chain_f64(int N, int n, const int32_t* ranks, const double* const
   return TRALS_OK;
 }
 
-int64_t trals_cholesky_aux_elems(int m) { return m > kCholSmemMax ? blocked_aux_elems(m) : 0; }
+int64_t trals_cholesky_aux_elems(int m) {
+  if (m <= kInvMax) return static_cast<int64_t>(m) * m;                        // V = U^{-T}
+  return blocked_aux_elems(m) + 4 * static_cast<int64_t>(m) * m;             // block inverses + split-K
+}
 
-int trals_cholesky_f64(const double* S, int m, double* U, double* L, double* aux, int check_degen, int* info,
+int trals_cholesky_f64(const double* S, int m, double* U, double* F, double* aux, int check_degen, int* info,
                        void* stream) {
-  if (!S || !U || !L || !info || m < 1) return TRALS_ERR_ARG;
+  if (!S || !U || !F || !aux || !info || m < 1) return TRALS_ERR_ARG;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (m > kCholSmemMax) {
-    if (!aux) return TRALS_ERR_WORKSPACE;
-    return blocked_cholesky(S, m, U, L, aux, check_degen, info, s);
+  if (m > kInvMax) {
+    double* gws = aux + blocked_aux_elems(m);
+    return blocked_cholesky(S, m, U, F, aux, gws, 4 * static_cast<int64_t>(m) * m, check_degen, info, s);
   }
-  const size_t smem = cholesky_smem(m);
+  const size_t smem = sizeof(double) * static_cast<size_t>(m) * (2 * m + 1);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(cholesky_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     attr = true;
   }
-  cholesky_kernel<true><<<1, kCholThreads, smem, s>>>(S, m, U, L, check_degen, info);
+  chol_inv_kernel<<<1, 512, smem, s>>>(S, m, U, F, aux, check_degen, info);
   return launch_status();
 }
 
-int64_t trals_chol_solve_ws_elems(int64_t rows, int m) { return m > kCholSmemMax ? blocked_solve_ws(rows, m) : 0; }
+int64_t trals_chol_solve_ws_elems(int64_t rows, int m) {
+  const int64_t base = rows * m;
+  return base + std::max(gemm_ws(1, rows, m, m), m > kInvMax ? 8 * base : int64_t(0));
+}
 
-int trals_chol_solve_f64(const double* U, const double* L, const double* aux, int m, const double* Mr, int64_t rows,
+int trals_chol_solve_f64(const double* U, const double* F, const double* aux, int m, const double* Mr, int64_t rows,
                          double* Z, double* ws, int64_t ws_elems, void* stream) {
-  if (!U || !L || !Mr || !Z || m < 1) return TRALS_ERR_ARG;
+  if (!U || !F || !aux || !Mr || !Z || !ws || m < 1) return TRALS_ERR_ARG;
   if (rows <= 0) return TRALS_OK;
+  if (ws_elems < trals_chol_solve_ws_elems(rows, m)) return TRALS_ERR_WORKSPACE;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (m > kCholSmemMax) {
-    if (!aux || !ws || ws_elems < blocked_solve_ws(rows, m)) return TRALS_ERR_WORKSPACE;
-    return blocked_solve(U, L, aux, m, Mr, rows, Z, ws, s);
-  }
-  switch ((m + 31) / 32) {
-    case 1: return launch_solve<1>(U, L, m, Mr, rows, Z, s);
-    case 2: return launch_solve<2>(U, L, m, Mr, rows, Z, s);
-    case 3: return launch_solve<3>(U, L, m, Mr, rows, Z, s);
-    case 4: return launch_solve<4>(U, L, m, Mr, rows, Z, s);
-    case 5: return launch_solve<5>(U, L, m, Mr, rows, Z, s);
-  }
-  return TRALS_ERR_UNSUPPORTED;
+  double* gws = ws + rows * m;
+  const int64_t gws_elems = ws_elems - rows * m;
+  if (m > kInvMax) return blocked_solve(U, F, aux, m, Mr, rows, Z, ws, gws, gws_elems, s);
+  // Z = M U^{-1} U^{-T} = (M W) V
+  const CMap rm = rowmajor(m);
+  int st = gemm(Mr, 0, m, 1, 1, rows, m, m, F, m, ws, rm, 0, gws, gws_elems, s);
+  if (st) return st;
+  return gemm(ws, 0, m, 1, 1, rows, m, m, aux, m, Z, rm, 0, gws, gws_elems, s);
 }
 
 int64_t trals_sumsq_ws_elems(void) { return 2 * kSumsqBlocks; }

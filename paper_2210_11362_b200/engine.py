@@ -54,6 +54,8 @@ class Step:
     bucket: str
     fn: object
     name: str = ""
+    stream: str = "main"   # "main" | "side"
+    kind: str = "op"       # "op" | "fork" (side waits for main) | "join" (main waits for side)
 
 
 @dataclass
@@ -133,7 +135,12 @@ class SweepEngine:
             s = self.s
             self.Gc_loc = self._empty(self.R(s), self.dl[s], self.R(s + 1))
         self.gws_need = 1
+        self.side_gws_need = 1
         self.gws = None  # sized after compile
+        self.side = torch.cuda.Stream(device=self.dev) if self.dev.type == "cuda" else _HostStream()
+        self._fork_ev = torch.cuda.Event() if self.dev.type == "cuda" else None
+        self._join_ev = torch.cuda.Event() if self.dev.type == "cuda" else None
+        self._cur = None
         self.graph = None
 
     # local views used by the X contractions
@@ -160,6 +167,9 @@ class SweepEngine:
     def _ws(self, elems):
         self.gws_need = max(self.gws_need, int(elems))
 
+    def _side_ws(self, elems):
+        self.side_gws_need = max(self.side_gws_need, int(elems))
+
     # ----------------------------------------------------------------- compile
     def _compile(self):
         N = self.N
@@ -167,6 +177,7 @@ class SweepEngine:
         self._bufs = []  # keep env buffers alive
         self._env_flops = []
         self.stats.x_passes_per_sweep = 0
+        self._factor(0)
         if N == 2:
             phases = [(0, 0), (1, 1)]
         else:
@@ -179,6 +190,7 @@ class SweepEngine:
         m = self.R(N - 1) * self.R(N)
         self.err_ws = self._empty(self.lib.trals_error_ws_elems(rows, m))
         self.gws = self._empty(self.gws_need)
+        self.side_gws = self._empty(self.side_gws_need)
         self.stats.steps_per_sweep = len(self.steps)
 
     def _choose_block(self, a, b):
@@ -328,29 +340,42 @@ class SweepEngine:
             cur, sa, sb = self._absorb_left(cur, sa, sb, leaf)
         self._tree(cur, m + 1, b)
 
-    def _solve(self, n):
-        """Steps for one block update once M_n is complete (local rows)."""
+    def _factor(self, n):
+        """S_n from the Gram chain and its Cholesky factor -- depends on cores only, so it runs on
+        the side stream as soon as core n-1 is final, overlapping the right-hand side of mode n."""
         N = self.N
         rr = self.R(n) * self.R(n + 1)
-        S, M = self.S[n], self.M[n]
-        if self.world > 1:
-            import torch.distributed as dist
-            self.steps.append(Step("mttsp", lambda M=M: dist.all_reduce(M, group=self.group), f"allreduce M{n}"))
+        S = self.S[n]
         ranks_a = L.i32_array(self.ranks)
         rmax = max(self.ranks)
-        self._ws(self.lib.trals_gemm_ws_elems(1, rmax ** 2, rmax ** 2, rmax ** 2))
+        self._side_ws(self.lib.trals_gemm_ws_elems(1, rmax ** 2, rmax ** 2, rmax ** 2))
+        self.steps.append(Step("other", None, f"fork S{n}", kind="fork"))
 
         def gram_chain(n=n, S=S, ranks_a=ranks_a):
             E = L.ptr_array([e.data_ptr() for e in self.E])
             L.check(self.lib.trals_gram_chain_f64(N, n, ranks_a, E, S.data_ptr(), self.chain_tmp.data_ptr(),
-                                                  self.gws.data_ptr(), self.gws.numel(), self._sp()), "gram_chain")
-        self.steps.append(Step("other", gram_chain, f"S{n}"))
+                                                  self.side_gws.data_ptr(), self.side_gws.numel(), self._sp()),
+                    "gram_chain")
+        self.steps.append(Step("other", gram_chain, f"S{n}", stream="side"))
         check_degen = 1 if self.variant == "qr" else 0
 
-        def solve(n=n, S=S, M=M, rr=rr, check_degen=check_degen):
+        def factor(S=S, rr=rr, check_degen=check_degen):
             L.check(self.lib.trals_cholesky_f64(S.data_ptr(), rr, self.U.data_ptr(), self.Lo.data_ptr(),
                                                 self.chol_aux.data_ptr(), check_degen, self.info.data_ptr(),
                                                 self._sp()), "cholesky")
+        self.steps.append(Step("solve", factor, f"chol{n}", stream="side"))
+
+    def _solve(self, n):
+        """Steps for one block update once M_n is complete (local rows)."""
+        N = self.N
+        rr = self.R(n) * self.R(n + 1)
+        M = self.M[n]
+        if self.world > 1:
+            import torch.distributed as dist
+            self.steps.append(Step("mttsp", lambda M=M: dist.all_reduce(M, group=self.group), f"allreduce M{n}"))
+        self.steps.append(Step("solve", None, f"join chol{n}", kind="join"))
+
+        def solve(n=n, M=M, rr=rr):
             L.check(self.lib.trals_chol_solve_f64(self.U.data_ptr(), self.Lo.data_ptr(), self.chol_aux.data_ptr(), rr,
                                                   M.data_ptr(), self.dims[n], self.Gt[n].data_ptr(),
                                                   self.solve_ws.data_ptr(), self.solve_ws.numel(), self._sp()),
@@ -372,10 +397,12 @@ class SweepEngine:
                                                  self.gws.data_ptr(), self.gws.numel(), sp), "core_gram")
         self._ws(self.lib.trals_gemm_ws_elems(1, rr, self.dims[n], rr))
         self.steps.append(Step("gramqr", refresh, f"refresh{n}"))
+        if n + 1 < N:
+            self._factor(n + 1)
 
     # ----------------------------------------------------------------- running
     def _sp(self):
-        return int(self.stream.cuda_stream)
+        return int((self._cur or self.stream).cuda_stream)
 
     def set_cores(self, cores_host):
         """Upload C-order host cores and derive every layout + Gram (the 'prepare' of solvers.py:366-367)."""
@@ -423,8 +450,20 @@ class SweepEngine:
         environment product (the dominant kernel, for the roofline).
         """
         prev = None
+        cuda = self.dev.type == "cuda"
         for st in self.steps:
-            if events is not None and st.bucket != prev:
+            if st.kind == "fork":
+                if cuda:
+                    self._fork_ev.record(self.stream)
+                    self.side.wait_event(self._fork_ev)
+                continue
+            if st.kind == "join":
+                if cuda:
+                    self._join_ev.record(self.side)
+                    self.stream.wait_event(self._join_ev)
+                continue
+            self._cur = self.side if st.stream == "side" else None
+            if events is not None and st.stream == "main" and st.bucket != prev:
                 ev = torch.cuda.Event(enable_timing=True)
                 ev.record(self.stream)
                 events.append((st.bucket, ev))
@@ -438,6 +477,7 @@ class SweepEngine:
                 env_events.append((e0, e1))
             else:
                 st.fn()
+        self._cur = None
 
     def error_step(self, out):
         """Cheap-error terms after a sweep into `out` (3 doubles): [e, <M,Z>, <S,Z^T Z>]."""

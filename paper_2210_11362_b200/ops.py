@@ -111,7 +111,7 @@ def coefficient_gram(cores_c, n: int) -> torch.Tensor:
 
 
 class CholFactor:
-    """Device Cholesky factor: U (upper), L = U^T, diagonal-block inverses (aux), info flags."""
+    """Device Cholesky factor: U (upper), companion F (U^{-1} for m <= 112, else U^T), aux, info flags."""
 
     def __init__(self, U, Lo, aux, info):
         self.U, self.L, self.aux, self.info = U, Lo, aux, info
