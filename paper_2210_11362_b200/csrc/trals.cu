@@ -57,20 +57,35 @@ struct SplitPlan {
   int64_t kchunk;
 };
 
+// Split-K choice: model the time of s splits as
+//   waves(s)/s * t_tile  +  [s > 1] * (3 us + (s+1) * M*N*8 B / 6 TB/s)
+// with waves(s) = ceil(tiles*s / slots) and t_tile the DMMA time of one full-K
+// tile on one CTA slot (37 TFLOP/s over 296 slots).  Small outputs get enough
+// splits to fill the GPU; large ones avoid a ragged last wave (c5: 1000
+// tiles -> 3.38 waves unsplit, 3.4/5 per unit with s = 5).  Every
+// configuration runs 2 CTAs/SM; splits keep >= 4 K-tiles; partials are
+// reduced in a fixed order (deterministic).
 SplitPlan plan_split(const Cfg& c, int64_t P, int64_t M, int64_t K, int64_t N) {
   const int64_t tiles = P * ((M + c.BM - 1) / c.BM) * ((N + c.BN - 1) / c.BN);
-  const int64_t target = 2 * kSMs;
-  int64_t splits = 1;
-  if (tiles < target) {
-    splits = (target + tiles - 1) / tiles;
-    const int64_t max_by_k = std::max<int64_t>(1, K / (8 * trals::kBK));  // >= 128 of K per split
-    splits = std::min(splits, max_by_k);
-    splits = std::min<int64_t>(splits, 64);
+  const int64_t slots = 2 * kSMs;
+  const int64_t smax = std::max<int64_t>(1, std::min<int64_t>(64, K / (4 * trals::kBK)));
+  const double t_tile = 2.0 * c.BM * c.BN * static_cast<double>(K) / (37.0e12 / slots);
+  const double out_bytes = 8.0 * static_cast<double>(P) * M * N;
+  int64_t best_s = 1;
+  double best = 1e300;
+  for (int64_t sp = 1; sp <= smax; ++sp) {
+    const int64_t waves = (tiles * sp + slots - 1) / slots;
+    double cost = static_cast<double>(waves) / sp * t_tile;
+    if (sp > 1) cost += 3e-6 + (sp + 1) * out_bytes / 6.0e12;
+    if (cost < best * (1 - 1e-9)) {
+      best = cost;
+      best_s = sp;
+    }
   }
-  int64_t kchunk = (K + splits - 1) / splits;
+  int64_t kchunk = (K + best_s - 1) / best_s;
   kchunk = ((kchunk + trals::kBK - 1) / trals::kBK) * trals::kBK;
   if (kchunk <= 0) kchunk = trals::kBK;
-  splits = std::max<int64_t>(1, (K + kchunk - 1) / kchunk);
+  const int64_t splits = std::max<int64_t>(1, (K + kchunk - 1) / kchunk);
   return {static_cast<int>(splits), kchunk};
 }
 

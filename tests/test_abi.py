@@ -28,7 +28,9 @@ def test_library_exports_every_symbol():
 
 def test_workspace_queries_without_gpu():
     h = _lib.load()
-    assert h.trals_gemm_ws_elems(1, 25600, 25600, 400) == 0  # big GEMMs need no split-K
+    # ragged-wave fix: the c5 environment GEMM (1000 tiles on 296 slots) is split 5-way in K
+    assert h.trals_gemm_ws_elems(1, 25600, 25600, 400) == 5 * 25600 * 400
+    assert h.trals_gemm_ws_elems(1, 250000, 500, 100) == 0
     assert h.trals_gemm_ws_elems(1, 1600, 64000, 64) > 0      # long-K shapes split K deterministically
     dims = _lib.i64_array([160] * 4)
     ranks = _lib.i32_array([20] * 4)
