@@ -20,6 +20,7 @@
  *   SLICE : [i][r_n][r_{n+1}]   lateral slices G_n(i) contiguous
  *   ZT    : [i][r_{n+1}][r_n]   = classical 2-unfolding Z[i, r_n + R_n r_{n+1}]
  *                               (tensor_ops.py:100-108), the solve's output
+ *   TT    : [r_{n+1}][r_n][i]   (transposed slices; operand of the fused reconstruct)
  *
  * Each entry point cites the reference code it replaces.
  */
@@ -39,7 +40,7 @@ enum {
   TRALS_ERR_UNSUPPORTED = 4  /* size outside the kernels' envelope */
 };
 
-enum { TRALS_LAYOUT_C = 0, TRALS_LAYOUT_SLICE = 1, TRALS_LAYOUT_ZT = 2 };
+enum { TRALS_LAYOUT_C = 0, TRALS_LAYOUT_SLICE = 1, TRALS_LAYOUT_ZT = 2, TRALS_LAYOUT_TT = 3 };
 
 /* d_info slots written by the solve kernels (int32 each, 0 = no event) */
 enum {
@@ -74,11 +75,14 @@ int trals_core_relayout_f64(const double* d_src, int src_layout, int Ra, int64_t
 /* Half chain H[i_u..i_v][r_u][r_{v+1}] = G_u(i_u) ... G_v(i_v) of a contiguous
  * block of cores (ring.py:110-152 subchain_merge/skip restricted to a block).
  * d_cores_c[j] = core u+j in layout C, d_first_slice = core u in layout SLICE.
- * d_tmp must hold the largest intermediate chain (trals_half_chain_tmp_elems). */
+ * d_tmp must hold the largest intermediate chain (trals_half_chain_tmp_elems).
+ * transposed != 0 writes [r_{v+1}][r_u][i_u..i_v] instead (the K x post operand
+ * of trals_residual_f64). */
 int64_t trals_half_chain_tmp_elems(int nblk, const int64_t* dims, const int32_t* ranks);
 int trals_half_chain_f64(int nblk, const int64_t* dims, const int32_t* ranks,
                          const double* d_first_slice, const double* const* h_cores_c,
-                         double* d_out, double* d_tmp, double* d_ws, int64_t ws_elems, void* stream);
+                         double* d_out, double* d_tmp, double* d_ws, int64_t ws_elems, int transposed,
+                         void* stream);
 
 /* Environment of the prefix/suffix segment complementary to a half chain
  * (the X_[n] * G^{!=n}_[2] product of solvers.py:379 restricted to the
@@ -164,6 +168,18 @@ int trals_mttsp_f64(const double* d_X, int N, const int64_t* dims, const int32_t
                     const double* const* h_cores_c, const double* const* h_cores_s,
                     const double* const* h_cores_zt, double* d_M, double* d_ws, int64_t ws_elems,
                     void* stream);
+
+/* Exact relative error (solvers.py:164-174, exact_relative_error):
+ * ||X - TR(G)||_F / ||X||_F with the dense reconstruction (ring.py:155-170)
+ * fused into a DMMA GEMM X_hat = HL * HRt whose epilogue accumulates
+ * (X - X_hat)^2 tile by tile -- X_hat is never stored.  X viewed as [pre][post];
+ * HL = half chain of the prefix cores [pre][r_0][r_h]; HRt = half chain of the
+ * suffix cores written transposed, [r_0][r_h][post]; K = R_0 R_h.
+ * d_out[1] = sum of squared residuals, d_out[0] = sqrt(d_out[1] / d_xnorm2[0]). */
+int64_t trals_residual_ws_elems(int64_t pre, int64_t post);
+int trals_residual_f64(const double* d_X, int64_t pre, int64_t post, const double* d_HL, const double* d_HRt,
+                       int64_t K, const double* d_xnorm2, double* d_out, double* d_ws, int64_t ws_elems,
+                       void* stream);
 
 #ifdef __cplusplus
 }

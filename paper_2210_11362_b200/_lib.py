@@ -14,7 +14,7 @@ from ctypes import POINTER, c_double, c_int, c_int32, c_int64, c_void_p
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libtrals.so")
 
-LAYOUT_C, LAYOUT_SLICE, LAYOUT_ZT = 0, 1, 2
+LAYOUT_C, LAYOUT_SLICE, LAYOUT_ZT, LAYOUT_TT = 0, 1, 2, 3
 INFO_CHOL, INFO_ASYM, INFO_DEGEN, INFO_SLOTS = 0, 1, 2, 4
 
 _dp = c_void_p  # device pointers travel as void*
@@ -31,7 +31,7 @@ _SIGNATURES = {
     "trals_core_relayout_f64": (c_int, [_dp, c_int, c_int, c_int64, c_int, _dp, c_int, c_void_p]),
     "trals_half_chain_tmp_elems": (c_int64, [c_int, POINTER(c_int64), POINTER(c_int32)]),
     "trals_half_chain_f64": (c_int, [c_int, POINTER(c_int64), POINTER(c_int32), _dp, POINTER(c_void_p),
-                                     _dp, _dp, _dp, c_int64, c_void_p]),
+                                     _dp, _dp, _dp, c_int64, c_int, c_void_p]),
     "trals_env_f64": (c_int, [_dp, c_int64, c_int64, c_int, _dp, c_int, c_int, _dp, c_int, _dp, c_int64,
                               c_void_p]),
     "trals_absorb_right_f64": (c_int, [_dp, c_int, c_int64, c_int64, c_int, c_int, _dp, _dp, c_int, _dp,
@@ -49,6 +49,8 @@ _SIGNATURES = {
     "trals_sumsq_f64": (c_int, [_dp, c_int64, _dp, _dp, c_void_p]),
     "trals_error_ws_elems": (c_int64, [c_int64, c_int]),
     "trals_error_terms_f64": (c_int, [_dp, _dp, _dp, c_int64, c_int, _dp, _dp, _dp, c_int64, c_void_p]),
+    "trals_residual_ws_elems": (c_int64, [c_int64, c_int64]),
+    "trals_residual_f64": (c_int, [_dp, c_int64, c_int64, _dp, _dp, c_int64, _dp, _dp, _dp, c_int64, c_void_p]),
     "trals_mttsp_ws_elems": (c_int64, [c_int, POINTER(c_int64), POINTER(c_int32), c_int]),
     "trals_mttsp_f64": (c_int, [_dp, c_int, POINTER(c_int64), POINTER(c_int32), c_int, POINTER(c_void_p),
                                 POINTER(c_void_p), POINTER(c_void_p), _dp, _dp, c_int64, c_void_p]),

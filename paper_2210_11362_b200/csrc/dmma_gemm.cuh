@@ -47,6 +47,8 @@ struct GemmArgs {
   int64_t kchunk;     // K range per split (multiple of kBK)
   int splits;         // > 1: write raw partials to ws[split][p][m][n]
   double* ws;
+  const double* X;    // residual mode: X[m * ldx + n]
+  int64_t ldx;
 };
 
 __device__ __forceinline__ void cp_async_zfill(void* smem, const void* gmem, int bytes_valid, int bytes) {
@@ -91,7 +93,10 @@ struct Tile {
   static constexpr size_t kSmemBytes = sizeof(double) * STAGE * kStages;
 };
 
-template <int WM, int WN, int TM, int TN, bool AK, int VEC>
+// RES: instead of storing C, accumulate sum((X - C)^2) over the tile and write
+// one partial per CTA to ws[blockIdx.y * gridDim.x + blockIdx.x] (the fused
+// residual of the exact error, solvers.py:164-174; no split-K).
+template <int WM, int WN, int TM, int TN, bool AK, int VEC, bool RES = false>
 __global__ void __launch_bounds__(WM * WN * 32, 2)
 dmma_gemm_kernel(const GemmArgs g) {
   using T = Tile<WM, WN, TM, TN, AK, VEC>;
@@ -194,6 +199,42 @@ dmma_gemm_kernel(const GemmArgs g) {
   }
   cp_async_wait<0>();
 
+  if constexpr (RES) {
+    double local = 0.0;
+#pragma unroll
+    for (int i = 0; i < TM; ++i) {
+      const int64_t m = m0 + wm0 + i * 8 + fr;
+      if (m >= g.M) continue;
+#pragma unroll
+      for (int j = 0; j < TN; ++j) {
+        const int64_t n = n0 + wn0 + j * 8 + 2 * fk;
+        if (VEC == 2 && n + 1 < g.N) {
+          const double2 xv = *reinterpret_cast<const double2*>(g.X + m * g.ldx + n);
+          const double d0 = xv.x - acc[i][j][0], d1 = xv.y - acc[i][j][1];
+          local = fma(d0, d0, local);
+          local = fma(d1, d1, local);
+        } else {
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            if (n + e >= g.N) continue;
+            const double d = g.X[m * g.ldx + n + e] - acc[i][j][e];
+            local = fma(d, d, local);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
+    __syncthreads();  // smem ring is free now: reuse it for the warp partials
+    if (lane == 0) smem[warp] = local;
+    __syncthreads();
+    if (tid == 0) {
+      double t = 0.0;
+      for (int w = 0; w < WM * WN; ++w) t += smem[w];
+      g.ws[static_cast<int64_t>(blockIdx.y) * gridDim.x + blockIdx.x] = t;
+    }
+    return;
+  }
   // epilogue: C fragment (row fr, cols 2*fk, 2*fk+1) of every m8n8 block.
   // Address parts are computed once per row / column (32-bit div/mod).
   int64_t row_off[TM];

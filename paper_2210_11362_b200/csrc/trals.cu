@@ -120,6 +120,35 @@ int launch_cfg(int id, const GemmArgs& g, cudaStream_t s) {
   return TRALS_ERR_ARG;
 }
 
+// fused residual sum((X - A B)^2): A = HL [M x K] row-major, B = HRt [K x N] row-major
+int64_t residual_blocks(int64_t M, int64_t N) { return ((M + 127) / 128) * ((N + 63) / 64); }
+
+int residual(const double* A, int64_t M, int64_t K, const double* B, int64_t N, const double* X, double* part,
+             cudaStream_t s) {
+  GemmArgs g{};
+  g.A = A; g.sAp = 0; g.sAm = K; g.sAk = 1;
+  g.B = B; g.ldb = N; g.C = nullptr;
+  g.P = 1; g.M = M; g.K = K; g.N = N; g.beta = 0; g.alpha = 1.0;
+  g.kchunk = ((K + trals::kBK - 1) / trals::kBK) * trals::kBK; g.splits = 1; g.ws = part;
+  g.X = X; g.ldx = N;
+  const bool vec2 = (reinterpret_cast<uintptr_t>(A) % 16 == 0) && (reinterpret_cast<uintptr_t>(B) % 16 == 0) &&
+                    (reinterpret_cast<uintptr_t>(X) % 16 == 0) && K % 2 == 0 && N % 2 == 0;
+  using T = trals::Tile<4, 2, 4, 4, true, 2>;
+  dim3 grid(static_cast<unsigned>((N + T::BN - 1) / T::BN), static_cast<unsigned>((M + T::BM - 1) / T::BM), 1);
+  if (grid.y > 65535u || grid.x > 65535u) return TRALS_ERR_UNSUPPORTED;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(trals::dmma_gemm_kernel<4, 2, 4, 4, true, 2, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(T::kSmemBytes));
+    cudaFuncSetAttribute(trals::dmma_gemm_kernel<4, 2, 4, 4, true, 1, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(T::kSmemBytes));
+    attr = true;
+  }
+  if (vec2) trals::dmma_gemm_kernel<4, 2, 4, 4, true, 2, true><<<grid, T::kThreads, T::kSmemBytes, s>>>(g);
+  else trals::dmma_gemm_kernel<4, 2, 4, 4, true, 1, true><<<grid, T::kThreads, T::kSmemBytes, s>>>(g);
+  return launch_status();
+}
+
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 int gemm(const double* A, int64_t sAp, int64_t sAm, int64_t sAk, int64_t P, int64_t M, int64_t K, int64_t N,
@@ -192,6 +221,7 @@ __device__ __forceinline__ int64_t core_index(int layout, int64_t a, int64_t i, 
                                               int Rb) {
   if (layout == TRALS_LAYOUT_C) return (a * I + i) * Rb + b;
   if (layout == TRALS_LAYOUT_SLICE) return (i * Ra + a) * Rb + b;
+  if (layout == TRALS_LAYOUT_TT) return (b * Ra + a) * I + i;
   return (i * Rb + b) * Ra + a;  // ZT
 }
 
@@ -206,6 +236,7 @@ __global__ void relayout_kernel(const double* __restrict__ src, int sl, int Ra, 
     int64_t a, i, b;
     if (dl == TRALS_LAYOUT_C) { b = u % rb; i = (u / rb) % I32; a = u / (rb * I32); }
     else if (dl == TRALS_LAYOUT_SLICE) { b = u % rb; a = (u / rb) % ra; i = u / (rb * ra); }
+    else if (dl == TRALS_LAYOUT_TT) { i = u % I32; a = (u / I32) % ra; b = u / (I32 * ra); }
     else { a = u % ra; b = (u / ra) % rb; i = u / (ra * rb); }
     dst[t] = src[core_index(sl, a, i, b, Ra, I, Rb)];
   }
@@ -597,6 +628,22 @@ __global__ void reshuffle_kernel(const double* __restrict__ F, int64_t rows, int
     C[trals::cmap_addr(cm, 0, t / cols, t % cols)] = F[t];
 }
 
+// out[1] = sum of the per-CTA squared-residual partials (fixed order),
+// out[0] = sqrt(out[1]) / |X| (solvers.py:164-174; zero input -> 0)
+__global__ void __launch_bounds__(1024) residual_final_kernel(const double* __restrict__ part, int np,
+                                                              const double* __restrict__ xnorm2,
+                                                              double* __restrict__ out) {
+  __shared__ double red[32];
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < np; i += blockDim.x) acc += part[i];
+  const double s = block_sum<1024>(acc, red);
+  if (threadIdx.x == 0) {
+    const double xn = sqrt(xnorm2 ? xnorm2[0] : 0.0);
+    out[1] = s;
+    out[0] = xn == 0.0 ? 0.0 : sqrt(s) / xn;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // error terms: out[1] = <M,Z>, out[2] = <S, G> with G = Z^T Z (precomputed)
 // ---------------------------------------------------------------------------
@@ -630,12 +677,18 @@ __global__ void __launch_bounds__(1024) error_terms_kernel(const double* __restr
 // ---------------------------------------------------------------------------
 int half_chain(int nblk, const int64_t* dims, const int32_t* ranks, const double* first_slice,
                const double* const* cores_c, double* out, double* tmp, double* ws, int64_t ws_elems,
-               cudaStream_t s) {
+               cudaStream_t s, int transposed = 0) {
   // chain of cores u..u+nblk-1; dims[j], ranks[j] = left bond of core j, ranks[nblk] = right bond of last
   if (nblk < 1) return TRALS_ERR_ARG;
   const int64_t Ru = ranks[0];
   if (nblk == 1) {
     const int64_t n = dims[0] * Ru * ranks[1];
+    if (transposed) {
+      const int blocks = static_cast<int>(std::min<int64_t>((n + 255) / 256, 4 * kSMs));
+      relayout_kernel<<<blocks, 256, 0, s>>>(first_slice, TRALS_LAYOUT_SLICE, static_cast<int>(Ru), dims[0],
+                                             ranks[1], out, TRALS_LAYOUT_TT);
+      return launch_status();
+    }
     if (cudaMemcpyAsync(out, first_slice, n * sizeof(double), cudaMemcpyDeviceToDevice, s) != cudaSuccess)
       return TRALS_ERR_CUDA;
     return TRALS_OK;
@@ -649,6 +702,11 @@ int half_chain(int nblk, const int64_t* dims, const int32_t* ranks, const double
     // A(m = (i_pre, r_u), k = t) = cur[m*Rt + t]; B[t][(i_j, r')] = core_c[j]
     // Out[i_pre][i_j][r_u][r'] : m1 = i_pre, m2 = r_u ; n1 = i_j, n2 = r'
     CMap cm{0, Ru, Ij * Ru * Rn, Rn, Rn, Ru * Rn, 1};
+    if (transposed && j == nblk - 1) {
+      // [r'][r_u][(i_pre, i_j)] : the K x post operand of the fused reconstruct
+      const int64_t P = pre * Ij;
+      cm = CMap{0, Ru, Ij, P, Rn, 1, Ru * P};
+    }
     int st = gemm(cur, 0, Rt, 1, 1, pre * Ru, Rt, Ij * Rn, cores_c[j], Ij * Rn, dst, cm, 0, ws, ws_elems, s);
     if (st) return st;
     cur = dst;
@@ -873,7 +931,7 @@ int trals_gemm_f64(const double* A, int64_t sAp, int64_t sAm, int64_t sAk, int64
 
 int trals_core_relayout_f64(const double* src, int sl, int Ra, int64_t I, int Rb, double* dst, int dl,
                             void* stream) {
-  if (!src || !dst || Ra < 1 || Rb < 1 || I < 1 || sl < 0 || sl > 2 || dl < 0 || dl > 2) return TRALS_ERR_ARG;
+  if (!src || !dst || Ra < 1 || Rb < 1 || I < 1 || sl < 0 || sl > 3 || dl < 0 || dl > 3) return TRALS_ERR_ARG;
   const int64_t total = static_cast<int64_t>(Ra) * I * Rb;
   const int threads = 256;
   const int blocks = static_cast<int>(std::min<int64_t>((total + threads - 1) / threads, 4 * kSMs));
@@ -887,11 +945,11 @@ int64_t trals_half_chain_tmp_elems(int nblk, const int64_t* dims, const int32_t*
 
 int trals_half_chain_f64(int nblk, const int64_t* dims, const int32_t* ranks, const double* first_slice,
                          const double* const* cores_c, double* out, double* tmp, double* ws, int64_t ws_elems,
-                         void* stream) {
+                         int transposed, void* stream) {
   if (!dims || !ranks || !first_slice || !out) return TRALS_ERR_ARG;
   if (nblk > 1 && (!cores_c || !tmp)) return TRALS_ERR_ARG;
   return half_chain(nblk, dims, ranks, first_slice, cores_c, out, tmp, ws, ws_elems,
-                    static_cast<cudaStream_t>(stream));
+                    static_cast<cudaStream_t>(stream), transposed);
 }
 
 int trals_env_f64(const double* X, int64_t pre, int64_t post, int side, const double* H, int r_lo, int r_hi,
@@ -1043,6 +1101,19 @@ int trals_mttsp_f64(const double* X, int N, const int64_t* dims, const int32_t* 
                     double* ws, int64_t ws_elems, void* stream) {
   if (!X || N < 2 || !dims || !ranks || n < 0 || n >= N || !cc || !cs || !czt || !M || !ws) return TRALS_ERR_ARG;
   return run_mttsp(X, N, dims, ranks, n, cc, cs, czt, M, ws, ws_elems, static_cast<cudaStream_t>(stream));
+}
+
+int64_t trals_residual_ws_elems(int64_t pre, int64_t post) { return residual_blocks(pre, post); }
+
+int trals_residual_f64(const double* X, int64_t pre, int64_t post, const double* HL, const double* HRt, int64_t K,
+                       const double* xnorm2, double* out, double* ws, int64_t ws_elems, void* stream) {
+  if (!X || !HL || !HRt || !out || !ws || pre < 1 || post < 1 || K < 1) return TRALS_ERR_ARG;
+  if (ws_elems < residual_blocks(pre, post)) return TRALS_ERR_WORKSPACE;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int st = residual(HL, pre, K, HRt, post, X, ws, s);
+  if (st) return st;
+  residual_final_kernel<<<1, 1024, 0, s>>>(ws, static_cast<int>(residual_blocks(pre, post)), xnorm2, out);
+  return launch_status();
 }
 
 }  // extern "C"

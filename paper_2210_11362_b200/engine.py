@@ -142,6 +142,7 @@ class SweepEngine:
         self._join_ev = torch.cuda.Event() if self.dev.type == "cuda" else None
         self._cur = None
         self.graph = None
+        self.graph_exact = None
 
     # local views used by the X contractions
     def core_c(self, j):
@@ -231,7 +232,7 @@ class SweepEngine:
             cc = L.ptr_array([self.core_c(j).data_ptr() for j in blk])
             L.check(self.lib.trals_half_chain_f64(nblk, bd_a, br_a, self.core_s(blk[0]).data_ptr(), cc,
                                                   H.data_ptr(), tmp.data_ptr(), self.gws.data_ptr(),
-                                                  self.gws.numel(), self._sp()), "half_chain")
+                                                  self.gws.numel(), 0, self._sp()), "half_chain")
         self.steps.append(Step("subchain", chain_step, f"chain[{lo}..{hi}]"))
 
         if a == 0:
@@ -479,8 +480,15 @@ class SweepEngine:
                 st.fn()
         self._cur = None
 
-    def error_step(self, out):
-        """Cheap-error terms after a sweep into `out` (3 doubles): [e, <M,Z>, <S,Z^T Z>]."""
+    def error_step(self, out, exact=False):
+        """Per-sweep relative error into `out` (3 doubles).
+
+        exact=False: cheap identity from the last block (solvers.py:177-212): [e, <M,Z>, <S,Z^T Z>].
+        exact=True : ||X - TR(G)|| / ||X|| (solvers.py:164-174) by the fused reconstruct-residual
+                     GEMM: [e, sum (X - X_hat)^2, 0]."""
+        if exact:
+            self._exact_error(out)
+            return
         N = self.N
         n = N - 1
         rr = self.R(n) * self.R(n + 1)
@@ -489,11 +497,62 @@ class SweepEngine:
                                                self.err_ws.data_ptr(), self.err_ws.numel(), self._sp()),
                 "error_terms")
 
+    def _exact_plan(self):
+        if getattr(self, "_xp", None) is not None:
+            return self._xp
+        N = self.N
+        h = max(1, N // 2)
+        pre, post = _prod(self.dl[:h]), _prod(self.dl[h:])
+        R0, Rh = self.R(0), self.R(h)
+        need = 1
+
+        def chain_need(lo, hi):
+            bd = self.dl[lo:hi + 1]
+            br = [self.R(j) for j in range(lo, hi + 2)]
+            n = 1
+            p = bd[0]
+            for j in range(1, len(bd)):
+                n = max(n, self.lib.trals_gemm_ws_elems(1, p * br[0], br[j], bd[j] * br[j + 1]))
+                p *= bd[j]
+            tmp = self.lib.trals_half_chain_tmp_elems(len(bd), L.i64_array(bd), L.i32_array(br))
+            return n, tmp, L.i64_array(bd), L.i32_array(br)
+
+        nl, tl, bdl, brl = chain_need(0, h - 1)
+        nr, tr, bdr, brr = chain_need(h, N - 1)
+        self._xp = {
+            "h": h, "pre": pre, "post": post, "K": R0 * Rh,
+            "HL": self._empty(pre * R0 * Rh), "HRt": self._empty(R0 * Rh * post),
+            "tmp": self._empty(max(1, tl, tr)), "ws": self._empty(max(1, nl, nr)),
+            "part": self._empty(max(1, self.lib.trals_residual_ws_elems(pre, post))),
+            "bdl": bdl, "brl": brl, "bdr": bdr, "brr": brr,
+        }
+        return self._xp
+
+    def _exact_error(self, out):
+        xp = self._exact_plan()
+        N, h = self.N, xp["h"]
+        sp = self._sp()
+        for lo, hi, H, bd, br, tr in ((0, h - 1, xp["HL"], xp["bdl"], xp["brl"], 0),
+                                      (h, N - 1, xp["HRt"], xp["bdr"], xp["brr"], 1)):
+            blk = list(range(lo, hi + 1))
+            cc = L.ptr_array([self.core_c(j).data_ptr() for j in blk])
+            L.check(self.lib.trals_half_chain_f64(len(blk), bd, br, self.core_s(lo).data_ptr(), cc, H.data_ptr(),
+                                                  xp["tmp"].data_ptr(), xp["ws"].data_ptr(), xp["ws"].numel(), tr, sp),
+                    "half_chain")
+        L.check(self.lib.trals_residual_f64(self.x.data_ptr(), xp["pre"], xp["post"], xp["HL"].data_ptr(),
+                                            xp["HRt"].data_ptr(), xp["K"], self.xnorm2.data_ptr(), out.data_ptr(),
+                                            xp["part"].data_ptr(), xp["part"].numel(), sp), "residual")
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.all_reduce(out[1:2], group=self.group)
+            x2 = self.xnorm2[0:1]
+            out[0:1].copy_(torch.where(x2 > 0, torch.sqrt(out[1:2] / x2), torch.zeros_like(x2)))
+
     def cores_host(self):
         return [g.detach().cpu().numpy().copy() for g in self.Gc]
 
     # ------------------------------------------------------------ CUDA graphs
-    def capture(self, with_error=True):
+    def capture(self, with_error=True, exact=False):
         """Capture one sweep (+ the error terms into `err_cur`) as a CUDA graph.
 
         Every buffer is owned by the engine, so the graph stays valid for the
@@ -513,12 +572,13 @@ class SweepEngine:
                 g.capture_begin()
                 self.run_sweep()
                 if with_error:
-                    self.error_step(self.err_cur)
+                    self.error_step(self.err_cur, exact=exact)
                 g.capture_end()
         finally:
             self.stream = old
         old.wait_stream(cap)
         self.graph = g
+        self.graph_exact = exact
         return g
 
     def replay(self):

@@ -180,9 +180,10 @@ def _run(x, config, variant):
     t1.record(stream)
 
     track = config.error_mode in ("exact", "cheap")
+    exact = config.error_mode == "exact"
     use_graph = (world == 1 and not config.timing_buckets)
-    if use_graph and eng.graph is None:
-        eng.capture(with_error=True)
+    if use_graph and (eng.graph is None or eng.graph_exact != exact):
+        eng.capture(with_error=True, exact=exact)
     errs = torch.zeros((config.max_iters, 3), dtype=torch.float64, device=x_local.device)
     sweep_events = []
     report.termination = "max_iters"
@@ -201,7 +202,7 @@ def _run(x, config, variant):
             eng.run_sweep(ev)
             b.record(stream)
             if track:
-                eng.error_step(errs[k])
+                eng.error_step(errs[k], exact=exact)
         sweep_events.append((a, b, ev))
         done = k + 1
         if config.tol > 0 and k >= 1:

@@ -35,7 +35,7 @@ def reconstruct_device(cores, device="cuda") -> torch.Tensor:
     h = N // 2
     sp = _stream()
 
-    def chain(lo, hi):
+    def chain(lo, hi, transposed):
         blk = list(range(lo, hi + 1))
         bd = [dims[j] for j in blk]
         br = [ranks[j % N] for j in range(lo, hi + 2)]
@@ -54,13 +54,12 @@ def reconstruct_device(cores, device="cuda") -> torch.Tensor:
         ws = torch.empty(need, dtype=torch.float64, device=device)
         L.check(lib.trals_half_chain_f64(len(blk), L.i64_array(bd), L.i32_array(br), first.data_ptr(),
                                          L.ptr_array([cs[j].data_ptr() for j in blk]), out.data_ptr(),
-                                         tmp.data_ptr(), ws.data_ptr(), ws.numel(), sp), "half_chain")
+                                         tmp.data_ptr(), ws.data_ptr(), ws.numel(), transposed, sp), "half_chain")
         return out, int(np.prod(bd))
 
-    HL, pre = chain(0, h - 1)      # [pre][r_0][r_h]
-    HR, post = chain(h, N - 1)     # [post][r_h][r_0]
+    HL, pre = chain(0, h - 1, 0)   # [pre][r_0][r_h]
+    B, post = chain(h, N - 1, 1)   # [r_0][r_h][post]
     R0, Rh = ranks[0], ranks[h]
-    B = HR.view(post, Rh, R0).permute(2, 1, 0).contiguous()  # [r_0][r_h][post]
     X = torch.empty(dims, dtype=torch.float64, device=device)
     K = R0 * Rh
     need = lib.trals_gemm_ws_elems(1, pre, K, post)

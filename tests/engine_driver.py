@@ -7,7 +7,7 @@ from paper_2210_11362_b200.engine import SweepEngine
 
 
 def run_engine(x, ranks, variant, init_cores, sweeps, lib=None, device="cpu", shard_mode=None, lo=0, hi=None,
-               world=1, group=None):
+               world=1, group=None, exact=False):
     x = np.asarray(x, dtype=np.float64)
     dims = x.shape
     if shard_mode is not None and world > 1:
@@ -26,6 +26,6 @@ def run_engine(x, ranks, variant, init_cores, sweeps, lib=None, device="cpu", sh
     out = torch.zeros(3, dtype=torch.float64, device=device)
     for _ in range(sweeps):
         eng.run_sweep()
-        eng.error_step(out)
+        eng.error_step(out, exact=exact)
         errs.append(float(out[0].item()))
     return eng.cores_host(), errs, eng

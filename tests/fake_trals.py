@@ -107,7 +107,8 @@ class FakeTrals:
         return 0
 
     # --- ring pieces -----------------------------------------------------
-    def trals_half_chain_f64(self, nblk, dims, ranks, first_slice, cores_c, out, tmp, ws, ws_elems, stream):
+    def trals_half_chain_f64(self, nblk, dims, ranks, first_slice, cores_c, out, tmp, ws, ws_elems, transposed,
+                             stream):
         self._count("half_chain")
         d = _vals(dims, nblk)
         r = _vals(ranks, nblk + 1)
@@ -116,7 +117,24 @@ class FakeTrals:
         for j in range(1, nblk):
             g = _arr(cc[j], r[j] * d[j] * r[j + 1]).reshape(r[j], d[j], r[j + 1])
             h = np.einsum("pat,tic->piac", h, g).reshape(-1, r[0], r[j + 1])
+        if transposed:
+            h = np.ascontiguousarray(h.transpose(2, 1, 0))
         _arr(out, h.size)[:] = h.ravel()
+        return 0
+
+    def trals_residual_ws_elems(self, pre, post):
+        return 1
+
+    def trals_residual_f64(self, X, pre, post, HL, HRt, K, xnorm2, out, ws, ws_elems, stream):
+        self._count("residual")
+        x = _arr(X, pre * post).reshape(pre, post)
+        hl = _arr(HL, pre * K).reshape(pre, K)
+        hr = _arr(HRt, K * post).reshape(K, post)
+        ssr = float(np.sum((x - hl @ hr) ** 2))
+        x2 = float(_arr(xnorm2, 1)[0])
+        o = _arr(out, 3)
+        o[1] = ssr
+        o[0] = 0.0 if x2 == 0 else np.sqrt(ssr / x2)
         return 0
 
     def trals_env_f64(self, X, pre, post, side, H, r_lo, r_hi, E, leaf, ws, ws_elems, stream):

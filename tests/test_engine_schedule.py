@@ -35,6 +35,18 @@ def test_schedule_matches_reference_sweeps(name):
         assert rel(cores[j], g[f"ne_core_{j}"]) < 1e-6
 
 
+@pytest.mark.parametrize("name", SMALL)
+def test_exact_error_matches_reference(name):
+    g = load_golden(name)
+    dims = tuple(int(d) for d in g["dims"])
+    N = len(dims)
+    ranks = [int(r) for r in g["ranks"]]
+    lib = FakeTrals()
+    _, errs, _ = run_engine(g["x"], ranks, "ne", golden_cores(g, "init", N), int(g["sweeps"]), lib=lib, exact=True)
+    assert lib.calls["residual"] == int(g["sweeps"])
+    np.testing.assert_allclose(errs, g["ne_exact_errors"], rtol=0, atol=1e-9)
+
+
 @pytest.mark.parametrize("N,dims,ranks", [
     (3, (9, 8, 7), (2, 3, 4)),
     (4, (5, 4, 6, 3), (2, 3, 2, 3)),

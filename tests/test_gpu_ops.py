@@ -145,3 +145,22 @@ def test_sumsq_and_error_terms():
     assert abs(out[1] - cross) < 1e-10 * abs(cross)
     assert abs(out[2] - model) < 1e-10 * abs(model)
     assert abs(out[0] - O.residual_from_sweep(100.0, cross, model)) < 1e-12
+
+
+@pytest.mark.parametrize("dims,ranks", [((9, 8, 7), (2, 3, 4)), ((6, 5, 4, 7), (3, 2, 2, 3)),
+                                        ((5, 4, 3, 4, 3), (2, 2, 3, 2, 2)), ((30, 40), (3, 2))])
+def test_reconstruct_and_exact_residual(dims, ranks):
+    from paper_2210_11362_b200 import _lib as L
+    from paper_2210_11362_b200.synthetic import reconstruct_device
+    cores = O.gaussian_ring(dims, ranks, O.philox(4))
+    ref = O.dense_from_ring(cores)
+    got = reconstruct_device(cores).cpu().numpy()
+    assert rel(got, ref) < 1e-13
+    # exact error through the fused residual == ||x - dense|| / ||x||
+    x = ref + 0.05 * np.random.default_rng(1).standard_normal(dims)
+    from engine_driver import run_engine
+    N = len(dims)
+    _, errs, eng = run_engine(x, list(ranks), "ne", cores, 1, device="cuda", lib=None, exact=True)
+    # after one sweep the cores changed: compare with the oracle's exact error for those cores
+    ocores, orep = O.solve(x, "ne", O.Config(ranks=ranks, max_iters=1, init_cores=cores, error_mode="exact"))
+    assert abs(errs[0] - orep.errors[0]) < 1e-12
