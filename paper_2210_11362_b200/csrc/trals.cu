@@ -351,12 +351,30 @@ __device__ int chol_aug_smem(double* a, int ld, int n, int aug) {
     for (int c = j + tid; c < n; c += blockDim.x) a[j * ld + c] *= dinv;
     for (int c = tid; c <= j; c += blockDim.x) a[j * ld + aug + c] *= dinv;
     __syncthreads();
+    // row r: columns [r, n) of the A part, then [0, j] of the augmented part, as one
+    // index range of width (n - r) + (j + 1); loads for a whole row are issued first
+    const double* aj = a + j * ld;
     for (int r = j + 1 + warp; r < n; r += nwarps) {
-      const double mult = a[j * ld + r];
+      const double mult = aj[r];
       double* ar = a + r * ld;
-      const double* aj = a + j * ld;
-      for (int c = r + lane; c < n; c += 32) ar[c] = fma(-mult, aj[c], ar[c]);
-      for (int c = lane; c <= j; c += 32) ar[aug + c] = fma(-mult, aj[aug + c], ar[aug + c]);
+      const int wa = n - r, wt = wa + j + 1;
+      double x[4], y[4];
+      int off[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int c = lane + 32 * q;
+        off[q] = c < wa ? r + c : aug + (c - wa);
+        const bool ok = c < wt;
+        x[q] = ok ? aj[off[q]] : 0.0;
+        y[q] = ok ? ar[off[q]] : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (lane + 32 * q < wt) ar[off[q]] = fma(-mult, x[q], y[q]);
+      for (int c = lane + 128; c < wt; c += 32) {  // n > 127: remaining columns
+        const int o = c < wa ? r + c : aug + (c - wa);
+        ar[o] = fma(-mult, aj[o], ar[o]);
+      }
     }
     __syncthreads();
   }
@@ -366,7 +384,7 @@ __device__ int chol_aug_smem(double* a, int ld, int n, int aug) {
 // Resident factor + inverse for m <= kInvMax: U (upper), W = U^{-1} (upper), V = U^{-T} (lower).
 constexpr int kInvMax = 112;
 
-__global__ void __launch_bounds__(512) chol_inv_kernel(const double* __restrict__ S, int m, double* __restrict__ U,
+__global__ void __launch_bounds__(1024) chol_inv_kernel(const double* __restrict__ S, int m, double* __restrict__ U,
                                                        double* __restrict__ W, double* __restrict__ V,
                                                        int check_degen, int* __restrict__ info) {
   extern __shared__ __align__(16) double a[];
@@ -450,7 +468,7 @@ __global__ void __launch_bounds__(1024) chol_sym_kernel(const double* __restrict
 }
 
 // factor the pb x pb diagonal block at (p0, p0) of U in place; W = block^{-1}, WT = W^T (ld kBlkNB)
-__global__ void __launch_bounds__(256) chol_diag_kernel(double* __restrict__ U, int m, int p0, int pb,
+__global__ void __launch_bounds__(1024) chol_diag_kernel(double* __restrict__ U, int m, int p0, int pb,
                                                         double* __restrict__ W, double* __restrict__ WT,
                                                         int* __restrict__ info) {
   extern __shared__ __align__(16) double a[];  // [pb][2*kBlkNB + 1]
@@ -557,7 +575,7 @@ int blocked_cholesky(const double* S, int m, double* U, double* L, double* aux, 
       cudaFuncSetAttribute(chol_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kDiagSmem);
       attr = true;
     }
-    chol_diag_kernel<<<1, 256, kDiagSmem, s>>>(U, m, p0, pb, W, WT, info);
+    chol_diag_kernel<<<1, 1024, kDiagSmem, s>>>(U, m, p0, pb, W, WT, info);
     if (int st = launch_status()) return st;
     if (rest == 0) continue;
     double* U12 = U + static_cast<int64_t>(p0) * m + p0 + pb;
@@ -579,6 +597,148 @@ int blocked_cholesky(const double* S, int m, double* U, double* L, double* aux, 
   return TRALS_OK;
 }
 
+
+// Fused blocked substitution for m > kInvMax: one CTA per 8 right-hand-side
+// rows (one DMMA m8 row tile), all 2*nblk block steps in one launch.
+//   forward  (Y U = M):   R_b -= Y_{<b} U_{<b,b};  Y_b = R_b W_b
+//   backward (Z U^T = Y): T_b = Y_b - Z_{>b} L_{>b,b};  Z_b = T_b W_b^T
+// The RHS rows live in shared memory; U / L column blocks and the diagonal
+// inverses stream through a cp.async double buffer; warp w owns columns
+// [8w, 8w+8) of the current 64-column block.
+constexpr int kFsRows = 8;
+constexpr int kFsLd = kBlkNB + 4;  // staged 64x64 pitch (conflict-free B fragments)
+
+__global__ void __launch_bounds__(256) fused_solve_kernel(const double* __restrict__ U, const double* __restrict__ L,
+                                                          const double* __restrict__ aux, int m,
+                                                          const double* __restrict__ Mr, int64_t rows,
+                                                          double* __restrict__ Z) {
+  extern __shared__ __align__(16) double fs[];
+  const int mp = ((m + kBlkNB - 1) / kBlkNB) * kBlkNB;
+  const int ldr = mp + 4;
+  double* Rs = fs;                       // [8][ldr] running rhs, later Z
+  double* Ys = Rs + kFsRows * ldr;       // [8][ldr] forward solution
+  double* Bst = Ys + kFsRows * ldr;      // [2][64][kFsLd] staged operand blocks
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int fr = lane >> 2, fk = lane & 3;
+  const int64_t row0 = static_cast<int64_t>(blockIdx.x) * kFsRows;
+  const int nblk = mp / kBlkNB;
+  for (int t = tid; t < kFsRows * ldr; t += blockDim.x) {
+    const int r = t / ldr, c = t - r * ldr;
+    Rs[t] = (row0 + r < rows && c < m) ? Mr[(row0 + r) * m + c] : 0.0;
+    Ys[t] = 0.0;
+  }
+  // stage a 64x64 block src[(k0 + kk) * lds + c0 + c] (zero outside [0,m)^2) into buffer `buf`
+  auto stage = [&](const double* src, int lds, int k0, int c0, int limk, int limc, int buf) {
+    double* dst = Bst + buf * kBlkNB * kFsLd;
+    for (int t = tid; t < kBlkNB * (kBlkNB / 2); t += blockDim.x) {
+      const int kk = t / (kBlkNB / 2), c = (t - kk * (kBlkNB / 2)) * 2;
+      const int gk = k0 + kk, gc = c0 + c;
+      const int valid = (gk < limk) ? max(0, min(2, limc - gc)) : 0;
+      const double* p = valid ? src + static_cast<int64_t>(gk) * lds + gc : src;
+      trals::cp_async_zfill(dst + kk * kFsLd + c, p, valid * 8, (lds % 2 == 0) ? 16 : 8);
+      if (lds % 2 != 0) trals::cp_async_zfill(dst + kk * kFsLd + c + 1, valid > 1 ? p + 1 : src, valid > 1 ? 8 : 0, 8);
+    }
+    trals::cp_async_commit();
+  };
+  __syncthreads();
+  // ---------------- forward ----------------
+  for (int b = 0; b < nblk; ++b) {
+    const int j0 = b * kBlkNB;
+    double acc0 = 0.0, acc1 = 0.0;
+    const int nk = j0 / kBlkNB;  // K chunks of 64 rows of U
+    const double* Wb = aux + static_cast<int64_t>(b) * 2 * kBlkNB * kBlkNB;
+    // chunks: U[kc*64 .. +64][j0 .. j0+64] for kc < nk, then W_b
+    stage(nk > 0 ? U : Wb, nk > 0 ? m : kBlkNB, 0, nk > 0 ? j0 : 0, nk > 0 ? m : kBlkNB, nk > 0 ? m : kBlkNB, 0);
+    for (int kc = 0; kc <= nk; ++kc) {
+      if (kc + 1 <= nk) {
+        if (kc + 1 < nk) stage(U, m, (kc + 1) * kBlkNB, j0, m, m, (kc + 1) & 1);
+        else stage(Wb, kBlkNB, 0, 0, kBlkNB, kBlkNB, (kc + 1) & 1);
+        trals::cp_async_wait<1>();
+      } else {
+        trals::cp_async_wait<0>();
+      }
+      __syncthreads();
+      const double* B = Bst + (kc & 1) * kBlkNB * kFsLd;
+      if (kc < nk) {
+        // acc += Y[:, kc*64 .. +64] * U-block
+#pragma unroll 4
+        for (int k4 = 0; k4 < kBlkNB; k4 += 4) {
+          const double a = Ys[fr * ldr + kc * kBlkNB + k4 + fk];
+          const double bb = B[(k4 + fk) * kFsLd + warp * 8 + fr];
+          trals::dmma884(acc0, acc1, a, bb);
+        }
+      } else {
+        // R_b -= acc, then Y_b = R_b W_b
+        Rs[fr * ldr + j0 + warp * 8 + 2 * fk] -= acc0;
+        Rs[fr * ldr + j0 + warp * 8 + 2 * fk + 1] -= acc1;
+        __syncthreads();
+        double y0 = 0.0, y1 = 0.0;
+#pragma unroll 4
+        for (int k4 = 0; k4 < kBlkNB; k4 += 4) {
+          const double a = Rs[fr * ldr + j0 + k4 + fk];
+          const double bb = B[(k4 + fk) * kFsLd + warp * 8 + fr];
+          trals::dmma884(y0, y1, a, bb);
+        }
+        Ys[fr * ldr + j0 + warp * 8 + 2 * fk] = y0;
+        Ys[fr * ldr + j0 + warp * 8 + 2 * fk + 1] = y1;
+      }
+      __syncthreads();
+    }
+  }
+  // ---------------- backward (Z overwrites Rs) ----------------
+  for (int b = nblk - 1; b >= 0; --b) {
+    const int j0 = b * kBlkNB, j1 = j0 + kBlkNB;
+    double acc0 = 0.0, acc1 = 0.0;
+    const int nk = (mp - j1) / kBlkNB;  // K chunks: L rows j1.. (blocks b+1 .. nblk-1)
+    const double* WTb = aux + static_cast<int64_t>(b) * 2 * kBlkNB * kBlkNB + kBlkNB * kBlkNB;
+    stage(nk > 0 ? L : WTb, nk > 0 ? m : kBlkNB, nk > 0 ? j1 : 0, nk > 0 ? j0 : 0, nk > 0 ? m : kBlkNB,
+          nk > 0 ? m : kBlkNB, 0);
+    for (int kc = 0; kc <= nk; ++kc) {
+      if (kc + 1 <= nk) {
+        if (kc + 1 < nk) stage(L, m, j1 + (kc + 1) * kBlkNB, j0, m, m, (kc + 1) & 1);
+        else stage(WTb, kBlkNB, 0, 0, kBlkNB, kBlkNB, (kc + 1) & 1);
+        trals::cp_async_wait<1>();
+      } else {
+        trals::cp_async_wait<0>();
+      }
+      __syncthreads();
+      const double* B = Bst + (kc & 1) * kBlkNB * kFsLd;
+      if (kc < nk) {
+        const int kb = j1 + kc * kBlkNB;
+#pragma unroll 4
+        for (int k4 = 0; k4 < kBlkNB; k4 += 4) {
+          const double a = Rs[fr * ldr + kb + k4 + fk];  // Z_{>b}
+          const double bb = B[(k4 + fk) * kFsLd + warp * 8 + fr];
+          trals::dmma884(acc0, acc1, a, bb);
+        }
+      } else {
+        // T_b = Y_b - acc (kept in Ys), Z_b = T_b W_b^T -> Rs
+        Ys[fr * ldr + j0 + warp * 8 + 2 * fk] -= acc0;
+        Ys[fr * ldr + j0 + warp * 8 + 2 * fk + 1] -= acc1;
+        __syncthreads();
+        double z0 = 0.0, z1 = 0.0;
+#pragma unroll 4
+        for (int k4 = 0; k4 < kBlkNB; k4 += 4) {
+          const double a = Ys[fr * ldr + j0 + k4 + fk];
+          const double bb = B[(k4 + fk) * kFsLd + warp * 8 + fr];
+          trals::dmma884(z0, z1, a, bb);
+        }
+        Rs[fr * ldr + j0 + warp * 8 + 2 * fk] = z0;
+        Rs[fr * ldr + j0 + warp * 8 + 2 * fk + 1] = z1;
+      }
+      __syncthreads();
+    }
+  }
+  for (int t = tid; t < kFsRows * m; t += blockDim.x) {
+    const int r = t / m, c = t - r * m;
+    if (row0 + r < rows) Z[(row0 + r) * m + c] = Rs[r * ldr + c];
+  }
+}
+
+size_t fused_solve_smem(int m) {
+  const int mp = ((m + kBlkNB - 1) / kBlkNB) * kBlkNB;
+  return sizeof(double) * (2 * kFsRows * (mp + 4) + 2 * kBlkNB * kFsLd);
+}
 
 // Z S = M, S = U^T U:  Y U = M (forward), Z U^T = Y (backward), 64-column blocks
 int blocked_solve(const double* U, const double* L, const double* aux, int m, const double* Mr, int64_t rows,
@@ -1037,7 +1197,7 @@ int trals_cholesky_f64(const double* S, int m, double* U, double* F, double* aux
     cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     attr = true;
   }
-  chol_inv_kernel<<<1, 512, smem, s>>>(S, m, U, F, aux, check_degen, info);
+  chol_inv_kernel<<<1, 1024, smem, s>>>(S, m, U, F, aux, check_degen, info);
   return launch_status();
 }
 
@@ -1054,7 +1214,20 @@ int trals_chol_solve_f64(const double* U, const double* F, const double* aux, in
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   double* gws = ws + rows * m;
   const int64_t gws_elems = ws_elems - rows * m;
-  if (m > kInvMax) return blocked_solve(U, F, aux, m, Mr, rows, Z, ws, gws, gws_elems, s);
+  if (m > kInvMax) {
+    const size_t smem = fused_solve_smem(m);
+    if (smem <= 200 * 1024) {
+      static bool attr = false;
+      if (!attr) {
+        cudaFuncSetAttribute(fused_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr = true;
+      }
+      const unsigned blocks = static_cast<unsigned>((rows + kFsRows - 1) / kFsRows);
+      fused_solve_kernel<<<blocks, 256, smem, s>>>(U, F, aux, m, Mr, rows, Z);
+      return launch_status();
+    }
+    return blocked_solve(U, F, aux, m, Mr, rows, Z, ws, gws, gws_elems, s);
+  }
   // Z = M U^{-1} U^{-T} = (M W) V
   const CMap rm = rowmajor(m);
   int st = gemm(Mr, 0, m, 1, 1, rows, m, m, F, m, ws, rm, 0, gws, gws_elems, s);
