@@ -256,13 +256,11 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   if (l == 0) red[w] = v;
   __syncthreads();
-  double r = 0.0;
-  if (w == 0) {
-    r = (l < NT / 32) ? red[l] : 0.0;
-    r = warp_sum(r);
-  }
+  // every warp reduces the partials (no shuffles under a warp-dependent branch)
+  double r = (l < NT / 32) ? red[l] : 0.0;
+  r = warp_sum(r);
   __syncthreads();
-  return r;  // valid in warp 0
+  return r;  // valid in every thread
 }
 
 // partial sums of squares and of non-finite entries (the check of validation.py:53-54)
@@ -335,48 +333,177 @@ __device__ __forceinline__ void chol_reduce_flags(double amax, double asym, doub
   __syncthreads();
 }
 
-// In-place upper Cholesky of an n x n SPD block held in shared memory rows
-// a[r*ld + c], with an n-column identity block appended at column `aug`:
-// the right-looking row operations that turn A into U turn I into
-// V = U^{-T} (Gauss-Jordan on [A | I]), so the factor and its inverse come
-// out of one pass.  Only the upper triangle of the A part is maintained.
-// Returns the 1-based failing pivot (0 on success); uniform across the CTA.
-__device__ int chol_aug_smem(double* a, int ld, int n, int aug) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
-  for (int j = 0; j < n; ++j) {
-    const double d = a[j * ld + j];
-    if (!(d > 0.0)) return j + 1;  // dpotrf failure (also NaN)
-    const double dinv = rsqrt(d);
-    __syncthreads();  // everyone has read the pivot before row j changes
-    for (int c = j + tid; c < n; c += blockDim.x) a[j * ld + c] *= dinv;
-    for (int c = tid; c <= j; c += blockDim.x) a[j * ld + aug + c] *= dinv;
-    __syncthreads();
-    // row r: columns [r, n) of the A part, then [0, j] of the augmented part, as one
-    // index range of width (n - r) + (j + 1); loads for a whole row are issued first
-    const double* aj = a + j * ld;
-    for (int r = j + 1 + warp; r < n; r += nwarps) {
-      const double mult = aj[r];
-      double* ar = a + r * ld;
-      const int wa = n - r, wt = wa + j + 1;
-      double x[4], y[4];
-      int off[4];
+// Blocked in-place upper Cholesky of an n x n SPD block (n <= 112) held in shared
+// memory, augmented with the identity (Gauss-Jordan on [A | I]): on return the
+// A part holds U (upper) and the augmented part holds V = U^{-T} (lower).
+// Rows are processed in panels of 8.  Warp 0 factors each 8x8 diagonal block in
+// registers (rows of [D | I_8] in lanes, shuffles, one rsqrt per pivot, no
+// divisions); with one panel of look-ahead it updates and factors the NEXT
+// diagonal block while the other warps apply the rank-8 update of the current
+// panel to the trailing rows on the DMMA pipe.  Two barriers per 8 pivots.
+// Layout: row r at a + r*ld, A part columns [0, npad), augmented columns
+// [aug, aug + npad); padding rows/columns are 0.  scratch >= 256 doubles.
+// Returns the 1-based failing pivot (0 on success), uniform across the CTA.
+__device__ __forceinline__ int chol8_factor_block(const double* a, int ld, int p, int pb, double* Ud, double* Xd) {
+  // warp-level: lane i < pb holds row i of [D | I_8]
+  const int lane = threadIdx.x & 31;
+  double d[8], x[8];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int c = lane + 32 * q;
-        off[q] = c < wa ? r + c : aug + (c - wa);
-        const bool ok = c < wt;
-        x[q] = ok ? aj[off[q]] : 0.0;
-        y[q] = ok ? ar[off[q]] : 0.0;
+  for (int c = 0; c < 8; ++c) {
+    double v = 0.0;
+    if (lane < pb && c < pb) v = c >= lane ? a[(p + lane) * ld + p + c] : a[(p + c) * ld + p + lane];
+    d[c] = v;
+    x[c] = (c == lane) ? 1.0 : 0.0;
+  }
+  // Every shuffle is executed unconditionally by the whole warp (shuffles under a
+  // branch the compiler cannot prove uniform compile to a slow collective path);
+  // pivots beyond pb or after a failure are masked arithmetically.
+  int bad = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const double dk = __shfl_sync(0xffffffffu, d[k], k);
+    const bool live = (k < pb) && (bad == 0);
+    const bool ok = live && (dk > 0.0);
+    if (live && !ok) bad = k + 1;  // non-positive or NaN pivot (dpotrf failure)
+    const double sk = rsqrt(ok ? dk : 1.0);
+    if (ok && lane == k) {
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        d[c] = c >= k ? d[c] * sk : 0.0;
+        x[c] *= sk;
       }
+    }
+    double u[8], xk[8];
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (lane + 32 * q < wt) ar[off[q]] = fma(-mult, x[q], y[q]);
-      for (int c = lane + 128; c < wt; c += 32) {  // n > 127: remaining columns
-        const int o = c < wa ? r + c : aug + (c - wa);
-        ar[o] = fma(-mult, aj[o], ar[o]);
+    for (int c = 0; c < 8; ++c) {
+      u[c] = __shfl_sync(0xffffffffu, d[c], k);
+      xk[c] = __shfl_sync(0xffffffffu, x[c], k);
+    }
+    double uki = 0.0;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) uki = (c == lane) ? u[c] : uki;
+    if (ok && lane > k && lane < pb) {
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        if (c >= lane) d[c] = fma(-uki, u[c], d[c]);
+        x[c] = fma(-uki, xk[c], x[c]);
+      }
+    }
+  }
+  if (!bad && lane < 8) {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      Ud[lane * 8 + c] = (lane < pb && c < pb && c >= lane) ? d[c] : 0.0;
+      Xd[lane * 8 + c] = (lane < pb && c < pb && c <= lane) ? x[c] : 0.0;
+    }
+  }
+  return bad;
+}
+
+__device__ int chol8_aug_smem(double* a, int ld, int n, int aug, double* scratch /* >= 256 doubles */) {
+  const int tid = threadIdx.x, lane = tid & 31, nwarps = blockDim.x >> 5;
+  // warp index through a shuffle from lane 0: provably warp-uniform, so the warp-0
+  // branches below keep the fast (non-collective) shuffle path
+  const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
+  const int fr = lane >> 2, fk = lane & 3;
+  __shared__ int fail_at;
+  if (tid == 0) fail_at = 0;
+  if (warp == 0) {
+    const int bad = chol8_factor_block(a, ld, 0, min(8, n), scratch, scratch + 64);
+    if (bad && lane == 0) fail_at = bad;
+  }
+  __syncthreads();
+  if (fail_at) return fail_at;
+  for (int p = 0, it = 0; p < n; p += 8, ++it) {
+    const int pb = min(8, n - p);
+    const double* Ud = scratch + (it & 1) * 128;
+    const double* Xd = Ud + 64;
+    // (A) panel rows <- Xd * panel rows: A part columns [p, n), augmented columns [0, p + pb)
+    {
+      const int wa = n - p, wt = wa + p + pb;
+      for (int cc = tid; cc < wt; cc += blockDim.x) {
+        const int col = cc < wa ? p + cc : aug + (cc - wa);
+        double old[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) old[t] = t < pb ? a[(p + t) * ld + col] : 0.0;
+        const bool diag = cc < pb;  // inside the diagonal block: write Ud (exact zeros below)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          if (i >= pb) break;
+          double v = 0.0;
+#pragma unroll
+          for (int t = 0; t <= i; ++t) v = fma(Xd[i * 8 + t], old[t], v);
+          a[(p + i) * ld + col] = diag ? Ud[i * 8 + cc] : v;
+        }
       }
     }
     __syncthreads();
+    // (B) trailing rows r >= p + 8: a[r][c] -= sum_t P[t][r] P[t][c]  (A part c >= r, augmented c < p + 8)
+    const int r0 = p + 8;
+    if (r0 < n) {
+      const int nbr = (n - r0 + 7) / 8;                 // trailing row blocks
+      const int nba = (p + 8) / 8;                      // augmented column blocks
+      const int nupper = nbr * (nbr + 1) / 2;
+      const int ntiles = nupper + nbr * nba;
+      auto update_tile = [&](int rb, int cbase) {
+        double* c = a + (rb + fr) * ld + cbase + 2 * fk;
+        double c0 = c[0], c1 = c[1];
+#pragma unroll
+        for (int k0 = 0; k0 < 8; k0 += 4) {
+          const double av = -a[(p + k0 + fk) * ld + rb + fr];
+          const double bv = a[(p + k0 + fk) * ld + cbase + fr];
+          trals::dmma884(c0, c1, av, bv);
+        }
+        c[0] = c0;
+        c[1] = c1;
+      };
+      if (warp == 0) {
+        // look-ahead: next diagonal block first, then factor it into the other scratch half
+        update_tile(r0, r0);
+        __syncwarp();
+        double* nUd = scratch + ((it + 1) & 1) * 128;
+        const int bad = chol8_factor_block(a, ld, r0, min(8, n - r0), nUd, nUd + 64);
+        if (bad && lane == 0) fail_at = r0 + bad;
+      } else {
+        auto tile_base = [&](int tile, int& rb, int& cbase) -> bool {
+          if (tile < nupper) {  // upper-triangular tile grid of the trailing A part
+            int bi = 0, rem = tile;
+            while (rem >= nbr - bi) { rem -= nbr - bi; ++bi; }
+            if (bi == 0 && rem == 0) return false;  // next diagonal block: warp 0 owns it
+            rb = r0 + bi * 8;
+            cbase = r0 + (bi + rem) * 8;
+          } else {
+            const int q = tile - nupper;
+            rb = r0 + (q / nba) * 8;
+            cbase = aug + (q % nba) * 8;
+          }
+          return true;
+        };
+        const int stride = nwarps - 1;
+        for (int tile = warp - 1; tile < ntiles; tile += 2 * stride) {
+          // two independent tiles per iteration: their load/DMMA/store chains overlap
+          int rb0 = 0, cb0 = 0, rb1 = 0, cb1 = 0;
+          const bool v0 = tile_base(tile, rb0, cb0);
+          const bool v1 = tile + stride < ntiles && tile_base(tile + stride, rb1, cb1);
+          double* c0p = a + (rb0 + fr) * ld + cb0 + 2 * fk;
+          double* c1p = a + (rb1 + fr) * ld + cb1 + 2 * fk;
+          double x0 = v0 ? c0p[0] : 0.0, x1 = v0 ? c0p[1] : 0.0;
+          double y0 = v1 ? c1p[0] : 0.0, y1 = v1 ? c1p[1] : 0.0;
+#pragma unroll
+          for (int k0 = 0; k0 < 8; k0 += 4) {
+            const double* prow = a + (p + k0 + fk) * ld;
+            const double a0 = -prow[rb0 + fr], b0 = prow[cb0 + fr];
+            const double a1 = -prow[rb1 + fr], b1 = prow[cb1 + fr];
+            trals::dmma884(x0, x1, a0, b0);
+            trals::dmma884(y0, y1, a1, b1);
+          }
+          if (v0) { c0p[0] = x0; c0p[1] = x1; }
+          if (v1) { c1p[0] = y0; c1p[1] = y1; }
+        }
+      }
+    }
+    __syncthreads();
+    if (fail_at) return fail_at;
   }
   return 0;
 }
@@ -384,26 +511,35 @@ __device__ int chol_aug_smem(double* a, int ld, int n, int aug) {
 // Resident factor + inverse for m <= kInvMax: U (upper), W = U^{-1} (upper), V = U^{-T} (lower).
 constexpr int kInvMax = 112;
 
-__global__ void __launch_bounds__(1024) chol_inv_kernel(const double* __restrict__ S, int m, double* __restrict__ U,
+__global__ void __launch_bounds__(512) chol_inv_kernel(const double* __restrict__ S, int m, double* __restrict__ U,
                                                        double* __restrict__ W, double* __restrict__ V,
                                                        int check_degen, int* __restrict__ info) {
   extern __shared__ __align__(16) double a[];
   __shared__ double red[64];
-  const int ld = 2 * m + 1;
+  __shared__ double scratch[256];
+  const int npad = (m + 7) & ~7, ld = 2 * npad + 4;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  // coalesced load of S, then symmetrise in shared memory (linalg.py:70-73)
+  for (int t = tid; t < npad * npad; t += blockDim.x) {
+    const int i = t / npad, j = t - i * npad;
+    a[i * ld + j] = (i < m && j < m) ? S[i * m + j] : 0.0;
+    a[i * ld + npad + j] = (i == j && i < m) ? 1.0 : 0.0;
+  }
+  __syncthreads();
   double amax = 0.0, asym = 0.0;
-  for (int i = warp; i < m; i += nwarps) {
-    for (int j = lane; j < m; j += 32) {
-      const double sij = S[i * m + j], sji = S[j * m + i];
-      amax = fmax(amax, fabs(sij));
-      asym = fmax(asym, fabs(sij - sji));
-      a[i * ld + j] = 0.5 * (sij + sji);
-      a[i * ld + m + j] = (i == j) ? 1.0 : 0.0;
-    }
+  for (int t = tid; t < m * m; t += blockDim.x) {
+    const int i = t / m, j = t - i * m;
+    if (j < i) continue;
+    const double sij = a[i * ld + j], sji = a[j * ld + i];
+    amax = fmax(amax, fmax(fabs(sij), fabs(sji)));
+    asym = fmax(asym, fabs(sij - sji));
+    const double v = 0.5 * (sij + sji);
+    a[i * ld + j] = v;
+    a[j * ld + i] = v;
   }
   __syncthreads();
   chol_reduce_flags(amax, asym, red, info);
-  const int fail = chol_aug_smem(a, ld, m, m);
+  const int fail = chol8_aug_smem(a, ld, m, npad, scratch);
   if (fail) {
     if (tid == 0) info[TRALS_INFO_CHOL] = fail;
     return;
@@ -414,8 +550,8 @@ __global__ void __launch_bounds__(1024) chol_inv_kernel(const double* __restrict
     for (int j = lane; j < m; j += 32) {
       const double u = j >= i ? a[i * ld + j] : 0.0;
       U[i * m + j] = u;
-      V[i * m + j] = j <= i ? a[i * ld + m + j] : 0.0;
-      W[i * m + j] = j >= i ? a[j * ld + m + i] : 0.0;
+      V[i * m + j] = j <= i ? a[i * ld + npad + j] : 0.0;
+      W[i * m + j] = j >= i ? a[j * ld + npad + i] : 0.0;
       umax = fmax(umax, fabs(u));
       if (i == j && fabs(u) < dmin) { dmin = fabs(u); didx = i; }
     }
@@ -452,38 +588,65 @@ __global__ void __launch_bounds__(1024) chol_inv_kernel(const double* __restrict
 // ---------------------------------------------------------------------------
 constexpr int kBlkNB = 64;
 
-__global__ void __launch_bounds__(1024) chol_sym_kernel(const double* __restrict__ S, int m,
-                                                        double* __restrict__ U, int* __restrict__ info) {
-  __shared__ double red[64];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+// U = (S + S^T)/2 tile by tile (coalesced through a shared-memory transpose); the
+// largest |S| and |S - S^T| go to flags[0..1] as atomicMax on the (non-negative)
+// double bit patterns -- order-independent, so deterministic.
+__global__ void chol_sym_kernel(const double* __restrict__ S, int m, double* __restrict__ U,
+                                unsigned long long* __restrict__ flags) {
+  __shared__ double t1[32][33], t2[32][33];
+  const int bi = blockIdx.y * 32, bj = blockIdx.x * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+  for (int r = ty; r < 32; r += 8) {
+    t1[r][tx] = (bi + r < m && bj + tx < m) ? S[(bi + r) * m + bj + tx] : 0.0;  // S[bi+r][bj+tx]
+    t2[r][tx] = (bj + r < m && bi + tx < m) ? S[(bj + r) * m + bi + tx] : 0.0;  // S[bj+r][bi+tx]
+  }
+  __syncthreads();
   double amax = 0.0, asym = 0.0;
-  for (int i = warp; i < m; i += nwarps)
-    for (int j = lane; j < m; j += 32) {
-      const double sij = S[i * m + j], sji = S[j * m + i];
+  for (int r = ty; r < 32; r += 8) {
+    const int i = bi + r, j = bj + tx;
+    if (i < m && j < m) {
+      const double sij = t1[r][tx], sji = t2[tx][r];
       amax = fmax(amax, fabs(sij));
       asym = fmax(asym, fabs(sij - sji));
       U[i * m + j] = 0.5 * (sij + sji);
     }
-  chol_reduce_flags(amax, asym, red, info);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    asym = fmax(asym, __shfl_xor_sync(0xffffffffu, asym, o));
+  }
+  if (tx == 0) {
+    atomicMax(flags, static_cast<unsigned long long>(__double_as_longlong(amax)));
+    atomicMax(flags + 1, static_cast<unsigned long long>(__double_as_longlong(asym)));
+  }
 }
 
 // factor the pb x pb diagonal block at (p0, p0) of U in place; W = block^{-1}, WT = W^T (ld kBlkNB)
-__global__ void __launch_bounds__(1024) chol_diag_kernel(double* __restrict__ U, int m, int p0, int pb,
-                                                        double* __restrict__ W, double* __restrict__ WT,
-                                                        int* __restrict__ info) {
-  extern __shared__ __align__(16) double a[];  // [pb][2*kBlkNB + 1]
-  constexpr int ld = 2 * kBlkNB + 1;
+__global__ void __launch_bounds__(512) chol_diag_kernel(double* __restrict__ U, int m, int p0, int pb,
+                                                       double* __restrict__ W, double* __restrict__ WT,
+                                                       int* __restrict__ info,
+                                                       const unsigned long long* __restrict__ flags) {
+  extern __shared__ __align__(16) double a[];  // [kBlkNB][2*kBlkNB + 4]
+  constexpr int ld = 2 * kBlkNB + 4;
+  __shared__ double scratch[256];
   __shared__ int failed;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
-  if (tid == 0) failed = info[TRALS_INFO_CHOL];
-  for (int r = warp; r < pb; r += nwarps)
-    for (int c = lane; c < pb; c += 32) {
-      a[r * ld + c] = c >= r ? U[(p0 + r) * m + p0 + c] : 0.0;
-      a[r * ld + kBlkNB + c] = (r == c) ? 1.0 : 0.0;
+  if (tid == 0) {
+    failed = info[TRALS_INFO_CHOL];
+    if (p0 == 0) {  // symmetry check of linalg.py:70-72 from chol_sym_kernel's maxima
+      const double amax = __longlong_as_double(static_cast<long long>(flags[0]));
+      const double asym = __longlong_as_double(static_cast<long long>(flags[1]));
+      if (amax > 0 && asym > 1e-8 * amax) info[TRALS_INFO_ASYM] = 1;
+    }
+  }
+  for (int r = warp; r < kBlkNB; r += nwarps)
+    for (int c = lane; c < kBlkNB; c += 32) {
+      a[r * ld + c] = (r < pb && c < pb && c >= r) ? U[(p0 + r) * m + p0 + c] : 0.0;
+      a[r * ld + kBlkNB + c] = (r == c && r < pb) ? 1.0 : 0.0;
     }
   __syncthreads();
   if (failed) return;
-  const int f = chol_aug_smem(a, ld, pb, kBlkNB);
+  const int f = chol8_aug_smem(a, ld, pb, kBlkNB, scratch);
   if (f) {
     if (tid == 0) info[TRALS_INFO_CHOL] = p0 + f;
     return;
@@ -554,28 +717,33 @@ __global__ void __launch_bounds__(1024) degen_kernel(const double* __restrict__ 
   }
 }
 
-int64_t blocked_aux_elems(int m) {
+int64_t blocked_aux_elems(int m) {  // diagonal-block inverses + 2 flag words
   const int nblk = (m + kBlkNB - 1) / kBlkNB;
-  return static_cast<int64_t>(nblk) * 2 * kBlkNB * kBlkNB;
+  return static_cast<int64_t>(nblk) * 2 * kBlkNB * kBlkNB + 2;
 }
 
 int blocked_cholesky(const double* S, int m, double* U, double* L, double* aux, double* gws, int64_t gws_elems,
                      int check_degen, int* info, cudaStream_t s) {
-  chol_sym_kernel<<<1, 1024, 0, s>>>(S, m, U, info);
-  if (int st = launch_status()) return st;
+  unsigned long long* flags = reinterpret_cast<unsigned long long*>(aux + blocked_aux_elems(m) - 2);
+  if (cudaMemsetAsync(flags, 0, 2 * sizeof(unsigned long long), s) != cudaSuccess) return TRALS_ERR_CUDA;
+  {
+    dim3 grid((m + 31) / 32, (m + 31) / 32);
+    chol_sym_kernel<<<grid, dim3(32, 8), 0, s>>>(S, m, U, flags);
+    if (int st = launch_status()) return st;
+  }
   const CMap rm = rowmajor(m);
   for (int p0 = 0, b = 0; p0 < m; p0 += kBlkNB, ++b) {
     const int pb = std::min(kBlkNB, m - p0);
     const int rest = m - p0 - pb;
     double* W = aux + static_cast<int64_t>(b) * 2 * kBlkNB * kBlkNB;
     double* WT = W + kBlkNB * kBlkNB;
-    constexpr size_t kDiagSmem = sizeof(double) * kBlkNB * (2 * kBlkNB + 1);
+    constexpr size_t kDiagSmem = sizeof(double) * kBlkNB * (2 * kBlkNB + 4);
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(chol_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kDiagSmem);
       attr = true;
     }
-    chol_diag_kernel<<<1, 1024, kDiagSmem, s>>>(U, m, p0, pb, W, WT, info);
+    chol_diag_kernel<<<1, 512, kDiagSmem, s>>>(U, m, p0, pb, W, WT, info, flags);
     if (int st = launch_status()) return st;
     if (rest == 0) continue;
     double* U12 = U + static_cast<int64_t>(p0) * m + p0 + pb;
@@ -1191,13 +1359,14 @@ int trals_cholesky_f64(const double* S, int m, double* U, double* F, double* aux
     double* gws = aux + blocked_aux_elems(m);
     return blocked_cholesky(S, m, U, F, aux, gws, 4 * static_cast<int64_t>(m) * m, check_degen, info, s);
   }
-  const size_t smem = sizeof(double) * static_cast<size_t>(m) * (2 * m + 1);
+  const size_t npad = (m + 7) & ~7;
+  const size_t smem = sizeof(double) * npad * (2 * npad + 4);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     attr = true;
   }
-  chol_inv_kernel<<<1, 1024, smem, s>>>(S, m, U, F, aux, check_degen, info);
+  chol_inv_kernel<<<1, 512, smem, s>>>(S, m, U, F, aux, check_degen, info);
   return launch_status();
 }
 
