@@ -47,6 +47,7 @@ enum {
   TRALS_INFO_CHOL = 0,       /* 1-based index of first non-positive pivot */
   TRALS_INFO_ASYM = 1,       /* 1 if |S - S^T| > 1e-8 max|S| (linalg.py:70-72) */
   TRALS_INFO_DEGEN = 2,      /* 1-based index of diag <= 1e-13 max|R| (linalg.py:96-99) */
+  TRALS_INFO_FALLBACKS = 3,  /* number of fallback solves taken (AlsReport.fallback_count) */
   TRALS_INFO_SLOTS = 4
 };
 
@@ -145,6 +146,22 @@ int trals_cholesky_f64(const double* d_S, int m, double* d_U, double* d_F, doubl
 int64_t trals_chol_solve_ws_elems(int64_t rows, int m);
 int trals_chol_solve_f64(const double* d_U, const double* d_F, const double* d_aux, int m, const double* d_M,
                          int64_t rows, double* d_Z, double* d_ws, int64_t ws_elems, void* stream);
+
+/* Numerical fallback of spd_solve / solve_triangular_block, run right after
+ * trals_chol_solve_f64 on the same stream; it returns immediately unless its
+ * trigger flag is set.  mode 0 (NE/QRNE, linalg.py:77-81): on a Cholesky
+ * failure, Z = least-squares solution of Z sym = M with the rank cut at
+ * rcond * sigma_max (scipy lstsq gelsy with cond = eps: pass rcond = 2.22e-16).
+ * mode 1 (QR, solvers.py:262-273 + linalg.py:104-112): on a failed or
+ * degenerate R0 = chol(S), the min-norm solve with singular values of R0 cut at
+ * rcond * sigma_max(R0) (AlsConfig.svd_rcond).  mode 2: the reference's
+ * non-square R0 (prod_{j!=n} k_j < R^2, solvers.py:264-266): always that min-norm
+ * solve, not counted as a fallback.  All via a one-CTA one-sided
+ * Jacobi SVD of S.  When it fires it overwrites Z, clears the trigger flag and
+ * increments d_info[TRALS_INFO_FALLBACKS]. */
+int64_t trals_spd_fallback_ws_elems(int64_t rows, int m);
+int trals_spd_fallback_f64(const double* d_S, int m, const double* d_M, int64_t rows, double* d_Z, int* d_info,
+                           int mode, double rcond, double* d_ws, int64_t ws_elems, void* stream);
 
 /* Sum of squares of n doubles into d_out[0] (tensor_ops.py:237-239 norm) and the
  * number of non-finite entries into d_out[1] (validation.py:53-54). */

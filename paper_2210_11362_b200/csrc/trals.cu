@@ -947,6 +947,132 @@ int blocked_solve(const double* U, const double* L, const double* aux, int m, co
   return TRALS_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Numerical fallbacks (rare path, one CTA):
+//   NE / QRNE (linalg.py:77-81): Cholesky failed -> least-squares solve of
+//     Z sym = M with rank cut at eps * sigma_max (scipy lstsq gelsy, cond=eps);
+//   QR (solvers.py:262-273, linalg.py:104-112): R0 = chol(S) degenerate (or
+//     failed) and rank_deficient_fallback -> min-norm solve with singular values
+//     of R0 cut at rcond * sigma_max(R0), i.e. eigenvalues of S at rcond^2.
+// Both are Z = M pinv(S) with a relative cut; pinv(S) comes from a one-sided
+// (Hestenes) Jacobi SVD of S with round-robin parallel rotations.  The kernel
+// exits at once when its trigger flag is clear, so it sits in the sweep graph
+// unconditionally; when it fires it overwrites Z, clears the flag and bumps
+// d_info[TRALS_INFO_FALLBACKS] (report.fallback_count).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024) pinv_fallback_kernel(const double* __restrict__ S, int m,
+                                                             const double* __restrict__ Mr, int64_t rows,
+                                                             double* __restrict__ Z, int* __restrict__ info, int mode,
+                                                             double rcond, double* __restrict__ ws) {
+  const int tid = threadIdx.x, lane = tid & 31, nwarps = blockDim.x >> 5;
+  const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
+  const int trig_chol = info[TRALS_INFO_CHOL];
+  const int trig_degen = info[TRALS_INFO_DEGEN];
+  // mode 2: non-square R0 in the reference (prod_j k_j < R^2): always the SVD solve, not counted
+  const bool fire = (mode == 0) ? (trig_chol != 0) : (mode == 1 ? (trig_chol != 0 || trig_degen != 0) : true);
+  if (!fire) return;
+  const int m2 = (m + 1) & ~1;
+  double* A = ws;                          // [m2][m] columns of S (column-major), zero column if padded
+  double* V = A + static_cast<int64_t>(m2) * m;   // [m2][m2]
+  double* sig = V + static_cast<int64_t>(m2) * m2;  // [m2]
+  double* coef = sig + m2;                 // [rows][m2]
+  for (int t = tid; t < m2 * m; t += blockDim.x) {
+    const int c = t / m, r = t - c * m;
+    A[t] = (c < m) ? 0.5 * (S[r * m + c] + S[c * m + r]) : 0.0;
+  }
+  for (int t = tid; t < m2 * m2; t += blockDim.x) V[t] = ((t / m2) == (t % m2)) ? 1.0 : 0.0;
+  __syncthreads();
+  __shared__ int rotated;
+  const double eps = 2.220446049250313e-16;
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    if (tid == 0) rotated = 0;
+    __syncthreads();
+    for (int round = 0; round < m2 - 1; ++round) {
+      for (int k = warp; k < m2 / 2; k += nwarps) {
+        int i, j;
+        if (k == 0) { i = round % (m2 - 1); j = m2 - 1; }
+        else { i = (round + k) % (m2 - 1); j = (round - k + m2 - 1) % (m2 - 1); }
+        double* ai = A + static_cast<int64_t>(i) * m;
+        double* aj = A + static_cast<int64_t>(j) * m;
+        double al = 0.0, be = 0.0, ga = 0.0;
+        for (int r = lane; r < m; r += 32) {
+          const double x = ai[r], y = aj[r];
+          al = fma(x, x, al);
+          be = fma(y, y, be);
+          ga = fma(x, y, ga);
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+          al += __shfl_xor_sync(0xffffffffu, al, o);
+          be += __shfl_xor_sync(0xffffffffu, be, o);
+          ga += __shfl_xor_sync(0xffffffffu, ga, o);
+        }
+        if (fabs(ga) > eps * sqrt(al * be) && ga != 0.0) {
+          const double zeta = (be - al) / (2.0 * ga);
+          const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+          const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
+          for (int r = lane; r < m; r += 32) {
+            const double x = ai[r], y = aj[r];
+            ai[r] = c * x - s * y;
+            aj[r] = s * x + c * y;
+          }
+          double* vi = V + static_cast<int64_t>(i) * m2;
+          double* vj = V + static_cast<int64_t>(j) * m2;
+          for (int r = lane; r < m2; r += 32) {
+            const double x = vi[r], y = vj[r];
+            vi[r] = c * x - s * y;
+            vj[r] = s * x + c * y;
+          }
+          if (lane == 0) rotated = 1;
+        }
+      }
+      __syncthreads();
+    }
+    if (!rotated) break;
+    __syncthreads();
+  }
+  // singular values (= eigenvalues of the PSD part), relative cut
+  for (int c = warp; c < m2; c += nwarps) {
+    double s2 = 0.0;
+    for (int r = lane; r < m; r += 32) s2 = fma(A[c * m + r], A[c * m + r], s2);
+    for (int o = 16; o > 0; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    if (lane == 0) sig[c] = sqrt(s2);
+  }
+  __syncthreads();
+  __shared__ double smax;
+  if (tid == 0) {
+    double mx = 0.0;
+    for (int c = 0; c < m2; ++c) mx = fmax(mx, sig[c]);
+    smax = mx;
+  }
+  __syncthreads();
+  const double cut = (mode == 0 ? rcond : rcond * rcond) * smax;
+  // Z = M pinv(S) = sum_{sig_i > cut} (M a_i / sig_i^2) v_i^T
+  for (int t = tid; t < rows * m2; t += blockDim.x) {
+    const int64_t r = t / m2;
+    const int i = static_cast<int>(t - r * m2);
+    double v = 0.0;
+    if (sig[i] > cut) {
+      for (int k = 0; k < m; ++k) v = fma(Mr[r * m + k], A[static_cast<int64_t>(i) * m + k], v);
+      v /= sig[i] * sig[i];
+    }
+    coef[t] = v;
+  }
+  __syncthreads();
+  for (int64_t t = tid; t < rows * m; t += blockDim.x) {
+    const int64_t r = t / m;
+    const int c = static_cast<int>(t - r * m);
+    double v = 0.0;
+    for (int i = 0; i < m2; ++i) v = fma(coef[r * m2 + i], V[static_cast<int64_t>(i) * m2 + c], v);
+    Z[t] = v;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    info[TRALS_INFO_CHOL] = 0;
+    if (mode != 0) info[TRALS_INFO_DEGEN] = 0;
+    if (mode != 2) info[TRALS_INFO_FALLBACKS] += 1;
+  }
+}
+
 // C(m, n) = F[m * ncols + n] scattered through a CMap
 __global__ void reshuffle_kernel(const double* __restrict__ F, int64_t rows, int64_t cols, CMap cm,
                                  double* __restrict__ C) {
@@ -1455,6 +1581,19 @@ int trals_residual_f64(const double* X, int64_t pre, int64_t post, const double*
   int st = residual(HL, pre, K, HRt, post, X, ws, s);
   if (st) return st;
   residual_final_kernel<<<1, 1024, 0, s>>>(ws, static_cast<int>(residual_blocks(pre, post)), xnorm2, out);
+  return launch_status();
+}
+
+int64_t trals_spd_fallback_ws_elems(int64_t rows, int m) {
+  const int64_t m2 = (m + 1) & ~1;
+  return m2 * m + m2 * m2 + m2 + rows * m2;
+}
+
+int trals_spd_fallback_f64(const double* S, int m, const double* Mr, int64_t rows, double* Z, int* info, int mode,
+                           double rcond, double* ws, int64_t ws_elems, void* stream) {
+  if (!S || !Mr || !Z || !info || !ws || m < 1 || rows < 1 || mode < 0 || mode > 2) return TRALS_ERR_ARG;
+  if (ws_elems < trals_spd_fallback_ws_elems(rows, m)) return TRALS_ERR_WORKSPACE;
+  pinv_fallback_kernel<<<1, 1024, 0, static_cast<cudaStream_t>(stream)>>>(S, m, Mr, rows, Z, info, mode, rcond, ws);
   return launch_status();
 }
 

@@ -71,7 +71,8 @@ class SweepEngine:
     """Compiles and runs TR-ALS sweeps on one GPU (one rank of a sharded run)."""
 
     def __init__(self, x_local: torch.Tensor, dims, ranks, variant: str, *, shard_mode=None, lo=0, hi=None,
-                 group=None, world_size: int = 1, _test_lib=None):
+                 group=None, world_size: int = 1, rank_deficient_fallback=True, svd_rcond=1e-12,
+                 _test_lib=None):
         if variant not in ("ne", "qr", "qrne"):
             raise ValueError(f"unsupported device variant {variant!r}")
         # `_test_lib` lets the CPU test-suite drive this exact schedule through a numpy
@@ -97,6 +98,8 @@ class SweepEngine:
         if tuple(x_local.shape) != tuple(self.dl):
             raise ValueError(f"local slab shape {tuple(x_local.shape)} != expected {tuple(self.dl)}")
         self.x = x_local
+        self.fallback_ok = bool(rank_deficient_fallback)
+        self.svd_rcond = float(svd_rcond)
         self.stream = torch.cuda.current_stream(self.dev) if x_local.is_cuda else _HostStream()
         self.stats = EngineStats()
         self._alloc()
@@ -124,6 +127,8 @@ class SweepEngine:
                                               for n in range(N))))
         self.solve_ws = self._empty(max(1, max(self.lib.trals_chol_solve_ws_elems(self.dims[n], self.R(n) * self.R(n + 1))
                                               for n in range(N))))
+        self.fb_ws = self._empty(max(1, max(self.lib.trals_spd_fallback_ws_elems(self.dims[n], self.R(n) * self.R(n + 1))
+                                            for n in range(N))))
         self.info = torch.zeros(L.INFO_SLOTS, dtype=torch.int32, device=self.dev)
         self.xnorm2 = self._empty(2)  # [|X|^2, #non-finite]
         self.err_cur = self._empty(3)
@@ -382,6 +387,25 @@ class SweepEngine:
                                                   self.solve_ws.data_ptr(), self.solve_ws.numel(), self._sp()),
                     "chol_solve")
         self.steps.append(Step("solve", solve, f"solve{n}"))
+        # numerical fallbacks of the reference (linalg.py:77-81, solvers.py:262-273): the kernel is a
+        # no-op unless the factorisation flagged a failure, so it stays in the (graph-captured) sweep
+        rr_rows = self.dims[n]
+        if self.variant == "qr":
+            ks = 1
+            for j in range(N):
+                if j != n:
+                    ks *= min(self.dims[j], self.R(j) * self.R(j + 1))
+            mode = 2 if ks < rr else (1 if self.fallback_ok else None)
+            rcond = self.svd_rcond
+        else:
+            mode, rcond = 0, 2.220446049250313e-16
+        if mode is not None:
+            def fallback(n=n, M=M, rr=rr, mode=mode, rcond=rcond, rows=rr_rows):
+                L.check(self.lib.trals_spd_fallback_f64(self.S[n].data_ptr(), rr, M.data_ptr(), rows,
+                                                        self.Gt[n].data_ptr(), self.info.data_ptr(), mode, rcond,
+                                                        self.fb_ws.data_ptr(), self.fb_ws.numel(), self._sp()),
+                        "spd_fallback")
+            self.steps.append(Step("solve", fallback, f"fallback{n}"))
 
         def refresh(n=n):
             ra, i, rb = self.R(n), self.dims[n], self.R(n + 1)

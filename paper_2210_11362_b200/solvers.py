@@ -135,7 +135,8 @@ def _run(x, config, variant):
         lo, hi = _slab(dims[shard], world, rank)
         src = t.narrow(shard, lo, hi - lo)
     from .engine import SweepEngine
-    key = (dims, tuple(ranks), variant, dev.index, world, shard, lo, hi)
+    key = (dims, tuple(ranks), variant, dev.index, world, shard, lo, hi, bool(config.rank_deficient_fallback),
+           float(config.svd_rcond))
     eng = _PLAN_CACHE.pop(key, None)
     if eng is None:
         x_local = torch.empty(tuple(src.shape), dtype=torch.float64, device=dev)
@@ -149,7 +150,8 @@ def _run(x, config, variant):
         x_local.copy_(src, non_blocking=bool(src.is_pinned()))
     if eng is None:
         eng = SweepEngine(x_local, dims, ranks, variant, shard_mode=shard, lo=lo, hi=hi, group=group,
-                          world_size=world)
+                          world_size=world, rank_deficient_fallback=config.rank_deficient_fallback,
+                          svd_rcond=config.svd_rcond)
     eng.stream = torch.cuda.current_stream(dev)
     _PLAN_CACHE[key] = eng
     while len(_PLAN_CACHE) > _PLAN_CACHE_MAX:
@@ -236,20 +238,17 @@ def clear_plan_cache():
 
 
 def _raise_on_info(eng, config, report):
-    info = eng.info.cpu().numpy()
+    info = eng.info.cpu().numpy().copy()
     eng.info.zero_()
+    report.fallback_count = int(info[L.INFO_FALLBACKS])  # solvers.py:262-279
     if info[L.INFO_ASYM]:
         raise ValueError("matrix is not symmetric within 1e-8 relative")  # linalg.py:70-72
+    if info[L.INFO_DEGEN] or (config is not None and eng.variant == "qr" and info[L.INFO_CHOL]):
+        # only left set when rank_deficient_fallback is off (linalg.py:96-99, solvers.py:269-270)
+        idx = int(info[L.INFO_DEGEN] or info[L.INFO_CHOL]) - 1
+        raise DegenerateTriangularError(idx, 0.0, 0.0)
     if info[L.INFO_CHOL]:
-        # the reference falls back to a pivoted least-squares solve (linalg.py:77-81)
-        raise np.linalg.LinAlgError(
-            f"normal-equation matrix not positive definite at pivot {int(info[L.INFO_CHOL])}; "
-            "the device least-squares fallback is not available in this build")
-    if info[L.INFO_DEGEN]:
-        idx = int(info[L.INFO_DEGEN]) - 1
-        if not config.rank_deficient_fallback:
-            raise DegenerateTriangularError(idx, 0.0, 0.0)
-        raise np.linalg.LinAlgError("degenerate triangular factor; device SVD fallback not available in this build")
+        raise np.linalg.LinAlgError(f"Cholesky failed at pivot {int(info[L.INFO_CHOL])}")
 
 
 def _dist_context():

@@ -237,6 +237,30 @@ class FakeTrals:
         _arr(Z, rows * m)[:] = z.ravel()
         return 0
 
+    def trals_spd_fallback_ws_elems(self, rows, m):
+        return 1
+
+    def trals_spd_fallback_f64(self, S, m, M, rows, Z, info, mode, rcond, ws, ws_elems, stream):
+        self._count("fallback")
+        inf = _iarr(info, 4)
+        fire = inf[0] != 0 if mode == 0 else (inf[0] != 0 or inf[2] != 0 if mode == 1 else True)
+        if not fire:
+            return 0
+        s = _arr(S, m * m).reshape(m, m)
+        sym = 0.5 * (s + s.T)
+        rhs = _arr(M, rows * m).reshape(rows, m)
+        cut = rcond if mode == 0 else rcond * rcond
+        u, sig, vt = np.linalg.svd(sym)
+        keep = sig > cut * sig[0]
+        pinv = (vt[keep].T / sig[keep]) @ u[:, keep].T
+        _arr(Z, rows * m)[:] = (rhs @ pinv).ravel()
+        inf[0] = 0
+        if mode != 0:
+            inf[2] = 0
+        if mode != 2:
+            inf[3] += 1
+        return 0
+
     def trals_sumsq_f64(self, x, n, out, ws, stream):
         self._count("sumsq")
         v = _arr(x, n)

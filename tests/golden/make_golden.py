@@ -69,7 +69,7 @@ def small_cases():
                 if mode == "exact":
                     for j, g in enumerate(cores):
                         rec[f"{v}_core_{j}"] = g
-                    rec[f"{v}_fallbacks"] = rep.fallback_count
+                rec[f"{v}_{mode}_fallbacks"] = rep.fallback_count
             # per-sweep cores for one-sweep-from-state tests (chained 1-sweep runs == continuous)
             state = init
             for k in range(min(sweeps, 3)):
@@ -90,6 +90,8 @@ def small_cases():
     ring_case("n2_mat", (20, 30), (3, 3), (3, 2), 1e-2, 41, 42, 6, ("ne", "qr", "qrne"))
     # odd / prime sizes exercise every tail path of the kernels
     ring_case("odd_n3", (13, 7, 11), (2, 3, 2), (3, 2, 3), 1e-2, 51, 52, 5, ("ne", "qr"))
+    # rank-deficient blocks: prod_{j != n} I_j < R^2 -> gelsy fallback (NE/QRNE), SVD solve (QR)
+    ring_case("rankdef_n3", (2, 2, 30), (2, 2, 2), (3, 3, 3), 1e-2, 61, 62, 3, ("ne", "qr", "qrne"))
     return cases
 
 

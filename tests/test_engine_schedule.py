@@ -15,6 +15,7 @@ from fake_trals import FakeTrals
 from oracle import tenring_oracle as O
 
 SMALL = ["spec_n3_i30_r3", "nonuni_n4", "n5_i6", "n2_mat", "odd_n3"]
+RANKDEF = "rankdef_n3"
 
 
 @pytest.mark.parametrize("name", SMALL)
@@ -62,3 +63,18 @@ def test_schedule_one_sweep_vs_oracle(N, dims, ranks):
     np.testing.assert_allclose(errs, rep.errors, rtol=0, atol=1e-12)
     for j in range(N):
         assert rel(cores[j], ocores[j]) < 1e-9
+
+
+@pytest.mark.parametrize("variant", ["ne", "qr", "qrne"])
+def test_rank_deficient_fallback_schedule(variant):
+    """prod_{j!=n} I_j < R^2: the fallback step of the schedule fires and errors match the reference."""
+    g = load_golden(RANKDEF)
+    dims = tuple(int(d) for d in g["dims"])
+    N = len(dims)
+    ranks = [int(r) for r in g["ranks"]]
+    lib = FakeTrals()
+    _, errs, eng = run_engine(g["x"], ranks, variant, golden_cores(g, "init", N), int(g["sweeps"]), lib=lib,
+                              exact=True)
+    # the fit is exact: compare the exact errors (the cheap identity sits at its sqrt(eps) floor here)
+    np.testing.assert_allclose(errs, g[f"{variant}_exact_errors"], rtol=0, atol=1e-9)
+    assert lib.calls["fallback"] == N * int(g["sweeps"])

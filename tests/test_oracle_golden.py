@@ -9,7 +9,7 @@ import pytest
 from conftest import golden_cores, load_golden, rel
 from oracle import tenring_oracle as O
 
-SMALL = ["spec_n3_i30_r3", "nonuni_n4", "n5_i6", "n2_mat", "odd_n3"]
+SMALL = ["spec_n3_i30_r3", "nonuni_n4", "n5_i6", "n2_mat", "odd_n3", "rankdef_n3"]
 
 
 def test_spec_known_answers():
@@ -54,6 +54,7 @@ def test_solver_pins(name):
         for mode in ("exact", "cheap"):
             cores, rep = O.solve(g["x"], v, O.Config(ranks=ranks, max_iters=sweeps, init_cores=init, error_mode=mode))
             assert np.max(np.abs(np.array(rep.errors) - g[f"{v}_{mode}_errors"])) < 1e-12
+            assert rep.fallback_count == int(g[f"{v}_{mode}_fallbacks"])
             if mode == "exact":
                 for j in range(N):
                     assert rel(cores[j], g[f"{v}_core_{j}"]) < 1e-10
