@@ -1045,7 +1045,9 @@ __global__ void __launch_bounds__(1024) pinv_fallback_kernel(const double* __res
     smax = mx;
   }
   __syncthreads();
-  const double cut = (mode == 0 ? rcond : rcond * rcond) * smax;
+  // singular values of S below ~eps * sigma_max are rounding noise (they are the squares of R0's),
+  // so the R0-level cut rcond maps to max(rcond^2, eps) on S
+  const double cut = (mode == 0 ? rcond : fmax(rcond * rcond, eps)) * smax;
   // Z = M pinv(S) = sum_{sig_i > cut} (M a_i / sig_i^2) v_i^T
   for (int t = tid; t < rows * m2; t += blockDim.x) {
     const int64_t r = t / m2;
@@ -1066,10 +1068,10 @@ __global__ void __launch_bounds__(1024) pinv_fallback_kernel(const double* __res
     Z[t] = v;
   }
   __syncthreads();
-  if (tid == 0) {
+  if (tid == 0 && mode != 2) {  // mode 2 replaces the factorisation outright: no flags, not counted
     info[TRALS_INFO_CHOL] = 0;
-    if (mode != 0) info[TRALS_INFO_DEGEN] = 0;
-    if (mode != 2) info[TRALS_INFO_FALLBACKS] += 1;
+    if (mode == 1) info[TRALS_INFO_DEGEN] = 0;
+    info[TRALS_INFO_FALLBACKS] += 1;
   }
 }
 

@@ -346,6 +346,18 @@ class SweepEngine:
             cur, sa, sb = self._absorb_left(cur, sa, sb, leaf)
         self._tree(cur, m + 1, b)
 
+    def _r0_nonsquare(self, n):
+        """QR variant: the reference's R0 is non-square when prod_{j!=n} k_j < R_n R_{n+1}
+        (k_j = min(I_j, R_j R_{j+1}), ring.py:236-249) and it always takes the SVD solve
+        (solvers.py:264-266) -- no Cholesky, no fallback count."""
+        if self.variant != "qr":
+            return False
+        ks = 1
+        for j in range(self.N):
+            if j != n:
+                ks *= min(self.dims[j], self.R(j) * self.R(j + 1))
+        return ks < self.R(n) * self.R(n + 1)
+
     def _factor(self, n):
         """S_n from the Gram chain and its Cholesky factor -- depends on cores only, so it runs on
         the side stream as soon as core n-1 is final, overlapping the right-hand side of mode n."""
@@ -369,7 +381,8 @@ class SweepEngine:
             L.check(self.lib.trals_cholesky_f64(S.data_ptr(), rr, self.U.data_ptr(), self.Lo.data_ptr(),
                                                 self.chol_aux.data_ptr(), check_degen, self.info.data_ptr(),
                                                 self._sp()), "cholesky")
-        self.steps.append(Step("solve", factor, f"chol{n}", stream="side"))
+        if not self._r0_nonsquare(n):
+            self.steps.append(Step("solve", factor, f"chol{n}", stream="side"))
 
     def _solve(self, n):
         """Steps for one block update once M_n is complete (local rows)."""
@@ -386,16 +399,13 @@ class SweepEngine:
                                                   M.data_ptr(), self.dims[n], self.Gt[n].data_ptr(),
                                                   self.solve_ws.data_ptr(), self.solve_ws.numel(), self._sp()),
                     "chol_solve")
-        self.steps.append(Step("solve", solve, f"solve{n}"))
+        if not self._r0_nonsquare(n):
+            self.steps.append(Step("solve", solve, f"solve{n}"))
         # numerical fallbacks of the reference (linalg.py:77-81, solvers.py:262-273): the kernel is a
         # no-op unless the factorisation flagged a failure, so it stays in the (graph-captured) sweep
         rr_rows = self.dims[n]
         if self.variant == "qr":
-            ks = 1
-            for j in range(N):
-                if j != n:
-                    ks *= min(self.dims[j], self.R(j) * self.R(j + 1))
-            mode = 2 if ks < rr else (1 if self.fallback_ok else None)
+            mode = 2 if self._r0_nonsquare(n) else (1 if self.fallback_ok else None)
             rcond = self.svd_rcond
         else:
             mode, rcond = 0, 2.220446049250313e-16

@@ -249,15 +249,15 @@ class FakeTrals:
         s = _arr(S, m * m).reshape(m, m)
         sym = 0.5 * (s + s.T)
         rhs = _arr(M, rows * m).reshape(rows, m)
-        cut = rcond if mode == 0 else rcond * rcond
+        cut = rcond if mode == 0 else max(rcond * rcond, 2.220446049250313e-16)
         u, sig, vt = np.linalg.svd(sym)
         keep = sig > cut * sig[0]
         pinv = (vt[keep].T / sig[keep]) @ u[:, keep].T
         _arr(Z, rows * m)[:] = (rhs @ pinv).ravel()
-        inf[0] = 0
-        if mode != 0:
-            inf[2] = 0
         if mode != 2:
+            inf[0] = 0
+            if mode == 1:
+                inf[2] = 0
             inf[3] += 1
         return 0
 
