@@ -116,6 +116,16 @@ int trals_absorb_left_f64(const double* d_env, int Ra, int64_t Ia, int64_t rest,
 int trals_core_gram_f64(const double* d_core_slice, int Ra, int64_t I, int Rb, double* d_E,
                         double* d_ws, int64_t ws_elems, void* stream);
 
+/* Householder QR of a core's classical 2-unfolding (mode2_qr, ring.py:236-249;
+ * qr_economy sign convention, linalg.py:36-52): d_Gzt = the core in layout ZT
+ * viewed as an I x RR row-major matrix; writes R (k x RR, k = min(I, RR),
+ * nonnegative diagonal) -- the R-tensor of the QR / QRNE variants.  One CTA
+ * when the matrix fits shared memory, TSQR for tall, left-block + parallel Q^T
+ * application for wide matrices.  Returns TRALS_ERR_UNSUPPORTED when
+ * trals_core_qr_ws_elems is negative. */
+int64_t trals_core_qr_ws_elems(int I, int RR);
+int trals_core_qr_f64(const double* d_Gzt, int I, int RR, double* d_R, double* d_ws, int64_t ws_elems, void* stream);
+
 /* Coefficient Gram S_n = (G^{!=n}_[2])^T G^{!=n}_[2] from the chain of transfer
  * matrices (ring.py:191-214 gram_chain(_order), Prop. 3).  h_E[j] = transfer
  * matrix of core j; d_tmp holds two R^2 x R^2 buffers. */
@@ -156,7 +166,8 @@ int trals_chol_solve_f64(const double* d_U, const double* d_F, const double* d_a
  * degenerate R0 = chol(S), the min-norm solve with singular values of R0 cut at
  * rcond * sigma_max(R0) (AlsConfig.svd_rcond).  mode 2: the reference's
  * non-square R0 (prod_{j!=n} k_j < R^2, solvers.py:264-266): always that min-norm
- * solve, not counted as a fallback.  All via a one-CTA one-sided
+ * solve, not counted as a fallback.  Cuts never go below the Jacobi noise floor
+ * m * eps * sigma_max(S).  All via a one-CTA one-sided
  * Jacobi SVD of S.  When it fires it overwrites Z, clears the trigger flag and
  * increments d_info[TRALS_INFO_FALLBACKS]. */
 int64_t trals_spd_fallback_ws_elems(int64_t rows, int m);

@@ -39,6 +39,8 @@ _SIGNATURES = {
     "trals_absorb_left_f64": (c_int, [_dp, c_int, c_int64, c_int64, c_int, c_int, _dp, _dp, c_int, _dp,
                                       c_int64, c_void_p]),
     "trals_core_gram_f64": (c_int, [_dp, c_int, c_int64, c_int, _dp, _dp, c_int64, c_void_p]),
+    "trals_core_qr_ws_elems": (c_int64, [c_int, c_int]),
+    "trals_core_qr_f64": (c_int, [_dp, c_int, c_int, _dp, _dp, c_int64, c_void_p]),
     "trals_gram_chain_f64": (c_int, [c_int, c_int, POINTER(c_int32), POINTER(c_void_p), _dp, _dp, _dp,
                                      c_int64, c_void_p]),
     "trals_cholesky_aux_elems": (c_int64, [c_int]),

@@ -1045,9 +1045,11 @@ __global__ void __launch_bounds__(1024) pinv_fallback_kernel(const double* __res
     smax = mx;
   }
   __syncthreads();
-  // singular values of S below ~eps * sigma_max are rounding noise (they are the squares of R0's),
-  // so the R0-level cut rcond maps to max(rcond^2, eps) on S
-  const double cut = (mode == 0 ? rcond : fmax(rcond * rcond, eps)) * smax;
+  // singular values of S below ~m eps sigma_max are rounding noise of the Jacobi SVD (and, for the
+  // QR modes, squares of R0's), so the cut never goes below that noise floor: mode 0 (gelsy, cond = eps)
+  // uses max(rcond, m eps), modes 1/2 map R0's rcond to max(rcond^2, m eps) on S
+  const double floor_noise = m * eps;
+  const double cut = (mode == 0 ? fmax(rcond, floor_noise) : fmax(rcond * rcond, floor_noise)) * smax;
   // Z = M pinv(S) = sum_{sig_i > cut} (M a_i / sig_i^2) v_i^T
   for (int t = tid; t < rows * m2; t += blockDim.x) {
     const int64_t r = t / m2;
@@ -1073,6 +1075,279 @@ __global__ void __launch_bounds__(1024) pinv_fallback_kernel(const double* __res
     if (mode == 1) info[TRALS_INFO_DEGEN] = 0;
     info[TRALS_INFO_FALLBACKS] += 1;
   }
+}
+
+// ---------------------------------------------------------------------------
+// Per-core Householder QR of the classical 2-unfolding G_(2) (I x R R') for the
+// QR / QRNE variants (mode2_qr, ring.py:236-249 + qr_economy, linalg.py:36-52):
+// only R (k x RR, k = min(I, RR)) is needed -- the sweep never compresses X
+// (one right-hand side serves all variants), the R-tensor feeds the R-Grams.
+// LAPACK-style reflectors H = I - tau v v^T (v_0 = 1, beta = -sign(alpha)|x|),
+// then rows of R with a negative diagonal are negated (nonnegative diag, the
+// deterministic convention of qr_economy).
+//  * whole matrix fits shared memory: one CTA;
+//  * tall (I > RR) otherwise: TSQR -- row chunks factored by independent CTAs,
+//    their R factors stacked pairwise and re-factored up a binary tree;
+//  * wide (I < RR) otherwise: the I x I left block is factored in one CTA that
+//    also stores its reflectors, then column chunks of the rest are multiplied
+//    by Q^T in parallel CTAs.
+// ---------------------------------------------------------------------------
+constexpr int kHhThreads = 512;
+constexpr size_t kHhSmemMax = 216 * 1024;
+
+// In-place Householder on A (mr x nc, row pitch ld) in shared memory. Reflector j
+// is left in A[j+1.., j] with tau[j]; R in the upper triangle.
+__device__ void hh_factor_smem(double* A, int ld, int mr, int nc, double* tau, double* red) {
+  const int tid = threadIdx.x, lane = tid & 31, nwarps = blockDim.x >> 5;
+  const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
+  const int k = min(mr, nc);
+  for (int j = 0; j < k; ++j) {
+    // |x|^2 of the sub-column below the diagonal (fixed-order block reduction)
+    double s = 0.0;
+    for (int r = j + 1 + tid; r < mr; r += blockDim.x) s = fma(A[r * ld + j], A[r * ld + j], s);
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) red[warp] = s;
+    __syncthreads();
+    double sig = 0.0;
+    for (int w = 0; w < nwarps; ++w) sig += red[w];
+    const double alpha = A[j * ld + j];
+    double t = 0.0, scale = 0.0, beta = alpha;
+    if (sig > 0.0) {
+      const double nrm = sqrt(alpha * alpha + sig);
+      beta = alpha >= 0.0 ? -nrm : nrm;
+      t = (beta - alpha) / beta;
+      scale = 1.0 / (alpha - beta);
+    }
+    __syncthreads();  // everyone has alpha before it changes
+    if (tid == 0) {
+      tau[j] = t;
+      A[j * ld + j] = beta;
+    }
+    for (int r = j + 1 + tid; r < mr; r += blockDim.x) A[r * ld + j] *= scale;  // v (v_0 = 1 implicit)
+    __syncthreads();
+    if (t != 0.0) {
+      // columns c > j: w = v^T A[j:, c];  A[j:, c] -= t v w   (one warp per column)
+      for (int c = j + 1 + warp; c < nc; c += nwarps) {
+        double w = (lane == 0) ? A[j * ld + c] : 0.0;
+        for (int r = j + 1 + lane; r < mr; r += 32) w = fma(A[r * ld + j], A[r * ld + c], w);
+        for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+        const double tw = t * w;
+        if (lane == 0) A[j * ld + c] -= tw;
+        for (int r = j + 1 + lane; r < mr; r += 32) A[r * ld + c] = fma(-tw, A[r * ld + j], A[r * ld + c]);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// load rows [r0, r0+mr) x cols [0, nc) of a row-major global matrix (pitch gld) into smem (pitch ld)
+__device__ void hh_load(double* A, int ld, const double* G, int64_t gld, int r0, int mr, int nc) {
+  for (int t = threadIdx.x; t < mr * nc; t += blockDim.x) {
+    const int r = t / nc, c = t - r * nc;
+    A[r * ld + c] = G[(static_cast<int64_t>(r0) + r) * gld + c];
+  }
+}
+
+// write the upper part as R (row pitch nc, `rows_out` rows, zero below row min(mr, nc));
+// sign-normalise rows if `sign`
+__device__ void hh_store_r(const double* A, int ld, int mr, int nc, double* R, bool sign, int rows_out) {
+  const int k = min(mr, nc);
+  for (int t = threadIdx.x; t < rows_out * nc; t += blockDim.x) {
+    const int r = t / nc, c = t - r * nc;
+    if (r >= k) {
+      R[static_cast<int64_t>(r) * nc + c] = 0.0;
+      continue;
+    }
+    double v = c >= r ? A[r * ld + c] : 0.0;
+    if (sign && A[r * ld + r] < 0.0) v = -v;
+    R[static_cast<int64_t>(r) * nc + c] = v;
+  }
+}
+
+// one CTA: QR of rows [r0, r0+mr) of G (or of two stacked R blocks when G2 != nullptr)
+__global__ void __launch_bounds__(kHhThreads) hh_block_kernel(const double* __restrict__ G, int64_t gld, int mr, int nc,
+                                                              const double* __restrict__ G2, int mr2,
+                                                              double* __restrict__ R, int64_t rstride, int sign) {
+  extern __shared__ __align__(16) double A[];
+  __shared__ double red[32];
+  __shared__ double tau[512];
+  const int ld = nc + 1;
+  const int b = blockIdx.x;
+  int m_all;
+  if (G2 == nullptr) {
+    // chunk b of a tall matrix: rows [b*mr, min((b+1)*mr, total)) -- total passed through mr2
+    const int total = mr2;
+    const int r0 = b * mr, rows = min(mr, total - r0);
+    hh_load(A, ld, G, gld, r0, rows, nc);
+    m_all = rows;
+  } else {
+    // stack pair b: blocks 2b and 2b+1 of k x nc R factors (the last may be absent)
+    const int k = min(mr, nc);
+    const double* Ra = G + static_cast<int64_t>(2 * b) * rstride;
+    hh_load(A, ld, Ra, nc, 0, k, nc);
+    m_all = k;
+    if (2 * b + 1 < mr2) {
+      hh_load(A + k * ld, ld, Ra + rstride, nc, 0, k, nc);
+      m_all = 2 * k;
+    }
+  }
+  __syncthreads();
+  hh_factor_smem(A, ld, m_all, nc, tau, red);
+  // intermediate TSQR factors are zero-padded to nc rows so they stack uniformly
+  const int rows_out = sign ? min(m_all, nc) : nc;
+  hh_store_r(A, ld, m_all, nc, R + static_cast<int64_t>(b) * rstride, sign != 0, rows_out);
+}
+
+// wide: factor the left I x I block, keep its reflectors (V below the diagonal, tau) in global
+__global__ void __launch_bounds__(kHhThreads) hh_left_kernel(const double* __restrict__ G, int I, int nc,
+                                                             double* __restrict__ R, double* __restrict__ Vg,
+                                                             double* __restrict__ taug) {
+  extern __shared__ __align__(16) double A[];
+  __shared__ double red[32];
+  __shared__ double tau[512];
+  const int ld = I + 1;
+  for (int t = threadIdx.x; t < I * I; t += blockDim.x) {
+    const int r = t / I, c = t - r * I;
+    A[r * ld + c] = G[static_cast<int64_t>(r) * nc + c];
+  }
+  __syncthreads();
+  hh_factor_smem(A, ld, I, I, tau, red);
+  for (int t = threadIdx.x; t < I * I; t += blockDim.x) {
+    const int r = t / I, c = t - r * I;
+    const double v = A[r * ld + c];
+    Vg[t] = v;  // full: upper = R_left, strict lower = reflectors
+    const double sgn = A[r * ld + r] < 0.0 ? -1.0 : 1.0;
+    R[static_cast<int64_t>(r) * nc + c] = c >= r ? sgn * v : 0.0;
+  }
+  for (int t = threadIdx.x; t < I; t += blockDim.x) taug[t] = tau[t];
+}
+
+// wide: R[:, c0:c0+w] = Q^T G[:, c0:c0+w] for a column chunk (one CTA), sign-normalised by diag(R_left)
+__global__ void __launch_bounds__(kHhThreads) hh_apply_kernel(const double* __restrict__ G, int I, int nc,
+                                                              const double* __restrict__ Vg,
+                                                              const double* __restrict__ taug, int cw,
+                                                              double* __restrict__ R) {
+  extern __shared__ __align__(16) double A[];  // [I][cw + 1]
+  const int tid = threadIdx.x, lane = tid & 31, nwarps = blockDim.x >> 5;
+  const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
+  const int c0 = I + blockIdx.x * cw;
+  const int w = min(cw, nc - c0);
+  const int ld = cw + 1;
+  for (int t = tid; t < I * w; t += blockDim.x) {
+    const int r = t / w, c = t - r * w;
+    A[r * ld + c] = G[static_cast<int64_t>(r) * nc + c0 + c];
+  }
+  __syncthreads();
+  for (int j = 0; j < I; ++j) {
+    const double t = taug[j];
+    if (t != 0.0) {
+      for (int c = warp; c < w; c += nwarps) {
+        double s = (lane == 0) ? A[j * ld + c] : 0.0;
+        for (int r = j + 1 + lane; r < I; r += 32) s = fma(Vg[r * I + j], A[r * ld + c], s);
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        const double ts = t * s;
+        if (lane == 0) A[j * ld + c] -= ts;
+        for (int r = j + 1 + lane; r < I; r += 32) A[r * ld + c] = fma(-ts, Vg[r * I + j], A[r * ld + c]);
+      }
+    }
+    __syncthreads();
+  }
+  for (int t = tid; t < I * w; t += blockDim.x) {
+    const int r = t / w, c = t - r * w;
+    const double sgn = Vg[r * I + r] < 0.0 ? -1.0 : 1.0;
+    R[static_cast<int64_t>(r) * nc + c0 + c] = sgn * A[r * ld + c];
+  }
+}
+
+struct HhPlan {
+  int kind;     // 0 resident, 1 tsqr, 2 wide
+  int chunk;    // tsqr rows per leaf / wide column chunk
+  int leaves;
+  int64_t ws;   // doubles
+};
+
+HhPlan hh_plan(int I, int nc) {
+  HhPlan p{};
+  const size_t whole = sizeof(double) * static_cast<size_t>(I) * (nc + 1);
+  if (whole <= kHhSmemMax && I <= 4096) {
+    p.kind = 0;
+    return p;
+  }
+  if (I > nc) {
+    // rows per leaf such that a leaf and a stacked pair (2 nc rows) both fit
+    int chunk = static_cast<int>(kHhSmemMax / (sizeof(double) * (nc + 1)));
+    chunk = std::min(chunk, 4096);
+    p.kind = 1;
+    p.chunk = chunk;
+    p.leaves = (I + chunk - 1) / chunk;
+    p.ws = 2 * static_cast<int64_t>(p.leaves) * nc * nc;  // ping-pong R stacks
+    return p;
+  }
+  p.kind = 2;
+  int cw = static_cast<int>(kHhSmemMax / (sizeof(double) * I)) - 1;
+  cw = std::max(8, std::min(cw, 256));
+  p.chunk = cw;
+  p.ws = static_cast<int64_t>(I) * I + I;
+  return p;
+}
+
+bool hh_supported(int I, int nc) {
+  if (I > nc) return 2 * static_cast<size_t>(nc) * (nc + 1) * sizeof(double) <= kHhSmemMax && nc <= 512;
+  return static_cast<size_t>(I) * (I + 1) * sizeof(double) <= kHhSmemMax && I <= 512;
+}
+
+int hh_qr(const double* G, int I, int nc, double* R, double* ws, int64_t ws_elems, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(hh_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kHhSmemMax);
+    cudaFuncSetAttribute(hh_left_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kHhSmemMax);
+    cudaFuncSetAttribute(hh_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kHhSmemMax);
+    attr = true;
+  }
+  if (!hh_supported(I, nc)) return TRALS_ERR_UNSUPPORTED;
+  const HhPlan p = hh_plan(I, nc);
+  if (ws_elems < p.ws) return TRALS_ERR_WORKSPACE;
+  if (p.kind == 0) {
+    const size_t smem = sizeof(double) * static_cast<size_t>(I) * (nc + 1);
+    hh_block_kernel<<<1, kHhThreads, smem, s>>>(G, nc, I, nc, nullptr, I, R, 0, 1);
+    return launch_status();
+  }
+  if (p.kind == 1) {
+    // leaves -> k x nc factors (k = nc), then pairwise stacking up the tree
+    const int64_t rs = static_cast<int64_t>(nc) * nc;
+    double* cur = ws;
+    double* nxt = ws + static_cast<int64_t>(p.leaves) * rs;
+    {
+      const size_t smem = sizeof(double) * static_cast<size_t>(p.chunk) * (nc + 1);
+      hh_block_kernel<<<p.leaves, kHhThreads, smem, s>>>(G, nc, p.chunk, nc, nullptr, I, p.leaves == 1 ? R : cur, rs,
+                                                        p.leaves == 1 ? 1 : 0);
+      if (int st = launch_status()) return st;
+    }
+    int n = p.leaves;
+    while (n > 1) {
+      const int pairs = (n + 1) / 2;
+      const size_t smem = sizeof(double) * static_cast<size_t>(2 * nc) * (nc + 1);
+      const bool last = (pairs == 1);
+      hh_block_kernel<<<pairs, kHhThreads, smem, s>>>(cur, nc, nc, nc, cur, n, last ? R : nxt, rs, last ? 1 : 0);
+      if (int st = launch_status()) return st;
+      std::swap(cur, nxt);
+      n = pairs;
+    }
+    return TRALS_OK;
+  }
+  // wide
+  double* Vg = ws;
+  double* taug = ws + static_cast<int64_t>(I) * I;
+  hh_left_kernel<<<1, kHhThreads, sizeof(double) * static_cast<size_t>(I) * (I + 1), s>>>(G, I, nc, R, Vg, taug);
+  if (int st = launch_status()) return st;
+  const int rest = nc - I;
+  if (rest > 0) {
+    const int blocks = (rest + p.chunk - 1) / p.chunk;
+    hh_apply_kernel<<<blocks, kHhThreads, sizeof(double) * static_cast<size_t>(I) * (p.chunk + 1), s>>>(
+        G, I, nc, Vg, taug, p.chunk, R);
+    return launch_status();
+  }
+  return TRALS_OK;
 }
 
 // C(m, n) = F[m * ncols + n] scattered through a CMap
@@ -1597,6 +1872,13 @@ int trals_spd_fallback_f64(const double* S, int m, const double* Mr, int64_t row
   if (ws_elems < trals_spd_fallback_ws_elems(rows, m)) return TRALS_ERR_WORKSPACE;
   pinv_fallback_kernel<<<1, 1024, 0, static_cast<cudaStream_t>(stream)>>>(S, m, Mr, rows, Z, info, mode, rcond, ws);
   return launch_status();
+}
+
+int64_t trals_core_qr_ws_elems(int I, int RR) { return hh_supported(I, RR) ? hh_plan(I, RR).ws : -1; }
+
+int trals_core_qr_f64(const double* Gzt, int I, int RR, double* R, double* ws, int64_t ws_elems, void* stream) {
+  if (!Gzt || !R || I < 1 || RR < 1) return TRALS_ERR_ARG;
+  return hh_qr(Gzt, I, RR, R, ws, ws_elems, static_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

@@ -127,6 +127,16 @@ class SweepEngine:
                                               for n in range(N))))
         self.solve_ws = self._empty(max(1, max(self.lib.trals_chol_solve_ws_elems(self.dims[n], self.R(n) * self.R(n + 1))
                                               for n in range(N))))
+        self.use_rqr = self.variant in ("qr", "qrne")
+        if self.use_rqr:
+            ks = [min(self.dims[j], self.R(j) * self.R(j + 1)) for j in range(N)]
+            rrs = [self.R(j) * self.R(j + 1) for j in range(N)]
+            self.Rmat = self._empty(max(k * r for k, r in zip(ks, rrs)))
+            self.Rslice = self._empty(max(k * r for k, r in zip(ks, rrs)))
+            qws = [self.lib.trals_core_qr_ws_elems(self.dims[j], rrs[j]) for j in range(N)]
+            if min(qws) < 0:
+                raise ValueError("per-core QR size outside the kernel envelope")
+            self.qr_ws = self._empty(max(1, max(qws)))
         self.fb_ws = self._empty(max(1, max(self.lib.trals_spd_fallback_ws_elems(self.dims[n], self.R(n) * self.R(n + 1))
                                             for n in range(N))))
         self.info = torch.zeros(L.INFO_SLOTS, dtype=torch.int32, device=self.dev)
@@ -428,12 +438,27 @@ class SweepEngine:
                 L.check(self.lib.trals_core_relayout_f64(self.core_zt(n).data_ptr(), L.LAYOUT_ZT, ra,
                                                          self.hi - self.lo, rb, self.Gc_loc.data_ptr(),
                                                          L.LAYOUT_C, sp), "relayout")
-            L.check(self.lib.trals_core_gram_f64(self.Gs[n].data_ptr(), ra, i, rb, self.E[n].data_ptr(),
-                                                 self.gws.data_ptr(), self.gws.numel(), sp), "core_gram")
+            self._gram(n, sp)
         self._ws(self.lib.trals_gemm_ws_elems(1, rr, self.dims[n], rr))
         self.steps.append(Step("gramqr", refresh, f"refresh{n}"))
         if n + 1 < N:
             self._factor(n + 1)
+
+    def _gram(self, n, sp):
+        """Transfer matrix of core n: from the core itself (NE, ring.py:188) or, for QR/QRNE, from the
+        R-tensor of its Householder QR (mode2_qr + lateral_gram of the R-tensor, solvers.py:417,468-470)."""
+        ra, i, rb = self.R(n), self.dims[n], self.R(n + 1)
+        if not self.use_rqr:
+            L.check(self.lib.trals_core_gram_f64(self.Gs[n].data_ptr(), ra, i, rb, self.E[n].data_ptr(),
+                                                 self.gws.data_ptr(), self.gws.numel(), sp), "core_gram")
+            return
+        k = min(i, ra * rb)
+        L.check(self.lib.trals_core_qr_f64(self.Gt[n].data_ptr(), i, ra * rb, self.Rmat.data_ptr(),
+                                           self.qr_ws.data_ptr(), self.qr_ws.numel(), sp), "core_qr")
+        L.check(self.lib.trals_core_relayout_f64(self.Rmat.data_ptr(), L.LAYOUT_ZT, ra, k, rb,
+                                                 self.Rslice.data_ptr(), L.LAYOUT_SLICE, sp), "relayout")
+        L.check(self.lib.trals_core_gram_f64(self.Rslice.data_ptr(), ra, k, rb, self.E[n].data_ptr(),
+                                             self.gws.data_ptr(), self.gws.numel(), sp), "core_gram")
 
     # ----------------------------------------------------------------- running
     def _sp(self):
@@ -458,11 +483,7 @@ class SweepEngine:
             L.check(self.lib.trals_core_relayout_f64(self.core_zt(j).data_ptr(), L.LAYOUT_ZT, ra,
                                                      self.hi - self.lo, rb, self.Gc_loc.data_ptr(), L.LAYOUT_C,
                                                      sp), "relayout")
-        need = self.lib.trals_gemm_ws_elems(1, ra * rb, i, ra * rb)
-        if need > self.gws.numel():
-            self.gws = self._empty(need)
-        L.check(self.lib.trals_core_gram_f64(self.Gs[j].data_ptr(), ra, i, rb, self.E[j].data_ptr(),
-                                             self.gws.data_ptr(), self.gws.numel(), sp), "core_gram")
+        self._gram(j, sp)
 
     def compute_xnorm2(self):
         """Device [|X|^2, #non-finite entries] (all-reduced over ranks)."""

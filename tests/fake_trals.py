@@ -184,6 +184,19 @@ class FakeTrals:
         _arr(E, e.size)[:] = e.ravel()
         return 0
 
+    def trals_core_qr_ws_elems(self, I, RR):
+        return 1
+
+    def trals_core_qr_f64(self, Gzt, I, RR, R, ws, ws_elems, stream):
+        self._count("core_qr")
+        g = _arr(Gzt, I * RR).reshape(I, RR)
+        r = np.linalg.qr(g, mode="r")
+        sg = np.sign(np.diagonal(r)).copy()
+        sg[sg == 0] = 1.0
+        r = r * sg[:, None]
+        _arr(R, r.size)[:] = r.ravel()
+        return 0
+
     def trals_gram_chain_f64(self, N, n, ranks, E, S, tmp, ws, ws_elems, stream):
         self._count("gram_chain")
         r = _vals(ranks, N)
@@ -249,7 +262,8 @@ class FakeTrals:
         s = _arr(S, m * m).reshape(m, m)
         sym = 0.5 * (s + s.T)
         rhs = _arr(M, rows * m).reshape(rows, m)
-        cut = rcond if mode == 0 else max(rcond * rcond, 2.220446049250313e-16)
+        nf = m * 2.220446049250313e-16
+        cut = max(rcond, nf) if mode == 0 else max(rcond * rcond, nf)
         u, sig, vt = np.linalg.svd(sym)
         keep = sig > cut * sig[0]
         pinv = (vt[keep].T / sig[keep]) @ u[:, keep].T
