@@ -1215,7 +1215,9 @@ __global__ void __launch_bounds__(kHhThreads) hh_left_kernel(const double* __res
   for (int t = threadIdx.x; t < I * I; t += blockDim.x) {
     const int r = t / I, c = t - r * I;
     const double v = A[r * ld + c];
-    Vg[t] = v;  // full: upper = R_left, strict lower = reflectors
+    // transposed: row j of Vg = column j of the factored block (reflector j below the diagonal,
+    // R_left's column j above it) so the apply kernel streams reflectors contiguously
+    Vg[static_cast<int64_t>(c) * I + r] = v;
     const double sgn = A[r * ld + r] < 0.0 ? -1.0 : 1.0;
     R[static_cast<int64_t>(r) * nc + c] = c >= r ? sgn * v : 0.0;
   }
@@ -1243,18 +1245,19 @@ __global__ void __launch_bounds__(kHhThreads) hh_apply_kernel(const double* __re
     if (t != 0.0) {
       for (int c = warp; c < w; c += nwarps) {
         double s = (lane == 0) ? A[j * ld + c] : 0.0;
-        for (int r = j + 1 + lane; r < I; r += 32) s = fma(Vg[r * I + j], A[r * ld + c], s);
+        const double* vj = Vg + static_cast<int64_t>(j) * I;
+        for (int r = j + 1 + lane; r < I; r += 32) s = fma(vj[r], A[r * ld + c], s);
         for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
         const double ts = t * s;
         if (lane == 0) A[j * ld + c] -= ts;
-        for (int r = j + 1 + lane; r < I; r += 32) A[r * ld + c] = fma(-ts, Vg[r * I + j], A[r * ld + c]);
+        for (int r = j + 1 + lane; r < I; r += 32) A[r * ld + c] = fma(-ts, vj[r], A[r * ld + c]);
       }
     }
     __syncthreads();
   }
   for (int t = tid; t < I * w; t += blockDim.x) {
     const int r = t / w, c = t - r * w;
-    const double sgn = Vg[r * I + r] < 0.0 ? -1.0 : 1.0;
+    const double sgn = Vg[static_cast<int64_t>(r) * I + r] < 0.0 ? -1.0 : 1.0;
     R[static_cast<int64_t>(r) * nc + c0 + c] = sgn * A[r * ld + c];
   }
 }
