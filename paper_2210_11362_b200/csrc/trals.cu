@@ -7,11 +7,17 @@
 #include <cstdint>
 #include <vector>
 
+#include <cudaTypedefs.h>
+
+#include <cstdlib>
+
 #include "../../include/trals.h"
 #include "dmma_gemm.cuh"
+#include "dmma_tma_gemm.cuh"
 
 using trals::CMap;
 using trals::GemmArgs;
+using trals::kTmaBK;
 
 namespace {
 
@@ -209,6 +215,138 @@ int64_t gemm_ws(int64_t P, int64_t M, int64_t K, int64_t N) {
   const Cfg c = pick_cfg(N);
   const SplitPlan sp = plan_split(c, P, M, K, N);
   return sp.splits > 1 ? static_cast<int64_t>(sp.splits) * P * M * N : 0;
+}
+
+// ---------------------------------------------------------------------------
+// TMA-fed, warp-specialised DMMA GEMM for the X-streaming environment products
+// ---------------------------------------------------------------------------
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+bool make_map(CUtensorMap* map, const double* base, uint64_t inner, uint64_t outer, uint64_t row_stride_elems,
+              uint32_t box_inner, uint32_t box_outer, bool swizzle128) {
+  auto enc = tensor_map_encoder();
+  if (!enc) return false;
+  const cuuint64_t dims[2] = {inner, outer};
+  const cuuint64_t strides[1] = {row_stride_elems * sizeof(double)};
+  const cuuint32_t box[2] = {box_inner, box_outer};
+  const cuuint32_t estr[2] = {1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+bool tma_disabled() {
+  static int v = -1;
+  if (v < 0) v = std::getenv("TRALS_NO_TMA") ? 1 : 0;
+  return v == 1;
+}
+
+int tma_tn_for(int64_t N) {
+  // BN = 16 * TN in {32, 64, 80, 112}; least padding, then widest
+  const int tns[] = {2, 4, 5, 7};
+  int best = 5;
+  double bs = -1;
+  for (int tn : tns) {
+    const int64_t bn = 16 * tn, nt = (N + bn - 1) / bn;
+    const double sc = static_cast<double>(N) / static_cast<double>(nt * bn) + 0.002 * bn;
+    if (sc > bs + 1e-12) { bs = sc; best = tn; }
+  }
+  return best;
+}
+
+SplitPlan plan_split_tma(int tn, int64_t M, int64_t K, int64_t N) {
+  const int64_t BM = 128, BN = 16 * tn;
+  const int64_t tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
+  const int64_t slots = kSMs;  // one CTA per SM
+  const int64_t smax = std::max<int64_t>(1, std::min<int64_t>(64, K / (4 * kTmaBK)));
+  const double t_tile = 2.0 * BM * BN * static_cast<double>(K) / (37.0e12 / slots);
+  const double out_bytes = 8.0 * static_cast<double>(M) * N;
+  int64_t best_s = 1;
+  double best = 1e300;
+  for (int64_t sp = 1; sp <= smax; ++sp) {
+    const int64_t waves = (tiles * sp + slots - 1) / slots;
+    double cost = static_cast<double>(waves) / sp * t_tile;
+    if (sp > 1) cost += 3e-6 + (sp + 1) * out_bytes / 6.0e12;
+    if (cost < best * (1 - 1e-9)) { best = cost; best_s = sp; }
+  }
+  int64_t kchunk = (K + best_s - 1) / best_s;
+  kchunk = ((kchunk + kTmaBK - 1) / kTmaBK) * kTmaBK;
+  return {static_cast<int>(std::max<int64_t>(1, (K + kchunk - 1) / kchunk)), kchunk};
+}
+
+int64_t gemm_tma_ws(int64_t M, int64_t K, int64_t N) {
+  const SplitPlan sp = plan_split_tma(tma_tn_for(N), M, K, N);
+  return sp.splits > 1 ? static_cast<int64_t>(sp.splits) * M * N : 0;
+}
+
+template <int TN, bool AK>
+int launch_tma(const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& g, cudaStream_t s) {
+  using T = trals::TmaTile<TN>;
+  auto kern = trals::dmma_tma_kernel<TN, AK>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(T::SMEM));
+    attr = true;
+  }
+  dim3 grid(static_cast<unsigned>((g.N + T::BN - 1) / T::BN), static_cast<unsigned>((g.M + T::BM - 1) / T::BM),
+            static_cast<unsigned>(g.splits));
+  if (grid.x > 65535u || grid.y > 65535u) return TRALS_ERR_UNSUPPORTED;
+  kern<<<grid, T::THREADS, T::SMEM, s>>>(a, b, g);
+  return launch_status();
+}
+
+// Returns TRALS_ERR_UNSUPPORTED (nothing launched) when the TMA path does not apply.
+int gemm_tma(const double* A, int64_t sAm, int64_t sAk, int64_t M, int64_t K, int64_t N, const double* B, int64_t ldb,
+             double* C, const CMap& cm, double* ws, int64_t ws_elems, cudaStream_t s) {
+  if (tma_disabled() || !tensor_map_encoder()) return TRALS_ERR_UNSUPPORTED;
+  const bool ak = (sAk == 1);
+  const int64_t lead = ak ? sAm : sAk;
+  if ((reinterpret_cast<uintptr_t>(A) & 15u) || (reinterpret_cast<uintptr_t>(B) & 15u) || (lead & 1) || (ldb & 1))
+    return TRALS_ERR_UNSUPPORTED;
+  if (M > INT32_MAX || K > INT32_MAX || N > INT32_MAX || K < kTmaBK || M < 128) return TRALS_ERR_UNSUPPORTED;
+  const int tn = tma_tn_for(N);
+  SplitPlan sp = plan_split_tma(tn, M, K, N);
+  if (sp.splits > 1 && (!ws || static_cast<int64_t>(sp.splits) * M * N > ws_elems)) return TRALS_ERR_UNSUPPORTED;
+  CUtensorMap ma, mb;
+  bool ok = ak ? make_map(&ma, A, K, M, sAm, kTmaBK, 128, true) : make_map(&ma, A, M, K, sAk, 8, kTmaBK, false);
+  ok = ok && make_map(&mb, B, N, K, ldb, 8, kTmaBK, false);
+  if (!ok) return TRALS_ERR_UNSUPPORTED;
+  GemmArgs g{};
+  g.A = A; g.sAp = 0; g.sAm = sAm; g.sAk = sAk;
+  g.B = B; g.ldb = ldb; g.C = C; g.cmap = cm;
+  g.P = 1; g.M = M; g.K = K; g.N = N; g.beta = 0; g.alpha = 1.0;
+  g.kchunk = sp.kchunk; g.splits = sp.splits; g.ws = ws;
+  int st;
+  switch (tn * 2 + (ak ? 1 : 0)) {
+    case 5: st = launch_tma<2, true>(ma, mb, g, s); break;
+    case 4: st = launch_tma<2, false>(ma, mb, g, s); break;
+    case 9: st = launch_tma<4, true>(ma, mb, g, s); break;
+    case 8: st = launch_tma<4, false>(ma, mb, g, s); break;
+    case 11: st = launch_tma<5, true>(ma, mb, g, s); break;
+    case 10: st = launch_tma<5, false>(ma, mb, g, s); break;
+    case 15: st = launch_tma<7, true>(ma, mb, g, s); break;
+    default: st = launch_tma<7, false>(ma, mb, g, s); break;
+  }
+  if (st) return st;
+  if (sp.splits > 1) {
+    const int64_t total = M * N;
+    const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 8 * kSMs));
+    trals::splitk_reduce_kernel<<<blocks, 256, 0, s>>>(g);
+    return launch_status();
+  }
+  return TRALS_OK;
 }
 
 inline CMap rowmajor(int64_t ldc) { return CMap{0, 1 << 30, 0, ldc, 1 << 30, 0, 1}; }
@@ -1476,6 +1614,8 @@ int env(const double* X, int64_t pre, int64_t post, int side, const double* H, i
     CMap cm{0, pre, 0, r_lo, r_hi, 1, pre * r_lo};
     // single-mode segment [0]: write M_0[i_0][r_0 + R_0 r_1] (r_y = r_1)
     if (leaf) cm = CMap{0, pre, 0, RR, r_hi, r_hi, 1};
+    const int st = gemm_tma(X, post, 1, pre, post, RR, H, RR, E, cm, ws, ws_elems, s);
+    if (st != TRALS_ERR_UNSUPPORTED) return st;
     return gemm(X, 0, post, 1, 1, pre, post, RR, H, RR, E, cm, 0, ws, ws_elems, s);
   }
   // H over pre modes (0..x): H[k][r_0][r_{x+1}], r_lo = r_0, r_hi = r_{x+1}
@@ -1483,6 +1623,8 @@ int env(const double* X, int64_t pre, int64_t post, int side, const double* H, i
   CMap cm{0, post, 0, r_lo, r_hi, 1, post * r_lo};
   // single-mode segment [N-1]: M_{N-1}[i][r_{N-1} + R_{N-1} r_0] (r_{x+1} = r_{N-1})
   if (leaf) cm = CMap{0, post, 0, RR, r_hi, r_hi, 1};
+  const int st = gemm_tma(X, 1, post, post, pre, RR, H, RR, E, cm, ws, ws_elems, s);
+  if (st != TRALS_ERR_UNSUPPORTED) return st;
   return gemm(X, 0, 1, post, 1, post, pre, RR, H, RR, E, cm, 0, ws, ws_elems, s);
 }
 
@@ -1653,7 +1795,10 @@ int trals_version(void) { return 1; }
 
 long long trals_launch_count(void) { return g_launches; }
 
-int64_t trals_gemm_ws_elems(int64_t P, int64_t M, int64_t K, int64_t N) { return gemm_ws(P, M, K, N); }
+int64_t trals_gemm_ws_elems(int64_t P, int64_t M, int64_t K, int64_t N) {
+  // P == 1 shapes may take the TMA kernel (environment products): size for either plan
+  return P == 1 ? std::max(gemm_ws(P, M, K, N), gemm_tma_ws(M, K, N)) : gemm_ws(P, M, K, N);
+}
 
 int trals_gemm_f64(const double* A, int64_t sAp, int64_t sAm, int64_t sAk, int64_t P, int64_t M, int64_t K,
                    int64_t N, const double* B, int64_t ldb, double* C, const int64_t* h_cmap, int beta,
