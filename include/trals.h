@@ -96,6 +96,42 @@ int trals_env_f64(const double* d_X, int64_t pre, int64_t post, int side,
                   const double* d_H, int r_lo, int r_hi, double* d_env, int leaf,
                   double* d_ws, int64_t ws_elems, void* stream);
 
+/* ---- fp32 variant (AlsConfig.dtype = "float32"; BASELINE config 4) ----
+ * X is stored in fp32 and only the X-streaming environment product changes;
+ * cores, Grams, solves and errors stay fp64. */
+/* fp32 variant, product path: digit-sliced GEMM on the int8 tensor cores
+ * (tcgen05 kind::i8, exact int32 accumulation; tc_int8_gemm.cuh).  Each
+ * K-major row r of X is held as ex[r] and four int8 planes with
+ *   x = 2^ex[r] * sum_{s<4} d_s 2^(-7(s+1)),  |x| < 2^ex[r],
+ * digits [4][out_rows][ld] (plane stride out_rows * ld, ld = trals_oz_ld(K),
+ * a multiple of 16).  trals_oz_split_f32 slices x [rows][cols] row-major, or
+ * its transpose when transpose = 1 (out_rows = cols); ws holds out_rows doubles.
+ * trals_env_oz: trals_env_f64 with X given sliced, K-major for `side` (side 0:
+ * rows = pre, side 1: rows = post); the half chain is sliced per call. */
+int64_t trals_oz_ld(int64_t k);
+int64_t trals_oz_split_ws_elems(int64_t rows, int64_t cols, int transpose);
+int trals_oz_split_f32(const float* d_x, int64_t rows, int64_t cols, int transpose, int8_t* d_digits, int64_t ld,
+                       int32_t* d_exps, double* d_ws, int64_t ws_elems, void* stream);
+int64_t trals_env_oz_ws_elems(int64_t pre, int64_t post, int side, int r_lo, int r_hi);
+int trals_env_oz(const int8_t* d_xdigits, const int32_t* d_xexps, int64_t ldx, int64_t pre, int64_t post, int side,
+                 const double* d_H, int r_lo, int r_hi, double* d_env, int leaf, double* d_ws, int64_t ws_elems,
+                 void* stream);
+/* 3xTF32 alternative (an operator kept for comparison, not used by the
+ * solvers: its truncated fp32 accumulation biases M_n by ~1e-6 relative).
+ * X held as hi = tf32(x), lo = x - hi (fp32, hi + lo == x exactly);
+ * kind::tf32 MMAs hi*hi + hi*lo + lo*hi per k-step, fp64 split-K reduction.
+ * trals_tf32_ld: padded row length (floats, multiple of 4 = 16 B TMA stride).
+ * trals_tf32_split_f32: x [rows][ld_in] -> hi, lo as [rows][ld_out]
+ *   (transpose = 0) or [cols][ld_out] (transpose = 1).
+ * trals_env_tf32: side 0: hi/lo [pre][ldx] (X itself), side 1: [post][ldx] (X^T). */
+int64_t trals_tf32_ld(int64_t cols);
+int trals_tf32_split_f32(const float* d_x, int64_t rows, int64_t cols, int64_t ld_in, int transpose,
+                         float* d_hi, float* d_lo, int64_t ld_out, void* stream);
+int64_t trals_env_tf32_ws_elems(int64_t pre, int64_t post, int side, int r_lo, int r_hi);
+int trals_env_tf32(const float* d_xhi, const float* d_xlo, int64_t ldx, int64_t pre, int64_t post, int side,
+                   const double* d_H, int r_lo, int r_hi, double* d_env, int leaf, double* d_ws,
+                   int64_t ws_elems, void* stream);
+
 /* Absorb the rightmost / leftmost core of an environment segment.
  * Env layout [r_a][i_a .. i_b][r_{b+1}].
  *   right: Out[r_a][pre][r_b]       = sum E[r_a][pre][i_b][r_{b+1}] G_b[r_b,i_b,r_{b+1}]
@@ -178,6 +214,8 @@ int trals_spd_fallback_f64(const double* d_S, int m, const double* d_M, int64_t 
  * number of non-finite entries into d_out[1] (validation.py:53-54). */
 int64_t trals_sumsq_ws_elems(void);
 int trals_sumsq_f64(const double* d_x, int64_t n, double* d_out, double* d_ws, void* stream);
+/* Same for fp32 input (the fp32 variant's X), accumulated in fp64. */
+int trals_sumsq_f32(const float* d_x, int64_t n, double* d_out, double* d_ws, void* stream);
 
 /* Relative error from sweep intermediates (solvers.py:177-212):
  * d_out[0] = sqrt(max(0, |X|^2 - 2<M,Z> + <S, Z^T Z>)) / |X|,

@@ -14,6 +14,8 @@
 #include "../../include/trals.h"
 #include "dmma_gemm.cuh"
 #include "dmma_tma_gemm.cuh"
+#include "tc_tf32_gemm.cuh"
+#include "tc_int8_gemm.cuh"
 
 using trals::CMap;
 using trals::GemmArgs;
@@ -349,6 +351,239 @@ int gemm_tma(const double* A, int64_t sAm, int64_t sAk, int64_t M, int64_t K, in
   return TRALS_OK;
 }
 
+// ---------------------------------------------------------------------------
+// fp32 variant: tcgen05 3xTF32 GEMM (tc_tf32_gemm.cuh), both operands K-major
+// ---------------------------------------------------------------------------
+bool make_map_f32(CUtensorMap* map, const float* base, uint64_t inner, uint64_t outer, uint64_t ld,
+                  uint32_t box_inner, uint32_t box_outer) {
+  auto enc = tensor_map_encoder();
+  if (!enc) return false;
+  const cuuint64_t dims[2] = {inner, outer};
+  const cuuint64_t strides[1] = {ld * sizeof(float)};
+  const cuuint32_t box[2] = {box_inner, box_outer};
+  const cuuint32_t estr[2] = {1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+int tc_bn_for(int64_t N) { return N <= 64 ? 64 : (N <= 128 ? 128 : 256); }
+
+// split-K over a byte-bound cost model: the operands (hi + lo of the A rows,
+// B from L2) stream at the per-SM share of HBM bandwidth; one CTA per SM.
+SplitPlan plan_split_tc(int bn, int64_t M, int64_t K, int64_t N) {
+  const int64_t tiles = ((M + trals::kTcBM - 1) / trals::kTcBM) * ((N + bn - 1) / bn);
+  const int64_t slots = kSMs;
+  const int64_t smax = std::max<int64_t>(1, std::min<int64_t>(64, K / (4 * trals::kTcBK)));
+  const double t_tile = 8.0 * trals::kTcBM * static_cast<double>(K) / (6.5e12 / slots);
+  const double out_bytes = 8.0 * static_cast<double>(M) * N;
+  int64_t best_s = 1;
+  double best = 1e300;
+  for (int64_t sp = 1; sp <= smax; ++sp) {
+    const int64_t waves = (tiles * sp + slots - 1) / slots;
+    double cost = static_cast<double>(waves) / sp * t_tile;
+    if (sp > 1) cost += 3e-6 + (sp + 1) * out_bytes / 6.0e12;
+    if (cost < best * (1 - 1e-9)) { best = cost; best_s = sp; }
+  }
+  int64_t kchunk = (K + best_s - 1) / best_s;
+  kchunk = ((kchunk + trals::kTcBK - 1) / trals::kTcBK) * trals::kTcBK;
+  return {static_cast<int>(std::max<int64_t>(1, (K + kchunk - 1) / kchunk)), kchunk};
+}
+
+inline int64_t tf32_ld(int64_t cols) { return (cols + 3) / 4 * 4; }
+inline int64_t f32_in_f64(int64_t n) { return (n + 3) / 4 * 2; }  // doubles holding n floats, 16 B multiple
+
+template <int BN>
+int launch_tc(const CUtensorMap* m, const trals::TcArgs& g, cudaStream_t s) {
+  using T = trals::TcTile<BN>;
+  auto kern = trals::tc_tf32_kernel<BN>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(T::SMEM));
+    attr = true;
+  }
+  dim3 grid(static_cast<unsigned>((g.N + BN - 1) / BN), static_cast<unsigned>((g.M + trals::kTcBM - 1) / trals::kTcBM),
+            static_cast<unsigned>(g.splits));
+  if (grid.y > 65535u) return TRALS_ERR_UNSUPPORTED;
+  kern<<<grid, T::THREADS, T::SMEM, s>>>(m[0], m[1], m[2], m[3], g);
+  return launch_status();
+}
+
+int64_t gemm_tc_ws(int64_t M, int64_t K, int64_t N) {
+  const SplitPlan sp = plan_split_tc(tc_bn_for(N), M, K, N);
+  return 2 * f32_in_f64(N * tf32_ld(K)) + (sp.splits > 1 ? static_cast<int64_t>(sp.splits) * M * N : 0);
+}
+
+// C(m, n) = sum_k A[m][k] B[k][n]: A = (ahi + alo) fp32 [M][lda] K-contiguous, B fp64 [K][ldb]
+// (split + transposed into the workspace), C fp64 through cm.
+int gemm_tc(const float* ahi, const float* alo, int64_t lda, int64_t M, int64_t K, int64_t N, const double* B,
+            int64_t ldb, double* C, const CMap& cm, double* ws, int64_t ws_elems, cudaStream_t s) {
+  if (!tensor_map_encoder()) return TRALS_ERR_CUDA;
+  if ((reinterpret_cast<uintptr_t>(ahi) & 15u) || (reinterpret_cast<uintptr_t>(alo) & 15u) || (lda & 3) ||
+      lda < K || M > INT32_MAX || K > INT32_MAX || N > 65535LL * 256)
+    return TRALS_ERR_ARG;
+  if (gemm_tc_ws(M, K, N) > ws_elems || !ws) return TRALS_ERR_ARG;
+  const int bn = tc_bn_for(N);
+  const SplitPlan sp = plan_split_tc(bn, M, K, N);
+  const int64_t ldk = tf32_ld(K);
+  float* bhi = reinterpret_cast<float*>(ws);
+  float* blo = reinterpret_cast<float*>(ws + f32_in_f64(N * ldk));
+  double* part = ws + 2 * f32_in_f64(N * ldk);
+  {
+    const int64_t tiles = ((K + 31) / 32) * ((N + 31) / 32);
+    const int blocks = static_cast<int>(std::min<int64_t>(tiles, 16 * kSMs));
+    trals::tf32_split_kernel<double><<<blocks, 256, 0, s>>>(B, K, N, ldb, 1, bhi, blo, ldk);
+    if (int st = launch_status()) return st;
+  }
+  CUtensorMap maps[4];
+  bool ok = make_map_f32(&maps[0], ahi, K, M, lda, trals::kTcBK, trals::kTcBM) && make_map_f32(&maps[1], alo, K, M, lda, trals::kTcBK, trals::kTcBM);
+  ok = ok && make_map_f32(&maps[2], bhi, K, N, ldk, trals::kTcBK, bn) && make_map_f32(&maps[3], blo, K, N, ldk, trals::kTcBK, bn);
+  if (!ok) return TRALS_ERR_CUDA;
+  trals::TcArgs g{};
+  g.M = M; g.K = K; g.N = N; g.kchunk = sp.kchunk; g.splits = sp.splits;
+  g.cmap = cm; g.C = C; g.ws = part;
+  int st;
+  switch (bn) {
+    case 64: st = launch_tc<64>(maps, g, s); break;
+    case 128: st = launch_tc<128>(maps, g, s); break;
+    default: st = launch_tc<256>(maps, g, s); break;
+  }
+  if (st) return st;
+  if (sp.splits > 1) {
+    GemmArgs r{};
+    r.P = 1; r.M = M; r.N = N; r.splits = sp.splits; r.ws = part; r.C = C; r.cmap = cm; r.alpha = 1.0; r.beta = 0;
+    const int64_t total = M * N;
+    const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 8 * kSMs));
+    trals::splitk_reduce_kernel<<<blocks, 256, 0, s>>>(r);
+    return launch_status();
+  }
+  return TRALS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// fp32 variant: int8 tcgen05 digit-sliced GEMM (tc_int8_gemm.cuh)
+// ---------------------------------------------------------------------------
+bool make_map_i8(CUtensorMap* map, const int8_t* base, uint64_t inner, uint64_t outer, uint64_t ld,
+                 uint32_t box_outer) {
+  auto enc = tensor_map_encoder();
+  if (!enc) return false;
+  const cuuint64_t dims[2] = {inner, outer};
+  const cuuint64_t strides[1] = {ld};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(trals::kOzBK), box_outer};
+  const cuuint32_t estr[2] = {1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<int8_t*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+constexpr int kOzBN = 64;
+inline int64_t oz_ld(int64_t k) { return (k + 15) / 16 * 16; }
+
+// split-K: byte-bound model (4 digit bytes per A element at the per-SM HBM share),
+// and never more than kOzKmax k per CTA (int32 accumulator bound)
+SplitPlan plan_split_oz(int64_t M, int64_t K, int64_t N) {
+  const int64_t BK = trals::kOzBK;
+  const int64_t tiles = ((M + trals::kOzBM - 1) / trals::kOzBM) * ((N + kOzBN - 1) / kOzBN);
+  const int64_t slots = kSMs;
+  const int64_t smin = std::max<int64_t>(1, (K + trals::kOzKmax - 1) / trals::kOzKmax);
+  const int64_t smax = std::max<int64_t>(smin, std::min<int64_t>(64, K / (4 * BK)));
+  const double t_tile = 4.0 * trals::kOzBM * static_cast<double>(K) / (6.5e12 / slots);
+  const double out_bytes = 8.0 * static_cast<double>(M) * N;
+  int64_t best_s = smin;
+  double best = 1e300;
+  for (int64_t sp = smin; sp <= smax; ++sp) {
+    const int64_t waves = (tiles * sp + slots - 1) / slots;
+    double cost = static_cast<double>(waves) / sp * t_tile;
+    if (sp > 1) cost += 3e-6 + (sp + 1) * out_bytes / 6.0e12;
+    if (cost < best * (1 - 1e-9)) { best = cost; best_s = sp; }
+  }
+  int64_t kchunk = (K + best_s - 1) / best_s;
+  kchunk = ((kchunk + BK - 1) / BK) * BK;
+  return {static_cast<int>(std::max<int64_t>(1, (K + kchunk - 1) / kchunk)), kchunk};
+}
+
+// workspace (doubles): B digit planes (4 x N x ldk bytes), eb (N int32), B column max (N), partials
+struct OzWs {
+  int64_t planes, eb, mx, part, total;
+};
+OzWs oz_ws_layout(int64_t M, int64_t K, int64_t N) {
+  const SplitPlan sp = plan_split_oz(M, K, N);
+  OzWs w{};
+  w.planes = 0;
+  w.eb = w.planes + (4 * N * oz_ld(K) + 15) / 16 * 2;
+  w.mx = w.eb + (N + 3) / 4 * 2;
+  w.part = w.mx + (N + 1) / 2 * 2;
+  w.total = w.part + (sp.splits > 1 ? static_cast<int64_t>(sp.splits) * M * N : 0);
+  return w;
+}
+
+int64_t gemm_oz_ws(int64_t M, int64_t K, int64_t N) { return oz_ws_layout(M, K, N).total; }
+
+int launch_colmax_f64(const double* x, int64_t rows, int64_t cols, int64_t ld, double* out, cudaStream_t s) {
+  cudaMemsetAsync(out, 0, cols * sizeof(double), s);
+  const int64_t rpb = std::max<int64_t>(64, (rows + 255) / 256);
+  dim3 grid(static_cast<unsigned>((cols + 255) / 256), static_cast<unsigned>((rows + rpb - 1) / rpb));
+  trals::oz_colmax_kernel<double><<<grid, 256, 0, s>>>(x, rows, cols, ld, rpb, out);
+  return launch_status();
+}
+
+// C(m, n) = sum_k A[m][k] B[k][n]: A given as digit planes [4][M][lda] + row exponents ea[M],
+// B fp64 [K][ldb] (sliced per call into the workspace), C fp64 through cm.
+int gemm_oz(const int8_t* ad, const int32_t* ea, int64_t lda, int64_t M, int64_t K, int64_t N, const double* B,
+            int64_t ldb, double* C, const CMap& cm, double* ws, int64_t ws_elems, cudaStream_t s) {
+  if (!tensor_map_encoder()) return TRALS_ERR_CUDA;
+  if ((reinterpret_cast<uintptr_t>(ad) & 15u) || (lda & 15) || lda < K || M > INT32_MAX || K > INT32_MAX ||
+      N > 65535LL * kOzBN)
+    return TRALS_ERR_ARG;
+  const OzWs w = oz_ws_layout(M, K, N);
+  if (!ws || w.total > ws_elems) return TRALS_ERR_ARG;
+  const SplitPlan sp = plan_split_oz(M, K, N);
+  const int64_t ldk = oz_ld(K);
+  int8_t* bd = reinterpret_cast<int8_t*>(ws + w.planes);
+  int32_t* eb = reinterpret_cast<int32_t*>(ws + w.eb);
+  double* bmx = ws + w.mx;
+  // B^T rows = columns of B: max over k, then digits (transposed)
+  if (int st = launch_colmax_f64(B, K, N, ldb, bmx, s)) return st;
+  {
+    const int64_t tiles = ((K + 31) / 32) * ((N + 31) / 32);
+    const int blocks = static_cast<int>(std::min<int64_t>(tiles, 16 * kSMs));
+    trals::oz_digits_kernel<double><<<blocks, 256, 0, s>>>(B, K, N, ldb, 1, bmx, bd, ldk, eb);
+    if (int st = launch_status()) return st;
+  }
+  trals::OzMaps maps;
+  const int64_t pa = M * lda, pb = N * ldk;
+  for (int d = 0; d < trals::kOzDigits; ++d) {
+    if (!make_map_i8(&maps.a[d], ad + d * pa, K, M, lda, trals::kOzBM) ||
+        !make_map_i8(&maps.b[d], bd + d * pb, K, N, ldk, kOzBN))
+      return TRALS_ERR_CUDA;
+  }
+  trals::OzArgs g{};
+  g.M = M; g.K = K; g.N = N; g.kchunk = sp.kchunk; g.splits = sp.splits;
+  g.cmap = cm; g.ea = ea; g.eb = eb; g.C = C; g.ws = ws + w.part;
+  using T = trals::OzTile<kOzBN>;
+  auto kern = trals::oz8_kernel<kOzBN>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(T::SMEM));
+    attr = true;
+  }
+  dim3 grid(static_cast<unsigned>((N + kOzBN - 1) / kOzBN), static_cast<unsigned>((M + trals::kOzBM - 1) / trals::kOzBM),
+            static_cast<unsigned>(sp.splits));
+  if (grid.y > 65535u) return TRALS_ERR_UNSUPPORTED;
+  kern<<<grid, T::THREADS, T::SMEM, s>>>(maps, g);
+  if (int st = launch_status()) return st;
+  if (sp.splits > 1) {
+    GemmArgs r{};
+    r.P = 1; r.M = M; r.N = N; r.splits = sp.splits; r.ws = ws + w.part; r.C = C; r.cmap = cm; r.alpha = 1.0;
+    r.beta = 0;
+    const int64_t total = M * N;
+    const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 8 * kSMs));
+    trals::splitk_reduce_kernel<<<blocks, 256, 0, s>>>(r);
+    return launch_status();
+  }
+  return TRALS_OK;
+}
+
 inline CMap rowmajor(int64_t ldc) { return CMap{0, 1 << 30, 0, ldc, 1 << 30, 0, 1}; }
 
 // ---------------------------------------------------------------------------
@@ -402,13 +637,15 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
 }
 
 // partial sums of squares and of non-finite entries (the check of validation.py:53-54)
-__global__ void __launch_bounds__(512) sumsq_partial_kernel(const double* __restrict__ x, int64_t n,
+template <typename T>
+__global__ void __launch_bounds__(512) sumsq_partial_kernel(const T* __restrict__ x, int64_t n,
                                                             double* __restrict__ part) {
   __shared__ double red[16];
   double acc = 0.0, bad = 0.0;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if ((reinterpret_cast<uintptr_t>(x) & 15u) == 0) {
+  if (sizeof(T) == 8 && (reinterpret_cast<uintptr_t>(x) & 15u) == 0) {
+    const double* xd = reinterpret_cast<const double*>(x);
     const double2* x2 = reinterpret_cast<const double2*>(x);
     const int64_t n2 = n / 2;
     for (int64_t j = i; j < n2; j += stride) {
@@ -418,13 +655,14 @@ __global__ void __launch_bounds__(512) sumsq_partial_kernel(const double* __rest
       bad += (isfinite(v.x) ? 0.0 : 1.0) + (isfinite(v.y) ? 0.0 : 1.0);
     }
     if (i == 0 && (n & 1)) {
-      acc = fma(x[n - 1], x[n - 1], acc);
-      bad += isfinite(x[n - 1]) ? 0.0 : 1.0;
+      acc = fma(xd[n - 1], xd[n - 1], acc);
+      bad += isfinite(xd[n - 1]) ? 0.0 : 1.0;
     }
   } else {
     for (int64_t j = i; j < n; j += stride) {
-      acc = fma(x[j], x[j], acc);
-      bad += isfinite(x[j]) ? 0.0 : 1.0;
+      const double v = static_cast<double>(x[j]);
+      acc = fma(v, v, acc);
+      bad += isfinite(v) ? 0.0 : 1.0;
     }
   }
   const double s = block_sum<512>(acc, red);
@@ -1628,6 +1866,36 @@ int env(const double* X, int64_t pre, int64_t post, int side, const double* H, i
   return gemm(X, 0, 1, post, 1, post, pre, RR, H, RR, E, cm, 0, ws, ws_elems, s);
 }
 
+// fp32 variant of env(): X given as its tf32 hi/lo split, stored K-major for this side
+// (side 0: [pre][ldx] as X itself; side 1: [post][ldx], the transposed copy).
+int env_tf32(const float* xhi, const float* xlo, int64_t ldx, int64_t pre, int64_t post, int side, const double* H,
+             int r_lo, int r_hi, double* E, int leaf, double* ws, int64_t ws_elems, cudaStream_t s) {
+  const int64_t RR = static_cast<int64_t>(r_lo) * r_hi;
+  if (side == 0) {
+    CMap cm{0, pre, 0, r_lo, r_hi, 1, pre * r_lo};
+    if (leaf) cm = CMap{0, pre, 0, RR, r_hi, r_hi, 1};
+    return gemm_tc(xhi, xlo, ldx, pre, post, RR, H, RR, E, cm, ws, ws_elems, s);
+  }
+  CMap cm{0, post, 0, r_lo, r_hi, 1, post * r_lo};
+  if (leaf) cm = CMap{0, post, 0, RR, r_hi, r_hi, 1};
+  return gemm_tc(xhi, xlo, ldx, post, pre, RR, H, RR, E, cm, ws, ws_elems, s);
+}
+
+// fp32 variant of env() on the int8 tensor cores: X given as digit planes + row exponents,
+// K-major for this side (side 0: rows = pre, side 1: rows = post, the transposed copy).
+int env_oz(const int8_t* xd, const int32_t* xe, int64_t ldx, int64_t pre, int64_t post, int side, const double* H,
+           int r_lo, int r_hi, double* E, int leaf, double* ws, int64_t ws_elems, cudaStream_t s) {
+  const int64_t RR = static_cast<int64_t>(r_lo) * r_hi;
+  if (side == 0) {
+    CMap cm{0, pre, 0, r_lo, r_hi, 1, pre * r_lo};
+    if (leaf) cm = CMap{0, pre, 0, RR, r_hi, r_hi, 1};
+    return gemm_oz(xd, xe, ldx, pre, post, RR, H, RR, E, cm, ws, ws_elems, s);
+  }
+  CMap cm{0, post, 0, r_lo, r_hi, 1, post * r_lo};
+  if (leaf) cm = CMap{0, post, 0, RR, r_hi, r_hi, 1};
+  return gemm_oz(xd, xe, ldx, post, pre, RR, H, RR, E, cm, ws, ws_elems, s);
+}
+
 int absorb_right(const double* E, int Ra, int64_t pre, int64_t Ib, int Rb, int Rb1, const double* core_zt,
                  double* out, int leaf, double* ws, int64_t ws_elems, cudaStream_t s) {
   const int64_t M = static_cast<int64_t>(Ra) * pre, K = Ib * Rb1;
@@ -1838,6 +2106,77 @@ int trals_env_f64(const double* X, int64_t pre, int64_t post, int side, const do
   return env(X, pre, post, side, H, r_lo, r_hi, E, leaf, ws, ws_elems, static_cast<cudaStream_t>(stream));
 }
 
+int64_t trals_oz_ld(int64_t k) { return k < 1 ? 0 : oz_ld(k); }
+
+int64_t trals_oz_split_ws_elems(int64_t rows, int64_t cols, int transpose) { return transpose ? cols : rows; }
+
+int trals_oz_split_f32(const float* x, int64_t rows, int64_t cols, int transpose, int8_t* digits, int64_t ld,
+                       int32_t* exps, double* ws, int64_t ws_elems, void* stream) {
+  const int64_t out_rows = transpose ? cols : rows, out_cols = transpose ? rows : cols;
+  if (!x || !digits || !exps || !ws || rows < 1 || cols < 1 || (transpose != 0 && transpose != 1) ||
+      ld < out_cols || (ld & 15) || ws_elems < out_rows)
+    return TRALS_ERR_ARG;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (!transpose) {
+    const int blocks = static_cast<int>(std::min<int64_t>((rows + 7) / 8, 64 * kSMs));
+    trals::oz_rowmax_kernel<float><<<blocks, 256, 0, s>>>(x, rows, cols, cols, ws);
+  } else {
+    cudaMemsetAsync(ws, 0, cols * sizeof(double), s);
+    const int64_t rpb = std::max<int64_t>(64, (rows + 255) / 256);
+    dim3 grid(static_cast<unsigned>((cols + 255) / 256), static_cast<unsigned>((rows + rpb - 1) / rpb));
+    trals::oz_colmax_kernel<float><<<grid, 256, 0, s>>>(x, rows, cols, cols, rpb, ws);
+  }
+  if (int st = launch_status()) return st;
+  const int64_t tiles = ((rows + 31) / 32) * ((cols + 31) / 32);
+  const int blocks = static_cast<int>(std::min<int64_t>(tiles, 16 * kSMs));
+  trals::oz_digits_kernel<float><<<blocks, 256, 0, s>>>(x, rows, cols, cols, transpose, ws, digits, ld, exps);
+  return launch_status();
+}
+
+int64_t trals_env_oz_ws_elems(int64_t pre, int64_t post, int side, int r_lo, int r_hi) {
+  const int64_t RR = static_cast<int64_t>(r_lo) * r_hi;
+  return side == 0 ? gemm_oz_ws(pre, post, RR) : gemm_oz_ws(post, pre, RR);
+}
+
+int trals_env_oz(const int8_t* xd, const int32_t* xe, int64_t ldx, int64_t pre, int64_t post, int side,
+                 const double* H, int r_lo, int r_hi, double* E, int leaf, double* ws, int64_t ws_elems,
+                 void* stream) {
+  if (!xd || !xe || !H || !E || !ws || pre < 1 || post < 1 || r_lo < 1 || r_hi < 1 || (side != 0 && side != 1) ||
+      ldx < (side == 0 ? post : pre))
+    return TRALS_ERR_ARG;
+  return env_oz(xd, xe, ldx, pre, post, side, H, r_lo, r_hi, E, leaf, ws, ws_elems,
+                static_cast<cudaStream_t>(stream));
+}
+
+int64_t trals_tf32_ld(int64_t cols) { return cols < 1 ? 0 : tf32_ld(cols); }
+
+int trals_tf32_split_f32(const float* x, int64_t rows, int64_t cols, int64_t ld_in, int transpose, float* hi,
+                         float* lo, int64_t ld_out, void* stream) {
+  if (!x || !hi || !lo || rows < 1 || cols < 1 || ld_in < cols || (transpose != 0 && transpose != 1) ||
+      ld_out < (transpose ? rows : cols))
+    return TRALS_ERR_ARG;
+  const int64_t tiles = ((rows + 31) / 32) * ((cols + 31) / 32);
+  const int blocks = static_cast<int>(std::min<int64_t>(tiles, 16 * kSMs));
+  trals::tf32_split_kernel<float><<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(x, rows, cols, ld_in,
+                                                                                        transpose, hi, lo, ld_out);
+  return launch_status();
+}
+
+int64_t trals_env_tf32_ws_elems(int64_t pre, int64_t post, int side, int r_lo, int r_hi) {
+  const int64_t RR = static_cast<int64_t>(r_lo) * r_hi;
+  return side == 0 ? gemm_tc_ws(pre, post, RR) : gemm_tc_ws(post, pre, RR);
+}
+
+int trals_env_tf32(const float* xhi, const float* xlo, int64_t ldx, int64_t pre, int64_t post, int side,
+                   const double* H, int r_lo, int r_hi, double* E, int leaf, double* ws, int64_t ws_elems,
+                   void* stream) {
+  if (!xhi || !xlo || !H || !E || !ws || pre < 1 || post < 1 || r_lo < 1 || r_hi < 1 || (side != 0 && side != 1) ||
+      ldx < (side == 0 ? post : pre))
+    return TRALS_ERR_ARG;
+  return env_tf32(xhi, xlo, ldx, pre, post, side, H, r_lo, r_hi, E, leaf, ws, ws_elems,
+                  static_cast<cudaStream_t>(stream));
+}
+
 int trals_absorb_right_f64(const double* E, int Ra, int64_t pre, int64_t Ib, int Rb, int Rb1, const double* core_zt,
                            double* out, int leaf, double* ws, int64_t ws_elems, void* stream) {
   if (!E || !core_zt || !out || Ra < 1 || pre < 1 || Ib < 1 || Rb < 1 || Rb1 < 1) return TRALS_ERR_ARG;
@@ -1960,7 +2299,16 @@ int64_t trals_sumsq_ws_elems(void) { return 2 * kSumsqBlocks; }
 int trals_sumsq_f64(const double* x, int64_t n, double* out, double* ws, void* stream) {
   if (!x || !out || !ws || n < 0) return TRALS_ERR_ARG;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  sumsq_partial_kernel<<<kSumsqBlocks, 512, 0, s>>>(x, n, ws);
+  sumsq_partial_kernel<double><<<kSumsqBlocks, 512, 0, s>>>(x, n, ws);
+  ++g_launches;
+  sum_final_kernel<<<1, 1024, 0, s>>>(ws, kSumsqBlocks, out);
+  return launch_status();
+}
+
+int trals_sumsq_f32(const float* x, int64_t n, double* out, double* ws, void* stream) {
+  if (!x || !out || !ws || n < 0) return TRALS_ERR_ARG;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  sumsq_partial_kernel<float><<<kSumsqBlocks, 512, 0, s>>>(x, n, ws);
   ++g_launches;
   sum_final_kernel<<<1, 1024, 0, s>>>(ws, kSumsqBlocks, out);
   return launch_status();

@@ -79,8 +79,12 @@ class SweepEngine:
         # model of the C-ABI (tests/fake_trals.py); the solvers never pass it.
         if _test_lib is None and not x_local.is_cuda:
             raise TypeError("x_local must be a CUDA tensor")
-        if not (x_local.dtype == torch.float64 and x_local.is_contiguous()):
-            raise TypeError("x_local must be a contiguous float64 tensor")
+        if not (x_local.dtype in (torch.float64, torch.float32) and x_local.is_contiguous()):
+            raise TypeError("x_local must be a contiguous float64 or float32 tensor")
+        # fp32 variant: X stays fp32 and the environment products run on the int8
+        # tcgen05 tensor cores over X's digit slices (exact int32 accumulation);
+        # cores, Grams, solves and errors stay fp64.
+        self.fp32 = x_local.dtype == torch.float32
         self.lib = _test_lib if _test_lib is not None else L.lib()
         self.dev = x_local.device
         self.variant = variant
@@ -98,6 +102,8 @@ class SweepEngine:
         if tuple(x_local.shape) != tuple(self.dl):
             raise ValueError(f"local slab shape {tuple(x_local.shape)} != expected {tuple(self.dl)}")
         self.x = x_local
+        self._xsplit = {}   # fp32: (side, pre, post) -> (digits, exps, ld): X sliced K-major for that side
+        self._x64 = None    # fp32 + exact errors: fp64 copy of X for the residual kernel
         self.fallback_ok = bool(rank_deficient_fallback)
         self.svd_rcond = float(svd_rcond)
         self.stream = torch.cuda.current_stream(self.dev) if x_local.is_cuda else _HostStream()
@@ -270,9 +276,27 @@ class SweepEngine:
             self._bufs.append(E0)
             target = lambda E0=E0: E0.data_ptr()
 
-        def env_step(pre=pre, post=post, side=side, H=H, r_lo=r_lo, r_hi=r_hi, target=target, leaf=int(root_leaf)):
-            L.check(self.lib.trals_env_f64(self.x.data_ptr(), pre, post, side, H.data_ptr(), r_lo, r_hi, target(),
-                                           leaf, self.gws.data_ptr(), self.gws.numel(), self._sp()), "env")
+        if self.fp32:
+            key = (side, pre, post)
+            if key not in self._xsplit:
+                rows, k = (pre, post) if side == 0 else (post, pre)
+                ld = int(self.lib.trals_oz_ld(k))
+                self._xsplit[key] = (torch.empty(4 * rows * ld, dtype=torch.int8, device=self.dev),
+                                     torch.empty(rows, dtype=torch.int32, device=self.dev), ld)
+            self._ws(self.lib.trals_env_oz_ws_elems(pre, post, side, r_lo, r_hi))
+
+            def env_step(pre=pre, post=post, side=side, H=H, r_lo=r_lo, r_hi=r_hi, target=target,
+                         leaf=int(root_leaf), key=key):
+                xd, xe, ld = self._xsplit[key]
+                L.check(self.lib.trals_env_oz(xd.data_ptr(), xe.data_ptr(), ld, pre, post, side, H.data_ptr(),
+                                              r_lo, r_hi, target(), leaf, self.gws.data_ptr(), self.gws.numel(),
+                                              self._sp()), "env_oz")
+        else:
+            def env_step(pre=pre, post=post, side=side, H=H, r_lo=r_lo, r_hi=r_hi, target=target,
+                         leaf=int(root_leaf)):
+                L.check(self.lib.trals_env_f64(self.x.data_ptr(), pre, post, side, H.data_ptr(), r_lo, r_hi,
+                                               target(), leaf, self.gws.data_ptr(), self.gws.numel(), self._sp()),
+                        "env")
         self.steps.append(Step("mttsp", env_step, f"env[{seg_a}..{seg_b}]"))
         self.stats.x_passes_per_sweep += 1
         self._env_flops.append(2.0 * pre * post * RR)
@@ -485,10 +509,32 @@ class SweepEngine:
                                                      sp), "relayout")
         self._gram(j, sp)
 
+    def prepare_x(self):
+        """Derive the per-X state after X (self.x) was (re)loaded: for the fp32
+        variant, X's int8 digit planes + row exponents, K-major for each
+        X-streaming phase (phase L slices X as stored, phase R its transpose)."""
+        if not self.fp32:
+            return
+        sp = self._sp()
+        for (side, pre, post), (xd, xe, ld) in self._xsplit.items():
+            need = self.lib.trals_oz_split_ws_elems(pre, post, side)
+            ws = torch.empty(max(1, need), dtype=torch.float64, device=self.dev)
+            L.check(self.lib.trals_oz_split_f32(self.x.data_ptr(), pre, post, side, xd.data_ptr(), ld, xe.data_ptr(),
+                                                ws.data_ptr(), ws.numel(), sp), "oz_split")
+        if self._x64 is not None:
+            self._x64.copy_(self.x)
+
+    def ensure_x64(self):
+        """fp32 variant with exact errors: the residual kernel reads an fp64 copy of X
+        (made once per X, outside any graph capture; refreshed by prepare_x)."""
+        if self.fp32 and self._x64 is None:
+            self._x64 = self.x.to(torch.float64)
+
     def compute_xnorm2(self):
         """Device [|X|^2, #non-finite entries] (all-reduced over ranks)."""
-        L.check(self.lib.trals_sumsq_f64(self.x.data_ptr(), self.x.numel(), self.xnorm2.data_ptr(),
-                                         self.sumsq_ws.data_ptr(), self._sp()), "sumsq")
+        fn = self.lib.trals_sumsq_f32 if self.fp32 else self.lib.trals_sumsq_f64
+        L.check(fn(self.x.data_ptr(), self.x.numel(), self.xnorm2.data_ptr(), self.sumsq_ws.data_ptr(), self._sp()),
+                "sumsq")
         if self.world > 1:
             import torch.distributed as dist
             dist.all_reduce(self.xnorm2, group=self.group)
@@ -594,7 +640,10 @@ class SweepEngine:
             L.check(self.lib.trals_half_chain_f64(len(blk), bd, br, self.core_s(lo).data_ptr(), cc, H.data_ptr(),
                                                   xp["tmp"].data_ptr(), xp["ws"].data_ptr(), xp["ws"].numel(), tr, sp),
                     "half_chain")
-        L.check(self.lib.trals_residual_f64(self.x.data_ptr(), xp["pre"], xp["post"], xp["HL"].data_ptr(),
+        if self.fp32 and self._x64 is None:
+            self.ensure_x64()
+        xd = self._x64 if self.fp32 else self.x
+        L.check(self.lib.trals_residual_f64(xd.data_ptr(), xp["pre"], xp["post"], xp["HL"].data_ptr(),
                                             xp["HRt"].data_ptr(), xp["K"], self.xnorm2.data_ptr(), out.data_ptr(),
                                             xp["part"].data_ptr(), xp["part"].numel(), sp), "residual")
         if self.world > 1:

@@ -28,6 +28,7 @@ DEVICE_VARIANTS = ("ne", "qr", "qrne")
 ERROR_MODES = ("exact", "cheap", "none")         # solvers.py:56
 BUCKETS = ("subchain", "mttsp", "solve", "gramqr", "other")  # solvers.py:57
 SVD_RCOND_DEFAULT = 1e-12                        # linalg.py:20
+DTYPES = ("float64", "float32")                  # AlsConfig.dtype (extension)
 
 
 @dataclass
@@ -39,6 +40,12 @@ class AlsConfig:
     process per GPU); it is ignored for single-process runs.  The default 0 is
     BASELINE's "mode 1" in the paper's 1-based numbering; with it every rank's
     slab is a contiguous block of X.
+
+    `dtype` (extension) selects the storage/compute type of X's contractions:
+    "float64" (default, the reference's) or "float32" -- the fp32 variant of
+    BASELINE config 4: X is held in fp32 and the environment products run as
+    3xTF32 on the tcgen05 tensor cores, everything downstream in fp64; parity
+    with the fp64 reference is ~1e-4 instead of 1e-9.
     """
 
     ranks: tuple
@@ -53,6 +60,7 @@ class AlsConfig:
     debug_checks: bool = False
     shard_mode: int = 0
     timing_buckets: bool = True
+    dtype: str = "float64"
 
 
 @dataclass
@@ -86,20 +94,23 @@ def _validate(x, config, variant):
         raise ValueError("tol-based termination needs error tracking enabled")
     if config.max_iters < 1:
         raise ValueError("max_iters must be at least 1")
+    if config.dtype not in DTYPES:
+        raise ValueError(f"unknown dtype {config.dtype!r}; expected one of {DTYPES}")
 
 
-def _host_or_device_tensor(x):
+def _host_or_device_tensor(x, dtype="float64"):
     """Coerce the input like check_dense_tensor (validation.py:43-55) without a host pass over the data.
 
-    Returns a float64 torch tensor (host or device, possibly a view); the finite
-    check runs later on the device (sumsq kernel)."""
+    Returns a torch tensor of `dtype` (host or device, possibly a view); the
+    finite check runs later on the device (sumsq kernel)."""
     import torch
+    td = torch.float64 if dtype == "float64" else torch.float32
     if isinstance(x, torch.Tensor):
         t = x.detach()
-        if t.dtype != torch.float64:
-            t = t.to(torch.float64)
+        if t.dtype != td:
+            t = t.to(td)
     else:
-        t = torch.from_numpy(np.asarray(x, dtype=np.float64))
+        t = torch.from_numpy(np.asarray(x, dtype=np.float64 if dtype == "float64" else np.float32))
     if t.dim() < 2:
         raise ValueError(f"tensor order {t.dim()} is below the minimum 2")
     if t.numel() == 0:
@@ -113,7 +124,7 @@ def _run(x, config, variant):
     _validate(x, config, variant)
     if variant not in DEVICE_VARIANTS:
         raise NotImplementedError("tr_als (Alg. 1) is outside the B200 hot path; use ne/qr/qrne")
-    t = _host_or_device_tensor(x)
+    t = _host_or_device_tensor(x, config.dtype)
     dims = tuple(int(d) for d in t.shape)
     N = len(dims)
     ranks = check_ranks(config.ranks, N)
@@ -136,10 +147,10 @@ def _run(x, config, variant):
         src = t.narrow(shard, lo, hi - lo)
     from .engine import SweepEngine
     key = (dims, tuple(ranks), variant, dev.index, world, shard, lo, hi, bool(config.rank_deficient_fallback),
-           float(config.svd_rcond))
+           float(config.svd_rcond), config.dtype)
     eng = _PLAN_CACHE.pop(key, None)
     if eng is None:
-        x_local = torch.empty(tuple(src.shape), dtype=torch.float64, device=dev)
+        x_local = torch.empty(tuple(src.shape), dtype=t.dtype, device=dev)
     else:
         x_local = eng.x
     if src.is_cuda:
@@ -153,6 +164,9 @@ def _run(x, config, variant):
                           world_size=world, rank_deficient_fallback=config.rank_deficient_fallback,
                           svd_rcond=config.svd_rcond)
     eng.stream = torch.cuda.current_stream(dev)
+    eng.prepare_x()
+    if config.error_mode == "exact":
+        eng.ensure_x64()
     _PLAN_CACHE[key] = eng
     while len(_PLAN_CACHE) > _PLAN_CACHE_MAX:
         _PLAN_CACHE.pop(next(iter(_PLAN_CACHE)))

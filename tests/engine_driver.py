@@ -7,8 +7,8 @@ from paper_2210_11362_b200.engine import SweepEngine
 
 
 def run_engine(x, ranks, variant, init_cores, sweeps, lib=None, device="cpu", shard_mode=None, lo=0, hi=None,
-               world=1, group=None, exact=False):
-    x = np.asarray(x, dtype=np.float64)
+               world=1, group=None, exact=False, dtype=np.float64):
+    x = np.asarray(x, dtype=dtype)
     dims = x.shape
     if shard_mode is not None and world > 1:
         idx = [slice(None)] * x.ndim
@@ -20,6 +20,7 @@ def run_engine(x, ranks, variant, init_cores, sweeps, lib=None, device="cpu", sh
     xt = torch.from_numpy(xl).to(device)
     eng = SweepEngine(xt, dims, ranks, variant, shard_mode=shard_mode, lo=lo, hi=hi, world_size=world, group=group,
                       _test_lib=lib)
+    eng.prepare_x()
     eng.compute_xnorm2()
     eng.set_cores(init_cores)
     errs = []

@@ -22,6 +22,11 @@ def _arr(ptr, n):
     return np.ctypeslib.as_array((ctypes.c_double * int(n)).from_address(ptr))
 
 
+def _farr(ptr, n):
+    ptr = int(ptr.value if isinstance(ptr, ctypes.c_void_p) else ptr)
+    return np.ctypeslib.as_array((ctypes.c_float * int(n)).from_address(ptr))
+
+
 def _iarr(ptr, n):
     ptr = int(ptr.value if isinstance(ptr, ctypes.c_void_p) else ptr)
     return np.ctypeslib.as_array((ctypes.c_int32 * int(n)).from_address(ptr))
@@ -135,6 +140,82 @@ class FakeTrals:
         o = _arr(out, 3)
         o[1] = ssr
         o[0] = 0.0 if x2 == 0 else np.sqrt(ssr / x2)
+        return 0
+
+    # --- fp32 variant: the 3xTF32 split and the K-major environment product ---
+    def trals_tf32_ld(self, cols):
+        return (int(cols) + 3) // 4 * 4
+
+    def trals_tf32_split_f32(self, x, rows, cols, ld_in, transpose, hi, lo, ld_out, stream):
+        self._count("tf32_split")
+        v = _farr(x, rows * ld_in).reshape(rows, ld_in)[:, :cols]
+        h = (v.view(np.uint32) & np.uint32(0xFFFFE000)).view(np.float32)
+        l = v - h
+        if transpose:
+            h, l = h.T, l.T
+        r, c = h.shape
+        _farr(hi, r * ld_out).reshape(r, ld_out)[:, :c] = h
+        _farr(lo, r * ld_out).reshape(r, ld_out)[:, :c] = l
+        return 0
+
+    # int8 digit slicing (Ozaki-style) of the fp32 variant's product path
+    def trals_oz_ld(self, k):
+        return (int(k) + 15) // 16 * 16
+
+    def trals_oz_split_ws_elems(self, rows, cols, transpose):
+        return cols if transpose else rows
+
+    def trals_oz_split_f32(self, x, rows, cols, transpose, digits, ld, exps, ws, ws_elems, stream):
+        self._count("oz_split")
+        v = _farr(x, rows * cols).reshape(rows, cols).astype(np.float64)
+        if transpose:
+            v = v.T
+        r, c = v.shape
+        mx = np.max(np.abs(v), axis=1)
+        e = np.where(mx > 0, np.frexp(mx)[1], 0).astype(np.int32)   # |x| < 2^e
+        v = np.ldexp(v, -e[:, None])
+        ptr = int(digits.value if isinstance(digits, ctypes.c_void_p) else digits)
+        planes = np.ctypeslib.as_array((ctypes.c_int8 * (4 * r * ld)).from_address(ptr)).reshape(4, r, ld)
+        for s in range(4):
+            t = v * 128.0
+            q = np.trunc(t)
+            planes[s, :, :c] = q.astype(np.int8)
+            v = t - q
+        eptr = int(exps.value if isinstance(exps, ctypes.c_void_p) else exps)
+        np.ctypeslib.as_array((ctypes.c_int32 * r).from_address(eptr))[:] = e
+        return 0
+
+    def trals_env_oz_ws_elems(self, pre, post, side, r_lo, r_hi):
+        return 1
+
+    def trals_env_oz(self, xd, xe, ldx, pre, post, side, H, r_lo, r_hi, E, leaf, ws, ws_elems, stream):
+        rows, k = (pre, post) if side == 0 else (post, pre)
+        ptr = int(xd.value if isinstance(xd, ctypes.c_void_p) else xd)
+        planes = np.ctypeslib.as_array((ctypes.c_int8 * (4 * rows * ldx)).from_address(ptr)).reshape(4, rows, ldx)
+        eptr = int(xe.value if isinstance(xe, ctypes.c_void_p) else xe)
+        e = np.ctypeslib.as_array((ctypes.c_int32 * rows).from_address(eptr)).astype(np.int64)
+        a = sum(planes[s, :, :k].astype(np.float64) * 2.0 ** (-7 * (s + 1)) for s in range(4))
+        a = np.ldexp(a, e[:, None])
+        x = np.ascontiguousarray(a if side == 0 else a.T)
+        return self.trals_env_f64(x.ctypes.data, pre, post, side, H, r_lo, r_hi, E, leaf, ws, ws_elems, stream)
+
+    def trals_env_tf32_ws_elems(self, pre, post, side, r_lo, r_hi):
+        return 1
+
+    def trals_env_tf32(self, xhi, xlo, ldx, pre, post, side, H, r_lo, r_hi, E, leaf, ws, ws_elems, stream):
+        rows, k = (pre, post) if side == 0 else (post, pre)
+        a = (_farr(xhi, rows * ldx).reshape(rows, ldx)[:, :k].astype(np.float64)
+             + _farr(xlo, rows * ldx).reshape(rows, ldx)[:, :k].astype(np.float64))
+        x = a if side == 0 else a.T
+        x = np.ascontiguousarray(x)
+        return self.trals_env_f64(x.ctypes.data, pre, post, side, H, r_lo, r_hi, E, leaf, ws, ws_elems, stream)
+
+    def trals_sumsq_f32(self, x, n, out, ws, stream):
+        self._count("sumsq")
+        v = _farr(x, n).astype(np.float64)
+        o = _arr(out, 2)
+        o[0] = float(np.dot(v, v))
+        o[1] = float(np.count_nonzero(~np.isfinite(v)))
         return 0
 
     def trals_env_f64(self, X, pre, post, side, H, r_lo, r_hi, E, leaf, ws, ws_elems, stream):

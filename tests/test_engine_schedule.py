@@ -37,6 +37,26 @@ def test_schedule_matches_reference_sweeps(name):
 
 
 @pytest.mark.parametrize("name", SMALL)
+@pytest.mark.parametrize("exact", [False, True])
+def test_fp32_schedule_matches_reference(name, exact):
+    """fp32 variant: X held in fp32, sliced into int8 digit planes K-major per phase
+    (the phase-R copy transposed); the numpy model rebuilds X from the digits, so
+    this pins the slicing/transpose bookkeeping and the 1e-4 contract against
+    the fp64 goldens."""
+    g = load_golden(name)
+    dims = tuple(int(d) for d in g["dims"])
+    N = len(dims)
+    ranks = [int(r) for r in g["ranks"]]
+    lib = FakeTrals()
+    cores, errs, eng = run_engine(g["x"], ranks, "ne", golden_cores(g, "init", N), int(g["sweeps"]), lib=lib,
+                                  exact=exact, dtype=np.float32)
+    assert eng.fp32 and lib.calls["oz_split"] == len(eng._xsplit) == 2
+    np.testing.assert_allclose(errs, g["ne_exact_errors" if exact else "ne_cheap_errors"], rtol=0, atol=1e-4)
+    for j in range(N):
+        assert rel(cores[j], g[f"ne_core_{j}"]) < 1e-4
+
+
+@pytest.mark.parametrize("name", SMALL)
 def test_exact_error_matches_reference(name):
     g = load_golden(name)
     dims = tuple(int(d) for d in g["dims"])

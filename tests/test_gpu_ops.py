@@ -164,3 +164,84 @@ def test_reconstruct_and_exact_residual(dims, ranks):
     # after one sweep the cores changed: compare with the oracle's exact error for those cores
     ocores, orep = O.solve(x, "ne", O.Config(ranks=ranks, max_iters=1, init_cores=cores, error_mode="exact"))
     assert abs(errs[0] - orep.errors[0]) < 1e-12
+
+
+@pytest.mark.parametrize("pre,post,side,r_lo,r_hi,leaf", [
+    (300, 77, 0, 3, 5, 0), (77, 300, 1, 4, 4, 0), (5, 13, 0, 2, 2, 1), (13, 5, 1, 2, 3, 1),
+    (129, 1000, 1, 20, 20, 0), (1000, 129, 0, 11, 9, 0), (1600, 4000, 0, 8, 8, 0), (4000, 1600, 1, 8, 8, 1),
+])
+def test_env_tf32_matches_f64(pre, post, side, r_lo, r_hi, leaf):
+    """fp32 variant: the tcgen05 3xTF32 environment product against the fp64 one on the
+    same fp32 X (tails in every dimension, BN 64/128/256, split-K, leaf CMap).  The
+    3xTF32 products are fp32-exact to ~2^-22; the fp32 TMEM accumulation bounds the rest."""
+    from paper_2210_11362_b200 import _lib as L
+    lib = L.lib()
+    rng = np.random.default_rng(pre + post + r_lo)
+    x32 = torch.from_numpy(rng.standard_normal((pre, post)).astype(np.float32)).cuda()
+    K = post if side == 0 else pre
+    H = cuda(rng.standard_normal((K, r_lo * r_hi)))
+    rows = pre if side == 0 else post
+    ld = lib.trals_tf32_ld(K)
+    hi = torch.empty(rows * ld, dtype=torch.float32, device="cuda")
+    lo = torch.empty_like(hi)
+    s = int(torch.cuda.current_stream().cuda_stream)
+    L.check(lib.trals_tf32_split_f32(x32.data_ptr(), pre, post, post, side, hi.data_ptr(), lo.data_ptr(), ld, s), "split")
+    n_out = rows * r_lo * r_hi
+    ref = torch.empty(n_out, dtype=torch.float64, device="cuda")
+    got = torch.empty(n_out, dtype=torch.float64, device="cuda")
+    ws = torch.empty(max(lib.trals_gemm_ws_elems(1, rows, K, r_lo * r_hi), 1 << 22), dtype=torch.float64, device="cuda")
+    x64 = x32.double()
+    L.check(lib.trals_env_f64(x64.data_ptr(), pre, post, side, H.data_ptr(), r_lo, r_hi, ref.data_ptr(), leaf,
+                              ws.data_ptr(), ws.numel(), s), "env_f64")
+    ws32 = torch.empty(lib.trals_env_tf32_ws_elems(pre, post, side, r_lo, r_hi), dtype=torch.float64, device="cuda")
+    L.check(lib.trals_env_tf32(hi.data_ptr(), lo.data_ptr(), ld, pre, post, side, H.data_ptr(), r_lo, r_hi,
+                               got.data_ptr(), leaf, ws32.data_ptr(), ws32.numel(), s), "env_tf32")
+    torch.cuda.synchronize()
+    # hi + lo reproduces X exactly
+    h = hi.view(rows, ld)[:, :K].double() + lo.view(rows, ld)[:, :K].double()
+    assert torch.equal(h, x64 if side == 0 else x64.t())
+    assert rel(got.cpu().numpy(), ref.cpu().numpy()) < 1e-5
+
+
+@pytest.mark.parametrize("pre,post,side,r_lo,r_hi,leaf", [
+    (300, 77, 0, 3, 5, 0), (77, 300, 1, 4, 4, 0), (5, 13, 0, 2, 2, 1), (13, 5, 1, 2, 3, 1),
+    (129, 1000, 1, 20, 20, 0), (1000, 129, 0, 11, 9, 0), (1600, 4000, 0, 8, 8, 0), (4000, 1600, 1, 8, 8, 1),
+    (200, 70000, 0, 8, 8, 0), (70000, 150, 1, 6, 8, 0),
+])
+def test_env_oz_matches_f64(pre, post, side, r_lo, r_hi, leaf):
+    """fp32 variant product path: the int8-tensor-core digit-sliced environment product
+    (tcgen05 kind::i8, exact int32 accumulation) against the fp64 one on the same fp32 X:
+    tails in every dimension, N tiles, split-K incl. the forced K > 32768 split, leaf CMap.
+    Slicing keeps 28 bits below each row max (truncated digits: random ~2^-28 x max/|x|
+    per element), so the product is good to a few 1e-8, below fp32 rounding itself (6e-8)."""
+    from paper_2210_11362_b200 import _lib as L
+    lib = L.lib()
+    rng = np.random.default_rng(pre + post + r_lo)
+    x32 = torch.from_numpy(rng.standard_normal((pre, post)).astype(np.float32)).cuda()
+    K = post if side == 0 else pre
+    rows = pre if side == 0 else post
+    H = cuda(rng.standard_normal((K, r_lo * r_hi)))
+    ld = lib.trals_oz_ld(K)
+    digits = torch.empty(4 * rows * ld, dtype=torch.int8, device="cuda")
+    exps = torch.empty(rows, dtype=torch.int32, device="cuda")
+    s = int(torch.cuda.current_stream().cuda_stream)
+    sws = torch.empty(lib.trals_oz_split_ws_elems(pre, post, side), dtype=torch.float64, device="cuda")
+    L.check(lib.trals_oz_split_f32(x32.data_ptr(), pre, post, side, digits.data_ptr(), ld, exps.data_ptr(),
+                                   sws.data_ptr(), sws.numel(), s), "oz_split")
+    n_out = rows * r_lo * r_hi
+    ref = torch.empty(n_out, dtype=torch.float64, device="cuda")
+    got = torch.empty(n_out, dtype=torch.float64, device="cuda")
+    ws = torch.empty(max(lib.trals_gemm_ws_elems(1, rows, K, r_lo * r_hi), 1 << 22), dtype=torch.float64, device="cuda")
+    x64 = x32.double()
+    L.check(lib.trals_env_f64(x64.data_ptr(), pre, post, side, H.data_ptr(), r_lo, r_hi, ref.data_ptr(), leaf,
+                              ws.data_ptr(), ws.numel(), s), "env_f64")
+    wso = torch.empty(lib.trals_env_oz_ws_elems(pre, post, side, r_lo, r_hi), dtype=torch.float64, device="cuda")
+    L.check(lib.trals_env_oz(digits.data_ptr(), exps.data_ptr(), ld, pre, post, side, H.data_ptr(), r_lo, r_hi,
+                             got.data_ptr(), leaf, wso.data_ptr(), wso.numel(), s), "env_oz")
+    torch.cuda.synchronize()
+    # the digits rebuild X to 28 bits below each row's max
+    d = digits.view(4, rows, ld)[:, :, :K].double()
+    a = sum(d[j] * 2.0 ** (-7 * (j + 1)) for j in range(4)) * torch.pow(2.0, exps.double())[:, None]
+    xs = x64 if side == 0 else x64.t()
+    assert torch.max(torch.abs(a - xs) / torch.abs(xs).amax(dim=1, keepdim=True)).item() < 2.0 ** -27
+    assert rel(got.cpu().numpy(), ref.cpu().numpy()) < 5e-8

@@ -162,3 +162,36 @@ def test_baseline_full_size(name):
         if name == "c3":
             for j in range(order):
                 assert rel(cores[j], g[f"{v}_core_{j}"]) < 1e-6
+
+
+@pytest.mark.parametrize("name", SMALL)
+@pytest.mark.parametrize("variant", ["ne", "qr", "qrne"])
+@pytest.mark.parametrize("mode", ["cheap", "exact"])
+def test_fp32_small_goldens(name, variant, mode):
+    """fp32 variant (AlsConfig.dtype="float32", tcgen05 3xTF32 environments) against the
+    fp64 reference at the north-star fp32 tolerance 1e-4."""
+    from paper_2210_11362_b200 import AlsConfig, decompose
+    g = load_golden(name)
+    if f"{variant}_{mode}_errors" not in g:
+        pytest.skip("variant not in fixture")
+    dims = tuple(int(d) for d in g["dims"])
+    N = len(dims)
+    ranks = tuple(int(r) for r in g["ranks"])
+    cfg = AlsConfig(ranks=ranks, max_iters=int(g["sweeps"]), init_cores=golden_cores(g, "init", N), error_mode=mode,
+                    dtype="float32")
+    cores, rep = decompose(g["x"], variant, cfg)
+    np.testing.assert_allclose(rep.errors, g[f"{variant}_{mode}_errors"], rtol=0, atol=1e-4)
+    for j in range(N):
+        assert rel(cores[j], g[f"{variant}_core_{j}"]) < 1e-4
+
+
+def test_fp32_baseline_c4():
+    """BASELINE c4 in fp32 (40^5, R 6->8, 15 sweeps): per-sweep exact errors within 1e-4 of the
+    reference's fp64 run, and within 1e-4 of our fp64 run's cores' reconstruction error."""
+    from paper_2210_11362_b200 import AlsConfig, decompose
+    g = load_golden("base_c4")
+    order, dim, rt, sd, rf, si, sweeps = (int(v) for v in g["recipe"])
+    x, _ = O.synth(O.Recipe(order=order, dim=dim, rank=rt, noise=float(g["noise"]), seed=sd))
+    cores, rep = decompose(x.astype(np.float32), "ne", AlsConfig(ranks=(rf,) * order, max_iters=sweeps, seed=si,
+                                                                dtype="float32"))
+    np.testing.assert_allclose(rep.errors, g["ne_exact_errors"], rtol=0, atol=1e-4)
