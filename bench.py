@@ -38,6 +38,8 @@ CONFIGS = {
     "c5": (4, 160, 20, 1e-3, 8, 20, 9, 10),
 }
 FP64_PEAK_TFLOPS = 37.1      # measured DMMA.8x8x4 ceiling on this pool's B200 (profiles/r01_fp64_pipes.md)
+# fp32 variant: 13 int8 MMAs per fp32-equivalent multiply-add; int8 dense ~2x the measured bf16 burst
+INT8_FP32_EQ_TFLOPS = 2 * 1715.0 / 13
 PEAK_SOURCE = "profiles/r01_fp64_pipes.md: mma.sync m8n8k4 f64 microbenchmark, 148 SMs"
 
 
@@ -121,13 +123,13 @@ def flops_per_sweep(dims, ranks):
     return sum(2.0 * tot * ranks[n] * ranks[(n + 1) % N] for n in range(N))
 
 
-def roofline_sweep_time(dims, ranks, peak_tf, bw_gbs, world):
+def roofline_sweep_time(dims, ranks, peak_tf, bw_gbs, world, elem_bytes=8):
     tot = float(np.prod(dims)) / world
     N = len(dims)
     t = 0.0
     for n in range(N):
         f = 2.0 * tot * ranks[n] * ranks[(n + 1) % N]
-        t += max(f / (peak_tf * 1e12), tot * 8 / (bw_gbs * 1e9))
+        t += max(f / (peak_tf * 1e12), tot * elem_bytes / (bw_gbs * 1e9))
     return t
 
 
@@ -238,6 +240,9 @@ def run_ours(args):
     dims, ranks = [dim] * order, [rf] * order
     dev = torch.device("cuda", torch.cuda.current_device())
     x_full, _ = make_dataset_device(order, dim, rt, noise, sd, device=dev)
+    fp32 = args.dtype == "float32"
+    if fp32:
+        x_full = x_full.float()
     shard = 0
     if world > 1:
         lo, hi = _slab(dim, world, rank)
@@ -248,6 +253,7 @@ def run_ours(args):
     cores0 = random_cores(dims, ranks, make_rng(si))
     eng = SweepEngine(x_local, dims, ranks, args.variant, shard_mode=shard if world > 1 else None, lo=lo, hi=hi,
                       world_size=world)
+    eng.prepare_x()
     eng.compute_xnorm2()
     eng.set_cores(cores0)
     errs = torch.zeros((args.warmup + args.steps, 3), dtype=torch.float64, device=dev)
@@ -313,7 +319,7 @@ def run_ours(args):
     env_tf = float(np.mean(per_launch))
     env_share = env_avg_ms * len(env_flops) / ms
     traffic = None
-    tpath = os.path.join(ROOT, "profiles", f"{args.config}_env_traffic.json")
+    tpath = os.path.join(ROOT, "profiles", f"{args.config}{'_fp32' if fp32 else ''}_env_traffic.json")
     if os.path.exists(tpath):
         try:
             traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
@@ -323,19 +329,22 @@ def run_ours(args):
     peaks = load_peaks()
     bw = float(peaks.get("hbm_gbs", 6458.1))
     F = flops_per_sweep(dims, ranks)
-    t_roof = roofline_sweep_time(dims, ranks, FP64_PEAK_TFLOPS, bw, world)
+    ebytes = 4 if fp32 else 8
+    peak_tf = INT8_FP32_EQ_TFLOPS if fp32 else FP64_PEAK_TFLOPS
+    t_roof = roofline_sweep_time(dims, ranks, peak_tf, bw, world, ebytes)
     sweep_s = ms_max * 1e-3
     value = 1.0 / sweep_s
 
     # e2e through the public API: host (pinned) X -> decompose(max_iters=BASELINE sweeps) -> host cores
     e2e = None
     if not args.no_e2e:
-        xh = torch.empty(x_full.shape, dtype=torch.float64, pin_memory=True)
+        xh = torch.empty(x_full.shape, dtype=x_full.dtype, pin_memory=True)
         xh.copy_(x_full)
         del x_full, x_local
         eng = None
         torch.cuda.empty_cache()
-        cfg = AlsConfig(ranks=tuple(ranks), max_iters=sweeps, seed=si, error_mode="cheap", timing_buckets=False)
+        cfg = AlsConfig(ranks=tuple(ranks), max_iters=sweeps, seed=si, error_mode="cheap", timing_buckets=False,
+                        dtype=args.dtype)
         decompose(xh, args.variant, cfg)  # warm-up call (allocator, plan)
         torch.cuda.synchronize()
         reps = []
@@ -350,9 +359,11 @@ def run_ours(args):
             tdist.all_reduce(tt, op=tdist.ReduceOp.MAX)
         t_call = float(tt.item())
         core_bytes = sum(int(np.prod(c.shape)) * 8 for c in cores)
-        e2e = {"value": sweeps / t_call, "unit": "sweeps/s", "h2d_bytes_per_step": int(np.prod(dims)) * 8 + core_bytes,
+        e2e = {"value": sweeps / t_call, "unit": "sweeps/s",
+               "h2d_bytes_per_step": int(np.prod(dims)) * ebytes + core_bytes,
                "d2h_bytes_per_step": core_bytes + 8 * sweeps + 16,
-               "step": f"one decompose(x_host_pinned, '{args.variant}', AlsConfig(max_iters={sweeps})) call",
+               "step": f"one decompose(x_host_pinned, '{args.variant}', AlsConfig(max_iters={sweeps}, "
+                       f"dtype='{args.dtype}')) call",
                "seconds_per_call": t_call, "final_error": float(rep.errors[-1])}
         del xh
 
@@ -367,25 +378,37 @@ def run_ours(args):
                           f"numpy/OpenBLAS")}
         del x
 
+    if fp32:
+        # fp32 variant: the int8-tensor-core digit-sliced GEMM streams X (4 B/elem) once per launch
+        xbytes = float(np.prod(dims)) / world * 4
+        gbs = xbytes / (env_avg_ms * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": gbs, "peak": bw, "unit": "GB/s", "frac": gbs / bw, "traffic": traffic,
+                "kernel": "oz8_kernel (int8 tcgen05 digit-sliced X x half-chain environment product)",
+                "bytes_per_launch": xbytes, "avg_launch_ms": env_avg_ms, "share_of_step": env_share,
+                "flops_per_launch": env_flops, "tflops_fp32_equiv": env_tf,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth)"}
+    else:
+        roof = {"bound": "tensor", "achieved": env_tf, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "frac": env_tf / FP64_PEAK_TFLOPS, "traffic": traffic,
+                "kernel": "dmma_tma_kernel (X x half-chain environment product)",
+                "flops_per_launch": env_flops, "avg_launch_ms": env_avg_ms, "share_of_step": env_share,
+                "peak_source": PEAK_SOURCE}
     line = {
         "metric": METRIC, "value": value, "unit": "sweeps/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE recipe; cores from the reference Philox "
+        "vs_baseline": None, "dtype": "f32 (X) / f64" if fp32 else "f64", "data": "synthetic (BASELINE recipe; cores from the reference Philox "
                                                      "stream, X reconstructed on the GPU, device noise)",
-        "config": {"workload": f"{args.config} {args.variant.upper()} sweep", "dims": dims, "ranks": ranks,
+        "config": {"workload": f"{args.config} {args.variant.upper()} sweep" + (" (fp32 variant)" if fp32 else ""),
+                   "dims": dims, "ranks": ranks, "dtype": args.dtype,
                    "variant": args.variant, "parallelism": f"shard mode 0 x{world}" if world > 1 else "single",
-                   "l2": "X (%.2f GB) larger than the 126 MB L2, no flush needed" % (np.prod(dims) * 8 / 1e9),
+                   "l2": "X (%.2f GB) larger than the 126 MB L2, no flush needed" % (np.prod(dims) * ebytes / 1e9),
                    "step": "one full sweep + per-sweep relative error",
                    "launch": "CUDA graph replay" if use_graph else "eager stream launches"},
         "contraction_tflops": F / sweep_s / 1e12,
         "contraction_roofline_frac": t_roof / sweep_s,
         "roofline_sweep_ms": t_roof * 1e3,
         "x_passes_per_sweep": eng.stats.x_passes_per_sweep if eng is not None else 2,
-        "roofline": {"bound": "tensor", "achieved": env_tf, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                     "frac": env_tf / FP64_PEAK_TFLOPS, "traffic": traffic,
-                     "kernel": "dmma_gemm_kernel (X x half-chain environment product)",
-                     "flops_per_launch": env_flops, "avg_launch_ms": env_avg_ms, "share_of_step": env_share,
-                     "peak_source": PEAK_SOURCE},
+        "roofline": roof,
         "gpu_launches": int(launches),
         "clocks": clocks,
         "final_error": final_err,
@@ -410,6 +433,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c5")
     ap.add_argument("--variant", choices=["ne", "qr", "qrne"], default="ne")
+    ap.add_argument("--dtype", choices=["float64", "float32"], default="float64",
+                    help="float32 = the fp32 variant (BASELINE config 4): int8 tensor-core environment products")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--eager", action="store_true", help="no CUDA graph for the small configs")
     ap.add_argument("--e2e-reps", type=int, default=2)

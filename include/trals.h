@@ -101,19 +101,22 @@ int trals_env_f64(const double* d_X, int64_t pre, int64_t post, int side,
  * cores, Grams, solves and errors stay fp64. */
 /* fp32 variant, product path: digit-sliced GEMM on the int8 tensor cores
  * (tcgen05 kind::i8, exact int32 accumulation; tc_int8_gemm.cuh).  Each
- * K-major row r of X is held as ex[r] and four int8 planes with
+ * K-major row r of X is held as ex[r] and four int8 digit planes with
  *   x = 2^ex[r] * sum_{s<4} d_s 2^(-7(s+1)),  |x| < 2^ex[r],
- * digits [4][out_rows][ld] (plane stride out_rows * ld, ld = trals_oz_ld(K),
- * a multiple of 16).  trals_oz_split_f32 slices x [rows][cols] row-major, or
- * its transpose when transpose = 1 (out_rows = cols); ws holds out_rows doubles.
+ * stored as the MMA's shared-memory image: [128-row tile][64-k block][plane]
+ * [128 x 64 B], each plane in the UMMA K-major SWIZZLE_64B pattern, zero
+ * padded (trals_oz_digits_bytes bytes for rows x K).  trals_oz_split_f32
+ * slices x [rows][cols] row-major, or its transpose when transpose = 1
+ * (out rows = cols, K = rows); ws holds out_rows doubles.
  * trals_env_oz: trals_env_f64 with X given sliced, K-major for `side` (side 0:
- * rows = pre, side 1: rows = post); the half chain is sliced per call. */
-int64_t trals_oz_ld(int64_t k);
+ * rows = pre, K = post; side 1: rows = post, K = pre); the half chain is
+ * sliced per call. */
+int64_t trals_oz_digits_bytes(int64_t rows, int64_t k);
 int64_t trals_oz_split_ws_elems(int64_t rows, int64_t cols, int transpose);
-int trals_oz_split_f32(const float* d_x, int64_t rows, int64_t cols, int transpose, int8_t* d_digits, int64_t ld,
+int trals_oz_split_f32(const float* d_x, int64_t rows, int64_t cols, int transpose, int8_t* d_digits,
                        int32_t* d_exps, double* d_ws, int64_t ws_elems, void* stream);
 int64_t trals_env_oz_ws_elems(int64_t pre, int64_t post, int side, int r_lo, int r_hi);
-int trals_env_oz(const int8_t* d_xdigits, const int32_t* d_xexps, int64_t ldx, int64_t pre, int64_t post, int side,
+int trals_env_oz(const int8_t* d_xdigits, const int32_t* d_xexps, int64_t pre, int64_t post, int side,
                  const double* d_H, int r_lo, int r_hi, double* d_env, int leaf, double* d_ws, int64_t ws_elems,
                  void* stream);
 /* 3xTF32 alternative (an operator kept for comparison, not used by the

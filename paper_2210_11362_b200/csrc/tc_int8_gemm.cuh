@@ -13,21 +13,36 @@
 //
 // (per-row / per-column power-of-two scales with |x| < 2^e, truncated base-128
 // digits: 28 bits below the row maximum, exact for fp32 values within 16x of
-// it), and the product keeps every digit pair with s + t <= 4 (13 int8 MMAs per
-// k-step).  Measured on N(0,1) data: 1.2-1.9e-8 relative Frobenius against an
-// fp64 product of the same fp32 X, dominated by the digit truncation of the
-// row/column maxima's 28-bit window (keeping only s + t <= 3 gave 6e-8).
-// Pairs of equal level L = s + t share one int32 TMEM accumulator (5 x BN
-// columns); the epilogue combines them exactly in fp64 (Horner in 2^-7):
+// it).  All 16 digit pairs are kept, in 4 MMAs per 32-k step: the B tile holds
+// the 4 B planes stacked as one N = 4 BN operand, so the MMA of A plane s
+// writes pair (s, t) into accumulator column block s + t -- i.e. issuing A plane
+// s at TMEM column offset s BN makes every level L = s + t land in one int32
+// block (7 x BN columns), each A plane is read from shared memory once per step
+// (SS-mode operand reads, not the tensor pipe, bounded the 13-MMA pairwise
+// form).  The epilogue zeroes the levels for the next tile and combines them
+// exactly in fp64 (Horner in 2^-7):
 //   C = 2^(ea+eb-14) * sum_L acc_L 2^(-7L).
+// Measured on N(0,1) data: 1.2-1.9e-8 relative Frobenius against an fp64
+// product of the same fp32 X, i.e. the digit truncation of the row / column
+// maxima's 28-bit window.
 // No overflow: a level sums at most 4 pairs of |a b| <= 127^2 over at most
 // kOzKmax (32768) k per CTA, < 2^31; longer K is always split.
 //
-// Structure (one 128 x BN tile per CTA, split-K): warp 0 = TMA producer (4 A
-// digit planes + 4 B digit planes per stage, {128 k, rows} boxes, 128B
-// swizzle), warp 1 = TMEM allocator + single-thread MMA issuer
-// (tcgen05.mma.cta_group::1.kind::i8, K-major both, 32 k per MMA),
-// warps 2-5 = epilogue (tcgen05.ld 32x32b; warp w owns TMEM lanes 32*(w%4)).
+// Operand layout in HBM: the digits are stored as the exact shared-memory image
+// of the MMA operand tiles -- blocks of [row tile][64-k block][digit plane]
+// [rows x 64 B], each plane already in the UMMA K-major SWIZZLE_64B pattern
+// (16-byte chunk c of row r at chunk c ^ ((r >> 1) & 3)), zero padded to whole
+// tiles.  One pipeline stage is then two contiguous bulk copies (A: 32 KB, B:
+// 16 KB, cp.async.bulk), so X streams from HBM strictly sequentially instead
+// of as 64 B pieces of 128 different rows (which capped the tensor-map version
+// at 2.8 TB/s).
+//
+// Structure (persistent, one CTA per SM over 128 x BN x kchunk tiles): warp 0 =
+// bulk-copy producer (a STAGES-deep ring running across tiles), warp 1 = TMEM
+// allocator + single-thread MMA issuer (tcgen05.mma.cta_group::1.kind::i8,
+// K-major both, 32 k per MMA), warps 2-5 = epilogue (tcgen05.ld 32x32b; warp w
+// owns TMEM lanes 32*(w%4)); acc_full / acc_empty mbarriers hand the
+// accumulators over.
 #pragma once
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -39,27 +54,33 @@
 
 namespace trals {
 
-constexpr int kOzBK = 128;       // int8 k per stage (one 128 B swizzle row)
+constexpr int kOzBK = 64;        // int8 k per stage (one 64 B swizzle row)
 constexpr int kOzBM = 128;
 constexpr int kOzDigits = 4;
-constexpr int kOzLevels = 5;     // digit-pair levels L = s + t kept (0..4)
+constexpr int kOzLevels = 7;     // digit-pair levels L = s + t (0..6): every pair is kept
 constexpr int64_t kOzKmax = 32768;
 
 template <int BN>
 struct OzTile {
-  static constexpr int A_PLANE = kOzBM * kOzBK;  // 16 KB
+  static constexpr int A_PLANE = kOzBM * kOzBK;  // 8 KB
   static constexpr int B_PLANE = BN * kOzBK;
   static constexpr int STAGE = kOzDigits * (A_PLANE + B_PLANE);
-  static constexpr int STAGES = (200 * 1024) / STAGE < 4 ? (200 * 1024) / STAGE : 4;
-  static constexpr int TMEM_COLS = kOzLevels * BN <= 256 ? 256 : 512;
+  static constexpr int OUT_LD = BN + 1;                   // fp64 output staging row (odd: no bank conflicts)
+  static constexpr int OUT_BYTES = kOzBM * OUT_LD * 8;
+  static constexpr int STAGES = (212 * 1024 - OUT_BYTES) / STAGE < 6 ? (212 * 1024 - OUT_BYTES) / STAGE : 6;
+  static constexpr int TMEM_COLS = 512;  // kOzLevels * BN = 448 accumulator columns
   static constexpr int THREADS = 6 * 32;
-  static constexpr size_t SMEM = static_cast<size_t>(STAGES) * STAGE + 1024 + 256;
+  static constexpr size_t SMEM = static_cast<size_t>(STAGES) * STAGE + OUT_BYTES + 1024 + 256;
 };
 
 struct OzArgs {
   int64_t M, K, N;
   int64_t kchunk;
   int splits;
+  int mtiles, ntiles;  // tile t -> (split, m-tile, n-tile), n fastest
+  int64_t kblocks;     // 64-k blocks of the tiled digit layout (ceil(K / 64))
+  const int8_t* ad;    // A digits, tiled: [mtiles][kblocks][4][128 x 64 B]
+  const int8_t* bd;    // B digits, tiled: [ntiles][kblocks][4][BN x 64 B]
   CMap cmap;
   const int32_t* ea;  // [M] row exponents of A
   const int32_t* eb;  // [N] row exponents of B
@@ -67,14 +88,30 @@ struct OzArgs {
   double* ws;
 };
 
-// UMMA shared-memory descriptor (K-major, SWIZZLE_128B, version 1): 8-row groups 1 KB apart
+// byte offset of (row r, k) inside the tiled digit layout of one plane block
+// (rows_per_tile rows x 64 B, SWIZZLE_64B)
+__host__ __device__ __forceinline__ int64_t oz_tiled_offset(int64_t r, int64_t k, int plane, int rows_per_tile,
+                                                            int64_t kblocks) {
+  const int64_t t = r / rows_per_tile, rr = r % rows_per_tile, kb = k >> 6, c = k & 63;
+  const int64_t block = (t * kblocks + kb) * kOzDigits + plane;
+  return block * rows_per_tile * 64 + rr * 64 + ((((c >> 4) ^ ((rr >> 1) & 3))) << 4) + (c & 15);
+}
+
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// UMMA shared-memory descriptor (K-major, SWIZZLE_64B, version 1): 64 B rows, 8-row groups 512 B apart
 __device__ __forceinline__ uint64_t oz_desc(uint32_t saddr) {
   uint64_t d = 0;
   d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
   d |= static_cast<uint64_t>(1) << 16;             // LBO (unused for swizzled K-major)
-  d |= static_cast<uint64_t>(1024 >> 4) << 32;     // SBO
+  d |= static_cast<uint64_t>(512 >> 4) << 32;      // SBO
   d |= static_cast<uint64_t>(1) << 46;
-  d |= static_cast<uint64_t>(2) << 61;
+  d |= static_cast<uint64_t>(4) << 61;             // SWIZZLE_64B
   return d;
 }
 
@@ -97,9 +134,40 @@ __device__ __forceinline__ void umma_i8(uint32_t tmem_d, uint64_t da, uint64_t d
       "l"(da), "l"(db), "r"(idesc), "r"(acc));
 }
 
+// Warp-wide forms: all 32 lanes execute them with warp-uniform operands (so the
+// descriptors live in uniform registers, no per-MMA R2UR), one elected lane issues.
+__device__ __forceinline__ void umma_i8_warp(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void oz_commit_warp(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n" ::"r"(smem_u32(bar))
+      : "memory");
+}
+
 __device__ __forceinline__ void oz_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar))
                : "memory");
+}
+
+// zero this warp's 32 TMEM lanes over the kOzLevels x 64 accumulator columns
+__device__ __forceinline__ void tmem_zero(uint32_t tlane) {
+#pragma unroll
+  for (int c = 0; c < kOzLevels * 64; c += 16)
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};\n" ::"r"(
+            tlane + c),
+        "r"(0u)
+        : "memory");
+  asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
 }
 
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
@@ -110,39 +178,35 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
       : "r"(taddr));
 }
 
-// A maps: 4 digit planes of A, B maps: 4 digit planes of B (each a 2-D int8 tensor map)
-struct OzMaps {
-  CUtensorMap a[kOzDigits];
-  CUtensorMap b[kOzDigits];
-};
-
 template <int BN>
 __global__ void __launch_bounds__(OzTile<BN>::THREADS, 1)
-oz8_kernel(const __grid_constant__ OzMaps maps, const OzArgs g) {
+oz8_kernel(const __grid_constant__ OzArgs g) {
+  // Persistent: CTA b takes tiles b, b + gridDim.x, ...; the smem ring runs across
+  // tile boundaries, so the producer prefetches the next tile while the
+  // epilogue drains the accumulators of the current one.
   using T = OzTile<BN>;
   constexpr int S = T::STAGES;
   extern __shared__ uint8_t smraw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(sm + S * T::STAGE);
+  double* otile = reinterpret_cast<double*>(sm + S * T::STAGE);  // [kOzBM][OUT_LD] epilogue staging
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + S * T::STAGE + T::OUT_BYTES);
   uint64_t* empty = full + S;
-  uint64_t* accum = empty + S;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
+  uint64_t* acc_full = empty + S;
+  uint64_t* acc_empty = acc_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
 
   const int tid = threadIdx.x, lane = tid & 31;
   const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
-  const int64_t n0 = static_cast<int64_t>(blockIdx.x) * BN;
-  const int64_t m0 = static_cast<int64_t>(blockIdx.y) * kOzBM;
-  const int split = blockIdx.z;
-  const int64_t kbeg = static_cast<int64_t>(split) * g.kchunk;
-  const int64_t kend = (g.K < kbeg + g.kchunk) ? g.K : kbeg + g.kchunk;
-  const int ktiles = kend > kbeg ? static_cast<int>((kend - kbeg + kOzBK - 1) / kOzBK) : 0;
+  const int per_split = g.mtiles * g.ntiles;
+  const int total = per_split * g.splits;
 
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(full + s, 1);
       mbar_init(empty + s, 1);
     }
-    mbar_init(accum, 1);
+    mbar_init(acc_full, 1);
+    mbar_init(acc_empty, 4);  // one arrive per epilogue warp
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 1) {
@@ -155,102 +219,144 @@ oz8_kernel(const __grid_constant__ OzMaps maps, const OzArgs g) {
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const uint32_t tmem = *tmem_slot;
 
+  auto tile_k = [&](int t, int64_t& kbeg, int& ktiles) {
+    const int split = t / per_split;
+    kbeg = static_cast<int64_t>(split) * g.kchunk;
+    const int64_t kend = (g.K < kbeg + g.kchunk) ? g.K : kbeg + g.kchunk;
+    ktiles = kend > kbeg ? static_cast<int>((kend - kbeg + kOzBK - 1) / kOzBK) : 0;
+  };
+
   if (warp == 0) {
     // ------------------------------ TMA producer ------------------------------
     if (lane == 0) {
-      for (int kt = 0; kt < ktiles; ++kt) {
-        const int s = kt % S;
-        if (kt >= S) mbar_wait(empty + s, ((kt / S) - 1) & 1);
-        uint8_t* st = sm + s * T::STAGE;
-        mbar_expect_tx(full + s, T::STAGE);
-        const int k0 = static_cast<int>(kbeg + static_cast<int64_t>(kt) * kOzBK);
-#pragma unroll
-        for (int d = 0; d < kOzDigits; ++d) {
-          tma_load_2d(st + d * T::A_PLANE, &maps.a[d], full + s, k0, static_cast<int>(m0));
-          tma_load_2d(st + kOzDigits * T::A_PLANE + d * T::B_PLANE, &maps.b[d], full + s, k0, static_cast<int>(n0));
+      uint32_t gk = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        int64_t kbeg;
+        int ktiles;
+        tile_k(t, kbeg, ktiles);
+        const int rem = t % per_split;
+        const int m0 = (rem / g.ntiles) * kOzBM, n0 = (rem % g.ntiles) * BN;
+        // k blocks in a per-CTA rotated order: the int32 accumulation is exact, so the
+        // order is free, and it keeps 148 CTAs from reading the same B block at once
+        const int rot = ktiles > 0 ? static_cast<int>(blockIdx.x % ktiles) : 0;
+        for (int kt = 0; kt < ktiles; ++kt, ++gk) {
+          const uint32_t s = gk % S;
+          if (gk >= S) mbar_wait(empty + s, ((gk / S) - 1) & 1);
+          uint8_t* st = sm + s * T::STAGE;
+          mbar_expect_tx(full + s, T::STAGE);
+          const int kr = kt + rot < ktiles ? kt + rot : kt + rot - ktiles;
+          const int64_t kb = kbeg / kOzBK + kr;
+          bulk_load(st, g.ad + (static_cast<int64_t>(m0 / kOzBM) * g.kblocks + kb) * (kOzDigits * T::A_PLANE),
+                    kOzDigits * T::A_PLANE, full + s);
+          bulk_load(st + kOzDigits * T::A_PLANE,
+                    g.bd + (static_cast<int64_t>(n0 / BN) * g.kblocks + kb) * (kOzDigits * T::B_PLANE),
+                    kOzDigits * T::B_PLANE, full + s);
         }
       }
     }
   } else if (warp == 1) {
     // ------------------------------ MMA issuer ------------------------------
-    const uint32_t idesc = i8_idesc(BN);
-    for (int kt = 0; kt < ktiles; ++kt) {
-      const int s = kt % S;
-      mbar_wait(full + s, (kt / S) & 1);
+    // The whole warp runs this loop with warp-uniform values; descriptors are
+    // linear in the smem address (start field = addr >> 4), so each MMA's pair is
+    // the stage base descriptor plus a compile-time offset.
+    const uint32_t idesc = i8_idesc(kOzDigits * BN);  // B = the 4 digit planes stacked: N = 4 BN
+    const uint64_t dA0 = oz_desc(smem_u32(sm)), dB0 = oz_desc(smem_u32(sm) + kOzDigits * T::A_PLANE);
+    uint32_t gk = 0, it = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
+      int64_t kbeg;
+      int ktiles;
+      tile_k(t, kbeg, ktiles);
+      mbar_wait(acc_empty, it & 1);  // accumulators drained and zeroed by the epilogue
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-      if (lane == 0) {
-        const uint32_t a0 = smem_u32(sm + s * T::STAGE), b0 = a0 + kOzDigits * T::A_PLANE;
+      for (int kt = 0; kt < ktiles; ++kt, ++gk) {
+        const uint32_t s = gk % S;
+        mbar_wait(full + s, (gk / S) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        {
+          const uint64_t da = dA0 + ((s * T::STAGE) >> 4), db = dB0 + ((s * T::STAGE) >> 4);
 #pragma unroll
-        for (int k = 0; k < kOzBK / 32; ++k) {
-          const uint32_t first = (kt > 0 || k > 0) ? 1u : 0u;
+          for (int k = 0; k < kOzBK / 32; ++k)
 #pragma unroll
-          for (int L = 0; L < kOzLevels; ++L) {
-            const int s_lo = L < kOzDigits ? 0 : L - (kOzDigits - 1);
-            const int s_hi = L < kOzDigits ? L : kOzDigits - 1;
-#pragma unroll
-            for (int sa = s_lo; sa <= s_hi; ++sa) {
-              const int tb = L - sa;
-              umma_i8(tmem + L * BN, oz_desc(a0 + sa * T::A_PLANE + k * 32), oz_desc(b0 + tb * T::B_PLANE + k * 32),
-                      idesc, sa == s_lo ? first : 1u);
-            }
-          }
+            for (int sa = 0; sa < kOzDigits; ++sa)
+              umma_i8_warp(tmem + sa * BN, da + ((sa * T::A_PLANE + k * 32) >> 4), db + ((k * 32) >> 4), idesc, 1u);
+          oz_commit_warp(empty + s);  // the stage is free once these MMAs have read it
         }
-        oz_commit(empty + s);
+        __syncwarp();
       }
+      if (ktiles > 0) oz_commit_warp(acc_full);
+      else if (lane == 0) mbar_arrive(acc_full);
       __syncwarp();
     }
-    if (lane == 0) {
-      if (ktiles > 0) oz_commit(accum);
-      else mbar_arrive(accum);
-    }
-    __syncwarp();
   } else {
     // ------------------------------ epilogue ------------------------------
-    mbar_wait(accum, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    // (1) TMEM -> exact fp64 combination -> smem tile (lane = row), release TMEM;
+    // (2) smem tile -> global with lanes along n (contiguous for every CMap the
+    //     engine uses), row / column offsets computed once per row / per tile.
     const int quad = warp & 3;
-    const int64_t m = m0 + quad * 32 + lane;
-    const bool mok = m < g.M;
-    const bool have = ktiles > 0;
-    const uint32_t m2 = static_cast<uint32_t>(g.cmap.M2), n2 = static_cast<uint32_t>(g.cmap.N2);
-    const int ea = mok ? g.ea[m] : 0;
-    const int64_t row_off = !mok ? 0
-                                 : (g.splits > 1 ? (static_cast<int64_t>(split) * g.M + m) * g.N
-                                                 : static_cast<int64_t>(static_cast<uint32_t>(m) / m2) * g.cmap.sm1 +
-                                                       static_cast<int64_t>(static_cast<uint32_t>(m) % m2) * g.cmap.sm2);
-    for (int c0 = 0; c0 < BN; c0 += 16) {
-      if (n0 + c0 >= g.N) break;  // warp-uniform
-      uint32_t v0[16], v1[16], v2[16], v3[16], v4[16];
-      const uint32_t taddr = tmem + (static_cast<uint32_t>(quad * 32) << 16) + c0;
-      tmem_ld16(taddr, v0);
-      tmem_ld16(taddr + BN, v1);
-      tmem_ld16(taddr + 2 * BN, v2);
-      tmem_ld16(taddr + 3 * BN, v3);
-      tmem_ld16(taddr + 4 * BN, v4);
-      asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-      if (mok) {
+    const uint32_t tlane = tmem + (static_cast<uint32_t>(quad * 32) << 16);
+    tmem_zero(tlane);  // every MMA accumulates: the levels start from zero
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncwarp();
+    if (lane == 0) mbar_arrive(acc_empty);
+    uint32_t it = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
+      int64_t kbeg;
+      int ktiles;
+      tile_k(t, kbeg, ktiles);
+      const int split = t / per_split, rem = t % per_split;
+      const int64_t m0 = static_cast<int64_t>(rem / g.ntiles) * kOzBM, n0 = static_cast<int64_t>(rem % g.ntiles) * BN;
+      mbar_wait(acc_full, it & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      const int r = quad * 32 + lane;
+      const int64_t m = m0 + r;
+      const double sa = (m < g.M && ktiles > 0) ? ldexp(1.0, g.ea[m] - 14) : 0.0;
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 16) {
+        uint32_t v[kOzLevels][16];
+#pragma unroll
+        for (int L = 0; L < kOzLevels; ++L) tmem_ld16(tlane + L * BN + c0, v[L]);
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 #pragma unroll
         for (int q = 0; q < 16; ++q) {
-          const int64_t n = n0 + c0 + q;
-          if (n >= g.N) continue;
-          double val = 0.0;
-          if (have) {
-            val = static_cast<double>(static_cast<int32_t>(v4[q]));
-            val = fma(val, 0.0078125, static_cast<double>(static_cast<int32_t>(v3[q])));
-            val = fma(val, 0.0078125, static_cast<double>(static_cast<int32_t>(v2[q])));
-            val = fma(val, 0.0078125, static_cast<double>(static_cast<int32_t>(v1[q])));
-            val = fma(val, 0.0078125, static_cast<double>(static_cast<int32_t>(v0[q])));
-            val = ldexp(val, ea + g.eb[n] - 14);
-          }
-          if (g.splits > 1) {
-            g.ws[row_off + n] = val;
-          } else {
-            const uint32_t un = static_cast<uint32_t>(n);
-            g.C[row_off + static_cast<int64_t>(un / n2) * g.cmap.sn1 + static_cast<int64_t>(un % n2) * g.cmap.sn2] =
-                val;
-          }
+          double val = static_cast<double>(static_cast<int32_t>(v[kOzLevels - 1][q]));
+#pragma unroll
+          for (int L = kOzLevels - 2; L >= 0; --L)
+            val = fma(val, 0.0078125, static_cast<double>(static_cast<int32_t>(v[L][q])));
+          otile[r * T::OUT_LD + c0 + q] = val * sa;
         }
       }
+      tmem_zero(tlane);
+      asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(acc_empty);  // the MMA warp may start the next tile
+      asm volatile("bar.sync 1, 128;\n" ::: "memory");
+      // (2) coalesced stores: lane -> column n (BN / 32 per lane), warp -> rows quad, quad + 4, ...
+      const bool part = g.splits > 1;
+      const uint32_t M2 = part ? (1u << 30) : static_cast<uint32_t>(g.cmap.M2);
+      const uint32_t N2 = part ? (1u << 30) : static_cast<uint32_t>(g.cmap.N2);
+      const int64_t sm1 = part ? 0 : g.cmap.sm1, sm2 = part ? g.N : g.cmap.sm2;
+      const int64_t sn1 = part ? 0 : g.cmap.sn1, sn2 = part ? 1 : g.cmap.sn2;
+      double* base = part ? g.ws + static_cast<int64_t>(split) * g.M * g.N : g.C;
+      int64_t coff[BN / 32];
+      double sb[BN / 32];
+      bool nok[BN / 32];
+#pragma unroll
+      for (int j = 0; j < BN / 32; ++j) {
+        const int64_t n = n0 + lane + 32 * j;
+        nok[j] = n < g.N;
+        const uint32_t un = static_cast<uint32_t>(n);
+        coff[j] = nok[j] ? static_cast<int64_t>(un / N2) * sn1 + static_cast<int64_t>(un % N2) * sn2 : 0;
+        sb[j] = nok[j] ? ldexp(1.0, g.eb[n]) : 0.0;
+      }
+      const int rows = static_cast<int>((g.M - m0) < kOzBM ? (g.M - m0) : kOzBM);
+      for (int rr = quad; rr < rows; rr += 4) {
+        const uint32_t mm = static_cast<uint32_t>(m0 + rr);
+        const int64_t roff = static_cast<int64_t>(mm / M2) * sm1 + static_cast<int64_t>(mm % M2) * sm2;
+#pragma unroll
+        for (int j = 0; j < BN / 32; ++j)
+          if (nok[j]) base[roff + coff[j]] = otile[rr * T::OUT_LD + lane + 32 * j] * sb[j];
+      }
+      asm volatile("bar.sync 1, 128;\n" ::: "memory");  // otile reused by the next tile
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
@@ -280,16 +386,22 @@ __global__ void __launch_bounds__(256) oz_rowmax_kernel(const Tin* __restrict__ 
   }
 }
 
-// column max of a row-major [rows][ld] matrix; out[c] must be zeroed (atomicMax on the bit pattern)
+// column max of a row-major [rows][ld] matrix; out[c] must be zeroed (atomicMax on the
+// bit pattern of non-negative doubles).  A block covers min(cols, 256) columns x
+// (256 / that) row phases of a rows_per_block slab, so narrow matrices (the half
+// chain's 64 columns) still use every thread.
 template <typename Tin>
 __global__ void __launch_bounds__(256) oz_colmax_kernel(const Tin* __restrict__ x, int64_t rows, int64_t cols,
                                                         int64_t ld, int64_t rows_per_block, double* __restrict__ out) {
-  const int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (c >= cols) return;
+  const int cw = cols < 256 ? static_cast<int>(cols) : 256;
+  const int phases = 256 / cw;
+  const int tc = threadIdx.x % cw, tr = threadIdx.x / cw;
+  const int64_t c = blockIdx.x * static_cast<int64_t>(cw) + tc;
+  if (tr >= phases || c >= cols) return;
   const int64_t r0 = blockIdx.y * rows_per_block;
   const int64_t r1 = (r0 + rows_per_block < rows) ? r0 + rows_per_block : rows;
   double m = 0.0;
-  for (int64_t r = r0; r < r1; ++r) m = fmax(m, fabs(static_cast<double>(x[r * ld + c])));
+  for (int64_t r = r0 + tr; r < r1; r += phases) m = fmax(m, fabs(static_cast<double>(x[r * ld + c])));
   atomicMax(reinterpret_cast<unsigned long long*>(out) + c, static_cast<unsigned long long>(__double_as_longlong(m)));
 }
 
@@ -309,44 +421,53 @@ __device__ __forceinline__ void oz_digits(double v, int8_t (&d)[kOzDigits]) {
   }
 }
 
-// x [rows][ld_in] -> digit planes of the output rows (rows, or cols when transposed),
-// planes [4][out_rows][ld_out] int8 (plane stride out_rows * ld_out), exps[out_rows];
-// mx[out_rows] = max |x| of each output row.
+// x [rows][ld_in] -> tiled digit planes of the output rows (rows, or cols when
+// transposed; K = the other extent), covering the whole padded layout (zero
+// digits in the tile padding, so no memset is needed); mx[out_rows] = max |x| of
+// each output row, exps[out_rows] its exponent.  One thread per (output row,
+// 16-k chunk): 16 values -> 4 planes x one 16 B store.
 template <typename Tin>
-__global__ void __launch_bounds__(256) oz_digits_kernel(const Tin* __restrict__ x, int64_t rows, int64_t cols,
-                                                        int64_t ld_in, int transpose, const double* __restrict__ mx,
-                                                        int8_t* __restrict__ planes, int64_t ld_out,
-                                                        int32_t* __restrict__ exps) {
-  __shared__ double tile[32][33];
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
-  const int64_t out_rows = transpose ? cols : rows;
-  const int64_t pstride = out_rows * ld_out;
-  const int64_t tiles_c = (cols + 31) / 32, tiles = ((rows + 31) / 32) * tiles_c;
-  for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
-    const int64_t r0 = (t / tiles_c) * 32, c0 = (t % tiles_c) * 32;
+__global__ void __launch_bounds__(256) oz_digits_tiled_kernel(const Tin* __restrict__ x, int64_t rows, int64_t cols,
+                                                              int64_t ld_in, int transpose,
+                                                              const double* __restrict__ mx, int8_t* __restrict__ out,
+                                                              int rows_per_tile, int32_t* __restrict__ exps) {
+  const int64_t out_rows = transpose ? cols : rows, K = transpose ? rows : cols;
+  const int64_t kblocks = (K + 63) / 64, kchunks = kblocks * 4;
+  const int64_t rows_pad = (out_rows + rows_per_tile - 1) / rows_per_tile * rows_per_tile;
+  const int64_t total = rows_pad * kchunks;
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    // coalesced reads: consecutive threads walk k within a row (row-major input)
+    // or rows at a fixed k (transposed input)
+    const int64_t orow = transpose ? idx % rows_pad : idx / kchunks;
+    const int64_t ch = transpose ? idx / rows_pad : idx % kchunks;
+    const bool rok = orow < out_rows;
+    const int e = rok ? oz_exponent(mx[orow]) : 0;
+    const double sc = ldexp(1.0, -e);
+    uint32_t w[kOzDigits][4];
 #pragma unroll
-    for (int j = 0; j < 32; j += 8) {
-      const int64_t r = r0 + ty + j, c = c0 + tx;
-      tile[ty + j][tx] = (r < rows && c < cols) ? static_cast<double>(x[r * ld_in + c]) : 0.0;
-    }
-    __syncthreads();
+    for (int d = 0; d < kOzDigits; ++d)
 #pragma unroll
-    for (int j = 0; j < 32; j += 8) {
-      // output element (orow, ocol): orow = r (or c), ocol = c (or r)
-      const int64_t orow = transpose ? c0 + ty + j : r0 + ty + j;
-      const int64_t ocol = transpose ? r0 + tx : c0 + tx;
-      const bool ok = transpose ? (orow < cols && ocol < rows) : (orow < rows && ocol < cols);
-      if (ok) {
-        const int e = oz_exponent(mx[orow]);
-        const double v = transpose ? tile[tx][ty + j] : tile[ty + j][tx];
-        int8_t d[kOzDigits];
-        oz_digits(ldexp(v, -e), d);
+      for (int q = 0; q < 4; ++q) w[d][q] = 0;
+    if (rok && ch * 16 < K) {
 #pragma unroll
-        for (int s = 0; s < kOzDigits; ++s) planes[s * pstride + orow * ld_out + ocol] = d[s];
-        if (ocol == 0) exps[orow] = e;
+      for (int j = 0; j < 16; ++j) {
+        const int64_t k = ch * 16 + j;
+        double v = 0.0;
+        if (k < K) v = static_cast<double>(transpose ? x[k * ld_in + orow] : x[orow * ld_in + k]);
+        int8_t dg[kOzDigits];
+        oz_digits(v * sc, dg);
+#pragma unroll
+        for (int d = 0; d < kOzDigits; ++d)
+          w[d][j >> 2] |= static_cast<uint32_t>(static_cast<uint8_t>(dg[d])) << (8 * (j & 3));
       }
     }
-    __syncthreads();
+#pragma unroll
+    for (int d = 0; d < kOzDigits; ++d) {
+      const int64_t off = oz_tiled_offset(orow, ch * 16, d, rows_per_tile, kblocks);
+      *reinterpret_cast<uint4*>(out + off) = make_uint4(w[d][0], w[d][1], w[d][2], w[d][3]);
+    }
+    if (rok && ch == 0) exps[orow] = e;
   }
 }
 

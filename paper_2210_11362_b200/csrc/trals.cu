@@ -463,21 +463,11 @@ int gemm_tc(const float* ahi, const float* alo, int64_t lda, int64_t M, int64_t 
 // ---------------------------------------------------------------------------
 // fp32 variant: int8 tcgen05 digit-sliced GEMM (tc_int8_gemm.cuh)
 // ---------------------------------------------------------------------------
-bool make_map_i8(CUtensorMap* map, const int8_t* base, uint64_t inner, uint64_t outer, uint64_t ld,
-                 uint32_t box_outer) {
-  auto enc = tensor_map_encoder();
-  if (!enc) return false;
-  const cuuint64_t dims[2] = {inner, outer};
-  const cuuint64_t strides[1] = {ld};
-  const cuuint32_t box[2] = {static_cast<cuuint32_t>(trals::kOzBK), box_outer};
-  const cuuint32_t estr[2] = {1, 1};
-  return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<int8_t*>(base), dims, strides, box, estr,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
 constexpr int kOzBN = 64;
-inline int64_t oz_ld(int64_t k) { return (k + 15) / 16 * 16; }
+// bytes of a tiled digit layout: 4 planes x rows padded to the tile x K padded to 64
+inline int64_t oz_digits_bytes(int64_t rows, int64_t k, int rows_per_tile) {
+  return 4 * ((rows + rows_per_tile - 1) / rows_per_tile * rows_per_tile) * ((k + 63) / 64 * 64);
+}
 
 // split-K: byte-bound model (4 digit bytes per A element at the per-SM HBM share),
 // and never more than kOzKmax k per CTA (int32 accumulator bound)
@@ -510,7 +500,7 @@ OzWs oz_ws_layout(int64_t M, int64_t K, int64_t N) {
   const SplitPlan sp = plan_split_oz(M, K, N);
   OzWs w{};
   w.planes = 0;
-  w.eb = w.planes + (4 * N * oz_ld(K) + 15) / 16 * 2;
+  w.eb = w.planes + (oz_digits_bytes(N, K, kOzBN) + 15) / 16 * 2;
   w.mx = w.eb + (N + 3) / 4 * 2;
   w.part = w.mx + (N + 1) / 2 * 2;
   w.total = w.part + (sp.splits > 1 ? static_cast<int64_t>(sp.splits) * M * N : 0);
@@ -519,46 +509,43 @@ OzWs oz_ws_layout(int64_t M, int64_t K, int64_t N) {
 
 int64_t gemm_oz_ws(int64_t M, int64_t K, int64_t N) { return oz_ws_layout(M, K, N).total; }
 
-int launch_colmax_f64(const double* x, int64_t rows, int64_t cols, int64_t ld, double* out, cudaStream_t s) {
+template <typename T>
+int launch_colmax(const T* x, int64_t rows, int64_t cols, int64_t ld, double* out, cudaStream_t s) {
   cudaMemsetAsync(out, 0, cols * sizeof(double), s);
-  const int64_t rpb = std::max<int64_t>(64, (rows + 255) / 256);
-  dim3 grid(static_cast<unsigned>((cols + 255) / 256), static_cast<unsigned>((rows + rpb - 1) / rpb));
-  trals::oz_colmax_kernel<double><<<grid, 256, 0, s>>>(x, rows, cols, ld, rpb, out);
+  const int64_t cw = std::min<int64_t>(cols, 256), cblocks = (cols + cw - 1) / cw;
+  // about 4 blocks per SM in total, at least 64 rows per block
+  const int64_t want = std::max<int64_t>(1, 4 * kSMs / cblocks);
+  const int64_t rpb = std::max<int64_t>(64, (rows + want - 1) / want);
+  dim3 grid(static_cast<unsigned>(cblocks), static_cast<unsigned>((rows + rpb - 1) / rpb));
+  trals::oz_colmax_kernel<T><<<grid, 256, 0, s>>>(x, rows, cols, ld, rpb, out);
   return launch_status();
 }
 
-// C(m, n) = sum_k A[m][k] B[k][n]: A given as digit planes [4][M][lda] + row exponents ea[M],
+// C(m, n) = sum_k A[m][k] B[k][n]: A given as tiled digits [4 x 128-row tiles] + row exponents ea[M],
 // B fp64 [K][ldb] (sliced per call into the workspace), C fp64 through cm.
-int gemm_oz(const int8_t* ad, const int32_t* ea, int64_t lda, int64_t M, int64_t K, int64_t N, const double* B,
-            int64_t ldb, double* C, const CMap& cm, double* ws, int64_t ws_elems, cudaStream_t s) {
-  if (!tensor_map_encoder()) return TRALS_ERR_CUDA;
-  if ((reinterpret_cast<uintptr_t>(ad) & 15u) || (lda & 15) || lda < K || M > INT32_MAX || K > INT32_MAX ||
-      N > 65535LL * kOzBN)
-    return TRALS_ERR_ARG;
+int gemm_oz(const int8_t* ad, const int32_t* ea, int64_t M, int64_t K, int64_t N, const double* B, int64_t ldb,
+            double* C, const CMap& cm, double* ws, int64_t ws_elems, cudaStream_t s) {
+  if ((reinterpret_cast<uintptr_t>(ad) & 15u) || M > INT32_MAX || K > INT32_MAX || N > INT32_MAX) return TRALS_ERR_ARG;
   const OzWs w = oz_ws_layout(M, K, N);
   if (!ws || w.total > ws_elems) return TRALS_ERR_ARG;
   const SplitPlan sp = plan_split_oz(M, K, N);
-  const int64_t ldk = oz_ld(K);
   int8_t* bd = reinterpret_cast<int8_t*>(ws + w.planes);
   int32_t* eb = reinterpret_cast<int32_t*>(ws + w.eb);
   double* bmx = ws + w.mx;
-  // B^T rows = columns of B: max over k, then digits (transposed)
-  if (int st = launch_colmax_f64(B, K, N, ldb, bmx, s)) return st;
+  // B^T rows = columns of B: max over k, then tiled digits (transposed read)
+  if (int st = launch_colmax<double>(B, K, N, ldb, bmx, s)) return st;
   {
-    const int64_t tiles = ((K + 31) / 32) * ((N + 31) / 32);
-    const int blocks = static_cast<int>(std::min<int64_t>(tiles, 16 * kSMs));
-    trals::oz_digits_kernel<double><<<blocks, 256, 0, s>>>(B, K, N, ldb, 1, bmx, bd, ldk, eb);
+    const int64_t work = oz_digits_bytes(N, K, kOzBN) / 64;  // (padded row, 16-k chunk) items
+    const int blocks = static_cast<int>(std::min<int64_t>((work + 255) / 256, 16 * kSMs));
+    trals::oz_digits_tiled_kernel<double><<<blocks, 256, 0, s>>>(B, K, N, ldb, 1, bmx, bd, kOzBN, eb);
     if (int st = launch_status()) return st;
-  }
-  trals::OzMaps maps;
-  const int64_t pa = M * lda, pb = N * ldk;
-  for (int d = 0; d < trals::kOzDigits; ++d) {
-    if (!make_map_i8(&maps.a[d], ad + d * pa, K, M, lda, trals::kOzBM) ||
-        !make_map_i8(&maps.b[d], bd + d * pb, K, N, ldk, kOzBN))
-      return TRALS_ERR_CUDA;
   }
   trals::OzArgs g{};
   g.M = M; g.K = K; g.N = N; g.kchunk = sp.kchunk; g.splits = sp.splits;
+  g.mtiles = static_cast<int>((M + trals::kOzBM - 1) / trals::kOzBM);
+  g.ntiles = static_cast<int>((N + kOzBN - 1) / kOzBN);
+  g.kblocks = (K + trals::kOzBK - 1) / trals::kOzBK;
+  g.ad = ad; g.bd = bd;
   g.cmap = cm; g.ea = ea; g.eb = eb; g.C = C; g.ws = ws + w.part;
   using T = trals::OzTile<kOzBN>;
   auto kern = trals::oz8_kernel<kOzBN>;
@@ -567,10 +554,10 @@ int gemm_oz(const int8_t* ad, const int32_t* ea, int64_t lda, int64_t M, int64_t
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(T::SMEM));
     attr = true;
   }
-  dim3 grid(static_cast<unsigned>((N + kOzBN - 1) / kOzBN), static_cast<unsigned>((M + trals::kOzBM - 1) / trals::kOzBM),
-            static_cast<unsigned>(sp.splits));
-  if (grid.y > 65535u) return TRALS_ERR_UNSUPPORTED;
-  kern<<<grid, T::THREADS, T::SMEM, s>>>(maps, g);
+  const int64_t tiles = static_cast<int64_t>(g.mtiles) * g.ntiles * sp.splits;
+  if (tiles > INT32_MAX) return TRALS_ERR_UNSUPPORTED;
+  const int grid = static_cast<int>(std::min<int64_t>(tiles, kSMs));
+  kern<<<grid, T::THREADS, T::SMEM, s>>>(g);
   if (int st = launch_status()) return st;
   if (sp.splits > 1) {
     GemmArgs r{};
@@ -1883,17 +1870,17 @@ int env_tf32(const float* xhi, const float* xlo, int64_t ldx, int64_t pre, int64
 
 // fp32 variant of env() on the int8 tensor cores: X given as digit planes + row exponents,
 // K-major for this side (side 0: rows = pre, side 1: rows = post, the transposed copy).
-int env_oz(const int8_t* xd, const int32_t* xe, int64_t ldx, int64_t pre, int64_t post, int side, const double* H,
-           int r_lo, int r_hi, double* E, int leaf, double* ws, int64_t ws_elems, cudaStream_t s) {
+int env_oz(const int8_t* xd, const int32_t* xe, int64_t pre, int64_t post, int side, const double* H, int r_lo,
+           int r_hi, double* E, int leaf, double* ws, int64_t ws_elems, cudaStream_t s) {
   const int64_t RR = static_cast<int64_t>(r_lo) * r_hi;
   if (side == 0) {
     CMap cm{0, pre, 0, r_lo, r_hi, 1, pre * r_lo};
     if (leaf) cm = CMap{0, pre, 0, RR, r_hi, r_hi, 1};
-    return gemm_oz(xd, xe, ldx, pre, post, RR, H, RR, E, cm, ws, ws_elems, s);
+    return gemm_oz(xd, xe, pre, post, RR, H, RR, E, cm, ws, ws_elems, s);
   }
   CMap cm{0, post, 0, r_lo, r_hi, 1, post * r_lo};
   if (leaf) cm = CMap{0, post, 0, RR, r_hi, r_hi, 1};
-  return gemm_oz(xd, xe, ldx, post, pre, RR, H, RR, E, cm, ws, ws_elems, s);
+  return gemm_oz(xd, xe, post, pre, RR, H, RR, E, cm, ws, ws_elems, s);
 }
 
 int absorb_right(const double* E, int Ra, int64_t pre, int64_t Ib, int Rb, int Rb1, const double* core_zt,
@@ -2106,30 +2093,30 @@ int trals_env_f64(const double* X, int64_t pre, int64_t post, int side, const do
   return env(X, pre, post, side, H, r_lo, r_hi, E, leaf, ws, ws_elems, static_cast<cudaStream_t>(stream));
 }
 
-int64_t trals_oz_ld(int64_t k) { return k < 1 ? 0 : oz_ld(k); }
+int64_t trals_oz_digits_bytes(int64_t rows, int64_t k) {
+  return rows < 1 || k < 1 ? 0 : oz_digits_bytes(rows, k, trals::kOzBM);
+}
 
 int64_t trals_oz_split_ws_elems(int64_t rows, int64_t cols, int transpose) { return transpose ? cols : rows; }
 
-int trals_oz_split_f32(const float* x, int64_t rows, int64_t cols, int transpose, int8_t* digits, int64_t ld,
-                       int32_t* exps, double* ws, int64_t ws_elems, void* stream) {
-  const int64_t out_rows = transpose ? cols : rows, out_cols = transpose ? rows : cols;
+int trals_oz_split_f32(const float* x, int64_t rows, int64_t cols, int transpose, int8_t* digits, int32_t* exps,
+                       double* ws, int64_t ws_elems, void* stream) {
+  const int64_t out_rows = transpose ? cols : rows, K = transpose ? rows : cols;
   if (!x || !digits || !exps || !ws || rows < 1 || cols < 1 || (transpose != 0 && transpose != 1) ||
-      ld < out_cols || (ld & 15) || ws_elems < out_rows)
+      ws_elems < out_rows || (reinterpret_cast<uintptr_t>(digits) & 15u))
     return TRALS_ERR_ARG;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (!transpose) {
     const int blocks = static_cast<int>(std::min<int64_t>((rows + 7) / 8, 64 * kSMs));
     trals::oz_rowmax_kernel<float><<<blocks, 256, 0, s>>>(x, rows, cols, cols, ws);
+    if (int st = launch_status()) return st;
   } else {
-    cudaMemsetAsync(ws, 0, cols * sizeof(double), s);
-    const int64_t rpb = std::max<int64_t>(64, (rows + 255) / 256);
-    dim3 grid(static_cast<unsigned>((cols + 255) / 256), static_cast<unsigned>((rows + rpb - 1) / rpb));
-    trals::oz_colmax_kernel<float><<<grid, 256, 0, s>>>(x, rows, cols, cols, rpb, ws);
+    if (int st = launch_colmax<float>(x, rows, cols, cols, ws, s)) return st;
   }
-  if (int st = launch_status()) return st;
-  const int64_t tiles = ((rows + 31) / 32) * ((cols + 31) / 32);
-  const int blocks = static_cast<int>(std::min<int64_t>(tiles, 16 * kSMs));
-  trals::oz_digits_kernel<float><<<blocks, 256, 0, s>>>(x, rows, cols, cols, transpose, ws, digits, ld, exps);
+  const int64_t work = oz_digits_bytes(out_rows, K, trals::kOzBM) / 64;  // (padded row, 16-k chunk) items
+  const int blocks = static_cast<int>(std::min<int64_t>((work + 255) / 256, 64 * kSMs));
+  trals::oz_digits_tiled_kernel<float><<<blocks, 256, 0, s>>>(x, rows, cols, cols, transpose, ws, digits,
+                                                             trals::kOzBM, exps);
   return launch_status();
 }
 
@@ -2138,14 +2125,11 @@ int64_t trals_env_oz_ws_elems(int64_t pre, int64_t post, int side, int r_lo, int
   return side == 0 ? gemm_oz_ws(pre, post, RR) : gemm_oz_ws(post, pre, RR);
 }
 
-int trals_env_oz(const int8_t* xd, const int32_t* xe, int64_t ldx, int64_t pre, int64_t post, int side,
-                 const double* H, int r_lo, int r_hi, double* E, int leaf, double* ws, int64_t ws_elems,
-                 void* stream) {
-  if (!xd || !xe || !H || !E || !ws || pre < 1 || post < 1 || r_lo < 1 || r_hi < 1 || (side != 0 && side != 1) ||
-      ldx < (side == 0 ? post : pre))
+int trals_env_oz(const int8_t* xd, const int32_t* xe, int64_t pre, int64_t post, int side, const double* H, int r_lo,
+                 int r_hi, double* E, int leaf, double* ws, int64_t ws_elems, void* stream) {
+  if (!xd || !xe || !H || !E || !ws || pre < 1 || post < 1 || r_lo < 1 || r_hi < 1 || (side != 0 && side != 1))
     return TRALS_ERR_ARG;
-  return env_oz(xd, xe, ldx, pre, post, side, H, r_lo, r_hi, E, leaf, ws, ws_elems,
-                static_cast<cudaStream_t>(stream));
+  return env_oz(xd, xe, pre, post, side, H, r_lo, r_hi, E, leaf, ws, ws_elems, static_cast<cudaStream_t>(stream));
 }
 
 int64_t trals_tf32_ld(int64_t cols) { return cols < 1 ? 0 : tf32_ld(cols); }

@@ -102,7 +102,7 @@ class SweepEngine:
         if tuple(x_local.shape) != tuple(self.dl):
             raise ValueError(f"local slab shape {tuple(x_local.shape)} != expected {tuple(self.dl)}")
         self.x = x_local
-        self._xsplit = {}   # fp32: (side, pre, post) -> (digits, exps, ld): X sliced K-major for that side
+        self._xsplit = {}   # fp32: (side, pre, post) -> (digits, exps): X sliced, K-major for that side
         self._x64 = None    # fp32 + exact errors: fp64 copy of X for the residual kernel
         self.fallback_ok = bool(rank_deficient_fallback)
         self.svd_rcond = float(svd_rcond)
@@ -280,15 +280,15 @@ class SweepEngine:
             key = (side, pre, post)
             if key not in self._xsplit:
                 rows, k = (pre, post) if side == 0 else (post, pre)
-                ld = int(self.lib.trals_oz_ld(k))
-                self._xsplit[key] = (torch.empty(4 * rows * ld, dtype=torch.int8, device=self.dev),
-                                     torch.empty(rows, dtype=torch.int32, device=self.dev), ld)
+                self._xsplit[key] = (torch.empty(int(self.lib.trals_oz_digits_bytes(rows, k)), dtype=torch.int8,
+                                                 device=self.dev),
+                                     torch.empty(rows, dtype=torch.int32, device=self.dev))
             self._ws(self.lib.trals_env_oz_ws_elems(pre, post, side, r_lo, r_hi))
 
             def env_step(pre=pre, post=post, side=side, H=H, r_lo=r_lo, r_hi=r_hi, target=target,
                          leaf=int(root_leaf), key=key):
-                xd, xe, ld = self._xsplit[key]
-                L.check(self.lib.trals_env_oz(xd.data_ptr(), xe.data_ptr(), ld, pre, post, side, H.data_ptr(),
+                xd, xe = self._xsplit[key]
+                L.check(self.lib.trals_env_oz(xd.data_ptr(), xe.data_ptr(), pre, post, side, H.data_ptr(),
                                               r_lo, r_hi, target(), leaf, self.gws.data_ptr(), self.gws.numel(),
                                               self._sp()), "env_oz")
         else:
@@ -516,10 +516,10 @@ class SweepEngine:
         if not self.fp32:
             return
         sp = self._sp()
-        for (side, pre, post), (xd, xe, ld) in self._xsplit.items():
+        for (side, pre, post), (xd, xe) in self._xsplit.items():
             need = self.lib.trals_oz_split_ws_elems(pre, post, side)
             ws = torch.empty(max(1, need), dtype=torch.float64, device=self.dev)
-            L.check(self.lib.trals_oz_split_f32(self.x.data_ptr(), pre, post, side, xd.data_ptr(), ld, xe.data_ptr(),
+            L.check(self.lib.trals_oz_split_f32(self.x.data_ptr(), pre, post, side, xd.data_ptr(), xe.data_ptr(),
                                                 ws.data_ptr(), ws.numel(), sp), "oz_split")
         if self._x64 is not None:
             self._x64.copy_(self.x)

@@ -27,6 +27,46 @@ def _farr(ptr, n):
     return np.ctypeslib.as_array((ctypes.c_float * int(n)).from_address(ptr))
 
 
+def _i8arr(ptr, n):
+    ptr = int(ptr.value if isinstance(ptr, ctypes.c_void_p) else ptr)
+    return np.ctypeslib.as_array((ctypes.c_int8 * int(n)).from_address(ptr))
+
+
+def _i32arr(ptr, n):
+    ptr = int(ptr.value if isinstance(ptr, ctypes.c_void_p) else ptr)
+    return np.ctypeslib.as_array((ctypes.c_int32 * int(n)).from_address(ptr))
+
+
+def oz_digits_bytes(rows, k, rows_per_tile=128):
+    """Bytes of the tiled int8 digit layout (include/trals.h, trals_oz_digits_bytes)."""
+    return 4 * (-(-rows // rows_per_tile) * rows_per_tile) * (-(-k // 64) * 64)
+
+
+def oz_offsets(rows, k, plane, rows_per_tile=128):
+    """Byte offsets [rows, k] of one digit plane in the tiled, SWIZZLE_64B layout:
+    [row tile][64-k block][plane][rows_per_tile x 64 B], chunk c of row r at c ^ ((r >> 1) & 3)."""
+    r = np.arange(rows, dtype=np.int64)[:, None]
+    kk = np.arange(k, dtype=np.int64)[None, :]
+    kblocks = -(-k // 64)
+    t, rr, kb, c = r // rows_per_tile, r % rows_per_tile, kk >> 6, kk & 63
+    block = (t * kblocks + kb) * 4 + plane
+    return block * rows_per_tile * 64 + rr * 64 + (((c >> 4) ^ ((rr >> 1) & 3)) << 4) + (c & 15)
+
+
+def oz_slice(v):
+    """Row exponents (|x| < 2^e) and four truncated base-128 digit planes of v [rows, k]."""
+    mx = np.max(np.abs(v), axis=1)
+    e = np.where(mx > 0, np.frexp(mx)[1], 0).astype(np.int32)
+    w = np.ldexp(v, -e[:, None].astype(np.int64))
+    planes = []
+    for _ in range(4):
+        t = w * 128.0
+        q = np.trunc(t)
+        planes.append(q.astype(np.int8))
+        w = t - q
+    return planes, e
+
+
 def _iarr(ptr, n):
     ptr = int(ptr.value if isinstance(ptr, ctypes.c_void_p) else ptr)
     return np.ctypeslib.as_array((ctypes.c_int32 * int(n)).from_address(ptr))
@@ -159,42 +199,34 @@ class FakeTrals:
         return 0
 
     # int8 digit slicing (Ozaki-style) of the fp32 variant's product path
-    def trals_oz_ld(self, k):
-        return (int(k) + 15) // 16 * 16
+    def trals_oz_digits_bytes(self, rows, k):
+        return oz_digits_bytes(rows, k)
 
     def trals_oz_split_ws_elems(self, rows, cols, transpose):
         return cols if transpose else rows
 
-    def trals_oz_split_f32(self, x, rows, cols, transpose, digits, ld, exps, ws, ws_elems, stream):
+    def trals_oz_split_f32(self, x, rows, cols, transpose, digits, exps, ws, ws_elems, stream):
         self._count("oz_split")
         v = _farr(x, rows * cols).reshape(rows, cols).astype(np.float64)
         if transpose:
             v = v.T
-        r, c = v.shape
-        mx = np.max(np.abs(v), axis=1)
-        e = np.where(mx > 0, np.frexp(mx)[1], 0).astype(np.int32)   # |x| < 2^e
-        v = np.ldexp(v, -e[:, None])
-        ptr = int(digits.value if isinstance(digits, ctypes.c_void_p) else digits)
-        planes = np.ctypeslib.as_array((ctypes.c_int8 * (4 * r * ld)).from_address(ptr)).reshape(4, r, ld)
+        r, k = v.shape
+        planes, e = oz_slice(v)
+        buf = _i8arr(digits, oz_digits_bytes(r, k))
+        buf[:] = 0
         for s in range(4):
-            t = v * 128.0
-            q = np.trunc(t)
-            planes[s, :, :c] = q.astype(np.int8)
-            v = t - q
-        eptr = int(exps.value if isinstance(exps, ctypes.c_void_p) else exps)
-        np.ctypeslib.as_array((ctypes.c_int32 * r).from_address(eptr))[:] = e
+            buf[oz_offsets(r, k, s)] = planes[s]
+        _i32arr(exps, r)[:] = e
         return 0
 
     def trals_env_oz_ws_elems(self, pre, post, side, r_lo, r_hi):
         return 1
 
-    def trals_env_oz(self, xd, xe, ldx, pre, post, side, H, r_lo, r_hi, E, leaf, ws, ws_elems, stream):
+    def trals_env_oz(self, xd, xe, pre, post, side, H, r_lo, r_hi, E, leaf, ws, ws_elems, stream):
         rows, k = (pre, post) if side == 0 else (post, pre)
-        ptr = int(xd.value if isinstance(xd, ctypes.c_void_p) else xd)
-        planes = np.ctypeslib.as_array((ctypes.c_int8 * (4 * rows * ldx)).from_address(ptr)).reshape(4, rows, ldx)
-        eptr = int(xe.value if isinstance(xe, ctypes.c_void_p) else xe)
-        e = np.ctypeslib.as_array((ctypes.c_int32 * rows).from_address(eptr)).astype(np.int64)
-        a = sum(planes[s, :, :k].astype(np.float64) * 2.0 ** (-7 * (s + 1)) for s in range(4))
+        buf = _i8arr(xd, oz_digits_bytes(rows, k))
+        e = _i32arr(xe, rows).astype(np.int64)
+        a = sum(buf[oz_offsets(rows, k, s)].astype(np.float64) * 2.0 ** (-7 * (s + 1)) for s in range(4))
         a = np.ldexp(a, e[:, None])
         x = np.ascontiguousarray(a if side == 0 else a.T)
         return self.trals_env_f64(x.ctypes.data, pre, post, side, H, r_lo, r_hi, E, leaf, ws, ws_elems, stream)

@@ -215,18 +215,18 @@ def test_env_oz_matches_f64(pre, post, side, r_lo, r_hi, leaf):
     Slicing keeps 28 bits below each row max (truncated digits: random ~2^-28 x max/|x|
     per element), so the product is good to a few 1e-8, below fp32 rounding itself (6e-8)."""
     from paper_2210_11362_b200 import _lib as L
+    from fake_trals import oz_offsets
     lib = L.lib()
     rng = np.random.default_rng(pre + post + r_lo)
     x32 = torch.from_numpy(rng.standard_normal((pre, post)).astype(np.float32)).cuda()
     K = post if side == 0 else pre
     rows = pre if side == 0 else post
     H = cuda(rng.standard_normal((K, r_lo * r_hi)))
-    ld = lib.trals_oz_ld(K)
-    digits = torch.empty(4 * rows * ld, dtype=torch.int8, device="cuda")
+    digits = torch.empty(lib.trals_oz_digits_bytes(rows, K), dtype=torch.int8, device="cuda")
     exps = torch.empty(rows, dtype=torch.int32, device="cuda")
     s = int(torch.cuda.current_stream().cuda_stream)
     sws = torch.empty(lib.trals_oz_split_ws_elems(pre, post, side), dtype=torch.float64, device="cuda")
-    L.check(lib.trals_oz_split_f32(x32.data_ptr(), pre, post, side, digits.data_ptr(), ld, exps.data_ptr(),
+    L.check(lib.trals_oz_split_f32(x32.data_ptr(), pre, post, side, digits.data_ptr(), exps.data_ptr(),
                                    sws.data_ptr(), sws.numel(), s), "oz_split")
     n_out = rows * r_lo * r_hi
     ref = torch.empty(n_out, dtype=torch.float64, device="cuda")
@@ -236,12 +236,14 @@ def test_env_oz_matches_f64(pre, post, side, r_lo, r_hi, leaf):
     L.check(lib.trals_env_f64(x64.data_ptr(), pre, post, side, H.data_ptr(), r_lo, r_hi, ref.data_ptr(), leaf,
                               ws.data_ptr(), ws.numel(), s), "env_f64")
     wso = torch.empty(lib.trals_env_oz_ws_elems(pre, post, side, r_lo, r_hi), dtype=torch.float64, device="cuda")
-    L.check(lib.trals_env_oz(digits.data_ptr(), exps.data_ptr(), ld, pre, post, side, H.data_ptr(), r_lo, r_hi,
+    L.check(lib.trals_env_oz(digits.data_ptr(), exps.data_ptr(), pre, post, side, H.data_ptr(), r_lo, r_hi,
                              got.data_ptr(), leaf, wso.data_ptr(), wso.numel(), s), "env_oz")
     torch.cuda.synchronize()
-    # the digits rebuild X to 28 bits below each row's max
-    d = digits.view(4, rows, ld)[:, :, :K].double()
-    a = sum(d[j] * 2.0 ** (-7 * (j + 1)) for j in range(4)) * torch.pow(2.0, exps.double())[:, None]
-    xs = x64 if side == 0 else x64.t()
-    assert torch.max(torch.abs(a - xs) / torch.abs(xs).amax(dim=1, keepdim=True)).item() < 2.0 ** -27
+    # the tiled, swizzled digits rebuild X to 28 bits below each row's max
+    if rows * K <= 4_000_000:
+        buf = digits.cpu().numpy()
+        a = sum(buf[oz_offsets(rows, K, j)].astype(np.float64) * 2.0 ** (-7 * (j + 1)) for j in range(4))
+        a = np.ldexp(a, exps.cpu().numpy().astype(np.int64)[:, None])
+        xs = x64.cpu().numpy() if side == 0 else x64.cpu().numpy().T
+        assert np.max(np.abs(a - xs) / np.abs(xs).max(axis=1, keepdims=True)) < 2.0 ** -27
     assert rel(got.cpu().numpy(), ref.cpu().numpy()) < 5e-8
