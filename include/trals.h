@@ -213,6 +213,12 @@ int64_t trals_spd_fallback_ws_elems(int64_t rows, int m);
 int trals_spd_fallback_f64(const double* d_S, int m, const double* d_M, int64_t rows, double* d_Z, int* d_info,
                            int mode, double rcond, double* d_ws, int64_t ws_elems, void* stream);
 
+/* Axis reversal (io.py:10-11, read_tensor's reshape(order="F").copy()): src is
+ * first-index-fastest over dims[0..N-1], dst the same tensor last-index-fastest
+ * (C order).  N <= 16; src and dst must not alias.  Used to land a .dten payload
+ * uploaded verbatim into the engine's C-order X on the device. */
+int trals_reverse_axes_f64(const double* d_src, int N, const int64_t* h_dims, double* d_dst, void* stream);
+
 /* Sum of squares of n doubles into d_out[0] (tensor_ops.py:237-239 norm) and the
  * number of non-finite entries into d_out[1] (validation.py:53-54). */
 int64_t trals_sumsq_ws_elems(void);

@@ -49,6 +49,7 @@ _SIGNATURES = {
     "trals_chol_solve_f64": (c_int, [_dp, _dp, _dp, c_int, _dp, c_int64, _dp, _dp, c_int64, c_void_p]),
     "trals_spd_fallback_ws_elems": (c_int64, [c_int64, c_int]),
     "trals_spd_fallback_f64": (c_int, [_dp, c_int, _dp, c_int64, _dp, _dp, c_int, c_double, _dp, c_int64, c_void_p]),
+    "trals_reverse_axes_f64": (c_int, [_dp, c_int, POINTER(c_int64), _dp, c_void_p]),
     "trals_sumsq_ws_elems": (c_int64, []),
     "trals_sumsq_f64": (c_int, [_dp, c_int64, _dp, _dp, c_void_p]),
     "trals_sumsq_f32": (c_int, [_dp, c_int64, _dp, _dp, c_void_p]),

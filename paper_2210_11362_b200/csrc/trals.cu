@@ -1717,6 +1717,60 @@ int hh_qr(const double* G, int I, int nc, double* R, double* ws, int64_t ws_elem
 }
 
 // C(m, n) = F[m * ncols + n] scattered through a CMap
+// Axis reversal of a dense N-d tensor: src first-index-fastest (Fortran, the .dten
+// payload order, io.py:10-11) -> dst last-index-fastest (C, the engine's X).  The
+// first and last axes are swapped through 32 x 32 shared-memory tiles (reads run
+// along axis 0 of src, writes along axis N-1 of dst, both coalesced); the middle
+// axes are reversed by index arithmetic, one tile column per middle index.
+constexpr int kRevMaxN = 16;
+struct RevDims {
+  int N;
+  int64_t d[kRevMaxN];
+};
+
+__global__ void __launch_bounds__(256) reverse_axes_kernel(const double* __restrict__ src, RevDims rd,
+                                                           double* __restrict__ dst) {
+  __shared__ double tile[32][33];
+  const int N = rd.N;
+  const int64_t da = rd.d[0], dz = rd.d[N - 1];
+  int64_t mid = 1;
+  for (int j = 1; j < N - 1; ++j) mid *= rd.d[j];
+  const int64_t ta = (da + 31) / 32, tz = (dz + 31) / 32, tiles = ta * tz * mid;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+    const int64_t q = t / (ta * tz), rem = t - q * (ta * tz);
+    const int64_t a0 = (rem % ta) * 32, z0 = (rem / ta) * 32;
+    // middle multi-index q = i_1 + d_1 (i_2 + ...) -> offsets in both layouts:
+    // src (F) = sum_j i_j prod_{k<j} d_k, dst (C) = sum_j i_j prod_{k>j} d_k
+    int64_t idx[kRevMaxN];
+    int64_t soff = 0, sZ = da, qq = q;
+    for (int j = 1; j < N - 1; ++j) {
+      idx[j] = qq % rd.d[j];
+      qq /= rd.d[j];
+      soff += idx[j] * sZ;
+      sZ *= rd.d[j];
+    }
+    int64_t doff = 0, dA = dz;
+    for (int j = N - 2; j >= 1; --j) {
+      doff += idx[j] * dA;
+      dA *= rd.d[j];
+    }
+    // sZ = src stride of axis N-1, dA = dst stride of axis 0
+#pragma unroll
+    for (int j = 0; j < 32; j += 8) {
+      const int64_t a = a0 + tx, z = z0 + ty + j;
+      tile[ty + j][tx] = (a < da && z < dz) ? src[soff + a + z * sZ] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 32; j += 8) {
+      const int64_t z = z0 + tx, a = a0 + ty + j;
+      if (a < da && z < dz) dst[doff + a * dA + z] = tile[tx][ty + j];
+    }
+    __syncthreads();
+  }
+}
+
 __global__ void reshuffle_kernel(const double* __restrict__ F, int64_t rows, int64_t cols, CMap cm,
                                  double* __restrict__ C) {
   const int64_t total = rows * cols;
@@ -2061,6 +2115,28 @@ int trals_gemm_f64(const double* A, int64_t sAp, int64_t sAm, int64_t sAk, int64
   if (!h_cmap) return TRALS_ERR_ARG;
   CMap cm{h_cmap[0], h_cmap[1], h_cmap[2], h_cmap[3], h_cmap[4], h_cmap[5], h_cmap[6]};
   return gemm(A, sAp, sAm, sAk, P, M, K, N, B, ldb, C, cm, beta, ws, ws_elems, static_cast<cudaStream_t>(stream));
+}
+
+int trals_reverse_axes_f64(const double* src, int N, const int64_t* dims, double* dst, void* stream) {
+  if (!src || !dst || !dims || N < 1 || N > kRevMaxN || src == dst) return TRALS_ERR_ARG;
+  RevDims rd{};
+  rd.N = N;
+  int64_t total = 1;
+  for (int j = 0; j < N; ++j) {
+    if (dims[j] < 1) return TRALS_ERR_ARG;
+    rd.d[j] = dims[j];
+    total *= dims[j];
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (N == 1) {
+    if (cudaMemcpyAsync(dst, src, total * sizeof(double), cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+      return TRALS_ERR_CUDA;
+    return TRALS_OK;
+  }
+  const int64_t tiles = ((dims[0] + 31) / 32) * ((dims[N - 1] + 31) / 32) * (total / (dims[0] * dims[N - 1]));
+  const int blocks = static_cast<int>(std::min<int64_t>(tiles, 32 * kSMs));
+  reverse_axes_kernel<<<blocks, 256, 0, s>>>(src, rd, dst);
+  return launch_status();
 }
 
 int trals_core_relayout_f64(const double* src, int sl, int Ra, int64_t I, int Rb, double* dst, int dl,

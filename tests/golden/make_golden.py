@@ -95,6 +95,28 @@ def small_cases():
     return cases
 
 
+def io_and_synth_cases():
+    """.dten bytes written by the reference (io.py) and the three synthetic generators (synthetic.py)."""
+    from tenring import io as tio
+    x = np.arange(60, dtype=np.float64).reshape(3, 4, 5) * 0.5 - 7.25
+    x[1, 2, 3] = np.nan
+    tio.write_tensor(os.path.join(OUT, "io_3x4x5.dten"), x)
+    rec = {}
+    specs = {
+        "gaussian": SynthSpec(order=3, dim=12, rank=3, kind="gaussian", noise=1e-2, seed=71),
+        "congruent": SynthSpec(order=3, dim=12, rank=3, kind="congruent", gamma=0.9, noise=1e-3, seed=72),
+        "student_t": SynthSpec(order=4, dim=10, rank=2, kind="student_t", theta=0.7, dof=3, noise=0.0,
+                               seed=(7, 3)),
+    }
+    for kind, spec in specs.items():
+        xs, cores = make_dataset(spec)
+        rec[f"{kind}_x"] = xs
+        for j, g in enumerate(cores):
+            rec[f"{kind}_core_{j}"] = g
+    np.savez_compressed(os.path.join(OUT, "synth_kinds.npz"), **rec)
+    print("wrote io_3x4x5.dten, synth_kinds.npz", flush=True)
+
+
 BASE_CONFIGS = {
     # name: (order, dim, rank_true, noise, seed_data, rank_fit, seed_init, sweeps, variants)
     "c1": (3, 100, 5, 1e-3, 0, 5, 1, 10, ("ne",)),
@@ -141,8 +163,12 @@ if __name__ == "__main__":
     ap.add_argument("--only", default=None)
     args = ap.parse_args()
     print("tenring", tenring.__version__, "numpy", np.__version__)
+    if args.only == "io":
+        io_and_synth_cases()
+        sys.exit(0)
     if args.only is None:
         small_cases()
+        io_and_synth_cases()
     if args.big or args.only:
         for name in BASE_CONFIGS:
             if args.only and name != args.only:
