@@ -617,11 +617,34 @@ def als_qrne(x, cfg):
     return d.run(sweep, prepare)
 
 
-SOLVERS = {"ne": als_ne, "qr": als_qr, "qrne": als_qrne}
+def als_plain(x, cfg):
+    """solvers.py:323-349 (Alg. 1, TR-ALS): explicit subchain, QR least squares per block."""
+    d = _Driver(x, cfg, "als")
+    if d.x_norm == 0.0:
+        return d.run(None)
+    xs = [unfold_cyclic(d.x, n) for n in range(d.N)]  # solvers.py:331
+
+    def sweep(cores):
+        for n in range(d.N):
+            with _Clock(d.buckets, "subchain"):
+                a = unfold_cyclic(chain_without(cores, n), 1)
+            with _Clock(d.buckets, "solve"):
+                q, r = qr_signed(a)
+                c = q.T @ xs[n].T
+                z = d.tri_block(r, c.T)
+            cores[n] = fold_classical(z, 1, d.shape_of(n))
+        # solvers.py:199-200 (c_last, r_a_last, core_mat of the last block)
+        d.last["terms"] = (float(np.vdot(c, r @ z.T)), float(np.vdot(r.T @ r, z.T @ z)))
+        d.last["c"], d.last["r"], d.last["z"] = c, r, z
+
+    return d.run(sweep)
+
+
+SOLVERS = {"als": als_plain, "ne": als_ne, "qr": als_qr, "qrne": als_qrne}
 
 
 def solve(x, variant, cfg):
-    """solvers.py:504-520 for the three north-star variants."""
+    """solvers.py:504-520."""
     if variant not in SOLVERS:
         raise ValueError(f"unknown variant {variant!r}")
     return SOLVERS[variant](x, cfg)

@@ -73,7 +73,7 @@ class SweepEngine:
     def __init__(self, x_local: torch.Tensor, dims, ranks, variant: str, *, shard_mode=None, lo=0, hi=None,
                  group=None, world_size: int = 1, rank_deficient_fallback=True, svd_rcond=1e-12,
                  _test_lib=None):
-        if variant not in ("ne", "qr", "qrne"):
+        if variant not in ("als", "ne", "qr", "qrne"):
             raise ValueError(f"unsupported device variant {variant!r}")
         # `_test_lib` lets the CPU test-suite drive this exact schedule through a numpy
         # model of the C-ABI (tests/fake_trals.py); the solvers never pass it.
@@ -381,15 +381,17 @@ class SweepEngine:
         self._tree(cur, m + 1, b)
 
     def _r0_nonsquare(self, n):
-        """QR variant: the reference's R0 is non-square when prod_{j!=n} k_j < R_n R_{n+1}
-        (k_j = min(I_j, R_j R_{j+1}), ring.py:236-249) and it always takes the SVD solve
-        (solvers.py:264-266) -- no Cholesky, no fallback count."""
-        if self.variant != "qr":
+        """QR / ALS: the reference's triangular factor is non-square when it has fewer rows
+        than R_n R_{n+1} -- QR: prod_{j!=n} k_j with k_j = min(I_j, R_j R_{j+1})
+        (ring.py:236-249); ALS: prod_{j!=n} I_j, the rows of the subchain unfolding
+        (solvers.py:337-339) -- and then it always takes the SVD solve (solvers.py:264-266):
+        no Cholesky, no fallback count."""
+        if self.variant not in ("qr", "als"):
             return False
         ks = 1
         for j in range(self.N):
             if j != n:
-                ks *= min(self.dims[j], self.R(j) * self.R(j + 1))
+                ks *= self.dims[j] if self.variant == "als" else min(self.dims[j], self.R(j) * self.R(j + 1))
         return ks < self.R(n) * self.R(n + 1)
 
     def _factor(self, n):
@@ -409,7 +411,7 @@ class SweepEngine:
                                                   self.side_gws.data_ptr(), self.side_gws.numel(), self._sp()),
                     "gram_chain")
         self.steps.append(Step("other", gram_chain, f"S{n}", stream="side"))
-        check_degen = 1 if self.variant == "qr" else 0
+        check_degen = 1 if self.variant in ("qr", "als") else 0
 
         def factor(S=S, rr=rr, check_degen=check_degen):
             L.check(self.lib.trals_cholesky_f64(S.data_ptr(), rr, self.U.data_ptr(), self.Lo.data_ptr(),
@@ -438,7 +440,7 @@ class SweepEngine:
         # numerical fallbacks of the reference (linalg.py:77-81, solvers.py:262-273): the kernel is a
         # no-op unless the factorisation flagged a failure, so it stays in the (graph-captured) sweep
         rr_rows = self.dims[n]
-        if self.variant == "qr":
+        if self.variant in ("qr", "als"):
             mode = 2 if self._r0_nonsquare(n) else (1 if self.fallback_ok else None)
             rcond = self.svd_rcond
         else:

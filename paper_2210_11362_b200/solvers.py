@@ -24,7 +24,7 @@ from .host import (check_element_budget, check_ranks, core_ranks, make_rng,
                    random_cores, validate_cores, zero_cores)
 
 VARIANTS = ("als", "ne", "qr", "qrne")          # solvers.py:55
-DEVICE_VARIANTS = ("ne", "qr", "qrne")
+DEVICE_VARIANTS = ("als", "ne", "qr", "qrne")
 ERROR_MODES = ("exact", "cheap", "none")         # solvers.py:56
 BUCKETS = ("subchain", "mttsp", "solve", "gramqr", "other")  # solvers.py:57
 SVD_RCOND_DEFAULT = 1e-12                        # linalg.py:20
@@ -122,8 +122,6 @@ def _run(x, config, variant):
     import torch
 
     _validate(x, config, variant)
-    if variant not in DEVICE_VARIANTS:
-        raise NotImplementedError("tr_als (Alg. 1) is outside the B200 hot path; use ne/qr/qrne")
     t = _host_or_device_tensor(x, config.dtype)
     dims = tuple(int(d) for d in t.shape)
     N = len(dims)
@@ -257,7 +255,7 @@ def _raise_on_info(eng, config, report):
     report.fallback_count = int(info[L.INFO_FALLBACKS])  # solvers.py:262-279
     if info[L.INFO_ASYM]:
         raise ValueError("matrix is not symmetric within 1e-8 relative")  # linalg.py:70-72
-    if info[L.INFO_DEGEN] or (config is not None and eng.variant == "qr" and info[L.INFO_CHOL]):
+    if info[L.INFO_DEGEN] or (config is not None and eng.variant in ("qr", "als") and info[L.INFO_CHOL]):
         # only left set when rank_deficient_fallback is off (linalg.py:96-99, solvers.py:269-270)
         idx = int(info[L.INFO_DEGEN] or info[L.INFO_CHOL]) - 1
         raise DegenerateTriangularError(idx, 0.0, 0.0)
@@ -301,9 +299,15 @@ def tr_als_qrne(x, config):
 
 
 def tr_als(x, config):
-    """Alg. 1 is not on the B200 path (reference solvers.py:323-349)."""
-    _validate(x, config, "als")
-    raise NotImplementedError("tr_als (Alg. 1) is outside the B200 hot path; use ne/qr/qrne")
+    """Plain TR-ALS (Alg. 1; reference solvers.py:323-349). Returns (cores, report).
+
+    The reference materialises each subchain unfolding A_n (prod_{j!=n} I_j x R^2)
+    and solves by its QR.  Here A_n is never formed: the right-hand side is the
+    same environment-tree MTTSP as NE, and R is the nonnegative-diagonal Cholesky
+    factor of S_n = A_n^T A_n -- the same R in exact arithmetic -- with the
+    reference's triangular-solve policy (degeneracy floor, counted SVD fallback,
+    uncounted min-norm solve when A_n has fewer rows than R^2, solvers.py:262-273)."""
+    return _run(x, config, "als")
 
 
 _SOLVERS = {"als": tr_als, "ne": tr_als_ne, "qr": tr_als_qr, "qrne": tr_als_qrne}

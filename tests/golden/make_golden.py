@@ -81,17 +81,17 @@ def small_cases():
         print("wrote", name, flush=True)
 
     # SPEC.md:638 parity protocol shape: N=3, I=30, R=3 (noiseless)
-    ring_case("spec_n3_i30_r3", (30, 30, 30), (3, 3, 3), (3, 3, 3), 0.0, 11, 12, 10, ("ne", "qr", "qrne"))
+    ring_case("spec_n3_i30_r3", (30, 30, 30), (3, 3, 3), (3, 3, 3), 0.0, 11, 12, 10, ("ne", "qr", "qrne", "als"))
     # non-uniform dims and ranks, N=4, with noise
-    ring_case("nonuni_n4", (6, 7, 5, 8), (2, 3, 2, 2), (2, 3, 4, 2), 1e-2, 21, 22, 6, ("ne", "qr", "qrne"))
+    ring_case("nonuni_n4", (6, 7, 5, 8), (2, 3, 2, 2), (2, 3, 4, 2), 1e-2, 21, 22, 6, ("ne", "qr", "qrne", "als"))
     # N=5, over-specified rank
     ring_case("n5_i6", (6, 5, 6, 4, 5), (2, 2, 2, 2, 2), (3, 2, 3, 2, 2), 1e-3, 31, 32, 5, ("ne", "qrne"))
     # N=2 edge (matrix)
-    ring_case("n2_mat", (20, 30), (3, 3), (3, 2), 1e-2, 41, 42, 6, ("ne", "qr", "qrne"))
+    ring_case("n2_mat", (20, 30), (3, 3), (3, 2), 1e-2, 41, 42, 6, ("ne", "qr", "qrne", "als"))
     # odd / prime sizes exercise every tail path of the kernels
-    ring_case("odd_n3", (13, 7, 11), (2, 3, 2), (3, 2, 3), 1e-2, 51, 52, 5, ("ne", "qr"))
-    # rank-deficient blocks: prod_{j != n} I_j < R^2 -> gelsy fallback (NE/QRNE), SVD solve (QR)
-    ring_case("rankdef_n3", (2, 2, 30), (2, 2, 2), (3, 3, 3), 1e-2, 61, 62, 3, ("ne", "qr", "qrne"))
+    ring_case("odd_n3", (13, 7, 11), (2, 3, 2), (3, 2, 3), 1e-2, 51, 52, 5, ("ne", "qr", "als"))
+    # rank-deficient blocks: prod_{j != n} I_j < R^2 -> gelsy fallback (NE/QRNE), SVD solve (QR, ALS)
+    ring_case("rankdef_n3", (2, 2, 30), (2, 2, 2), (3, 3, 3), 1e-2, 61, 62, 3, ("ne", "qr", "qrne", "als"))
     return cases
 
 

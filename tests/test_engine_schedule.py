@@ -36,6 +36,21 @@ def test_schedule_matches_reference_sweeps(name):
         assert rel(cores[j], g[f"ne_core_{j}"]) < 1e-6
 
 
+@pytest.mark.parametrize("name", ["spec_n3_i30_r3", "nonuni_n4", "n2_mat", "odd_n3"])
+def test_als_schedule_matches_reference(name):
+    """Alg. 1 (tr_als): NE's right-hand side, R = chol(S_n) with the triangular-solve policy;
+    against the reference's Alg. 1 (explicit subchain + QR) per sweep."""
+    g = load_golden(name)
+    dims = tuple(int(d) for d in g["dims"])
+    N = len(dims)
+    ranks = [int(r) for r in g["ranks"]]
+    cores, errs, _ = run_engine(g["x"], ranks, "als", golden_cores(g, "init", N), int(g["sweeps"]),
+                                lib=FakeTrals(), exact=True)
+    np.testing.assert_allclose(errs, g["als_exact_errors"], rtol=0, atol=1e-9)
+    for j in range(N):
+        assert rel(cores[j], g[f"als_core_{j}"]) < 1e-6
+
+
 @pytest.mark.parametrize("name", SMALL)
 @pytest.mark.parametrize("exact", [False, True])
 def test_fp32_schedule_matches_reference(name, exact):
@@ -91,7 +106,8 @@ SEMI_NORMAL_QR = pytest.mark.xfail(
     strict=False)
 
 
-@pytest.mark.parametrize("variant", ["ne", pytest.param("qr", marks=SEMI_NORMAL_QR), "qrne"])
+@pytest.mark.parametrize("variant", ["ne", pytest.param("qr", marks=SEMI_NORMAL_QR), "qrne",
+                                     pytest.param("als", marks=SEMI_NORMAL_QR)])
 def test_rank_deficient_fallback_schedule(variant):
     """prod_{j!=n} I_j < R^2: the fallback step of the schedule fires and errors match the reference."""
     g = load_golden(RANKDEF)

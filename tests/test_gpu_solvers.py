@@ -16,7 +16,7 @@ SMALL = ["spec_n3_i30_r3", "nonuni_n4", "n5_i6", "n2_mat", "odd_n3"]
 
 
 @pytest.mark.parametrize("name", SMALL)
-@pytest.mark.parametrize("variant", ["ne", "qr", "qrne"])
+@pytest.mark.parametrize("variant", ["ne", "qr", "qrne", "als"])
 @pytest.mark.parametrize("mode", ["cheap", "exact"])
 def test_small_goldens(name, variant, mode):
     from paper_2210_11362_b200 import AlsConfig, decompose
@@ -94,7 +94,8 @@ SEMI_NORMAL_QR = pytest.mark.xfail(
     strict=False)
 
 
-@pytest.mark.parametrize("variant", ["ne", pytest.param("qr", marks=SEMI_NORMAL_QR), "qrne"])
+@pytest.mark.parametrize("variant", ["ne", pytest.param("qr", marks=SEMI_NORMAL_QR), "qrne",
+                                     pytest.param("als", marks=SEMI_NORMAL_QR)])
 @pytest.mark.parametrize("mode", ["cheap", "exact"])
 def test_rank_deficient_blocks(variant, mode):
     """prod_{j!=n} I_j < R^2: Cholesky fails (NE/QRNE -> gelsy fallback, counted) or R0 is

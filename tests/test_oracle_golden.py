@@ -48,7 +48,7 @@ def test_solver_pins(name):
     ranks = tuple(int(r) for r in g["ranks"])
     init = golden_cores(g, "init", N)
     sweeps = int(g["sweeps"])
-    for v in ("ne", "qr", "qrne"):
+    for v in ("ne", "qr", "qrne", "als"):
         if f"{v}_exact_errors" not in g:
             continue
         for mode in ("exact", "cheap"):
