@@ -675,7 +675,9 @@ class SweepEngine:
         self.stream = cap
         try:
             with torch.cuda.stream(cap):
-                g.capture_begin()
+                # relaxed: first-use cudaFuncSetAttribute calls (dynamic shared memory opt-in) may
+                # happen inside the capture when no eager sweep preceded it
+                g.capture_begin(capture_error_mode="relaxed")
                 self.run_sweep()
                 if with_error:
                     self.error_step(self.err_cur, exact=exact)
