@@ -119,7 +119,7 @@ def io_and_synth_cases():
 
 BASE_CONFIGS = {
     # name: (order, dim, rank_true, noise, seed_data, rank_fit, seed_init, sweeps, variants)
-    "c1": (3, 100, 5, 1e-3, 0, 5, 1, 10, ("ne",)),
+    "c1": (3, 100, 5, 1e-3, 0, 5, 1, 10, ("ne", "als")),
     "c2": (4, 64, 8, 1e-2, 2, 8, 3, 20, ("ne", "qr")),
     "c3": (3, 500, 10, 1e-3, 4, 10, 5, 10, ("ne", "qr")),
     "c4": (5, 40, 6, 1e-2, 6, 8, 7, 15, ("ne",)),

@@ -43,7 +43,7 @@ def test_baseline_configs(name):
     g = load_golden(f"base_{name}")
     order, dim, rt, sd, rf, si, sweeps = (int(v) for v in g["recipe"])
     x, _ = O.synth(O.Recipe(order=order, dim=dim, rank=rt, noise=float(g["noise"]), seed=sd))
-    for v in ("ne", "qr"):
+    for v in ("ne", "qr", "als"):
         if f"{v}_exact_errors" not in g:
             continue
         cores, rep = decompose(x, v, AlsConfig(ranks=(rf,) * order, max_iters=sweeps, seed=si))
