@@ -254,3 +254,30 @@ def test_spec_criterion9_cheap_matches_exact():
             _, rc = decompose(x, v, AlsConfig(error_mode="cheap", **cfg))
             _, rx = decompose(x, v, AlsConfig(error_mode="exact", **cfg))
             np.testing.assert_allclose(rc.errors, rx.errors, rtol=0, atol=1e-6)
+
+
+@pytest.mark.parametrize("dims,ranks,counts", [
+    ((1, 4, 5), (2, 2, 2), True),
+    # exactly singular blocks: whether a factorisation "fails" is decided by the last bit
+    # of a zero pivot (LAPACK vs this kernel), so only the solution is compared
+    ((3, 1, 1, 6), (1, 2, 2, 1), False),
+    ((4, 3, 5, 2, 3, 4), (2, 2, 3, 2, 2, 2), True),
+    ((2, 3, 2, 3, 2, 3, 2), (2, 1, 2, 2, 1, 2, 2), True),
+    ((7, 2), (1, 1), True),
+])
+@pytest.mark.parametrize("variant", ["ne", "qr", "qrne", "als"])
+def test_odd_shapes_vs_oracle(dims, ranks, counts, variant):
+    """Degenerate and long rings (unit modes, rank-1 bonds, N = 2..7) against the oracle:
+    every GEMM shape edge of the environment tree and the small-matrix solves."""
+    from paper_2210_11362_b200 import AlsConfig, decompose
+    rng = np.random.default_rng(sum(dims) * 10 + len(dims))
+    x = rng.standard_normal(dims)
+    init = O.gaussian_ring(dims, ranks, O.philox(len(dims) + 3))
+    cfg = dict(ranks=ranks, max_iters=3, init_cores=init, error_mode="exact")
+    cores, rep = decompose(x, variant, AlsConfig(**cfg))
+    ocores, orep = O.solve(x, variant, O.Config(**cfg))
+    np.testing.assert_allclose(rep.errors, orep.errors, rtol=0, atol=1e-9)
+    if counts:
+        assert rep.fallback_count == orep.fallback_count
+    for j in range(len(dims)):
+        assert rel(cores[j], ocores[j]) < 1e-6
