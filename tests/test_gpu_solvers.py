@@ -259,7 +259,8 @@ def test_spec_criterion9_cheap_matches_exact():
 @pytest.mark.parametrize("dims,ranks,counts", [
     ((1, 4, 5), (2, 2, 2), True),
     # exactly singular blocks: whether a factorisation "fails" is decided by the last bit
-    # of a zero pivot (LAPACK vs this kernel), so only the solution is compared
+    # of a zero pivot (LAPACK vs this kernel) and the block solution is not unique, so the
+    # fitted tensor (not the cores or the fallback count) is compared
     ((3, 1, 1, 6), (1, 2, 2, 1), False),
     ((4, 3, 5, 2, 3, 4), (2, 2, 3, 2, 2, 2), True),
     ((2, 3, 2, 3, 2, 3, 2), (2, 1, 2, 2, 1, 2, 2), True),
@@ -279,5 +280,7 @@ def test_odd_shapes_vs_oracle(dims, ranks, counts, variant):
     np.testing.assert_allclose(rep.errors, orep.errors, rtol=0, atol=1e-9)
     if counts:
         assert rep.fallback_count == orep.fallback_count
-    for j in range(len(dims)):
-        assert rel(cores[j], ocores[j]) < 1e-6
+        for j in range(len(dims)):
+            assert rel(cores[j], ocores[j]) < 1e-6
+    else:
+        assert rel(O.dense_from_ring(cores), O.dense_from_ring(ocores)) < 1e-9
