@@ -31,6 +31,7 @@ from __future__ import annotations
 import math
 from dataclasses import dataclass, field
 
+import numpy as np
 import torch
 
 from . import _lib as L
@@ -47,6 +48,12 @@ def _prod(v):
 
 class _HostStream:
     cuda_stream = 0
+
+
+def _assert_close(actual, desired, rel=1e-10):
+    """The reference's debug-mode identity check (solvers.py:215-218)."""
+    scale = max(1.0, float(np.max(np.abs(desired))))
+    np.testing.assert_allclose(actual, desired, rtol=rel, atol=rel * scale)
 
 
 @dataclass
@@ -72,7 +79,7 @@ class SweepEngine:
 
     def __init__(self, x_local: torch.Tensor, dims, ranks, variant: str, *, shard_mode=None, lo=0, hi=None,
                  group=None, world_size: int = 1, rank_deficient_fallback=True, svd_rcond=1e-12,
-                 _test_lib=None):
+                 debug_checks=False, _test_lib=None):
         if variant not in ("als", "ne", "qr", "qrne"):
             raise ValueError(f"unsupported device variant {variant!r}")
         # `_test_lib` lets the CPU test-suite drive this exact schedule through a numpy
@@ -105,6 +112,9 @@ class SweepEngine:
         self._xsplit = {}   # fp32: (side, pre, post) -> (digits, exps): X sliced, K-major for that side
         self._x64 = None    # fp32 + exact errors: fp64 copy of X for the residual kernel
         self.fallback_ok = bool(rank_deficient_fallback)
+        # AlsConfig.debug_checks (solvers.py:376-377, 432-438, 485-487): assert the coefficient
+        # Gram against the explicitly assembled subchain every block (host sync; eager only)
+        self.debug_checks = bool(debug_checks)
         self.svd_rcond = float(svd_rcond)
         self.stream = torch.cuda.current_stream(self.dev) if x_local.is_cuda else _HostStream()
         self.stats = EngineStats()
@@ -429,6 +439,8 @@ class SweepEngine:
             import torch.distributed as dist
             self.steps.append(Step("mttsp", lambda M=M: dist.all_reduce(M, group=self.group), f"allreduce M{n}"))
         self.steps.append(Step("solve", None, f"join chol{n}", kind="join"))
+        if self.debug_checks:
+            self.steps.append(Step("other", lambda n=n: self._debug_check(n), f"debug S{n}"))
 
         def solve(n=n, M=M, rr=rr):
             L.check(self.lib.trals_chol_solve_f64(self.U.data_ptr(), self.Lo.data_ptr(), self.chol_aux.data_ptr(), rr,
@@ -485,6 +497,60 @@ class SweepEngine:
                                                  self.Rslice.data_ptr(), L.LAYOUT_SLICE, sp), "relayout")
         L.check(self.lib.trals_core_gram_f64(self.Rslice.data_ptr(), ra, k, rb, self.E[n].data_ptr(),
                                              self.gws.data_ptr(), self.gws.numel(), sp), "core_gram")
+
+    def _debug_check(self, n):
+        """The reference's debug identities for block n (solvers.py:376-377 NE, 485-487 QRNE,
+        432-438 QR): the Gram chain S_n equals A^T A of the explicitly assembled subchain
+        unfolding -- A = G^{!=n}_[2] for NE / ALS, V_[2] of the R-tensor subchain for QR / QRNE
+        (for QR also R0^T R0 = S_n) -- within the reference's tolerance
+        (_assert_close, rel 1e-10: scale = max(1, max |desired|))."""
+        N, sp = self.N, self._sp()
+        order = [(n + 1 + j) % N for j in range(N - 1)]
+        cores = []
+        for j in order:
+            ra, i, rb = self.R(j), self.dims[j], self.R(j + 1)
+            if not self.use_rqr:
+                cores.append((self.Gc[j], i))
+                continue
+            k = min(i, ra * rb)  # R-tensor of core j's lateral QR (ring.py:236-249), layout C
+            rm = self._empty(k * ra * rb)
+            ws = self._empty(max(1, self.lib.trals_core_qr_ws_elems(i, ra * rb)))
+            L.check(self.lib.trals_core_qr_f64(self.Gt[j].data_ptr(), i, ra * rb, rm.data_ptr(), ws.data_ptr(),
+                                               ws.numel(), sp), "core_qr")
+            rc = self._empty(ra, k, rb)
+            L.check(self.lib.trals_core_relayout_f64(rm.data_ptr(), L.LAYOUT_ZT, ra, k, rb, rc.data_ptr(),
+                                                     L.LAYOUT_C, sp), "relayout")
+            cores.append((rc, k))
+        bd = [k for _, k in cores]
+        br = [self.R(j) for j in order] + [self.R(n)]
+        first = self._empty(bd[0], br[0], br[1])
+        L.check(self.lib.trals_core_relayout_f64(cores[0][0].data_ptr(), L.LAYOUT_C, br[0], bd[0], br[1],
+                                                 first.data_ptr(), L.LAYOUT_SLICE, sp), "relayout")
+        rows = _prod(bd)
+        rr = br[0] * br[-1]
+        H = self._empty(rows * rr)
+        tmp = self._empty(max(1, self.lib.trals_half_chain_tmp_elems(len(bd), L.i64_array(bd), L.i32_array(br))))
+        need, pre = 1, bd[0]
+        for j in range(1, len(bd)):
+            need = max(need, self.lib.trals_gemm_ws_elems(1, pre * br[0], br[j], bd[j] * br[j + 1]))
+            pre *= bd[j]
+        need = max(need, self.lib.trals_gemm_ws_elems(1, rr, rows, rr))
+        ws = self._empty(need)
+        L.check(self.lib.trals_half_chain_f64(len(bd), L.i64_array(bd), L.i32_array(br), first.data_ptr(),
+                                              L.ptr_array([c.data_ptr() for c, _ in cores]), H.data_ptr(),
+                                              tmp.data_ptr(), ws.data_ptr(), ws.numel(), 0, sp), "half_chain")
+        # H[k][(r_{n+1}, r_n)] -> column r_n + R_n r_{n+1}: the S_n index order
+        G = self._empty(rr * rr)
+        L.check(self.lib.trals_gemm_f64(H.data_ptr(), 0, 1, rr, 1, rr, rows, rr, H.data_ptr(), rr, G.data_ptr(),
+                                        L.i64_array([0, 1 << 40, 0, rr, 1 << 40, 0, 1]), 0, ws.data_ptr(),
+                                        ws.numel(), sp), "gram")
+        s_dev = self.S[n].reshape(rr, rr)
+        want = G.reshape(rr, rr).cpu().numpy()
+        got = s_dev.cpu().numpy()
+        _assert_close(got, want)
+        if self.variant == "qr" and not self._r0_nonsquare(n):
+            u = self.U.reshape(-1)[:rr * rr].reshape(rr, rr).cpu().numpy()
+            _assert_close(u.T @ u, got, rel=1e-9)
 
     # ----------------------------------------------------------------- running
     def _sp(self):

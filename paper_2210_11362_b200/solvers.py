@@ -145,7 +145,7 @@ def _run(x, config, variant):
         src = t.narrow(shard, lo, hi - lo)
     from .engine import SweepEngine
     key = (dims, tuple(ranks), variant, dev.index, world, shard, lo, hi, bool(config.rank_deficient_fallback),
-           float(config.svd_rcond), config.dtype)
+           float(config.svd_rcond), config.dtype, bool(config.debug_checks))
     eng = _PLAN_CACHE.pop(key, None)
     if eng is None:
         x_local = torch.empty(tuple(src.shape), dtype=t.dtype, device=dev)
@@ -160,7 +160,7 @@ def _run(x, config, variant):
     if eng is None:
         eng = SweepEngine(x_local, dims, ranks, variant, shard_mode=shard, lo=lo, hi=hi, group=group,
                           world_size=world, rank_deficient_fallback=config.rank_deficient_fallback,
-                          svd_rcond=config.svd_rcond)
+                          svd_rcond=config.svd_rcond, debug_checks=config.debug_checks)
     eng.stream = torch.cuda.current_stream(dev)
     eng.prepare_x()
     if config.error_mode == "exact":
@@ -195,7 +195,7 @@ def _run(x, config, variant):
 
     track = config.error_mode in ("exact", "cheap")
     exact = config.error_mode == "exact"
-    use_graph = (world == 1 and not config.timing_buckets)
+    use_graph = (world == 1 and not config.timing_buckets and not config.debug_checks)
     if use_graph and (eng.graph is None or eng.graph_exact != exact):
         eng.capture(with_error=True, exact=exact)
     errs = torch.zeros((config.max_iters, 3), dtype=torch.float64, device=x_local.device)

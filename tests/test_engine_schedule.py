@@ -120,3 +120,41 @@ def test_rank_deficient_fallback_schedule(variant):
     # the fit is exact: compare the exact errors (the cheap identity sits at its sqrt(eps) floor here)
     np.testing.assert_allclose(errs, g[f"{variant}_exact_errors"], rtol=0, atol=1e-9)
     assert lib.calls["fallback"] == N * int(g["sweeps"])
+
+
+@pytest.mark.parametrize("variant", ["ne", "qr", "qrne", "als"])
+def test_debug_checks_schedule(variant):
+    """AlsConfig.debug_checks: the explicit-subchain identity runs every block and passes."""
+    g = load_golden("nonuni_n4")
+    dims = tuple(int(d) for d in g["dims"])
+    N = len(dims)
+    ranks = [int(r) for r in g["ranks"]]
+    x = np.asarray(g["x"])
+    import torch
+
+    from paper_2210_11362_b200.engine import SweepEngine
+    lib = FakeTrals()
+    eng = SweepEngine(torch.from_numpy(np.ascontiguousarray(x)), dims, ranks, variant, debug_checks=True,
+                      _test_lib=lib)
+    eng.compute_xnorm2()
+    eng.set_cores(golden_cores(g, "init", N))
+    eng.run_sweep()
+    assert sum(1 for st in eng.steps if st.name.startswith("debug")) == N
+
+
+def test_debug_check_detects_a_wrong_gram():
+    import torch
+
+    from paper_2210_11362_b200.engine import SweepEngine
+    g = load_golden("nonuni_n4")
+    dims = tuple(int(d) for d in g["dims"])
+    ranks = [int(r) for r in g["ranks"]]
+    eng = SweepEngine(torch.from_numpy(np.ascontiguousarray(g["x"])), dims, ranks, "ne", debug_checks=True,
+                      _test_lib=FakeTrals())
+    eng.compute_xnorm2()
+    eng.set_cores(golden_cores(g, "init", len(dims)))
+    next(st for st in eng.steps if st.name == "S0").fn()  # S_0 of the current cores
+    eng._debug_check(0)                                     # consistent: passes
+    eng.S[0].mul_(1.0 + 1e-6)                               # corrupted: the check must fire
+    with pytest.raises(AssertionError):
+        eng._debug_check(0)

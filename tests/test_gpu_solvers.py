@@ -284,3 +284,17 @@ def test_odd_shapes_vs_oracle(dims, ranks, counts, variant):
             assert rel(cores[j], ocores[j]) < 1e-6
     else:
         assert rel(O.dense_from_ring(cores), O.dense_from_ring(ocores)) < 1e-9
+
+
+@pytest.mark.parametrize("variant", ["ne", "qr", "qrne", "als"])
+def test_debug_checks_on_device(variant):
+    """AlsConfig(debug_checks=True) evaluates the reference's identities on the GPU every block
+    and the run still matches the goldens (the checks are read-only)."""
+    from paper_2210_11362_b200 import AlsConfig, decompose
+    g = load_golden("nonuni_n4")
+    N = len(g["dims"])
+    ranks = tuple(int(r) for r in g["ranks"])
+    cfg = AlsConfig(ranks=ranks, max_iters=int(g["sweeps"]), init_cores=golden_cores(g, "init", N),
+                    error_mode="exact", debug_checks=True)
+    cores, rep = decompose(g["x"], variant, cfg)
+    np.testing.assert_allclose(rep.errors, g[f"{variant}_exact_errors"], rtol=0, atol=1e-9)
