@@ -40,29 +40,15 @@ struct Cfg {
   int BM, BN;
   int id;
 };
-// (WM, WN, TM, TN): 128x64, 128x80, 128x32, 128x24, 128x16, 128x8, 64x112
-constexpr Cfg kCfgs[] = {{128, 64, 0}, {128, 80, 1}, {128, 32, 2}, {128, 24, 3},
-                         {128, 16, 4}, {128, 8, 5},  {64, 112, 6}};
-
-Cfg pick_cfg(int64_t N) {
-  Cfg best = kCfgs[0];
-  double best_score = -1;
-  for (const Cfg& c : kCfgs) {
-    const int64_t nt = (N + c.BN - 1) / c.BN;
-    const double eff = static_cast<double>(N) / static_cast<double>(nt * c.BN);
-    // favour wide tiles (fewer re-reads of A) once padding waste is similar
-    const double score = eff + 0.002 * c.BN;
-    if (score > best_score + 1e-12) {
-      best_score = score;
-      best = c;
-    }
-  }
-  return best;
-}
+// (WM, WN, TM, TN): 128x64, 128x80, 128x32, 128x24, 128x16, 128x8, 64x112, and the
+// 64-row tiles 64x8, 64x16, 64x32, 64x64 that spread small products over more SMs
+constexpr Cfg kCfgs[] = {{128, 64, 0}, {128, 80, 1}, {128, 32, 2}, {128, 24, 3}, {128, 16, 4}, {128, 8, 5},
+                         {64, 112, 6}, {64, 8, 7},   {64, 16, 8},  {64, 32, 9},  {64, 64, 10}};
 
 struct SplitPlan {
   int splits;
   int64_t kchunk;
+  double cost = 0.0;  // modelled seconds (plan_split only)
 };
 
 // Split-K choice: model the time of s splits as
@@ -77,13 +63,17 @@ SplitPlan plan_split(const Cfg& c, int64_t P, int64_t M, int64_t K, int64_t N) {
   const int64_t tiles = P * ((M + c.BM - 1) / c.BM) * ((N + c.BN - 1) / c.BN);
   const int64_t slots = 2 * kSMs;
   const int64_t smax = std::max<int64_t>(1, std::min<int64_t>(64, K / (4 * trals::kBK)));
-  const double t_tile = 2.0 * c.BM * c.BN * static_cast<double>(K) / (37.0e12 / slots);
   const double out_bytes = 8.0 * static_cast<double>(P) * M * N;
   int64_t best_s = 1;
   double best = 1e300;
   for (int64_t sp = 1; sp <= smax; ++sp) {
     const int64_t waves = (tiles * sp + slots - 1) / slots;
-    double cost = static_cast<double>(waves) / sp * t_tile;
+    // a CTA's K chunk: DMMA time at a slot's share of the peak, but never below the
+    // pipeline's per-K-tile latency (small tiles are latency-, not flop-bound)
+    const double kc = std::ceil(static_cast<double>(K) / sp);
+    const double t_unit = std::max(2.0 * c.BM * c.BN * kc / (37.0e12 / slots),
+                                   std::ceil(kc / trals::kBK) * 0.25e-6);
+    double cost = static_cast<double>(waves) * t_unit;
     if (sp > 1) cost += 3e-6 + (sp + 1) * out_bytes / 6.0e12;
     if (cost < best * (1 - 1e-9)) {
       best = cost;
@@ -94,7 +84,26 @@ SplitPlan plan_split(const Cfg& c, int64_t P, int64_t M, int64_t K, int64_t N) {
   kchunk = ((kchunk + trals::kBK - 1) / trals::kBK) * trals::kBK;
   if (kchunk <= 0) kchunk = trals::kBK;
   const int64_t splits = std::max<int64_t>(1, (K + kchunk - 1) / kchunk);
-  return {static_cast<int>(splits), kchunk};
+  return {static_cast<int>(splits), kchunk, best};
+}
+
+// Tile shape for one product: the modelled time of every configuration (with its own
+// split-K plan), ties within 3 % going to the larger tile (fewer operand re-reads).
+Cfg pick_cfg_for(int64_t P, int64_t M, int64_t K, int64_t N) {
+  double cost[sizeof(kCfgs) / sizeof(kCfgs[0])];
+  double best = 1e300;
+  for (size_t i = 0; i < sizeof(kCfgs) / sizeof(kCfgs[0]); ++i) {
+    cost[i] = plan_split(kCfgs[i], P, M, K, N).cost;
+    best = std::min(best, cost[i]);
+  }
+  Cfg pick = kCfgs[0];
+  int area = -1;
+  for (size_t i = 0; i < sizeof(kCfgs) / sizeof(kCfgs[0]); ++i)
+    if (cost[i] <= best * 1.03 && kCfgs[i].BM * kCfgs[i].BN > area) {
+      pick = kCfgs[i];
+      area = kCfgs[i].BM * kCfgs[i].BN;
+    }
+  return pick;
 }
 
 template <int WM, int WN, int TM, int TN, bool AK, int VEC>
@@ -124,6 +133,10 @@ int launch_cfg(int id, const GemmArgs& g, cudaStream_t s) {
     case 4: return launch_tile<8, 1, 2, 2, AK, VEC>(g, s);
     case 5: return launch_tile<8, 1, 2, 1, AK, VEC>(g, s);
     case 6: return launch_tile<4, 2, 2, 7, AK, VEC>(g, s);
+    case 7: return launch_tile<8, 1, 1, 1, AK, VEC>(g, s);
+    case 8: return launch_tile<8, 1, 1, 2, AK, VEC>(g, s);
+    case 9: return launch_tile<4, 2, 2, 2, AK, VEC>(g, s);
+    case 10: return launch_tile<4, 2, 2, 4, AK, VEC>(g, s);
   }
   return TRALS_ERR_ARG;
 }
@@ -172,7 +185,7 @@ int gemm(const double* A, int64_t sAp, int64_t sAm, int64_t sAk, int64_t P, int6
     if (beta) return TRALS_OK;
     return TRALS_ERR_ARG;
   }
-  const Cfg c = pick_cfg(N);
+  const Cfg c = pick_cfg_for(P, M, K, N);
   SplitPlan sp = plan_split(c, P, M, K, N);
   if (sp.splits > 1) {
     const int64_t need = static_cast<int64_t>(sp.splits) * P * M * N;
@@ -214,7 +227,7 @@ int gemm(const double* A, int64_t sAp, int64_t sAm, int64_t sAk, int64_t P, int6
 }
 
 int64_t gemm_ws(int64_t P, int64_t M, int64_t K, int64_t N) {
-  const Cfg c = pick_cfg(N);
+  const Cfg c = pick_cfg_for(P, M, K, N);
   const SplitPlan sp = plan_split(c, P, M, K, N);
   return sp.splits > 1 ? static_cast<int64_t>(sp.splits) * P * M * N : 0;
 }
