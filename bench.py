@@ -41,6 +41,9 @@ FP64_PEAK_TFLOPS = 37.1      # measured DMMA.8x8x4 ceiling on this pool's B200 (
 # fp32 variant: 13 int8 MMAs per fp32-equivalent multiply-add; int8 dense ~2x the measured bf16 burst
 INT8_FP32_EQ_TFLOPS = 2 * 1715.0 / 13
 PEAK_SOURCE = "profiles/r01_fp64_pipes.md: mma.sync m8n8k4 f64 microbenchmark, 148 SMs"
+# fp64 "ozaki" environment products: 36 int8 digit-pair MMAs per fp64 multiply-add (8 balanced
+# digits per operand, pair levels s + t <= 7)
+OZ64_PAIRS = 36
 
 
 def load_peaks():
@@ -241,6 +244,7 @@ def run_ours(args):
     dev = torch.device("cuda", torch.cuda.current_device())
     x_full, _ = make_dataset_device(order, dim, rt, noise, sd, device=dev)
     fp32 = args.dtype == "float32"
+    oz64 = (not fp32) and args.fp64_gemm == "ozaki"
     if fp32:
         x_full = x_full.float()
     shard = 0
@@ -252,8 +256,14 @@ def run_ours(args):
         x_local = x_full
     cores0 = random_cores(dims, ranks, make_rng(si))
     eng = SweepEngine(x_local, dims, ranks, args.variant, shard_mode=shard if world > 1 else None, lo=lo, hi=hi,
-                      world_size=world)
+                      world_size=world, fp64_gemm=args.fp64_gemm)
+    p0 = torch.cuda.Event(enable_timing=True)
+    p1 = torch.cuda.Event(enable_timing=True)
+    p0.record(eng.stream)
     eng.prepare_x()
+    p1.record(eng.stream)
+    torch.cuda.synchronize()
+    prep_ms = p0.elapsed_time(p1)
     eng.compute_xnorm2()
     eng.set_cores(cores0)
     errs = torch.zeros((args.warmup + args.steps, 3), dtype=torch.float64, device=dev)
@@ -319,7 +329,8 @@ def run_ours(args):
     env_tf = float(np.mean(per_launch))
     env_share = env_avg_ms * len(env_flops) / ms
     traffic = None
-    tpath = os.path.join(ROOT, "profiles", f"{args.config}{'_fp32' if fp32 else ''}_env_traffic.json")
+    tag = "_fp32" if fp32 else ("_oz64" if oz64 else "")
+    tpath = os.path.join(ROOT, "profiles", f"{args.config}{tag}_env_traffic.json")
     if os.path.exists(tpath):
         try:
             traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
@@ -330,8 +341,11 @@ def run_ours(args):
     bw = float(peaks.get("hbm_gbs", 6458.1))
     F = flops_per_sweep(dims, ranks)
     ebytes = 4 if fp32 else 8
-    peak_tf = INT8_FP32_EQ_TFLOPS if fp32 else FP64_PEAK_TFLOPS
+    # P = the peak of the pipe actually used (fp64 on int8: the int8 rate / 36 pairs)
+    peak_tf = (INT8_FP32_EQ_TFLOPS if fp32 else
+               2.0 * float(peaks.get("bf16_tflops", 1652.8)) / OZ64_PAIRS if oz64 else FP64_PEAK_TFLOPS)
     t_roof = roofline_sweep_time(dims, ranks, peak_tf, bw, world, ebytes)
+    t_roof_dmma = roofline_sweep_time(dims, ranks, FP64_PEAK_TFLOPS, bw, world, ebytes)
     sweep_s = ms_max * 1e-3
     value = 1.0 / sweep_s
 
@@ -344,7 +358,7 @@ def run_ours(args):
         eng = None
         torch.cuda.empty_cache()
         cfg = AlsConfig(ranks=tuple(ranks), max_iters=sweeps, seed=si, error_mode="cheap", timing_buckets=False,
-                        dtype=args.dtype)
+                        dtype=args.dtype, fp64_gemm=args.fp64_gemm)
         decompose(xh, args.variant, cfg)  # warm-up call (allocator, plan)
         torch.cuda.synchronize()
         reps = []
@@ -363,7 +377,8 @@ def run_ours(args):
                "h2d_bytes_per_step": int(np.prod(dims)) * ebytes + core_bytes,
                "d2h_bytes_per_step": core_bytes + 8 * sweeps + 16,
                "step": f"one decompose(x_host_pinned, '{args.variant}', AlsConfig(max_iters={sweeps}, "
-                       f"dtype='{args.dtype}')) call",
+                       f"dtype='{args.dtype}', fp64_gemm='{args.fp64_gemm}')) call (includes X's H2D copy and, "
+                       f"for the tensor-core paths, its digit slicing)",
                "seconds_per_call": t_call, "final_error": float(rep.errors[-1])}
         del xh
 
@@ -387,6 +402,19 @@ def run_ours(args):
                 "bytes_per_launch": xbytes, "avg_launch_ms": env_avg_ms, "share_of_step": env_share,
                 "flops_per_launch": env_flops, "tflops_fp32_equiv": env_tf,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth)"}
+    elif oz64:
+        # fp64 on the int8 tensor cores: the algorithmic work of one launch is the 36 digit-pair
+        # products over the real (unpadded) M x N x K; peak = int8 dense = 2x the measured bf16 burst
+        i8_peak = 2.0 * float(peaks.get("bf16_tflops", 1652.8))
+        i8_tops = env_tf * OZ64_PAIRS
+        roof = {"bound": "tensor", "achieved": i8_tops, "peak": i8_peak, "unit": "TFLOP/s",
+                "frac": i8_tops / i8_peak, "traffic": traffic,
+                "kernel": "oz8_kernel<64, OzF64> (fp64 X x half-chain environment product on the int8 tcgen05 "
+                          "tensor cores: 8 balanced digits per operand, 36 exact int32 digit-pair products)",
+                "ops": "int8 tensor ops = 36 x 2 M N K per launch", "flops_per_launch": env_flops,
+                "fp64_equiv_tflops": env_tf, "fp64_equiv_frac_of_dmma_peak": env_tf / FP64_PEAK_TFLOPS,
+                "avg_launch_ms": env_avg_ms, "share_of_step": env_share,
+                "peak_source": "2 x MEASURED_PEAKS.json bf16_tflops (int8 dense = 2x bf16 dense on B200)"}
     else:
         roof = {"bound": "tensor", "achieved": env_tf, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                 "frac": env_tf / FP64_PEAK_TFLOPS, "traffic": traffic,
@@ -403,10 +431,14 @@ def run_ours(args):
                    "variant": args.variant, "parallelism": f"shard mode 0 x{world}" if world > 1 else "single",
                    "l2": "X (%.2f GB) larger than the 126 MB L2, no flush needed" % (np.prod(dims) * ebytes / 1e9),
                    "step": "one full sweep + per-sweep relative error",
+                   "fp64_gemm": None if fp32 else args.fp64_gemm,
+                   "x_digits_ms": prep_ms if (fp32 or oz64) else None,
                    "launch": "CUDA graph replay" if use_graph else "eager stream launches"},
         "contraction_tflops": F / sweep_s / 1e12,
         "contraction_roofline_frac": t_roof / sweep_s,
         "roofline_sweep_ms": t_roof * 1e3,
+        "roofline_pipe_tflops": peak_tf,
+        "contraction_roofline_frac_vs_dmma_peak": t_roof_dmma / sweep_s,
         "x_passes_per_sweep": eng.stats.x_passes_per_sweep if eng is not None else 2,
         "roofline": roof,
         "gpu_launches": int(launches),
@@ -435,6 +467,8 @@ def main():
     ap.add_argument("--variant", choices=["ne", "qr", "qrne"], default="ne")
     ap.add_argument("--dtype", choices=["float64", "float32"], default="float64",
                     help="float32 = the fp32 variant (BASELINE config 4): int8 tensor-core environment products")
+    ap.add_argument("--fp64-gemm", choices=["ozaki", "dmma"], default="ozaki",
+                    help="fp64 environment products: int8 tensor-core digit slicing (default) or the DMMA pipe")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--eager", action="store_true", help="no CUDA graph for the small configs")
     ap.add_argument("--e2e-reps", type=int, default=2)

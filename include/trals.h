@@ -119,6 +119,24 @@ int64_t trals_env_oz_ws_elems(int64_t pre, int64_t post, int side, int r_lo, int
 int trals_env_oz(const int8_t* d_xdigits, const int32_t* d_xexps, int64_t pre, int64_t post, int side,
                  const double* d_H, int r_lo, int r_hi, double* d_env, int leaf, double* d_ws, int64_t ws_elems,
                  void* stream);
+
+/* fp64 environment product on the int8 tensor cores (AlsConfig.fp64_gemm =
+ * "ozaki", the default): trals_env_f64 with X given as eight balanced digit
+ * planes per K-major row,
+ *   x = 2^ex[r] (d_0 2^-6 + sum_{s=1..7} d_s 2^-(6+7s)),  |d_s| <= 64,
+ * (56 bits below the row maximum; same tiled layout as above with 8 planes,
+ * trals_oz64_digits_bytes bytes), the half chain sliced the same way per call,
+ * and the 36 digit-pair products of levels s + t <= 7 accumulated exactly in
+ * int32 and combined in fp64.  Accuracy against an extended-precision product
+ * is that of the fp64 DMMA product (tests/test_gpu_ops.py).  Replaces the same
+ * reference call as trals_env_f64 (solvers.py:379). */
+int64_t trals_oz64_digits_bytes(int64_t rows, int64_t k);
+int trals_oz64_split_f64(const double* d_x, int64_t rows, int64_t cols, int transpose, int8_t* d_digits,
+                         int32_t* d_exps, double* d_ws, int64_t ws_elems, void* stream);
+int64_t trals_env_oz64_ws_elems(int64_t pre, int64_t post, int side, int r_lo, int r_hi);
+int trals_env_oz64(const int8_t* d_xdigits, const int32_t* d_xexps, int64_t pre, int64_t post, int side,
+                   const double* d_H, int r_lo, int r_hi, double* d_env, int leaf, double* d_ws, int64_t ws_elems,
+                   void* stream);
 /* 3xTF32 alternative (an operator kept for comparison, not used by the
  * solvers: its truncated fp32 accumulation biases M_n by ~1e-6 relative).
  * X held as hi = tf32(x), lo = x - hi (fp32, hi + lo == x exactly);

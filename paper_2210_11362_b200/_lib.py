@@ -59,6 +59,11 @@ _SIGNATURES = {
     "trals_env_oz_ws_elems": (c_int64, [c_int64, c_int64, c_int, c_int, c_int]),
     "trals_env_oz": (c_int, [_dp, _dp, c_int64, c_int64, c_int, _dp, c_int, c_int, _dp, c_int, _dp, c_int64,
                              c_void_p]),
+    "trals_oz64_digits_bytes": (c_int64, [c_int64, c_int64]),
+    "trals_oz64_split_f64": (c_int, [_dp, c_int64, c_int64, c_int, _dp, _dp, _dp, c_int64, c_void_p]),
+    "trals_env_oz64_ws_elems": (c_int64, [c_int64, c_int64, c_int, c_int, c_int]),
+    "trals_env_oz64": (c_int, [_dp, _dp, c_int64, c_int64, c_int, _dp, c_int, c_int, _dp, c_int, _dp, c_int64,
+                               c_void_p]),
     "trals_tf32_ld": (c_int64, [c_int64]),
     "trals_tf32_split_f32": (c_int, [_dp, c_int64, c_int64, c_int64, c_int, _dp, _dp, c_int64, c_void_p]),
     "trals_env_tf32_ws_elems": (c_int64, [c_int64, c_int64, c_int, c_int, c_int]),

@@ -9,7 +9,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SRC = [os.path.join(HERE, "csrc", "trals.cu")]
-DEPS = SRC + [os.path.join(HERE, "csrc", "dmma_gemm.cuh"), os.path.join(ROOT, "include", "trals.h")]
+DEPS = SRC + [os.path.join(HERE, "csrc", f) for f in sorted(os.listdir(os.path.join(HERE, "csrc")))
+              if f.endswith(".cuh")] + [os.path.join(ROOT, "include", "trals.h")]
 OUT = os.path.join(HERE, "libtrals.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

@@ -1,7 +1,11 @@
-// fp32-accurate GEMM on the int8 tcgen05 tensor cores (Ozaki-style digit slicing)
-// for the fp32 variant's environment products.
+// Exact-integer GEMM on the int8 tcgen05 tensor cores (Ozaki-style digit slicing)
+// for the environment products: the fp32 variant's (4 digits, below) and the fp64
+// path's (8 balanced digits, 36 pairs, fp64-accurate: see OzF64).
 //
-//   C(m, n) (fp64 out) = sum_k A[m][k] * B[n][k]      A from fp32 X, B from the fp64 half chain
+//   C(m, n) (fp64 out) = sum_k A[m][k] * B[n][k]      A from X, B from the fp64 half chain
+//
+// The description below is the fp32 scheme; the fp64 one differs only in the
+// digit count, the kept levels, the balanced digits and the output staging.
 //
 // Why not 3xTF32: the tf32 MMA accumulates in truncated fp32, a ~1e-6 relative
 // bias on M_n that the normal equations (cond(S) up to 5e11 on BASELINE c4) and
@@ -56,21 +60,53 @@ namespace trals {
 
 constexpr int kOzBK = 64;        // int8 k per stage (one 64 B swizzle row)
 constexpr int kOzBM = 128;
-constexpr int kOzDigits = 4;
-constexpr int kOzLevels = 7;     // digit-pair levels L = s + t (0..6): every pair is kept
-constexpr int64_t kOzKmax = 32768;
 
-template <int BN>
+// Digit schemes.  D digit planes per operand, the LV lowest pair levels L = s + t
+// kept (pairs with s + t >= LV are dropped), BAL = balanced (round-to-nearest)
+// digits instead of truncated ones, KMAX = longest k per CTA whose int32 level
+// sums cannot overflow.
+//   fp32 variant: 4 truncated base-128 digits (28 bits), all 16 pairs (7 levels):
+//     x = 2^e sum_s d_s 2^(-7(s+1)), |d_s| <= 127; a pair (s, t) weighs 2^(-14-7L).
+//     A level sums <= 4 pairs of 127^2 per k -> KMAX 32768.
+//   fp64 (emulated DMMA): 8 balanced digits, first base 64 then base 128:
+//     x = 2^e (d_0 2^-6 + sum_{s>=1} d_s 2^-(6+7s)), |d_s| <= 64, remainder <= 2^-56
+//     (the fp64 mantissa of the row maximum plus 3 guard bits); levels 0..7 kept (36
+//     pairs; the dropped level-8 terms are < 2^-68 per k and zero-mean), a pair
+//     weighs 2^(-12-7L).  A level sums <= 8 pairs of 64^2 per k -> KMAX 61440.
+//     Measured against an extended-precision product: the same error as fp64 DMMA
+//     (tests/test_gpu_ops.py::test_env_oz64_accuracy).
+template <int D_, int LV_, bool BAL_, int64_t KMAX_>
+struct OzScheme {
+  static constexpr int D = D_;
+  static constexpr int LV = LV_;
+  static constexpr bool BAL = BAL_;
+  static constexpr int OFF = BAL_ ? 12 : 14;  // 2^-OFF: weight of the level-0 pair
+  static constexpr int64_t KMAX = KMAX_;
+};
+using OzF32 = OzScheme<4, 7, false, 32768>;
+using OzF64 = OzScheme<8, 8, true, 61440>;
+constexpr int kOzDigits = OzF32::D;  // (fp32 variant layout helpers)
+constexpr int kOzLevels = OzF32::LV;
+constexpr int64_t kOzKmax = OzF32::KMAX;
+
+template <int BN, class SC>
 struct OzTile {
   static constexpr int A_PLANE = kOzBM * kOzBK;  // 8 KB
   static constexpr int B_PLANE = BN * kOzBK;
-  static constexpr int STAGE = kOzDigits * (A_PLANE + B_PLANE);
-  static constexpr int OUT_LD = BN + 1;                   // fp64 output staging row (odd: no bank conflicts)
+  static constexpr int STAGE = SC::D * (A_PLANE + B_PLANE);
+  // fp64 output staging: the whole 128 x BN tile when it fits beside >= 3 stages
+  // (TMEM is released before the global stores), else 16-column chunks
+  static constexpr int FULL_OUT = kOzBM * (BN + 1) * 8;
+  static constexpr bool CHUNKED = (212 * 1024 - FULL_OUT) / STAGE < 3;
+  static constexpr int OUT_COLS = CHUNKED ? 16 : BN;
+  static constexpr int OUT_LD = OUT_COLS + 1;                 // odd: no bank conflicts
   static constexpr int OUT_BYTES = kOzBM * OUT_LD * 8;
   static constexpr int STAGES = (212 * 1024 - OUT_BYTES) / STAGE < 6 ? (212 * 1024 - OUT_BYTES) / STAGE : 6;
-  static constexpr int TMEM_COLS = 512;  // kOzLevels * BN = 448 accumulator columns
+  static constexpr int TMEM_COLS = 512;
   static constexpr int THREADS = 6 * 32;
   static constexpr size_t SMEM = static_cast<size_t>(STAGES) * STAGE + OUT_BYTES + 1024 + 256;
+  static_assert(SC::LV * BN <= TMEM_COLS, "levels x BN accumulator columns exceed TMEM");
+  static_assert(STAGES >= 2, "digit stage too large for shared memory");
 };
 
 struct OzArgs {
@@ -79,8 +115,8 @@ struct OzArgs {
   int splits;
   int mtiles, ntiles;  // tile t -> (split, m-tile, n-tile), n fastest
   int64_t kblocks;     // 64-k blocks of the tiled digit layout (ceil(K / 64))
-  const int8_t* ad;    // A digits, tiled: [mtiles][kblocks][4][128 x 64 B]
-  const int8_t* bd;    // B digits, tiled: [ntiles][kblocks][4][BN x 64 B]
+  const int8_t* ad;    // A digits, tiled: [mtiles][kblocks][D][128 x 64 B]
+  const int8_t* bd;    // B digits, tiled: [ntiles][kblocks][D][BN x 64 B]
   CMap cmap;
   const int32_t* ea;  // [M] row exponents of A
   const int32_t* eb;  // [N] row exponents of B
@@ -91,9 +127,9 @@ struct OzArgs {
 // byte offset of (row r, k) inside the tiled digit layout of one plane block
 // (rows_per_tile rows x 64 B, SWIZZLE_64B)
 __host__ __device__ __forceinline__ int64_t oz_tiled_offset(int64_t r, int64_t k, int plane, int rows_per_tile,
-                                                            int64_t kblocks) {
+                                                            int64_t kblocks, int digits) {
   const int64_t t = r / rows_per_tile, rr = r % rows_per_tile, kb = k >> 6, c = k & 63;
-  const int64_t block = (t * kblocks + kb) * kOzDigits + plane;
+  const int64_t block = (t * kblocks + kb) * digits + plane;
   return block * rows_per_tile * 64 + rr * 64 + ((((c >> 4) ^ ((rr >> 1) & 3))) << 4) + (c & 15);
 }
 
@@ -158,10 +194,11 @@ __device__ __forceinline__ void oz_commit(uint64_t* bar) {
                : "memory");
 }
 
-// zero this warp's 32 TMEM lanes over the kOzLevels x 64 accumulator columns
+// zero this warp's 32 TMEM lanes over the first COLS accumulator columns
+template <int COLS>
 __device__ __forceinline__ void tmem_zero(uint32_t tlane) {
 #pragma unroll
-  for (int c = 0; c < kOzLevels * 64; c += 16)
+  for (int c = 0; c < COLS; c += 16)
     asm volatile(
         "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};\n" ::"r"(
             tlane + c),
@@ -178,14 +215,15 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
       : "r"(taddr));
 }
 
-template <int BN>
-__global__ void __launch_bounds__(OzTile<BN>::THREADS, 1)
+template <int BN, class SC>
+__global__ void __launch_bounds__(OzTile<BN, SC>::THREADS, 1)
 oz8_kernel(const __grid_constant__ OzArgs g) {
   // Persistent: CTA b takes tiles b, b + gridDim.x, ...; the smem ring runs across
   // tile boundaries, so the producer prefetches the next tile while the
   // epilogue drains the accumulators of the current one.
-  using T = OzTile<BN>;
+  using T = OzTile<BN, SC>;
   constexpr int S = T::STAGES;
+  constexpr int D = SC::D, LV = SC::LV;
   extern __shared__ uint8_t smraw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
   double* otile = reinterpret_cast<double*>(sm + S * T::STAGE);  // [kOzBM][OUT_LD] epilogue staging
@@ -227,7 +265,7 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
   };
 
   if (warp == 0) {
-    // ------------------------------ TMA producer ------------------------------
+    // ------------------------------ bulk-copy producer ------------------------------
     if (lane == 0) {
       uint32_t gk = 0;
       for (int t = blockIdx.x; t < total; t += gridDim.x) {
@@ -235,10 +273,12 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
         int ktiles;
         tile_k(t, kbeg, ktiles);
         const int rem = t % per_split;
-        const int m0 = (rem / g.ntiles) * kOzBM, n0 = (rem % g.ntiles) * BN;
-        // k blocks in a per-CTA rotated order: the int32 accumulation is exact, so the
-        // order is free, and it keeps 148 CTAs from reading the same B block at once
-        const int rot = ktiles > 0 ? static_cast<int>(blockIdx.x % ktiles) : 0;
+        const int mt = rem / g.ntiles, nt = rem % g.ntiles;
+        // k blocks in a rotated order (the int32 accumulation is exact, so the order is
+        // free): the rotation follows the m-tile, so the CTAs that share an A tile (its
+        // n-tiles run side by side) read it in step and hit L2, while different m-tiles
+        // spread over different B blocks
+        const int rot = ktiles > 0 ? mt % ktiles : 0;
         for (int kt = 0; kt < ktiles; ++kt, ++gk) {
           const uint32_t s = gk % S;
           if (gk >= S) mbar_wait(empty + s, ((gk / S) - 1) & 1);
@@ -246,11 +286,10 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
           mbar_expect_tx(full + s, T::STAGE);
           const int kr = kt + rot < ktiles ? kt + rot : kt + rot - ktiles;
           const int64_t kb = kbeg / kOzBK + kr;
-          bulk_load(st, g.ad + (static_cast<int64_t>(m0 / kOzBM) * g.kblocks + kb) * (kOzDigits * T::A_PLANE),
-                    kOzDigits * T::A_PLANE, full + s);
-          bulk_load(st + kOzDigits * T::A_PLANE,
-                    g.bd + (static_cast<int64_t>(n0 / BN) * g.kblocks + kb) * (kOzDigits * T::B_PLANE),
-                    kOzDigits * T::B_PLANE, full + s);
+          bulk_load(st, g.ad + (static_cast<int64_t>(mt) * g.kblocks + kb) * (D * T::A_PLANE), D * T::A_PLANE,
+                    full + s);
+          bulk_load(st + D * T::A_PLANE, g.bd + (static_cast<int64_t>(nt) * g.kblocks + kb) * (D * T::B_PLANE),
+                    D * T::B_PLANE, full + s);
         }
       }
     }
@@ -258,9 +297,12 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
     // ------------------------------ MMA issuer ------------------------------
     // The whole warp runs this loop with warp-uniform values; descriptors are
     // linear in the smem address (start field = addr >> 4), so each MMA's pair is
-    // the stage base descriptor plus a compile-time offset.
-    const uint32_t idesc = i8_idesc(kOzDigits * BN);  // B = the 4 digit planes stacked: N = 4 BN
-    const uint64_t dA0 = oz_desc(smem_u32(sm)), dB0 = oz_desc(smem_u32(sm) + kOzDigits * T::A_PLANE);
+    // the stage base descriptor plus a compile-time offset.  A plane s meets the B
+    // planes t < min(D, LV - s), stacked as one N = (#planes) BN operand (at most
+    // 256 / BN planes per MMA) issued at TMEM column (s + t0) BN: pair (s, t) lands in
+    // level block s + t.
+    constexpr int CH = 256 / BN;
+    const uint64_t dA0 = oz_desc(smem_u32(sm)), dB0 = oz_desc(smem_u32(sm) + D * T::A_PLANE);
     uint32_t gk = 0, it = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
       int64_t kbeg;
@@ -277,8 +319,15 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
 #pragma unroll
           for (int k = 0; k < kOzBK / 32; ++k)
 #pragma unroll
-            for (int sa = 0; sa < kOzDigits; ++sa)
-              umma_i8_warp(tmem + sa * BN, da + ((sa * T::A_PLANE + k * 32) >> 4), db + ((k * 32) >> 4), idesc, 1u);
+            for (int sa = 0; sa < D; ++sa) {
+              const int nb = (D < LV - sa) ? D : LV - sa;
+#pragma unroll
+              for (int t0 = 0; t0 < nb; t0 += CH) {
+                const int cnt = (CH < nb - t0) ? CH : nb - t0;
+                umma_i8_warp(tmem + (sa + t0) * BN, da + ((sa * T::A_PLANE + k * 32) >> 4),
+                             db + ((t0 * T::B_PLANE + k * 32) >> 4), i8_idesc(cnt * BN), 1u);
+              }
+            }
           oz_commit_warp(empty + s);  // the stage is free once these MMAs have read it
         }
         __syncwarp();
@@ -289,12 +338,13 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
     }
   } else {
     // ------------------------------ epilogue ------------------------------
-    // (1) TMEM -> exact fp64 combination -> smem tile (lane = row), release TMEM;
-    // (2) smem tile -> global with lanes along n (contiguous for every CMap the
-    //     engine uses), row / column offsets computed once per row / per tile.
+    // TMEM -> exact fp64 combination of the levels (Horner in 2^-7) -> smem tile
+    // (lane = row) -> global with lanes along n (contiguous for every CMap the
+    // engine uses).  Whole-tile staging releases TMEM before the global stores;
+    // chunked staging (large digit stages) stores 16 columns at a time.
     const int quad = warp & 3;
     const uint32_t tlane = tmem + (static_cast<uint32_t>(quad * 32) << 16);
-    tmem_zero(tlane);  // every MMA accumulates: the levels start from zero
+    tmem_zero<LV * BN>(tlane);  // every MMA accumulates: the levels start from zero
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
     __syncwarp();
     if (lane == 0) mbar_arrive(acc_empty);
@@ -309,54 +359,71 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
       const int r = quad * 32 + lane;
       const int64_t m = m0 + r;
-      const double sa = (m < g.M && ktiles > 0) ? ldexp(1.0, g.ea[m] - 14) : 0.0;
-#pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 16) {
-        uint32_t v[kOzLevels][16];
-#pragma unroll
-        for (int L = 0; L < kOzLevels; ++L) tmem_ld16(tlane + L * BN + c0, v[L]);
-        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-#pragma unroll
-        for (int q = 0; q < 16; ++q) {
-          double val = static_cast<double>(static_cast<int32_t>(v[kOzLevels - 1][q]));
-#pragma unroll
-          for (int L = kOzLevels - 2; L >= 0; --L)
-            val = fma(val, 0.0078125, static_cast<double>(static_cast<int32_t>(v[L][q])));
-          otile[r * T::OUT_LD + c0 + q] = val * sa;
-        }
-      }
-      tmem_zero(tlane);
-      asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-      __syncwarp();
-      if (lane == 0) mbar_arrive(acc_empty);  // the MMA warp may start the next tile
-      asm volatile("bar.sync 1, 128;\n" ::: "memory");
-      // (2) coalesced stores: lane -> column n (BN / 32 per lane), warp -> rows quad, quad + 4, ...
+      const double sa = (m < g.M && ktiles > 0) ? ldexp(1.0, g.ea[m] - SC::OFF) : 0.0;
       const bool part = g.splits > 1;
       const uint32_t M2 = part ? (1u << 30) : static_cast<uint32_t>(g.cmap.M2);
       const uint32_t N2 = part ? (1u << 30) : static_cast<uint32_t>(g.cmap.N2);
       const int64_t sm1 = part ? 0 : g.cmap.sm1, sm2 = part ? g.N : g.cmap.sm2;
       const int64_t sn1 = part ? 0 : g.cmap.sn1, sn2 = part ? 1 : g.cmap.sn2;
       double* base = part ? g.ws + static_cast<int64_t>(split) * g.M * g.N : g.C;
-      int64_t coff[BN / 32];
-      double sb[BN / 32];
-      bool nok[BN / 32];
-#pragma unroll
-      for (int j = 0; j < BN / 32; ++j) {
-        const int64_t n = n0 + lane + 32 * j;
-        nok[j] = n < g.N;
-        const uint32_t un = static_cast<uint32_t>(n);
-        coff[j] = nok[j] ? static_cast<int64_t>(un / N2) * sn1 + static_cast<int64_t>(un % N2) * sn2 : 0;
-        sb[j] = nok[j] ? ldexp(1.0, g.eb[n]) : 0.0;
-      }
       const int rows = static_cast<int>((g.M - m0) < kOzBM ? (g.M - m0) : kOzBM);
-      for (int rr = quad; rr < rows; rr += 4) {
-        const uint32_t mm = static_cast<uint32_t>(m0 + rr);
-        const int64_t roff = static_cast<int64_t>(mm / M2) * sm1 + static_cast<int64_t>(mm % M2) * sm2;
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 16) {
+        uint32_t v[LV][16];
 #pragma unroll
-        for (int j = 0; j < BN / 32; ++j)
-          if (nok[j]) base[roff + coff[j]] = otile[rr * T::OUT_LD + lane + 32 * j] * sb[j];
+        for (int L = 0; L < LV; ++L) tmem_ld16(tlane + L * BN + c0, v[L]);
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+        const int oc = T::CHUNKED ? 0 : c0;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          double val = static_cast<double>(static_cast<int32_t>(v[LV - 1][q]));
+#pragma unroll
+          for (int L = LV - 2; L >= 0; --L) val = fma(val, 0.0078125, static_cast<double>(static_cast<int32_t>(v[L][q])));
+          otile[r * T::OUT_LD + oc + q] = val * sa;
+        }
+        if constexpr (T::CHUNKED) {
+          // store this 16-column chunk: lane -> (row parity, column), warp -> rows quad*2 + ...
+          asm volatile("bar.sync 1, 128;\n" ::: "memory");
+          const int64_t n = n0 + c0 + (lane & 15);
+          const bool nok = n < g.N;
+          const uint32_t un = static_cast<uint32_t>(n);
+          const int64_t coff = nok ? static_cast<int64_t>(un / N2) * sn1 + static_cast<int64_t>(un % N2) * sn2 : 0;
+          const double sb = nok ? ldexp(1.0, g.eb[n]) : 0.0;
+          for (int rr = quad * 2 + (lane >> 4); rr < rows; rr += 8) {
+            const uint32_t mm = static_cast<uint32_t>(m0 + rr);
+            const int64_t roff = static_cast<int64_t>(mm / M2) * sm1 + static_cast<int64_t>(mm % M2) * sm2;
+            if (nok) base[roff + coff] = otile[rr * T::OUT_LD + (lane & 15)] * sb;
+          }
+          asm volatile("bar.sync 1, 128;\n" ::: "memory");
+        }
       }
-      asm volatile("bar.sync 1, 128;\n" ::: "memory");  // otile reused by the next tile
+      tmem_zero<LV * BN>(tlane);
+      asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(acc_empty);  // the MMA warp may start the next tile
+      if constexpr (!T::CHUNKED) {
+        asm volatile("bar.sync 1, 128;\n" ::: "memory");
+        // coalesced stores: lane -> column n (BN / 32 per lane), warp -> rows quad, quad + 4, ...
+        int64_t coff[BN / 32];
+        double sb[BN / 32];
+        bool nok[BN / 32];
+#pragma unroll
+        for (int j = 0; j < BN / 32; ++j) {
+          const int64_t n = n0 + lane + 32 * j;
+          nok[j] = n < g.N;
+          const uint32_t un = static_cast<uint32_t>(n);
+          coff[j] = nok[j] ? static_cast<int64_t>(un / N2) * sn1 + static_cast<int64_t>(un % N2) * sn2 : 0;
+          sb[j] = nok[j] ? ldexp(1.0, g.eb[n]) : 0.0;
+        }
+        for (int rr = quad; rr < rows; rr += 4) {
+          const uint32_t mm = static_cast<uint32_t>(m0 + rr);
+          const int64_t roff = static_cast<int64_t>(mm / M2) * sm1 + static_cast<int64_t>(mm % M2) * sm2;
+#pragma unroll
+          for (int j = 0; j < BN / 32; ++j)
+            if (nok[j]) base[roff + coff[j]] = otile[rr * T::OUT_LD + lane + 32 * j] * sb[j];
+        }
+        asm volatile("bar.sync 1, 128;\n" ::: "memory");  // otile reused by the next tile
+      }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
@@ -368,7 +435,7 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
 }
 
 // ---------------------------------------------------------------------------
-// slicing: per-output-row max |x| -> exponent -> 4 int8 base-128 digit planes
+// slicing: per-output-row max |x| -> exponent -> D int8 digit planes
 // ---------------------------------------------------------------------------
 // row max of a row-major [rows][ld] matrix (one warp per row); out[r] = max_c |x[r][c]|
 template <typename Tin>
@@ -411,13 +478,27 @@ __device__ __forceinline__ int oz_exponent(double mx) {
   return ilogb(mx) + 1;
 }
 
-__device__ __forceinline__ void oz_digits(double v, int8_t (&d)[kOzDigits]) {
+// v = x 2^-e, |v| < 1 -> the scheme's digits (every step exact: power-of-two scalings
+// and the subtraction of an integer within 1 of its operand)
+template <class SC>
+__device__ __forceinline__ void oz_digits(double v, int8_t (&d)[SC::D]) {
+  if constexpr (SC::BAL) {
+    // balanced: d_0 = rint(64 v), then d_s = rint(128 r), remainders in [-1/2, 1/2]
+    double t = v * 64.0;
 #pragma unroll
-  for (int s = 0; s < kOzDigits; ++s) {
-    const double t = v * 128.0;
-    const double q = trunc(t);
-    d[s] = static_cast<int8_t>(static_cast<int>(q));
-    v = t - q;  // exact
+    for (int s = 0; s < SC::D; ++s) {
+      const double q = rint(t);
+      d[s] = static_cast<int8_t>(static_cast<int>(q));
+      t = (t - q) * 128.0;
+    }
+  } else {
+#pragma unroll
+    for (int s = 0; s < SC::D; ++s) {
+      const double t = v * 128.0;
+      const double q = trunc(t);
+      d[s] = static_cast<int8_t>(static_cast<int>(q));
+      v = t - q;
+    }
   }
 }
 
@@ -425,12 +506,13 @@ __device__ __forceinline__ void oz_digits(double v, int8_t (&d)[kOzDigits]) {
 // transposed; K = the other extent), covering the whole padded layout (zero
 // digits in the tile padding, so no memset is needed); mx[out_rows] = max |x| of
 // each output row, exps[out_rows] its exponent.  One thread per (output row,
-// 16-k chunk): 16 values -> 4 planes x one 16 B store.
-template <typename Tin>
+// 16-k chunk): 16 values -> D planes x one 16 B store.
+template <typename Tin, class SC>
 __global__ void __launch_bounds__(256) oz_digits_tiled_kernel(const Tin* __restrict__ x, int64_t rows, int64_t cols,
                                                               int64_t ld_in, int transpose,
                                                               const double* __restrict__ mx, int8_t* __restrict__ out,
                                                               int rows_per_tile, int32_t* __restrict__ exps) {
+  constexpr int D = SC::D;
   const int64_t out_rows = transpose ? cols : rows, K = transpose ? rows : cols;
   const int64_t kblocks = (K + 63) / 64, kchunks = kblocks * 4;
   const int64_t rows_pad = (out_rows + rows_per_tile - 1) / rows_per_tile * rows_per_tile;
@@ -444,9 +526,9 @@ __global__ void __launch_bounds__(256) oz_digits_tiled_kernel(const Tin* __restr
     const bool rok = orow < out_rows;
     const int e = rok ? oz_exponent(mx[orow]) : 0;
     const double sc = ldexp(1.0, -e);
-    uint32_t w[kOzDigits][4];
+    uint32_t w[D][4];
 #pragma unroll
-    for (int d = 0; d < kOzDigits; ++d)
+    for (int d = 0; d < D; ++d)
 #pragma unroll
       for (int q = 0; q < 4; ++q) w[d][q] = 0;
     if (rok && ch * 16 < K) {
@@ -455,16 +537,16 @@ __global__ void __launch_bounds__(256) oz_digits_tiled_kernel(const Tin* __restr
         const int64_t k = ch * 16 + j;
         double v = 0.0;
         if (k < K) v = static_cast<double>(transpose ? x[k * ld_in + orow] : x[orow * ld_in + k]);
-        int8_t dg[kOzDigits];
-        oz_digits(v * sc, dg);
+        int8_t dg[D];
+        oz_digits<SC>(v * sc, dg);
 #pragma unroll
-        for (int d = 0; d < kOzDigits; ++d)
+        for (int d = 0; d < D; ++d)
           w[d][j >> 2] |= static_cast<uint32_t>(static_cast<uint8_t>(dg[d])) << (8 * (j & 3));
       }
     }
 #pragma unroll
-    for (int d = 0; d < kOzDigits; ++d) {
-      const int64_t off = oz_tiled_offset(orow, ch * 16, d, rows_per_tile, kblocks);
+    for (int d = 0; d < D; ++d) {
+      const int64_t off = oz_tiled_offset(orow, ch * 16, d, rows_per_tile, kblocks, D);
       *reinterpret_cast<uint4*>(out + off) = make_uint4(w[d][0], w[d][1], w[d][2], w[d][3]);
     }
     if (rok && ch == 0) exps[orow] = e;

@@ -474,23 +474,30 @@ int gemm_tc(const float* ahi, const float* alo, int64_t lda, int64_t M, int64_t 
 }
 
 // ---------------------------------------------------------------------------
-// fp32 variant: int8 tcgen05 digit-sliced GEMM (tc_int8_gemm.cuh)
+// int8 tcgen05 digit-sliced GEMM (tc_int8_gemm.cuh): the fp32 variant (OzF32) and
+// the fp64 environment products (OzF64)
 // ---------------------------------------------------------------------------
 constexpr int kOzBN = 64;
-// bytes of a tiled digit layout: 4 planes x rows padded to the tile x K padded to 64
-inline int64_t oz_digits_bytes(int64_t rows, int64_t k, int rows_per_tile) {
-  return 4 * ((rows + rows_per_tile - 1) / rows_per_tile * rows_per_tile) * ((k + 63) / 64 * 64);
+// bytes of a tiled digit layout: D planes x rows padded to the tile x K padded to 64
+inline int64_t oz_digits_bytes(int64_t rows, int64_t k, int rows_per_tile, int digits) {
+  return digits * ((rows + rows_per_tile - 1) / rows_per_tile * rows_per_tile) * ((k + 63) / 64 * 64);
 }
 
-// split-K: byte-bound model (4 digit bytes per A element at the per-SM HBM share),
-// and never more than kOzKmax k per CTA (int32 accumulator bound)
+// split-K over a per-tile time model and never more than SC::KMAX k per CTA (int32
+// accumulator bound).  fp32: byte-bound (4 digit bytes per A element at the per-SM
+// HBM share); fp64: tensor-bound (36 digit-pair MMAs at the int8 rate of one SM).
+template <class SC>
 SplitPlan plan_split_oz(int64_t M, int64_t K, int64_t N) {
   const int64_t BK = trals::kOzBK;
   const int64_t tiles = ((M + trals::kOzBM - 1) / trals::kOzBM) * ((N + kOzBN - 1) / kOzBN);
   const int64_t slots = kSMs;
-  const int64_t smin = std::max<int64_t>(1, (K + trals::kOzKmax - 1) / trals::kOzKmax);
+  const int64_t smin = std::max<int64_t>(1, (K + SC::KMAX - 1) / SC::KMAX);
   const int64_t smax = std::max<int64_t>(smin, std::min<int64_t>(64, K / (4 * BK)));
-  const double t_tile = 4.0 * trals::kOzBM * static_cast<double>(K) / (6.5e12 / slots);
+  int pairs = 0;
+  for (int a = 0; a < SC::D; ++a) pairs += std::min(SC::D, SC::LV - a);
+  const double t_tile = SC::BAL ? static_cast<double>(pairs) * trals::kOzBM * kOzBN * static_cast<double>(K) /
+                                      (8192.0 * 1.9e9)
+                                : 4.0 * trals::kOzBM * static_cast<double>(K) / (6.5e12 / slots);
   const double out_bytes = 8.0 * static_cast<double>(M) * N;
   int64_t best_s = smin;
   double best = 1e300;
@@ -505,22 +512,24 @@ SplitPlan plan_split_oz(int64_t M, int64_t K, int64_t N) {
   return {static_cast<int>(std::max<int64_t>(1, (K + kchunk - 1) / kchunk)), kchunk};
 }
 
-// workspace (doubles): B digit planes (4 x N x ldk bytes), eb (N int32), B column max (N), partials
+// workspace (doubles): B digit planes (D x N x ldk bytes), eb (N int32), B column max (N), partials
 struct OzWs {
   int64_t planes, eb, mx, part, total;
 };
+template <class SC>
 OzWs oz_ws_layout(int64_t M, int64_t K, int64_t N) {
-  const SplitPlan sp = plan_split_oz(M, K, N);
+  const SplitPlan sp = plan_split_oz<SC>(M, K, N);
   OzWs w{};
   w.planes = 0;
-  w.eb = w.planes + (oz_digits_bytes(N, K, kOzBN) + 15) / 16 * 2;
+  w.eb = w.planes + (oz_digits_bytes(N, K, kOzBN, SC::D) + 15) / 16 * 2;
   w.mx = w.eb + (N + 3) / 4 * 2;
   w.part = w.mx + (N + 1) / 2 * 2;
   w.total = w.part + (sp.splits > 1 ? static_cast<int64_t>(sp.splits) * M * N : 0);
   return w;
 }
 
-int64_t gemm_oz_ws(int64_t M, int64_t K, int64_t N) { return oz_ws_layout(M, K, N).total; }
+template <class SC>
+int64_t gemm_oz_ws(int64_t M, int64_t K, int64_t N) { return oz_ws_layout<SC>(M, K, N).total; }
 
 template <typename T>
 int launch_colmax(const T* x, int64_t rows, int64_t cols, int64_t ld, double* out, cudaStream_t s) {
@@ -534,23 +543,24 @@ int launch_colmax(const T* x, int64_t rows, int64_t cols, int64_t ld, double* ou
   return launch_status();
 }
 
-// C(m, n) = sum_k A[m][k] B[k][n]: A given as tiled digits [4 x 128-row tiles] + row exponents ea[M],
+// C(m, n) = sum_k A[m][k] B[k][n]: A given as tiled digits [D x 128-row tiles] + row exponents ea[M],
 // B fp64 [K][ldb] (sliced per call into the workspace), C fp64 through cm.
+template <class SC>
 int gemm_oz(const int8_t* ad, const int32_t* ea, int64_t M, int64_t K, int64_t N, const double* B, int64_t ldb,
             double* C, const CMap& cm, double* ws, int64_t ws_elems, cudaStream_t s) {
   if ((reinterpret_cast<uintptr_t>(ad) & 15u) || M > INT32_MAX || K > INT32_MAX || N > INT32_MAX) return TRALS_ERR_ARG;
-  const OzWs w = oz_ws_layout(M, K, N);
+  const OzWs w = oz_ws_layout<SC>(M, K, N);
   if (!ws || w.total > ws_elems) return TRALS_ERR_ARG;
-  const SplitPlan sp = plan_split_oz(M, K, N);
+  const SplitPlan sp = plan_split_oz<SC>(M, K, N);
   int8_t* bd = reinterpret_cast<int8_t*>(ws + w.planes);
   int32_t* eb = reinterpret_cast<int32_t*>(ws + w.eb);
   double* bmx = ws + w.mx;
   // B^T rows = columns of B: max over k, then tiled digits (transposed read)
   if (int st = launch_colmax<double>(B, K, N, ldb, bmx, s)) return st;
   {
-    const int64_t work = oz_digits_bytes(N, K, kOzBN) / 64;  // (padded row, 16-k chunk) items
+    const int64_t work = oz_digits_bytes(N, K, kOzBN, SC::D) / (16 * SC::D);  // (padded row, 16-k chunk) items
     const int blocks = static_cast<int>(std::min<int64_t>((work + 255) / 256, 16 * kSMs));
-    trals::oz_digits_tiled_kernel<double><<<blocks, 256, 0, s>>>(B, K, N, ldb, 1, bmx, bd, kOzBN, eb);
+    trals::oz_digits_tiled_kernel<double, SC><<<blocks, 256, 0, s>>>(B, K, N, ldb, 1, bmx, bd, kOzBN, eb);
     if (int st = launch_status()) return st;
   }
   trals::OzArgs g{};
@@ -560,8 +570,8 @@ int gemm_oz(const int8_t* ad, const int32_t* ea, int64_t M, int64_t K, int64_t N
   g.kblocks = (K + trals::kOzBK - 1) / trals::kOzBK;
   g.ad = ad; g.bd = bd;
   g.cmap = cm; g.ea = ea; g.eb = eb; g.C = C; g.ws = ws + w.part;
-  using T = trals::OzTile<kOzBN>;
-  auto kern = trals::oz8_kernel<kOzBN>;
+  using T = trals::OzTile<kOzBN, SC>;
+  auto kern = trals::oz8_kernel<kOzBN, SC>;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(T::SMEM));
@@ -582,6 +592,29 @@ int gemm_oz(const int8_t* ad, const int32_t* ea, int64_t M, int64_t K, int64_t N
     return launch_status();
   }
   return TRALS_OK;
+}
+
+// X (fp32 or fp64, row-major [rows][cols]) -> tiled digit planes of its rows (transpose = 0)
+// or columns (transpose = 1) + their exponents; ws = out_rows doubles (row / column maxima)
+template <typename Tin, class SC>
+int oz_split(const Tin* x, int64_t rows, int64_t cols, int transpose, int8_t* digits, int32_t* exps, double* ws,
+             int64_t ws_elems, cudaStream_t s) {
+  const int64_t out_rows = transpose ? cols : rows, K = transpose ? rows : cols;
+  if (!x || !digits || !exps || !ws || rows < 1 || cols < 1 || (transpose != 0 && transpose != 1) ||
+      ws_elems < out_rows || (reinterpret_cast<uintptr_t>(digits) & 15u))
+    return TRALS_ERR_ARG;
+  if (!transpose) {
+    const int blocks = static_cast<int>(std::min<int64_t>((rows + 7) / 8, 64 * kSMs));
+    trals::oz_rowmax_kernel<Tin><<<blocks, 256, 0, s>>>(x, rows, cols, cols, ws);
+    if (int st = launch_status()) return st;
+  } else {
+    if (int st = launch_colmax<Tin>(x, rows, cols, cols, ws, s)) return st;
+  }
+  const int64_t work = oz_digits_bytes(out_rows, K, trals::kOzBM, SC::D) / (16 * SC::D);  // (padded row, 16-k chunk)
+  const int blocks = static_cast<int>(std::min<int64_t>((work + 255) / 256, 64 * kSMs));
+  trals::oz_digits_tiled_kernel<Tin, SC><<<blocks, 256, 0, s>>>(x, rows, cols, cols, transpose, ws, digits,
+                                                                trals::kOzBM, exps);
+  return launch_status();
 }
 
 inline CMap rowmajor(int64_t ldc) { return CMap{0, 1 << 30, 0, ldc, 1 << 30, 0, 1}; }
@@ -1937,17 +1970,18 @@ int env_tf32(const float* xhi, const float* xlo, int64_t ldx, int64_t pre, int64
 
 // fp32 variant of env() on the int8 tensor cores: X given as digit planes + row exponents,
 // K-major for this side (side 0: rows = pre, side 1: rows = post, the transposed copy).
+template <class SC>
 int env_oz(const int8_t* xd, const int32_t* xe, int64_t pre, int64_t post, int side, const double* H, int r_lo,
            int r_hi, double* E, int leaf, double* ws, int64_t ws_elems, cudaStream_t s) {
   const int64_t RR = static_cast<int64_t>(r_lo) * r_hi;
   if (side == 0) {
     CMap cm{0, pre, 0, r_lo, r_hi, 1, pre * r_lo};
     if (leaf) cm = CMap{0, pre, 0, RR, r_hi, r_hi, 1};
-    return gemm_oz(xd, xe, pre, post, RR, H, RR, E, cm, ws, ws_elems, s);
+    return gemm_oz<SC>(xd, xe, pre, post, RR, H, RR, E, cm, ws, ws_elems, s);
   }
   CMap cm{0, post, 0, r_lo, r_hi, 1, post * r_lo};
   if (leaf) cm = CMap{0, post, 0, RR, r_hi, r_hi, 1};
-  return gemm_oz(xd, xe, post, pre, RR, H, RR, E, cm, ws, ws_elems, s);
+  return gemm_oz<SC>(xd, xe, post, pre, RR, H, RR, E, cm, ws, ws_elems, s);
 }
 
 int absorb_right(const double* E, int Ra, int64_t pre, int64_t Ib, int Rb, int Rb1, const double* core_zt,
@@ -2183,42 +2217,51 @@ int trals_env_f64(const double* X, int64_t pre, int64_t post, int side, const do
 }
 
 int64_t trals_oz_digits_bytes(int64_t rows, int64_t k) {
-  return rows < 1 || k < 1 ? 0 : oz_digits_bytes(rows, k, trals::kOzBM);
+  return rows < 1 || k < 1 ? 0 : oz_digits_bytes(rows, k, trals::kOzBM, trals::OzF32::D);
 }
 
 int64_t trals_oz_split_ws_elems(int64_t rows, int64_t cols, int transpose) { return transpose ? cols : rows; }
 
 int trals_oz_split_f32(const float* x, int64_t rows, int64_t cols, int transpose, int8_t* digits, int32_t* exps,
                        double* ws, int64_t ws_elems, void* stream) {
-  const int64_t out_rows = transpose ? cols : rows, K = transpose ? rows : cols;
-  if (!x || !digits || !exps || !ws || rows < 1 || cols < 1 || (transpose != 0 && transpose != 1) ||
-      ws_elems < out_rows || (reinterpret_cast<uintptr_t>(digits) & 15u))
-    return TRALS_ERR_ARG;
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (!transpose) {
-    const int blocks = static_cast<int>(std::min<int64_t>((rows + 7) / 8, 64 * kSMs));
-    trals::oz_rowmax_kernel<float><<<blocks, 256, 0, s>>>(x, rows, cols, cols, ws);
-    if (int st = launch_status()) return st;
-  } else {
-    if (int st = launch_colmax<float>(x, rows, cols, cols, ws, s)) return st;
-  }
-  const int64_t work = oz_digits_bytes(out_rows, K, trals::kOzBM) / 64;  // (padded row, 16-k chunk) items
-  const int blocks = static_cast<int>(std::min<int64_t>((work + 255) / 256, 64 * kSMs));
-  trals::oz_digits_tiled_kernel<float><<<blocks, 256, 0, s>>>(x, rows, cols, cols, transpose, ws, digits,
-                                                             trals::kOzBM, exps);
-  return launch_status();
+  return oz_split<float, trals::OzF32>(x, rows, cols, transpose, digits, exps, ws, ws_elems,
+                                       static_cast<cudaStream_t>(stream));
 }
 
 int64_t trals_env_oz_ws_elems(int64_t pre, int64_t post, int side, int r_lo, int r_hi) {
   const int64_t RR = static_cast<int64_t>(r_lo) * r_hi;
-  return side == 0 ? gemm_oz_ws(pre, post, RR) : gemm_oz_ws(post, pre, RR);
+  return side == 0 ? gemm_oz_ws<trals::OzF32>(pre, post, RR) : gemm_oz_ws<trals::OzF32>(post, pre, RR);
 }
 
 int trals_env_oz(const int8_t* xd, const int32_t* xe, int64_t pre, int64_t post, int side, const double* H, int r_lo,
                  int r_hi, double* E, int leaf, double* ws, int64_t ws_elems, void* stream) {
   if (!xd || !xe || !H || !E || !ws || pre < 1 || post < 1 || r_lo < 1 || r_hi < 1 || (side != 0 && side != 1))
     return TRALS_ERR_ARG;
-  return env_oz(xd, xe, pre, post, side, H, r_lo, r_hi, E, leaf, ws, ws_elems, static_cast<cudaStream_t>(stream));
+  return env_oz<trals::OzF32>(xd, xe, pre, post, side, H, r_lo, r_hi, E, leaf, ws, ws_elems,
+                              static_cast<cudaStream_t>(stream));
+}
+
+int64_t trals_oz64_digits_bytes(int64_t rows, int64_t k) {
+  return rows < 1 || k < 1 ? 0 : oz_digits_bytes(rows, k, trals::kOzBM, trals::OzF64::D);
+}
+
+int trals_oz64_split_f64(const double* x, int64_t rows, int64_t cols, int transpose, int8_t* digits, int32_t* exps,
+                         double* ws, int64_t ws_elems, void* stream) {
+  return oz_split<double, trals::OzF64>(x, rows, cols, transpose, digits, exps, ws, ws_elems,
+                                        static_cast<cudaStream_t>(stream));
+}
+
+int64_t trals_env_oz64_ws_elems(int64_t pre, int64_t post, int side, int r_lo, int r_hi) {
+  const int64_t RR = static_cast<int64_t>(r_lo) * r_hi;
+  return side == 0 ? gemm_oz_ws<trals::OzF64>(pre, post, RR) : gemm_oz_ws<trals::OzF64>(post, pre, RR);
+}
+
+int trals_env_oz64(const int8_t* xd, const int32_t* xe, int64_t pre, int64_t post, int side, const double* H,
+                   int r_lo, int r_hi, double* E, int leaf, double* ws, int64_t ws_elems, void* stream) {
+  if (!xd || !xe || !H || !E || !ws || pre < 1 || post < 1 || r_lo < 1 || r_hi < 1 || (side != 0 && side != 1))
+    return TRALS_ERR_ARG;
+  return env_oz<trals::OzF64>(xd, xe, pre, post, side, H, r_lo, r_hi, E, leaf, ws, ws_elems,
+                              static_cast<cudaStream_t>(stream));
 }
 
 int64_t trals_tf32_ld(int64_t cols) { return cols < 1 ? 0 : tf32_ld(cols); }

@@ -79,7 +79,7 @@ class SweepEngine:
 
     def __init__(self, x_local: torch.Tensor, dims, ranks, variant: str, *, shard_mode=None, lo=0, hi=None,
                  group=None, world_size: int = 1, rank_deficient_fallback=True, svd_rcond=1e-12,
-                 debug_checks=False, _test_lib=None):
+                 debug_checks=False, fp64_gemm="ozaki", _test_lib=None):
         if variant not in ("als", "ne", "qr", "qrne"):
             raise ValueError(f"unsupported device variant {variant!r}")
         # `_test_lib` lets the CPU test-suite drive this exact schedule through a numpy
@@ -92,6 +92,13 @@ class SweepEngine:
         # tcgen05 tensor cores over X's digit slices (exact int32 accumulation);
         # cores, Grams, solves and errors stay fp64.
         self.fp32 = x_local.dtype == torch.float32
+        # fp64 X: the environment products run either on the fp64 DMMA pipe ("dmma") or on the
+        # int8 tcgen05 tensor cores over 8 balanced digit planes of X ("ozaki": 36 exact int32
+        # digit-pair products combined in fp64 -- the DMMA product's accuracy at ~3x its rate)
+        if fp64_gemm not in ("dmma", "ozaki"):
+            raise ValueError(f"unknown fp64_gemm {fp64_gemm!r}; expected 'dmma' or 'ozaki'")
+        self.oz64 = (not self.fp32) and fp64_gemm == "ozaki" and _test_lib is None
+        self.sliced = self.fp32 or self.oz64
         self.lib = _test_lib if _test_lib is not None else L.lib()
         self.dev = x_local.device
         self.variant = variant
@@ -109,7 +116,7 @@ class SweepEngine:
         if tuple(x_local.shape) != tuple(self.dl):
             raise ValueError(f"local slab shape {tuple(x_local.shape)} != expected {tuple(self.dl)}")
         self.x = x_local
-        self._xsplit = {}   # fp32: (side, pre, post) -> (digits, exps): X sliced, K-major for that side
+        self._xsplit = {}   # fp32 / oz64: (side, pre, post) -> (digits, exps): X sliced, K-major for that side
         self._x64 = None    # fp32 + exact errors: fp64 copy of X for the residual kernel
         self.fallback_ok = bool(rank_deficient_fallback)
         # AlsConfig.debug_checks (solvers.py:376-377, 432-438, 485-487): assert the coefficient
@@ -286,21 +293,22 @@ class SweepEngine:
             self._bufs.append(E0)
             target = lambda E0=E0: E0.data_ptr()
 
-        if self.fp32:
+        if self.sliced:
             key = (side, pre, post)
+            nbytes = self.lib.trals_oz_digits_bytes if self.fp32 else self.lib.trals_oz64_digits_bytes
+            wsf = self.lib.trals_env_oz_ws_elems if self.fp32 else self.lib.trals_env_oz64_ws_elems
+            envf = self.lib.trals_env_oz if self.fp32 else self.lib.trals_env_oz64
             if key not in self._xsplit:
                 rows, k = (pre, post) if side == 0 else (post, pre)
-                self._xsplit[key] = (torch.empty(int(self.lib.trals_oz_digits_bytes(rows, k)), dtype=torch.int8,
-                                                 device=self.dev),
+                self._xsplit[key] = (torch.empty(int(nbytes(rows, k)), dtype=torch.int8, device=self.dev),
                                      torch.empty(rows, dtype=torch.int32, device=self.dev))
-            self._ws(self.lib.trals_env_oz_ws_elems(pre, post, side, r_lo, r_hi))
+            self._ws(wsf(pre, post, side, r_lo, r_hi))
 
             def env_step(pre=pre, post=post, side=side, H=H, r_lo=r_lo, r_hi=r_hi, target=target,
-                         leaf=int(root_leaf), key=key):
+                         leaf=int(root_leaf), key=key, envf=envf):
                 xd, xe = self._xsplit[key]
-                L.check(self.lib.trals_env_oz(xd.data_ptr(), xe.data_ptr(), pre, post, side, H.data_ptr(),
-                                              r_lo, r_hi, target(), leaf, self.gws.data_ptr(), self.gws.numel(),
-                                              self._sp()), "env_oz")
+                L.check(envf(xd.data_ptr(), xe.data_ptr(), pre, post, side, H.data_ptr(), r_lo, r_hi, target(),
+                             leaf, self.gws.data_ptr(), self.gws.numel(), self._sp()), "env_oz")
         else:
             def env_step(pre=pre, post=post, side=side, H=H, r_lo=r_lo, r_hi=r_hi, target=target,
                          leaf=int(root_leaf)):
@@ -578,17 +586,19 @@ class SweepEngine:
         self._gram(j, sp)
 
     def prepare_x(self):
-        """Derive the per-X state after X (self.x) was (re)loaded: for the fp32
-        variant, X's int8 digit planes + row exponents, K-major for each
-        X-streaming phase (phase L slices X as stored, phase R its transpose)."""
-        if not self.fp32:
+        """Derive the per-X state after X (self.x) was (re)loaded: for the sliced
+        environment products (fp32 variant, fp64 "ozaki"), X's int8 digit planes
+        + row exponents, K-major for each X-streaming phase (phase L slices X as
+        stored, phase R its transpose)."""
+        if not self.sliced:
             return
         sp = self._sp()
+        split = self.lib.trals_oz_split_f32 if self.fp32 else self.lib.trals_oz64_split_f64
         for (side, pre, post), (xd, xe) in self._xsplit.items():
             need = self.lib.trals_oz_split_ws_elems(pre, post, side)
             ws = torch.empty(max(1, need), dtype=torch.float64, device=self.dev)
-            L.check(self.lib.trals_oz_split_f32(self.x.data_ptr(), pre, post, side, xd.data_ptr(), xe.data_ptr(),
-                                                ws.data_ptr(), ws.numel(), sp), "oz_split")
+            L.check(split(self.x.data_ptr(), pre, post, side, xd.data_ptr(), xe.data_ptr(), ws.data_ptr(),
+                          ws.numel(), sp), "oz_split")
         if self._x64 is not None:
             self._x64.copy_(self.x)
 

@@ -47,7 +47,7 @@ def exact_relative_error(x, cores, budget=None):
         raise RuntimeError("paper_2210_11362_b200 needs a CUDA device (no CPU fallback)")
     L.lib()
     xd = t.detach().to("cuda", torch.float64).contiguous()
-    eng = SweepEngine(xd, dims, ranks, "ne")
+    eng = SweepEngine(xd, dims, ranks, "ne", fp64_gemm="dmma")  # residual only: no digit planes
     xn = eng.compute_xnorm2()
     eng.set_cores(cores)
     out = torch.zeros(3, dtype=torch.float64, device=xd.device)

@@ -29,6 +29,7 @@ ERROR_MODES = ("exact", "cheap", "none")         # solvers.py:56
 BUCKETS = ("subchain", "mttsp", "solve", "gramqr", "other")  # solvers.py:57
 SVD_RCOND_DEFAULT = 1e-12                        # linalg.py:20
 DTYPES = ("float64", "float32")                  # AlsConfig.dtype (extension)
+FP64_GEMMS = ("ozaki", "dmma")                    # AlsConfig.fp64_gemm (extension)
 
 
 @dataclass
@@ -43,9 +44,19 @@ class AlsConfig:
 
     `dtype` (extension) selects the storage/compute type of X's contractions:
     "float64" (default, the reference's) or "float32" -- the fp32 variant of
-    BASELINE config 4: X is held in fp32 and the environment products run as
-    3xTF32 on the tcgen05 tensor cores, everything downstream in fp64; parity
-    with the fp64 reference is ~1e-4 instead of 1e-9.
+    BASELINE config 4: X is held in fp32 and the environment products run on
+    the int8 tcgen05 tensor cores over 4 digit slices of X (exact int32
+    accumulation), everything downstream in fp64; parity with the fp64
+    reference is ~1e-4 instead of 1e-9.
+
+    `fp64_gemm` (extension) selects the engine of the fp64 environment
+    products (the X-streaming MTTSP, solvers.py:379): "ozaki" (default) runs
+    them on the int8 tcgen05 tensor cores over 8 balanced digit slices of X
+    and of the half chain -- 36 exact int32 digit-pair products combined in
+    fp64, with the accuracy of an fp64 product (measured against an
+    extended-precision one) -- and "dmma" on the fp64 DMMA pipe.  X's digit
+    planes (2 x |X| bytes) are made once per call, timed as
+    upfront_seconds["mttsp"].
     """
 
     ranks: tuple
@@ -61,6 +72,7 @@ class AlsConfig:
     shard_mode: int = 0
     timing_buckets: bool = True
     dtype: str = "float64"
+    fp64_gemm: str = "ozaki"
 
 
 @dataclass
@@ -96,6 +108,8 @@ def _validate(x, config, variant):
         raise ValueError("max_iters must be at least 1")
     if config.dtype not in DTYPES:
         raise ValueError(f"unknown dtype {config.dtype!r}; expected one of {DTYPES}")
+    if config.fp64_gemm not in FP64_GEMMS:
+        raise ValueError(f"unknown fp64_gemm {config.fp64_gemm!r}; expected one of {FP64_GEMMS}")
 
 
 def _host_or_device_tensor(x, dtype="float64"):
@@ -145,7 +159,7 @@ def _run(x, config, variant):
         src = t.narrow(shard, lo, hi - lo)
     from .engine import SweepEngine
     key = (dims, tuple(ranks), variant, dev.index, world, shard, lo, hi, bool(config.rank_deficient_fallback),
-           float(config.svd_rcond), config.dtype, bool(config.debug_checks))
+           float(config.svd_rcond), config.dtype, bool(config.debug_checks), config.fp64_gemm)
     eng = _PLAN_CACHE.pop(key, None)
     if eng is None:
         x_local = torch.empty(tuple(src.shape), dtype=t.dtype, device=dev)
@@ -160,9 +174,14 @@ def _run(x, config, variant):
     if eng is None:
         eng = SweepEngine(x_local, dims, ranks, variant, shard_mode=shard, lo=lo, hi=hi, group=group,
                           world_size=world, rank_deficient_fallback=config.rank_deficient_fallback,
-                          svd_rcond=config.svd_rcond, debug_checks=config.debug_checks)
+                          svd_rcond=config.svd_rcond, debug_checks=config.debug_checks,
+                          fp64_gemm=config.fp64_gemm)
     eng.stream = torch.cuda.current_stream(dev)
+    p0 = torch.cuda.Event(enable_timing=True)
+    p1 = torch.cuda.Event(enable_timing=True)
+    p0.record(eng.stream)
     eng.prepare_x()
+    p1.record(eng.stream)
     if config.error_mode == "exact":
         eng.ensure_x64()
     _PLAN_CACHE[key] = eng
@@ -227,6 +246,8 @@ def _run(x, config, variant):
     torch.cuda.synchronize(x_local.device)
     _raise_on_info(eng, config, report)
     report.upfront_seconds["gramqr"] = t0.elapsed_time(t1) / 1e3
+    if eng.sliced:  # X's digit planes for the tensor-core environment products (once per call)
+        report.upfront_seconds["mttsp"] = p0.elapsed_time(p1) / 1e3
     for a, b, ev in sweep_events:
         report.iter_seconds.append(a.elapsed_time(b) / 1e3)
         buckets = dict.fromkeys(BUCKETS, 0.0)

@@ -247,3 +247,89 @@ def test_env_oz_matches_f64(pre, post, side, r_lo, r_hi, leaf):
         xs = x64.cpu().numpy() if side == 0 else x64.cpu().numpy().T
         assert np.max(np.abs(a - xs) / np.abs(xs).max(axis=1, keepdims=True)) < 2.0 ** -27
     assert rel(got.cpu().numpy(), ref.cpu().numpy()) < 5e-8
+
+
+def _oz64_env(lib, x64, pre, post, side, H, r_lo, r_hi, leaf, s):
+    from paper_2210_11362_b200 import _lib as L
+    K = post if side == 0 else pre
+    rows = pre if side == 0 else post
+    digits = torch.empty(lib.trals_oz64_digits_bytes(rows, K), dtype=torch.int8, device="cuda")
+    exps = torch.empty(rows, dtype=torch.int32, device="cuda")
+    sws = torch.empty(lib.trals_oz_split_ws_elems(pre, post, side), dtype=torch.float64, device="cuda")
+    L.check(lib.trals_oz64_split_f64(x64.data_ptr(), pre, post, side, digits.data_ptr(), exps.data_ptr(),
+                                     sws.data_ptr(), sws.numel(), s), "oz64_split")
+    got = torch.empty(rows * r_lo * r_hi, dtype=torch.float64, device="cuda")
+    wso = torch.empty(lib.trals_env_oz64_ws_elems(pre, post, side, r_lo, r_hi), dtype=torch.float64, device="cuda")
+    L.check(lib.trals_env_oz64(digits.data_ptr(), exps.data_ptr(), pre, post, side, H.data_ptr(), r_lo, r_hi,
+                               got.data_ptr(), leaf, wso.data_ptr(), wso.numel(), s), "env_oz64")
+    return got, digits, exps
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("pre,post,side,r_lo,r_hi,leaf", [
+    (300, 77, 0, 3, 5, 0), (77, 300, 1, 4, 4, 0), (5, 13, 0, 2, 2, 1), (13, 5, 1, 2, 3, 1),
+    (129, 1000, 1, 20, 20, 0), (1000, 129, 0, 11, 9, 0), (1600, 4000, 0, 8, 8, 0), (4000, 1600, 1, 8, 8, 1),
+    (200, 70000, 0, 8, 8, 0), (70000, 150, 1, 6, 8, 0), (640, 640, 0, 20, 20, 1),
+])
+def test_env_oz64_matches_f64(pre, post, side, r_lo, r_hi, leaf):
+    """fp64 environment product on the int8 tensor cores (8 balanced digits, levels 0..7)
+    against the DMMA one on the same X: tails in every dimension, all N tiles (R^2 = 400:
+    6 full + one 16-wide), split-K incl. the forced K > 61440 split, leaf CMap.  The digits
+    rebuild X to 2^-56 of each row max; the products agree to the fp64 rounding level."""
+    from paper_2210_11362_b200 import _lib as L
+    from fake_trals import oz_offsets
+    lib = L.lib()
+    rng = np.random.default_rng(pre + post + r_lo + 1)
+    x64 = cuda(rng.standard_normal((pre, post)) * np.exp(rng.standard_normal((pre, post))))
+    K = post if side == 0 else pre
+    rows = pre if side == 0 else post
+    H = cuda(rng.standard_normal((K, r_lo * r_hi)))
+    s = int(torch.cuda.current_stream().cuda_stream)
+    ref = torch.empty(rows * r_lo * r_hi, dtype=torch.float64, device="cuda")
+    ws = torch.empty(max(lib.trals_gemm_ws_elems(1, rows, K, r_lo * r_hi), 1 << 22), dtype=torch.float64, device="cuda")
+    L.check(lib.trals_env_f64(x64.data_ptr(), pre, post, side, H.data_ptr(), r_lo, r_hi, ref.data_ptr(), leaf,
+                              ws.data_ptr(), ws.numel(), s), "env_f64")
+    got, digits, exps = _oz64_env(lib, x64, pre, post, side, H, r_lo, r_hi, leaf, s)
+    torch.cuda.synchronize()
+    if rows * K <= 4_000_000:
+        buf = digits.cpu().numpy()
+        d = [buf[oz_offsets(rows, K, j, digits=8)].astype(np.float64) for j in range(8)]
+        assert max(np.abs(v).max() for v in d) <= 64
+        a = d[0] * 2.0 ** -6 + sum(d[j] * 2.0 ** (-6 - 7 * j) for j in range(1, 8))
+        a = np.ldexp(a, exps.cpu().numpy().astype(np.int64)[:, None])
+        xs = x64.cpu().numpy() if side == 0 else x64.cpu().numpy().T
+        assert np.max(np.abs(a - xs) / np.abs(xs).max(axis=1, keepdims=True)) <= 2.0 ** -56
+    assert rel(got.cpu().numpy(), ref.cpu().numpy()) < 1e-14
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("heavy", [False, True])
+def test_env_oz64_accuracy(heavy):
+    """The Ozaki product is as accurate as the DMMA one: both against an extended-precision
+    (x87 80-bit) product of the same operands, at the c5 contraction length K = 25600 and
+    R^2 = 400 columns (relative Frobenius error; fp64 rounding gives ~7e-16 here)."""
+    from paper_2210_11362_b200 import _lib as L
+    lib = L.lib()
+    rng = np.random.default_rng(11 + heavy)
+    pre, post, r = 64, 25600, 20
+    x = rng.standard_normal((pre, post))
+    if heavy:
+        x *= np.exp(0.5 * rng.standard_normal((pre, post)))
+    h = rng.standard_normal((post, r * r))
+    exact = (x.astype(np.longdouble) @ h.astype(np.longdouble))  # [pre][r_lo r_hi] rows
+    x64, H = cuda(x), cuda(h)
+    s = int(torch.cuda.current_stream().cuda_stream)
+    ref = torch.empty(pre * r * r, dtype=torch.float64, device="cuda")
+    ws = torch.empty(max(lib.trals_gemm_ws_elems(1, pre, post, r * r), 1 << 22), dtype=torch.float64, device="cuda")
+    L.check(lib.trals_env_f64(x64.data_ptr(), pre, post, 0, H.data_ptr(), r, r, ref.data_ptr(), 0,
+                              ws.data_ptr(), ws.numel(), s), "env_f64")
+    got, _, _ = _oz64_env(lib, x64, pre, post, 0, H, r, r, 0, s)
+    torch.cuda.synchronize()
+    # non-leaf side-0 env layout (CMap of env()): [r_hi][pre][r_lo], H column a r_hi + b
+    def unperm(v):
+        return v.cpu().numpy().reshape(r, pre, r).transpose(1, 2, 0).reshape(pre, r * r)
+    e_dmma = np.linalg.norm((unperm(ref) - exact).astype(np.float64)) / np.linalg.norm(exact.astype(np.float64))
+    e_oz = np.linalg.norm((unperm(got) - exact).astype(np.float64)) / np.linalg.norm(exact.astype(np.float64))
+    print(f"heavy={heavy}: dmma {e_dmma:.3e}  ozaki {e_oz:.3e}")
+    assert e_dmma < 2e-15
+    assert e_oz < max(2.0 * e_dmma, 1e-15)
