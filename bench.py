@@ -44,6 +44,9 @@ PEAK_SOURCE = "profiles/r01_fp64_pipes.md: mma.sync m8n8k4 f64 microbenchmark, 1
 # fp64 "ozaki" environment products: 36 int8 digit-pair MMAs per fp64 multiply-add (8 balanced
 # digits per operand, pair levels s + t <= 7)
 OZ64_PAIRS = 36
+# int8 tcgen05 ceiling on this pool's B200: tools/micro/i8_peak.cu (M128 N256 K32 MMAs back to back,
+# 148 SMs), profiles/r01_i8_peak.jsonl
+INT8_PEAK_TOPS = 4374.8
 
 
 def load_peaks():
@@ -244,7 +247,6 @@ def run_ours(args):
     dev = torch.device("cuda", torch.cuda.current_device())
     x_full, _ = make_dataset_device(order, dim, rt, noise, sd, device=dev)
     fp32 = args.dtype == "float32"
-    oz64 = (not fp32) and args.fp64_gemm == "ozaki"
     if fp32:
         x_full = x_full.float()
     shard = 0
@@ -257,6 +259,8 @@ def run_ours(args):
     cores0 = random_cores(dims, ranks, make_rng(si))
     eng = SweepEngine(x_local, dims, ranks, args.variant, shard_mode=shard if world > 1 else None, lo=lo, hi=hi,
                       world_size=world, fp64_gemm=args.fp64_gemm)
+    oz64 = eng.oz64
+    eng_gemm = eng.fp64_gemm
     p0 = torch.cuda.Event(enable_timing=True)
     p1 = torch.cuda.Event(enable_timing=True)
     p0.record(eng.stream)
@@ -323,6 +327,7 @@ def run_ours(args):
     final_err = float(errs[args.warmup + args.steps - 1, 0].item()) if not use_graph else float(eng.err_cur[0].item())
 
     # dominant kernel: the X-streaming environment GEMM (one per phase)
+    oz64 = (not fp32) and eng_gemm == "ozaki"
     env_flops = eng.env_flops()
     per_launch = [env_flops[i % len(env_flops)] / (env_ms[i] * 1e-3) / 1e12 for i in range(len(env_ms))]
     env_avg_ms = float(np.mean(env_ms))
@@ -343,7 +348,7 @@ def run_ours(args):
     ebytes = 4 if fp32 else 8
     # P = the peak of the pipe actually used (fp64 on int8: the int8 rate / 36 pairs)
     peak_tf = (INT8_FP32_EQ_TFLOPS if fp32 else
-               2.0 * float(peaks.get("bf16_tflops", 1652.8)) / OZ64_PAIRS if oz64 else FP64_PEAK_TFLOPS)
+               INT8_PEAK_TOPS / OZ64_PAIRS if oz64 else FP64_PEAK_TFLOPS)
     t_roof = roofline_sweep_time(dims, ranks, peak_tf, bw, world, ebytes)
     t_roof_dmma = roofline_sweep_time(dims, ranks, FP64_PEAK_TFLOPS, bw, world, ebytes)
     sweep_s = ms_max * 1e-3
@@ -405,7 +410,7 @@ def run_ours(args):
     elif oz64:
         # fp64 on the int8 tensor cores: the algorithmic work of one launch is the 36 digit-pair
         # products over the real (unpadded) M x N x K; peak = int8 dense = 2x the measured bf16 burst
-        i8_peak = 2.0 * float(peaks.get("bf16_tflops", 1652.8))
+        i8_peak = INT8_PEAK_TOPS
         i8_tops = env_tf * OZ64_PAIRS
         roof = {"bound": "tensor", "achieved": i8_tops, "peak": i8_peak, "unit": "TFLOP/s",
                 "frac": i8_tops / i8_peak, "traffic": traffic,
@@ -414,7 +419,8 @@ def run_ours(args):
                 "ops": "int8 tensor ops = 36 x 2 M N K per launch", "flops_per_launch": env_flops,
                 "fp64_equiv_tflops": env_tf, "fp64_equiv_frac_of_dmma_peak": env_tf / FP64_PEAK_TFLOPS,
                 "avg_launch_ms": env_avg_ms, "share_of_step": env_share,
-                "peak_source": "2 x MEASURED_PEAKS.json bf16_tflops (int8 dense = 2x bf16 dense on B200)"}
+                "peak_source": "profiles/r01_i8_peak.jsonl: tcgen05 kind::i8 M128 N256 K32 microbenchmark, 148 SMs "
+                               "(burst; 4260 sustained)"}
     else:
         roof = {"bound": "tensor", "achieved": env_tf, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                 "frac": env_tf / FP64_PEAK_TFLOPS, "traffic": traffic,
@@ -431,7 +437,7 @@ def run_ours(args):
                    "variant": args.variant, "parallelism": f"shard mode 0 x{world}" if world > 1 else "single",
                    "l2": "X (%.2f GB) larger than the 126 MB L2, no flush needed" % (np.prod(dims) * ebytes / 1e9),
                    "step": "one full sweep + per-sweep relative error",
-                   "fp64_gemm": None if fp32 else args.fp64_gemm,
+                   "fp64_gemm": None if fp32 else eng_gemm,
                    "x_digits_ms": prep_ms if (fp32 or oz64) else None,
                    "launch": "CUDA graph replay" if use_graph else "eager stream launches"},
         "contraction_tflops": F / sweep_s / 1e12,
@@ -467,8 +473,9 @@ def main():
     ap.add_argument("--variant", choices=["ne", "qr", "qrne"], default="ne")
     ap.add_argument("--dtype", choices=["float64", "float32"], default="float64",
                     help="float32 = the fp32 variant (BASELINE config 4): int8 tensor-core environment products")
-    ap.add_argument("--fp64-gemm", choices=["ozaki", "dmma"], default="ozaki",
-                    help="fp64 environment products: int8 tensor-core digit slicing (default) or the DMMA pipe")
+    ap.add_argument("--fp64-gemm", choices=["auto", "ozaki", "dmma"], default="auto",
+                    help="fp64 environment products: int8 tensor-core digit slicing, the DMMA pipe, or "
+                         "auto (ozaki for products >= 4 GFLOP: c3-c5)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--eager", action="store_true", help="no CUDA graph for the small configs")
     ap.add_argument("--e2e-reps", type=int, default=2)

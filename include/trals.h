@@ -124,7 +124,7 @@ int trals_env_oz(const int8_t* d_xdigits, const int32_t* d_xexps, int64_t pre, i
  * "ozaki", the default): trals_env_f64 with X given as eight balanced digit
  * planes per K-major row,
  *   x = 2^ex[r] (d_0 2^-6 + sum_{s=1..7} d_s 2^-(6+7s)),  |d_s| <= 64,
- * (56 bits below the row maximum; same tiled layout as above with 8 planes,
+ * (remainder <= 2^-56 2^ex[r], |x| < 2^ex[r]; same tiled layout as above with 8 planes,
  * trals_oz64_digits_bytes bytes), the half chain sliced the same way per call,
  * and the 36 digit-pair products of levels s + t <= 7 accumulated exactly in
  * int32 and combined in fp64.  Accuracy against an extended-precision product

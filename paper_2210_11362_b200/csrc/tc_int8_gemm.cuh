@@ -109,14 +109,49 @@ struct OzTile {
   static_assert(STAGES >= 2, "digit stage too large for shared memory");
 };
 
+// Row tiling of a digit operand: tiles [0, nbig) are wbig rows, the rest wsmall rows
+// (A: all 128; B: N split into ceil(N / 64) tiles of widths 16 q or 16 (q + 1) <= 64,
+// so R^2 = 400 is 4 x 64 + 3 x 48 -- no MMA work on padding columns).
+struct OzRowTiles {
+  int ntiles, nbig, wbig, wsmall;
+  __host__ __device__ __forceinline__ int64_t start(int t) const {
+    return t < nbig ? static_cast<int64_t>(t) * wbig
+                    : static_cast<int64_t>(nbig) * wbig + static_cast<int64_t>(t - nbig) * wsmall;
+  }
+  __host__ __device__ __forceinline__ int width(int t) const { return t < nbig ? wbig : wsmall; }
+  __host__ __device__ __forceinline__ int64_t rows_pad() const { return start(ntiles); }
+  __host__ __device__ __forceinline__ void locate(int64_t r, int& t, int& rr) const {
+    const int64_t nb = static_cast<int64_t>(nbig) * wbig;
+    if (r < nb) {
+      t = static_cast<int>(r / wbig);
+      rr = static_cast<int>(r % wbig);
+    } else {
+      t = nbig + static_cast<int>((r - nb) / wsmall);
+      rr = static_cast<int>((r - nb) % wsmall);
+    }
+  }
+  static OzRowTiles fixed(int64_t rows, int w) {
+    const int n = static_cast<int>((rows + w - 1) / w);
+    return {n, 0, w, w};
+  }
+  static OzRowTiles balanced(int64_t rows, int wmax) {
+    const int n = static_cast<int>((rows + wmax - 1) / wmax);
+    const int units = static_cast<int>((rows + 15) / 16);
+    const int q = units / n, big = units % n;
+    return {n, big, 16 * (q + 1), 16 * q};
+  }
+};
+
 struct OzArgs {
   int64_t M, K, N;
   int64_t kchunk;
   int splits;
   int mtiles, ntiles;  // tile t -> (split, m-tile, n-tile), n fastest
+  OzRowTiles nt;       // widths of the n-tiles (<= BN)
+  int rotate;          // rotate the k-block order by the m-tile index
   int64_t kblocks;     // 64-k blocks of the tiled digit layout (ceil(K / 64))
   const int8_t* ad;    // A digits, tiled: [mtiles][kblocks][D][128 x 64 B]
-  const int8_t* bd;    // B digits, tiled: [ntiles][kblocks][D][BN x 64 B]
+  const int8_t* bd;    // B digits, tiled: [n-tile][kblocks][D][width x 64 B]
   CMap cmap;
   const int32_t* ea;  // [M] row exponents of A
   const int32_t* eb;  // [N] row exponents of B
@@ -126,11 +161,14 @@ struct OzArgs {
 
 // byte offset of (row r, k) inside the tiled digit layout of one plane block
 // (rows_per_tile rows x 64 B, SWIZZLE_64B)
-__host__ __device__ __forceinline__ int64_t oz_tiled_offset(int64_t r, int64_t k, int plane, int rows_per_tile,
+__host__ __device__ __forceinline__ int64_t oz_tiled_offset(int64_t r, int64_t k, int plane, const OzRowTiles& rt,
                                                             int64_t kblocks, int digits) {
-  const int64_t t = r / rows_per_tile, rr = r % rows_per_tile, kb = k >> 6, c = k & 63;
-  const int64_t block = (t * kblocks + kb) * digits + plane;
-  return block * rows_per_tile * 64 + rr * 64 + ((((c >> 4) ^ ((rr >> 1) & 3))) << 4) + (c & 15);
+  int t, rr;
+  rt.locate(r, t, rr);
+  const int w = rt.width(t);
+  const int64_t kb = k >> 6, c = k & 63;
+  return rt.start(t) * kblocks * 64 * digits + (kb * digits + plane) * w * 64 + rr * 64 +
+         ((((c >> 4) ^ ((rr >> 1) & 3))) << 4) + (c & 15);
 }
 
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -215,6 +253,56 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
       : "r"(taddr));
 }
 
+// One 64-k stage of MMAs for an n-tile of width W (<= BN): A plane s meets the B planes
+// t < min(D, LV - s), stacked as one N = (#planes) W operand (at most 256 / W planes per
+// MMA) issued at TMEM column (s + t0) W -- the level stride equals the plane stride of the
+// stacked operand -- so pair (s, t) lands in level block s + t (W columns each).  The
+// descriptors are linear in the smem address (start field = addr >> 4), so each MMA's
+// pair is the stage base plus a compile-time offset.
+template <int W, int BN, int D, int LV>
+__device__ __forceinline__ void oz_issue_stage(uint32_t tmem, uint64_t da, uint64_t db) {
+  constexpr int CH = 256 / W;
+  constexpr int A_PLANE = kOzBM * kOzBK, B_PLANE = W * kOzBK;
+#pragma unroll
+  for (int k = 0; k < kOzBK / 32; ++k)
+#pragma unroll
+    for (int sa = 0; sa < D; ++sa) {
+      const int nb = (D < LV - sa) ? D : LV - sa;
+#pragma unroll
+      for (int t0 = 0; t0 < nb; t0 += CH) {
+        const int cnt = (CH < nb - t0) ? CH : nb - t0;
+        umma_i8_warp(tmem + (sa + t0) * W, da + ((sa * A_PLANE + k * 32) >> 4), db + ((t0 * B_PLANE + k * 32) >> 4),
+                     i8_idesc(cnt * W), 1u);
+      }
+    }
+}
+
+// Persistent tile schedule shared by the producer, MMA and epilogue roles: CTA b runs
+// tiles b, b + gridDim.x, ...; tile t -> (split, m-tile, n-tile) with, inside a split,
+// first every wide n-tile (nbig per m-tile) of every m-tile, then every narrow one, n
+// fastest -- so the n-tiles of an m-tile run side by side in one round and read their
+// shared A stages from L2 together.  (Measured at c5, ncu: widths mixed inside a round
+// let the CTAs drift apart, 21 GB of DRAM reads per launch instead of 11; rounds cut to
+// whole m-tile groups were slower still.)
+template <class F>
+__device__ __forceinline__ void oz_for_tiles(const OzArgs& g, F&& body) {
+  const int per_split = g.mtiles * g.ntiles, total = per_split * g.splits;
+  const int nb = g.nt.nbig, ns = g.ntiles - g.nt.nbig;
+  for (int t = blockIdx.x; t < total; t += gridDim.x) {
+    const int rem = t % per_split;
+    int mt, nt;
+    if (rem < g.mtiles * nb) {
+      mt = rem / nb;
+      nt = rem % nb;
+    } else {
+      const int r2 = rem - g.mtiles * nb;
+      mt = r2 / ns;
+      nt = nb + r2 % ns;
+    }
+    body(t / per_split, mt, nt);
+  }
+}
+
 template <int BN, class SC>
 __global__ void __launch_bounds__(OzTile<BN, SC>::THREADS, 1)
 oz8_kernel(const __grid_constant__ OzArgs g) {
@@ -235,9 +323,6 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
 
   const int tid = threadIdx.x, lane = tid & 31;
   const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
-  const int per_split = g.mtiles * g.ntiles;
-  const int total = per_split * g.splits;
-
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(full + s, 1);
@@ -257,8 +342,7 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const uint32_t tmem = *tmem_slot;
 
-  auto tile_k = [&](int t, int64_t& kbeg, int& ktiles) {
-    const int split = t / per_split;
+  auto tile_k = [&](int split, int64_t& kbeg, int& ktiles) {
     kbeg = static_cast<int64_t>(split) * g.kchunk;
     const int64_t kend = (g.K < kbeg + g.kchunk) ? g.K : kbeg + g.kchunk;
     ktiles = kend > kbeg ? static_cast<int>((kend - kbeg + kOzBK - 1) / kOzBK) : 0;
@@ -268,46 +352,41 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
     // ------------------------------ bulk-copy producer ------------------------------
     if (lane == 0) {
       uint32_t gk = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      oz_for_tiles(g, [&](int split, int mt, int nt) {
         int64_t kbeg;
         int ktiles;
-        tile_k(t, kbeg, ktiles);
-        const int rem = t % per_split;
-        const int mt = rem / g.ntiles, nt = rem % g.ntiles;
+        tile_k(split, kbeg, ktiles);
+        const int bw = g.nt.width(nt);
+        const int64_t bstart = g.nt.start(nt) * g.kblocks * kOzBK * D;
         // k blocks in a rotated order (the int32 accumulation is exact, so the order is
         // free): the rotation follows the m-tile, so the CTAs that share an A tile (its
         // n-tiles run side by side) read it in step and hit L2, while different m-tiles
         // spread over different B blocks
-        const int rot = ktiles > 0 ? mt % ktiles : 0;
+        const int rot = (ktiles > 0 && g.rotate) ? mt % ktiles : 0;
         for (int kt = 0; kt < ktiles; ++kt, ++gk) {
           const uint32_t s = gk % S;
           if (gk >= S) mbar_wait(empty + s, ((gk / S) - 1) & 1);
           uint8_t* st = sm + s * T::STAGE;
-          mbar_expect_tx(full + s, T::STAGE);
+          const uint32_t bbytes = static_cast<uint32_t>(D * bw * kOzBK);
+          mbar_expect_tx(full + s, D * T::A_PLANE + bbytes);
           const int kr = kt + rot < ktiles ? kt + rot : kt + rot - ktiles;
           const int64_t kb = kbeg / kOzBK + kr;
           bulk_load(st, g.ad + (static_cast<int64_t>(mt) * g.kblocks + kb) * (D * T::A_PLANE), D * T::A_PLANE,
                     full + s);
-          bulk_load(st + D * T::A_PLANE, g.bd + (static_cast<int64_t>(nt) * g.kblocks + kb) * (D * T::B_PLANE),
-                    D * T::B_PLANE, full + s);
+          bulk_load(st + D * T::A_PLANE, g.bd + bstart + kb * bbytes, bbytes, full + s);
         }
-      }
+      });
     }
   } else if (warp == 1) {
     // ------------------------------ MMA issuer ------------------------------
-    // The whole warp runs this loop with warp-uniform values; descriptors are
-    // linear in the smem address (start field = addr >> 4), so each MMA's pair is
-    // the stage base descriptor plus a compile-time offset.  A plane s meets the B
-    // planes t < min(D, LV - s), stacked as one N = (#planes) BN operand (at most
-    // 256 / BN planes per MMA) issued at TMEM column (s + t0) BN: pair (s, t) lands in
-    // level block s + t.
-    constexpr int CH = 256 / BN;
+    // The whole warp runs this loop with warp-uniform values (oz_issue_stage).
     const uint64_t dA0 = oz_desc(smem_u32(sm)), dB0 = oz_desc(smem_u32(sm) + D * T::A_PLANE);
     uint32_t gk = 0, it = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
+    oz_for_tiles(g, [&](int split, int, int nt) {
       int64_t kbeg;
       int ktiles;
-      tile_k(t, kbeg, ktiles);
+      tile_k(split, kbeg, ktiles);
+      const int bw = g.nt.width(nt);
       mbar_wait(acc_empty, it & 1);  // accumulators drained and zeroed by the epilogue
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
       for (int kt = 0; kt < ktiles; ++kt, ++gk) {
@@ -316,18 +395,12 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         {
           const uint64_t da = dA0 + ((s * T::STAGE) >> 4), db = dB0 + ((s * T::STAGE) >> 4);
-#pragma unroll
-          for (int k = 0; k < kOzBK / 32; ++k)
-#pragma unroll
-            for (int sa = 0; sa < D; ++sa) {
-              const int nb = (D < LV - sa) ? D : LV - sa;
-#pragma unroll
-              for (int t0 = 0; t0 < nb; t0 += CH) {
-                const int cnt = (CH < nb - t0) ? CH : nb - t0;
-                umma_i8_warp(tmem + (sa + t0) * BN, da + ((sa * T::A_PLANE + k * 32) >> 4),
-                             db + ((t0 * T::B_PLANE + k * 32) >> 4), i8_idesc(cnt * BN), 1u);
-              }
-            }
+          switch (bw) {  // warp-uniform: the n-tile width fixes the MMA shapes
+            case 64: oz_issue_stage<64, BN, D, LV>(tmem, da, db); break;
+            case 48: oz_issue_stage<48, BN, D, LV>(tmem, da, db); break;
+            case 32: oz_issue_stage<32, BN, D, LV>(tmem, da, db); break;
+            default: oz_issue_stage<16, BN, D, LV>(tmem, da, db); break;
+          }
           oz_commit_warp(empty + s);  // the stage is free once these MMAs have read it
         }
         __syncwarp();
@@ -335,7 +408,8 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
       if (ktiles > 0) oz_commit_warp(acc_full);
       else if (lane == 0) mbar_arrive(acc_full);
       __syncwarp();
-    }
+      ++it;
+    });
   } else {
     // ------------------------------ epilogue ------------------------------
     // TMEM -> exact fp64 combination of the levels (Horner in 2^-7) -> smem tile
@@ -349,12 +423,13 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
     __syncwarp();
     if (lane == 0) mbar_arrive(acc_empty);
     uint32_t it = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
+    oz_for_tiles(g, [&](int split, int mt, int nt) {
       int64_t kbeg;
       int ktiles;
-      tile_k(t, kbeg, ktiles);
-      const int split = t / per_split, rem = t % per_split;
-      const int64_t m0 = static_cast<int64_t>(rem / g.ntiles) * kOzBM, n0 = static_cast<int64_t>(rem % g.ntiles) * BN;
+      tile_k(split, kbeg, ktiles);
+      const int64_t m0 = static_cast<int64_t>(mt) * kOzBM, n0 = g.nt.start(nt);
+      const int bw = g.nt.width(nt);
+      const int64_t nend = (n0 + bw < g.N) ? n0 + bw : g.N;
       mbar_wait(acc_full, it & 1);
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
       const int r = quad * 32 + lane;
@@ -368,10 +443,10 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
       double* base = part ? g.ws + static_cast<int64_t>(split) * g.M * g.N : g.C;
       const int rows = static_cast<int>((g.M - m0) < kOzBM ? (g.M - m0) : kOzBM);
 #pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 16) {
+      for (int c0 = 0; c0 < bw; c0 += 16) {
         uint32_t v[LV][16];
 #pragma unroll
-        for (int L = 0; L < LV; ++L) tmem_ld16(tlane + L * BN + c0, v[L]);
+        for (int L = 0; L < LV; ++L) tmem_ld16(tlane + L * bw + c0, v[L]);
         asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
         const int oc = T::CHUNKED ? 0 : c0;
 #pragma unroll
@@ -385,7 +460,7 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
           // store this 16-column chunk: lane -> (row parity, column), warp -> rows quad*2 + ...
           asm volatile("bar.sync 1, 128;\n" ::: "memory");
           const int64_t n = n0 + c0 + (lane & 15);
-          const bool nok = n < g.N;
+          const bool nok = n < nend;
           const uint32_t un = static_cast<uint32_t>(n);
           const int64_t coff = nok ? static_cast<int64_t>(un / N2) * sn1 + static_cast<int64_t>(un % N2) * sn2 : 0;
           const double sb = nok ? ldexp(1.0, g.eb[n]) : 0.0;
@@ -410,7 +485,7 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
 #pragma unroll
         for (int j = 0; j < BN / 32; ++j) {
           const int64_t n = n0 + lane + 32 * j;
-          nok[j] = n < g.N;
+          nok[j] = n < nend;
           const uint32_t un = static_cast<uint32_t>(n);
           coff[j] = nok[j] ? static_cast<int64_t>(un / N2) * sn1 + static_cast<int64_t>(un % N2) * sn2 : 0;
           sb[j] = nok[j] ? ldexp(1.0, g.eb[n]) : 0.0;
@@ -424,7 +499,8 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
         }
         asm volatile("bar.sync 1, 128;\n" ::: "memory");  // otile reused by the next tile
       }
-    }
+      ++it;
+    });
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
@@ -511,11 +587,11 @@ template <typename Tin, class SC>
 __global__ void __launch_bounds__(256) oz_digits_tiled_kernel(const Tin* __restrict__ x, int64_t rows, int64_t cols,
                                                               int64_t ld_in, int transpose,
                                                               const double* __restrict__ mx, int8_t* __restrict__ out,
-                                                              int rows_per_tile, int32_t* __restrict__ exps) {
+                                                              OzRowTiles rt, int32_t* __restrict__ exps) {
   constexpr int D = SC::D;
   const int64_t out_rows = transpose ? cols : rows, K = transpose ? rows : cols;
   const int64_t kblocks = (K + 63) / 64, kchunks = kblocks * 4;
-  const int64_t rows_pad = (out_rows + rows_per_tile - 1) / rows_per_tile * rows_per_tile;
+  const int64_t rows_pad = rt.rows_pad();
   const int64_t total = rows_pad * kchunks;
   for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
        idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -546,7 +622,7 @@ __global__ void __launch_bounds__(256) oz_digits_tiled_kernel(const Tin* __restr
     }
 #pragma unroll
     for (int d = 0; d < D; ++d) {
-      const int64_t off = oz_tiled_offset(orow, ch * 16, d, rows_per_tile, kblocks, D);
+      const int64_t off = oz_tiled_offset(orow, ch * 16, d, rt, kblocks, D);
       *reinterpret_cast<uint4*>(out + off) = make_uint4(w[d][0], w[d][1], w[d][2], w[d][3]);
     }
     if (rok && ch == 0) exps[orow] = e;

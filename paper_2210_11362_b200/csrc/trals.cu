@@ -478,9 +478,16 @@ int gemm_tc(const float* ahi, const float* alo, int64_t lda, int64_t M, int64_t 
 // the fp64 environment products (OzF64)
 // ---------------------------------------------------------------------------
 constexpr int kOzBN = 64;
-// bytes of a tiled digit layout: D planes x rows padded to the tile x K padded to 64
-inline int64_t oz_digits_bytes(int64_t rows, int64_t k, int rows_per_tile, int digits) {
-  return digits * ((rows + rows_per_tile - 1) / rows_per_tile * rows_per_tile) * ((k + 63) / 64 * 64);
+// bytes of a tiled digit layout: D planes x rows padded to the tiling x K padded to 64
+inline int64_t oz_digits_bytes(const trals::OzRowTiles& rt, int64_t k, int digits) {
+  return digits * rt.rows_pad() * ((k + 63) / 64 * 64);
+}
+inline trals::OzRowTiles oz_a_tiles(int64_t rows) { return trals::OzRowTiles::fixed(rows, trals::kOzBM); }
+// TRALS_OZ_FIXED_TILES=1 (experiments): every n-tile kOzBN wide, the last one zero padded
+inline trals::OzRowTiles oz_b_tiles(int64_t n) {
+  static int fixed = -1;
+  if (fixed < 0) fixed = std::getenv("TRALS_OZ_FIXED_TILES") ? 1 : 0;
+  return fixed ? trals::OzRowTiles::fixed(n, kOzBN) : trals::OzRowTiles::balanced(n, kOzBN);
 }
 
 // split-K over a per-tile time model and never more than SC::KMAX k per CTA (int32
@@ -489,13 +496,14 @@ inline int64_t oz_digits_bytes(int64_t rows, int64_t k, int rows_per_tile, int d
 template <class SC>
 SplitPlan plan_split_oz(int64_t M, int64_t K, int64_t N) {
   const int64_t BK = trals::kOzBK;
-  const int64_t tiles = ((M + trals::kOzBM - 1) / trals::kOzBM) * ((N + kOzBN - 1) / kOzBN);
+  const int64_t tiles = ((M + trals::kOzBM - 1) / trals::kOzBM) * oz_b_tiles(N).ntiles;
   const int64_t slots = kSMs;
   const int64_t smin = std::max<int64_t>(1, (K + SC::KMAX - 1) / SC::KMAX);
   const int64_t smax = std::max<int64_t>(smin, std::min<int64_t>(64, K / (4 * BK)));
   int pairs = 0;
   for (int a = 0; a < SC::D; ++a) pairs += std::min(SC::D, SC::LV - a);
-  const double t_tile = SC::BAL ? static_cast<double>(pairs) * trals::kOzBM * kOzBN * static_cast<double>(K) /
+  const double t_tile = SC::BAL ? static_cast<double>(pairs) * trals::kOzBM * N / oz_b_tiles(N).ntiles *
+                                      static_cast<double>(K) /
                                       (8192.0 * 1.9e9)
                                 : 4.0 * trals::kOzBM * static_cast<double>(K) / (6.5e12 / slots);
   const double out_bytes = 8.0 * static_cast<double>(M) * N;
@@ -521,7 +529,7 @@ OzWs oz_ws_layout(int64_t M, int64_t K, int64_t N) {
   const SplitPlan sp = plan_split_oz<SC>(M, K, N);
   OzWs w{};
   w.planes = 0;
-  w.eb = w.planes + (oz_digits_bytes(N, K, kOzBN, SC::D) + 15) / 16 * 2;
+  w.eb = w.planes + (oz_digits_bytes(oz_b_tiles(N), K, SC::D) + 15) / 16 * 2;
   w.mx = w.eb + (N + 3) / 4 * 2;
   w.part = w.mx + (N + 1) / 2 * 2;
   w.total = w.part + (sp.splits > 1 ? static_cast<int64_t>(sp.splits) * M * N : 0);
@@ -558,15 +566,19 @@ int gemm_oz(const int8_t* ad, const int32_t* ea, int64_t M, int64_t K, int64_t N
   // B^T rows = columns of B: max over k, then tiled digits (transposed read)
   if (int st = launch_colmax<double>(B, K, N, ldb, bmx, s)) return st;
   {
-    const int64_t work = oz_digits_bytes(N, K, kOzBN, SC::D) / (16 * SC::D);  // (padded row, 16-k chunk) items
+    const int64_t work = oz_digits_bytes(oz_b_tiles(N), K, SC::D) / (16 * SC::D);  // (padded row, 16-k chunk) items
     const int blocks = static_cast<int>(std::min<int64_t>((work + 255) / 256, 16 * kSMs));
-    trals::oz_digits_tiled_kernel<double, SC><<<blocks, 256, 0, s>>>(B, K, N, ldb, 1, bmx, bd, kOzBN, eb);
+    trals::oz_digits_tiled_kernel<double, SC><<<blocks, 256, 0, s>>>(B, K, N, ldb, 1, bmx, bd, oz_b_tiles(N), eb);
     if (int st = launch_status()) return st;
   }
   trals::OzArgs g{};
   g.M = M; g.K = K; g.N = N; g.kchunk = sp.kchunk; g.splits = sp.splits;
   g.mtiles = static_cast<int>((M + trals::kOzBM - 1) / trals::kOzBM);
-  g.ntiles = static_cast<int>((N + kOzBN - 1) / kOzBN);
+  g.nt = oz_b_tiles(N);
+  g.ntiles = g.nt.ntiles;
+  static int norot = -1;  // TRALS_OZ_NOROT=1 (experiments): k blocks in natural order
+  if (norot < 0) norot = std::getenv("TRALS_OZ_NOROT") ? 1 : 0;
+  g.rotate = norot ? 0 : 1;
   g.kblocks = (K + trals::kOzBK - 1) / trals::kOzBK;
   g.ad = ad; g.bd = bd;
   g.cmap = cm; g.ea = ea; g.eb = eb; g.C = C; g.ws = ws + w.part;
@@ -610,10 +622,10 @@ int oz_split(const Tin* x, int64_t rows, int64_t cols, int transpose, int8_t* di
   } else {
     if (int st = launch_colmax<Tin>(x, rows, cols, cols, ws, s)) return st;
   }
-  const int64_t work = oz_digits_bytes(out_rows, K, trals::kOzBM, SC::D) / (16 * SC::D);  // (padded row, 16-k chunk)
+  const int64_t work = oz_digits_bytes(oz_a_tiles(out_rows), K, SC::D) / (16 * SC::D);  // (padded row, 16-k chunk)
   const int blocks = static_cast<int>(std::min<int64_t>((work + 255) / 256, 64 * kSMs));
   trals::oz_digits_tiled_kernel<Tin, SC><<<blocks, 256, 0, s>>>(x, rows, cols, cols, transpose, ws, digits,
-                                                                trals::kOzBM, exps);
+                                                                oz_a_tiles(out_rows), exps);
   return launch_status();
 }
 
@@ -2217,7 +2229,7 @@ int trals_env_f64(const double* X, int64_t pre, int64_t post, int side, const do
 }
 
 int64_t trals_oz_digits_bytes(int64_t rows, int64_t k) {
-  return rows < 1 || k < 1 ? 0 : oz_digits_bytes(rows, k, trals::kOzBM, trals::OzF32::D);
+  return rows < 1 || k < 1 ? 0 : oz_digits_bytes(oz_a_tiles(rows), k, trals::OzF32::D);
 }
 
 int64_t trals_oz_split_ws_elems(int64_t rows, int64_t cols, int transpose) { return transpose ? cols : rows; }
@@ -2242,7 +2254,7 @@ int trals_env_oz(const int8_t* xd, const int32_t* xe, int64_t pre, int64_t post,
 }
 
 int64_t trals_oz64_digits_bytes(int64_t rows, int64_t k) {
-  return rows < 1 || k < 1 ? 0 : oz_digits_bytes(rows, k, trals::kOzBM, trals::OzF64::D);
+  return rows < 1 || k < 1 ? 0 : oz_digits_bytes(oz_a_tiles(rows), k, trals::OzF64::D);
 }
 
 int trals_oz64_split_f64(const double* x, int64_t rows, int64_t cols, int transpose, int8_t* digits, int32_t* exps,

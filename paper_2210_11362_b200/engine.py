@@ -37,6 +37,7 @@ import torch
 from . import _lib as L
 
 BUCKETS = ("subchain", "mttsp", "solve", "gramqr", "other")  # solvers.py:57
+OZ64_MIN_FLOPS = 4e9  # fp64_gemm="auto": smallest environment product run on the int8 tensor cores
 
 
 def _prod(v):
@@ -79,7 +80,7 @@ class SweepEngine:
 
     def __init__(self, x_local: torch.Tensor, dims, ranks, variant: str, *, shard_mode=None, lo=0, hi=None,
                  group=None, world_size: int = 1, rank_deficient_fallback=True, svd_rcond=1e-12,
-                 debug_checks=False, fp64_gemm="ozaki", _test_lib=None):
+                 debug_checks=False, fp64_gemm="auto", _test_lib=None):
         if variant not in ("als", "ne", "qr", "qrne"):
             raise ValueError(f"unsupported device variant {variant!r}")
         # `_test_lib` lets the CPU test-suite drive this exact schedule through a numpy
@@ -94,9 +95,15 @@ class SweepEngine:
         self.fp32 = x_local.dtype == torch.float32
         # fp64 X: the environment products run either on the fp64 DMMA pipe ("dmma") or on the
         # int8 tcgen05 tensor cores over 8 balanced digit planes of X ("ozaki": 36 exact int32
-        # digit-pair products combined in fp64 -- the DMMA product's accuracy at ~3x its rate)
-        if fp64_gemm not in ("dmma", "ozaki"):
-            raise ValueError(f"unknown fp64_gemm {fp64_gemm!r}; expected 'dmma' or 'ozaki'")
+        # digit-pair products combined in fp64 -- the DMMA product's accuracy at ~3x its rate).
+        # "auto": ozaki once an environment product is large enough to amortise the per-call
+        # slicing of the half chain (measured crossover: BASELINE c2, 2.1 GFLOP, is a tie)
+        if fp64_gemm not in ("auto", "dmma", "ozaki"):
+            raise ValueError(f"unknown fp64_gemm {fp64_gemm!r}; expected 'auto', 'dmma' or 'ozaki'")
+        if fp64_gemm == "auto":
+            env_flops = 2.0 * _prod(x_local.shape) * max(int(r) for r in ranks) ** 2
+            fp64_gemm = "ozaki" if env_flops >= OZ64_MIN_FLOPS else "dmma"
+        self.fp64_gemm = fp64_gemm
         self.oz64 = (not self.fp32) and fp64_gemm == "ozaki" and _test_lib is None
         self.sliced = self.fp32 or self.oz64
         self.lib = _test_lib if _test_lib is not None else L.lib()

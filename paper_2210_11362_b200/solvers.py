@@ -29,7 +29,7 @@ ERROR_MODES = ("exact", "cheap", "none")         # solvers.py:56
 BUCKETS = ("subchain", "mttsp", "solve", "gramqr", "other")  # solvers.py:57
 SVD_RCOND_DEFAULT = 1e-12                        # linalg.py:20
 DTYPES = ("float64", "float32")                  # AlsConfig.dtype (extension)
-FP64_GEMMS = ("ozaki", "dmma")                    # AlsConfig.fp64_gemm (extension)
+FP64_GEMMS = ("auto", "ozaki", "dmma")            # AlsConfig.fp64_gemm (extension)
 
 
 @dataclass
@@ -50,11 +50,12 @@ class AlsConfig:
     reference is ~1e-4 instead of 1e-9.
 
     `fp64_gemm` (extension) selects the engine of the fp64 environment
-    products (the X-streaming MTTSP, solvers.py:379): "ozaki" (default) runs
+    products (the X-streaming MTTSP, solvers.py:379): "ozaki" runs
     them on the int8 tcgen05 tensor cores over 8 balanced digit slices of X
     and of the half chain -- 36 exact int32 digit-pair products combined in
     fp64, with the accuracy of an fp64 product (measured against an
-    extended-precision one) -- and "dmma" on the fp64 DMMA pipe.  X's digit
+    extended-precision one) -- "dmma" on the fp64 DMMA pipe, and "auto"
+    (default) picks ozaki when 2 |X| R^2 >= 4 GFLOP (BASELINE c3-c5).  X's digit
     planes (2 x |X| bytes) are made once per call, timed as
     upfront_seconds["mttsp"].
     """
@@ -72,7 +73,7 @@ class AlsConfig:
     shard_mode: int = 0
     timing_buckets: bool = True
     dtype: str = "float64"
-    fp64_gemm: str = "ozaki"
+    fp64_gemm: str = "auto"
 
 
 @dataclass
