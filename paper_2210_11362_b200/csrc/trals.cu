@@ -1513,12 +1513,13 @@ __global__ void __launch_bounds__(1024) pinv_fallback_kernel(const double* __res
 //    also stores its reflectors, then column chunks of the rest are multiplied
 //    by Q^T in parallel CTAs.
 // ---------------------------------------------------------------------------
-constexpr int kHhThreads = 512;
+constexpr int kHhThreads = 256;
 constexpr size_t kHhSmemMax = 216 * 1024;
+constexpr int kHhNB = 8;           // reflectors per panel (compact WY block)
+constexpr int kHhPanelRows = 224;  // rows one warp holds in registers for a panel (7 per lane)
 
-// In-place Householder on A (mr x nc, row pitch ld) in shared memory. Reflector j
-// is left in A[j+1.., j] with tau[j]; R in the upper triangle.
-__device__ void hh_factor_smem(double* A, int ld, int mr, int nc, double* tau, double* red) {
+// Unblocked fallback for matrices taller than kHhPanelRows (three barriers per reflector).
+__device__ void hh_factor_unblocked(double* A, int ld, int mr, int nc, double* tau, double* red) {
   const int tid = threadIdx.x, lane = tid & 31, nwarps = blockDim.x >> 5;
   const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
   const int k = min(mr, nc);
@@ -1561,6 +1562,233 @@ __device__ void hh_factor_smem(double* A, int ld, int mr, int nc, double* tau, d
   }
 }
 
+
+// Panel [p, p+nb) x rows [p, mr) factored by one warp in registers (lane holds rows
+// p + lane + 32 i): per column a shuffle-reduced norm, the LAPACK reflector (v_0 = 1,
+// beta = -sign(alpha)|x|, tau = (beta - alpha)/beta), and its application to the rest of
+// the panel with all the column dot products reduced together.  Writes the panel back,
+// tau[p..], and the panel's compact-WY factor T (8 x 8 upper, H_1..H_nb = I - V T V^T;
+// dlarft's forward recurrence) to T and, if Tg != nullptr, to Tg.  Columns >= nb and
+// rows >= mr are zero padding, so every step runs unconditionally (no branch around
+// the shuffles) and yields tau = 0 there.
+template <int RPL>
+__device__ void hh_panel_warp(double* A, int ld, int mr, int p, int nb, double* tau, double* T, double* Tg) {
+  const int lane = threadIdx.x & 31;
+  double a[RPL][kHhNB];
+#pragma unroll
+  for (int i = 0; i < RPL; ++i)
+#pragma unroll
+    for (int c = 0; c < kHhNB; ++c) {
+      const int r = p + lane + 32 * i;
+      a[i][c] = (r < mr && c < nb) ? A[r * ld + p + c] : 0.0;
+    }
+  double taus[kHhNB];
+#pragma unroll
+  for (int jj = 0; jj < kHhNB; ++jj) {
+    // one fused reduction per column: |x|^2 below the diagonal and x . a_c for every
+    // panel column c > jj (v = scale x is applied afterwards: v . a_c = a_jj,c + scale x . a_c)
+    double red[kHhNB];
+#pragma unroll
+    for (int c = jj; c < kHhNB; ++c) red[c] = 0.0;
+#pragma unroll
+    for (int i = 0; i < RPL; ++i)
+      if (lane + 32 * i > jj) {
+#pragma unroll
+        for (int c = jj; c < kHhNB; ++c) red[c] = fma(a[i][jj], a[i][c], red[c]);
+      }
+    double top[kHhNB];  // row jj of the panel (lane jj), broadcast while the reduction runs
+#pragma unroll
+    for (int c = jj; c < kHhNB; ++c) top[c] = __shfl_sync(0xffffffffu, a[0][c], jj);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int c = jj; c < kHhNB; ++c) red[c] += __shfl_xor_sync(0xffffffffu, red[c], o);
+    const double s = red[jj], alpha = top[jj];
+    double t = 0.0, scale = 0.0, beta = alpha;
+    if (s > 0.0) {
+      const double nrm = sqrt(alpha * alpha + s);
+      beta = alpha >= 0.0 ? -nrm : nrm;
+      t = (beta - alpha) / beta;
+      scale = 1.0 / (alpha - beta);
+    }
+#pragma unroll
+    for (int i = 0; i < RPL; ++i)
+      if (lane + 32 * i > jj) a[i][jj] *= scale;
+    if (lane == jj) a[0][jj] = beta;
+    taus[jj] = t;
+#pragma unroll
+    for (int c = jj + 1; c < kHhNB; ++c) {
+      const double w = t * fma(scale, red[c], top[c]);
+      if (lane == jj) a[0][c] -= w;
+#pragma unroll
+      for (int i = 0; i < RPL; ++i)
+        if (lane + 32 * i > jj) a[i][c] = fma(-w, a[i][jj], a[i][c]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < RPL; ++i)
+#pragma unroll
+    for (int c = 0; c < kHhNB; ++c) {
+      const int r = p + lane + 32 * i;
+      if (r < mr && c < nb) A[r * ld + p + c] = a[i][c];
+    }
+  // G = V^T V (strict upper part): v_c1 . v_c2 = v_c1[row c2] + sum_{rows > c2} v_c1 v_c2
+  double g[kHhNB][kHhNB];
+#pragma unroll
+  for (int c1 = 0; c1 < kHhNB; ++c1)
+#pragma unroll
+    for (int c2 = c1 + 1; c2 < kHhNB; ++c2) {
+      double v = (lane == c2) ? a[0][c1] : 0.0;
+#pragma unroll
+      for (int i = 0; i < RPL; ++i)
+        if (lane + 32 * i > c2) v = fma(a[i][c1], a[i][c2], v);
+      g[c1][c2] = v;
+    }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int c1 = 0; c1 < kHhNB; ++c1)
+#pragma unroll
+      for (int c2 = c1 + 1; c2 < kHhNB; ++c2) g[c1][c2] += __shfl_xor_sync(0xffffffffu, g[c1][c2], o);
+  // T row by row in parallel: lane i < 8 owns row i, T[i][jj] = -tau_jj sum_{i<=l<jj} T[i][l] G[l][jj]
+  // (every index compile-time; the lane's own row selected by predicates)
+  {
+    double trow[kHhNB];
+#pragma unroll
+    for (int jj = 0; jj < kHhNB; ++jj) {
+      double acc = 0.0;
+#pragma unroll
+      for (int l = 0; l < jj; ++l) acc = (l >= lane) ? fma(trow[l], g[l][jj], acc) : acc;
+      trow[jj] = (jj < lane) ? 0.0 : (jj == lane ? taus[jj] : -taus[jj] * acc);
+    }
+    if (lane < kHhNB) {
+#pragma unroll
+      for (int jj = 0; jj < kHhNB; ++jj) {
+        T[lane * kHhNB + jj] = trow[jj];
+        if (Tg) Tg[lane * kHhNB + jj] = trow[jj];
+      }
+    }
+  }
+#pragma unroll
+  for (int jj = 0; jj < kHhNB; ++jj)
+    if (lane == jj && jj < nb) tau[p + jj] = taus[jj];
+}
+
+// V(r, t) of a staged panel: reflector t at absolute row r (1 at row p + t, 0 above or
+// for padding reflectors t >= nb or rows >= mr, the stored entry below)
+__device__ __forceinline__ double hh_v(const double* V, int vld, int p, int nb, int mr, int r, int t) {
+  const int rel = r - p;
+  if (t >= nb || r >= mr || rel < t) return 0.0;
+  return rel == t ? 1.0 : V[r * vld + t];
+}
+
+// Q_panel^T applied to the columns [c_lo, c_hi) of A (rows [p, mr)) on the DMMA pipe
+// (mma.sync m8n8k4 f64): per 8-column group, W = V^T A_c (8 x 8, k over the rows),
+// W' = T^T W, A_c -= V W' (8-row tiles, k over the 8 reflectors).  V[r * vld + t] =
+// reflector t at absolute row r.  Column groups go to warps wid, wid + nw, ...;
+// scratch = 64 doubles per warp (W / W' handed from the accumulator to the operand
+// layout).  Reductions run in a fixed order: deterministic.
+__device__ void hh_panel_apply(const double* V, int vld, const double* T, int nb, double* A, int ld, int mr, int p,
+                               int c_lo, int c_hi, int wid, int nw, double* scratch) {
+  if (c_hi <= c_lo || wid >= nw) return;
+  const int lane = threadIdx.x & 31, fr = lane >> 2, fk = lane & 3;
+  const int groups = (c_hi - c_lo + 7) / 8;
+  for (int gi = wid; gi < groups; gi += nw) {
+    const int c0 = c_lo + 8 * gi;
+    // W[t][c] = sum_r V(r, t) A[r][c0 + c]
+    // two independent accumulation chains (even / odd 4-row steps), summed at the end
+    double w0 = 0.0, w1 = 0.0, y0 = 0.0, y1 = 0.0;
+    const int colb = c0 + fr;
+    const bool cb = colb < c_hi;
+    for (int r0 = p; r0 < mr; r0 += 8) {
+      const int r = r0 + fk, r2 = r0 + 4 + fk;
+      const double av = hh_v(V, vld, p, nb, mr, r, fr);
+      const double bv = (cb && r < mr) ? A[r * ld + colb] : 0.0;
+      const double av2 = hh_v(V, vld, p, nb, mr, r2, fr);
+      const double bv2 = (cb && r2 < mr) ? A[r2 * ld + colb] : 0.0;
+      trals::dmma884(w0, w1, av, bv);
+      trals::dmma884(y0, y1, av2, bv2);
+    }
+    scratch[fr * 8 + 2 * fk] = w0 + y0;
+    scratch[fr * 8 + 2 * fk + 1] = w1 + y1;
+    __syncwarp();
+    // W'[t][c] = sum_u T[u][t] W[u][c]
+    double x0 = 0.0, x1 = 0.0;
+#pragma unroll
+    for (int u0 = 0; u0 < 8; u0 += 4) {
+      const double av = T[(u0 + fk) * 8 + fr];
+      const double bv = scratch[(u0 + fk) * 8 + fr];
+      trals::dmma884(x0, x1, av, bv);
+    }
+    __syncwarp();
+    scratch[fr * 8 + 2 * fk] = x0;
+    scratch[fr * 8 + 2 * fk + 1] = x1;
+    __syncwarp();
+    // A[r][c0 + c] -= sum_t V(r, t) W'[t][c], 8-row tiles
+    const double b0 = scratch[fk * 8 + fr], b1 = scratch[(4 + fk) * 8 + fr];
+    const int cc = c0 + 2 * fk;
+#pragma unroll 2
+    for (int r8 = p; r8 < mr; r8 += 8) {
+      const int r = r8 + fr;
+      const bool rok = r < mr;
+      double* row = A + r * ld;
+      double d0 = (rok && cc < c_hi) ? row[cc] : 0.0;
+      double d1 = (rok && cc + 1 < c_hi) ? row[cc + 1] : 0.0;
+      trals::dmma884(d0, d1, -hh_v(V, vld, p, nb, mr, r, fk), b0);
+      trals::dmma884(d0, d1, -hh_v(V, vld, p, nb, mr, r, 4 + fk), b1);
+      if (rok && cc < c_hi) row[cc] = d0;
+      if (rok && cc + 1 < c_hi) row[cc + 1] = d1;
+    }
+    __syncwarp();
+  }
+}
+
+// Blocked in-place Householder QR of A (mr x nc, pitch ld, mr <= 32 RPL) in shared
+// memory: reflector j in A[j+1.., j], tau[j], R in the upper triangle; the T factor of
+// panel b goes to Tg + 64 b when Tg != nullptr.  Look-ahead: warp 0 applies panel b
+// to the columns of panel b+1 and factors panel b+1 while the other warps apply panel
+// b to everything right of it -- one barrier per 8 reflectors.
+template <int RPL>
+__device__ void hh_factor_blocked(double* A, int ld, int mr, int nc, double* tau, double* Tbuf, double* Tg,
+                                  double* scratch) {
+  const int warp = __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0);
+  const int nwarps = blockDim.x >> 5;
+  const int k = min(mr, nc);
+  if (warp == 0) hh_panel_warp<RPL>(A, ld, mr, 0, min(kHhNB, k), tau, Tbuf, Tg);
+  __syncthreads();
+  int it = 0;
+  for (int p = 0; p < k; p += kHhNB, ++it) {
+    const int nb = min(kHhNB, k - p);
+    const int nx = p + nb;
+    const int nbx = min(kHhNB, k - nx);
+    const double* T = Tbuf + (it & 1) * 64;
+    double* Tn = Tbuf + ((it + 1) & 1) * 64;
+    if (warp == 0) {
+      if (nbx > 0) {
+        hh_panel_apply(A + p, ld, T, nb, A, ld, mr, p, nx, nx + nbx, 0, 1, scratch);
+        __syncwarp();
+        hh_panel_warp<RPL>(A, ld, mr, nx, nbx, tau, Tn, Tg ? Tg + static_cast<int64_t>(it + 1) * 64 : nullptr);
+      }
+    } else {
+      hh_panel_apply(A + p, ld, T, nb, A, ld, mr, p, nbx > 0 ? nx + nbx : nx, nc, warp - 1, nwarps - 1,
+                     scratch + 64 * warp);
+    }
+    __syncthreads();
+  }
+}
+
+// In-place QR of the smem matrix: blocked for mr <= kHhPanelRows, else unblocked.
+// Tbuf: 128 doubles; Tg: optional per-panel T output (blocked path only).
+// scratch: 64 doubles per warp.
+__device__ void hh_factor_smem(double* A, int ld, int mr, int nc, double* tau, double* red, double* Tbuf,
+                               double* Tg, double* scratch) {
+  if (mr <= 32) hh_factor_blocked<1>(A, ld, mr, nc, tau, Tbuf, Tg, scratch);
+  else if (mr <= 64) hh_factor_blocked<2>(A, ld, mr, nc, tau, Tbuf, Tg, scratch);
+  else if (mr <= 128) hh_factor_blocked<4>(A, ld, mr, nc, tau, Tbuf, Tg, scratch);
+  else if (mr <= kHhPanelRows) hh_factor_blocked<7>(A, ld, mr, nc, tau, Tbuf, Tg, scratch);
+  else hh_factor_unblocked(A, ld, mr, nc, tau, red);
+}
+
 // load rows [r0, r0+mr) x cols [0, nc) of a row-major global matrix (pitch gld) into smem (pitch ld)
 __device__ void hh_load(double* A, int ld, const double* G, int64_t gld, int r0, int mr, int nc) {
   for (int t = threadIdx.x; t < mr * nc; t += blockDim.x) {
@@ -1586,12 +1814,14 @@ __device__ void hh_store_r(const double* A, int ld, int mr, int nc, double* R, b
 }
 
 // one CTA: QR of rows [r0, r0+mr) of G (or of two stacked R blocks when G2 != nullptr)
-__global__ void __launch_bounds__(kHhThreads) hh_block_kernel(const double* __restrict__ G, int64_t gld, int mr, int nc,
+__global__ void __launch_bounds__(kHhThreads, 1) hh_block_kernel(const double* __restrict__ G, int64_t gld, int mr, int nc,
                                                               const double* __restrict__ G2, int mr2,
                                                               double* __restrict__ R, int64_t rstride, int sign) {
   extern __shared__ __align__(16) double A[];
   __shared__ double red[32];
   __shared__ double tau[512];
+  __shared__ double Tbuf[128];
+  __shared__ double scratch[64 * (kHhThreads / 32)];
   const int ld = nc + 1;
   const int b = blockIdx.x;
   int m_all;
@@ -1613,67 +1843,77 @@ __global__ void __launch_bounds__(kHhThreads) hh_block_kernel(const double* __re
     }
   }
   __syncthreads();
-  hh_factor_smem(A, ld, m_all, nc, tau, red);
+  hh_factor_smem(A, ld, m_all, nc, tau, red, Tbuf, nullptr, scratch);
   // intermediate TSQR factors are zero-padded to nc rows so they stack uniformly
   const int rows_out = sign ? min(m_all, nc) : nc;
   hh_store_r(A, ld, m_all, nc, R + static_cast<int64_t>(b) * rstride, sign != 0, rows_out);
 }
 
-// wide: factor the left I x I block, keep its reflectors (V below the diagonal, tau) in global
-__global__ void __launch_bounds__(kHhThreads) hh_left_kernel(const double* __restrict__ G, int I, int nc,
+// wide: factor the left I x I block (I <= kHhPanelRows, blocked); keep it row-major in
+// Vg (reflectors below the diagonal, R_left above) and the per-panel T factors in Tg
+__global__ void __launch_bounds__(kHhThreads, 1) hh_left_kernel(const double* __restrict__ G, int I, int nc,
                                                              double* __restrict__ R, double* __restrict__ Vg,
-                                                             double* __restrict__ taug) {
+                                                             double* __restrict__ Tg) {
   extern __shared__ __align__(16) double A[];
   __shared__ double red[32];
   __shared__ double tau[512];
+  __shared__ double Tbuf[128];
+  __shared__ double scratch[64 * (kHhThreads / 32)];
   const int ld = I + 1;
   for (int t = threadIdx.x; t < I * I; t += blockDim.x) {
     const int r = t / I, c = t - r * I;
     A[r * ld + c] = G[static_cast<int64_t>(r) * nc + c];
   }
   __syncthreads();
-  hh_factor_smem(A, ld, I, I, tau, red);
+  hh_factor_smem(A, ld, I, I, tau, red, Tbuf, Tg, scratch);
+  __syncthreads();
   for (int t = threadIdx.x; t < I * I; t += blockDim.x) {
     const int r = t / I, c = t - r * I;
     const double v = A[r * ld + c];
-    // transposed: row j of Vg = column j of the factored block (reflector j below the diagonal,
-    // R_left's column j above it) so the apply kernel streams reflectors contiguously
-    Vg[static_cast<int64_t>(c) * I + r] = v;
+    Vg[static_cast<int64_t>(r) * I + c] = v;
     const double sgn = A[r * ld + r] < 0.0 ? -1.0 : 1.0;
     R[static_cast<int64_t>(r) * nc + c] = c >= r ? sgn * v : 0.0;
   }
-  for (int t = threadIdx.x; t < I; t += blockDim.x) taug[t] = tau[t];
 }
 
-// wide: R[:, c0:c0+w] = Q^T G[:, c0:c0+w] for a column chunk (one CTA), sign-normalised by diag(R_left)
-__global__ void __launch_bounds__(kHhThreads) hh_apply_kernel(const double* __restrict__ G, int I, int nc,
+// wide: R[:, c0:c0+w] = Q^T G[:, c0:c0+w] for a column chunk (one CTA), sign-normalised by
+// diag(R_left): the left block's panels applied in order (compact WY), each panel's
+// V (I x 8) and T staged in shared memory, the next one prefetched while the current
+// one is applied -- one barrier per 8 reflectors.
+__global__ void __launch_bounds__(kHhThreads, 1) hh_apply_kernel(const double* __restrict__ G, int I, int nc,
                                                               const double* __restrict__ Vg,
-                                                              const double* __restrict__ taug, int cw,
+                                                              const double* __restrict__ Tg, int cw,
                                                               double* __restrict__ R) {
-  extern __shared__ __align__(16) double A[];  // [I][cw + 1]
-  const int tid = threadIdx.x, lane = tid & 31, nwarps = blockDim.x >> 5;
+  extern __shared__ __align__(16) double A[];  // [I][cw + 1], then 2 x (V [I][8] + T [64])
+  __shared__ double scratch[64 * (kHhThreads / 32)];
+  const int tid = threadIdx.x;
   const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
   const int c0 = I + blockIdx.x * cw;
   const int w = min(cw, nc - c0);
   const int ld = cw + 1;
+  const int stage = I * kHhNB + 64;
+  double* buf = A + static_cast<int64_t>(I) * ld;
+  auto fetch = [&](int panel, double* dst) {
+    const int p = panel * kHhNB, nb = min(kHhNB, I - p);
+    for (int t = tid; t < (I - p) * kHhNB; t += blockDim.x) {
+      const int r = p + t / kHhNB, c = t % kHhNB;
+      dst[r * kHhNB + c] = c < nb ? Vg[static_cast<int64_t>(r) * I + p + c] : 0.0;
+    }
+    for (int t = tid; t < 64; t += blockDim.x) dst[I * kHhNB + t] = Tg[static_cast<int64_t>(panel) * 64 + t];
+  };
   for (int t = tid; t < I * w; t += blockDim.x) {
     const int r = t / w, c = t - r * w;
     A[r * ld + c] = G[static_cast<int64_t>(r) * nc + c0 + c];
   }
+  const int panels = (I + kHhNB - 1) / kHhNB;
+  fetch(0, buf);
   __syncthreads();
-  for (int j = 0; j < I; ++j) {
-    const double t = taug[j];
-    if (t != 0.0) {
-      for (int c = warp; c < w; c += nwarps) {
-        double s = (lane == 0) ? A[j * ld + c] : 0.0;
-        const double* vj = Vg + static_cast<int64_t>(j) * I;
-        for (int r = j + 1 + lane; r < I; r += 32) s = fma(vj[r], A[r * ld + c], s);
-        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        const double ts = t * s;
-        if (lane == 0) A[j * ld + c] -= ts;
-        for (int r = j + 1 + lane; r < I; r += 32) A[r * ld + c] = fma(-ts, vj[r], A[r * ld + c]);
-      }
-    }
+  for (int b = 0; b < panels; ++b) {
+    double* cur = buf + (b & 1) * stage;
+    if (b + 1 < panels) fetch(b + 1, buf + ((b + 1) & 1) * stage);
+    const int p = b * kHhNB;
+    hh_panel_apply(cur, kHhNB, cur + I * kHhNB, min(kHhNB, I - p), A, ld, I, p, 0, w, warp, blockDim.x >> 5,
+                   scratch + 64 * warp);
     __syncthreads();
   }
   for (int t = tid; t < I * w; t += blockDim.x) {
@@ -1693,14 +1933,15 @@ struct HhPlan {
 HhPlan hh_plan(int I, int nc) {
   HhPlan p{};
   const size_t whole = sizeof(double) * static_cast<size_t>(I) * (nc + 1);
-  if (whole <= kHhSmemMax && I <= 4096) {
+  if (whole <= kHhSmemMax && I <= kHhPanelRows) {
     p.kind = 0;
     return p;
   }
   if (I > nc) {
-    // rows per leaf such that a leaf and a stacked pair (2 nc rows) both fit
+    // rows per leaf: a leaf and a stacked pair (2 nc rows) both fit; the register-panel
+    // (blocked) factorisation when both are <= kHhPanelRows rows
     int chunk = static_cast<int>(kHhSmemMax / (sizeof(double) * (nc + 1)));
-    chunk = std::min(chunk, 4096);
+    chunk = std::min(chunk, 2 * nc <= kHhPanelRows ? kHhPanelRows : 4096);
     p.kind = 1;
     p.chunk = chunk;
     p.leaves = (I + chunk - 1) / chunk;
@@ -1708,16 +1949,19 @@ HhPlan hh_plan(int I, int nc) {
     return p;
   }
   p.kind = 2;
-  int cw = static_cast<int>(kHhSmemMax / (sizeof(double) * I)) - 1;
-  cw = std::max(8, std::min(cw, 256));
+  // column chunk: A [I][cw + 1] + two staged panels (V [I][8] + T [64])
+  int cw = static_cast<int>((kHhSmemMax / sizeof(double) - 2 * (static_cast<size_t>(I) * kHhNB + 64)) / I) - 1;
+  // narrow chunks: an apply CTA's time is the per-panel latency chain, not its columns,
+  // so more CTAs finish sooner (one 8-column group per warp)
+  cw = std::max(8, std::min(cw, 8 * (kHhThreads / 32)));
   p.chunk = cw;
-  p.ws = static_cast<int64_t>(I) * I + I;
+  p.ws = static_cast<int64_t>(I) * I + 64 * ((I + kHhNB - 1) / kHhNB);
   return p;
 }
 
 bool hh_supported(int I, int nc) {
   if (I > nc) return 2 * static_cast<size_t>(nc) * (nc + 1) * sizeof(double) <= kHhSmemMax && nc <= 512;
-  return static_cast<size_t>(I) * (I + 1) * sizeof(double) <= kHhSmemMax && I <= 512;
+  return static_cast<size_t>(I) * (I + 1) * sizeof(double) <= kHhSmemMax && I <= kHhPanelRows;
 }
 
 int hh_qr(const double* G, int I, int nc, double* R, double* ws, int64_t ws_elems, cudaStream_t s) {
@@ -1761,14 +2005,14 @@ int hh_qr(const double* G, int I, int nc, double* R, double* ws, int64_t ws_elem
   }
   // wide
   double* Vg = ws;
-  double* taug = ws + static_cast<int64_t>(I) * I;
-  hh_left_kernel<<<1, kHhThreads, sizeof(double) * static_cast<size_t>(I) * (I + 1), s>>>(G, I, nc, R, Vg, taug);
+  double* Tg = ws + static_cast<int64_t>(I) * I;
+  hh_left_kernel<<<1, kHhThreads, sizeof(double) * static_cast<size_t>(I) * (I + 1), s>>>(G, I, nc, R, Vg, Tg);
   if (int st = launch_status()) return st;
   const int rest = nc - I;
   if (rest > 0) {
     const int blocks = (rest + p.chunk - 1) / p.chunk;
-    hh_apply_kernel<<<blocks, kHhThreads, sizeof(double) * static_cast<size_t>(I) * (p.chunk + 1), s>>>(
-        G, I, nc, Vg, taug, p.chunk, R);
+    const size_t smem = sizeof(double) * (static_cast<size_t>(I) * (p.chunk + 1) + 2 * (static_cast<size_t>(I) * kHhNB + 64));
+    hh_apply_kernel<<<blocks, kHhThreads, smem, s>>>(G, I, nc, Vg, Tg, p.chunk, R);
     return launch_status();
   }
   return TRALS_OK;
