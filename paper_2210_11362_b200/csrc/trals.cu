@@ -1516,7 +1516,7 @@ __global__ void __launch_bounds__(1024) pinv_fallback_kernel(const double* __res
 constexpr int kHhThreads = 256;
 constexpr size_t kHhSmemMax = 216 * 1024;
 constexpr int kHhNB = 8;           // reflectors per panel (compact WY block)
-constexpr int kHhPanelRows = 224;  // rows one warp holds in registers for a panel (7 per lane)
+constexpr int kHhPanelRows = 256;  // panel rows a team of up to 4 warps holds in registers (2 per lane)
 
 // Unblocked fallback for matrices taller than kHhPanelRows (three barriers per reflector).
 __device__ void hh_factor_unblocked(double* A, int ld, int mr, int nc, double* tau, double* red) {
@@ -1562,117 +1562,6 @@ __device__ void hh_factor_unblocked(double* A, int ld, int mr, int nc, double* t
   }
 }
 
-
-// Panel [p, p+nb) x rows [p, mr) factored by one warp in registers (lane holds rows
-// p + lane + 32 i): per column a shuffle-reduced norm, the LAPACK reflector (v_0 = 1,
-// beta = -sign(alpha)|x|, tau = (beta - alpha)/beta), and its application to the rest of
-// the panel with all the column dot products reduced together.  Writes the panel back,
-// tau[p..], and the panel's compact-WY factor T (8 x 8 upper, H_1..H_nb = I - V T V^T;
-// dlarft's forward recurrence) to T and, if Tg != nullptr, to Tg.  Columns >= nb and
-// rows >= mr are zero padding, so every step runs unconditionally (no branch around
-// the shuffles) and yields tau = 0 there.
-template <int RPL>
-__device__ void hh_panel_warp(double* A, int ld, int mr, int p, int nb, double* tau, double* T, double* Tg) {
-  const int lane = threadIdx.x & 31;
-  double a[RPL][kHhNB];
-#pragma unroll
-  for (int i = 0; i < RPL; ++i)
-#pragma unroll
-    for (int c = 0; c < kHhNB; ++c) {
-      const int r = p + lane + 32 * i;
-      a[i][c] = (r < mr && c < nb) ? A[r * ld + p + c] : 0.0;
-    }
-  double taus[kHhNB];
-#pragma unroll
-  for (int jj = 0; jj < kHhNB; ++jj) {
-    // one fused reduction per column: |x|^2 below the diagonal and x . a_c for every
-    // panel column c > jj (v = scale x is applied afterwards: v . a_c = a_jj,c + scale x . a_c)
-    double red[kHhNB];
-#pragma unroll
-    for (int c = jj; c < kHhNB; ++c) red[c] = 0.0;
-#pragma unroll
-    for (int i = 0; i < RPL; ++i)
-      if (lane + 32 * i > jj) {
-#pragma unroll
-        for (int c = jj; c < kHhNB; ++c) red[c] = fma(a[i][jj], a[i][c], red[c]);
-      }
-    double top[kHhNB];  // row jj of the panel (lane jj), broadcast while the reduction runs
-#pragma unroll
-    for (int c = jj; c < kHhNB; ++c) top[c] = __shfl_sync(0xffffffffu, a[0][c], jj);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-      for (int c = jj; c < kHhNB; ++c) red[c] += __shfl_xor_sync(0xffffffffu, red[c], o);
-    const double s = red[jj], alpha = top[jj];
-    double t = 0.0, scale = 0.0, beta = alpha;
-    if (s > 0.0) {
-      const double nrm = sqrt(alpha * alpha + s);
-      beta = alpha >= 0.0 ? -nrm : nrm;
-      t = (beta - alpha) / beta;
-      scale = 1.0 / (alpha - beta);
-    }
-#pragma unroll
-    for (int i = 0; i < RPL; ++i)
-      if (lane + 32 * i > jj) a[i][jj] *= scale;
-    if (lane == jj) a[0][jj] = beta;
-    taus[jj] = t;
-#pragma unroll
-    for (int c = jj + 1; c < kHhNB; ++c) {
-      const double w = t * fma(scale, red[c], top[c]);
-      if (lane == jj) a[0][c] -= w;
-#pragma unroll
-      for (int i = 0; i < RPL; ++i)
-        if (lane + 32 * i > jj) a[i][c] = fma(-w, a[i][jj], a[i][c]);
-    }
-  }
-#pragma unroll
-  for (int i = 0; i < RPL; ++i)
-#pragma unroll
-    for (int c = 0; c < kHhNB; ++c) {
-      const int r = p + lane + 32 * i;
-      if (r < mr && c < nb) A[r * ld + p + c] = a[i][c];
-    }
-  // G = V^T V (strict upper part): v_c1 . v_c2 = v_c1[row c2] + sum_{rows > c2} v_c1 v_c2
-  double g[kHhNB][kHhNB];
-#pragma unroll
-  for (int c1 = 0; c1 < kHhNB; ++c1)
-#pragma unroll
-    for (int c2 = c1 + 1; c2 < kHhNB; ++c2) {
-      double v = (lane == c2) ? a[0][c1] : 0.0;
-#pragma unroll
-      for (int i = 0; i < RPL; ++i)
-        if (lane + 32 * i > c2) v = fma(a[i][c1], a[i][c2], v);
-      g[c1][c2] = v;
-    }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-    for (int c1 = 0; c1 < kHhNB; ++c1)
-#pragma unroll
-      for (int c2 = c1 + 1; c2 < kHhNB; ++c2) g[c1][c2] += __shfl_xor_sync(0xffffffffu, g[c1][c2], o);
-  // T row by row in parallel: lane i < 8 owns row i, T[i][jj] = -tau_jj sum_{i<=l<jj} T[i][l] G[l][jj]
-  // (every index compile-time; the lane's own row selected by predicates)
-  {
-    double trow[kHhNB];
-#pragma unroll
-    for (int jj = 0; jj < kHhNB; ++jj) {
-      double acc = 0.0;
-#pragma unroll
-      for (int l = 0; l < jj; ++l) acc = (l >= lane) ? fma(trow[l], g[l][jj], acc) : acc;
-      trow[jj] = (jj < lane) ? 0.0 : (jj == lane ? taus[jj] : -taus[jj] * acc);
-    }
-    if (lane < kHhNB) {
-#pragma unroll
-      for (int jj = 0; jj < kHhNB; ++jj) {
-        T[lane * kHhNB + jj] = trow[jj];
-        if (Tg) Tg[lane * kHhNB + jj] = trow[jj];
-      }
-    }
-  }
-#pragma unroll
-  for (int jj = 0; jj < kHhNB; ++jj)
-    if (lane == jj && jj < nb) tau[p + jj] = taus[jj];
-}
 
 // V(r, t) of a staged panel: reflector t at absolute row r (1 at row p + t, 0 above or
 // for padding reflectors t >= nb or rows >= mr, the stored entry below)
@@ -1743,18 +1632,158 @@ __device__ void hh_panel_apply(const double* V, int vld, const double* T, int nb
   }
 }
 
-// Blocked in-place Householder QR of A (mr x nc, pitch ld, mr <= 32 RPL) in shared
+// Panel [p, p+nb) x rows [p, mr) factored by a team of NT warps (warps [0, NT)) in
+// registers: row p + rel with rel = lane + 32 (wt + NT i), i < 2, lives in warp wt, so
+// the diagonal rows p..p+7 are in warp 0.  Per column one fused reduction (|x|^2 below
+// the diagonal and x . a_c for the later panel columns: v . a_c = a_jj,c + scale x . a_c),
+// warp shuffles then, for NT > 1, a fixed-order sum of the warps' partials through
+// shared memory (named barrier 1, double-buffered slots), and the LAPACK reflector
+// (v_0 = 1, beta = -sign(alpha)|x|, tau = (beta - alpha)/beta).  Afterwards warp 0
+// forms G = V^T V on the DMMA pipe and the compact-WY factor T (8 x 8 upper,
+// H_1..H_nb = I - V T V^T, dlarft's forward recurrence, one row per lane) into T and,
+// if Tg != nullptr, Tg.  Columns >= nb and rows >= mr are zero padding: every step runs
+// unconditionally (tau = 0 there).  xch: 2 x (NT + 1) x 8 doubles; scratch: 64 doubles.
+__device__ __forceinline__ void hh_team_sync(int nt) {
+  if (nt > 1) asm volatile("bar.sync 1, %0;\n" ::"r"(nt * 32) : "memory");
+  else __syncwarp();
+}
+
+__device__ void hh_panel_team(double* A, int ld, int mr, int p, int nb, double* tau, double* T, double* Tg, int NT,
+                              double* xch, double* scratch) {
+  constexpr int RW = 2;
+  const int lane = threadIdx.x & 31;
+  const int wt = __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0);
+  double a[RW][kHhNB];
+#pragma unroll
+  for (int i = 0; i < RW; ++i)
+#pragma unroll
+    for (int c = 0; c < kHhNB; ++c) {
+      const int r = p + lane + 32 * (wt + NT * i);
+      a[i][c] = (r < mr && c < nb) ? A[r * ld + p + c] : 0.0;
+    }
+  double taus[kHhNB];
+#pragma unroll
+  for (int jj = 0; jj < kHhNB; ++jj) {
+    double red[kHhNB];
+#pragma unroll
+    for (int c = jj; c < kHhNB; ++c) red[c] = 0.0;
+#pragma unroll
+    for (int i = 0; i < RW; ++i)
+      if (lane + 32 * (wt + NT * i) > jj) {
+#pragma unroll
+        for (int c = jj; c < kHhNB; ++c) red[c] = fma(a[i][jj], a[i][c], red[c]);
+      }
+    double top[kHhNB];
+#pragma unroll
+    for (int c = jj; c < kHhNB; ++c) top[c] = __shfl_sync(0xffffffffu, a[0][c], jj);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int c = jj; c < kHhNB; ++c) red[c] += __shfl_xor_sync(0xffffffffu, red[c], o);
+    if (NT > 1) {
+      double* slot = xch + (jj & 1) * (NT + 1) * kHhNB;
+      if (lane == 0) {
+#pragma unroll
+        for (int c = jj; c < kHhNB; ++c) slot[wt * kHhNB + c] = red[c];
+      }
+      if (wt == 0 && lane == 0) {
+#pragma unroll
+        for (int c = jj; c < kHhNB; ++c) slot[NT * kHhNB + c] = top[c];
+      }
+      hh_team_sync(NT);
+#pragma unroll
+      for (int c = jj; c < kHhNB; ++c) {
+        double v = 0.0;
+        for (int w = 0; w < NT; ++w) v += slot[w * kHhNB + c];
+        red[c] = v;
+        top[c] = slot[NT * kHhNB + c];
+      }
+    }
+    const double s = red[jj], alpha = top[jj];
+    double t = 0.0, scale = 0.0, beta = alpha;
+    if (s > 0.0) {
+      const double nrm = sqrt(alpha * alpha + s);
+      beta = alpha >= 0.0 ? -nrm : nrm;
+      t = (beta - alpha) / beta;
+      scale = 1.0 / (alpha - beta);
+    }
+    const bool diag = (wt == 0 && lane == jj);
+#pragma unroll
+    for (int i = 0; i < RW; ++i)
+      if (lane + 32 * (wt + NT * i) > jj) a[i][jj] *= scale;
+    if (diag) a[0][jj] = beta;
+    taus[jj] = t;
+#pragma unroll
+    for (int c = jj + 1; c < kHhNB; ++c) {
+      const double w = t * fma(scale, red[c], top[c]);
+      if (diag) a[0][c] -= w;
+#pragma unroll
+      for (int i = 0; i < RW; ++i)
+        if (lane + 32 * (wt + NT * i) > jj) a[i][c] = fma(-w, a[i][jj], a[i][c]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < RW; ++i)
+#pragma unroll
+    for (int c = 0; c < kHhNB; ++c) {
+      const int r = p + lane + 32 * (wt + NT * i);
+      if (r < mr && c < nb) A[r * ld + p + c] = a[i][c];
+    }
+  if (wt == 0) {
+#pragma unroll
+    for (int jj = 0; jj < kHhNB; ++jj)
+      if (lane == jj && jj < nb) tau[p + jj] = taus[jj];
+  }
+  hh_team_sync(NT);
+  if (wt != 0) return;
+  // G = V^T V on the DMMA pipe (two accumulation chains), via scratch to every lane
+  {
+    const int fr = lane >> 2, fk = lane & 3;
+    const double* V = A + p;
+    double g0 = 0.0, g1 = 0.0, h0 = 0.0, h1 = 0.0;
+    for (int r0 = p; r0 < mr; r0 += 8) {
+      const int r = r0 + fk, r2 = r0 + 4 + fk;
+      trals::dmma884(g0, g1, hh_v(V, ld, p, nb, mr, r, fr), hh_v(V, ld, p, nb, mr, r, fr));
+      trals::dmma884(h0, h1, hh_v(V, ld, p, nb, mr, r2, fr), hh_v(V, ld, p, nb, mr, r2, fr));
+    }
+    scratch[fr * 8 + 2 * fk] = g0 + h0;
+    scratch[fr * 8 + 2 * fk + 1] = g1 + h1;
+    __syncwarp();
+  }
+  // T row by row in parallel: lane i < 8 owns row i, T[i][jj] = -tau_jj sum_{i<=l<jj} T[i][l] G[l][jj]
+  double trow[kHhNB];
+#pragma unroll
+  for (int jj = 0; jj < kHhNB; ++jj) {
+    double acc = 0.0;
+#pragma unroll
+    for (int l = 0; l < jj; ++l) acc = (l >= lane) ? fma(trow[l], scratch[l * 8 + jj], acc) : acc;
+    trow[jj] = (jj < lane) ? 0.0 : (jj == lane ? taus[jj] : -taus[jj] * acc);
+  }
+  __syncwarp();
+  if (lane < kHhNB) {
+#pragma unroll
+    for (int jj = 0; jj < kHhNB; ++jj) {
+      T[lane * kHhNB + jj] = trow[jj];
+      if (Tg) Tg[lane * kHhNB + jj] = trow[jj];
+    }
+  }
+  __syncwarp();
+}
+
+// Blocked in-place Householder QR of A (mr x nc, pitch ld, mr <= kHhPanelRows) in shared
 // memory: reflector j in A[j+1.., j], tau[j], R in the upper triangle; the T factor of
-// panel b goes to Tg + 64 b when Tg != nullptr.  Look-ahead: warp 0 applies panel b
-// to the columns of panel b+1 and factors panel b+1 while the other warps apply panel
-// b to everything right of it -- one barrier per 8 reflectors.
-template <int RPL>
+// panel b goes to Tg + 64 b when Tg != nullptr.  A team of NT = ceil(mr / 64) warps
+// factors the panels; look-ahead: team warp 0 applies panel b to the columns of panel
+// b+1, the team factors panel b+1, while the other warps apply panel b to everything
+// right of it -- one CTA barrier per 8 reflectors.  xch: 2 x 5 x 8 doubles, scratch:
+// 64 doubles per warp.
 __device__ void hh_factor_blocked(double* A, int ld, int mr, int nc, double* tau, double* Tbuf, double* Tg,
-                                  double* scratch) {
+                                  double* scratch, double* xch) {
   const int warp = __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0);
   const int nwarps = blockDim.x >> 5;
+  const int NT = (mr + 63) / 64;
   const int k = min(mr, nc);
-  if (warp == 0) hh_panel_warp<RPL>(A, ld, mr, 0, min(kHhNB, k), tau, Tbuf, Tg);
+  if (warp < NT) hh_panel_team(A, ld, mr, 0, min(kHhNB, k), tau, Tbuf, Tg, NT, xch, scratch);
   __syncthreads();
   int it = 0;
   for (int p = 0; p < k; p += kHhNB, ++it) {
@@ -1763,14 +1792,15 @@ __device__ void hh_factor_blocked(double* A, int ld, int mr, int nc, double* tau
     const int nbx = min(kHhNB, k - nx);
     const double* T = Tbuf + (it & 1) * 64;
     double* Tn = Tbuf + ((it + 1) & 1) * 64;
-    if (warp == 0) {
+    if (warp < NT) {
       if (nbx > 0) {
-        hh_panel_apply(A + p, ld, T, nb, A, ld, mr, p, nx, nx + nbx, 0, 1, scratch);
-        __syncwarp();
-        hh_panel_warp<RPL>(A, ld, mr, nx, nbx, tau, Tn, Tg ? Tg + static_cast<int64_t>(it + 1) * 64 : nullptr);
+        if (warp == 0) hh_panel_apply(A + p, ld, T, nb, A, ld, mr, p, nx, nx + nbx, 0, 1, scratch);
+        hh_team_sync(NT);
+        hh_panel_team(A, ld, mr, nx, nbx, tau, Tn, Tg ? Tg + static_cast<int64_t>(it + 1) * 64 : nullptr, NT, xch,
+                      scratch);
       }
     } else {
-      hh_panel_apply(A + p, ld, T, nb, A, ld, mr, p, nbx > 0 ? nx + nbx : nx, nc, warp - 1, nwarps - 1,
+      hh_panel_apply(A + p, ld, T, nb, A, ld, mr, p, nbx > 0 ? nx + nbx : nx, nc, warp - NT, nwarps - NT,
                      scratch + 64 * warp);
     }
     __syncthreads();
@@ -1779,13 +1809,9 @@ __device__ void hh_factor_blocked(double* A, int ld, int mr, int nc, double* tau
 
 // In-place QR of the smem matrix: blocked for mr <= kHhPanelRows, else unblocked.
 // Tbuf: 128 doubles; Tg: optional per-panel T output (blocked path only).
-// scratch: 64 doubles per warp.
 __device__ void hh_factor_smem(double* A, int ld, int mr, int nc, double* tau, double* red, double* Tbuf,
-                               double* Tg, double* scratch) {
-  if (mr <= 32) hh_factor_blocked<1>(A, ld, mr, nc, tau, Tbuf, Tg, scratch);
-  else if (mr <= 64) hh_factor_blocked<2>(A, ld, mr, nc, tau, Tbuf, Tg, scratch);
-  else if (mr <= 128) hh_factor_blocked<4>(A, ld, mr, nc, tau, Tbuf, Tg, scratch);
-  else if (mr <= kHhPanelRows) hh_factor_blocked<7>(A, ld, mr, nc, tau, Tbuf, Tg, scratch);
+                               double* Tg, double* scratch, double* xch) {
+  if (mr <= kHhPanelRows) hh_factor_blocked(A, ld, mr, nc, tau, Tbuf, Tg, scratch, xch);
   else hh_factor_unblocked(A, ld, mr, nc, tau, red);
 }
 
@@ -1822,6 +1848,7 @@ __global__ void __launch_bounds__(kHhThreads, 1) hh_block_kernel(const double* _
   __shared__ double tau[512];
   __shared__ double Tbuf[128];
   __shared__ double scratch[64 * (kHhThreads / 32)];
+  __shared__ double xch[2 * 5 * kHhNB];
   const int ld = nc + 1;
   const int b = blockIdx.x;
   int m_all;
@@ -1843,7 +1870,7 @@ __global__ void __launch_bounds__(kHhThreads, 1) hh_block_kernel(const double* _
     }
   }
   __syncthreads();
-  hh_factor_smem(A, ld, m_all, nc, tau, red, Tbuf, nullptr, scratch);
+  hh_factor_smem(A, ld, m_all, nc, tau, red, Tbuf, nullptr, scratch, xch);
   // intermediate TSQR factors are zero-padded to nc rows so they stack uniformly
   const int rows_out = sign ? min(m_all, nc) : nc;
   hh_store_r(A, ld, m_all, nc, R + static_cast<int64_t>(b) * rstride, sign != 0, rows_out);
@@ -1859,13 +1886,14 @@ __global__ void __launch_bounds__(kHhThreads, 1) hh_left_kernel(const double* __
   __shared__ double tau[512];
   __shared__ double Tbuf[128];
   __shared__ double scratch[64 * (kHhThreads / 32)];
+  __shared__ double xch[2 * 5 * kHhNB];
   const int ld = I + 1;
   for (int t = threadIdx.x; t < I * I; t += blockDim.x) {
     const int r = t / I, c = t - r * I;
     A[r * ld + c] = G[static_cast<int64_t>(r) * nc + c];
   }
   __syncthreads();
-  hh_factor_smem(A, ld, I, I, tau, red, Tbuf, Tg, scratch);
+  hh_factor_smem(A, ld, I, I, tau, red, Tbuf, Tg, scratch, xch);
   __syncthreads();
   for (int t = threadIdx.x; t < I * I; t += blockDim.x) {
     const int r = t / I, c = t - r * I;

@@ -5,21 +5,19 @@
 
 __global__ void panel_probe(const double* G, int mr, int nc, long long* out) {
   extern __shared__ __align__(16) double A[];
-  __shared__ double tau[512], red[32], Tbuf[128], scratch[64 * 8];
+  __shared__ double tau[512], red[32], Tbuf[128], scratch[64 * 8], xch[80];
   const int ld = nc + 1;
   for (int t = threadIdx.x; t < mr * nc; t += blockDim.x) A[(t / nc) * ld + t % nc] = G[t];
   __syncthreads();
   long long t0 = clock64();
-  if (threadIdx.x < 32) {
-    if (mr <= 64) hh_panel_warp<2>(A, ld, mr, 0, 8, tau, Tbuf, nullptr);
-    else hh_panel_warp<7>(A, ld, mr, 0, 8, tau, Tbuf, nullptr);
-  }
+  const int nt = (mr + 63) / 64;
+  if (static_cast<int>(threadIdx.x) < 32 * nt) hh_panel_team(A, ld, mr, 0, 8, tau, Tbuf, nullptr, nt, xch, scratch);
   __syncthreads();
   long long t1 = clock64();
   for (int t = threadIdx.x; t < mr * nc; t += blockDim.x) A[(t / nc) * ld + t % nc] = G[t];
   __syncthreads();
   long long t2 = clock64();
-  hh_factor_smem(A, ld, mr, nc, tau, red, Tbuf, nullptr, scratch);
+  hh_factor_smem(A, ld, mr, nc, tau, red, Tbuf, nullptr, scratch, xch);
   __syncthreads();
   long long t3 = clock64();
   if (threadIdx.x == 0) { out[0] = t1 - t0; out[1] = t3 - t2; }
