@@ -33,3 +33,26 @@ def test_budget_guard():
     with pytest.raises(ElementBudgetError):
         check_element_budget((1024, 1024, 1024))
     assert check_element_budget((1024, 1024, 1024), budget=1 << 30) == 1 << 30
+
+
+def test_fp64_gemm_option_validated():
+    x = np.ones((3, 3, 3))
+    with pytest.raises(ValueError, match="unknown fp64_gemm"):
+        tr_als_ne(x, AlsConfig(ranks=(1, 1, 1), fp64_gemm="tf32"))
+
+
+@pytest.mark.parametrize("dims,ranks,want", [((30, 40, 50), (3, 4, 5), "dmma"),      # 2|X|R^2 = 1.5 MFLOP
+                                             ((64, 64, 64, 64), (8,) * 4, "dmma"),   # BASELINE c2: 2.1 GFLOP
+                                             ((2000, 1100), (32, 32), "ozaki")])     # 4.5 GFLOP
+def test_fp64_gemm_auto_policy(dims, ranks, want):
+    """fp64_gemm="auto" puts environment products of >= 4 GFLOP (2 |X| R_max^2) on the int8
+    tensor cores and leaves the small, launch-bound ones on DMMA; explicit choices stick."""
+    import torch
+    from fake_trals import FakeTrals
+    from paper_2210_11362_b200.engine import OZ64_MIN_FLOPS, SweepEngine
+    x = torch.zeros(dims, dtype=torch.float64)
+    assert (2.0 * x.numel() * max(ranks) ** 2 >= OZ64_MIN_FLOPS) == (want == "ozaki")
+    assert SweepEngine(x, dims, ranks, "ne", _test_lib=FakeTrals()).fp64_gemm == want
+    assert SweepEngine(x, dims, ranks, "ne", fp64_gemm="dmma", _test_lib=FakeTrals()).fp64_gemm == "dmma"
+    with pytest.raises(ValueError, match="unknown fp64_gemm"):
+        SweepEngine(x, dims, ranks, "ne", fp64_gemm="fast", _test_lib=FakeTrals())
