@@ -149,6 +149,12 @@ struct OzArgs {
   int mtiles, ntiles;  // tile t -> (split, m-tile, n-tile), n fastest
   OzRowTiles nt;       // widths of the n-tiles (<= BN)
   int rotate;          // rotate the k-block order by the m-tile index
+  // two-way split-K fix-up (chunked epilogue): the first of a tile's two K halves to finish
+  // leaves its partial in ws ([M][N]) and raises ready[tile]; the second adds it to its own
+  // and stores the result (fp addition commutes: the sum is the same whichever is first)
+  int fixup;
+  int* tickets;        // [mtiles * ntiles], zero at launch
+  int* ready;          // [mtiles * ntiles], zero at launch
   int64_t kblocks;     // 64-k blocks of the tiled digit layout (ceil(K / 64))
   const int8_t* ad;    // A digits, tiled: [mtiles][kblocks][D][128 x 64 B]
   const int8_t* bd;    // B digits, tiled: [n-tile][kblocks][D][width x 64 B]
@@ -435,12 +441,29 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
       const int r = quad * 32 + lane;
       const int64_t m = m0 + r;
       const double sa = (m < g.M && ktiles > 0) ? ldexp(1.0, g.ea[m] - SC::OFF) : 0.0;
-      const bool part = g.splits > 1;
+      bool part = g.splits > 1;
+      bool second = false;  // fix-up: this CTA finishes the tile (adds the other half's partial)
+      const int tile = mt * g.ntiles + nt;
+      if (T::CHUNKED && g.fixup) {
+        __shared__ int ticket_s;
+        if (quad == 0 && lane == 0) {
+          const int tk = atomicAdd(g.tickets + tile, 1);
+          if (tk == 1) {
+            while (atomicAdd(g.ready + tile, 0) == 0) __nanosleep(200);
+            __threadfence();
+          }
+          ticket_s = tk;
+        }
+        asm volatile("bar.sync 1, 128;\n" ::: "memory");
+        second = ticket_s == 1;
+        part = !second;
+      }
+      const bool fix = T::CHUNKED && g.fixup;
       const uint32_t M2 = part ? (1u << 30) : static_cast<uint32_t>(g.cmap.M2);
       const uint32_t N2 = part ? (1u << 30) : static_cast<uint32_t>(g.cmap.N2);
       const int64_t sm1 = part ? 0 : g.cmap.sm1, sm2 = part ? g.N : g.cmap.sm2;
       const int64_t sn1 = part ? 0 : g.cmap.sn1, sn2 = part ? 1 : g.cmap.sn2;
-      double* base = part ? g.ws + static_cast<int64_t>(split) * g.M * g.N : g.C;
+      double* base = part ? g.ws + (fix ? 0 : static_cast<int64_t>(split) * g.M * g.N) : g.C;
       const int rows = static_cast<int>((g.M - m0) < kOzBM ? (g.M - m0) : kOzBM);
 #pragma unroll 1
       for (int c0 = 0; c0 < bw; c0 += 16) {
@@ -464,13 +487,29 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
           const uint32_t un = static_cast<uint32_t>(n);
           const int64_t coff = nok ? static_cast<int64_t>(un / N2) * sn1 + static_cast<int64_t>(un % N2) * sn2 : 0;
           const double sb = nok ? ldexp(1.0, g.eb[n]) : 0.0;
-          for (int rr = quad * 2 + (lane >> 4); rr < rows; rr += 8) {
+          // the other K half's partial for this chunk: all 16 loads issued before any use
+          double pv[kOzBM / 8];
+#pragma unroll
+          for (int k = 0; k < kOzBM / 8; ++k) {
+            const int rr = quad * 2 + (lane >> 4) + 8 * k;
+            pv[k] = (second && nok && rr < rows) ? __ldcg(g.ws + static_cast<int64_t>(m0 + rr) * g.N + n) : 0.0;
+          }
+#pragma unroll
+          for (int k = 0; k < kOzBM / 8; ++k) {
+            const int rr = quad * 2 + (lane >> 4) + 8 * k;
+            if (rr >= rows) break;
             const uint32_t mm = static_cast<uint32_t>(m0 + rr);
             const int64_t roff = static_cast<int64_t>(mm / M2) * sm1 + static_cast<int64_t>(mm % M2) * sm2;
-            if (nok) base[roff + coff] = otile[rr * T::OUT_LD + (lane & 15)] * sb;
+            const double o = otile[rr * T::OUT_LD + (lane & 15)] * sb + pv[k];
+            if (nok) base[roff + coff] = o;
           }
           asm volatile("bar.sync 1, 128;\n" ::: "memory");
         }
+      }
+      if (T::CHUNKED && g.fixup && part) {  // publish this half's partial
+        __threadfence();
+        asm volatile("bar.sync 1, 128;\n" ::: "memory");
+        if (quad == 0 && lane == 0) atomicExch(g.ready + tile, 1);
       }
       tmem_zero<LV * BN>(tlane);
       asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");

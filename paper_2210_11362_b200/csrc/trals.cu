@@ -522,8 +522,14 @@ SplitPlan plan_split_oz(int64_t M, int64_t K, int64_t N) {
 
 // workspace (doubles): B digit planes (D x N x ldk bytes), eb (N int32), B column max (N), partials
 struct OzWs {
-  int64_t planes, eb, mx, part, total;
+  int64_t planes, eb, mx, flags, part, total;
 };
+// in-kernel two-way split-K fix-up (no reduce launch) for the chunked-epilogue scheme
+template <class SC>
+bool oz_fixup(const SplitPlan& sp) {
+  return sp.splits == 2 && trals::OzTile<kOzBN, SC>::CHUNKED;
+}
+
 template <class SC>
 OzWs oz_ws_layout(int64_t M, int64_t K, int64_t N) {
   const SplitPlan sp = plan_split_oz<SC>(M, K, N);
@@ -531,8 +537,10 @@ OzWs oz_ws_layout(int64_t M, int64_t K, int64_t N) {
   w.planes = 0;
   w.eb = w.planes + (oz_digits_bytes(oz_b_tiles(N), K, SC::D) + 15) / 16 * 2;
   w.mx = w.eb + (N + 3) / 4 * 2;
-  w.part = w.mx + (N + 1) / 2 * 2;
-  w.total = w.part + (sp.splits > 1 ? static_cast<int64_t>(sp.splits) * M * N : 0);
+  w.flags = w.mx + (N + 1) / 2 * 2;
+  const int64_t tiles = ((M + trals::kOzBM - 1) / trals::kOzBM) * oz_b_tiles(N).ntiles;
+  w.part = w.flags + (oz_fixup<SC>(sp) ? (2 * tiles + 1) / 2 + 1 : 0);
+  w.total = w.part + (sp.splits > 1 ? (oz_fixup<SC>(sp) ? 1 : static_cast<int64_t>(sp.splits)) * M * N : 0);
   return w;
 }
 
@@ -579,6 +587,13 @@ int gemm_oz(const int8_t* ad, const int32_t* ea, int64_t M, int64_t K, int64_t N
   static int norot = -1;  // TRALS_OZ_NOROT=1 (experiments): k blocks in natural order
   if (norot < 0) norot = std::getenv("TRALS_OZ_NOROT") ? 1 : 0;
   g.rotate = norot ? 0 : 1;
+  g.fixup = oz_fixup<SC>(sp) ? 1 : 0;
+  if (g.fixup) {
+    const int64_t tiles = static_cast<int64_t>(g.mtiles) * g.ntiles;
+    g.tickets = reinterpret_cast<int*>(ws + w.flags);
+    g.ready = g.tickets + tiles;
+    if (cudaMemsetAsync(g.tickets, 0, 2 * tiles * sizeof(int), s) != cudaSuccess) return TRALS_ERR_CUDA;
+  }
   g.kblocks = (K + trals::kOzBK - 1) / trals::kOzBK;
   g.ad = ad; g.bd = bd;
   g.cmap = cm; g.ea = ea; g.eb = eb; g.C = C; g.ws = ws + w.part;
@@ -594,7 +609,7 @@ int gemm_oz(const int8_t* ad, const int32_t* ea, int64_t M, int64_t K, int64_t N
   const int grid = static_cast<int>(std::min<int64_t>(tiles, kSMs));
   kern<<<grid, T::THREADS, T::SMEM, s>>>(g);
   if (int st = launch_status()) return st;
-  if (sp.splits > 1) {
+  if (sp.splits > 1 && !g.fixup) {
     GemmArgs r{};
     r.P = 1; r.M = M; r.N = N; r.splits = sp.splits; r.ws = ws + w.part; r.C = C; r.cmap = cm; r.alpha = 1.0;
     r.beta = 0;
