@@ -124,7 +124,11 @@ struct OzRowTiles {
     const int64_t nb = static_cast<int64_t>(nbig) * wbig;
     if (r < nb) {
       t = static_cast<int>(r / wbig);
-      rr = static_cast<int>(r % wbig);
+      rr = static_cast<int>(r - static_cast<int64_t>(t) * wbig);
+    } else if (r - nb < 0x7fffffff) {  // 32-bit division (the common case)
+      const uint32_t q = static_cast<uint32_t>(r - nb);
+      t = nbig + static_cast<int>(q / static_cast<uint32_t>(wsmall));
+      rr = static_cast<int>(q % static_cast<uint32_t>(wsmall));
     } else {
       t = nbig + static_cast<int>((r - nb) / wsmall);
       rr = static_cast<int>((r - nb) % wsmall);
@@ -659,13 +663,66 @@ __global__ void __launch_bounds__(256) oz_digits_tiled_kernel(const Tin* __restr
           w[d][j >> 2] |= static_cast<uint32_t>(static_cast<uint8_t>(dg[d])) << (8 * (j & 3));
       }
     }
+    // plane d of a row sits width x 64 bytes after plane d - 1
+    int tt, rr_;
+    rt.locate(orow, tt, rr_);
+    const int64_t pstride = static_cast<int64_t>(rt.width(tt)) * 64;
+    const int64_t off0 = oz_tiled_offset(orow, ch * 16, 0, rt, kblocks, D);
 #pragma unroll
-    for (int d = 0; d < D; ++d) {
-      const int64_t off = oz_tiled_offset(orow, ch * 16, d, rt, kblocks, D);
-      *reinterpret_cast<uint4*>(out + off) = make_uint4(w[d][0], w[d][1], w[d][2], w[d][3]);
-    }
+    for (int d = 0; d < D; ++d)
+      *reinterpret_cast<uint4*>(out + off0 + d * pstride) = make_uint4(w[d][0], w[d][1], w[d][2], w[d][3]);
     if (rok && ch == 0) exps[orow] = e;
   }
+}
+
+// Transposed slicing (out rows = columns of x, K = rows of x): a CTA owns a 64 k x 64 n
+// block, reads it coalesced along n into shared memory, and each group of 4 threads
+// writes one output row's full 64-byte digit row per plane (4 x 16 B, contiguous), so
+// the tiled digit layout is written in whole sectors.  256 threads; grid (ceil(rows/64)
+// k blocks, ceil(padded out rows / 64)) covers the layout's padding too (zero digits there).
+template <typename Tin, class SC>
+__global__ void __launch_bounds__(256) oz_digits_tiled_t_kernel(const Tin* __restrict__ x, int64_t rows, int64_t cols,
+                                                                int64_t ld_in, const double* __restrict__ mx,
+                                                                int8_t* __restrict__ out, OzRowTiles rt,
+                                                                int32_t* __restrict__ exps) {
+  constexpr int D = SC::D;
+  __shared__ double tile[64][65];
+  const int64_t K = rows, out_rows = cols;
+  const int64_t kblocks = (K + 63) / 64;
+  const int64_t n0 = static_cast<int64_t>(blockIdx.y) * 64, k0 = static_cast<int64_t>(blockIdx.x) * 64;
+  const int tid = threadIdx.x;
+  for (int e = tid; e < 64 * 64; e += 256) {
+    const int kk = e >> 6, nn = e & 63;
+    const int64_t k = k0 + kk, n = n0 + nn;
+    tile[kk][nn] = (k < K && n < out_rows) ? static_cast<double>(x[k * ld_in + n]) : 0.0;
+  }
+  __syncthreads();
+  const int nl = tid >> 2, ch = tid & 3;
+  const int64_t orow = n0 + nl;
+  if (orow >= rt.rows_pad()) return;
+  const bool rok = orow < out_rows;
+  const int e = rok ? oz_exponent(mx[orow]) : 0;
+  const double sc = ldexp(1.0, -e);
+  uint32_t w[D][4];
+#pragma unroll
+  for (int d = 0; d < D; ++d)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) w[d][q] = 0;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    int8_t dg[D];
+    oz_digits<SC>(tile[ch * 16 + j][nl] * sc, dg);
+#pragma unroll
+    for (int d = 0; d < D; ++d) w[d][j >> 2] |= static_cast<uint32_t>(static_cast<uint8_t>(dg[d])) << (8 * (j & 3));
+  }
+  int tt, rr_;
+  rt.locate(orow, tt, rr_);
+  const int64_t pstride = static_cast<int64_t>(rt.width(tt)) * 64;
+  const int64_t off0 = oz_tiled_offset(orow, k0 + ch * 16, 0, rt, kblocks, D);
+#pragma unroll
+  for (int d = 0; d < D; ++d)
+    *reinterpret_cast<uint4*>(out + off0 + d * pstride) = make_uint4(w[d][0], w[d][1], w[d][2], w[d][3]);
+  if (rok && blockIdx.x == 0 && ch == 0) exps[orow] = e;
 }
 
 }  // namespace trals

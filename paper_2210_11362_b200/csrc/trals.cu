@@ -574,9 +574,9 @@ int gemm_oz(const int8_t* ad, const int32_t* ea, int64_t M, int64_t K, int64_t N
   // B^T rows = columns of B: max over k, then tiled digits (transposed read)
   if (int st = launch_colmax<double>(B, K, N, ldb, bmx, s)) return st;
   {
-    const int64_t work = oz_digits_bytes(oz_b_tiles(N), K, SC::D) / (16 * SC::D);  // (padded row, 16-k chunk) items
-    const int blocks = static_cast<int>(std::min<int64_t>((work + 255) / 256, 16 * kSMs));
-    trals::oz_digits_tiled_kernel<double, SC><<<blocks, 256, 0, s>>>(B, K, N, ldb, 1, bmx, bd, oz_b_tiles(N), eb);
+    const trals::OzRowTiles bt = oz_b_tiles(N);
+    dim3 grid(static_cast<unsigned>((K + 63) / 64), static_cast<unsigned>((bt.rows_pad() + 63) / 64));
+    trals::oz_digits_tiled_t_kernel<double, SC><<<grid, 256, 0, s>>>(B, K, N, ldb, bmx, bd, bt, eb);
     if (int st = launch_status()) return st;
   }
   trals::OzArgs g{};
@@ -636,6 +636,14 @@ int oz_split(const Tin* x, int64_t rows, int64_t cols, int transpose, int8_t* di
     if (int st = launch_status()) return st;
   } else {
     if (int st = launch_colmax<Tin>(x, rows, cols, cols, ws, s)) return st;
+  }
+  if (transpose) {
+    const trals::OzRowTiles at = oz_a_tiles(out_rows);
+    const int64_t gy = (at.rows_pad() + 63) / 64;
+    if (gy > 65535 || (K + 63) / 64 > INT32_MAX) return TRALS_ERR_UNSUPPORTED;
+    dim3 grid(static_cast<unsigned>((K + 63) / 64), static_cast<unsigned>(gy));
+    trals::oz_digits_tiled_t_kernel<Tin, SC><<<grid, 256, 0, s>>>(x, rows, cols, cols, ws, digits, at, exps);
+    return launch_status();
   }
   const int64_t work = oz_digits_bytes(oz_a_tiles(out_rows), K, SC::D) / (16 * SC::D);  // (padded row, 16-k chunk)
   const int blocks = static_cast<int>(std::min<int64_t>((work + 255) / 256, 64 * kSMs));
