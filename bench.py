@@ -272,7 +272,7 @@ def run_ours(args):
     eng.set_cores(cores0)
     errs = torch.zeros((args.warmup + args.steps, 3), dtype=torch.float64, device=dev)
     stream = eng.stream
-    use_graph = (world == 1 and not args.eager and args.config != "c5")
+    use_graph = (world == 1 and not args.eager)
     if use_graph:
         eng.capture(with_error=True)
     for k in range(args.warmup):
