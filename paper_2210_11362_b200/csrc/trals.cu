@@ -1671,58 +1671,64 @@ __device__ __forceinline__ void hh_team_sync(int nt) {
   else __syncwarp();
 }
 
+template <int RW>
 __device__ void hh_panel_team(double* A, int ld, int mr, int p, int nb, double* tau, double* T, double* Tg, int NT,
                               double* xch, double* scratch) {
-  constexpr int RW = 2;
   const int lane = threadIdx.x & 31;
   const int wt = __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0);
+  // a[i][c] = panel column jj + c of this lane's rows: a window that rotates left as the
+  // columns are finished, so every register index is a compile-time constant while the
+  // column loop itself stays rolled (the fully unrolled form was ~300 KB of SASS per
+  // kernel: single-warp code then ran at the instruction-fetch rate)
   double a[RW][kHhNB];
+  int rel[RW];
 #pragma unroll
-  for (int i = 0; i < RW; ++i)
+  for (int i = 0; i < RW; ++i) {
+    rel[i] = lane + 32 * (wt + NT * i);
 #pragma unroll
     for (int c = 0; c < kHhNB; ++c) {
-      const int r = p + lane + 32 * (wt + NT * i);
+      const int r = p + rel[i];
       a[i][c] = (r < mr && c < nb) ? A[r * ld + p + c] : 0.0;
     }
-  double taus[kHhNB];
-#pragma unroll
+  }
+#pragma unroll 1
   for (int jj = 0; jj < kHhNB; ++jj) {
     double red[kHhNB];
 #pragma unroll
-    for (int c = jj; c < kHhNB; ++c) red[c] = 0.0;
+    for (int c = 0; c < kHhNB; ++c) red[c] = 0.0;
 #pragma unroll
     for (int i = 0; i < RW; ++i)
-      if (lane + 32 * (wt + NT * i) > jj) {
+      if (rel[i] > jj) {
 #pragma unroll
-        for (int c = jj; c < kHhNB; ++c) red[c] = fma(a[i][jj], a[i][c], red[c]);
+        for (int c = 0; c < kHhNB; ++c) red[c] = fma(a[i][0], a[i][c], red[c]);
       }
     double top[kHhNB];
 #pragma unroll
-    for (int c = jj; c < kHhNB; ++c) top[c] = __shfl_sync(0xffffffffu, a[0][c], jj);
+    for (int c = 0; c < kHhNB; ++c) top[c] = __shfl_sync(0xffffffffu, a[0][c], jj);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
-      for (int c = jj; c < kHhNB; ++c) red[c] += __shfl_xor_sync(0xffffffffu, red[c], o);
+      for (int c = 0; c < kHhNB; ++c) red[c] += __shfl_xor_sync(0xffffffffu, red[c], o);
     if (NT > 1) {
       double* slot = xch + (jj & 1) * (NT + 1) * kHhNB;
       if (lane == 0) {
 #pragma unroll
-        for (int c = jj; c < kHhNB; ++c) slot[wt * kHhNB + c] = red[c];
+        for (int c = 0; c < kHhNB; ++c) slot[wt * kHhNB + c] = red[c];
       }
       if (wt == 0 && lane == 0) {
 #pragma unroll
-        for (int c = jj; c < kHhNB; ++c) slot[NT * kHhNB + c] = top[c];
+        for (int c = 0; c < kHhNB; ++c) slot[NT * kHhNB + c] = top[c];
       }
       hh_team_sync(NT);
 #pragma unroll
-      for (int c = jj; c < kHhNB; ++c) {
+      for (int c = 0; c < kHhNB; ++c) {
         double v = 0.0;
         for (int w = 0; w < NT; ++w) v += slot[w * kHhNB + c];
         red[c] = v;
         top[c] = slot[NT * kHhNB + c];
       }
     }
-    const double s = red[jj], alpha = top[jj];
+    const double s = red[0], alpha = top[0];
     double t = 0.0, scale = 0.0, beta = alpha;
     if (s > 0.0) {
       const double nrm = sqrt(alpha * alpha + s);
@@ -1733,29 +1739,29 @@ __device__ void hh_panel_team(double* A, int ld, int mr, int p, int nb, double* 
     const bool diag = (wt == 0 && lane == jj);
 #pragma unroll
     for (int i = 0; i < RW; ++i)
-      if (lane + 32 * (wt + NT * i) > jj) a[i][jj] *= scale;
-    if (diag) a[0][jj] = beta;
-    taus[jj] = t;
+      if (rel[i] > jj) a[i][0] *= scale;
+    if (diag) a[0][0] = beta;
+    // column jj is final: store it (reflector below the diagonal, R entries above)
 #pragma unroll
-    for (int c = jj + 1; c < kHhNB; ++c) {
+    for (int i = 0; i < RW; ++i) {
+      const int r = p + rel[i];
+      if (r < mr && jj < nb) A[r * ld + p + jj] = a[i][0];
+    }
+    if (wt == 0 && lane == 0 && jj < nb) tau[p + jj] = t;
+#pragma unroll
+    for (int c = 1; c < kHhNB; ++c) {
       const double w = t * fma(scale, red[c], top[c]);
       if (diag) a[0][c] -= w;
 #pragma unroll
       for (int i = 0; i < RW; ++i)
-        if (lane + 32 * (wt + NT * i) > jj) a[i][c] = fma(-w, a[i][jj], a[i][c]);
+        if (rel[i] > jj) a[i][c] = fma(-w, a[i][0], a[i][c]);
     }
-  }
 #pragma unroll
-  for (int i = 0; i < RW; ++i)
+    for (int i = 0; i < RW; ++i) {
 #pragma unroll
-    for (int c = 0; c < kHhNB; ++c) {
-      const int r = p + lane + 32 * (wt + NT * i);
-      if (r < mr && c < nb) A[r * ld + p + c] = a[i][c];
+      for (int c = 0; c + 1 < kHhNB; ++c) a[i][c] = a[i][c + 1];
+      a[i][kHhNB - 1] = 0.0;
     }
-  if (wt == 0) {
-#pragma unroll
-    for (int jj = 0; jj < kHhNB; ++jj)
-      if (lane == jj && jj < nb) tau[p + jj] = taus[jj];
   }
   hh_team_sync(NT);
   if (wt != 0) return;
@@ -1777,10 +1783,11 @@ __device__ void hh_panel_team(double* A, int ld, int mr, int p, int nb, double* 
   double trow[kHhNB];
 #pragma unroll
   for (int jj = 0; jj < kHhNB; ++jj) {
+    const double tj = jj < nb ? tau[p + jj] : 0.0;
     double acc = 0.0;
 #pragma unroll
     for (int l = 0; l < jj; ++l) acc = (l >= lane) ? fma(trow[l], scratch[l * 8 + jj], acc) : acc;
-    trow[jj] = (jj < lane) ? 0.0 : (jj == lane ? taus[jj] : -taus[jj] * acc);
+    trow[jj] = (jj < lane) ? 0.0 : (jj == lane ? tj : -tj * acc);
   }
   __syncwarp();
   if (lane < kHhNB) {
@@ -1800,13 +1807,15 @@ __device__ void hh_panel_team(double* A, int ld, int mr, int p, int nb, double* 
 // b+1, the team factors panel b+1, while the other warps apply panel b to everything
 // right of it -- one CTA barrier per 8 reflectors.  xch: 2 x 5 x 8 doubles, scratch:
 // 64 doubles per warp.
+template <int RW>
 __device__ void hh_factor_blocked(double* A, int ld, int mr, int nc, double* tau, double* Tbuf, double* Tg,
                                   double* scratch, double* xch) {
   const int warp = __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0);
   const int nwarps = blockDim.x >> 5;
-  const int NT = (mr + 63) / 64;
+  constexpr int NT = 1;  // one warp, RW rows per lane (measured: a multi-warp team paid ~2000
+                         // cycles per column in the named-barrier exchange)
   const int k = min(mr, nc);
-  if (warp < NT) hh_panel_team(A, ld, mr, 0, min(kHhNB, k), tau, Tbuf, Tg, NT, xch, scratch);
+  if (warp < NT) hh_panel_team<RW>(A, ld, mr, 0, min(kHhNB, k), tau, Tbuf, Tg, NT, xch, scratch);
   __syncthreads();
   int it = 0;
   for (int p = 0; p < k; p += kHhNB, ++it) {
@@ -1819,7 +1828,7 @@ __device__ void hh_factor_blocked(double* A, int ld, int mr, int nc, double* tau
       if (nbx > 0) {
         if (warp == 0) hh_panel_apply(A + p, ld, T, nb, A, ld, mr, p, nx, nx + nbx, 0, 1, scratch);
         hh_team_sync(NT);
-        hh_panel_team(A, ld, mr, nx, nbx, tau, Tn, Tg ? Tg + static_cast<int64_t>(it + 1) * 64 : nullptr, NT, xch,
+        hh_panel_team<RW>(A, ld, mr, nx, nbx, tau, Tn, Tg ? Tg + static_cast<int64_t>(it + 1) * 64 : nullptr, NT, xch,
                       scratch);
       }
     } else {
@@ -1834,7 +1843,10 @@ __device__ void hh_factor_blocked(double* A, int ld, int mr, int nc, double* tau
 // Tbuf: 128 doubles; Tg: optional per-panel T output (blocked path only).
 __device__ void hh_factor_smem(double* A, int ld, int mr, int nc, double* tau, double* red, double* Tbuf,
                                double* Tg, double* scratch, double* xch) {
-  if (mr <= kHhPanelRows) hh_factor_blocked(A, ld, mr, nc, tau, Tbuf, Tg, scratch, xch);
+  if (mr <= 32) hh_factor_blocked<1>(A, ld, mr, nc, tau, Tbuf, Tg, scratch, xch);
+  else if (mr <= 64) hh_factor_blocked<2>(A, ld, mr, nc, tau, Tbuf, Tg, scratch, xch);
+  else if (mr <= 128) hh_factor_blocked<4>(A, ld, mr, nc, tau, Tbuf, Tg, scratch, xch);
+  else if (mr <= kHhPanelRows) hh_factor_blocked<8>(A, ld, mr, nc, tau, Tbuf, Tg, scratch, xch);
   else hh_factor_unblocked(A, ld, mr, nc, tau, red);
 }
 

@@ -10,8 +10,10 @@ __global__ void panel_probe(const double* G, int mr, int nc, long long* out) {
   for (int t = threadIdx.x; t < mr * nc; t += blockDim.x) A[(t / nc) * ld + t % nc] = G[t];
   __syncthreads();
   long long t0 = clock64();
-  const int nt = (mr + 63) / 64;
-  if (static_cast<int>(threadIdx.x) < 32 * nt) hh_panel_team(A, ld, mr, 0, 8, tau, Tbuf, nullptr, nt, xch, scratch);
+  if (threadIdx.x < 32) {
+    if (mr <= 64) hh_panel_team<2>(A, ld, mr, 0, 8, tau, Tbuf, nullptr, 1, xch, scratch);
+    else hh_panel_team<8>(A, ld, mr, 0, 8, tau, Tbuf, nullptr, 1, xch, scratch);
+  }
   __syncthreads();
   long long t1 = clock64();
   for (int t = threadIdx.x; t < mr * nc; t += blockDim.x) A[(t / nc) * ld + t % nc] = G[t];
