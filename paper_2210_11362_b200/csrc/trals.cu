@@ -1807,15 +1807,39 @@ __device__ void hh_panel_team(double* A, int ld, int mr, int p, int nb, double* 
 // b+1, the team factors panel b+1, while the other warps apply panel b to everything
 // right of it -- one CTA barrier per 8 reflectors.  xch: 2 x 5 x 8 doubles, scratch:
 // 64 doubles per warp.
+// Panel publication for the fused wide QR: after panel b is factored, its columns (rows
+// p.., reflectors below the diagonal, R above) go to Vg (row-major, pitch ldv), then
+// flags[b] is raised (release) for the CTAs applying the panels to the other columns.
+struct HhPub {
+  double* Vg;
+  int ldv;
+  int* flags;
+};
+
+__device__ __forceinline__ void hh_publish(const HhPub* pub, const double* A, int ld, int mr, int p, int nb, int b) {
+  if (!pub) return;
+  const int lane = threadIdx.x & 31;
+  for (int t = lane; t < (mr - p) * kHhNB; t += 32) {
+    const int r = p + t / kHhNB, c = t % kHhNB;
+    if (c < nb) pub->Vg[static_cast<int64_t>(r) * pub->ldv + p + c] = A[r * ld + p + c];
+  }
+  __threadfence();
+  __syncwarp();
+  if (lane == 0) atomicExch(pub->flags + b, 1);
+}
+
 template <int RW>
 __device__ void hh_factor_blocked(double* A, int ld, int mr, int nc, double* tau, double* Tbuf, double* Tg,
-                                  double* scratch, double* xch) {
+                                  double* scratch, double* xch, const HhPub* pub) {
   const int warp = __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0);
   const int nwarps = blockDim.x >> 5;
   constexpr int NT = 1;  // one warp, RW rows per lane (measured: a multi-warp team paid ~2000
                          // cycles per column in the named-barrier exchange)
   const int k = min(mr, nc);
-  if (warp < NT) hh_panel_team<RW>(A, ld, mr, 0, min(kHhNB, k), tau, Tbuf, Tg, NT, xch, scratch);
+  if (warp < NT) {
+    hh_panel_team<RW>(A, ld, mr, 0, min(kHhNB, k), tau, Tbuf, Tg, NT, xch, scratch);
+    if (warp == 0) hh_publish(pub, A, ld, mr, 0, min(kHhNB, k), 0);
+  }
   __syncthreads();
   int it = 0;
   for (int p = 0; p < k; p += kHhNB, ++it) {
@@ -1829,7 +1853,8 @@ __device__ void hh_factor_blocked(double* A, int ld, int mr, int nc, double* tau
         if (warp == 0) hh_panel_apply(A + p, ld, T, nb, A, ld, mr, p, nx, nx + nbx, 0, 1, scratch);
         hh_team_sync(NT);
         hh_panel_team<RW>(A, ld, mr, nx, nbx, tau, Tn, Tg ? Tg + static_cast<int64_t>(it + 1) * 64 : nullptr, NT, xch,
-                      scratch);
+                          scratch);
+        if (warp == 0) hh_publish(pub, A, ld, mr, nx, nbx, it + 1);
       }
     } else {
       hh_panel_apply(A + p, ld, T, nb, A, ld, mr, p, nbx > 0 ? nx + nbx : nx, nc, warp - NT, nwarps - NT,
@@ -1842,11 +1867,11 @@ __device__ void hh_factor_blocked(double* A, int ld, int mr, int nc, double* tau
 // In-place QR of the smem matrix: blocked for mr <= kHhPanelRows, else unblocked.
 // Tbuf: 128 doubles; Tg: optional per-panel T output (blocked path only).
 __device__ void hh_factor_smem(double* A, int ld, int mr, int nc, double* tau, double* red, double* Tbuf,
-                               double* Tg, double* scratch, double* xch) {
-  if (mr <= 32) hh_factor_blocked<1>(A, ld, mr, nc, tau, Tbuf, Tg, scratch, xch);
-  else if (mr <= 64) hh_factor_blocked<2>(A, ld, mr, nc, tau, Tbuf, Tg, scratch, xch);
-  else if (mr <= 128) hh_factor_blocked<4>(A, ld, mr, nc, tau, Tbuf, Tg, scratch, xch);
-  else if (mr <= kHhPanelRows) hh_factor_blocked<8>(A, ld, mr, nc, tau, Tbuf, Tg, scratch, xch);
+                               double* Tg, double* scratch, double* xch, const HhPub* pub = nullptr) {
+  if (mr <= 32) hh_factor_blocked<1>(A, ld, mr, nc, tau, Tbuf, Tg, scratch, xch, pub);
+  else if (mr <= 64) hh_factor_blocked<2>(A, ld, mr, nc, tau, Tbuf, Tg, scratch, xch, pub);
+  else if (mr <= 128) hh_factor_blocked<4>(A, ld, mr, nc, tau, Tbuf, Tg, scratch, xch, pub);
+  else if (mr <= kHhPanelRows) hh_factor_blocked<8>(A, ld, mr, nc, tau, Tbuf, Tg, scratch, xch, pub);
   else hh_factor_unblocked(A, ld, mr, nc, tau, red);
 }
 
@@ -1911,77 +1936,71 @@ __global__ void __launch_bounds__(kHhThreads, 1) hh_block_kernel(const double* _
   hh_store_r(A, ld, m_all, nc, R + static_cast<int64_t>(b) * rstride, sign != 0, rows_out);
 }
 
-// wide: factor the left I x I block (I <= kHhPanelRows, blocked); keep it row-major in
-// Vg (reflectors below the diagonal, R_left above) and the per-panel T factors in Tg
-__global__ void __launch_bounds__(kHhThreads, 1) hh_left_kernel(const double* __restrict__ G, int I, int nc,
+// Wide QR (I < nc) in one launch.  CTA 0 factors the left I x I block (blocked, I <=
+// kHhPanelRows) and publishes every panel (V columns to Vg, T to Tg, then flags[b]);
+// CTAs 1.. each own a chunk of cw of the remaining columns and apply the panels in
+// order as they appear (compact WY: W = V^T A, W' = T^T W, A -= V W' on DMMA), so the
+// application runs behind the factorisation instead of after it.  R gets the rows
+// sign-normalised by diag(R_left).  flags must be zero at launch.
+__global__ void __launch_bounds__(kHhThreads, 1) hh_wide_kernel(const double* __restrict__ G, int I, int nc,
                                                              double* __restrict__ R, double* __restrict__ Vg,
-                                                             double* __restrict__ Tg) {
+                                                             double* __restrict__ Tg, int* __restrict__ flags,
+                                                             int cw) {
   extern __shared__ __align__(16) double A[];
   __shared__ double red[32];
   __shared__ double tau[512];
   __shared__ double Tbuf[128];
   __shared__ double scratch[64 * (kHhThreads / 32)];
   __shared__ double xch[2 * 5 * kHhNB];
-  const int ld = I + 1;
-  for (int t = threadIdx.x; t < I * I; t += blockDim.x) {
-    const int r = t / I, c = t - r * I;
-    A[r * ld + c] = G[static_cast<int64_t>(r) * nc + c];
-  }
-  __syncthreads();
-  hh_factor_smem(A, ld, I, I, tau, red, Tbuf, Tg, scratch, xch);
-  __syncthreads();
-  for (int t = threadIdx.x; t < I * I; t += blockDim.x) {
-    const int r = t / I, c = t - r * I;
-    const double v = A[r * ld + c];
-    Vg[static_cast<int64_t>(r) * I + c] = v;
-    const double sgn = A[r * ld + r] < 0.0 ? -1.0 : 1.0;
-    R[static_cast<int64_t>(r) * nc + c] = c >= r ? sgn * v : 0.0;
-  }
-}
-
-// wide: R[:, c0:c0+w] = Q^T G[:, c0:c0+w] for a column chunk (one CTA), sign-normalised by
-// diag(R_left): the left block's panels applied in order (compact WY), each panel's
-// V (I x 8) and T staged in shared memory, the next one prefetched while the current
-// one is applied -- one barrier per 8 reflectors.
-__global__ void __launch_bounds__(kHhThreads, 1) hh_apply_kernel(const double* __restrict__ G, int I, int nc,
-                                                              const double* __restrict__ Vg,
-                                                              const double* __restrict__ Tg, int cw,
-                                                              double* __restrict__ R) {
-  extern __shared__ __align__(16) double A[];  // [I][cw + 1], then 2 x (V [I][8] + T [64])
-  __shared__ double scratch[64 * (kHhThreads / 32)];
   const int tid = threadIdx.x;
+  if (blockIdx.x == 0) {
+    const int ld = I + 1;
+    for (int t = tid; t < I * I; t += blockDim.x) {
+      const int r = t / I, c = t - r * I;
+      A[r * ld + c] = G[static_cast<int64_t>(r) * nc + c];
+    }
+    __syncthreads();
+    const HhPub pub{Vg, I, flags};
+    hh_factor_smem(A, ld, I, I, tau, red, Tbuf, Tg, scratch, xch, &pub);
+    __syncthreads();
+    for (int t = tid; t < I * I; t += blockDim.x) {
+      const int r = t / I, c = t - r * I;
+      const double v = A[r * ld + c];
+      const double sgn = A[r * ld + r] < 0.0 ? -1.0 : 1.0;
+      R[static_cast<int64_t>(r) * nc + c] = c >= r ? sgn * v : 0.0;
+    }
+    return;
+  }
   const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
-  const int c0 = I + blockIdx.x * cw;
+  const int c0 = I + (blockIdx.x - 1) * cw;
   const int w = min(cw, nc - c0);
   const int ld = cw + 1;
-  const int stage = I * kHhNB + 64;
-  double* buf = A + static_cast<int64_t>(I) * ld;
-  auto fetch = [&](int panel, double* dst) {
-    const int p = panel * kHhNB, nb = min(kHhNB, I - p);
-    for (int t = tid; t < (I - p) * kHhNB; t += blockDim.x) {
-      const int r = p + t / kHhNB, c = t % kHhNB;
-      dst[r * kHhNB + c] = c < nb ? Vg[static_cast<int64_t>(r) * I + p + c] : 0.0;
-    }
-    for (int t = tid; t < 64; t += blockDim.x) dst[I * kHhNB + t] = Tg[static_cast<int64_t>(panel) * 64 + t];
-  };
+  double* buf = A + static_cast<int64_t>(I) * ld;  // V [I][8] + T [64] of the current panel
   for (int t = tid; t < I * w; t += blockDim.x) {
     const int r = t / w, c = t - r * w;
     A[r * ld + c] = G[static_cast<int64_t>(r) * nc + c0 + c];
   }
   const int panels = (I + kHhNB - 1) / kHhNB;
-  fetch(0, buf);
-  __syncthreads();
   for (int b = 0; b < panels; ++b) {
-    double* cur = buf + (b & 1) * stage;
-    if (b + 1 < panels) fetch(b + 1, buf + ((b + 1) & 1) * stage);
-    const int p = b * kHhNB;
-    hh_panel_apply(cur, kHhNB, cur + I * kHhNB, min(kHhNB, I - p), A, ld, I, p, 0, w, warp, blockDim.x >> 5,
-                   scratch + 64 * warp);
+    if (tid == 0) {
+      volatile int* f = flags + b;
+      while (*f == 0) __nanosleep(100);
+      __threadfence();
+    }
+    __syncthreads();
+    const int p = b * kHhNB, nb = min(kHhNB, I - p);
+    for (int t = tid; t < (I - p) * kHhNB; t += blockDim.x) {
+      const int r = p + t / kHhNB, c = t % kHhNB;
+      buf[r * kHhNB + c] = c < nb ? __ldcg(Vg + static_cast<int64_t>(r) * I + p + c) : 0.0;
+    }
+    for (int t = tid; t < 64; t += blockDim.x) buf[I * kHhNB + t] = __ldcg(Tg + static_cast<int64_t>(b) * 64 + t);
+    __syncthreads();
+    hh_panel_apply(buf, kHhNB, buf + I * kHhNB, nb, A, ld, I, p, 0, w, warp, blockDim.x >> 5, scratch + 64 * warp);
     __syncthreads();
   }
   for (int t = tid; t < I * w; t += blockDim.x) {
     const int r = t / w, c = t - r * w;
-    const double sgn = Vg[static_cast<int64_t>(r) * I + r] < 0.0 ? -1.0 : 1.0;
+    const double sgn = __ldcg(Vg + static_cast<int64_t>(r) * I + r) < 0.0 ? -1.0 : 1.0;
     R[static_cast<int64_t>(r) * nc + c0 + c] = sgn * A[r * ld + c];
   }
 }
@@ -2012,13 +2031,13 @@ HhPlan hh_plan(int I, int nc) {
     return p;
   }
   p.kind = 2;
-  // column chunk: A [I][cw + 1] + two staged panels (V [I][8] + T [64])
-  int cw = static_cast<int>((kHhSmemMax / sizeof(double) - 2 * (static_cast<size_t>(I) * kHhNB + 64)) / I) - 1;
+  // column chunk: A [I][cw + 1] + the staged panel (V [I][8] + T [64])
+  int cw = static_cast<int>((kHhSmemMax / sizeof(double) - (static_cast<size_t>(I) * kHhNB + 64)) / I) - 1;
   // narrow chunks: an apply CTA's time is the per-panel latency chain, not its columns,
   // so more CTAs finish sooner (one 8-column group per warp)
   cw = std::max(8, std::min(cw, 8 * (kHhThreads / 32)));
   p.chunk = cw;
-  p.ws = static_cast<int64_t>(I) * I + 64 * ((I + kHhNB - 1) / kHhNB);
+  p.ws = static_cast<int64_t>(I) * I + 65 * ((I + kHhNB - 1) / kHhNB);  // Vg, T per panel, flags
   return p;
 }
 
@@ -2031,8 +2050,7 @@ int hh_qr(const double* G, int I, int nc, double* R, double* ws, int64_t ws_elem
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(hh_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kHhSmemMax);
-    cudaFuncSetAttribute(hh_left_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kHhSmemMax);
-    cudaFuncSetAttribute(hh_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kHhSmemMax);
+    cudaFuncSetAttribute(hh_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kHhSmemMax);
     attr = true;
   }
   if (!hh_supported(I, nc)) return TRALS_ERR_UNSUPPORTED;
@@ -2066,19 +2084,18 @@ int hh_qr(const double* G, int I, int nc, double* R, double* ws, int64_t ws_elem
     }
     return TRALS_OK;
   }
-  // wide
+  // wide: one launch, CTA 0 factors the left block, CTAs 1.. apply its panels as they appear
   double* Vg = ws;
   double* Tg = ws + static_cast<int64_t>(I) * I;
-  hh_left_kernel<<<1, kHhThreads, sizeof(double) * static_cast<size_t>(I) * (I + 1), s>>>(G, I, nc, R, Vg, Tg);
-  if (int st = launch_status()) return st;
+  const int panels = (I + kHhNB - 1) / kHhNB;
+  int* flags = reinterpret_cast<int*>(Tg + 64 * static_cast<int64_t>(panels));
+  if (cudaMemsetAsync(flags, 0, sizeof(int) * panels, s) != cudaSuccess) return TRALS_ERR_CUDA;
   const int rest = nc - I;
-  if (rest > 0) {
-    const int blocks = (rest + p.chunk - 1) / p.chunk;
-    const size_t smem = sizeof(double) * (static_cast<size_t>(I) * (p.chunk + 1) + 2 * (static_cast<size_t>(I) * kHhNB + 64));
-    hh_apply_kernel<<<blocks, kHhThreads, smem, s>>>(G, I, nc, Vg, Tg, p.chunk, R);
-    return launch_status();
-  }
-  return TRALS_OK;
+  const int blocks = 1 + (rest > 0 ? (rest + p.chunk - 1) / p.chunk : 0);
+  const size_t smem_left = sizeof(double) * static_cast<size_t>(I) * (I + 1);
+  const size_t smem_apply = sizeof(double) * (static_cast<size_t>(I) * (p.chunk + 1) + static_cast<size_t>(I) * kHhNB + 64);
+  hh_wide_kernel<<<blocks, kHhThreads, std::max(smem_left, smem_apply), s>>>(G, I, nc, R, Vg, Tg, flags, p.chunk);
+  return launch_status();
 }
 
 // C(m, n) = F[m * ncols + n] scattered through a CMap
