@@ -789,59 +789,67 @@ __device__ __forceinline__ void chol_reduce_flags(double amax, double asym, doub
 // [aug, aug + npad); padding rows/columns are 0.  scratch >= 256 doubles.
 // Returns the 1-based failing pivot (0 on success), uniform across the CTA.
 __device__ __forceinline__ int chol8_factor_block(const double* a, int ld, int p, int pb, double* Ud, double* Xd) {
-  // warp-level: lane i < pb holds row i of [D | I_8]
+  // Every lane factors the whole 8 x 8 block redundantly in registers (no shuffles, no
+  // shared-memory round trips on the pivot chain: the shuffle-broadcast form cost ~560
+  // cycles per pivot, tools/micro/chol_probe.cu), then inverts U in place; lane i writes
+  // row i of Ud = U and of Xd = U^{-T}.  Pivots beyond pb are identity padding; a
+  // non-positive (or NaN) pivot is reported 1-based.
   const int lane = threadIdx.x & 31;
-  double d[8], x[8];
+  double u[8][8];
 #pragma unroll
-  for (int c = 0; c < 8; ++c) {
-    double v = 0.0;
-    if (lane < pb && c < pb) v = c >= lane ? a[(p + lane) * ld + p + c] : a[(p + c) * ld + p + lane];
-    d[c] = v;
-    x[c] = (c == lane) ? 1.0 : 0.0;
-  }
-  // Every shuffle is executed unconditionally by the whole warp (shuffles under a
-  // branch the compiler cannot prove uniform compile to a slow collective path);
-  // pivots beyond pb or after a failure are masked arithmetically.
+  for (int r = 0; r < 8; ++r)
+#pragma unroll
+    for (int c = r; c < 8; ++c) {
+      double v = (r < pb && c < pb) ? a[(p + r) * ld + p + c] : 0.0;
+      if (r == c && r >= pb) v = 1.0;
+      u[r][c] = v;
+    }
   int bad = 0;
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
-    const double dk = __shfl_sync(0xffffffffu, d[k], k);
-    const bool live = (k < pb) && (bad == 0);
-    const bool ok = live && (dk > 0.0);
-    if (live && !ok) bad = k + 1;  // non-positive or NaN pivot (dpotrf failure)
-    const double sk = rsqrt(ok ? dk : 1.0);
-    if (ok && lane == k) {
+    const double dk = u[k][k];
+    const bool ok = bad == 0 && dk > 0.0;
+    if (bad == 0 && !ok) bad = k + 1;
+    const double rk = rsqrt(ok ? dk : 1.0);
+    u[k][k] = dk * rk;
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        d[c] = c >= k ? d[c] * sk : 0.0;
-        x[c] *= sk;
-      }
-    }
-    double u[8], xk[8];
+    for (int c = k + 1; c < 8; ++c) u[k][c] *= rk;
 #pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      u[c] = __shfl_sync(0xffffffffu, d[c], k);
-      xk[c] = __shfl_sync(0xffffffffu, x[c], k);
-    }
-    double uki = 0.0;
+    for (int i = k + 1; i < 8; ++i)
 #pragma unroll
-    for (int c = 0; c < 8; ++c) uki = (c == lane) ? u[c] : uki;
-    if (ok && lane > k && lane < pb) {
-#pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        if (c >= lane) d[c] = fma(-uki, u[c], d[c]);
-        x[c] = fma(-uki, xk[c], x[c]);
-      }
-    }
+      for (int c = i; c < 8; ++c) u[i][c] = fma(-u[k][i], u[k][c], u[i][c]);
   }
-  if (!bad && lane < 8) {
+  if (bad) return bad;
+  if (lane < 8) {
 #pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      Ud[lane * 8 + c] = (lane < pb && c < pb && c >= lane) ? d[c] : 0.0;
-      Xd[lane * 8 + c] = (lane < pb && c < pb && c <= lane) ? x[c] : 0.0;
-    }
+    for (int r = 0; r < 8; ++r)
+      if (r == lane) {
+#pragma unroll
+        for (int c = 0; c < 8; ++c) Ud[r * 8 + c] = (r < pb && c < pb && c >= r) ? u[r][c] : 0.0;
+      }
   }
-  return bad;
+  // in-place W = U^{-1} (upper), column by column, rows top-down
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const double wjj = 1.0 / u[j][j];
+#pragma unroll
+    for (int i = 0; i < j; ++i) {
+      double acc = 0.0;
+#pragma unroll
+      for (int l = i; l < j; ++l) acc = fma(u[i][l], u[l][j], acc);  // u[i][l] is W already (l < j)
+      u[i][j] = -wjj * acc;
+    }
+    u[j][j] = wjj;
+  }
+  if (lane < 8) {
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+      if (r == lane) {
+#pragma unroll
+        for (int c = 0; c < 8; ++c) Xd[r * 8 + c] = (r < pb && c < pb && c <= r) ? u[c][r] : 0.0;
+      }
+  }
+  return 0;
 }
 
 __device__ int chol8_aug_smem(double* a, int ld, int n, int aug, double* scratch /* >= 256 doubles */) {
