@@ -335,3 +335,21 @@ def test_env_oz64_accuracy(heavy):
     print(f"heavy={heavy}: dmma {e_dmma:.3e}  ozaki {e_oz:.3e}")
     assert e_dmma < 2e-15
     assert e_oz < max(2.0 * e_dmma, 1e-15)
+
+
+@pytest.mark.gpu
+def test_env_oz64_deterministic():
+    """Two launches of the split-K (fix-up) int8 environment product give bitwise-identical
+    results: the two K halves are added in whichever order they finish, and fp addition
+    commutes; the k-block rotation only reorders exact int32 sums."""
+    from paper_2210_11362_b200 import _lib as L
+    lib = L.lib()
+    rng = np.random.default_rng(5)
+    pre, post, r = 2560, 25600, 20
+    x64 = cuda(rng.standard_normal((pre, post)))
+    H = cuda(rng.standard_normal((post, r * r)))
+    s = int(torch.cuda.current_stream().cuda_stream)
+    a, _, _ = _oz64_env(lib, x64, pre, post, 0, H, r, r, 0, s)
+    b, _, _ = _oz64_env(lib, x64, pre, post, 0, H, r, r, 0, s)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)

@@ -128,7 +128,8 @@ def test_degenerate_without_fallback_raises():
 
 
 @pytest.mark.parametrize("I,RR", [(100, 25), (64, 64), (40, 64), (500, 100), (160, 400), (13, 6), (7, 30),
-                                  (300, 36), (1000, 100)])
+                                  (300, 36), (1000, 100), (161, 400), (57, 200), (250, 64), (33, 33), (130, 20),
+                                  (9, 100), (224, 112), (2, 9)])
 def test_core_householder_qr(I, RR):
     """mode2_qr's R (ring.py:236-249, sign convention linalg.py:36-52) for every size class."""
     import torch
