@@ -89,8 +89,12 @@ constexpr int kOzDigits = OzF32::D;  // (fp32 variant layout helpers)
 constexpr int kOzLevels = OzF32::LV;
 constexpr int64_t kOzKmax = OzF32::KMAX;
 
+// ACC = 512 / (levels x BN) accumulator buffers in TMEM: with two (fp64 digits, n-tiles
+// <= 32 wide) the epilogue drains tile i while the MMAs of tile i+1 run -- the short-K
+// shapes (c3 phase R: K = 500) are otherwise epilogue-bound.
 template <int BN, class SC>
 struct OzTile {
+  static constexpr int ACC = (512 / (SC::LV * BN)) >= 2 ? 2 : 1;
   static constexpr int A_PLANE = kOzBM * kOzBK;  // 8 KB
   static constexpr int B_PLANE = BN * kOzBK;
   static constexpr int STAGE = SC::D * (A_PLANE + B_PLANE);
@@ -106,6 +110,7 @@ struct OzTile {
   static constexpr int THREADS = 6 * 32;
   static constexpr size_t SMEM = static_cast<size_t>(STAGES) * STAGE + OUT_BYTES + 1024 + 256;
   static_assert(SC::LV * BN <= TMEM_COLS, "levels x BN accumulator columns exceed TMEM");
+  static constexpr int ACC_COLS = SC::LV * BN;  // one accumulator buffer
   static_assert(STAGES >= 2, "digit stage too large for shared memory");
 };
 
@@ -327,9 +332,9 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
   double* otile = reinterpret_cast<double*>(sm + S * T::STAGE);  // [kOzBM][OUT_LD] epilogue staging
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + S * T::STAGE + T::OUT_BYTES);
   uint64_t* empty = full + S;
-  uint64_t* acc_full = empty + S;
-  uint64_t* acc_empty = acc_full + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
+  uint64_t* acc_full = empty + S;          // [ACC]
+  uint64_t* acc_empty = acc_full + T::ACC;  // [ACC]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + T::ACC);
 
   const int tid = threadIdx.x, lane = tid & 31;
   const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
@@ -338,8 +343,10 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
       mbar_init(full + s, 1);
       mbar_init(empty + s, 1);
     }
-    mbar_init(acc_full, 1);
-    mbar_init(acc_empty, 4);  // one arrive per epilogue warp
+    for (int b = 0; b < T::ACC; ++b) {
+      mbar_init(acc_full + b, 1);
+      mbar_init(acc_empty + b, 4);  // one arrive per epilogue warp
+    }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 1) {
@@ -397,7 +404,9 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
       int ktiles;
       tile_k(split, kbeg, ktiles);
       const int bw = g.nt.width(nt);
-      mbar_wait(acc_empty, it & 1);  // accumulators drained and zeroed by the epilogue
+      const int ab = static_cast<int>(it % T::ACC);
+      const uint32_t tacc = tmem + ab * T::ACC_COLS;
+      mbar_wait(acc_empty + ab, (it / T::ACC) & 1);  // this buffer drained and zeroed by the epilogue
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
       for (int kt = 0; kt < ktiles; ++kt, ++gk) {
         const uint32_t s = gk % S;
@@ -405,18 +414,22 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         {
           const uint64_t da = dA0 + ((s * T::STAGE) >> 4), db = dB0 + ((s * T::STAGE) >> 4);
-          switch (bw) {  // warp-uniform: the n-tile width fixes the MMA shapes
-            case 64: oz_issue_stage<64, BN, D, LV>(tmem, da, db); break;
-            case 48: oz_issue_stage<48, BN, D, LV>(tmem, da, db); break;
-            case 32: oz_issue_stage<32, BN, D, LV>(tmem, da, db); break;
-            default: oz_issue_stage<16, BN, D, LV>(tmem, da, db); break;
+          // warp-uniform: the n-tile width fixes the MMA shapes (widths <= BN)
+          if constexpr (BN >= 64) {
+            if (bw == 64) oz_issue_stage<64, BN, D, LV>(tacc, da, db);
+            else if (bw == 48) oz_issue_stage<48, BN, D, LV>(tacc, da, db);
+            else if (bw == 32) oz_issue_stage<32, BN, D, LV>(tacc, da, db);
+            else oz_issue_stage<16, BN, D, LV>(tacc, da, db);
+          } else {
+            if (bw == 32) oz_issue_stage<32, BN, D, LV>(tacc, da, db);
+            else oz_issue_stage<16, BN, D, LV>(tacc, da, db);
           }
           oz_commit_warp(empty + s);  // the stage is free once these MMAs have read it
         }
         __syncwarp();
       }
-      if (ktiles > 0) oz_commit_warp(acc_full);
-      else if (lane == 0) mbar_arrive(acc_full);
+      if (ktiles > 0) oz_commit_warp(acc_full + ab);
+      else if (lane == 0) mbar_arrive(acc_full + ab);
       __syncwarp();
       ++it;
     });
@@ -427,11 +440,12 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
     // engine uses).  Whole-tile staging releases TMEM before the global stores;
     // chunked staging (large digit stages) stores 16 columns at a time.
     const int quad = warp & 3;
-    const uint32_t tlane = tmem + (static_cast<uint32_t>(quad * 32) << 16);
-    tmem_zero<LV * BN>(tlane);  // every MMA accumulates: the levels start from zero
+    const uint32_t tlane0 = tmem + (static_cast<uint32_t>(quad * 32) << 16);
+    for (int b = 0; b < T::ACC; ++b) tmem_zero<LV * BN>(tlane0 + b * T::ACC_COLS);  // MMAs always accumulate
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
     __syncwarp();
-    if (lane == 0) mbar_arrive(acc_empty);
+    if (lane == 0)
+      for (int b = 0; b < T::ACC; ++b) mbar_arrive(acc_empty + b);
     uint32_t it = 0;
     oz_for_tiles(g, [&](int split, int mt, int nt) {
       int64_t kbeg;
@@ -440,7 +454,9 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
       const int64_t m0 = static_cast<int64_t>(mt) * kOzBM, n0 = g.nt.start(nt);
       const int bw = g.nt.width(nt);
       const int64_t nend = (n0 + bw < g.N) ? n0 + bw : g.N;
-      mbar_wait(acc_full, it & 1);
+      const int ab = static_cast<int>(it % T::ACC);
+      const uint32_t tlane = tlane0 + ab * T::ACC_COLS;
+      mbar_wait(acc_full + ab, (it / T::ACC) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
       const int r = quad * 32 + lane;
       const int64_t m = m0 + r;
@@ -518,7 +534,7 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
       tmem_zero<LV * BN>(tlane);
       asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
       __syncwarp();
-      if (lane == 0) mbar_arrive(acc_empty);  // the MMA warp may start the next tile
+      if (lane == 0) mbar_arrive(acc_empty + ab);  // the MMA warp may reuse this buffer
       if constexpr (!T::CHUNKED) {
         asm volatile("bar.sync 1, 128;\n" ::: "memory");
         // coalesced stores: lane -> column n (BN / 32 per lane), warp -> rows quad, quad + 4, ...

@@ -483,11 +483,17 @@ inline int64_t oz_digits_bytes(const trals::OzRowTiles& rt, int64_t k, int digit
   return digits * rt.rows_pad() * ((k + 63) / 64 * 64);
 }
 inline trals::OzRowTiles oz_a_tiles(int64_t rows) { return trals::OzRowTiles::fixed(rows, trals::kOzBM); }
+// n-tiles of at most 32 columns (two TMEM accumulator buffers with 8 digit levels) when the
+// contraction is short: a tile's MMAs then last about as long as its epilogue, which the
+// second buffer overlaps (fp64 scheme only; the fp32 one keeps its staged epilogue)
+constexpr int64_t kOzShortK = 8192;
+template <class SC>
+inline int oz_bn(int64_t K) { return (SC::BAL && K < kOzShortK) ? 32 : kOzBN; }
 // TRALS_OZ_FIXED_TILES=1 (experiments): every n-tile kOzBN wide, the last one zero padded
-inline trals::OzRowTiles oz_b_tiles(int64_t n) {
+inline trals::OzRowTiles oz_b_tiles(int64_t n, int bn = kOzBN) {
   static int fixed = -1;
   if (fixed < 0) fixed = std::getenv("TRALS_OZ_FIXED_TILES") ? 1 : 0;
-  return fixed ? trals::OzRowTiles::fixed(n, kOzBN) : trals::OzRowTiles::balanced(n, kOzBN);
+  return fixed ? trals::OzRowTiles::fixed(n, bn) : trals::OzRowTiles::balanced(n, bn);
 }
 
 // split-K over a per-tile time model and never more than SC::KMAX k per CTA (int32
@@ -496,13 +502,14 @@ inline trals::OzRowTiles oz_b_tiles(int64_t n) {
 template <class SC>
 SplitPlan plan_split_oz(int64_t M, int64_t K, int64_t N) {
   const int64_t BK = trals::kOzBK;
-  const int64_t tiles = ((M + trals::kOzBM - 1) / trals::kOzBM) * oz_b_tiles(N).ntiles;
+  const int bn = oz_bn<SC>(K);
+  const int64_t tiles = ((M + trals::kOzBM - 1) / trals::kOzBM) * oz_b_tiles(N, bn).ntiles;
   const int64_t slots = kSMs;
   const int64_t smin = std::max<int64_t>(1, (K + SC::KMAX - 1) / SC::KMAX);
   const int64_t smax = std::max<int64_t>(smin, std::min<int64_t>(64, K / (4 * BK)));
   int pairs = 0;
   for (int a = 0; a < SC::D; ++a) pairs += std::min(SC::D, SC::LV - a);
-  const double t_tile = SC::BAL ? static_cast<double>(pairs) * trals::kOzBM * N / oz_b_tiles(N).ntiles *
+  const double t_tile = SC::BAL ? static_cast<double>(pairs) * trals::kOzBM * N / oz_b_tiles(N, bn).ntiles *
                                       static_cast<double>(K) /
                                       (8192.0 * 1.9e9)
                                 : 4.0 * trals::kOzBM * static_cast<double>(K) / (6.5e12 / slots);
@@ -526,8 +533,9 @@ struct OzWs {
 };
 // in-kernel two-way split-K fix-up (no reduce launch) for the chunked-epilogue scheme
 template <class SC>
-bool oz_fixup(const SplitPlan& sp) {
-  return sp.splits == 2 && trals::OzTile<kOzBN, SC>::CHUNKED;
+bool oz_fixup(const SplitPlan& sp, int64_t K) {
+  const bool chunked = oz_bn<SC>(K) == 32 ? trals::OzTile<32, SC>::CHUNKED : trals::OzTile<kOzBN, SC>::CHUNKED;
+  return sp.splits == 2 && chunked;
 }
 
 template <class SC>
@@ -535,12 +543,14 @@ OzWs oz_ws_layout(int64_t M, int64_t K, int64_t N) {
   const SplitPlan sp = plan_split_oz<SC>(M, K, N);
   OzWs w{};
   w.planes = 0;
-  w.eb = w.planes + (oz_digits_bytes(oz_b_tiles(N), K, SC::D) + 15) / 16 * 2;
+  const int bn = oz_bn<SC>(K);
+  w.eb = w.planes + (oz_digits_bytes(oz_b_tiles(N, bn), K, SC::D) + 15) / 16 * 2;
   w.mx = w.eb + (N + 3) / 4 * 2;
   w.flags = w.mx + (N + 1) / 2 * 2;
-  const int64_t tiles = ((M + trals::kOzBM - 1) / trals::kOzBM) * oz_b_tiles(N).ntiles;
-  w.part = w.flags + (oz_fixup<SC>(sp) ? (2 * tiles + 1) / 2 + 1 : 0);
-  w.total = w.part + (sp.splits > 1 ? (oz_fixup<SC>(sp) ? 1 : static_cast<int64_t>(sp.splits)) * M * N : 0);
+  const int64_t tiles = ((M + trals::kOzBM - 1) / trals::kOzBM) * oz_b_tiles(N, bn).ntiles;
+  const bool fix = oz_fixup<SC>(sp, K);
+  w.part = w.flags + (fix ? (2 * tiles + 1) / 2 + 1 : 0);
+  w.total = w.part + (sp.splits > 1 ? (fix ? 1 : static_cast<int64_t>(sp.splits)) * M * N : 0);
   return w;
 }
 
@@ -559,6 +569,19 @@ int launch_colmax(const T* x, int64_t rows, int64_t cols, int64_t ld, double* ou
   return launch_status();
 }
 
+template <int BN, class SC>
+int launch_oz(const trals::OzArgs& g, int grid, cudaStream_t s) {
+  using T = trals::OzTile<BN, SC>;
+  auto kern = trals::oz8_kernel<BN, SC>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(T::SMEM));
+    attr = true;
+  }
+  kern<<<grid, T::THREADS, T::SMEM, s>>>(g);
+  return launch_status();
+}
+
 // C(m, n) = sum_k A[m][k] B[k][n]: A given as tiled digits [D x 128-row tiles] + row exponents ea[M],
 // B fp64 [K][ldb] (sliced per call into the workspace), C fp64 through cm.
 template <class SC>
@@ -573,8 +596,9 @@ int gemm_oz(const int8_t* ad, const int32_t* ea, int64_t M, int64_t K, int64_t N
   double* bmx = ws + w.mx;
   // B^T rows = columns of B: max over k, then tiled digits (transposed read)
   if (int st = launch_colmax<double>(B, K, N, ldb, bmx, s)) return st;
+  const int bn = oz_bn<SC>(K);
   {
-    const trals::OzRowTiles bt = oz_b_tiles(N);
+    const trals::OzRowTiles bt = oz_b_tiles(N, bn);
     dim3 grid(static_cast<unsigned>((K + 63) / 64), static_cast<unsigned>((bt.rows_pad() + 63) / 64));
     trals::oz_digits_tiled_t_kernel<double, SC><<<grid, 256, 0, s>>>(B, K, N, ldb, bmx, bd, bt, eb);
     if (int st = launch_status()) return st;
@@ -582,12 +606,12 @@ int gemm_oz(const int8_t* ad, const int32_t* ea, int64_t M, int64_t K, int64_t N
   trals::OzArgs g{};
   g.M = M; g.K = K; g.N = N; g.kchunk = sp.kchunk; g.splits = sp.splits;
   g.mtiles = static_cast<int>((M + trals::kOzBM - 1) / trals::kOzBM);
-  g.nt = oz_b_tiles(N);
+  g.nt = oz_b_tiles(N, bn);
   g.ntiles = g.nt.ntiles;
   static int norot = -1;  // TRALS_OZ_NOROT=1 (experiments): k blocks in natural order
   if (norot < 0) norot = std::getenv("TRALS_OZ_NOROT") ? 1 : 0;
   g.rotate = norot ? 0 : 1;
-  g.fixup = oz_fixup<SC>(sp) ? 1 : 0;
+  g.fixup = oz_fixup<SC>(sp, K) ? 1 : 0;
   if (g.fixup) {
     const int64_t tiles = static_cast<int64_t>(g.mtiles) * g.ntiles;
     g.tickets = reinterpret_cast<int*>(ws + w.flags);
@@ -597,18 +621,10 @@ int gemm_oz(const int8_t* ad, const int32_t* ea, int64_t M, int64_t K, int64_t N
   g.kblocks = (K + trals::kOzBK - 1) / trals::kOzBK;
   g.ad = ad; g.bd = bd;
   g.cmap = cm; g.ea = ea; g.eb = eb; g.C = C; g.ws = ws + w.part;
-  using T = trals::OzTile<kOzBN, SC>;
-  auto kern = trals::oz8_kernel<kOzBN, SC>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(T::SMEM));
-    attr = true;
-  }
   const int64_t tiles = static_cast<int64_t>(g.mtiles) * g.ntiles * sp.splits;
   if (tiles > INT32_MAX) return TRALS_ERR_UNSUPPORTED;
   const int grid = static_cast<int>(std::min<int64_t>(tiles, kSMs));
-  kern<<<grid, T::THREADS, T::SMEM, s>>>(g);
-  if (int st = launch_status()) return st;
+  if (int st = bn == 32 ? launch_oz<32, SC>(g, grid, s) : launch_oz<kOzBN, SC>(g, grid, s)) return st;
   if (sp.splits > 1 && !g.fixup) {
     GemmArgs r{};
     r.P = 1; r.M = M; r.N = N; r.splits = sp.splits; r.ws = ws + w.part; r.C = C; r.cmap = cm; r.alpha = 1.0;
