@@ -103,6 +103,12 @@ class SweepEngine:
         if fp64_gemm == "auto":
             env_flops = 2.0 * _prod(x_local.shape) * max(int(r) for r in ranks) ** 2
             fp64_gemm = "ozaki" if env_flops >= OZ64_MIN_FLOPS else "dmma"
+            if fp64_gemm == "ozaki" and _test_lib is None and x_local.dtype == torch.float64:
+                # the digit planes (one K-major copy per X-streaming phase, 8 B per element each)
+                # must fit beside everything else; otherwise stay on the fp64 pipe
+                free, _ = torch.cuda.mem_get_info(x_local.device)
+                if 2 * 8 * x_local.numel() * 1.05 > free:
+                    fp64_gemm = "dmma"
         self.fp64_gemm = fp64_gemm
         self.oz64 = (not self.fp32) and fp64_gemm == "ozaki" and _test_lib is None
         self.sliced = self.fp32 or self.oz64

@@ -55,7 +55,8 @@ class AlsConfig:
     and of the half chain -- 36 exact int32 digit-pair products combined in
     fp64, with the accuracy of an fp64 product (measured against an
     extended-precision one) -- "dmma" on the fp64 DMMA pipe, and "auto"
-    (default) picks ozaki when 2 |X| R^2 >= 4 GFLOP (BASELINE c3-c5).  X's digit
+    (default) picks ozaki when 2 |X| R^2 >= 4 GFLOP (BASELINE c3-c5) and the
+    digit planes fit in free device memory.  X's digit
     planes (2 x |X| bytes) are made once per call, timed as
     upfront_seconds["mttsp"].
     """

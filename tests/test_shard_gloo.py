@@ -28,22 +28,25 @@ def _worker(rank, world, port, case, out_q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    dims, ranks, shard = case
+    dims, ranks, shard, variant, exact = case
     rng = np.random.default_rng(7)
     x = rng.standard_normal(dims)
     init = O.gaussian_ring(dims, ranks, O.philox(3))
     lo, hi = _slab(dims[shard], world, rank)
-    cores, errs, _ = run_engine(x, list(ranks), "ne", init, 2, lib=FakeTrals(), shard_mode=shard, lo=lo, hi=hi,
-                                world=world)
+    cores, errs, _ = run_engine(x, list(ranks), variant, init, 2, lib=FakeTrals(), shard_mode=shard, lo=lo, hi=hi,
+                                world=world, exact=exact)
     out_q.put((rank, [c.tolist() for c in cores], errs))
     dist.destroy_process_group()
 
 
 @pytest.mark.parametrize("case", [
-    ((7, 9, 5), (2, 3, 2), 1),
-    ((5, 4, 6, 3), (2, 3, 2, 2), 1),
-    ((5, 4, 6, 3), (2, 3, 2, 2), 3),
-    ((6, 5, 4, 3, 4), (2, 2, 2, 2, 2), 0),
+    ((7, 9, 5), (2, 3, 2), 1, "ne", False),
+    ((5, 4, 6, 3), (2, 3, 2, 2), 1, "ne", False),
+    ((5, 4, 6, 3), (2, 3, 2, 2), 3, "ne", False),
+    ((6, 5, 4, 3, 4), (2, 2, 2, 2, 2), 0, "ne", False),
+    ((5, 4, 6, 3), (2, 3, 2, 2), 0, "qr", False),      # per-core QR + R-Gram chain on every rank
+    ((7, 9, 5), (2, 3, 2), 2, "qrne", True),           # exact error: partial residuals all-reduced
+    ((6, 5, 4, 3, 4), (2, 2, 2, 2, 2), 4, "qrne", False),
 ])
 def test_two_rank_shard_matches_oracle(case):
     from oracle import tenring_oracle as O
@@ -61,11 +64,12 @@ def test_two_rank_shard_matches_oracle(case):
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    dims, ranks, shard = case
+    dims, ranks, shard, variant, exact = case
     rng = np.random.default_rng(7)
     x = rng.standard_normal(dims)
     init = O.gaussian_ring(dims, ranks, O.philox(3))
-    ocores, rep = O.solve(x, "ne", O.Config(ranks=ranks, max_iters=2, init_cores=init, error_mode="cheap"))
+    ocores, rep = O.solve(x, variant, O.Config(ranks=ranks, max_iters=2, init_cores=init,
+                                               error_mode="exact" if exact else "cheap"))
     c0, e0 = res[0]
     c1, e1 = res[1]
     assert e0 == e1  # replicas stay in lock-step
