@@ -274,6 +274,16 @@ int trals_residual_f64(const double* d_X, int64_t pre, int64_t post, const doubl
                        int64_t K, const double* d_xnorm2, double* d_out, double* d_ws, int64_t ws_elems,
                        void* stream);
 
+/* The same exact error with the product on the int8 tensor cores: HL (rows) and HRt
+ * (columns) sliced into 8 balanced digits each, the 36 digit-pair products of levels
+ * <= 7 accumulated exactly and combined in fp64 (the scheme of trals_env_oz64), the
+ * residual (X - HL HRt)^2 summed in the GEMM epilogue in a fixed order (one partial per
+ * CTA, then one fixed-order sum): X_hat is never stored.  K <= 61440. */
+int64_t trals_residual_oz64_ws_elems(int64_t pre, int64_t post, int64_t K);
+int trals_residual_oz64(const double* d_X, int64_t pre, int64_t post, const double* d_HL, const double* d_HRt,
+                        int64_t K, const double* d_xnorm2, double* d_out, double* d_ws, int64_t ws_elems,
+                        void* stream);
+
 #ifdef __cplusplus
 }
 #endif

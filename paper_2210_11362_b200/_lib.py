@@ -73,6 +73,8 @@ _SIGNATURES = {
     "trals_error_terms_f64": (c_int, [_dp, _dp, _dp, c_int64, c_int, _dp, _dp, _dp, c_int64, c_void_p]),
     "trals_residual_ws_elems": (c_int64, [c_int64, c_int64]),
     "trals_residual_f64": (c_int, [_dp, c_int64, c_int64, _dp, _dp, c_int64, _dp, _dp, _dp, c_int64, c_void_p]),
+    "trals_residual_oz64_ws_elems": (c_int64, [c_int64, c_int64, c_int64]),
+    "trals_residual_oz64": (c_int, [_dp, c_int64, c_int64, _dp, _dp, c_int64, _dp, _dp, _dp, c_int64, c_void_p]),
     "trals_mttsp_ws_elems": (c_int64, [c_int, POINTER(c_int64), POINTER(c_int32), c_int]),
     "trals_mttsp_f64": (c_int, [_dp, c_int, POINTER(c_int64), POINTER(c_int32), c_int, POINTER(c_void_p),
                                 POINTER(c_void_p), POINTER(c_void_p), _dp, _dp, c_int64, c_void_p]),

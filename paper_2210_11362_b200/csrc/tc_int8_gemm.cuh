@@ -164,6 +164,12 @@ struct OzArgs {
   int fixup;
   int* tickets;        // [mtiles * ntiles], zero at launch
   int* ready;          // [mtiles * ntiles], zero at launch
+  // residual mode (exact error, chunked epilogue, one K split): C is never stored; the
+  // epilogue accumulates sum (X[m][n] - C[m][n])^2 (X row-major, pitch ldx) and every CTA
+  // writes its fixed-order partial to rpart[blockIdx.x]
+  const double* X;
+  int64_t ldx;
+  double* rpart;
   int64_t kblocks;     // 64-k blocks of the tiled digit layout (ceil(K / 64))
   const int8_t* ad;    // A digits, tiled: [mtiles][kblocks][D][128 x 64 B]
   const int8_t* bd;    // B digits, tiled: [n-tile][kblocks][D][width x 64 B]
@@ -447,6 +453,7 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
     if (lane == 0)
       for (int b = 0; b < T::ACC; ++b) mbar_arrive(acc_empty + b);
     uint32_t it = 0;
+    double rsum = 0.0;  // residual mode: this thread's squared residuals, in tile order
     oz_for_tiles(g, [&](int split, int mt, int nt) {
       int64_t kbeg;
       int ktiles;
@@ -507,12 +514,14 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
           const uint32_t un = static_cast<uint32_t>(n);
           const int64_t coff = nok ? static_cast<int64_t>(un / N2) * sn1 + static_cast<int64_t>(un % N2) * sn2 : 0;
           const double sb = nok ? ldexp(1.0, g.eb[n]) : 0.0;
-          // the other K half's partial for this chunk: all 16 loads issued before any use
-          double pv[kOzBM / 8];
+          // the other K half's partial (fix-up) or X (residual mode) for this chunk: all 16
+          // loads issued before any use (one memory latency per chunk, not one per row)
+          double pv[kOzBM / 8], xv[kOzBM / 8];
 #pragma unroll
           for (int k = 0; k < kOzBM / 8; ++k) {
             const int rr = quad * 2 + (lane >> 4) + 8 * k;
             pv[k] = (second && nok && rr < rows) ? __ldcg(g.ws + static_cast<int64_t>(m0 + rr) * g.N + n) : 0.0;
+            xv[k] = (g.rpart && nok && rr < rows) ? __ldcs(g.X + static_cast<int64_t>(m0 + rr) * g.ldx + n) : 0.0;
           }
 #pragma unroll
           for (int k = 0; k < kOzBM / 8; ++k) {
@@ -521,7 +530,14 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
             const uint32_t mm = static_cast<uint32_t>(m0 + rr);
             const int64_t roff = static_cast<int64_t>(mm / M2) * sm1 + static_cast<int64_t>(mm % M2) * sm2;
             const double o = otile[rr * T::OUT_LD + (lane & 15)] * sb + pv[k];
-            if (nok) base[roff + coff] = o;
+            if (g.rpart) {
+              if (nok) {
+                const double d = xv[k] - o;
+                rsum = fma(d, d, rsum);
+              }
+            } else if (nok) {
+              base[roff + coff] = o;
+            }
           }
           asm volatile("bar.sync 1, 128;\n" ::: "memory");
         }
@@ -560,6 +576,14 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
       }
       ++it;
     });
+    if (g.rpart) {  // fixed-order CTA partial: warp shuffles, then the 4 warps in order
+      for (int o = 16; o > 0; o >>= 1) rsum += __shfl_xor_sync(0xffffffffu, rsum, o);
+      double* red = otile;  // free now
+      asm volatile("bar.sync 1, 128;\n" ::: "memory");
+      if (lane == 0) red[quad] = rsum;
+      asm volatile("bar.sync 1, 128;\n" ::: "memory");
+      if (quad == 0 && lane == 0) g.rpart[blockIdx.x] = ((red[0] + red[1]) + red[2]) + red[3];
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();

@@ -672,6 +672,34 @@ int oz_split(const Tin* x, int64_t rows, int64_t cols, int transpose, int8_t* di
 inline CMap rowmajor(int64_t ldc) { return CMap{0, 1 << 30, 0, ldc, 1 << 30, 0, 1}; }
 
 // ---------------------------------------------------------------------------
+// Exact error on the int8 tensor cores: ssr = sum (X - HL HRt)^2 with the product formed
+// tile by tile from 8-digit slices of HL (rows) and HRt (columns) -- the same fp64-accurate
+// scheme as the environment products -- and never stored (residual epilogue)
+// ---------------------------------------------------------------------------
+struct ResOzWs {
+  int64_t adig, aexp, amx, bdig, bexp, bmx, part, total;  // offsets in doubles
+};
+// 32-wide double-buffered n-tiles (c5, K = 400): 14.2 ms against 20 ms for the DMMA residual; the
+// launch streams ~90 GB of digit tiles through L2 (7.5 TB/s), so 64-wide tiles or a grouped
+// tile order that keeps HL's digits L2-resident measured the same
+constexpr int kResBN = 32;
+ResOzWs residual_oz64_layout(int64_t pre, int64_t post, int64_t K) {
+  using SC = trals::OzF64;
+  const int bn = kResBN;
+  ResOzWs w{};
+  w.adig = 0;
+  w.aexp = w.adig + (oz_digits_bytes(oz_a_tiles(pre), K, SC::D) + 15) / 16 * 2;
+  w.amx = w.aexp + (pre + 3) / 4 * 2;
+  w.bdig = w.amx + (pre + 1) / 2 * 2;
+  w.bexp = w.bdig + (oz_digits_bytes(oz_b_tiles(post, bn), K, SC::D) + 15) / 16 * 2;
+  w.bmx = w.bexp + (post + 3) / 4 * 2;
+  w.part = w.bmx + (post + 1) / 2 * 2;
+  w.total = w.part + kSMs;
+  return w;
+}
+
+
+// ---------------------------------------------------------------------------
 // small kernels
 // ---------------------------------------------------------------------------
 // index of core element (a, i, b) in each layout
@@ -2831,6 +2859,54 @@ int trals_residual_f64(const double* X, int64_t pre, int64_t post, const double*
   int st = residual(HL, pre, K, HRt, post, X, ws, s);
   if (st) return st;
   residual_final_kernel<<<1, 1024, 0, s>>>(ws, static_cast<int>(residual_blocks(pre, post)), xnorm2, out);
+  return launch_status();
+}
+
+int64_t trals_residual_oz64_ws_elems(int64_t pre, int64_t post, int64_t K) {
+  return pre < 1 || post < 1 || K < 1 ? 0 : residual_oz64_layout(pre, post, K).total;
+}
+
+int trals_residual_oz64(const double* X, int64_t pre, int64_t post, const double* HL, const double* HRt, int64_t K,
+                        const double* xnorm2, double* out, double* ws, int64_t ws_elems, void* stream) {
+  using SC = trals::OzF64;
+  if (!X || !HL || !HRt || !out || !ws || pre < 1 || post < 1 || K < 1 || K > SC::KMAX || pre > INT32_MAX ||
+      post > INT32_MAX)
+    return TRALS_ERR_ARG;
+  const ResOzWs w = residual_oz64_layout(pre, post, K);
+  if (ws_elems < w.total) return TRALS_ERR_WORKSPACE;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int8_t* adig = reinterpret_cast<int8_t*>(ws + w.adig);
+  int32_t* aexp = reinterpret_cast<int32_t*>(ws + w.aexp);
+  int8_t* bdig = reinterpret_cast<int8_t*>(ws + w.bdig);
+  int32_t* bexp = reinterpret_cast<int32_t*>(ws + w.bexp);
+  // A = HL [pre][K] by rows; B = the columns of HRt [K][post] (transposed slicing)
+  if (int st = oz_split<double, SC>(HL, pre, K, 0, adig, aexp, ws + w.amx, pre, s)) return st;
+  const int bn = kResBN;
+  if (int st = launch_colmax<double>(HRt, K, post, post, ws + w.bmx, s)) return st;
+  {
+    const trals::OzRowTiles bt = oz_b_tiles(post, bn);
+    const int64_t gy = (bt.rows_pad() + 63) / 64;
+    if (gy > 65535) return TRALS_ERR_UNSUPPORTED;
+    dim3 grid(static_cast<unsigned>((K + 63) / 64), static_cast<unsigned>(gy));
+    trals::oz_digits_tiled_t_kernel<double, SC><<<grid, 256, 0, s>>>(HRt, K, post, post, ws + w.bmx, bdig, bt, bexp);
+    if (int st = launch_status()) return st;
+  }
+  trals::OzArgs g{};
+  g.M = pre; g.K = K; g.N = post; g.kchunk = K; g.splits = 1;
+  g.mtiles = static_cast<int>((pre + trals::kOzBM - 1) / trals::kOzBM);
+  g.nt = oz_b_tiles(post, bn);
+  g.ntiles = g.nt.ntiles;
+  g.rotate = 1;
+  g.fixup = 0;
+  g.kblocks = (K + trals::kOzBK - 1) / trals::kOzBK;
+  g.ad = adig; g.bd = bdig; g.ea = aexp; g.eb = bexp;
+  g.cmap = rowmajor(post); g.C = nullptr; g.ws = nullptr;
+  g.X = X; g.ldx = post; g.rpart = ws + w.part;
+  const int64_t tiles = static_cast<int64_t>(g.mtiles) * g.ntiles;
+  if (tiles > INT32_MAX) return TRALS_ERR_UNSUPPORTED;
+  const int grid = static_cast<int>(std::min<int64_t>(tiles, kSMs));
+  if (int st = launch_oz<kResBN, SC>(g, grid, s)) return st;
+  residual_final_kernel<<<1, 1024, 0, s>>>(ws + w.part, grid, xnorm2, out);
   return launch_status();
 }
 

@@ -715,7 +715,9 @@ class SweepEngine:
             "h": h, "pre": pre, "post": post, "K": R0 * Rh,
             "HL": self._empty(pre * R0 * Rh), "HRt": self._empty(R0 * Rh * post),
             "tmp": self._empty(max(1, tl, tr)), "ws": self._empty(max(1, nl, nr)),
-            "part": self._empty(max(1, self.lib.trals_residual_ws_elems(pre, post))),
+            # the int8 engines also form the exact error's product on the tensor cores
+            "part": self._empty(max(1, self.lib.trals_residual_oz64_ws_elems(pre, post, R0 * Rh) if self.sliced
+                                    else self.lib.trals_residual_ws_elems(pre, post))),
             "bdl": bdl, "brl": brl, "bdr": bdr, "brr": brr,
         }
         return self._xp
@@ -734,9 +736,9 @@ class SweepEngine:
         if self.fp32 and self._x64 is None:
             self.ensure_x64()
         xd = self._x64 if self.fp32 else self.x
-        L.check(self.lib.trals_residual_f64(xd.data_ptr(), xp["pre"], xp["post"], xp["HL"].data_ptr(),
-                                            xp["HRt"].data_ptr(), xp["K"], self.xnorm2.data_ptr(), out.data_ptr(),
-                                            xp["part"].data_ptr(), xp["part"].numel(), sp), "residual")
+        res = self.lib.trals_residual_oz64 if self.sliced else self.lib.trals_residual_f64
+        L.check(res(xd.data_ptr(), xp["pre"], xp["post"], xp["HL"].data_ptr(), xp["HRt"].data_ptr(), xp["K"],
+                    self.xnorm2.data_ptr(), out.data_ptr(), xp["part"].data_ptr(), xp["part"].numel(), sp), "residual")
         if self.world > 1:
             import torch.distributed as dist
             dist.all_reduce(out[1:2], group=self.group)

@@ -170,6 +170,13 @@ class FakeTrals:
     def trals_residual_ws_elems(self, pre, post):
         return 1
 
+    def trals_residual_oz64_ws_elems(self, pre, post, K):
+        return 1
+
+    def trals_residual_oz64(self, X, pre, post, HL, HRt, K, xnorm2, out, ws, ws_elems, stream):
+        # same quantity as trals_residual_f64 (the int8 product is fp64-accurate)
+        return self.trals_residual_f64(X, pre, post, HL, HRt, K, xnorm2, out, ws, ws_elems, stream)
+
     def trals_residual_f64(self, X, pre, post, HL, HRt, K, xnorm2, out, ws, ws_elems, stream):
         self._count("residual")
         x = _arr(X, pre * post).reshape(pre, post)

@@ -18,7 +18,10 @@ SMALL = ["spec_n3_i30_r3", "nonuni_n4", "n5_i6", "n2_mat", "odd_n3"]
 @pytest.mark.parametrize("name", SMALL)
 @pytest.mark.parametrize("variant", ["ne", "qr", "qrne", "als"])
 @pytest.mark.parametrize("mode", ["cheap", "exact"])
-def test_small_goldens(name, variant, mode):
+@pytest.mark.parametrize("gemm", ["auto", "ozaki"])
+def test_small_goldens(name, variant, mode, gemm):
+    """Reference goldens at the fp64 tolerances on both product engines (auto = DMMA at these
+    sizes; ozaki = environment products and the exact error on the int8 tensor cores)."""
     from paper_2210_11362_b200 import AlsConfig, decompose
     g = load_golden(name)
     if f"{variant}_{mode}_errors" not in g:
@@ -26,7 +29,8 @@ def test_small_goldens(name, variant, mode):
     dims = tuple(int(d) for d in g["dims"])
     N = len(dims)
     ranks = tuple(int(r) for r in g["ranks"])
-    cfg = AlsConfig(ranks=ranks, max_iters=int(g["sweeps"]), init_cores=golden_cores(g, "init", N), error_mode=mode)
+    cfg = AlsConfig(ranks=ranks, max_iters=int(g["sweeps"]), init_cores=golden_cores(g, "init", N), error_mode=mode,
+                    fp64_gemm=gemm)
     cores, rep = decompose(g["x"], variant, cfg)
     assert rep.variant == variant and rep.termination == "max_iters"
     assert len(rep.iter_seconds) == int(g["sweeps"]) and set(rep.iter_buckets[0]) == {
