@@ -1921,11 +1921,18 @@ __device__ void hh_factor_blocked(double* A, int ld, int mr, int nc, double* tau
 // Tbuf: 128 doubles; Tg: optional per-panel T output (blocked path only).
 __device__ void hh_factor_smem(double* A, int ld, int mr, int nc, double* tau, double* red, double* Tbuf,
                                double* Tg, double* scratch, double* xch, const HhPub* pub = nullptr) {
-  if (mr <= 32) hh_factor_blocked<1>(A, ld, mr, nc, tau, Tbuf, Tg, scratch, xch, pub);
-  else if (mr <= 64) hh_factor_blocked<2>(A, ld, mr, nc, tau, Tbuf, Tg, scratch, xch, pub);
-  else if (mr <= 128) hh_factor_blocked<4>(A, ld, mr, nc, tau, Tbuf, Tg, scratch, xch, pub);
-  else if (mr <= kHhPanelRows) hh_factor_blocked<8>(A, ld, mr, nc, tau, Tbuf, Tg, scratch, xch, pub);
-  else hh_factor_unblocked(A, ld, mr, nc, tau, red);
+  // rows per lane = ceil(mr / 32) exactly: empty register rows still cost instructions
+  switch ((mr + 31) / 32) {
+    case 1: hh_factor_blocked<1>(A, ld, mr, nc, tau, Tbuf, Tg, scratch, xch, pub); break;
+    case 2: hh_factor_blocked<2>(A, ld, mr, nc, tau, Tbuf, Tg, scratch, xch, pub); break;
+    case 3: hh_factor_blocked<3>(A, ld, mr, nc, tau, Tbuf, Tg, scratch, xch, pub); break;
+    case 4: hh_factor_blocked<4>(A, ld, mr, nc, tau, Tbuf, Tg, scratch, xch, pub); break;
+    case 5: hh_factor_blocked<5>(A, ld, mr, nc, tau, Tbuf, Tg, scratch, xch, pub); break;
+    case 6: hh_factor_blocked<6>(A, ld, mr, nc, tau, Tbuf, Tg, scratch, xch, pub); break;
+    case 7: hh_factor_blocked<7>(A, ld, mr, nc, tau, Tbuf, Tg, scratch, xch, pub); break;
+    case 8: hh_factor_blocked<8>(A, ld, mr, nc, tau, Tbuf, Tg, scratch, xch, pub); break;
+    default: hh_factor_unblocked(A, ld, mr, nc, tau, red); break;
+  }
 }
 
 // load rows [r0, r0+mr) x cols [0, nc) of a row-major global matrix (pitch gld) into smem (pitch ld)
