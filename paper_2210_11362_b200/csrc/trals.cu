@@ -850,12 +850,14 @@ __device__ __forceinline__ int chol8_factor_block(const double* a, int ld, int p
       u[r][c] = v;
     }
   int bad = 0;
+  double rks[8];  // rsqrt of the pivots = the diagonal of U^{-1}
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
     const double dk = u[k][k];
     const bool ok = bad == 0 && dk > 0.0;
     if (bad == 0 && !ok) bad = k + 1;
     const double rk = rsqrt(ok ? dk : 1.0);
+    rks[k] = rk;
     u[k][k] = dk * rk;
 #pragma unroll
     for (int c = k + 1; c < 8; ++c) u[k][c] *= rk;
@@ -876,7 +878,7 @@ __device__ __forceinline__ int chol8_factor_block(const double* a, int ld, int p
   // in-place W = U^{-1} (upper), column by column, rows top-down
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
-    const double wjj = 1.0 / u[j][j];
+    const double wjj = rks[j];  // 1 / u_jj = 1 / sqrt(d_j)
 #pragma unroll
     for (int i = 0; i < j; ++i) {
       double acc = 0.0;
