@@ -1311,7 +1311,7 @@ __global__ void __launch_bounds__(256) fused_solve_kernel(const double* __restri
   // ---------------- forward ----------------
   for (int b = 0; b < nblk; ++b) {
     const int j0 = b * kBlkNB;
-    double acc0 = 0.0, acc1 = 0.0;
+    double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;  // two independent DMMA chains
     const int nk = j0 / kBlkNB;  // K chunks of 64 rows of U
     const double* Wb = aux + static_cast<int64_t>(b) * 2 * kBlkNB * kBlkNB;
     // chunks: U[kc*64 .. +64][j0 .. j0+64] for kc < nk, then W_b
@@ -1329,25 +1329,31 @@ __global__ void __launch_bounds__(256) fused_solve_kernel(const double* __restri
       if (kc < nk) {
         // acc += Y[:, kc*64 .. +64] * U-block
 #pragma unroll 4
-        for (int k4 = 0; k4 < kBlkNB; k4 += 4) {
+        for (int k4 = 0; k4 < kBlkNB; k4 += 8) {
           const double a = Ys[fr * ldr + kc * kBlkNB + k4 + fk];
           const double bb = B[(k4 + fk) * kFsLd + warp * 8 + fr];
+          const double a2 = Ys[fr * ldr + kc * kBlkNB + k4 + 4 + fk];
+          const double bb2 = B[(k4 + 4 + fk) * kFsLd + warp * 8 + fr];
           trals::dmma884(acc0, acc1, a, bb);
+          trals::dmma884(acc2, acc3, a2, bb2);
         }
       } else {
         // R_b -= acc, then Y_b = R_b W_b
-        Rs[fr * ldr + j0 + warp * 8 + 2 * fk] -= acc0;
-        Rs[fr * ldr + j0 + warp * 8 + 2 * fk + 1] -= acc1;
+        Rs[fr * ldr + j0 + warp * 8 + 2 * fk] -= acc0 + acc2;
+        Rs[fr * ldr + j0 + warp * 8 + 2 * fk + 1] -= acc1 + acc3;
         __syncthreads();
-        double y0 = 0.0, y1 = 0.0;
+        double y0 = 0.0, y1 = 0.0, y2 = 0.0, y3 = 0.0;
 #pragma unroll 4
-        for (int k4 = 0; k4 < kBlkNB; k4 += 4) {
+        for (int k4 = 0; k4 < kBlkNB; k4 += 8) {
           const double a = Rs[fr * ldr + j0 + k4 + fk];
           const double bb = B[(k4 + fk) * kFsLd + warp * 8 + fr];
+          const double a2 = Rs[fr * ldr + j0 + k4 + 4 + fk];
+          const double bb2 = B[(k4 + 4 + fk) * kFsLd + warp * 8 + fr];
           trals::dmma884(y0, y1, a, bb);
+          trals::dmma884(y2, y3, a2, bb2);
         }
-        Ys[fr * ldr + j0 + warp * 8 + 2 * fk] = y0;
-        Ys[fr * ldr + j0 + warp * 8 + 2 * fk + 1] = y1;
+        Ys[fr * ldr + j0 + warp * 8 + 2 * fk] = y0 + y2;
+        Ys[fr * ldr + j0 + warp * 8 + 2 * fk + 1] = y1 + y3;
       }
       __syncthreads();
     }
@@ -1355,7 +1361,7 @@ __global__ void __launch_bounds__(256) fused_solve_kernel(const double* __restri
   // ---------------- backward (Z overwrites Rs) ----------------
   for (int b = nblk - 1; b >= 0; --b) {
     const int j0 = b * kBlkNB, j1 = j0 + kBlkNB;
-    double acc0 = 0.0, acc1 = 0.0;
+    double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
     const int nk = (mp - j1) / kBlkNB;  // K chunks: L rows j1.. (blocks b+1 .. nblk-1)
     const double* WTb = aux + static_cast<int64_t>(b) * 2 * kBlkNB * kBlkNB + kBlkNB * kBlkNB;
     stage(nk > 0 ? L : WTb, nk > 0 ? m : kBlkNB, nk > 0 ? j1 : 0, nk > 0 ? j0 : 0, nk > 0 ? m : kBlkNB,
@@ -1373,25 +1379,31 @@ __global__ void __launch_bounds__(256) fused_solve_kernel(const double* __restri
       if (kc < nk) {
         const int kb = j1 + kc * kBlkNB;
 #pragma unroll 4
-        for (int k4 = 0; k4 < kBlkNB; k4 += 4) {
+        for (int k4 = 0; k4 < kBlkNB; k4 += 8) {
           const double a = Rs[fr * ldr + kb + k4 + fk];  // Z_{>b}
           const double bb = B[(k4 + fk) * kFsLd + warp * 8 + fr];
+          const double a2 = Rs[fr * ldr + kb + k4 + 4 + fk];
+          const double bb2 = B[(k4 + 4 + fk) * kFsLd + warp * 8 + fr];
           trals::dmma884(acc0, acc1, a, bb);
+          trals::dmma884(acc2, acc3, a2, bb2);
         }
       } else {
         // T_b = Y_b - acc (kept in Ys), Z_b = T_b W_b^T -> Rs
-        Ys[fr * ldr + j0 + warp * 8 + 2 * fk] -= acc0;
-        Ys[fr * ldr + j0 + warp * 8 + 2 * fk + 1] -= acc1;
+        Ys[fr * ldr + j0 + warp * 8 + 2 * fk] -= acc0 + acc2;
+        Ys[fr * ldr + j0 + warp * 8 + 2 * fk + 1] -= acc1 + acc3;
         __syncthreads();
-        double z0 = 0.0, z1 = 0.0;
+        double z0 = 0.0, z1 = 0.0, z2 = 0.0, z3 = 0.0;
 #pragma unroll 4
-        for (int k4 = 0; k4 < kBlkNB; k4 += 4) {
+        for (int k4 = 0; k4 < kBlkNB; k4 += 8) {
           const double a = Ys[fr * ldr + j0 + k4 + fk];
           const double bb = B[(k4 + fk) * kFsLd + warp * 8 + fr];
+          const double a2 = Ys[fr * ldr + j0 + k4 + 4 + fk];
+          const double bb2 = B[(k4 + 4 + fk) * kFsLd + warp * 8 + fr];
           trals::dmma884(z0, z1, a, bb);
+          trals::dmma884(z2, z3, a2, bb2);
         }
-        Rs[fr * ldr + j0 + warp * 8 + 2 * fk] = z0;
-        Rs[fr * ldr + j0 + warp * 8 + 2 * fk + 1] = z1;
+        Rs[fr * ldr + j0 + warp * 8 + 2 * fk] = z0 + z2;
+        Rs[fr * ldr + j0 + warp * 8 + 2 * fk + 1] = z1 + z3;
       }
       __syncthreads();
     }
