@@ -1273,18 +1273,19 @@ int blocked_cholesky(const double* S, int m, double* U, double* L, double* aux, 
 // inverses stream through a cp.async double buffer; warp w owns columns
 // [8w, 8w+8) of the current 64-column block.
 constexpr int kFsRows = 8;
-constexpr int kFsLd = kBlkNB + 4;  // staged 64x64 pitch (conflict-free B fragments)
 
 __global__ void __launch_bounds__(256) fused_solve_kernel(const double* __restrict__ U, const double* __restrict__ L,
                                                           const double* __restrict__ aux, int m,
                                                           const double* __restrict__ Mr, int64_t rows,
                                                           double* __restrict__ Z) {
+  // Operand blocks are read straight from L2 as DMMA fragments (each warp its own 8
+  // columns, all 16 loads of a 64-k chunk issued before the MMAs): no staging and no
+  // CTA barrier per chunk, two per 64-column block (R_b complete; Y_b / Z_b published).
   extern __shared__ __align__(16) double fs[];
   const int mp = ((m + kBlkNB - 1) / kBlkNB) * kBlkNB;
   const int ldr = mp + 4;
-  double* Rs = fs;                       // [8][ldr] running rhs, later Z
-  double* Ys = Rs + kFsRows * ldr;       // [8][ldr] forward solution
-  double* Bst = Ys + kFsRows * ldr;      // [2][64][kFsLd] staged operand blocks
+  double* Rs = fs;                  // [8][ldr] running rhs, later Z
+  double* Ys = Rs + kFsRows * ldr;  // [8][ldr] forward solution
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int fr = lane >> 2, fk = lane & 3;
   const int64_t row0 = static_cast<int64_t>(blockIdx.x) * kFsRows;
@@ -1294,119 +1295,54 @@ __global__ void __launch_bounds__(256) fused_solve_kernel(const double* __restri
     Rs[t] = (row0 + r < rows && c < m) ? Mr[(row0 + r) * m + c] : 0.0;
     Ys[t] = 0.0;
   }
-  // stage a 64x64 block src[(k0 + kk) * lds + c0 + c] (zero outside [0,m)^2) into buffer `buf`
-  auto stage = [&](const double* src, int lds, int k0, int c0, int limk, int limc, int buf) {
-    double* dst = Bst + buf * kBlkNB * kFsLd;
-    for (int t = tid; t < kBlkNB * (kBlkNB / 2); t += blockDim.x) {
-      const int kk = t / (kBlkNB / 2), c = (t - kk * (kBlkNB / 2)) * 2;
-      const int gk = k0 + kk, gc = c0 + c;
-      const int valid = (gk < limk) ? max(0, min(2, limc - gc)) : 0;
-      const double* p = valid ? src + static_cast<int64_t>(gk) * lds + gc : src;
-      trals::cp_async_zfill(dst + kk * kFsLd + c, p, valid * 8, (lds % 2 == 0) ? 16 : 8);
-      if (lds % 2 != 0) trals::cp_async_zfill(dst + kk * kFsLd + c + 1, valid > 1 ? p + 1 : src, valid > 1 ? 8 : 0, 8);
-    }
-    trals::cp_async_commit();
-  };
   __syncthreads();
-  // ---------------- forward ----------------
+  // acc (+)= Xs[:, xoff .. xoff+64] * G[k0 .. k0+64][col] for this warp's column col (G row-major,
+  // pitch ldg, zero outside [0, limk) x [0, limc)); two DMMA chains
+  auto chunk = [&](const double* Xs, int xoff, const double* G, int64_t ldg, int k0, int col, int limk, int limc,
+                   double& a0, double& a1, double& a2, double& a3) {
+    double bv[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int kk = k0 + 4 * q + fk;
+      bv[q] = (kk < limk && col < limc) ? __ldg(G + static_cast<int64_t>(kk) * ldg + col) : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < 16; q += 2) {
+      trals::dmma884(a0, a1, Xs[fr * ldr + xoff + 4 * q + fk], bv[q]);
+      trals::dmma884(a2, a3, Xs[fr * ldr + xoff + 4 * q + 4 + fk], bv[q + 1]);
+    }
+  };
+  // ---------------- forward: Y_b = (R_b - Y_{<b} U_{<b,b}) W_b ----------------
   for (int b = 0; b < nblk; ++b) {
     const int j0 = b * kBlkNB;
-    double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;  // two independent DMMA chains
-    const int nk = j0 / kBlkNB;  // K chunks of 64 rows of U
+    const int col = j0 + warp * 8 + fr;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    for (int kc = 0; kc < b; ++kc) chunk(Ys, kc * kBlkNB, U, m, kc * kBlkNB, col, m, m, a0, a1, a2, a3);
+    Rs[fr * ldr + j0 + warp * 8 + 2 * fk] -= a0 + a2;
+    Rs[fr * ldr + j0 + warp * 8 + 2 * fk + 1] -= a1 + a3;
+    __syncthreads();
     const double* Wb = aux + static_cast<int64_t>(b) * 2 * kBlkNB * kBlkNB;
-    // chunks: U[kc*64 .. +64][j0 .. j0+64] for kc < nk, then W_b
-    stage(nk > 0 ? U : Wb, nk > 0 ? m : kBlkNB, 0, nk > 0 ? j0 : 0, nk > 0 ? m : kBlkNB, nk > 0 ? m : kBlkNB, 0);
-    for (int kc = 0; kc <= nk; ++kc) {
-      if (kc + 1 <= nk) {
-        if (kc + 1 < nk) stage(U, m, (kc + 1) * kBlkNB, j0, m, m, (kc + 1) & 1);
-        else stage(Wb, kBlkNB, 0, 0, kBlkNB, kBlkNB, (kc + 1) & 1);
-        trals::cp_async_wait<1>();
-      } else {
-        trals::cp_async_wait<0>();
-      }
-      __syncthreads();
-      const double* B = Bst + (kc & 1) * kBlkNB * kFsLd;
-      if (kc < nk) {
-        // acc += Y[:, kc*64 .. +64] * U-block
-#pragma unroll 4
-        for (int k4 = 0; k4 < kBlkNB; k4 += 8) {
-          const double a = Ys[fr * ldr + kc * kBlkNB + k4 + fk];
-          const double bb = B[(k4 + fk) * kFsLd + warp * 8 + fr];
-          const double a2 = Ys[fr * ldr + kc * kBlkNB + k4 + 4 + fk];
-          const double bb2 = B[(k4 + 4 + fk) * kFsLd + warp * 8 + fr];
-          trals::dmma884(acc0, acc1, a, bb);
-          trals::dmma884(acc2, acc3, a2, bb2);
-        }
-      } else {
-        // R_b -= acc, then Y_b = R_b W_b
-        Rs[fr * ldr + j0 + warp * 8 + 2 * fk] -= acc0 + acc2;
-        Rs[fr * ldr + j0 + warp * 8 + 2 * fk + 1] -= acc1 + acc3;
-        __syncthreads();
-        double y0 = 0.0, y1 = 0.0, y2 = 0.0, y3 = 0.0;
-#pragma unroll 4
-        for (int k4 = 0; k4 < kBlkNB; k4 += 8) {
-          const double a = Rs[fr * ldr + j0 + k4 + fk];
-          const double bb = B[(k4 + fk) * kFsLd + warp * 8 + fr];
-          const double a2 = Rs[fr * ldr + j0 + k4 + 4 + fk];
-          const double bb2 = B[(k4 + 4 + fk) * kFsLd + warp * 8 + fr];
-          trals::dmma884(y0, y1, a, bb);
-          trals::dmma884(y2, y3, a2, bb2);
-        }
-        Ys[fr * ldr + j0 + warp * 8 + 2 * fk] = y0 + y2;
-        Ys[fr * ldr + j0 + warp * 8 + 2 * fk + 1] = y1 + y3;
-      }
-      __syncthreads();
-    }
+    double y0 = 0.0, y1 = 0.0, y2 = 0.0, y3 = 0.0;
+    chunk(Rs, j0, Wb, kBlkNB, 0, warp * 8 + fr, kBlkNB, kBlkNB, y0, y1, y2, y3);
+    Ys[fr * ldr + j0 + warp * 8 + 2 * fk] = y0 + y2;
+    Ys[fr * ldr + j0 + warp * 8 + 2 * fk + 1] = y1 + y3;
+    __syncthreads();
   }
-  // ---------------- backward (Z overwrites Rs) ----------------
+  // ---------------- backward (Z overwrites Rs): Z_b = (Y_b - Z_{>b} L_{>b,b}) W_b^T ----------------
   for (int b = nblk - 1; b >= 0; --b) {
     const int j0 = b * kBlkNB, j1 = j0 + kBlkNB;
-    double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
-    const int nk = (mp - j1) / kBlkNB;  // K chunks: L rows j1.. (blocks b+1 .. nblk-1)
+    const int col = j0 + warp * 8 + fr;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    for (int kb = j1; kb < mp; kb += kBlkNB) chunk(Rs, kb, L, m, kb, col, m, m, a0, a1, a2, a3);
+    Ys[fr * ldr + j0 + warp * 8 + 2 * fk] -= a0 + a2;
+    Ys[fr * ldr + j0 + warp * 8 + 2 * fk + 1] -= a1 + a3;
+    __syncthreads();
     const double* WTb = aux + static_cast<int64_t>(b) * 2 * kBlkNB * kBlkNB + kBlkNB * kBlkNB;
-    stage(nk > 0 ? L : WTb, nk > 0 ? m : kBlkNB, nk > 0 ? j1 : 0, nk > 0 ? j0 : 0, nk > 0 ? m : kBlkNB,
-          nk > 0 ? m : kBlkNB, 0);
-    for (int kc = 0; kc <= nk; ++kc) {
-      if (kc + 1 <= nk) {
-        if (kc + 1 < nk) stage(L, m, j1 + (kc + 1) * kBlkNB, j0, m, m, (kc + 1) & 1);
-        else stage(WTb, kBlkNB, 0, 0, kBlkNB, kBlkNB, (kc + 1) & 1);
-        trals::cp_async_wait<1>();
-      } else {
-        trals::cp_async_wait<0>();
-      }
-      __syncthreads();
-      const double* B = Bst + (kc & 1) * kBlkNB * kFsLd;
-      if (kc < nk) {
-        const int kb = j1 + kc * kBlkNB;
-#pragma unroll 4
-        for (int k4 = 0; k4 < kBlkNB; k4 += 8) {
-          const double a = Rs[fr * ldr + kb + k4 + fk];  // Z_{>b}
-          const double bb = B[(k4 + fk) * kFsLd + warp * 8 + fr];
-          const double a2 = Rs[fr * ldr + kb + k4 + 4 + fk];
-          const double bb2 = B[(k4 + 4 + fk) * kFsLd + warp * 8 + fr];
-          trals::dmma884(acc0, acc1, a, bb);
-          trals::dmma884(acc2, acc3, a2, bb2);
-        }
-      } else {
-        // T_b = Y_b - acc (kept in Ys), Z_b = T_b W_b^T -> Rs
-        Ys[fr * ldr + j0 + warp * 8 + 2 * fk] -= acc0 + acc2;
-        Ys[fr * ldr + j0 + warp * 8 + 2 * fk + 1] -= acc1 + acc3;
-        __syncthreads();
-        double z0 = 0.0, z1 = 0.0, z2 = 0.0, z3 = 0.0;
-#pragma unroll 4
-        for (int k4 = 0; k4 < kBlkNB; k4 += 8) {
-          const double a = Ys[fr * ldr + j0 + k4 + fk];
-          const double bb = B[(k4 + fk) * kFsLd + warp * 8 + fr];
-          const double a2 = Ys[fr * ldr + j0 + k4 + 4 + fk];
-          const double bb2 = B[(k4 + 4 + fk) * kFsLd + warp * 8 + fr];
-          trals::dmma884(z0, z1, a, bb);
-          trals::dmma884(z2, z3, a2, bb2);
-        }
-        Rs[fr * ldr + j0 + warp * 8 + 2 * fk] = z0 + z2;
-        Rs[fr * ldr + j0 + warp * 8 + 2 * fk + 1] = z1 + z3;
-      }
-      __syncthreads();
-    }
+    double z0 = 0.0, z1 = 0.0, z2 = 0.0, z3 = 0.0;
+    chunk(Ys, j0, WTb, kBlkNB, 0, warp * 8 + fr, kBlkNB, kBlkNB, z0, z1, z2, z3);
+    Rs[fr * ldr + j0 + warp * 8 + 2 * fk] = z0 + z2;
+    Rs[fr * ldr + j0 + warp * 8 + 2 * fk + 1] = z1 + z3;
+    __syncthreads();
   }
   for (int t = tid; t < kFsRows * m; t += blockDim.x) {
     const int r = t / m, c = t - r * m;
@@ -1416,7 +1352,7 @@ __global__ void __launch_bounds__(256) fused_solve_kernel(const double* __restri
 
 size_t fused_solve_smem(int m) {
   const int mp = ((m + kBlkNB - 1) / kBlkNB) * kBlkNB;
-  return sizeof(double) * (2 * kFsRows * (mp + 4) + 2 * kBlkNB * kFsLd);
+  return sizeof(double) * (2 * kFsRows * (mp + 4));
 }
 
 // Z S = M, S = U^T U:  Y U = M (forward), Z U^T = Y (backward), 64-column blocks
