@@ -324,7 +324,9 @@ __device__ __forceinline__ void oz_for_tiles(const OzArgs& g, F&& body) {
   }
 }
 
-template <int BN, class SC>
+// RES: residual mode (exact error) compiled in only where used -- its per-element loads and
+// branches cost the short-K tiles of the plain product ~10 % (c3) when merely predicated off
+template <int BN, class SC, bool RES = false>
 __global__ void __launch_bounds__(OzTile<BN, SC>::THREADS, 1)
 oz8_kernel(const __grid_constant__ OzArgs g) {
   // Persistent: CTA b takes tiles b, b + gridDim.x, ...; the smem ring runs across
@@ -521,7 +523,7 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
           for (int k = 0; k < kOzBM / 8; ++k) {
             const int rr = quad * 2 + (lane >> 4) + 8 * k;
             pv[k] = (second && nok && rr < rows) ? __ldcg(g.ws + static_cast<int64_t>(m0 + rr) * g.N + n) : 0.0;
-            xv[k] = (g.rpart && nok && rr < rows) ? __ldcs(g.X + static_cast<int64_t>(m0 + rr) * g.ldx + n) : 0.0;
+            xv[k] = (RES && nok && rr < rows) ? __ldcs(g.X + static_cast<int64_t>(m0 + rr) * g.ldx + n) : 0.0;
           }
 #pragma unroll
           for (int k = 0; k < kOzBM / 8; ++k) {
@@ -530,13 +532,13 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
             const uint32_t mm = static_cast<uint32_t>(m0 + rr);
             const int64_t roff = static_cast<int64_t>(mm / M2) * sm1 + static_cast<int64_t>(mm % M2) * sm2;
             const double o = otile[rr * T::OUT_LD + (lane & 15)] * sb + pv[k];
-            if (g.rpart) {
+            if constexpr (RES) {
               if (nok) {
                 const double d = xv[k] - o;
                 rsum = fma(d, d, rsum);
               }
-            } else if (nok) {
-              base[roff + coff] = o;
+            } else {
+              if (nok) base[roff + coff] = o;
             }
           }
           asm volatile("bar.sync 1, 128;\n" ::: "memory");
@@ -576,7 +578,7 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
       }
       ++it;
     });
-    if (g.rpart) {  // fixed-order CTA partial: warp shuffles, then the 4 warps in order
+    if constexpr (RES) {  // fixed-order CTA partial: warp shuffles, then the 4 warps in order
       for (int o = 16; o > 0; o >>= 1) rsum += __shfl_xor_sync(0xffffffffu, rsum, o);
       double* red = otile;  // free now
       asm volatile("bar.sync 1, 128;\n" ::: "memory");

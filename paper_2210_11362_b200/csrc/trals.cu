@@ -570,10 +570,10 @@ int launch_colmax(const T* x, int64_t rows, int64_t cols, int64_t ld, double* ou
   return launch_status();
 }
 
-template <int BN, class SC>
+template <int BN, class SC, bool RES = false>
 int launch_oz(const trals::OzArgs& g, int grid, cudaStream_t s) {
   using T = trals::OzTile<BN, SC>;
-  auto kern = trals::oz8_kernel<BN, SC>;
+  auto kern = trals::oz8_kernel<BN, SC, RES>;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(T::SMEM));
@@ -2866,7 +2866,7 @@ int trals_residual_oz64(const double* X, int64_t pre, int64_t post, const double
   const int64_t tiles = static_cast<int64_t>(g.mtiles) * g.ntiles;
   if (tiles > INT32_MAX) return TRALS_ERR_UNSUPPORTED;
   const int grid = static_cast<int>(std::min<int64_t>(tiles, kSMs));
-  if (int st = launch_oz<kResBN, SC>(g, grid, s)) return st;
+  if (int st = launch_oz<kResBN, SC, true>(g, grid, s)) return st;
   residual_final_kernel<<<1, 1024, 0, s>>>(ws + w.part, grid, xnorm2, out);
   return launch_status();
 }
