@@ -489,7 +489,11 @@ inline trals::OzRowTiles oz_a_tiles(int64_t rows) { return trals::OzRowTiles::fi
 // the narrower tiles measured slower at c4: 1965 vs 2040 sweeps/s)
 constexpr int64_t kOzShortK = 8192;
 template <class SC>
-inline int oz_bn(int64_t K) { return (SC::BAL && K < kOzShortK) ? 32 : kOzBN; }
+inline int oz_bn(int64_t K) {
+  static int64_t short_k = -1;  // TRALS_OZ_SHORT_K (experiments) overrides kOzShortK
+  if (short_k < 0) short_k = std::getenv("TRALS_OZ_SHORT_K") ? std::atoll(std::getenv("TRALS_OZ_SHORT_K")) : kOzShortK;
+  return (SC::BAL && K < short_k) ? 32 : kOzBN;
+}
 // TRALS_OZ_FIXED_TILES=1 (experiments): every n-tile kOzBN wide, the last one zero padded
 inline trals::OzRowTiles oz_b_tiles(int64_t n, int bn = kOzBN) {
   static int fixed = -1;
