@@ -143,10 +143,14 @@ struct OzRowTiles {
     const int n = static_cast<int>((rows + w - 1) / w);
     return {n, 0, w, w};
   }
-  static OzRowTiles balanced(int64_t rows, int wmax) {
-    const int n = static_cast<int>((rows + wmax - 1) / wmax);
+  // mult > 1: the tile count is rounded up to a multiple of mult (cluster groups of n-tiles);
+  // returns ntiles = 0 when that leaves a tile without a 16-row unit
+  static OzRowTiles balanced(int64_t rows, int wmax, int mult = 1) {
+    int n = static_cast<int>((rows + wmax - 1) / wmax);
+    n = (n + mult - 1) / mult * mult;
     const int units = static_cast<int>((rows + 15) / 16);
     const int q = units / n, big = units % n;
+    if (q == 0) return {0, 0, 16, 16};
     return {n, big, 16 * (q + 1), 16 * q};
   }
 };
@@ -248,6 +252,38 @@ __device__ __forceinline__ void oz_commit_warp(uint64_t* bar) {
       : "memory");
 }
 
+// cluster variants: the bulk copy lands at the same shared-memory offset in every CTA of
+// `mask` and signals each one's mbarrier at the same offset; the commit arrives on the
+// mbarrier of every CTA in `mask`
+__device__ __forceinline__ void bulk_load_mc(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                             uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], "
+      "%4;\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar)), "h"(mask)
+      : "memory");
+}
+
+__device__ __forceinline__ void oz_commit_mc_warp(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}\n" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+
 __device__ __forceinline__ void oz_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar))
                : "memory");
@@ -305,6 +341,19 @@ __device__ __forceinline__ void oz_issue_stage(uint32_t tmem, uint64_t da, uint6
 // shared A stages from L2 together.  (Measured at c5, ncu: widths mixed inside a round
 // let the CTAs drift apart, 21 GB of DRAM reads per launch instead of 11; rounds cut to
 // whole m-tile groups were slower still.)
+// Cluster schedule (CN > 1): a cluster of CN CTAs runs the CN consecutive n-tiles of one
+// (split, m-tile) together -- CTA rank r the n-tile group * CN + r -- sharing its A stages
+// by multicast; clusters stride over the (split, m-tile, group) units.
+template <int CN, class F>
+__device__ __forceinline__ void oz_for_tiles_cl(const OzArgs& g, int crank, F&& body) {
+  const int groups = g.ntiles / CN, per_split = g.mtiles * groups, total = per_split * g.splits;
+  const int cid = blockIdx.x / CN, ncl = gridDim.x / CN;
+  for (int u = cid; u < total; u += ncl) {
+    const int rem = u % per_split;
+    body(u / per_split, rem / groups, (rem % groups) * CN + crank);
+  }
+}
+
 template <class F>
 __device__ __forceinline__ void oz_for_tiles(const OzArgs& g, F&& body) {
   const int per_split = g.mtiles * g.ntiles, total = per_split * g.splits;
@@ -326,7 +375,10 @@ __device__ __forceinline__ void oz_for_tiles(const OzArgs& g, F&& body) {
 
 // RES: residual mode (exact error) compiled in only where used -- its per-element loads and
 // branches cost the short-K tiles of the plain product ~10 % (c3) when merely predicated off
-template <int BN, class SC, bool RES = false>
+// CN > 1: launched in clusters of CN along the n-tiles; every CTA loads D / CN of each A stage
+// and multicasts it to the cluster, its own B stage locally; a stage is free once all CN
+// CTAs' MMAs have read it (empty barriers count CN commits).
+template <int BN, class SC, bool RES = false, int CN = 1>
 __global__ void __launch_bounds__(OzTile<BN, SC>::THREADS, 1)
 oz8_kernel(const __grid_constant__ OzArgs g) {
   // Persistent: CTA b takes tiles b, b + gridDim.x, ...; the smem ring runs across
@@ -346,10 +398,13 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
 
   const int tid = threadIdx.x, lane = tid & 31;
   const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
+  const int crank = CN > 1 ? static_cast<int>(cluster_ctarank()) : 0;
+  constexpr uint16_t kMask = static_cast<uint16_t>((1u << CN) - 1u);
+  static_assert(SC::D % CN == 0, "A planes must split evenly over the cluster");
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(full + s, 1);
-      mbar_init(empty + s, 1);
+      mbar_init(empty + s, CN);
     }
     for (int b = 0; b < T::ACC; ++b) {
       mbar_init(acc_full + b, 1);
@@ -364,8 +419,13 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
+  if constexpr (CN > 1) cluster_sync_all();  // peers' barriers are initialised before any multicast
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const uint32_t tmem = *tmem_slot;
+  auto for_tiles = [&](auto&& body) {
+    if constexpr (CN > 1) oz_for_tiles_cl<CN>(g, crank, body);
+    else oz_for_tiles(g, body);
+  };
 
   auto tile_k = [&](int split, int64_t& kbeg, int& ktiles) {
     kbeg = static_cast<int64_t>(split) * g.kchunk;
@@ -377,7 +437,7 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
     // ------------------------------ bulk-copy producer ------------------------------
     if (lane == 0) {
       uint32_t gk = 0;
-      oz_for_tiles(g, [&](int split, int mt, int nt) {
+      for_tiles([&](int split, int mt, int nt) {
         int64_t kbeg;
         int ktiles;
         tile_k(split, kbeg, ktiles);
@@ -396,8 +456,14 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
           mbar_expect_tx(full + s, D * T::A_PLANE + bbytes);
           const int kr = kt + rot < ktiles ? kt + rot : kt + rot - ktiles;
           const int64_t kb = kbeg / kOzBK + kr;
-          bulk_load(st, g.ad + (static_cast<int64_t>(mt) * g.kblocks + kb) * (D * T::A_PLANE), D * T::A_PLANE,
-                    full + s);
+          const int8_t* asrc = g.ad + (static_cast<int64_t>(mt) * g.kblocks + kb) * (D * T::A_PLANE);
+          if constexpr (CN > 1) {
+#pragma unroll
+            for (int pl = crank * (D / CN); pl < (crank + 1) * (D / CN); ++pl)
+              bulk_load_mc(st + pl * T::A_PLANE, asrc + pl * T::A_PLANE, T::A_PLANE, full + s, kMask);
+          } else {
+            bulk_load(st, asrc, D * T::A_PLANE, full + s);
+          }
           bulk_load(st + D * T::A_PLANE, g.bd + bstart + kb * bbytes, bbytes, full + s);
         }
       });
@@ -407,7 +473,7 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
     // The whole warp runs this loop with warp-uniform values (oz_issue_stage).
     const uint64_t dA0 = oz_desc(smem_u32(sm)), dB0 = oz_desc(smem_u32(sm) + D * T::A_PLANE);
     uint32_t gk = 0, it = 0;
-    oz_for_tiles(g, [&](int split, int, int nt) {
+    for_tiles([&](int split, int, int nt) {
       int64_t kbeg;
       int ktiles;
       tile_k(split, kbeg, ktiles);
@@ -432,7 +498,9 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
             if (bw == 32) oz_issue_stage<32, BN, D, LV>(tacc, da, db);
             else oz_issue_stage<16, BN, D, LV>(tacc, da, db);
           }
-          oz_commit_warp(empty + s);  // the stage is free once these MMAs have read it
+          // the stage is free once these MMAs (and, in a cluster, every peer's) have read it
+          if constexpr (CN > 1) oz_commit_mc_warp(empty + s, kMask);
+          else oz_commit_warp(empty + s);
         }
         __syncwarp();
       }
@@ -456,7 +524,7 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
       for (int b = 0; b < T::ACC; ++b) mbar_arrive(acc_empty + b);
     uint32_t it = 0;
     double rsum = 0.0;  // residual mode: this thread's squared residuals, in tile order
-    oz_for_tiles(g, [&](int split, int mt, int nt) {
+    for_tiles([&](int split, int mt, int nt) {
       int64_t kbeg;
       int ktiles;
       tile_k(split, kbeg, ktiles);
@@ -589,6 +657,7 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
+  if constexpr (CN > 1) cluster_sync_all();  // no CTA leaves while peers may still signal it
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(T::TMEM_COLS));

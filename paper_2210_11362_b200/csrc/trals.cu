@@ -495,10 +495,20 @@ inline int oz_bn(int64_t K) {
   return (SC::BAL && K < short_k) ? 32 : kOzBN;
 }
 // TRALS_OZ_FIXED_TILES=1 (experiments): every n-tile kOzBN wide, the last one zero padded
-inline trals::OzRowTiles oz_b_tiles(int64_t n, int bn = kOzBN) {
+inline trals::OzRowTiles oz_b_tiles(int64_t n, int bn = kOzBN, int cn = 1) {
   static int fixed = -1;
   if (fixed < 0) fixed = std::getenv("TRALS_OZ_FIXED_TILES") ? 1 : 0;
-  return fixed ? trals::OzRowTiles::fixed(n, bn) : trals::OzRowTiles::balanced(n, bn);
+  return fixed ? trals::OzRowTiles::fixed(n, bn) : trals::OzRowTiles::balanced(n, bn, cn);
+}
+// cluster size of the fp64 int8 product (A stages multicast over CN n-tiles); 1 = no cluster.
+// TRALS_OZ_CLUSTER (experiments) picks 2 or 4.
+template <class SC>
+inline int oz_cn(int64_t N, int bn) {
+  static int env = -1;
+  if (env < 0) env = std::getenv("TRALS_OZ_CLUSTER") ? std::atoi(std::getenv("TRALS_OZ_CLUSTER")) : 1;
+  const int cn = (env == 2 || env == 4) ? env : 1;
+  if (!SC::BAL || cn == 1) return 1;
+  return oz_b_tiles(N, bn, cn).ntiles > 0 ? cn : 1;
 }
 
 // split-K over a per-tile time model and never more than SC::KMAX k per CTA (int32
@@ -508,13 +518,14 @@ template <class SC>
 SplitPlan plan_split_oz(int64_t M, int64_t K, int64_t N) {
   const int64_t BK = trals::kOzBK;
   const int bn = oz_bn<SC>(K);
-  const int64_t tiles = ((M + trals::kOzBM - 1) / trals::kOzBM) * oz_b_tiles(N, bn).ntiles;
+  const int cn = oz_cn<SC>(N, bn);
+  const int64_t tiles = ((M + trals::kOzBM - 1) / trals::kOzBM) * oz_b_tiles(N, bn, cn).ntiles;
   const int64_t slots = kSMs;
   const int64_t smin = std::max<int64_t>(1, (K + SC::KMAX - 1) / SC::KMAX);
   const int64_t smax = std::max<int64_t>(smin, std::min<int64_t>(64, K / (4 * BK)));
   int pairs = 0;
   for (int a = 0; a < SC::D; ++a) pairs += std::min(SC::D, SC::LV - a);
-  const double t_tile = SC::BAL ? static_cast<double>(pairs) * trals::kOzBM * N / oz_b_tiles(N, bn).ntiles *
+  const double t_tile = SC::BAL ? static_cast<double>(pairs) * trals::kOzBM * N / oz_b_tiles(N, bn, cn).ntiles *
                                       static_cast<double>(K) /
                                       (8192.0 * 1.9e9)
                                 : 4.0 * trals::kOzBM * static_cast<double>(K) / (6.5e12 / slots);
@@ -549,10 +560,11 @@ OzWs oz_ws_layout(int64_t M, int64_t K, int64_t N) {
   OzWs w{};
   w.planes = 0;
   const int bn = oz_bn<SC>(K);
-  w.eb = w.planes + (oz_digits_bytes(oz_b_tiles(N, bn), K, SC::D) + 15) / 16 * 2;
+  const int cn = oz_cn<SC>(N, bn);
+  w.eb = w.planes + (oz_digits_bytes(oz_b_tiles(N, bn, cn), K, SC::D) + 15) / 16 * 2;
   w.mx = w.eb + (N + 3) / 4 * 2;
   w.flags = w.mx + (N + 1) / 2 * 2;
-  const int64_t tiles = ((M + trals::kOzBM - 1) / trals::kOzBM) * oz_b_tiles(N, bn).ntiles;
+  const int64_t tiles = ((M + trals::kOzBM - 1) / trals::kOzBM) * oz_b_tiles(N, bn, cn).ntiles;
   const bool fix = oz_fixup<SC>(sp, K);
   w.part = w.flags + (fix ? (2 * tiles + 1) / 2 + 1 : 0);
   w.total = w.part + (sp.splits > 1 ? (fix ? 1 : static_cast<int64_t>(sp.splits)) * M * N : 0);
@@ -574,17 +586,42 @@ int launch_colmax(const T* x, int64_t rows, int64_t cols, int64_t ld, double* ou
   return launch_status();
 }
 
-template <int BN, class SC, bool RES = false>
+template <int BN, class SC, bool RES = false, int CN = 1>
 int launch_oz(const trals::OzArgs& g, int grid, cudaStream_t s) {
   using T = trals::OzTile<BN, SC>;
-  auto kern = trals::oz8_kernel<BN, SC, RES>;
+  auto kern = trals::oz8_kernel<BN, SC, RES, CN>;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(T::SMEM));
     attr = true;
   }
-  kern<<<grid, T::THREADS, T::SMEM, s>>>(g);
-  return launch_status();
+  if constexpr (CN == 1) {
+    kern<<<grid, T::THREADS, T::SMEM, s>>>(g);
+    return launch_status();
+  } else {
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CN;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.blockDim = dim3(T::THREADS);
+    cfg.dynamicSmemBytes = T::SMEM;
+    cfg.stream = s;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    // as many whole clusters as the GPCs hold at once (persistent), no more than the work units
+    static int max_clusters = 0;
+    if (!max_clusters) {
+      cfg.gridDim = dim3(kSMs / CN * CN);
+      if (cudaOccupancyMaxActiveClusters(&max_clusters, kern, &cfg) != cudaSuccess || max_clusters < 1)
+        max_clusters = kSMs / CN;
+    }
+    const int units = (grid + CN - 1) / CN;
+    cfg.gridDim = dim3(static_cast<unsigned>(std::min(units, max_clusters) * CN));
+    if (cudaLaunchKernelEx(&cfg, kern, g) != cudaSuccess) return TRALS_ERR_CUDA;
+    return launch_status();
+  }
 }
 
 // C(m, n) = sum_k A[m][k] B[k][n]: A given as tiled digits [D x 128-row tiles] + row exponents ea[M],
@@ -602,8 +639,9 @@ int gemm_oz(const int8_t* ad, const int32_t* ea, int64_t M, int64_t K, int64_t N
   // B^T rows = columns of B: max over k, then tiled digits (transposed read)
   if (int st = launch_colmax<double>(B, K, N, ldb, bmx, s)) return st;
   const int bn = oz_bn<SC>(K);
+  const int cn = oz_cn<SC>(N, bn);
   {
-    const trals::OzRowTiles bt = oz_b_tiles(N, bn);
+    const trals::OzRowTiles bt = oz_b_tiles(N, bn, cn);
     dim3 grid(static_cast<unsigned>((K + 63) / 64), static_cast<unsigned>((bt.rows_pad() + 63) / 64));
     trals::oz_digits_tiled_t_kernel<double, SC><<<grid, 256, 0, s>>>(B, K, N, ldb, bmx, bd, bt, eb);
     if (int st = launch_status()) return st;
@@ -611,7 +649,7 @@ int gemm_oz(const int8_t* ad, const int32_t* ea, int64_t M, int64_t K, int64_t N
   trals::OzArgs g{};
   g.M = M; g.K = K; g.N = N; g.kchunk = sp.kchunk; g.splits = sp.splits;
   g.mtiles = static_cast<int>((M + trals::kOzBM - 1) / trals::kOzBM);
-  g.nt = oz_b_tiles(N, bn);
+  g.nt = oz_b_tiles(N, bn, cn);
   g.ntiles = g.nt.ntiles;
   static int norot = -1;  // TRALS_OZ_NOROT=1 (experiments): k blocks in natural order
   if (norot < 0) norot = std::getenv("TRALS_OZ_NOROT") ? 1 : 0;
@@ -629,7 +667,11 @@ int gemm_oz(const int8_t* ad, const int32_t* ea, int64_t M, int64_t K, int64_t N
   const int64_t tiles = static_cast<int64_t>(g.mtiles) * g.ntiles * sp.splits;
   if (tiles > INT32_MAX) return TRALS_ERR_UNSUPPORTED;
   const int grid = static_cast<int>(std::min<int64_t>(tiles, kSMs));
-  if (int st = bn == 32 ? launch_oz<32, SC>(g, grid, s) : launch_oz<kOzBN, SC>(g, grid, s)) return st;
+  int st;
+  if (cn == 4) st = bn == 32 ? launch_oz<32, SC, false, 4>(g, grid, s) : launch_oz<kOzBN, SC, false, 4>(g, grid, s);
+  else if (cn == 2) st = bn == 32 ? launch_oz<32, SC, false, 2>(g, grid, s) : launch_oz<kOzBN, SC, false, 2>(g, grid, s);
+  else st = bn == 32 ? launch_oz<32, SC>(g, grid, s) : launch_oz<kOzBN, SC>(g, grid, s);
+  if (st) return st;
   if (sp.splits > 1 && !g.fixup) {
     GemmArgs r{};
     r.P = 1; r.M = M; r.N = N; r.splits = sp.splits; r.ws = ws + w.part; r.C = C; r.cmap = cm; r.alpha = 1.0;
