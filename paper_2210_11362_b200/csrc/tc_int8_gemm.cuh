@@ -58,7 +58,7 @@
 
 namespace trals {
 
-constexpr int kOzBK = 64;        // int8 k per stage (one 64 B swizzle row)
+constexpr int kOzBK = 64;        // int8 k per stage of the fp32 scheme (one 64 B swizzle row)
 constexpr int kOzBM = 128;
 
 // Digit schemes.  D digit planes per operand, the LV lowest pair levels L = s + t
@@ -75,16 +75,21 @@ constexpr int kOzBM = 128;
 //     weighs 2^(-12-7L).  A level sums <= 8 pairs of 64^2 per k -> KMAX 61440.
 //     Measured against an extended-precision product: the same error as fp64 DMMA
 //     (tests/test_gpu_ops.py::test_env_oz64_accuracy).
-template <int D_, int LV_, bool BAL_, int64_t KMAX_>
+// BK: int8 k per pipeline stage and digit row: 64 (SWIZZLE_64B rows) for the fp32 scheme,
+// 32 (SWIZZLE_32B rows) for the fp64 one -- its 8-plane stages are twice as large, and at
+// 32 k four of them fit in flight (the short-K shapes, c3/c4, were DRAM-latency bound
+// with two 64-k stages: tensor pipe 33 % busy at c3)
+template <int D_, int LV_, bool BAL_, int64_t KMAX_, int BK_>
 struct OzScheme {
   static constexpr int D = D_;
   static constexpr int LV = LV_;
   static constexpr bool BAL = BAL_;
   static constexpr int OFF = BAL_ ? 12 : 14;  // 2^-OFF: weight of the level-0 pair
   static constexpr int64_t KMAX = KMAX_;
+  static constexpr int BK = BK_;
 };
-using OzF32 = OzScheme<4, 7, false, 32768>;
-using OzF64 = OzScheme<8, 8, true, 61440>;
+using OzF32 = OzScheme<4, 7, false, 32768, 64>;
+using OzF64 = OzScheme<8, 8, true, 61440, 32>;
 constexpr int kOzDigits = OzF32::D;  // (fp32 variant layout helpers)
 constexpr int kOzLevels = OzF32::LV;
 constexpr int64_t kOzKmax = OzF32::KMAX;
@@ -95,13 +100,14 @@ constexpr int64_t kOzKmax = OzF32::KMAX;
 template <int BN, class SC>
 struct OzTile {
   static constexpr int ACC = (512 / (SC::LV * BN)) >= 2 ? 2 : 1;
-  static constexpr int A_PLANE = kOzBM * kOzBK;  // 8 KB
-  static constexpr int B_PLANE = BN * kOzBK;
+  static constexpr int A_PLANE = kOzBM * SC::BK;  // 8 KB (BK 64) / 4 KB (BK 32)
+  static constexpr int B_PLANE = BN * SC::BK;
   static constexpr int STAGE = SC::D * (A_PLANE + B_PLANE);
-  // fp64 output staging: the whole 128 x BN tile when it fits beside >= 3 stages
-  // (TMEM is released before the global stores), else 16-column chunks
+  // fp64 output staging: the whole 128 x BN tile for the fp32 scheme (TMEM is released
+  // before the global stores), 16-column chunks for the fp64 one (deeper stage ring; the
+  // split-K fix-up and the residual epilogue live in the chunked path)
   static constexpr int FULL_OUT = kOzBM * (BN + 1) * 8;
-  static constexpr bool CHUNKED = (212 * 1024 - FULL_OUT) / STAGE < 3;
+  static constexpr bool CHUNKED = SC::BAL || (212 * 1024 - FULL_OUT) / STAGE < 3;
   static constexpr int OUT_COLS = CHUNKED ? 16 : BN;
   static constexpr int OUT_LD = OUT_COLS + 1;                 // odd: no bank conflicts
   static constexpr int OUT_BYTES = kOzBM * OUT_LD * 8;
@@ -186,14 +192,17 @@ struct OzArgs {
 
 // byte offset of (row r, k) inside the tiled digit layout of one plane block
 // (rows_per_tile rows x 64 B, SWIZZLE_64B)
+// byte offset of (row r, k) of one digit plane in the tiled layout: rows of bk bytes,
+// SWIZZLE_64B (bk 64: 16-byte chunk c of row r at c ^ ((r >> 1) & 3)) or SWIZZLE_32B
+// (bk 32: chunk c at c ^ ((r >> 2) & 1))
 __host__ __device__ __forceinline__ int64_t oz_tiled_offset(int64_t r, int64_t k, int plane, const OzRowTiles& rt,
-                                                            int64_t kblocks, int digits) {
+                                                            int64_t kblocks, int digits, int bk = 64) {
   int t, rr;
   rt.locate(r, t, rr);
   const int w = rt.width(t);
-  const int64_t kb = k >> 6, c = k & 63;
-  return rt.start(t) * kblocks * 64 * digits + (kb * digits + plane) * w * 64 + rr * 64 +
-         ((((c >> 4) ^ ((rr >> 1) & 3))) << 4) + (c & 15);
+  const int64_t kb = k / bk, c = k % bk;
+  const int64_t sw = bk == 64 ? ((c >> 4) ^ ((rr >> 1) & 3)) : ((c >> 4) ^ ((rr >> 2) & 1));
+  return rt.start(t) * kblocks * bk * digits + (kb * digits + plane) * w * bk + rr * bk + (sw << 4) + (c & 15);
 }
 
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -204,13 +213,15 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
 }
 
 // UMMA shared-memory descriptor (K-major, SWIZZLE_64B, version 1): 64 B rows, 8-row groups 512 B apart
+template <int BK = 64>
 __device__ __forceinline__ uint64_t oz_desc(uint32_t saddr) {
+  // K-major, version 1; BK 64: SWIZZLE_64B, 8-row groups 512 B apart; BK 32: SWIZZLE_32B, 256 B
   uint64_t d = 0;
   d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
-  d |= static_cast<uint64_t>(1) << 16;             // LBO (unused for swizzled K-major)
-  d |= static_cast<uint64_t>(512 >> 4) << 32;      // SBO
+  d |= static_cast<uint64_t>(1) << 16;                  // LBO (unused for swizzled K-major)
+  d |= static_cast<uint64_t>((8 * BK) >> 4) << 32;      // SBO
   d |= static_cast<uint64_t>(1) << 46;
-  d |= static_cast<uint64_t>(4) << 61;             // SWIZZLE_64B
+  d |= static_cast<uint64_t>(BK == 64 ? 4 : 6) << 61;   // SWIZZLE_64B / SWIZZLE_32B
   return d;
 }
 
@@ -316,12 +327,12 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
 // stacked operand -- so pair (s, t) lands in level block s + t (W columns each).  The
 // descriptors are linear in the smem address (start field = addr >> 4), so each MMA's
 // pair is the stage base plus a compile-time offset.
-template <int W, int BN, int D, int LV>
+template <int W, int BN, int D, int LV, int BK = 64>
 __device__ __forceinline__ void oz_issue_stage(uint32_t tmem, uint64_t da, uint64_t db) {
   constexpr int CH = 256 / W;
-  constexpr int A_PLANE = kOzBM * kOzBK, B_PLANE = W * kOzBK;
+  constexpr int A_PLANE = kOzBM * BK, B_PLANE = W * BK;
 #pragma unroll
-  for (int k = 0; k < kOzBK / 32; ++k)
+  for (int k = 0; k < BK / 32; ++k)
 #pragma unroll
     for (int sa = 0; sa < D; ++sa) {
       const int nb = (D < LV - sa) ? D : LV - sa;
@@ -430,7 +441,7 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
   auto tile_k = [&](int split, int64_t& kbeg, int& ktiles) {
     kbeg = static_cast<int64_t>(split) * g.kchunk;
     const int64_t kend = (g.K < kbeg + g.kchunk) ? g.K : kbeg + g.kchunk;
-    ktiles = kend > kbeg ? static_cast<int>((kend - kbeg + kOzBK - 1) / kOzBK) : 0;
+    ktiles = kend > kbeg ? static_cast<int>((kend - kbeg + SC::BK - 1) / SC::BK) : 0;
   };
 
   if (warp == 0) {
@@ -442,7 +453,7 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
         int ktiles;
         tile_k(split, kbeg, ktiles);
         const int bw = g.nt.width(nt);
-        const int64_t bstart = g.nt.start(nt) * g.kblocks * kOzBK * D;
+        const int64_t bstart = g.nt.start(nt) * g.kblocks * SC::BK * D;
         // k blocks in a rotated order (the int32 accumulation is exact, so the order is
         // free): the rotation follows the m-tile, so the CTAs that share an A tile (its
         // n-tiles run side by side) read it in step and hit L2, while different m-tiles
@@ -452,10 +463,10 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
           const uint32_t s = gk % S;
           if (gk >= S) mbar_wait(empty + s, ((gk / S) - 1) & 1);
           uint8_t* st = sm + s * T::STAGE;
-          const uint32_t bbytes = static_cast<uint32_t>(D * bw * kOzBK);
+          const uint32_t bbytes = static_cast<uint32_t>(D * bw * SC::BK);
           mbar_expect_tx(full + s, D * T::A_PLANE + bbytes);
           const int kr = kt + rot < ktiles ? kt + rot : kt + rot - ktiles;
-          const int64_t kb = kbeg / kOzBK + kr;
+          const int64_t kb = kbeg / SC::BK + kr;
           const int8_t* asrc = g.ad + (static_cast<int64_t>(mt) * g.kblocks + kb) * (D * T::A_PLANE);
           if constexpr (CN > 1) {
 #pragma unroll
@@ -471,7 +482,7 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
   } else if (warp == 1) {
     // ------------------------------ MMA issuer ------------------------------
     // The whole warp runs this loop with warp-uniform values (oz_issue_stage).
-    const uint64_t dA0 = oz_desc(smem_u32(sm)), dB0 = oz_desc(smem_u32(sm) + D * T::A_PLANE);
+    const uint64_t dA0 = oz_desc<SC::BK>(smem_u32(sm)), dB0 = oz_desc<SC::BK>(smem_u32(sm) + D * T::A_PLANE);
     uint32_t gk = 0, it = 0;
     for_tiles([&](int split, int, int nt) {
       int64_t kbeg;
@@ -490,13 +501,13 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
           const uint64_t da = dA0 + ((s * T::STAGE) >> 4), db = dB0 + ((s * T::STAGE) >> 4);
           // warp-uniform: the n-tile width fixes the MMA shapes (widths <= BN)
           if constexpr (BN >= 64) {
-            if (bw == 64) oz_issue_stage<64, BN, D, LV>(tacc, da, db);
-            else if (bw == 48) oz_issue_stage<48, BN, D, LV>(tacc, da, db);
-            else if (bw == 32) oz_issue_stage<32, BN, D, LV>(tacc, da, db);
-            else oz_issue_stage<16, BN, D, LV>(tacc, da, db);
+            if (bw == 64) oz_issue_stage<64, BN, D, LV, SC::BK>(tacc, da, db);
+            else if (bw == 48) oz_issue_stage<48, BN, D, LV, SC::BK>(tacc, da, db);
+            else if (bw == 32) oz_issue_stage<32, BN, D, LV, SC::BK>(tacc, da, db);
+            else oz_issue_stage<16, BN, D, LV, SC::BK>(tacc, da, db);
           } else {
-            if (bw == 32) oz_issue_stage<32, BN, D, LV>(tacc, da, db);
-            else oz_issue_stage<16, BN, D, LV>(tacc, da, db);
+            if (bw == 32) oz_issue_stage<32, BN, D, LV, SC::BK>(tacc, da, db);
+            else oz_issue_stage<16, BN, D, LV, SC::BK>(tacc, da, db);
           }
           // the stage is free once these MMAs (and, in a cluster, every peer's) have read it
           if constexpr (CN > 1) oz_commit_mc_warp(empty + s, kMask);
@@ -742,9 +753,9 @@ __global__ void __launch_bounds__(256) oz_digits_tiled_kernel(const Tin* __restr
                                                               int64_t ld_in, int transpose,
                                                               const double* __restrict__ mx, int8_t* __restrict__ out,
                                                               OzRowTiles rt, int32_t* __restrict__ exps) {
-  constexpr int D = SC::D;
+  constexpr int D = SC::D, BK = SC::BK;
   const int64_t out_rows = transpose ? cols : rows, K = transpose ? rows : cols;
-  const int64_t kblocks = (K + 63) / 64, kchunks = kblocks * 4;
+  const int64_t kblocks = (K + BK - 1) / BK, kchunks = kblocks * (BK / 16);
   const int64_t rows_pad = rt.rows_pad();
   const int64_t total = rows_pad * kchunks;
   for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
@@ -777,8 +788,8 @@ __global__ void __launch_bounds__(256) oz_digits_tiled_kernel(const Tin* __restr
     // plane d of a row sits width x 64 bytes after plane d - 1
     int tt, rr_;
     rt.locate(orow, tt, rr_);
-    const int64_t pstride = static_cast<int64_t>(rt.width(tt)) * 64;
-    const int64_t off0 = oz_tiled_offset(orow, ch * 16, 0, rt, kblocks, D);
+    const int64_t pstride = static_cast<int64_t>(rt.width(tt)) * BK;
+    const int64_t off0 = oz_tiled_offset(orow, ch * 16, 0, rt, kblocks, D, BK);
 #pragma unroll
     for (int d = 0; d < D; ++d)
       *reinterpret_cast<uint4*>(out + off0 + d * pstride) = make_uint4(w[d][0], w[d][1], w[d][2], w[d][3]);
@@ -796,10 +807,10 @@ __global__ void __launch_bounds__(256) oz_digits_tiled_t_kernel(const Tin* __res
                                                                 int64_t ld_in, const double* __restrict__ mx,
                                                                 int8_t* __restrict__ out, OzRowTiles rt,
                                                                 int32_t* __restrict__ exps) {
-  constexpr int D = SC::D;
+  constexpr int D = SC::D, BK = SC::BK;
   __shared__ double tile[64][65];
   const int64_t K = rows, out_rows = cols;
-  const int64_t kblocks = (K + 63) / 64;
+  const int64_t kblocks = (K + BK - 1) / BK;
   const int64_t n0 = static_cast<int64_t>(blockIdx.y) * 64, k0 = static_cast<int64_t>(blockIdx.x) * 64;
   const int tid = threadIdx.x;
   for (int e = tid; e < 64 * 64; e += 256) {
@@ -810,7 +821,7 @@ __global__ void __launch_bounds__(256) oz_digits_tiled_t_kernel(const Tin* __res
   __syncthreads();
   const int nl = tid >> 2, ch = tid & 3;
   const int64_t orow = n0 + nl;
-  if (orow >= rt.rows_pad()) return;
+  if (orow >= rt.rows_pad() || k0 + ch * 16 >= kblocks * BK) return;  // (BK 32: a 64-k tile may pass the layout)
   const bool rok = orow < out_rows;
   const int e = rok ? oz_exponent(mx[orow]) : 0;
   const double sc = ldexp(1.0, -e);
@@ -828,8 +839,8 @@ __global__ void __launch_bounds__(256) oz_digits_tiled_t_kernel(const Tin* __res
   }
   int tt, rr_;
   rt.locate(orow, tt, rr_);
-  const int64_t pstride = static_cast<int64_t>(rt.width(tt)) * 64;
-  const int64_t off0 = oz_tiled_offset(orow, k0 + ch * 16, 0, rt, kblocks, D);
+  const int64_t pstride = static_cast<int64_t>(rt.width(tt)) * BK;
+  const int64_t off0 = oz_tiled_offset(orow, k0 + ch * 16, 0, rt, kblocks, D, BK);
 #pragma unroll
   for (int d = 0; d < D; ++d)
     *reinterpret_cast<uint4*>(out + off0 + d * pstride) = make_uint4(w[d][0], w[d][1], w[d][2], w[d][3]);

@@ -478,9 +478,9 @@ int gemm_tc(const float* ahi, const float* alo, int64_t lda, int64_t M, int64_t 
 // the fp64 environment products (OzF64)
 // ---------------------------------------------------------------------------
 constexpr int kOzBN = 64;
-// bytes of a tiled digit layout: D planes x rows padded to the tiling x K padded to 64
-inline int64_t oz_digits_bytes(const trals::OzRowTiles& rt, int64_t k, int digits) {
-  return digits * rt.rows_pad() * ((k + 63) / 64 * 64);
+// bytes of a tiled digit layout: D planes x rows padded to the tiling x K padded to the stage k
+inline int64_t oz_digits_bytes(const trals::OzRowTiles& rt, int64_t k, int digits, int bk = 64) {
+  return digits * rt.rows_pad() * ((k + bk - 1) / bk * bk);
 }
 inline trals::OzRowTiles oz_a_tiles(int64_t rows) { return trals::OzRowTiles::fixed(rows, trals::kOzBM); }
 // n-tiles of at most 32 columns (two TMEM accumulator buffers with 8 digit levels) when the
@@ -516,7 +516,7 @@ inline int oz_cn(int64_t N, int bn) {
 // HBM share); fp64: tensor-bound (36 digit-pair MMAs at the int8 rate of one SM).
 template <class SC>
 SplitPlan plan_split_oz(int64_t M, int64_t K, int64_t N) {
-  const int64_t BK = trals::kOzBK;
+  const int64_t BK = SC::BK;
   const int bn = oz_bn<SC>(K);
   const int cn = oz_cn<SC>(N, bn);
   const int64_t tiles = ((M + trals::kOzBM - 1) / trals::kOzBM) * oz_b_tiles(N, bn, cn).ntiles;
@@ -561,7 +561,7 @@ OzWs oz_ws_layout(int64_t M, int64_t K, int64_t N) {
   w.planes = 0;
   const int bn = oz_bn<SC>(K);
   const int cn = oz_cn<SC>(N, bn);
-  w.eb = w.planes + (oz_digits_bytes(oz_b_tiles(N, bn, cn), K, SC::D) + 15) / 16 * 2;
+  w.eb = w.planes + (oz_digits_bytes(oz_b_tiles(N, bn, cn), K, SC::D, SC::BK) + 15) / 16 * 2;
   w.mx = w.eb + (N + 3) / 4 * 2;
   w.flags = w.mx + (N + 1) / 2 * 2;
   const int64_t tiles = ((M + trals::kOzBM - 1) / trals::kOzBM) * oz_b_tiles(N, bn, cn).ntiles;
@@ -661,7 +661,7 @@ int gemm_oz(const int8_t* ad, const int32_t* ea, int64_t M, int64_t K, int64_t N
     g.ready = g.tickets + tiles;
     if (cudaMemsetAsync(g.tickets, 0, 2 * tiles * sizeof(int), s) != cudaSuccess) return TRALS_ERR_CUDA;
   }
-  g.kblocks = (K + trals::kOzBK - 1) / trals::kOzBK;
+  g.kblocks = (K + SC::BK - 1) / SC::BK;
   g.ad = ad; g.bd = bd;
   g.cmap = cm; g.ea = ea; g.eb = eb; g.C = C; g.ws = ws + w.part;
   const int64_t tiles = static_cast<int64_t>(g.mtiles) * g.ntiles * sp.splits;
@@ -708,7 +708,7 @@ int oz_split(const Tin* x, int64_t rows, int64_t cols, int transpose, int8_t* di
     trals::oz_digits_tiled_t_kernel<Tin, SC><<<grid, 256, 0, s>>>(x, rows, cols, cols, ws, digits, at, exps);
     return launch_status();
   }
-  const int64_t work = oz_digits_bytes(oz_a_tiles(out_rows), K, SC::D) / (16 * SC::D);  // (padded row, 16-k chunk)
+  const int64_t work = oz_digits_bytes(oz_a_tiles(out_rows), K, SC::D, SC::BK) / (16 * SC::D);  // (padded row, 16-k chunk)
   const int blocks = static_cast<int>(std::min<int64_t>((work + 255) / 256, 64 * kSMs));
   trals::oz_digits_tiled_kernel<Tin, SC><<<blocks, 256, 0, s>>>(x, rows, cols, cols, transpose, ws, digits,
                                                                 oz_a_tiles(out_rows), exps);
@@ -734,10 +734,10 @@ ResOzWs residual_oz64_layout(int64_t pre, int64_t post, int64_t K) {
   const int bn = kResBN;
   ResOzWs w{};
   w.adig = 0;
-  w.aexp = w.adig + (oz_digits_bytes(oz_a_tiles(pre), K, SC::D) + 15) / 16 * 2;
+  w.aexp = w.adig + (oz_digits_bytes(oz_a_tiles(pre), K, SC::D, SC::BK) + 15) / 16 * 2;
   w.amx = w.aexp + (pre + 3) / 4 * 2;
   w.bdig = w.amx + (pre + 1) / 2 * 2;
-  w.bexp = w.bdig + (oz_digits_bytes(oz_b_tiles(post, bn), K, SC::D) + 15) / 16 * 2;
+  w.bexp = w.bdig + (oz_digits_bytes(oz_b_tiles(post, bn), K, SC::D, SC::BK) + 15) / 16 * 2;
   w.bmx = w.bexp + (post + 3) / 4 * 2;
   w.part = w.bmx + (post + 1) / 2 * 2;
   w.total = w.part + kSMs;
@@ -2613,7 +2613,7 @@ int trals_env_f64(const double* X, int64_t pre, int64_t post, int side, const do
 }
 
 int64_t trals_oz_digits_bytes(int64_t rows, int64_t k) {
-  return rows < 1 || k < 1 ? 0 : oz_digits_bytes(oz_a_tiles(rows), k, trals::OzF32::D);
+  return rows < 1 || k < 1 ? 0 : oz_digits_bytes(oz_a_tiles(rows), k, trals::OzF32::D, trals::OzF32::BK);
 }
 
 int64_t trals_oz_split_ws_elems(int64_t rows, int64_t cols, int transpose) { return transpose ? cols : rows; }
@@ -2638,7 +2638,7 @@ int trals_env_oz(const int8_t* xd, const int32_t* xe, int64_t pre, int64_t post,
 }
 
 int64_t trals_oz64_digits_bytes(int64_t rows, int64_t k) {
-  return rows < 1 || k < 1 ? 0 : oz_digits_bytes(oz_a_tiles(rows), k, trals::OzF64::D);
+  return rows < 1 || k < 1 ? 0 : oz_digits_bytes(oz_a_tiles(rows), k, trals::OzF64::D, trals::OzF64::BK);
 }
 
 int trals_oz64_split_f64(const double* x, int64_t rows, int64_t cols, int transpose, int8_t* digits, int32_t* exps,
@@ -2905,7 +2905,7 @@ int trals_residual_oz64(const double* X, int64_t pre, int64_t post, const double
   g.ntiles = g.nt.ntiles;
   g.rotate = 1;
   g.fixup = 0;
-  g.kblocks = (K + trals::kOzBK - 1) / trals::kOzBK;
+  g.kblocks = (K + SC::BK - 1) / SC::BK;
   g.ad = adig; g.bd = bdig; g.ea = aexp; g.eb = bexp;
   g.cmap = rowmajor(post); g.C = nullptr; g.ws = nullptr;
   g.X = X; g.ldx = post; g.rpart = ws + w.part;

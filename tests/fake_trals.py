@@ -42,15 +42,17 @@ def oz_digits_bytes(rows, k, rows_per_tile=128):
     return 4 * (-(-rows // rows_per_tile) * rows_per_tile) * (-(-k // 64) * 64)
 
 
-def oz_offsets(rows, k, plane, rows_per_tile=128, digits=4):
-    """Byte offsets [rows, k] of one digit plane in the tiled, SWIZZLE_64B layout:
-    [row tile][64-k block][plane][rows_per_tile x 64 B], chunk c of row r at c ^ ((r >> 1) & 3)."""
+def oz_offsets(rows, k, plane, rows_per_tile=128, digits=4, bk=64):
+    """Byte offsets [rows, k] of one digit plane in the tiled layout
+    [row tile][bk-k block][plane][rows_per_tile x bk B]: SWIZZLE_64B rows (bk 64, chunk c of
+    row r at c ^ ((r >> 1) & 3)) or SWIZZLE_32B rows (bk 32, chunk c at c ^ ((r >> 2) & 1))."""
     r = np.arange(rows, dtype=np.int64)[:, None]
     kk = np.arange(k, dtype=np.int64)[None, :]
-    kblocks = -(-k // 64)
-    t, rr, kb, c = r // rows_per_tile, r % rows_per_tile, kk >> 6, kk & 63
+    kblocks = -(-k // bk)
+    t, rr, kb, c = r // rows_per_tile, r % rows_per_tile, kk // bk, kk % bk
     block = (t * kblocks + kb) * digits + plane
-    return block * rows_per_tile * 64 + rr * 64 + (((c >> 4) ^ ((rr >> 1) & 3)) << 4) + (c & 15)
+    sw = ((c >> 4) ^ ((rr >> 1) & 3)) if bk == 64 else ((c >> 4) ^ ((rr >> 2) & 1))
+    return block * rows_per_tile * bk + rr * bk + (sw << 4) + (c & 15)
 
 
 def oz_slice(v):

@@ -293,7 +293,7 @@ def test_env_oz64_matches_f64(pre, post, side, r_lo, r_hi, leaf):
     torch.cuda.synchronize()
     if rows * K <= 4_000_000:
         buf = digits.cpu().numpy()
-        d = [buf[oz_offsets(rows, K, j, digits=8)].astype(np.longdouble) for j in range(8)]
+        d = [buf[oz_offsets(rows, K, j, digits=8, bk=32)].astype(np.longdouble) for j in range(8)]
         assert max(np.abs(v).max() for v in d) <= 64
         # rebuilt in x87 extended precision (64-bit mantissa: the 8-digit sum is exact)
         a = d[0] * np.longdouble(2.0) ** -6 + sum(d[j] * np.longdouble(2.0) ** (-6 - 7 * j) for j in range(1, 8))
