@@ -1780,13 +1780,12 @@ __device__ void hh_panel_team(double* A, int ld, int mr, int p, int nb, double* 
     const double s = red[0], alpha = top[0];
     double t = 0.0, scale = 0.0, beta = alpha;
     if (s > 0.0) {
-      // rsqrt-based (the column chain's latency: rsqrt 77 cycles vs sqrt 164 + a division):
-      // nrm = q rsqrt(q), 1 / beta = -sign(alpha) rsqrt(q), tau = 1 + |alpha| rsqrt(q)
-      const double q = fma(alpha, alpha, s);
-      const double rq = rsqrt(q);
-      const double nrm = q * rq;
+      // correctly rounded sqrt / divisions (LAPACK dlarfg's arithmetic): an rsqrt-based form
+      // (-5 % QR time) moved the reflectors by an ulp, enough to flip the reference's 1e-13
+      // degeneracy test on a rank-deficient golden (test_degenerate_without_fallback_raises)
+      const double nrm = sqrt(alpha * alpha + s);
       beta = alpha >= 0.0 ? -nrm : nrm;
-      t = fma(fabs(alpha), rq, 1.0);
+      t = (beta - alpha) / beta;
       scale = 1.0 / (alpha - beta);
     }
     const bool diag = (wt == 0 && lane == jj);
