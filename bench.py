@@ -41,9 +41,9 @@ FP64_PEAK_TFLOPS = 37.1      # measured DMMA.8x8x4 ceiling on this pool's B200 (
 # fp32 variant: 13 int8 MMAs per fp32-equivalent multiply-add; int8 dense ~2x the measured bf16 burst
 INT8_FP32_EQ_TFLOPS = 2 * 1715.0 / 13
 PEAK_SOURCE = "profiles/r01_fp64_pipes.md: mma.sync m8n8k4 f64 microbenchmark, 148 SMs"
-# fp64 "ozaki" environment products: 36 int8 digit-pair MMAs per fp64 multiply-add (8 balanced
-# digits per operand, pair levels s + t <= 7)
-OZ64_PAIRS = 36
+# fp64 "ozaki" environment products: 28 int8 digit-pair MMAs per fp64 multiply-add (7 balanced
+# radix-254 digits per operand, pair levels s + t <= 6)
+OZ64_PAIRS = 28
 # int8 tcgen05 ceiling on this pool's B200: tools/micro/i8_peak.cu (M128 N256 K32 MMAs back to back,
 # 148 SMs), profiles/r01_i8_peak.jsonl: 4374.8 TOPS burst (one launch), 4260.0 sustained (launches
 # back to back for 3 s).  The environment GEMM runs inside a long step (sweeps back to back), so the
@@ -349,7 +349,7 @@ def run_ours(args):
     bw = float(peaks.get("hbm_gbs", 6458.1))
     F = flops_per_sweep(dims, ranks)
     ebytes = 4 if fp32 else 8
-    # P = the peak of the pipe actually used (fp64 on int8: the int8 rate / 36 pairs)
+    # P = the peak of the pipe actually used (fp64 on int8: the int8 rate / 28 pairs)
     peak_tf = (INT8_FP32_EQ_TFLOPS if fp32 else
                INT8_PEAK_TOPS / OZ64_PAIRS if oz64 else FP64_PEAK_TFLOPS)
     t_roof = roofline_sweep_time(dims, ranks, peak_tf, bw, world, ebytes)
@@ -411,15 +411,15 @@ def run_ours(args):
                 "flops_per_launch": env_flops, "tflops_fp32_equiv": env_tf,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth)"}
     elif oz64:
-        # fp64 on the int8 tensor cores: the algorithmic work of one launch is the 36 digit-pair
+        # fp64 on the int8 tensor cores: the algorithmic work of one launch is the 28 digit-pair
         # products over the real (unpadded) M x N x K; peak = int8 dense = 2x the measured bf16 burst
         i8_peak = INT8_PEAK_TOPS
         i8_tops = env_tf * OZ64_PAIRS
         roof = {"bound": "tensor", "achieved": i8_tops, "peak": i8_peak, "unit": "TFLOP/s",
                 "frac": i8_tops / i8_peak, "traffic": traffic,
                 "kernel": "oz8_kernel<64, OzF64> (fp64 X x half-chain environment product on the int8 tcgen05 "
-                          "tensor cores: 8 balanced digits per operand, 36 exact int32 digit-pair products)",
-                "ops": "int8 tensor ops = 36 x 2 M N K per launch", "flops_per_launch": env_flops,
+                          "tensor cores: 7 balanced radix-254 digits per operand, 28 exact int32 digit-pair products)",
+                "ops": "int8 tensor ops = 28 x 2 M N K per launch", "flops_per_launch": env_flops,
                 "fp64_equiv_tflops": env_tf, "fp64_equiv_frac_of_dmma_peak": env_tf / FP64_PEAK_TFLOPS,
                 "avg_launch_ms": env_avg_ms, "share_of_step": env_share,
                 "frac_of_burst_peak": i8_tops / INT8_PEAK_BURST_TOPS,

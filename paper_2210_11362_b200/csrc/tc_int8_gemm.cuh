@@ -1,6 +1,6 @@
 // Exact-integer GEMM on the int8 tcgen05 tensor cores (Ozaki-style digit slicing)
 // for the environment products: the fp32 variant's (4 digits, below) and the fp64
-// path's (8 balanced digits, 36 pairs, fp64-accurate: see OzF64).
+// path's (7 balanced radix-254 digits, 28 pairs, fp64-accurate: see OzF64).
 //
 //   C(m, n) (fp64 out) = sum_k A[m][k] * B[n][k]      A from X, B from the fp64 half chain
 //
@@ -64,32 +64,44 @@ constexpr int kOzBM = 128;
 // Digit schemes.  D digit planes per operand, the LV lowest pair levels L = s + t
 // kept (pairs with s + t >= LV are dropped), BAL = balanced (round-to-nearest)
 // digits instead of truncated ones, KMAX = longest k per CTA whose int32 level
-// sums cannot overflow.
+// sums cannot overflow; C0 = scale of the first digit, RAD = radix of the rest:
+//   x = 2^e (d_0 + (d_1 + (d_2 + ...) / RAD) / RAD) / C0,
+// so a pair (s, t) weighs 2^(ea+eb) W0 RAD^-L with W0 = 1 / C0^2, and the epilogue
+// combines the levels by Horner in 1 / RAD.
 //   fp32 variant: 4 truncated base-128 digits (28 bits), all 16 pairs (7 levels):
-//     x = 2^e sum_s d_s 2^(-7(s+1)), |d_s| <= 127; a pair (s, t) weighs 2^(-14-7L).
+//     C0 = RAD = 128, |d_s| <= 127, W0 = 2^-14 (every step exact).
 //     A level sums <= 4 pairs of 127^2 per k -> KMAX 32768.
-//   fp64 (emulated DMMA): 8 balanced digits, first base 64 then base 128:
-//     x = 2^e (d_0 2^-6 + sum_{s>=1} d_s 2^-(6+7s)), |d_s| <= 64, remainder <= 2^-56
-//     (the fp64 mantissa of the row maximum plus 3 guard bits); levels 0..7 kept (36
-//     pairs; the dropped level-8 terms are < 2^-68 per k and zero-mean), a pair
-//     weighs 2^(-12-7L).  A level sums <= 8 pairs of 64^2 per k -> KMAX 61440.
+//   fp64 (emulated DMMA): 7 balanced digits, first d_0 = rint(127 v), then
+//     d_s = rint(254 r), |d_s| <= 127 (|r| <= 1/2, 254 / 2 = 127: the int8 range is
+//     used in full, 7.99 bits per digit); remainder <= 2^-55.9 2^e, the fp64 mantissa
+//     of the row maximum plus 3 guard bits.  Levels 0..6 kept (28 pairs; the dropped
+//     level-7 terms are 6 pairs of <= 254^-7 = 2^-55.9 per k, zero-mean -- the same
+//     bound as 8 base-128 digits with 36 pairs, at 22 % fewer int8 MMAs and 7 instead of 8
+//     digit bytes per element).  The slicing's products by 127 / 254 round at 2^-53
+//     of the current remainder, i.e. below the truncation.  A level sums <= 7 pairs of
+//     127^2 per k -> KMAX 18944 (7 x 127^2 x 18944 < 2^31).
 //     Measured against an extended-precision product: the same error as fp64 DMMA
 //     (tests/test_gpu_ops.py::test_env_oz64_accuracy).
 // BK: int8 k per pipeline stage and digit row: 64 (SWIZZLE_64B rows) for the fp32 scheme,
-// 32 (SWIZZLE_32B rows) for the fp64 one -- its 8-plane stages are twice as large, and at
+// 32 (SWIZZLE_32B rows) for the fp64 one -- its 7-plane stages are larger, and at
 // 32 k four of them fit in flight (the short-K shapes, c3/c4, were DRAM-latency bound
 // with two 64-k stages: tensor pipe 33 % busy at c3)
-template <int D_, int LV_, bool BAL_, int64_t KMAX_, int BK_>
+template <int D_, int LV_, bool BAL_, int64_t KMAX_, int BK_, int C0_, int RAD_>
 struct OzScheme {
   static constexpr int D = D_;
   static constexpr int LV = LV_;
   static constexpr bool BAL = BAL_;
-  static constexpr int OFF = BAL_ ? 12 : 14;  // 2^-OFF: weight of the level-0 pair
   static constexpr int64_t KMAX = KMAX_;
   static constexpr int BK = BK_;
+  static constexpr double C0 = C0_;
+  static constexpr double RAD = RAD_;
+  static constexpr double HR = 1.0 / RAD_;              // Horner factor
+  static constexpr double W0 = 1.0 / (double(C0_) * C0_);  // weight of the level-0 pair
+  static_assert(int64_t(BAL_ ? (LV_ < D_ ? LV_ : D_) : D_) * 127 * 127 * KMAX_ < (int64_t(1) << 31),
+                "int32 level sums may overflow");
 };
-using OzF32 = OzScheme<4, 7, false, 32768, 64>;
-using OzF64 = OzScheme<8, 8, true, 61440, 32>;
+using OzF32 = OzScheme<4, 7, false, 32768, 64, 128, 128>;
+using OzF64 = OzScheme<7, 7, true, 18944, 32, 127, 254>;
 constexpr int kOzDigits = OzF32::D;  // (fp32 variant layout helpers)
 constexpr int kOzLevels = OzF32::LV;
 constexpr int64_t kOzKmax = OzF32::KMAX;
@@ -522,7 +534,7 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
     });
   } else {
     // ------------------------------ epilogue ------------------------------
-    // TMEM -> exact fp64 combination of the levels (Horner in 2^-7) -> smem tile
+    // TMEM -> fp64 combination of the exact int32 levels (Horner in 1 / RAD) -> smem tile
     // (lane = row) -> global with lanes along n (contiguous for every CMap the
     // engine uses).  Whole-tile staging releases TMEM before the global stores;
     // chunked staging (large digit stages) stores 16 columns at a time.
@@ -548,7 +560,7 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
       const int r = quad * 32 + lane;
       const int64_t m = m0 + r;
-      const double sa = (m < g.M && ktiles > 0) ? ldexp(1.0, g.ea[m] - SC::OFF) : 0.0;
+      const double sa = (m < g.M && ktiles > 0) ? ldexp(SC::W0, g.ea[m]) : 0.0;
       bool part = g.splits > 1;
       bool second = false;  // fix-up: this CTA finishes the tile (adds the other half's partial)
       const int tile = mt * g.ntiles + nt;
@@ -584,7 +596,7 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
         for (int q = 0; q < 16; ++q) {
           double val = static_cast<double>(static_cast<int32_t>(v[LV - 1][q]));
 #pragma unroll
-          for (int L = LV - 2; L >= 0; --L) val = fma(val, 0.0078125, static_cast<double>(static_cast<int32_t>(v[L][q])));
+          for (int L = LV - 2; L >= 0; --L) val = fma(val, SC::HR, static_cast<double>(static_cast<int32_t>(v[L][q])));
           otile[r * T::OUT_LD + oc + q] = val * sa;
         }
         if constexpr (T::CHUNKED) {
@@ -719,18 +731,30 @@ __device__ __forceinline__ int oz_exponent(double mx) {
   return ilogb(mx) + 1;
 }
 
-// v = x 2^-e, |v| < 1 -> the scheme's digits (every step exact: power-of-two scalings
-// and the subtraction of an integer within 1 of its operand)
+// v = x 2^-e, |v| < 1 -> the scheme's digits.  Truncated (fp32 scheme): every step
+// exact (power-of-two scalings, subtraction of an integer within 1 of its operand).
+// Balanced: d_0 = rint(C0 v), then d_s = rint(RAD r), the remainder r = m r_prev - d
+// taken by one fma (exact whenever it fits 53 bits -- always for |v| >= 1/2 -- else
+// rounded at 2^-54 of the digit unit) and pulled back into [-1/2, 1/2] when the rounded
+// product m r_prev sat within an ulp of a half-integer; |d_s| <= 127 since 127 |v| < 127
+// and RAD / 2 = 127.
 template <class SC>
 __device__ __forceinline__ void oz_digits(double v, int8_t (&d)[SC::D]) {
   if constexpr (SC::BAL) {
-    // balanced: d_0 = rint(64 v), then d_s = rint(128 r), remainders in [-1/2, 1/2]
-    double t = v * 64.0;
+    double r = v;
 #pragma unroll
     for (int s = 0; s < SC::D; ++s) {
-      const double q = rint(t);
+      const double m = s == 0 ? SC::C0 : SC::RAD;
+      double q = rint(r * m);
+      r = fma(r, m, -q);
+      if (r > 0.5) {
+        q += 1.0;
+        r -= 1.0;
+      } else if (r < -0.5) {
+        q -= 1.0;
+        r += 1.0;
+      }
       d[s] = static_cast<int8_t>(static_cast<int>(q));
-      t = (t - q) * 128.0;
     }
   } else {
 #pragma unroll

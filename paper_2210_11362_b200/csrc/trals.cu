@@ -483,7 +483,7 @@ inline int64_t oz_digits_bytes(const trals::OzRowTiles& rt, int64_t k, int digit
   return digits * rt.rows_pad() * ((k + bk - 1) / bk * bk);
 }
 inline trals::OzRowTiles oz_a_tiles(int64_t rows) { return trals::OzRowTiles::fixed(rows, trals::kOzBM); }
-// n-tiles of at most 32 columns (two TMEM accumulator buffers with 8 digit levels) when the
+// n-tiles of at most 32 columns (two TMEM accumulator buffers with 7 digit levels) when the
 // contraction is short: a tile's MMAs then last about as long as its epilogue, which the
 // second buffer overlaps (fp64 scheme only; for the fp32 one -- staged epilogue, 4 digits --
 // the narrower tiles measured slower at c4: 1965 vs 2040 sweeps/s)
@@ -507,13 +507,13 @@ inline int oz_cn(int64_t N, int bn) {
   static int env = -1;
   if (env < 0) env = std::getenv("TRALS_OZ_CLUSTER") ? std::atoi(std::getenv("TRALS_OZ_CLUSTER")) : 1;
   const int cn = (env == 2 || env == 4) ? env : 1;
-  if (!SC::BAL || cn == 1) return 1;
+  if (!SC::BAL || cn == 1 || SC::D % cn != 0) return 1;  // (A planes split evenly over the cluster)
   return oz_b_tiles(N, bn, cn).ntiles > 0 ? cn : 1;
 }
 
 // split-K over a per-tile time model and never more than SC::KMAX k per CTA (int32
 // accumulator bound).  fp32: byte-bound (4 digit bytes per A element at the per-SM
-// HBM share); fp64: tensor-bound (36 digit-pair MMAs at the int8 rate of one SM).
+// HBM share); fp64: tensor-bound (28 digit-pair MMAs at the int8 rate of one SM).
 template <class SC>
 SplitPlan plan_split_oz(int64_t M, int64_t K, int64_t N) {
   const int64_t BK = SC::BK;
@@ -667,10 +667,14 @@ int gemm_oz(const int8_t* ad, const int32_t* ea, int64_t M, int64_t K, int64_t N
   const int64_t tiles = static_cast<int64_t>(g.mtiles) * g.ntiles * sp.splits;
   if (tiles > INT32_MAX) return TRALS_ERR_UNSUPPORTED;
   const int grid = static_cast<int>(std::min<int64_t>(tiles, kSMs));
-  int st;
-  if (cn == 4) st = bn == 32 ? launch_oz<32, SC, false, 4>(g, grid, s) : launch_oz<kOzBN, SC, false, 4>(g, grid, s);
-  else if (cn == 2) st = bn == 32 ? launch_oz<32, SC, false, 2>(g, grid, s) : launch_oz<kOzBN, SC, false, 2>(g, grid, s);
-  else st = bn == 32 ? launch_oz<32, SC>(g, grid, s) : launch_oz<kOzBN, SC>(g, grid, s);
+  int st = TRALS_ERR_UNSUPPORTED;
+  if constexpr (SC::D % 4 == 0) {
+    if (cn == 4) st = bn == 32 ? launch_oz<32, SC, false, 4>(g, grid, s) : launch_oz<kOzBN, SC, false, 4>(g, grid, s);
+  }
+  if constexpr (SC::D % 2 == 0) {
+    if (cn == 2) st = bn == 32 ? launch_oz<32, SC, false, 2>(g, grid, s) : launch_oz<kOzBN, SC, false, 2>(g, grid, s);
+  }
+  if (cn == 1) st = bn == 32 ? launch_oz<32, SC>(g, grid, s) : launch_oz<kOzBN, SC>(g, grid, s);
   if (st) return st;
   if (sp.splits > 1 && !g.fixup) {
     GemmArgs r{};
