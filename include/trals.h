@@ -123,10 +123,10 @@ int trals_env_oz(const int8_t* d_xdigits, const int32_t* d_xexps, int64_t pre, i
 /* fp64 environment product on the int8 tensor cores (AlsConfig.fp64_gemm =
  * "ozaki", the default): trals_env_f64 with X given as eight balanced digit
  * planes per K-major row,
- *   x = 2^ex[r] (d_0 2^-6 + sum_{s=1..7} d_s 2^-(6+7s)),  |d_s| <= 64,
- * (remainder <= 2^-56 2^ex[r], |x| < 2^ex[r]; same tiled layout as above with 8 planes,
+ *   x = 2^ex[r] (d_0 + (d_1 + (d_2 + ...) / 254) / 254) / 127,  |d_s| <= 127  (7 digits),
+ * (remainder <= 2^-55.9 2^ex[r], |x| < 2^ex[r]; same tiled layout as above with 7 planes,
  * trals_oz64_digits_bytes bytes), the half chain sliced the same way per call,
- * and the 36 digit-pair products of levels s + t <= 7 accumulated exactly in
+ * and the 28 digit-pair products of levels s + t <= 6 accumulated exactly in
  * int32 and combined in fp64.  Accuracy against an extended-precision product
  * is that of the fp64 DMMA product (tests/test_gpu_ops.py).  Replaces the same
  * reference call as trals_env_f64 (solvers.py:379). */
@@ -275,10 +275,10 @@ int trals_residual_f64(const double* d_X, int64_t pre, int64_t post, const doubl
                        void* stream);
 
 /* The same exact error with the product on the int8 tensor cores: HL (rows) and HRt
- * (columns) sliced into 8 balanced digits each, the 36 digit-pair products of levels
- * <= 7 accumulated exactly and combined in fp64 (the scheme of trals_env_oz64), the
+ * (columns) sliced into 7 balanced digits each, the 28 digit-pair products of levels
+ * <= 6 accumulated exactly and combined in fp64 (the scheme of trals_env_oz64), the
  * residual (X - HL HRt)^2 summed in the GEMM epilogue in a fixed order (one partial per
- * CTA, then one fixed-order sum): X_hat is never stored.  K <= 61440. */
+ * CTA, then one fixed-order sum): X_hat is never stored.  K <= 18944. */
 int64_t trals_residual_oz64_ws_elems(int64_t pre, int64_t post, int64_t K);
 int trals_residual_oz64(const double* d_X, int64_t pre, int64_t post, const double* d_HL, const double* d_HRt,
                         int64_t K, const double* d_xnorm2, double* d_out, double* d_ws, int64_t ws_elems,

@@ -94,7 +94,7 @@ class SweepEngine:
         # cores, Grams, solves and errors stay fp64.
         self.fp32 = x_local.dtype == torch.float32
         # fp64 X: the environment products run either on the fp64 DMMA pipe ("dmma") or on the
-        # int8 tcgen05 tensor cores over 8 balanced digit planes of X ("ozaki": 36 exact int32
+        # int8 tcgen05 tensor cores over 7 balanced digit planes of X ("ozaki": 28 exact int32
         # digit-pair products combined in fp64 -- the DMMA product's accuracy at ~3x its rate).
         # "auto": ozaki once an environment product is large enough to amortise the per-call
         # slicing of the half chain (measured crossover: BASELINE c2, 2.1 GFLOP, is a tie)

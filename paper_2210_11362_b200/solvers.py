@@ -51,8 +51,8 @@ class AlsConfig:
 
     `fp64_gemm` (extension) selects the engine of the fp64 environment
     products (the X-streaming MTTSP, solvers.py:379): "ozaki" runs
-    them on the int8 tcgen05 tensor cores over 8 balanced digit slices of X
-    and of the half chain -- 36 exact int32 digit-pair products combined in
+    them on the int8 tcgen05 tensor cores over 7 balanced digit slices of X
+    and of the half chain -- 28 exact int32 digit-pair products combined in
     fp64, with the accuracy of an fp64 product (measured against an
     extended-precision one) -- "dmma" on the fp64 DMMA pipe, and "auto"
     (default) picks ozaki when 2 |X| R^2 >= 4 GFLOP (BASELINE c3-c5) and the
