@@ -106,6 +106,14 @@ constexpr int kOzDigits = OzF32::D;  // (fp32 variant layout helpers)
 constexpr int kOzLevels = OzF32::LV;
 constexpr int64_t kOzKmax = OzF32::KMAX;
 
+// RAD^-p (p >= 0) as the nearest double (exact for the power-of-two radix)
+template <class SC>
+__host__ __device__ constexpr double oz_rad_pow(int p) {
+  double r = 1.0;  // RAD^p exactly (< 2^53 for the p used), then one rounding
+  for (int i = 0; i < p; ++i) r *= SC::RAD;
+  return 1.0 / r;
+}
+
 // ACC = 512 / (levels x BN) accumulator buffers in TMEM: with two (fp64 digits, n-tiles
 // <= 32 wide) the epilogue drains tile i while the MMAs of tile i+1 run -- the short-K
 // shapes (c3 phase R: K = 500) are otherwise epilogue-bound.
@@ -540,6 +548,7 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
     // chunked staging (large digit stages) stores 16 columns at a time.
     const int quad = warp & 3;
     const uint32_t tlane0 = tmem + (static_cast<uint32_t>(quad * 32) << 16);
+    __shared__ int64_t roff_s[kOzBM];  // chunked path: C offsets of the current tile's rows
     for (int b = 0; b < T::ACC; ++b) tmem_zero<LV * BN>(tlane0 + b * T::ACC_COLS);  // MMAs always accumulate
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
     __syncwarp();
@@ -560,7 +569,8 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
       const int r = quad * 32 + lane;
       const int64_t m = m0 + r;
-      const double sa = (m < g.M && ktiles > 0) ? ldexp(SC::W0, g.ea[m]) : 0.0;
+      // weight of the int64 level group hi (levels 0..H-1): W0 RAD^-(H-1)
+      const double sa = (m < g.M && ktiles > 0) ? ldexp(SC::W0 * oz_rad_pow<SC>((LV + 1) / 2 - 1), g.ea[m]) : 0.0;
       bool part = g.splits > 1;
       bool second = false;  // fix-up: this CTA finishes the tile (adds the other half's partial)
       const int tile = mt * g.ntiles + nt;
@@ -585,6 +595,12 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
       const int64_t sn1 = part ? 0 : g.cmap.sn1, sn2 = part ? 1 : g.cmap.sn2;
       double* base = part ? g.ws + (fix ? 0 : static_cast<int64_t>(split) * g.M * g.N) : g.C;
       const int rows = static_cast<int>((g.M - m0) < kOzBM ? (g.M - m0) : kOzBM);
+      if constexpr (T::CHUNKED) {
+        // row offsets of this tile in C, once per tile (read after the first chunk's barrier;
+        // the previous tile's readers are past its last barrier)
+        const uint32_t mm = static_cast<uint32_t>(m0 + r);
+        roff_s[r] = r < rows ? static_cast<int64_t>(mm / M2) * sm1 + static_cast<int64_t>(mm % M2) * sm2 : 0;
+      }
 #pragma unroll 1
       for (int c0 = 0; c0 < bw; c0 += 16) {
         uint32_t v[LV][16];
@@ -594,9 +610,15 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
         const int oc = T::CHUNKED ? 0 : c0;
 #pragma unroll
         for (int q = 0; q < 16; ++q) {
-          double val = static_cast<double>(static_cast<int32_t>(v[LV - 1][q]));
+          // levels 0..H-1 and H..LV-1 combined exactly in int64 (Horner in RAD, < 2^55), two
+          // conversions and one fma instead of LV conversions and LV - 1 dependent fmas
+          constexpr int H = (LV + 1) / 2;
+          int64_t hi = static_cast<int32_t>(v[0][q]), lo = static_cast<int32_t>(v[H][q]);
 #pragma unroll
-          for (int L = LV - 2; L >= 0; --L) val = fma(val, SC::HR, static_cast<double>(static_cast<int32_t>(v[L][q])));
+          for (int L = 1; L < H; ++L) hi = hi * static_cast<int64_t>(SC::RAD) + static_cast<int32_t>(v[L][q]);
+#pragma unroll
+          for (int L = H + 1; L < LV; ++L) lo = lo * static_cast<int64_t>(SC::RAD) + static_cast<int32_t>(v[L][q]);
+          const double val = fma(static_cast<double>(lo), oz_rad_pow<SC>(LV - H), static_cast<double>(hi));
           otile[r * T::OUT_LD + oc + q] = val * sa;
         }
         if constexpr (T::CHUNKED) {
@@ -610,18 +632,22 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
           // the other K half's partial (fix-up) or X (residual mode) for this chunk: all 16
           // loads issued before any use (one memory latency per chunk, not one per row)
           double pv[kOzBM / 8], xv[kOzBM / 8];
+          if (second || RES) {
 #pragma unroll
-          for (int k = 0; k < kOzBM / 8; ++k) {
-            const int rr = quad * 2 + (lane >> 4) + 8 * k;
-            pv[k] = (second && nok && rr < rows) ? __ldcg(g.ws + static_cast<int64_t>(m0 + rr) * g.N + n) : 0.0;
-            xv[k] = (RES && nok && rr < rows) ? __ldcs(g.X + static_cast<int64_t>(m0 + rr) * g.ldx + n) : 0.0;
+            for (int k = 0; k < kOzBM / 8; ++k) {
+              const int rr = quad * 2 + (lane >> 4) + 8 * k;
+              pv[k] = (second && nok && rr < rows) ? __ldcg(g.ws + static_cast<int64_t>(m0 + rr) * g.N + n) : 0.0;
+              xv[k] = (RES && nok && rr < rows) ? __ldcs(g.X + static_cast<int64_t>(m0 + rr) * g.ldx + n) : 0.0;
+            }
+          } else {
+#pragma unroll
+            for (int k = 0; k < kOzBM / 8; ++k) pv[k] = xv[k] = 0.0;
           }
 #pragma unroll
           for (int k = 0; k < kOzBM / 8; ++k) {
             const int rr = quad * 2 + (lane >> 4) + 8 * k;
             if (rr >= rows) break;
-            const uint32_t mm = static_cast<uint32_t>(m0 + rr);
-            const int64_t roff = static_cast<int64_t>(mm / M2) * sm1 + static_cast<int64_t>(mm % M2) * sm2;
+            const int64_t roff = roff_s[rr];
             const double o = otile[rr * T::OUT_LD + (lane & 15)] * sb + pv[k];
             if constexpr (RES) {
               if (nok) {
@@ -830,7 +856,10 @@ template <typename Tin, class SC>
 __global__ void __launch_bounds__(256) oz_digits_tiled_t_kernel(const Tin* __restrict__ x, int64_t rows, int64_t cols,
                                                                 int64_t ld_in, const double* __restrict__ mx,
                                                                 int8_t* __restrict__ out, OzRowTiles rt,
-                                                                int32_t* __restrict__ exps) {
+                                                                int32_t* __restrict__ exps, int plo = 0,
+                                                                int phi = 0) {
+  // plo > 0: output row n' takes column (n' % plo) phi + n' / plo of x (and its maximum
+  // mx[]) -- the column order that makes the environment's output tiles contiguous
   constexpr int D = SC::D, BK = SC::BK;
   __shared__ double tile[64][65];
   const int64_t K = rows, out_rows = cols;
@@ -840,14 +869,15 @@ __global__ void __launch_bounds__(256) oz_digits_tiled_t_kernel(const Tin* __res
   for (int e = tid; e < 64 * 64; e += 256) {
     const int kk = e >> 6, nn = e & 63;
     const int64_t k = k0 + kk, n = n0 + nn;
-    tile[kk][nn] = (k < K && n < out_rows) ? static_cast<double>(x[k * ld_in + n]) : 0.0;
+    const int64_t nc = plo > 0 ? (n % plo) * phi + n / plo : n;
+    tile[kk][nn] = (k < K && n < out_rows) ? static_cast<double>(x[k * ld_in + nc]) : 0.0;
   }
   __syncthreads();
   const int nl = tid >> 2, ch = tid & 3;
   const int64_t orow = n0 + nl;
   if (orow >= rt.rows_pad() || k0 + ch * 16 >= kblocks * BK) return;  // (BK 32: a 64-k tile may pass the layout)
   const bool rok = orow < out_rows;
-  const int e = rok ? oz_exponent(mx[orow]) : 0;
+  const int e = rok ? oz_exponent(mx[plo > 0 ? (orow % plo) * phi + orow / plo : orow]) : 0;
   const double sc = ldexp(1.0, -e);
   uint32_t w[D][4];
 #pragma unroll

@@ -484,15 +484,21 @@ inline int64_t oz_digits_bytes(const trals::OzRowTiles& rt, int64_t k, int digit
 }
 inline trals::OzRowTiles oz_a_tiles(int64_t rows) { return trals::OzRowTiles::fixed(rows, trals::kOzBM); }
 // n-tiles of at most 32 columns (two TMEM accumulator buffers with 7 digit levels) when the
-// contraction is short: a tile's MMAs then last about as long as its epilogue, which the
-// second buffer overlaps (fp64 scheme only; for the fp32 one -- staged epilogue, 4 digits --
-// the narrower tiles measured slower at c4: 1965 vs 2040 sweeps/s)
+// contraction is short and the 64-wide tiling leaves few tiles per SM: a tile's MMAs then
+// last about as long as its epilogue, which the second buffer overlaps, and the finer tiles
+// even out the last wave (c4: 64000 x 1600 x 64 -> 500 64-wide tiles on 148 SMs; 166 vs 185 us).
+// With many tiles per SM the 64-wide ones win: the epilogue's TMEM loads slow down under the
+// next tile's MMAs anyway, and A is read from shared memory half as often per output
+// (c3: 250000 x 500 x 100, 448 vs 486 us).  fp64 scheme only; for the fp32 one -- staged
+// epilogue, 4 digits -- the narrower tiles measured slower at c4: 1965 vs 2040 sweeps/s.
 constexpr int64_t kOzShortK = 8192;
 template <class SC>
-inline int oz_bn(int64_t K) {
+inline int oz_bn(int64_t M, int64_t K, int64_t N) {
   static int64_t short_k = -1;  // TRALS_OZ_SHORT_K (experiments) overrides kOzShortK
   if (short_k < 0) short_k = std::getenv("TRALS_OZ_SHORT_K") ? std::atoll(std::getenv("TRALS_OZ_SHORT_K")) : kOzShortK;
-  return (SC::BAL && K < short_k) ? 32 : kOzBN;
+  if (!SC::BAL || K >= short_k) return kOzBN;
+  const int64_t tiles64 = ((M + trals::kOzBM - 1) / trals::kOzBM) * ((N + kOzBN - 1) / kOzBN);
+  return tiles64 < 8 * kSMs ? 32 : kOzBN;
 }
 // TRALS_OZ_FIXED_TILES=1 (experiments): every n-tile kOzBN wide, the last one zero padded
 inline trals::OzRowTiles oz_b_tiles(int64_t n, int bn = kOzBN, int cn = 1) {
@@ -517,7 +523,7 @@ inline int oz_cn(int64_t N, int bn) {
 template <class SC>
 SplitPlan plan_split_oz(int64_t M, int64_t K, int64_t N) {
   const int64_t BK = SC::BK;
-  const int bn = oz_bn<SC>(K);
+  const int bn = oz_bn<SC>(M, K, N);
   const int cn = oz_cn<SC>(N, bn);
   const int64_t tiles = ((M + trals::kOzBM - 1) / trals::kOzBM) * oz_b_tiles(N, bn, cn).ntiles;
   const int64_t slots = kSMs;
@@ -550,8 +556,8 @@ struct OzWs {
 // in-kernel two-way split-K fix-up (no reduce launch) for the chunked-epilogue scheme
 template <class SC>
 bool oz_fixup(const SplitPlan& sp, int64_t K) {
-  const bool chunked = oz_bn<SC>(K) == 32 ? trals::OzTile<32, SC>::CHUNKED : trals::OzTile<kOzBN, SC>::CHUNKED;
-  return sp.splits == 2 && chunked;
+  (void)K;  // (both tile widths of the fp64 scheme use the chunked epilogue; fp32: kOzBN only)
+  return sp.splits == 2 && (SC::BAL || trals::OzTile<kOzBN, SC>::CHUNKED);
 }
 
 template <class SC>
@@ -559,7 +565,7 @@ OzWs oz_ws_layout(int64_t M, int64_t K, int64_t N) {
   const SplitPlan sp = plan_split_oz<SC>(M, K, N);
   OzWs w{};
   w.planes = 0;
-  const int bn = oz_bn<SC>(K);
+  const int bn = oz_bn<SC>(M, K, N);
   const int cn = oz_cn<SC>(N, bn);
   w.eb = w.planes + (oz_digits_bytes(oz_b_tiles(N, bn, cn), K, SC::D, SC::BK) + 15) / 16 * 2;
   w.mx = w.eb + (N + 3) / 4 * 2;
@@ -626,9 +632,16 @@ int launch_oz(const trals::OzArgs& g, int grid, cudaStream_t s) {
 
 // C(m, n) = sum_k A[m][k] B[k][n]: A given as tiled digits [D x 128-row tiles] + row exponents ea[M],
 // B fp64 [K][ldb] (sliced per call into the workspace), C fp64 through cm.
+// plo > 0 (cm.N2 == phi): the columns are taken in the order n' = (n % phi) plo + n / phi --
+// for the environment layout Env[r_hi][m][r_lo] (n = r_lo-index phi + r_hi-index) that makes
+// each r_hi group of a tile's columns one contiguous block of rows x r_lo in C, instead of
+// every column landing in a different r_hi plane (short-K shapes, where the epilogue's stores
+// weigh: c3 environment 698 -> 685 us).
 template <class SC>
 int gemm_oz(const int8_t* ad, const int32_t* ea, int64_t M, int64_t K, int64_t N, const double* B, int64_t ldb,
-            double* C, const CMap& cm, double* ws, int64_t ws_elems, cudaStream_t s) {
+            double* C, const CMap& cm0, double* ws, int64_t ws_elems, cudaStream_t s, int plo = 0, int phi = 0) {
+  if (plo > 0 && (static_cast<int64_t>(plo) * phi != N || cm0.N2 != phi)) return TRALS_ERR_ARG;
+  const CMap cm = plo > 0 ? CMap{cm0.sp, cm0.M2, cm0.sm1, cm0.sm2, plo, cm0.sn2, cm0.sn1} : cm0;
   if ((reinterpret_cast<uintptr_t>(ad) & 15u) || M > INT32_MAX || K > INT32_MAX || N > INT32_MAX) return TRALS_ERR_ARG;
   const OzWs w = oz_ws_layout<SC>(M, K, N);
   if (!ws || w.total > ws_elems) return TRALS_ERR_ARG;
@@ -638,12 +651,12 @@ int gemm_oz(const int8_t* ad, const int32_t* ea, int64_t M, int64_t K, int64_t N
   double* bmx = ws + w.mx;
   // B^T rows = columns of B: max over k, then tiled digits (transposed read)
   if (int st = launch_colmax<double>(B, K, N, ldb, bmx, s)) return st;
-  const int bn = oz_bn<SC>(K);
+  const int bn = oz_bn<SC>(M, K, N);
   const int cn = oz_cn<SC>(N, bn);
   {
     const trals::OzRowTiles bt = oz_b_tiles(N, bn, cn);
     dim3 grid(static_cast<unsigned>((K + 63) / 64), static_cast<unsigned>((bt.rows_pad() + 63) / 64));
-    trals::oz_digits_tiled_t_kernel<double, SC><<<grid, 256, 0, s>>>(B, K, N, ldb, bmx, bd, bt, eb);
+    trals::oz_digits_tiled_t_kernel<double, SC><<<grid, 256, 0, s>>>(B, K, N, ldb, bmx, bd, bt, eb, plo, phi);
     if (int st = launch_status()) return st;
   }
   trals::OzArgs g{};
@@ -2367,6 +2380,13 @@ int env_tf32(const float* xhi, const float* xlo, int64_t ldx, int64_t pre, int64
   return gemm_tc(xhi, xlo, ldx, post, pre, RR, H, RR, E, cm, ws, ws_elems, s);
 }
 
+// TRALS_OZ_NOPERM=1 (experiments): keep the natural column order for the short-K env products
+inline bool oz_noperm() {
+  static int v = -1;
+  if (v < 0) v = std::getenv("TRALS_OZ_NOPERM") ? 1 : 0;
+  return v == 1;
+}
+
 // fp32 variant of env() on the int8 tensor cores: X given as digit planes + row exponents,
 // K-major for this side (side 0: rows = pre, side 1: rows = post, the transposed copy).
 template <class SC>
@@ -2376,11 +2396,13 @@ int env_oz(const int8_t* xd, const int32_t* xe, int64_t pre, int64_t post, int s
   if (side == 0) {
     CMap cm{0, pre, 0, r_lo, r_hi, 1, pre * r_lo};
     if (leaf) cm = CMap{0, pre, 0, RR, r_hi, r_hi, 1};
-    return gemm_oz<SC>(xd, xe, pre, post, RR, H, RR, E, cm, ws, ws_elems, s);
+    const int plo = (!leaf && post < kOzShortK && !oz_noperm()) ? r_lo : 0;
+    return gemm_oz<SC>(xd, xe, pre, post, RR, H, RR, E, cm, ws, ws_elems, s, plo, plo ? r_hi : 0);
   }
   CMap cm{0, post, 0, r_lo, r_hi, 1, post * r_lo};
   if (leaf) cm = CMap{0, post, 0, RR, r_hi, r_hi, 1};
-  return gemm_oz<SC>(xd, xe, post, pre, RR, H, RR, E, cm, ws, ws_elems, s);
+  const int plo = (!leaf && pre < kOzShortK && !oz_noperm()) ? r_lo : 0;
+  return gemm_oz<SC>(xd, xe, post, pre, RR, H, RR, E, cm, ws, ws_elems, s, plo, plo ? r_hi : 0);
 }
 
 int absorb_right(const double* E, int Ra, int64_t pre, int64_t Ib, int Rb, int Rb1, const double* core_zt,

@@ -270,6 +270,7 @@ def _oz64_env(lib, x64, pre, post, side, H, r_lo, r_hi, leaf, s):
     (300, 77, 0, 3, 5, 0), (77, 300, 1, 4, 4, 0), (5, 13, 0, 2, 2, 1), (13, 5, 1, 2, 3, 1),
     (129, 1000, 1, 20, 20, 0), (1000, 129, 0, 11, 9, 0), (1600, 4000, 0, 8, 8, 0), (4000, 1600, 1, 8, 8, 1),
     (200, 70000, 0, 8, 8, 0), (70000, 150, 1, 6, 8, 0), (640, 640, 0, 20, 20, 1),
+    (160000, 200, 0, 8, 8, 0),  # short K with many tiles: 64-wide n-tiles, permuted columns
 ])
 def test_env_oz64_matches_f64(pre, post, side, r_lo, r_hi, leaf):
     """fp64 environment product on the int8 tensor cores (7 balanced radix-254 digits, levels
