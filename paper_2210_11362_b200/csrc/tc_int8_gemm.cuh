@@ -128,10 +128,16 @@ struct OzTile {
   // split-K fix-up and the residual epilogue live in the chunked path)
   static constexpr int FULL_OUT = kOzBM * (BN + 1) * 8;
   static constexpr bool CHUNKED = SC::BAL || (212 * 1024 - FULL_OUT) / STAGE < 3;
-  static constexpr int OUT_COLS = CHUNKED ? 16 : BN;
+  // CW: columns per TMEM load step and staging chunk.  (CW = 8 for the 64-wide fp64 tiles,
+  // whose 9 KB staging buffer leaves room for a fifth 42 KB stage, measured no faster at c5
+  // -- 4.61 ms either way -- and 5 % slower at c3: 16 everywhere.)
+  static constexpr bool WIDE64 = false;
+  static constexpr int CW = WIDE64 ? 8 : 16;
+  static constexpr int OUT_COLS = CHUNKED ? CW : BN;
   static constexpr int OUT_LD = OUT_COLS + 1;                 // odd: no bank conflicts
   static constexpr int OUT_BYTES = kOzBM * OUT_LD * 8;
-  static constexpr int STAGES = (212 * 1024 - OUT_BYTES) / STAGE < 6 ? (212 * 1024 - OUT_BYTES) / STAGE : 6;
+  static constexpr int CAP = (WIDE64 ? 224 : 212) * 1024;   // dynamic smem for stages + staging
+  static constexpr int STAGES = (CAP - OUT_BYTES) / STAGE < 6 ? (CAP - OUT_BYTES) / STAGE : 6;
   static constexpr int TMEM_COLS = 512;
   static constexpr int THREADS = 6 * 32;
   static constexpr size_t SMEM = static_cast<size_t>(STAGES) * STAGE + OUT_BYTES + 1024 + 256;
@@ -333,6 +339,19 @@ __device__ __forceinline__ void tmem_zero(uint32_t tlane) {
   asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
 }
 
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&v)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+               : "r"(taddr));
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]);
+template <int CW>
+__device__ __forceinline__ void tmem_ldc(uint32_t taddr, uint32_t (&v)[CW]) {
+  if constexpr (CW == 8) tmem_ld8(taddr, v);
+  else tmem_ld16(taddr, v);
+}
+
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
@@ -431,7 +450,6 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
   const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
   const int crank = CN > 1 ? static_cast<int>(cluster_ctarank()) : 0;
   constexpr uint16_t kMask = static_cast<uint16_t>((1u << CN) - 1u);
-  static_assert(SC::D % CN == 0, "A planes must split evenly over the cluster");
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(full + s, 1);
@@ -490,7 +508,7 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
           const int8_t* asrc = g.ad + (static_cast<int64_t>(mt) * g.kblocks + kb) * (D * T::A_PLANE);
           if constexpr (CN > 1) {
 #pragma unroll
-            for (int pl = crank * (D / CN); pl < (crank + 1) * (D / CN); ++pl)
+            for (int pl = crank * D / CN; pl < (crank + 1) * D / CN; ++pl)  // (uneven split when CN does not divide D)
               bulk_load_mc(st + pl * T::A_PLANE, asrc + pl * T::A_PLANE, T::A_PLANE, full + s, kMask);
           } else {
             bulk_load(st, asrc, D * T::A_PLANE, full + s);
@@ -601,15 +619,19 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
         const uint32_t mm = static_cast<uint32_t>(m0 + r);
         roff_s[r] = r < rows ? static_cast<int64_t>(mm / M2) * sm1 + static_cast<int64_t>(mm % M2) * sm2 : 0;
       }
+      constexpr int CW = T::CW;
+      constexpr int RPW = 32 / CW;              // chunk rows per warp store instruction
+      constexpr int NIT = kOzBM / (4 * RPW);    // store iterations per chunk
+      const int cl = lane % CW, rsub = lane / CW;
 #pragma unroll 1
-      for (int c0 = 0; c0 < bw; c0 += 16) {
-        uint32_t v[LV][16];
+      for (int c0 = 0; c0 < bw; c0 += CW) {
+        uint32_t v[LV][CW];
 #pragma unroll
-        for (int L = 0; L < LV; ++L) tmem_ld16(tlane + L * bw + c0, v[L]);
+        for (int L = 0; L < LV; ++L) tmem_ldc<CW>(tlane + L * bw + c0, v[L]);
         asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
         const int oc = T::CHUNKED ? 0 : c0;
 #pragma unroll
-        for (int q = 0; q < 16; ++q) {
+        for (int q = 0; q < CW; ++q) {
           // levels 0..H-1 and H..LV-1 combined exactly in int64 (Horner in RAD, < 2^55), two
           // conversions and one fma instead of LV conversions and LV - 1 dependent fmas
           constexpr int H = (LV + 1) / 2;
@@ -622,33 +644,33 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
           otile[r * T::OUT_LD + oc + q] = val * sa;
         }
         if constexpr (T::CHUNKED) {
-          // store this 16-column chunk: lane -> (row parity, column), warp -> rows quad*2 + ...
+          // store this CW-column chunk: lane -> (row rsub, column cl), warp -> rows quad*RPW + ...
           asm volatile("bar.sync 1, 128;\n" ::: "memory");
-          const int64_t n = n0 + c0 + (lane & 15);
+          const int64_t n = n0 + c0 + cl;
           const bool nok = n < nend;
           const uint32_t un = static_cast<uint32_t>(n);
           const int64_t coff = nok ? static_cast<int64_t>(un / N2) * sn1 + static_cast<int64_t>(un % N2) * sn2 : 0;
           const double sb = nok ? ldexp(1.0, g.eb[n]) : 0.0;
           // the other K half's partial (fix-up) or X (residual mode) for this chunk: all 16
           // loads issued before any use (one memory latency per chunk, not one per row)
-          double pv[kOzBM / 8], xv[kOzBM / 8];
+          double pv[NIT], xv[NIT];
           if (second || RES) {
 #pragma unroll
-            for (int k = 0; k < kOzBM / 8; ++k) {
-              const int rr = quad * 2 + (lane >> 4) + 8 * k;
+            for (int k = 0; k < NIT; ++k) {
+              const int rr = quad * RPW + rsub + 4 * RPW * k;
               pv[k] = (second && nok && rr < rows) ? __ldcg(g.ws + static_cast<int64_t>(m0 + rr) * g.N + n) : 0.0;
               xv[k] = (RES && nok && rr < rows) ? __ldcs(g.X + static_cast<int64_t>(m0 + rr) * g.ldx + n) : 0.0;
             }
           } else {
 #pragma unroll
-            for (int k = 0; k < kOzBM / 8; ++k) pv[k] = xv[k] = 0.0;
+            for (int k = 0; k < NIT; ++k) pv[k] = xv[k] = 0.0;
           }
 #pragma unroll
-          for (int k = 0; k < kOzBM / 8; ++k) {
-            const int rr = quad * 2 + (lane >> 4) + 8 * k;
+          for (int k = 0; k < NIT; ++k) {
+            const int rr = quad * RPW + rsub + 4 * RPW * k;
             if (rr >= rows) break;
             const int64_t roff = roff_s[rr];
-            const double o = otile[rr * T::OUT_LD + (lane & 15)] * sb + pv[k];
+            const double o = otile[rr * T::OUT_LD + cl] * sb + pv[k];
             if constexpr (RES) {
               if (nok) {
                 const double d = xv[k] - o;
@@ -761,9 +783,9 @@ __device__ __forceinline__ int oz_exponent(double mx) {
 // exact (power-of-two scalings, subtraction of an integer within 1 of its operand).
 // Balanced: d_0 = rint(C0 v), then d_s = rint(RAD r), the remainder r = m r_prev - d
 // taken by one fma (exact whenever it fits 53 bits -- always for |v| >= 1/2 -- else
-// rounded at 2^-54 of the digit unit) and pulled back into [-1/2, 1/2] when the rounded
-// product m r_prev sat within an ulp of a half-integer; |d_s| <= 127 since 127 |v| < 127
-// and RAD / 2 = 127.
+// rounded at 2^-54 of the digit unit).  q comes from the rounded product m r_prev, so when
+// that sat within an ulp of a half-integer |r| may exceed 1/2 by ~2^-53: the next digit is
+// still rint(<= 127 + 2^-45) <= 127, and d_0 = rint(127 v) <= 127 since |v| < 1.
 template <class SC>
 __device__ __forceinline__ void oz_digits(double v, int8_t (&d)[SC::D]) {
   if constexpr (SC::BAL) {
@@ -771,15 +793,8 @@ __device__ __forceinline__ void oz_digits(double v, int8_t (&d)[SC::D]) {
 #pragma unroll
     for (int s = 0; s < SC::D; ++s) {
       const double m = s == 0 ? SC::C0 : SC::RAD;
-      double q = rint(r * m);
+      const double q = rint(r * m);
       r = fma(r, m, -q);
-      if (r > 0.5) {
-        q += 1.0;
-        r -= 1.0;
-      } else if (r < -0.5) {
-        q -= 1.0;
-        r += 1.0;
-      }
       d[s] = static_cast<int8_t>(static_cast<int>(q));
     }
   } else {

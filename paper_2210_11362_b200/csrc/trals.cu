@@ -513,7 +513,7 @@ inline int oz_cn(int64_t N, int bn) {
   static int env = -1;
   if (env < 0) env = std::getenv("TRALS_OZ_CLUSTER") ? std::atoi(std::getenv("TRALS_OZ_CLUSTER")) : 1;
   const int cn = (env == 2 || env == 4) ? env : 1;
-  if (!SC::BAL || cn == 1 || SC::D % cn != 0) return 1;  // (A planes split evenly over the cluster)
+  if (!SC::BAL || cn == 1) return 1;
   return oz_b_tiles(N, bn, cn).ntiles > 0 ? cn : 1;
 }
 
@@ -681,12 +681,8 @@ int gemm_oz(const int8_t* ad, const int32_t* ea, int64_t M, int64_t K, int64_t N
   if (tiles > INT32_MAX) return TRALS_ERR_UNSUPPORTED;
   const int grid = static_cast<int>(std::min<int64_t>(tiles, kSMs));
   int st = TRALS_ERR_UNSUPPORTED;
-  if constexpr (SC::D % 4 == 0) {
-    if (cn == 4) st = bn == 32 ? launch_oz<32, SC, false, 4>(g, grid, s) : launch_oz<kOzBN, SC, false, 4>(g, grid, s);
-  }
-  if constexpr (SC::D % 2 == 0) {
-    if (cn == 2) st = bn == 32 ? launch_oz<32, SC, false, 2>(g, grid, s) : launch_oz<kOzBN, SC, false, 2>(g, grid, s);
-  }
+  if (cn == 4) st = bn == 32 ? launch_oz<32, SC, false, 4>(g, grid, s) : launch_oz<kOzBN, SC, false, 4>(g, grid, s);
+  if (cn == 2) st = bn == 32 ? launch_oz<32, SC, false, 2>(g, grid, s) : launch_oz<kOzBN, SC, false, 2>(g, grid, s);
   if (cn == 1) st = bn == 32 ? launch_oz<32, SC>(g, grid, s) : launch_oz<kOzBN, SC>(g, grid, s);
   if (st) return st;
   if (sp.splits > 1 && !g.fixup) {
