@@ -587,8 +587,7 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
       const int r = quad * 32 + lane;
       const int64_t m = m0 + r;
-      // weight of the int64 level group hi (levels 0..H-1): W0 RAD^-(H-1)
-      const double sa = (m < g.M && ktiles > 0) ? ldexp(SC::W0 * oz_rad_pow<SC>((LV + 1) / 2 - 1), g.ea[m]) : 0.0;
+      const double sa = (m < g.M && ktiles > 0) ? ldexp(1.0, g.ea[m]) : 0.0;
       bool part = g.splits > 1;
       bool second = false;  // fix-up: this CTA finishes the tile (adds the other half's partial)
       const int tile = mt * g.ntiles + nt;
@@ -640,7 +639,11 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
           for (int L = 1; L < H; ++L) hi = hi * static_cast<int64_t>(SC::RAD) + static_cast<int32_t>(v[L][q]);
 #pragma unroll
           for (int L = H + 1; L < LV; ++L) lo = lo * static_cast<int64_t>(SC::RAD) + static_cast<int32_t>(v[L][q]);
-          const double val = fma(static_cast<double>(lo), oz_rad_pow<SC>(LV - H), static_cast<double>(hi));
+          // the pair weight W0 RAD^-(H-1) (~2^-38) is applied here, not folded into the row
+          // scale: 2^ea stays an exact power of two, so rows near the bottom of the exponent
+          // range do not lose bits to a subnormal scale factor
+          constexpr double CHI = SC::W0 * oz_rad_pow<SC>(H - 1), CLO = CHI * oz_rad_pow<SC>(LV - H);
+          const double val = fma(static_cast<double>(lo), CLO, static_cast<double>(hi) * CHI);
           otile[r * T::OUT_LD + oc + q] = val * sa;
         }
         if constexpr (T::CHUNKED) {

@@ -357,3 +357,57 @@ def test_env_oz64_deterministic():
     b, _, _ = _oz64_env(lib, x64, pre, post, 0, H, r, r, 0, s)
     torch.cuda.synchronize()
     assert torch.equal(a, b)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("K", [18944, 18945, 37888, 37889])
+def test_env_oz64_kmax_boundaries(K):
+    """Contraction lengths at the int32 level-sum bound of the 7-digit scheme (KMAX = 18944
+    k per CTA: 7 pairs x 127^2 x 18944 < 2^31) and one past it, for one and two forced
+    splits: the product stays at the fp64 rounding level of the DMMA one, so no level sum
+    wrapped around."""
+    from paper_2210_11362_b200 import _lib as L
+    lib = L.lib()
+    rng = np.random.default_rng(K)
+    pre, r = 130, 6
+    # worst case for the level sums: every digit of every row near the int8 bound
+    x = np.where(rng.random((pre, K)) < 0.5, -1.0, 1.0) * (1.0 - 2.0 ** -40 * rng.random((pre, K)))
+    x64, H = cuda(x), cuda(np.where(rng.random((K, r * r)) < 0.5, -1.0, 1.0))
+    s = int(torch.cuda.current_stream().cuda_stream)
+    ref = torch.empty(pre * r * r, dtype=torch.float64, device="cuda")
+    ws = torch.empty(max(lib.trals_gemm_ws_elems(1, pre, K, r * r), 1 << 22), dtype=torch.float64, device="cuda")
+    L.check(lib.trals_env_f64(x64.data_ptr(), pre, K, 0, H.data_ptr(), r, r, ref.data_ptr(), 1,
+                              ws.data_ptr(), ws.numel(), s), "env_f64")
+    got, _, _ = _oz64_env(lib, x64, pre, K, 0, H, r, r, 1, s)
+    torch.cuda.synchronize()
+    assert rel(got.cpu().numpy(), ref.cpu().numpy()) < 1e-14
+
+
+@pytest.mark.gpu
+def test_env_oz64_extreme_rows():
+    """Rows of zeros, of subnormal-scale (1e-300) and of huge (1e300) values, and a single
+    nonzero per row: per-row power-of-two scaling keeps every row at full relative accuracy
+    (and zero rows exactly zero)."""
+    from paper_2210_11362_b200 import _lib as L
+    lib = L.lib()
+    rng = np.random.default_rng(3)
+    pre, post, r = 64, 300, 5
+    x = rng.standard_normal((pre, post))
+    x[0] = 0.0
+    x[1] *= 1e-300
+    x[2] *= 1e300 / 8
+    x[3] = 0.0
+    x[3, 17] = 3.0
+    x[4, ::2] *= 1e-200  # mixed magnitudes within a row: the small half sits below the row's 2^-56
+    h = rng.standard_normal((post, r * r))
+    x64, H = cuda(x), cuda(h)
+    s = int(torch.cuda.current_stream().cuda_stream)
+    got, _, _ = _oz64_env(lib, x64, pre, post, 0, H, r, r, 1, s)
+    torch.cuda.synchronize()
+    g = got.cpu().numpy().reshape(pre, r * r)
+    exact = (x.astype(np.longdouble) @ h.astype(np.longdouble)).astype(np.float64)
+    assert np.all(g[0] == 0.0)
+    for i in (1, 2, 3, 5, 6):
+        assert np.abs(g[i] - exact[i]).max() <= 1e-14 * np.abs(exact[i]).max(), i
+    # row 4: accurate relative to its row maximum (the tiny entries are below the digit window)
+    assert np.abs(g[4] - exact[4]).max() <= 1e-13 * np.abs(x[4]).max() * np.abs(h).sum(axis=0).max()
