@@ -834,7 +834,7 @@ __global__ void __launch_bounds__(256) oz_digits_tiled_kernel(const Tin* __restr
     const int64_t ch = transpose ? idx / rows_pad : idx % kchunks;
     const bool rok = orow < out_rows;
     const int e = rok ? oz_exponent(mx[orow]) : 0;
-    const double sc = ldexp(1.0, -e);
+    const double sc = ldexp(1.0, -(e / 2)), sc2 = ldexp(1.0, e / 2 - e);  // (finite for subnormal rows)
     uint32_t w[D][4];
 #pragma unroll
     for (int d = 0; d < D; ++d)
@@ -847,7 +847,7 @@ __global__ void __launch_bounds__(256) oz_digits_tiled_kernel(const Tin* __restr
         double v = 0.0;
         if (k < K) v = static_cast<double>(transpose ? x[k * ld_in + orow] : x[orow * ld_in + k]);
         int8_t dg[D];
-        oz_digits<SC>(v * sc, dg);
+        oz_digits<SC>(v * sc * sc2, dg);
 #pragma unroll
         for (int d = 0; d < D; ++d)
           w[d][j >> 2] |= static_cast<uint32_t>(static_cast<uint8_t>(dg[d])) << (8 * (j & 3));
@@ -896,7 +896,7 @@ __global__ void __launch_bounds__(256) oz_digits_tiled_t_kernel(const Tin* __res
   if (orow >= rt.rows_pad() || k0 + ch * 16 >= kblocks * BK) return;  // (BK 32: a 64-k tile may pass the layout)
   const bool rok = orow < out_rows;
   const int e = rok ? oz_exponent(mx[plo > 0 ? (orow % plo) * phi + orow / plo : orow]) : 0;
-  const double sc = ldexp(1.0, -e);
+  const double sc = ldexp(1.0, -(e / 2)), sc2 = ldexp(1.0, e / 2 - e);  // (finite for subnormal rows)
   uint32_t w[D][4];
 #pragma unroll
   for (int d = 0; d < D; ++d)
@@ -905,7 +905,7 @@ __global__ void __launch_bounds__(256) oz_digits_tiled_t_kernel(const Tin* __res
 #pragma unroll
   for (int j = 0; j < 16; ++j) {
     int8_t dg[D];
-    oz_digits<SC>(tile[ch * 16 + j][nl] * sc, dg);
+    oz_digits<SC>(tile[ch * 16 + j][nl] * sc * sc2, dg);
 #pragma unroll
     for (int d = 0; d < D; ++d) w[d][j >> 2] |= static_cast<uint32_t>(static_cast<uint8_t>(dg[d])) << (8 * (j & 3));
   }

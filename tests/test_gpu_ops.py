@@ -385,8 +385,8 @@ def test_env_oz64_kmax_boundaries(K):
 
 @pytest.mark.gpu
 def test_env_oz64_extreme_rows():
-    """Rows of zeros, of subnormal-scale (1e-300) and of huge (1e300) values, and a single
-    nonzero per row: per-row power-of-two scaling keeps every row at full relative accuracy
+    """Rows of zeros, of tiny (1e-300), subnormal (1e-309) and huge (1e300) values, and a
+    single nonzero per row: per-row power-of-two scaling keeps every row at full relative accuracy
     (and zero rows exactly zero)."""
     from paper_2210_11362_b200 import _lib as L
     lib = L.lib()
@@ -399,6 +399,7 @@ def test_env_oz64_extreme_rows():
     x[3] = 0.0
     x[3, 17] = 3.0
     x[4, ::2] *= 1e-200  # mixed magnitudes within a row: the small half sits below the row's 2^-56
+    x[7] *= 1e-309       # subnormal inputs (the slicing scale 2^-e is applied in two exact halves)
     h = rng.standard_normal((post, r * r))
     x64, H = cuda(x), cuda(h)
     s = int(torch.cuda.current_stream().cuda_stream)
@@ -409,5 +410,6 @@ def test_env_oz64_extreme_rows():
     assert np.all(g[0] == 0.0)
     for i in (1, 2, 3, 5, 6):
         assert np.abs(g[i] - exact[i]).max() <= 1e-14 * np.abs(exact[i]).max(), i
+    assert np.abs(g[7] - exact[7]).max() <= 1e-14 * np.abs(exact[7]).max() + 1e-320
     # row 4: accurate relative to its row maximum (the tiny entries are below the digit window)
     assert np.abs(g[4] - exact[4]).max() <= 1e-13 * np.abs(x[4]).max() * np.abs(h).sum(axis=0).max()
