@@ -1357,18 +1357,39 @@ __global__ void __launch_bounds__(256) fused_solve_kernel(const double* __restri
   __syncthreads();
   // acc (+)= Xs[:, xoff .. xoff+64] * G[k0 .. k0+64][col] for this warp's column col (G row-major,
   // pitch ldg, zero outside [0, limk) x [0, limc)); two DMMA chains
-  auto chunk = [&](const double* Xs, int xoff, const double* G, int64_t ldg, int k0, int col, int limk, int limc,
-                   double& a0, double& a1, double& a2, double& a3) {
-    double bv[16];
+  auto load = [&](double (&bv)[16], const double* G, int64_t ldg, int k0, int col, int limk, int limc) {
 #pragma unroll
     for (int q = 0; q < 16; ++q) {
       const int kk = k0 + 4 * q + fk;
       bv[q] = (kk < limk && col < limc) ? __ldg(G + static_cast<int64_t>(kk) * ldg + col) : 0.0;
     }
+  };
+  auto mma = [&](const double (&bv)[16], const double* Xs, int xoff, double& a0, double& a1, double& a2, double& a3) {
 #pragma unroll
     for (int q = 0; q < 16; q += 2) {
       trals::dmma884(a0, a1, Xs[fr * ldr + xoff + 4 * q + fk], bv[q]);
       trals::dmma884(a2, a3, Xs[fr * ldr + xoff + 4 * q + 4 + fk], bv[q + 1]);
+    }
+  };
+  auto chunk = [&](const double* Xs, int xoff, const double* G, int64_t ldg, int k0, int col, int limk, int limc,
+                   double& a0, double& a1, double& a2, double& a3) {
+    double bv[16];
+    load(bv, G, ldg, k0, col, limk, limc);
+    mma(bv, Xs, xoff, a0, a1, a2, a3);
+  };
+  // chunks c = c0, c0 + 1, ... < c1 of 64 k (operand offset = k offset = 64 c): the next
+  // chunk's 16 L2 loads are in flight while this one's MMAs run (two named fragment
+  // buffers, compile-time indexed)
+  auto chunks = [&](const double* Xs, const double* G, int c0, int c1, int col, double& a0, double& a1, double& a2,
+                    double& a3) {
+    if (c0 >= c1) return;
+    double bA[16], bB[16];
+    load(bA, G, m, c0 * kBlkNB, col, m, m);
+    for (int c = c0; c < c1; c += 2) {
+      if (c + 1 < c1) load(bB, G, m, (c + 1) * kBlkNB, col, m, m);
+      mma(bA, Xs, c * kBlkNB, a0, a1, a2, a3);
+      if (c + 2 < c1) load(bA, G, m, (c + 2) * kBlkNB, col, m, m);
+      if (c + 1 < c1) mma(bB, Xs, (c + 1) * kBlkNB, a0, a1, a2, a3);
     }
   };
   // ---------------- forward: Y_b = (R_b - Y_{<b} U_{<b,b}) W_b ----------------
@@ -1376,7 +1397,7 @@ __global__ void __launch_bounds__(256) fused_solve_kernel(const double* __restri
     const int j0 = b * kBlkNB;
     const int col = j0 + warp * 8 + fr;
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-    for (int kc = 0; kc < b; ++kc) chunk(Ys, kc * kBlkNB, U, m, kc * kBlkNB, col, m, m, a0, a1, a2, a3);
+    chunks(Ys, U, 0, b, col, a0, a1, a2, a3);
     Rs[fr * ldr + j0 + warp * 8 + 2 * fk] -= a0 + a2;
     Rs[fr * ldr + j0 + warp * 8 + 2 * fk + 1] -= a1 + a3;
     __syncthreads();
@@ -1392,7 +1413,7 @@ __global__ void __launch_bounds__(256) fused_solve_kernel(const double* __restri
     const int j0 = b * kBlkNB, j1 = j0 + kBlkNB;
     const int col = j0 + warp * 8 + fr;
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-    for (int kb = j1; kb < mp; kb += kBlkNB) chunk(Rs, kb, L, m, kb, col, m, m, a0, a1, a2, a3);
+    chunks(Rs, L, b + 1, nblk, col, a0, a1, a2, a3);
     Ys[fr * ldr + j0 + warp * 8 + 2 * fk] -= a0 + a2;
     Ys[fr * ldr + j0 + warp * 8 + 2 * fk + 1] -= a1 + a3;
     __syncthreads();

@@ -1,2 +1,3 @@
-timeout 300 python -m pytest tests/test_gpu_ops.py -q -x -k "oz" 2>&1 | tail -1
-for c in c5 c3 c4; do timeout 120 python tools/env_time.py $c 5 2>&1 | tail -1; done
+timeout 600 python -m pytest tests -m gpu -q -x 2>&1 | tail -2
+python tools/sweep_timeline.py c5 ne 2>&1 | grep -E "solve|chol|S[0-9]" | head -12
+timeout 300 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['ms_per_step'])"
