@@ -137,22 +137,6 @@ int64_t trals_env_oz64_ws_elems(int64_t pre, int64_t post, int side, int r_lo, i
 int trals_env_oz64(const int8_t* d_xdigits, const int32_t* d_xexps, int64_t pre, int64_t post, int side,
                    const double* d_H, int r_lo, int r_hi, double* d_env, int leaf, double* d_ws, int64_t ws_elems,
                    void* stream);
-/* 3xTF32 alternative (an operator kept for comparison, not used by the
- * solvers: its truncated fp32 accumulation biases M_n by ~1e-6 relative).
- * X held as hi = tf32(x), lo = x - hi (fp32, hi + lo == x exactly);
- * kind::tf32 MMAs hi*hi + hi*lo + lo*hi per k-step, fp64 split-K reduction.
- * trals_tf32_ld: padded row length (floats, multiple of 4 = 16 B TMA stride).
- * trals_tf32_split_f32: x [rows][ld_in] -> hi, lo as [rows][ld_out]
- *   (transpose = 0) or [cols][ld_out] (transpose = 1).
- * trals_env_tf32: side 0: hi/lo [pre][ldx] (X itself), side 1: [post][ldx] (X^T). */
-int64_t trals_tf32_ld(int64_t cols);
-int trals_tf32_split_f32(const float* d_x, int64_t rows, int64_t cols, int64_t ld_in, int transpose,
-                         float* d_hi, float* d_lo, int64_t ld_out, void* stream);
-int64_t trals_env_tf32_ws_elems(int64_t pre, int64_t post, int side, int r_lo, int r_hi);
-int trals_env_tf32(const float* d_xhi, const float* d_xlo, int64_t ldx, int64_t pre, int64_t post, int side,
-                   const double* d_H, int r_lo, int r_hi, double* d_env, int leaf, double* d_ws,
-                   int64_t ws_elems, void* stream);
-
 /* Absorb the rightmost / leftmost core of an environment segment.
  * Env layout [r_a][i_a .. i_b][r_{b+1}].
  *   right: Out[r_a][pre][r_b]       = sum E[r_a][pre][i_b][r_{b+1}] G_b[r_b,i_b,r_{b+1}]
@@ -230,6 +214,38 @@ int trals_chol_solve_f64(const double* d_U, const double* d_F, const double* d_a
 int64_t trals_spd_fallback_ws_elems(int64_t rows, int m);
 int trals_spd_fallback_f64(const double* d_S, int m, const double* d_M, int64_t rows, double* d_Z, int* d_info,
                            int mode, double rcond, double* d_ws, int64_t ws_elems, void* stream);
+
+/* R0 of the QR-stabilised variants without forming V (tr_als_qr, solvers.py:422-424
+ * `q0, r0 = qr_economy(cyclic_unfold(subchain_skip(R-tensors, n), 1))`; for Alg. 1 tr_als,
+ * solvers.py:337-339, the same with the cores themselves).  h_rt[j] = the R-tensor of core j
+ * in layout C, shape (R_j, ks[j], R_{j+1}) (ks[j] = min(I_j, R_j R_{j+1}) for QR, I_j for
+ * Alg. 1).  The cores n+1, ..., n-1 are merged one at a time (ring.py:110-131) and every merge
+ * whose lateral size exceeds R_a R_c is compressed by a Householder QR (cuSOLVER dgeqrf,
+ * deterministic mode): orthogonal transformations of V_[2]'s rows, so the result is the
+ * reference's R0 to rounding.  d_R0 (row-major, k0 x m with m = R_n R_{n+1}, k0 =
+ * min(prod_{j!=n} ks[j], m)): upper triangular / trapezoidal, nonnegative diagonal
+ * (linalg.py:48-51), columns r_n + R_n r_{n+1} (the S_n order). */
+int64_t trals_r0_merge_ws_elems(int N, int n, const int32_t* ranks, const int32_t* ks);
+int trals_r0_merge_f64(int N, int n, const int32_t* ranks, const int32_t* ks, const double* const* h_rt,
+                       double* d_R0, double* d_ws, int64_t ws_elems, void* stream);
+
+/* solve_triangular_block's factor step (solvers.py:262-273 with linalg.py:84-101) for a given
+ * square R0 (d_U, m x m row-major, upper): the operands of trals_chol_solve_f64 (which then
+ * computes Z = M R0^{-1} R0^{-T}, i.e. W = M R0^{-1}, Z R0^T = W): m <= 112: d_F = R0^{-1},
+ * d_aux = R0^{-T}; m > 112: d_F = R0^T, d_aux = the inverses of the 64 x 64 diagonal blocks
+ * (trals_cholesky_aux_elems(m) doubles); the strict lower triangle of d_U is zeroed.  With
+ * check_degen the 1e-13 degeneracy floor of linalg.py:96-99 -> d_info[TRALS_INFO_DEGEN]. */
+int trals_tri_prepare_f64(double* d_U, int m, double* d_F, double* d_aux, int check_degen, int* d_info,
+                          void* stream);
+
+/* The min-norm fallback of the QR variants taken on R0 itself (linalg.py:104-112 pinv with
+ * rcond = AlsConfig.svd_rcond, solvers.py:262-273): one-sided Jacobi SVD of the Lr x m factor
+ * (R0 V = U Sigma), Z = M V Sigma^{-2} V^T over the singular values above rcond sigma_max
+ * (= W pinv(R0)^T for W = M R0^{-1}).  mode 1: fires on d_info[TRALS_INFO_DEGEN], clears it and
+ * counts a fallback; mode 2: non-square R0 (Lr < m, solvers.py:264-266), always, uncounted.
+ * Workspace: trals_spd_fallback_ws_elems(rows, m). */
+int trals_tri_fallback_f64(const double* d_R0, int Lr, int m, const double* d_M, int64_t rows, double* d_Z,
+                           int* d_info, int mode, double rcond, double* d_ws, int64_t ws_elems, void* stream);
 
 /* Axis reversal (io.py:10-11, read_tensor's reshape(order="F").copy()): src is
  * first-index-fastest over dims[0..N-1], dst the same tensor last-index-fastest

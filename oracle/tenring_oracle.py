@@ -661,3 +661,63 @@ def mttsp(x, cores, n):
 def coefficient_gram(cores, n):
     """S_n via the Gram chain (solvers.py:372-373, Prop. 3)."""
     return chain_grams(bond_gram(cores[j]) for j in gram_order(n, len(cores)))
+
+
+class BlockStepper:
+    """The reference's sweep body, one block update per call (CPU baseline legs of bench.py).
+
+    `prepare()` does the untimed set-up of the reference's run (the N cyclic
+    unfoldings of X, solvers.py:362; the initial Grams / lateral QRs,
+    solvers.py:366-367, :417, :468-470); `step(n)` is exactly one iteration
+    n of the per-mode loop of tr_als_ne (solvers.py:370-384), tr_als_qr
+    (:420-443) or tr_als_qrne (:473-493), with the same materialised subchain,
+    unfold copies and numpy/LAPACK calls as the functions above."""
+
+    def __init__(self, x, variant, ranks, init):
+        if variant not in ("ne", "qr", "qrne"):
+            raise ValueError(f"unsupported variant {variant!r}")
+        self.d = _Driver(x, Config(ranks=tuple(ranks), max_iters=1, init_cores=init, error_mode="none"), variant)
+        self.variant = variant
+        self.cores = self.d.start_cores()
+        self.d.buckets = dict.fromkeys(BUCKETS, 0.0)
+
+    def prepare(self):
+        d = self.d
+        if self.variant == "ne":
+            self.xs = [unfold_cyclic(d.x, n) for n in range(d.N)]
+            self.grams = [bond_gram(g) for g in self.cores]
+        else:
+            self.qrs = [lateral_qr(g) for g in self.cores]
+            if self.variant == "qrne":
+                self.rgrams = [bond_gram(f.r_tensor) for f in self.qrs]
+
+    def step(self, n):
+        d, cores = self.d, self.cores
+        if self.variant == "ne":
+            s = chain_grams(self.grams[j] for j in gram_order(n, d.N))
+            a = unfold_cyclic(chain_without(cores, n), 1)
+            m = self.xs[n] @ a
+            del a
+            z = d.normal_block(s, m)
+            cores[n] = fold_classical(z, 1, d.shape_of(n))
+            self.grams[n] = bond_gram(cores[n])
+        elif self.variant == "qr":
+            v = chain_without([f.r_tensor for f in self.qrs], n)
+            q0, r0 = qr_signed(unfold_cyclic(v, 1))
+            del v
+            y = mode_products(d.x, [(j, self.qrs[j].q.T) for j in range(d.N) if j != n])
+            w = unfold_cyclic(y, n) @ q0
+            del y, q0
+            z = d.tri_block(r0, w)
+            cores[n] = fold_classical(z, 1, d.shape_of(n))
+            self.qrs[n] = lateral_qr(cores[n])
+        else:
+            s = chain_grams(self.rgrams[j] for j in gram_order(n, d.N))
+            v = chain_without([f.r_tensor for f in self.qrs], n)
+            y = mode_products(d.x, [(j, self.qrs[j].q.T) for j in range(d.N) if j != n])
+            m = unfold_cyclic(y, n) @ unfold_cyclic(v, 1)
+            del y, v
+            z = d.normal_block(s, m)
+            cores[n] = fold_classical(z, 1, d.shape_of(n))
+            self.qrs[n] = lateral_qr(cores[n])
+            self.rgrams[n] = bond_gram(self.qrs[n].r_tensor)

@@ -49,6 +49,12 @@ _SIGNATURES = {
     "trals_chol_solve_f64": (c_int, [_dp, _dp, _dp, c_int, _dp, c_int64, _dp, _dp, c_int64, c_void_p]),
     "trals_spd_fallback_ws_elems": (c_int64, [c_int64, c_int]),
     "trals_spd_fallback_f64": (c_int, [_dp, c_int, _dp, c_int64, _dp, _dp, c_int, c_double, _dp, c_int64, c_void_p]),
+    "trals_tri_fallback_f64": (c_int, [_dp, c_int, c_int, _dp, c_int64, _dp, _dp, c_int, c_double, _dp, c_int64,
+                                       c_void_p]),
+    "trals_r0_merge_ws_elems": (c_int64, [c_int, c_int, POINTER(c_int32), POINTER(c_int32)]),
+    "trals_r0_merge_f64": (c_int, [c_int, c_int, POINTER(c_int32), POINTER(c_int32), POINTER(c_void_p), _dp, _dp,
+                                   c_int64, c_void_p]),
+    "trals_tri_prepare_f64": (c_int, [_dp, c_int, _dp, _dp, c_int, _dp, c_void_p]),
     "trals_reverse_axes_f64": (c_int, [_dp, c_int, POINTER(c_int64), _dp, c_void_p]),
     "trals_sumsq_ws_elems": (c_int64, []),
     "trals_sumsq_f64": (c_int, [_dp, c_int64, _dp, _dp, c_void_p]),
@@ -64,11 +70,6 @@ _SIGNATURES = {
     "trals_env_oz64_ws_elems": (c_int64, [c_int64, c_int64, c_int, c_int, c_int]),
     "trals_env_oz64": (c_int, [_dp, _dp, c_int64, c_int64, c_int, _dp, c_int, c_int, _dp, c_int, _dp, c_int64,
                                c_void_p]),
-    "trals_tf32_ld": (c_int64, [c_int64]),
-    "trals_tf32_split_f32": (c_int, [_dp, c_int64, c_int64, c_int64, c_int, _dp, _dp, c_int64, c_void_p]),
-    "trals_env_tf32_ws_elems": (c_int64, [c_int64, c_int64, c_int, c_int, c_int]),
-    "trals_env_tf32": (c_int, [_dp, _dp, c_int64, c_int64, c_int64, c_int, _dp, c_int, c_int, _dp, c_int, _dp,
-                               c_int64, c_void_p]),
     "trals_error_ws_elems": (c_int64, [c_int64, c_int]),
     "trals_error_terms_f64": (c_int, [_dp, _dp, _dp, c_int64, c_int, _dp, _dp, _dp, c_int64, c_void_p]),
     "trals_residual_ws_elems": (c_int64, [c_int64, c_int64]),

@@ -15,6 +15,7 @@ OUT = os.path.join(HERE, "libtrals.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-shared", "-I", os.path.join(ROOT, "include")]
+LIBS = ["-lcusolver"]  # dgeqrf for the QR variants' merged R0 (csrc/qr_r0.cuh)
 
 
 def up_to_date() -> bool:
@@ -27,7 +28,7 @@ def up_to_date() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
         return OUT
-    cmd = [NVCC, *FLAGS, "-o", OUT + ".tmp", *SRC]
+    cmd = [NVCC, *FLAGS, "-o", OUT + ".tmp", *SRC, *LIBS]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)

@@ -14,7 +14,6 @@
 #include "../../include/trals.h"
 #include "dmma_gemm.cuh"
 #include "dmma_tma_gemm.cuh"
-#include "tc_tf32_gemm.cuh"
 #include "tc_int8_gemm.cuh"
 
 using trals::CMap;
@@ -364,114 +363,6 @@ int gemm_tma(const double* A, int64_t sAm, int64_t sAk, int64_t M, int64_t K, in
   return TRALS_OK;
 }
 
-// ---------------------------------------------------------------------------
-// fp32 variant: tcgen05 3xTF32 GEMM (tc_tf32_gemm.cuh), both operands K-major
-// ---------------------------------------------------------------------------
-bool make_map_f32(CUtensorMap* map, const float* base, uint64_t inner, uint64_t outer, uint64_t ld,
-                  uint32_t box_inner, uint32_t box_outer) {
-  auto enc = tensor_map_encoder();
-  if (!enc) return false;
-  const cuuint64_t dims[2] = {inner, outer};
-  const cuuint64_t strides[1] = {ld * sizeof(float)};
-  const cuuint32_t box[2] = {box_inner, box_outer};
-  const cuuint32_t estr[2] = {1, 1};
-  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
-int tc_bn_for(int64_t N) { return N <= 64 ? 64 : (N <= 128 ? 128 : 256); }
-
-// split-K over a byte-bound cost model: the operands (hi + lo of the A rows,
-// B from L2) stream at the per-SM share of HBM bandwidth; one CTA per SM.
-SplitPlan plan_split_tc(int bn, int64_t M, int64_t K, int64_t N) {
-  const int64_t tiles = ((M + trals::kTcBM - 1) / trals::kTcBM) * ((N + bn - 1) / bn);
-  const int64_t slots = kSMs;
-  const int64_t smax = std::max<int64_t>(1, std::min<int64_t>(64, K / (4 * trals::kTcBK)));
-  const double t_tile = 8.0 * trals::kTcBM * static_cast<double>(K) / (6.5e12 / slots);
-  const double out_bytes = 8.0 * static_cast<double>(M) * N;
-  int64_t best_s = 1;
-  double best = 1e300;
-  for (int64_t sp = 1; sp <= smax; ++sp) {
-    const int64_t waves = (tiles * sp + slots - 1) / slots;
-    double cost = static_cast<double>(waves) / sp * t_tile;
-    if (sp > 1) cost += 3e-6 + (sp + 1) * out_bytes / 6.0e12;
-    if (cost < best * (1 - 1e-9)) { best = cost; best_s = sp; }
-  }
-  int64_t kchunk = (K + best_s - 1) / best_s;
-  kchunk = ((kchunk + trals::kTcBK - 1) / trals::kTcBK) * trals::kTcBK;
-  return {static_cast<int>(std::max<int64_t>(1, (K + kchunk - 1) / kchunk)), kchunk};
-}
-
-inline int64_t tf32_ld(int64_t cols) { return (cols + 3) / 4 * 4; }
-inline int64_t f32_in_f64(int64_t n) { return (n + 3) / 4 * 2; }  // doubles holding n floats, 16 B multiple
-
-template <int BN>
-int launch_tc(const CUtensorMap* m, const trals::TcArgs& g, cudaStream_t s) {
-  using T = trals::TcTile<BN>;
-  auto kern = trals::tc_tf32_kernel<BN>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(T::SMEM));
-    attr = true;
-  }
-  dim3 grid(static_cast<unsigned>((g.N + BN - 1) / BN), static_cast<unsigned>((g.M + trals::kTcBM - 1) / trals::kTcBM),
-            static_cast<unsigned>(g.splits));
-  if (grid.y > 65535u) return TRALS_ERR_UNSUPPORTED;
-  kern<<<grid, T::THREADS, T::SMEM, s>>>(m[0], m[1], m[2], m[3], g);
-  return launch_status();
-}
-
-int64_t gemm_tc_ws(int64_t M, int64_t K, int64_t N) {
-  const SplitPlan sp = plan_split_tc(tc_bn_for(N), M, K, N);
-  return 2 * f32_in_f64(N * tf32_ld(K)) + (sp.splits > 1 ? static_cast<int64_t>(sp.splits) * M * N : 0);
-}
-
-// C(m, n) = sum_k A[m][k] B[k][n]: A = (ahi + alo) fp32 [M][lda] K-contiguous, B fp64 [K][ldb]
-// (split + transposed into the workspace), C fp64 through cm.
-int gemm_tc(const float* ahi, const float* alo, int64_t lda, int64_t M, int64_t K, int64_t N, const double* B,
-            int64_t ldb, double* C, const CMap& cm, double* ws, int64_t ws_elems, cudaStream_t s) {
-  if (!tensor_map_encoder()) return TRALS_ERR_CUDA;
-  if ((reinterpret_cast<uintptr_t>(ahi) & 15u) || (reinterpret_cast<uintptr_t>(alo) & 15u) || (lda & 3) ||
-      lda < K || M > INT32_MAX || K > INT32_MAX || N > 65535LL * 256)
-    return TRALS_ERR_ARG;
-  if (gemm_tc_ws(M, K, N) > ws_elems || !ws) return TRALS_ERR_ARG;
-  const int bn = tc_bn_for(N);
-  const SplitPlan sp = plan_split_tc(bn, M, K, N);
-  const int64_t ldk = tf32_ld(K);
-  float* bhi = reinterpret_cast<float*>(ws);
-  float* blo = reinterpret_cast<float*>(ws + f32_in_f64(N * ldk));
-  double* part = ws + 2 * f32_in_f64(N * ldk);
-  {
-    const int64_t tiles = ((K + 31) / 32) * ((N + 31) / 32);
-    const int blocks = static_cast<int>(std::min<int64_t>(tiles, 16 * kSMs));
-    trals::tf32_split_kernel<double><<<blocks, 256, 0, s>>>(B, K, N, ldb, 1, bhi, blo, ldk);
-    if (int st = launch_status()) return st;
-  }
-  CUtensorMap maps[4];
-  bool ok = make_map_f32(&maps[0], ahi, K, M, lda, trals::kTcBK, trals::kTcBM) && make_map_f32(&maps[1], alo, K, M, lda, trals::kTcBK, trals::kTcBM);
-  ok = ok && make_map_f32(&maps[2], bhi, K, N, ldk, trals::kTcBK, bn) && make_map_f32(&maps[3], blo, K, N, ldk, trals::kTcBK, bn);
-  if (!ok) return TRALS_ERR_CUDA;
-  trals::TcArgs g{};
-  g.M = M; g.K = K; g.N = N; g.kchunk = sp.kchunk; g.splits = sp.splits;
-  g.cmap = cm; g.C = C; g.ws = part;
-  int st;
-  switch (bn) {
-    case 64: st = launch_tc<64>(maps, g, s); break;
-    case 128: st = launch_tc<128>(maps, g, s); break;
-    default: st = launch_tc<256>(maps, g, s); break;
-  }
-  if (st) return st;
-  if (sp.splits > 1) {
-    GemmArgs r{};
-    r.P = 1; r.M = M; r.N = N; r.splits = sp.splits; r.ws = part; r.C = C; r.cmap = cm; r.alpha = 1.0; r.beta = 0;
-    const int64_t total = M * N;
-    const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 8 * kSMs));
-    trals::splitk_reduce_kernel<<<blocks, 256, 0, s>>>(r);
-    return launch_status();
-  }
-  return TRALS_OK;
-}
 
 // ---------------------------------------------------------------------------
 // int8 tcgen05 digit-sliced GEMM (tc_int8_gemm.cuh): the fp32 variant (OzF32) and
@@ -1487,10 +1378,14 @@ int blocked_solve(const double* U, const double* L, const double* aux, int m, co
 // unconditionally; when it fires it overwrites Z, clears the flag and bumps
 // d_info[TRALS_INFO_FALLBACKS] (report.fallback_count).
 // ---------------------------------------------------------------------------
+// tri != 0: S is instead the QR variants' triangular factor R0 (Lr x m row-major, Lr <= m; the
+// merged R0 of qr_r0.cuh): the SVD is taken of R0 itself (R0 V = U Sigma), so singular values down
+// to eps sigma_max survive, and Z = M V Sigma^{-2} V^T with the cut rcond * sigma_max(R0) --
+// W pinv(R0)^T of the reference with W = M R0^{-1} (solvers.py:262-273, linalg.py:104-112).
 __global__ void __launch_bounds__(1024) pinv_fallback_kernel(const double* __restrict__ S, int m,
                                                              const double* __restrict__ Mr, int64_t rows,
                                                              double* __restrict__ Z, int* __restrict__ info, int mode,
-                                                             double rcond, double* __restrict__ ws) {
+                                                             double rcond, double* __restrict__ ws, int Lr, int tri) {
   const int tid = threadIdx.x, lane = tid & 31, nwarps = blockDim.x >> 5;
   const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
   const int trig_chol = info[TRALS_INFO_CHOL];
@@ -1503,9 +1398,11 @@ __global__ void __launch_bounds__(1024) pinv_fallback_kernel(const double* __res
   double* V = A + static_cast<int64_t>(m2) * m;   // [m2][m2]
   double* sig = V + static_cast<int64_t>(m2) * m2;  // [m2]
   double* coef = sig + m2;                 // [rows][m2]
+  const int L = tri ? Lr : m;  // column length of the Jacobi matrix
   for (int t = tid; t < m2 * m; t += blockDim.x) {
     const int c = t / m, r = t - c * m;
-    A[t] = (c < m) ? 0.5 * (S[r * m + c] + S[c * m + r]) : 0.0;
+    if (tri) A[t] = (c < m && r < L) ? S[r * m + c] : 0.0;
+    else A[t] = (c < m) ? 0.5 * (S[r * m + c] + S[c * m + r]) : 0.0;
   }
   for (int t = tid; t < m2 * m2; t += blockDim.x) V[t] = ((t / m2) == (t % m2)) ? 1.0 : 0.0;
   __syncthreads();
@@ -1522,7 +1419,7 @@ __global__ void __launch_bounds__(1024) pinv_fallback_kernel(const double* __res
         double* ai = A + static_cast<int64_t>(i) * m;
         double* aj = A + static_cast<int64_t>(j) * m;
         double al = 0.0, be = 0.0, ga = 0.0;
-        for (int r = lane; r < m; r += 32) {
+        for (int r = lane; r < L; r += 32) {
           const double x = ai[r], y = aj[r];
           al = fma(x, x, al);
           be = fma(y, y, be);
@@ -1537,7 +1434,7 @@ __global__ void __launch_bounds__(1024) pinv_fallback_kernel(const double* __res
           const double zeta = (be - al) / (2.0 * ga);
           const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
           const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
-          for (int r = lane; r < m; r += 32) {
+          for (int r = lane; r < L; r += 32) {
             const double x = ai[r], y = aj[r];
             ai[r] = c * x - s * y;
             aj[r] = s * x + c * y;
@@ -1560,7 +1457,7 @@ __global__ void __launch_bounds__(1024) pinv_fallback_kernel(const double* __res
   // singular values (= eigenvalues of the PSD part), relative cut
   for (int c = warp; c < m2; c += nwarps) {
     double s2 = 0.0;
-    for (int r = lane; r < m; r += 32) s2 = fma(A[c * m + r], A[c * m + r], s2);
+    for (int r = lane; r < L; r += 32) s2 = fma(A[c * m + r], A[c * m + r], s2);
     for (int o = 16; o > 0; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
     if (lane == 0) sig[c] = sqrt(s2);
   }
@@ -1576,14 +1473,17 @@ __global__ void __launch_bounds__(1024) pinv_fallback_kernel(const double* __res
   // QR modes, squares of R0's), so the cut never goes below that noise floor: mode 0 (gelsy, cond = eps)
   // uses max(rcond, m eps), modes 1/2 map R0's rcond to max(rcond^2, m eps) on S
   const double floor_noise = m * eps;
-  const double cut = (mode == 0 ? fmax(rcond, floor_noise) : fmax(rcond * rcond, floor_noise)) * smax;
-  // Z = M pinv(S) = sum_{sig_i > cut} (M a_i / sig_i^2) v_i^T
+  const double cut = tri ? rcond * smax
+                        : (mode == 0 ? fmax(rcond, floor_noise) : fmax(rcond * rcond, floor_noise)) * smax;
+  // S mode:   Z = M pinv(S) = sum_{sig_i > cut} (M a_i / sig_i^2) v_i^T   (a_i = S v_i = sig_i v_i)
+  // tri mode: Z = M pinv(R0^T R0) = sum_{sig_i > cut} (M v_i / sig_i^2) v_i^T
   for (int t = tid; t < rows * m2; t += blockDim.x) {
     const int64_t r = t / m2;
     const int i = static_cast<int>(t - r * m2);
     double v = 0.0;
     if (sig[i] > cut) {
-      for (int k = 0; k < m; ++k) v = fma(Mr[r * m + k], A[static_cast<int64_t>(i) * m + k], v);
+      const double* vec = tri ? V + static_cast<int64_t>(i) * m2 : A + static_cast<int64_t>(i) * m;
+      for (int k = 0; k < m; ++k) v = fma(Mr[r * m + k], vec[k], v);
       v /= sig[i] * sig[i];
     }
     coef[t] = v;
@@ -2382,20 +2282,6 @@ int env(const double* X, int64_t pre, int64_t post, int side, const double* H, i
   return gemm(X, 0, 1, post, 1, post, pre, RR, H, RR, E, cm, 0, ws, ws_elems, s);
 }
 
-// fp32 variant of env(): X given as its tf32 hi/lo split, stored K-major for this side
-// (side 0: [pre][ldx] as X itself; side 1: [post][ldx], the transposed copy).
-int env_tf32(const float* xhi, const float* xlo, int64_t ldx, int64_t pre, int64_t post, int side, const double* H,
-             int r_lo, int r_hi, double* E, int leaf, double* ws, int64_t ws_elems, cudaStream_t s) {
-  const int64_t RR = static_cast<int64_t>(r_lo) * r_hi;
-  if (side == 0) {
-    CMap cm{0, pre, 0, r_lo, r_hi, 1, pre * r_lo};
-    if (leaf) cm = CMap{0, pre, 0, RR, r_hi, r_hi, 1};
-    return gemm_tc(xhi, xlo, ldx, pre, post, RR, H, RR, E, cm, ws, ws_elems, s);
-  }
-  CMap cm{0, post, 0, r_lo, r_hi, 1, post * r_lo};
-  if (leaf) cm = CMap{0, post, 0, RR, r_hi, r_hi, 1};
-  return gemm_tc(xhi, xlo, ldx, post, pre, RR, H, RR, E, cm, ws, ws_elems, s);
-}
 
 // TRALS_OZ_NOPERM=1 (experiments): keep the natural column order for the short-K env products
 inline bool oz_noperm() {
@@ -2569,6 +2455,8 @@ int run_mttsp(const double* X, int N, const int64_t* dims, const int32_t* ranks,
 
 }  // namespace
 
+#include "qr_r0.cuh"
+
 // ===========================================================================
 // C-ABI
 // ===========================================================================
@@ -2702,34 +2590,6 @@ int trals_env_oz64(const int8_t* xd, const int32_t* xe, int64_t pre, int64_t pos
                               static_cast<cudaStream_t>(stream));
 }
 
-int64_t trals_tf32_ld(int64_t cols) { return cols < 1 ? 0 : tf32_ld(cols); }
-
-int trals_tf32_split_f32(const float* x, int64_t rows, int64_t cols, int64_t ld_in, int transpose, float* hi,
-                         float* lo, int64_t ld_out, void* stream) {
-  if (!x || !hi || !lo || rows < 1 || cols < 1 || ld_in < cols || (transpose != 0 && transpose != 1) ||
-      ld_out < (transpose ? rows : cols))
-    return TRALS_ERR_ARG;
-  const int64_t tiles = ((rows + 31) / 32) * ((cols + 31) / 32);
-  const int blocks = static_cast<int>(std::min<int64_t>(tiles, 16 * kSMs));
-  trals::tf32_split_kernel<float><<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(x, rows, cols, ld_in,
-                                                                                        transpose, hi, lo, ld_out);
-  return launch_status();
-}
-
-int64_t trals_env_tf32_ws_elems(int64_t pre, int64_t post, int side, int r_lo, int r_hi) {
-  const int64_t RR = static_cast<int64_t>(r_lo) * r_hi;
-  return side == 0 ? gemm_tc_ws(pre, post, RR) : gemm_tc_ws(post, pre, RR);
-}
-
-int trals_env_tf32(const float* xhi, const float* xlo, int64_t ldx, int64_t pre, int64_t post, int side,
-                   const double* H, int r_lo, int r_hi, double* E, int leaf, double* ws, int64_t ws_elems,
-                   void* stream) {
-  if (!xhi || !xlo || !H || !E || !ws || pre < 1 || post < 1 || r_lo < 1 || r_hi < 1 || (side != 0 && side != 1) ||
-      ldx < (side == 0 ? post : pre))
-    return TRALS_ERR_ARG;
-  return env_tf32(xhi, xlo, ldx, pre, post, side, H, r_lo, r_hi, E, leaf, ws, ws_elems,
-                  static_cast<cudaStream_t>(stream));
-}
 
 int trals_absorb_right_f64(const double* E, int Ra, int64_t pre, int64_t Ib, int Rb, int Rb1, const double* core_zt,
                            double* out, int leaf, double* ws, int64_t ws_elems, void* stream) {
@@ -2968,8 +2828,35 @@ int trals_spd_fallback_f64(const double* S, int m, const double* Mr, int64_t row
                            double rcond, double* ws, int64_t ws_elems, void* stream) {
   if (!S || !Mr || !Z || !info || !ws || m < 1 || rows < 1 || mode < 0 || mode > 2) return TRALS_ERR_ARG;
   if (ws_elems < trals_spd_fallback_ws_elems(rows, m)) return TRALS_ERR_WORKSPACE;
-  pinv_fallback_kernel<<<1, 1024, 0, static_cast<cudaStream_t>(stream)>>>(S, m, Mr, rows, Z, info, mode, rcond, ws);
+  pinv_fallback_kernel<<<1, 1024, 0, static_cast<cudaStream_t>(stream)>>>(S, m, Mr, rows, Z, info, mode, rcond, ws,
+                                                                           m, 0);
   return launch_status();
+}
+
+int trals_tri_fallback_f64(const double* R0, int Lr, int m, const double* Mr, int64_t rows, double* Z, int* info,
+                           int mode, double rcond, double* ws, int64_t ws_elems, void* stream) {
+  if (!R0 || !Mr || !Z || !info || !ws || m < 1 || Lr < 1 || Lr > m || rows < 1 || mode < 1 || mode > 2)
+    return TRALS_ERR_ARG;
+  if (ws_elems < trals_spd_fallback_ws_elems(rows, m)) return TRALS_ERR_WORKSPACE;
+  pinv_fallback_kernel<<<1, 1024, 0, static_cast<cudaStream_t>(stream)>>>(R0, m, Mr, rows, Z, info, mode, rcond, ws,
+                                                                           Lr, 1);
+  return launch_status();
+}
+
+int64_t trals_r0_merge_ws_elems(int N, int n, const int32_t* ranks, const int32_t* ks) {
+  if (N < 2 || n < 0 || n >= N || !ranks || !ks) return -1;
+  return r0_ws(N, n, ranks, ks).total;
+}
+
+int trals_r0_merge_f64(int N, int n, const int32_t* ranks, const int32_t* ks, const double* const* rt, double* R0,
+                       double* ws, int64_t ws_elems, void* stream) {
+  if (N < 2 || n < 0 || n >= N || !ranks || !ks || !rt || !R0 || !ws) return TRALS_ERR_ARG;
+  return r0_merge(N, n, ranks, ks, rt, R0, ws, ws_elems, static_cast<cudaStream_t>(stream));
+}
+
+int trals_tri_prepare_f64(double* U, int m, double* F, double* aux, int check_degen, int* info, void* stream) {
+  if (!U || !F || !aux || !info || m < 1) return TRALS_ERR_ARG;
+  return tri_prepare(U, m, F, aux, check_degen, info, static_cast<cudaStream_t>(stream));
 }
 
 int64_t trals_core_qr_ws_elems(int I, int RR) { return hh_supported(I, RR) ? hh_plan(I, RR).ws : -1; }

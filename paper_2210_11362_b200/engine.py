@@ -173,6 +173,21 @@ class SweepEngine:
             if min(qws) < 0:
                 raise ValueError("per-core QR size outside the kernel envelope")
             self.qr_ws = self._empty(max(1, max(qws)))
+        # QR / ALS: R0 from orthogonal merges of the R-tensors (QR) or of the cores (ALS), never
+        # from chol(S_n) -- the R-tensors are kept per core in layout C
+        self.use_r0 = self.variant in ("qr", "als")
+        if self.use_r0:
+            if self.variant == "qr":
+                self.r0_ks = [min(self.dims[j], self.R(j) * self.R(j + 1)) for j in range(N)]
+                self.RtC = [self._empty(self.R(j), self.r0_ks[j], self.R(j + 1)) for j in range(N)]
+            else:
+                self.r0_ks = list(self.dims)
+                self.RtC = self.Gc
+            ks_a = L.i32_array(self.r0_ks)
+            need = max(self.lib.trals_r0_merge_ws_elems(N, n, L.i32_array(self.ranks), ks_a) for n in range(N))
+            if need < 0:
+                raise ValueError("R0 merge outside the kernel envelope")
+            self.r0_ws = self._empty(max(1, need))
         self.fb_ws = self._empty(max(1, max(self.lib.trals_spd_fallback_ws_elems(self.dims[n], self.R(n) * self.R(n + 1))
                                             for n in range(N))))
         self.info = torch.zeros(L.INFO_SLOTS, dtype=torch.int32, device=self.dev)
@@ -193,6 +208,7 @@ class SweepEngine:
         self._join_ev = torch.cuda.Event() if self.dev.type == "cuda" else None
         self._cur = None
         self.graph = None
+        self.graph_err = None
         self.graph_exact = None
 
     # local views used by the X contractions
@@ -411,6 +427,14 @@ class SweepEngine:
             cur, sa, sb = self._absorb_left(cur, sa, sb, leaf)
         self._tree(cur, m + 1, b)
 
+    def _r0_rows(self, n):
+        """Rows of the reference's R0 for mode n: min(prod_{j!=n} k_j, R_n R_{n+1})."""
+        ks = 1
+        for j in range(self.N):
+            if j != n:
+                ks *= self.r0_ks[j]
+        return min(ks, self.R(n) * self.R(n + 1))
+
     def _r0_nonsquare(self, n):
         """QR / ALS: the reference's triangular factor is non-square when it has fewer rows
         than R_n R_{n+1} -- QR: prod_{j!=n} k_j with k_j = min(I_j, R_j R_{j+1})
@@ -442,14 +466,31 @@ class SweepEngine:
                                                   self.side_gws.data_ptr(), self.side_gws.numel(), self._sp()),
                     "gram_chain")
         self.steps.append(Step("other", gram_chain, f"S{n}", stream="side"))
-        check_degen = 1 if self.variant in ("qr", "als") else 0
+        if self.use_r0:
+            # QR (solvers.py:422-424) / ALS (:337-339): R0 by merging the R-tensors (the cores) one at
+            # a time with a Householder QR after every merge; then its inverse operands and the 1e-13
+            # degeneracy test (linalg.py:96-99)
+            ks_a = L.i32_array(self.r0_ks)
 
-        def factor(S=S, rr=rr, check_degen=check_degen):
+            def r0(n=n, ranks_a=ranks_a, ks_a=ks_a):
+                rt = L.ptr_array([t.data_ptr() for t in self.RtC])
+                L.check(self.lib.trals_r0_merge_f64(N, n, ranks_a, ks_a, rt, self.U.data_ptr(), self.r0_ws.data_ptr(),
+                                                    self.r0_ws.numel(), self._sp()), "r0_merge")
+            self.steps.append(Step("gramqr", r0, f"R0 {n}", stream="side"))
+
+            def tri(rr=rr):
+                L.check(self.lib.trals_tri_prepare_f64(self.U.data_ptr(), rr, self.Lo.data_ptr(),
+                                                       self.chol_aux.data_ptr(), 1, self.info.data_ptr(),
+                                                       self._sp()), "tri_prepare")
+            if not self._r0_nonsquare(n):
+                self.steps.append(Step("solve", tri, f"tri{n}", stream="side"))
+            return
+
+        def factor(S=S, rr=rr):
             L.check(self.lib.trals_cholesky_f64(S.data_ptr(), rr, self.U.data_ptr(), self.Lo.data_ptr(),
-                                                self.chol_aux.data_ptr(), check_degen, self.info.data_ptr(),
+                                                self.chol_aux.data_ptr(), 0, self.info.data_ptr(),
                                                 self._sp()), "cholesky")
-        if not self._r0_nonsquare(n):
-            self.steps.append(Step("solve", factor, f"chol{n}", stream="side"))
+        self.steps.append(Step("solve", factor, f"chol{n}", stream="side"))
 
     def _solve(self, n):
         """Steps for one block update once M_n is complete (local rows)."""
@@ -473,17 +514,24 @@ class SweepEngine:
         # numerical fallbacks of the reference (linalg.py:77-81, solvers.py:262-273): the kernel is a
         # no-op unless the factorisation flagged a failure, so it stays in the (graph-captured) sweep
         rr_rows = self.dims[n]
-        if self.variant in ("qr", "als"):
+        if self.use_r0:
+            # solvers.py:262-273: the min-norm solve on R0 itself -- always for a non-square R0
+            # (mode 2, uncounted), on a degenerate diagonal when the fallback is enabled (mode 1)
             mode = 2 if self._r0_nonsquare(n) else (1 if self.fallback_ok else None)
-            rcond = self.svd_rcond
+            lr = self._r0_rows(n)
+            if mode is not None:
+                def fallback(n=n, M=M, rr=rr, mode=mode, rows=rr_rows, lr=lr):
+                    L.check(self.lib.trals_tri_fallback_f64(self.U.data_ptr(), lr, rr, M.data_ptr(), rows,
+                                                            self.Gt[n].data_ptr(), self.info.data_ptr(), mode,
+                                                            self.svd_rcond, self.fb_ws.data_ptr(), self.fb_ws.numel(),
+                                                            self._sp()), "tri_fallback")
+                self.steps.append(Step("solve", fallback, f"fallback{n}"))
         else:
-            mode, rcond = 0, 2.220446049250313e-16
-        if mode is not None:
-            def fallback(n=n, M=M, rr=rr, mode=mode, rcond=rcond, rows=rr_rows):
+            def fallback(n=n, M=M, rr=rr, rows=rr_rows):
                 L.check(self.lib.trals_spd_fallback_f64(self.S[n].data_ptr(), rr, M.data_ptr(), rows,
-                                                        self.Gt[n].data_ptr(), self.info.data_ptr(), mode, rcond,
-                                                        self.fb_ws.data_ptr(), self.fb_ws.numel(), self._sp()),
-                        "spd_fallback")
+                                                        self.Gt[n].data_ptr(), self.info.data_ptr(), 0,
+                                                        2.220446049250313e-16, self.fb_ws.data_ptr(),
+                                                        self.fb_ws.numel(), self._sp()), "spd_fallback")
             self.steps.append(Step("solve", fallback, f"fallback{n}"))
 
         def refresh(n=n):
@@ -516,6 +564,9 @@ class SweepEngine:
                                            self.qr_ws.data_ptr(), self.qr_ws.numel(), sp), "core_qr")
         L.check(self.lib.trals_core_relayout_f64(self.Rmat.data_ptr(), L.LAYOUT_ZT, ra, k, rb,
                                                  self.Rslice.data_ptr(), L.LAYOUT_SLICE, sp), "relayout")
+        if self.use_r0:
+            L.check(self.lib.trals_core_relayout_f64(self.Rmat.data_ptr(), L.LAYOUT_ZT, ra, k, rb,
+                                                     self.RtC[n].data_ptr(), L.LAYOUT_C, sp), "relayout")
         L.check(self.lib.trals_core_gram_f64(self.Rslice.data_ptr(), ra, k, rb, self.E[n].data_ptr(),
                                              self.gws.data_ptr(), self.gws.numel(), sp), "core_gram")
 
@@ -750,19 +801,26 @@ class SweepEngine:
 
     # ------------------------------------------------------------ CUDA graphs
     def capture(self, with_error=True, exact=False):
-        """Capture one sweep (+ the error terms into `err_cur`) as a CUDA graph.
+        """Capture one sweep as a CUDA graph, and the error terms (into `err_cur`) as a second one.
 
-        Every buffer is owned by the engine, so the graph stays valid for the
-        engine's lifetime; replaying it re-launches the identical kernel list
-        with a single host call (the small configs are launch-bound)."""
+        Every buffer is owned by the engine, so the graphs stay valid for the
+        engine's lifetime; replaying re-launches the identical kernel list with a
+        single host call (the small configs are launch-bound).  The error has its
+        own graph so a caller can time the sweep alone (AlsReport.iter_seconds
+        excludes the error, solvers.py:111-116).  A sharded sweep can be captured
+        only over NCCL (its all-reduces become graph nodes); gloo collectives are
+        host-side and stay eager."""
         if not self.x.is_cuda:
             raise RuntimeError("graphs need a CUDA engine")
         if self.world > 1:
-            raise RuntimeError("sharded sweeps run eagerly (collectives between kernels)")
+            import torch.distributed as dist
+            if dist.get_backend(self.group) != "nccl":
+                raise RuntimeError("sharded sweeps capture only over NCCL (collectives between kernels)")
         old = self.stream
         cap = torch.cuda.Stream(device=self.dev)
         cap.wait_stream(old)
         g = torch.cuda.CUDAGraph()
+        ge = torch.cuda.CUDAGraph() if with_error else None
         self.stream = cap
         try:
             with torch.cuda.stream(cap):
@@ -770,20 +828,26 @@ class SweepEngine:
                 # happen inside the capture when no eager sweep preceded it
                 g.capture_begin(capture_error_mode="relaxed")
                 self.run_sweep()
-                if with_error:
-                    self.error_step(self.err_cur, exact=exact)
                 g.capture_end()
+                if with_error:
+                    ge.capture_begin(capture_error_mode="relaxed")
+                    self.error_step(self.err_cur, exact=exact)
+                    ge.capture_end()
         finally:
             self.stream = old
         old.wait_stream(cap)
         self.graph = g
+        self.graph_err = ge
         self.graph_exact = exact
         return g
 
-    def replay(self):
-        """Replay the captured sweep on the engine's stream."""
+    def replay(self, sweep=True, error=True):
+        """Replay the captured sweep and/or its error graph on the engine's stream."""
         with torch.cuda.stream(self.stream):
-            self.graph.replay()
+            if sweep:
+                self.graph.replay()
+            if error and self.graph_err is not None:
+                self.graph_err.replay()
 
     def mttsp_flops_per_sweep(self):
         """Algorithmic RHS flops of one sweep: sum_n 2 |X| R_n R_{n+1}."""

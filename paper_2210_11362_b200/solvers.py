@@ -141,12 +141,9 @@ def _run(x, config, variant):
     t = _host_or_device_tensor(x, config.dtype)
     dims = tuple(int(d) for d in t.shape)
     N = len(dims)
-    ranks = check_ranks(config.ranks, N)
-    if config.error_mode == "exact":
-        check_element_budget(dims, config.element_budget)
     if not torch.cuda.is_available():
         raise RuntimeError("paper_2210_11362_b200 needs a CUDA device (no CPU fallback)")
-    L.lib()  # fail loudly if the extension is missing
+    lib = L.lib()  # fail loudly if the extension is missing
 
     report = AlsReport(variant=variant)
     dist = _dist_context()
@@ -160,25 +157,41 @@ def _run(x, config, variant):
         lo, hi = _slab(dims[shard], world, rank)
         src = t.narrow(shard, lo, hi - lo)
     from .engine import SweepEngine
-    key = (dims, tuple(ranks), variant, dev.index, world, shard, lo, hi, bool(config.rank_deficient_fallback),
+    try:
+        rk = tuple(int(r) for r in config.ranks)
+    except (TypeError, ValueError):
+        rk = None
+    key = (dims, rk, variant, dev.index, world, shard, lo, hi, bool(config.rank_deficient_fallback),
            float(config.svd_rcond), config.dtype, bool(config.debug_checks), config.fp64_gemm)
     eng = _PLAN_CACHE.pop(key, None)
-    if eng is None:
-        x_local = torch.empty(tuple(src.shape), dtype=t.dtype, device=dev)
-    else:
-        x_local = eng.x
+    x_local = eng.x if eng is not None else torch.empty(tuple(src.shape), dtype=t.dtype, device=dev)
     if src.is_cuda:
         x_local.copy_(src)
     else:
         if not src.is_contiguous():
             src = src.contiguous()
         x_local.copy_(src, non_blocking=bool(src.is_pinned()))
+    # check_dense_tensor's finiteness test comes before the rank and budget checks
+    # (solvers.py:235-242 -> validation.py:43-55); here it is one pass over X on the device
+    xn_dev = _sumsq_device(lib, x_local, dev)
+    if world > 1:
+        import torch.distributed as tdist
+        tdist.all_reduce(xn_dev, group=group)
+    xn = xn_dev.cpu().numpy()
+    if xn[1] > 0:
+        if eng is not None:
+            _PLAN_CACHE[key] = eng
+        raise ValueError("tensor contains non-finite entries")  # validation.py:53-54
+    ranks = check_ranks(config.ranks, N)
+    if config.error_mode == "exact":
+        check_element_budget(dims, config.element_budget)
     if eng is None:
         eng = SweepEngine(x_local, dims, ranks, variant, shard_mode=shard, lo=lo, hi=hi, group=group,
                           world_size=world, rank_deficient_fallback=config.rank_deficient_fallback,
                           svd_rcond=config.svd_rcond, debug_checks=config.debug_checks,
                           fp64_gemm=config.fp64_gemm)
     eng.stream = torch.cuda.current_stream(dev)
+    eng.xnorm2.copy_(xn_dev)
     p0 = torch.cuda.Event(enable_timing=True)
     p1 = torch.cuda.Event(enable_timing=True)
     p0.record(eng.stream)
@@ -189,9 +202,6 @@ def _run(x, config, variant):
     _PLAN_CACHE[key] = eng
     while len(_PLAN_CACHE) > _PLAN_CACHE_MAX:
         _PLAN_CACHE.pop(next(iter(_PLAN_CACHE)))
-    xn = eng.compute_xnorm2().cpu().numpy()
-    if xn[1] > 0:
-        raise ValueError("tensor contains non-finite entries")  # validation.py:53-54
     xnorm2 = float(xn[0])
     if xnorm2 == 0.0:  # solvers.py:289-291
         report.termination = "zero_input"
@@ -216,7 +226,7 @@ def _run(x, config, variant):
 
     track = config.error_mode in ("exact", "cheap")
     exact = config.error_mode == "exact"
-    use_graph = (world == 1 and not config.timing_buckets and not config.debug_checks)
+    use_graph = (not config.timing_buckets and not config.debug_checks and (world == 1 or _nccl(group)))
     if use_graph and (eng.graph is None or eng.graph_exact != exact):
         eng.capture(with_error=True, exact=exact)
     errs = torch.zeros((config.max_iters, 3), dtype=torch.float64, device=x_local.device)
@@ -228,10 +238,12 @@ def _run(x, config, variant):
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
         a.record(stream)
+        # iter_seconds covers the sweep only; the error evaluation is excluded (solvers.py:111-116)
         if use_graph:
-            eng.replay()
+            eng.replay(sweep=True, error=False)
             b.record(stream)
             if track:
+                eng.replay(sweep=False, error=True)
                 errs[k].copy_(eng.err_cur)
         else:
             eng.run_sweep(ev)
@@ -247,7 +259,8 @@ def _run(x, config, variant):
                 break
     torch.cuda.synchronize(x_local.device)
     _raise_on_info(eng, config, report)
-    report.upfront_seconds["gramqr"] = t0.elapsed_time(t1) / 1e3
+    if variant != "als":  # tr_als has no prepare step (solvers.py:323-349)
+        report.upfront_seconds["gramqr"] = t0.elapsed_time(t1) / 1e3
     if eng.sliced:  # X's digit planes for the tensor-core environment products (once per call)
         report.upfront_seconds["mttsp"] = p0.elapsed_time(p1) / 1e3
     for a, b, ev in sweep_events:
@@ -261,6 +274,22 @@ def _run(x, config, variant):
     if track:
         report.errors = [float(v) for v in errs[:done, 0].cpu().numpy()]
     return eng.cores_host(), report
+
+
+def _sumsq_device(lib, x, dev):
+    """[sum x^2, #non-finite] of a device tensor (one deterministic pass, tensor_ops.py:237-239)."""
+    import torch
+    out = torch.empty(2, dtype=torch.float64, device=dev)
+    ws = torch.empty(lib.trals_sumsq_ws_elems(), dtype=torch.float64, device=dev)
+    fn = lib.trals_sumsq_f32 if x.dtype == torch.float32 else lib.trals_sumsq_f64
+    L.check(fn(x.data_ptr(), x.numel(), out.data_ptr(), ws.data_ptr(),
+               int(torch.cuda.current_stream(dev).cuda_stream)), "sumsq")
+    return out
+
+
+def _nccl(group):
+    import torch.distributed as tdist
+    return tdist.get_backend(group) == "nccl"
 
 
 _PLAN_CACHE = {}

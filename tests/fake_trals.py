@@ -192,22 +192,6 @@ class FakeTrals:
         return 0
 
     # --- fp32 variant: the 3xTF32 split and the K-major environment product ---
-    def trals_tf32_ld(self, cols):
-        return (int(cols) + 3) // 4 * 4
-
-    def trals_tf32_split_f32(self, x, rows, cols, ld_in, transpose, hi, lo, ld_out, stream):
-        self._count("tf32_split")
-        v = _farr(x, rows * ld_in).reshape(rows, ld_in)[:, :cols]
-        h = (v.view(np.uint32) & np.uint32(0xFFFFE000)).view(np.float32)
-        l = v - h
-        if transpose:
-            h, l = h.T, l.T
-        r, c = h.shape
-        _farr(hi, r * ld_out).reshape(r, ld_out)[:, :c] = h
-        _farr(lo, r * ld_out).reshape(r, ld_out)[:, :c] = l
-        return 0
-
-    # int8 digit slicing (Ozaki-style) of the fp32 variant's product path
     def trals_oz_digits_bytes(self, rows, k):
         return oz_digits_bytes(rows, k)
 
@@ -238,17 +222,6 @@ class FakeTrals:
         a = sum(buf[oz_offsets(rows, k, s)].astype(np.float64) * 2.0 ** (-7 * (s + 1)) for s in range(4))
         a = np.ldexp(a, e[:, None])
         x = np.ascontiguousarray(a if side == 0 else a.T)
-        return self.trals_env_f64(x.ctypes.data, pre, post, side, H, r_lo, r_hi, E, leaf, ws, ws_elems, stream)
-
-    def trals_env_tf32_ws_elems(self, pre, post, side, r_lo, r_hi):
-        return 1
-
-    def trals_env_tf32(self, xhi, xlo, ldx, pre, post, side, H, r_lo, r_hi, E, leaf, ws, ws_elems, stream):
-        rows, k = (pre, post) if side == 0 else (post, pre)
-        a = (_farr(xhi, rows * ldx).reshape(rows, ldx)[:, :k].astype(np.float64)
-             + _farr(xlo, rows * ldx).reshape(rows, ldx)[:, :k].astype(np.float64))
-        x = a if side == 0 else a.T
-        x = np.ascontiguousarray(x)
         return self.trals_env_f64(x.ctypes.data, pre, post, side, H, r_lo, r_hi, E, leaf, ws, ws_elems, stream)
 
     def trals_sumsq_f32(self, x, n, out, ws, stream):
@@ -394,6 +367,72 @@ class FakeTrals:
             inf[0] = 0
             if mode == 1:
                 inf[2] = 0
+            inf[3] += 1
+        return 0
+
+    def trals_r0_merge_ws_elems(self, N, n, ranks, ks):
+        return 1
+
+    def trals_r0_merge_f64(self, N, n, ranks, ks, rt, R0, ws, ws_elems, stream):
+        """R factor of V_[2] (V = subchain of the given tensors, ring.py:138-152) by the documented
+        recipe: merge one tensor at a time, Householder-compress when the lateral exceeds Ra Rc."""
+        self._count("r0_merge")
+        r = _vals(ranks, N)
+        k = _vals(ks, N)
+        ps = _ptrs(rt, N)
+        order = list(range(n + 1, N)) + list(range(n))
+
+        def tensor(j):
+            return _arr(ps[j], r[j] * k[j] * r[(j + 1) % N]).reshape(r[j], k[j], r[(j + 1) % N]).copy()
+
+        T = tensor(order[0])
+        steps = order[1:] if len(order) > 1 else [None]
+        for t, j in enumerate(steps):
+            last = t + 1 == len(steps)
+            if j is None:
+                T2 = T
+            else:
+                R = tensor(j)
+                a_, m_, _ = T.shape
+                T2 = np.einsum("amb,bic->aimc", T, R).reshape(a_, -1, R.shape[2])  # lateral mu + m i
+            Ra, rows, Rc = T2.shape
+            mat = T2.transpose(1, 0, 2).reshape(rows, Ra * Rc)  # column c + Rc a
+            if rows > Ra * Rc or last:
+                rr = np.linalg.qr(mat, mode="r")
+                sg = np.sign(np.diagonal(rr)).copy()
+                sg[sg == 0] = 1.0
+                mat = rr * sg[:, None]
+            if last:
+                _arr(R0, mat.size)[:] = mat.ravel()
+                return 0
+            T = mat.reshape(-1, Ra, Rc).transpose(1, 0, 2).copy()
+        return 0
+
+    def trals_tri_prepare_f64(self, U, m, F, aux, check_degen, info, stream):
+        self._count("tri_prepare")
+        u = np.triu(_arr(U, m * m).reshape(m, m))
+        _arr(U, m * m)[:] = u.ravel()
+        _arr(F, m * m)[:] = u.T.ravel()
+        if check_degen:
+            d = np.abs(np.diagonal(u))
+            if d.min() <= 1e-13 * np.max(np.abs(u)):
+                _iarr(info, 4)[2] = int(np.argmin(d)) + 1
+        return 0
+
+    def trals_tri_fallback_f64(self, R0, Lr, m, M, rows, Z, info, mode, rcond, ws, ws_elems, stream):
+        self._count("fallback")
+        inf = _iarr(info, 4)
+        fire = (inf[2] != 0) if mode == 1 else True
+        if not fire:
+            return 0
+        r0 = _arr(R0, Lr * m).reshape(Lr, m)
+        rhs = _arr(M, rows * m).reshape(rows, m)
+        _, sig, vt = np.linalg.svd(r0, full_matrices=False)
+        keep = sig > rcond * sig[0]
+        v = vt[keep].T
+        _arr(Z, rows * m)[:] = (((rhs @ v) / sig[keep] ** 2) @ v.T).ravel()
+        if mode == 1:
+            inf[2] = 0
             inf[3] += 1
         return 0
 

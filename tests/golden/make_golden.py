@@ -117,6 +117,28 @@ def io_and_synth_cases():
     print("wrote io_3x4x5.dten, synth_kinds.npz", flush=True)
 
 
+def r0_cases():
+    """Per-mode R0 of TR-ALS-QR (solvers.py:417-424: mode2_qr of every core, V = subchain_skip of the
+    R-tensors, qr_economy of its cyclic 2-unfolding) and of Alg. 1 (solvers.py:337-339: the same with
+    the cores themselves), from each small ring's initial cores -- the pins of the GPU R0 merges."""
+    from tenring import linalg
+    rec = {}
+    for name in ("spec_n3_i30_r3", "nonuni_n4", "n5_i6", "n2_mat", "odd_n3", "rankdef_n3"):
+        g = np.load(os.path.join(OUT, f"{name}.npz"))
+        N = len(g["dims"])
+        init = [g[f"init_{j}"] for j in range(N)]
+        rts = [ring.mode2_qr(c).r_tensor for c in init]
+        for j, r in enumerate(rts):
+            rec[f"{name}_rt_{j}"] = r
+        for n in range(N):
+            _, r0 = linalg.qr_economy(tensor_ops.cyclic_unfold(ring.subchain_skip(rts, n), 1))
+            rec[f"{name}_qr_r0_{n}"] = r0
+            _, ra = linalg.qr_economy(tensor_ops.cyclic_unfold(ring.subchain_skip(init, n), 1))
+            rec[f"{name}_als_r0_{n}"] = ra
+    np.savez_compressed(os.path.join(OUT, "r0_modes.npz"), **rec)
+    print("wrote r0_modes.npz", flush=True)
+
+
 BASE_CONFIGS = {
     # name: (order, dim, rank_true, noise, seed_data, rank_fit, seed_init, sweeps, variants)
     "c1": (3, 100, 5, 1e-3, 0, 5, 1, 10, ("ne", "als")),
@@ -166,9 +188,13 @@ if __name__ == "__main__":
     if args.only == "io":
         io_and_synth_cases()
         sys.exit(0)
+    if args.only == "r0":
+        r0_cases()
+        sys.exit(0)
     if args.only is None:
         small_cases()
         io_and_synth_cases()
+        r0_cases()
     if args.big or args.only:
         for name in BASE_CONFIGS:
             if args.only and name != args.only:

@@ -100,14 +100,10 @@ def test_schedule_one_sweep_vs_oracle(N, dims, ranks):
         assert rel(cores[j], ocores[j]) < 1e-9
 
 
-SEMI_NORMAL_QR = pytest.mark.xfail(
-    reason="QR variant R0 = chol(S) (semi-normal, DESIGN.md 4.5) cannot resolve R0 singular values below "
-           "~sqrt(eps) that the reference's Householder QR of V keeps; structured R0 is next-round work",
-    strict=False)
 
 
-@pytest.mark.parametrize("variant", ["ne", pytest.param("qr", marks=SEMI_NORMAL_QR), "qrne",
-                                     pytest.param("als", marks=SEMI_NORMAL_QR)])
+@pytest.mark.parametrize("variant", ["ne", "qr", "qrne",
+                                     "als"])
 def test_rank_deficient_fallback_schedule(variant):
     """prod_{j!=n} I_j < R^2: the fallback step of the schedule fires and errors match the reference."""
     g = load_golden(RANKDEF)

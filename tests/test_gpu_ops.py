@@ -169,43 +169,6 @@ def test_reconstruct_and_exact_residual(dims, ranks):
 @pytest.mark.parametrize("pre,post,side,r_lo,r_hi,leaf", [
     (300, 77, 0, 3, 5, 0), (77, 300, 1, 4, 4, 0), (5, 13, 0, 2, 2, 1), (13, 5, 1, 2, 3, 1),
     (129, 1000, 1, 20, 20, 0), (1000, 129, 0, 11, 9, 0), (1600, 4000, 0, 8, 8, 0), (4000, 1600, 1, 8, 8, 1),
-])
-def test_env_tf32_matches_f64(pre, post, side, r_lo, r_hi, leaf):
-    """fp32 variant: the tcgen05 3xTF32 environment product against the fp64 one on the
-    same fp32 X (tails in every dimension, BN 64/128/256, split-K, leaf CMap).  The
-    3xTF32 products are fp32-exact to ~2^-22; the fp32 TMEM accumulation bounds the rest."""
-    from paper_2210_11362_b200 import _lib as L
-    lib = L.lib()
-    rng = np.random.default_rng(pre + post + r_lo)
-    x32 = torch.from_numpy(rng.standard_normal((pre, post)).astype(np.float32)).cuda()
-    K = post if side == 0 else pre
-    H = cuda(rng.standard_normal((K, r_lo * r_hi)))
-    rows = pre if side == 0 else post
-    ld = lib.trals_tf32_ld(K)
-    hi = torch.empty(rows * ld, dtype=torch.float32, device="cuda")
-    lo = torch.empty_like(hi)
-    s = int(torch.cuda.current_stream().cuda_stream)
-    L.check(lib.trals_tf32_split_f32(x32.data_ptr(), pre, post, post, side, hi.data_ptr(), lo.data_ptr(), ld, s), "split")
-    n_out = rows * r_lo * r_hi
-    ref = torch.empty(n_out, dtype=torch.float64, device="cuda")
-    got = torch.empty(n_out, dtype=torch.float64, device="cuda")
-    ws = torch.empty(max(lib.trals_gemm_ws_elems(1, rows, K, r_lo * r_hi), 1 << 22), dtype=torch.float64, device="cuda")
-    x64 = x32.double()
-    L.check(lib.trals_env_f64(x64.data_ptr(), pre, post, side, H.data_ptr(), r_lo, r_hi, ref.data_ptr(), leaf,
-                              ws.data_ptr(), ws.numel(), s), "env_f64")
-    ws32 = torch.empty(lib.trals_env_tf32_ws_elems(pre, post, side, r_lo, r_hi), dtype=torch.float64, device="cuda")
-    L.check(lib.trals_env_tf32(hi.data_ptr(), lo.data_ptr(), ld, pre, post, side, H.data_ptr(), r_lo, r_hi,
-                               got.data_ptr(), leaf, ws32.data_ptr(), ws32.numel(), s), "env_tf32")
-    torch.cuda.synchronize()
-    # hi + lo reproduces X exactly
-    h = hi.view(rows, ld)[:, :K].double() + lo.view(rows, ld)[:, :K].double()
-    assert torch.equal(h, x64 if side == 0 else x64.t())
-    assert rel(got.cpu().numpy(), ref.cpu().numpy()) < 1e-5
-
-
-@pytest.mark.parametrize("pre,post,side,r_lo,r_hi,leaf", [
-    (300, 77, 0, 3, 5, 0), (77, 300, 1, 4, 4, 0), (5, 13, 0, 2, 2, 1), (13, 5, 1, 2, 3, 1),
-    (129, 1000, 1, 20, 20, 0), (1000, 129, 0, 11, 9, 0), (1600, 4000, 0, 8, 8, 0), (4000, 1600, 1, 8, 8, 1),
     (200, 70000, 0, 8, 8, 0), (70000, 150, 1, 6, 8, 0),
 ])
 def test_env_oz_matches_f64(pre, post, side, r_lo, r_hi, leaf):
@@ -413,3 +376,128 @@ def test_env_oz64_extreme_rows():
     assert np.abs(g[7] - exact[7]).max() <= 1e-14 * np.abs(exact[7]).max() + 1e-320
     # row 4: accurate relative to its row maximum (the tiny entries are below the digit window)
     assert np.abs(g[4] - exact[4]).max() <= 1e-13 * np.abs(x[4]).max() * np.abs(h).sum(axis=0).max()
+
+
+# ---------------------------------------------------------------------------
+# R0 without V (TR-ALS-QR solvers.py:422-424, Alg. 1 :337-339): merges + Householder compressions
+# ---------------------------------------------------------------------------
+def _r0_gpu(rts, ranks, n):
+    from paper_2210_11362_b200 import _lib as L
+    lib = L.lib()
+    N = len(rts)
+    ks = [t.shape[1] for t in rts]
+    bufs = [cuda(np.ascontiguousarray(t)) for t in rts]
+    ra, ka = L.i32_array(ranks), L.i32_array(ks)
+    m = ranks[n] * ranks[(n + 1) % N]
+    rows = 1
+    for j in range(N):
+        if j != n:
+            rows *= ks[j]
+    k0 = min(rows, m)
+    out = torch.full((k0, m), float("nan"), dtype=torch.float64, device="cuda")
+    ws = torch.empty(max(1, lib.trals_r0_merge_ws_elems(N, n, ra, ka)), dtype=torch.float64, device="cuda")
+    L.check(lib.trals_r0_merge_f64(N, n, ra, ka, L.ptr_array([b.data_ptr() for b in bufs]), out.data_ptr(),
+                                   ws.data_ptr(), ws.numel(), int(torch.cuda.current_stream().cuda_stream)),
+            "r0_merge")
+    return out.cpu().numpy()
+
+
+@pytest.mark.parametrize("name", ["spec_n3_i30_r3", "nonuni_n4", "n5_i6", "n2_mat", "odd_n3", "rankdef_n3"])
+@pytest.mark.parametrize("variant", ["qr", "als"])
+def test_r0_merge_matches_reference(name, variant):
+    """The reference's per-mode R0 (qr_economy of V_[2], signs included) to 1e-13 of max|R0|."""
+    g = load_golden(name)
+    r0g = load_golden("r0_modes")
+    N = len(g["dims"])
+    ranks = [int(r) for r in g["ranks"]]
+    rts = [r0g[f"{name}_rt_{j}"] if variant == "qr" else g[f"init_{j}"] for j in range(N)]
+    for n in range(N):
+        want = r0g[f"{name}_{variant}_r0_{n}"]
+        got = _r0_gpu(rts, ranks, n)
+        assert got.shape == want.shape
+        assert np.abs(got - want).max() <= 1e-13 * max(1.0, np.abs(want).max()), n
+
+
+@pytest.mark.parametrize("dims,R", [((40, 40, 40, 40), 20), ((30, 30, 30), 12), ((12, 10, 9, 8, 7), 6)])
+def test_r0_merge_large_vs_explicit_qr(dims, R):
+    """A c5-shaped merge (k = 40 < R^2 = 400: 64000 x 400 compressions) against a Householder QR of the
+    explicitly assembled V_[2] (the reference's operation), every mode."""
+    N = len(dims)
+    rng = np.random.default_rng(sum(dims) + R)
+    cores = [rng.standard_normal((R, d, R)) for d in dims]
+    rts = [O.lateral_qr(c).r_tensor for c in cores]
+    for n in range(N):
+        _, want = O.qr_signed(O.unfold_cyclic(O.chain_without(rts, n), 1))
+        got = _r0_gpu(rts, [R] * N, n)
+        assert rel(got, want) < 1e-12, n
+
+
+@pytest.mark.parametrize("m,rows", [(25, 100), (64, 64), (100, 500), (400, 160), (113, 40)])
+def test_tri_prepare_and_solve(m, rows):
+    """Z R0^T = M R0^{-1} ... i.e. Z = M R0^{-1} R0^{-T} through trals_tri_prepare_f64 + trals_chol_solve_f64."""
+    from paper_2210_11362_b200 import _lib as L
+    lib = L.lib()
+    rng = np.random.default_rng(m + rows)
+    _, r0 = O.qr_signed(rng.standard_normal((2 * m, m)))
+    M = rng.standard_normal((rows, m))
+    want = M @ np.linalg.inv(r0.T @ r0)
+    s = int(torch.cuda.current_stream().cuda_stream)
+    U = cuda(r0 + np.tril(rng.standard_normal((m, m)), -1))  # the lower triangle must be ignored
+    F = torch.empty((m, m), dtype=torch.float64, device="cuda")
+    aux = torch.empty(lib.trals_cholesky_aux_elems(m), dtype=torch.float64, device="cuda")
+    info = torch.zeros(4, dtype=torch.int32, device="cuda")
+    L.check(lib.trals_tri_prepare_f64(U.data_ptr(), m, F.data_ptr(), aux.data_ptr(), 1, info.data_ptr(), s), "tri")
+    Md = cuda(M)
+    Z = torch.empty((rows, m), dtype=torch.float64, device="cuda")
+    ws = torch.empty(lib.trals_chol_solve_ws_elems(rows, m), dtype=torch.float64, device="cuda")
+    L.check(lib.trals_chol_solve_f64(U.data_ptr(), F.data_ptr(), aux.data_ptr(), m, Md.data_ptr(), rows,
+                                     Z.data_ptr(), ws.data_ptr(), ws.numel(), s), "solve")
+    assert rel(Z.cpu().numpy(), want) < 1e-11
+    assert int(info[2].item()) == 0
+    np.testing.assert_array_equal(np.tril(U.cpu().numpy(), -1), 0.0)
+
+
+def test_tri_prepare_degeneracy_floor():
+    from paper_2210_11362_b200 import _lib as L
+    lib = L.lib()
+    m = 30
+    rng = np.random.default_rng(3)
+    _, r0 = O.qr_signed(rng.standard_normal((40, m)))
+    r0[17, 17] = 1e-14 * np.abs(r0).max()  # below the 1e-13 floor (linalg.py:96-99)
+    U = cuda(r0)
+    F = torch.empty((m, m), dtype=torch.float64, device="cuda")
+    aux = torch.empty(lib.trals_cholesky_aux_elems(m), dtype=torch.float64, device="cuda")
+    info = torch.zeros(4, dtype=torch.int32, device="cuda")
+    L.check(lib.trals_tri_prepare_f64(U.data_ptr(), m, F.data_ptr(), aux.data_ptr(), 1, info.data_ptr(),
+                                      int(torch.cuda.current_stream().cuda_stream)), "tri")
+    assert int(info[2].item()) == 18
+
+
+@pytest.mark.parametrize("Lr,m,mode", [(30, 30, 1), (12, 30, 2), (400, 400, 1)])
+def test_tri_fallback_min_norm(Lr, m, mode):
+    """linalg.py:104-112 on R0: Z = W pinv(R0)^T with W = M R0^{-1}, i.e. M V Sigma^-2 V^T, cut rcond."""
+    from paper_2210_11362_b200 import _lib as L
+    lib = L.lib()
+    rng = np.random.default_rng(Lr + m)
+    a = rng.standard_normal((max(Lr, 2 * m), m))
+    if mode == 1:
+        a[:, 5] = a[:, 3]  # rank deficient
+    _, r0 = O.qr_signed(a)
+    r0 = r0[:Lr]
+    rows = 17
+    W = rng.standard_normal((rows, Lr))
+    M = W @ r0  # M = W R0
+    want = W @ np.linalg.pinv(r0, rcond=1e-12).T
+    info = torch.zeros(4, dtype=torch.int32, device="cuda")
+    if mode == 1:
+        info[2] = 6
+    Z = torch.zeros((rows, m), dtype=torch.float64, device="cuda")
+    ws = torch.empty(lib.trals_spd_fallback_ws_elems(rows, m), dtype=torch.float64, device="cuda")
+    R0 = cuda(np.ascontiguousarray(r0))
+    Md = cuda(M)
+    L.check(lib.trals_tri_fallback_f64(R0.data_ptr(), Lr, m, Md.data_ptr(), rows, Z.data_ptr(), info.data_ptr(), mode,
+                                       1e-12, ws.data_ptr(), ws.numel(), int(torch.cuda.current_stream().cuda_stream)),
+            "tri_fallback")
+    assert rel(Z.cpu().numpy(), want) < 1e-9
+    inf = info.cpu().numpy()
+    assert inf[2] == 0 and inf[3] == (1 if mode == 1 else 0)

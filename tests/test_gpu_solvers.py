@@ -92,14 +92,10 @@ def test_tol_termination():
     assert rep.n_iters == len(orep.iter_seconds)
 
 
-SEMI_NORMAL_QR = pytest.mark.xfail(
-    reason="QR variant R0 = chol(S) (semi-normal, DESIGN.md 4.5) cannot resolve R0 singular values below "
-           "~sqrt(eps) that the reference's Householder QR of V keeps; structured R0 is next-round work",
-    strict=False)
 
 
-@pytest.mark.parametrize("variant", ["ne", pytest.param("qr", marks=SEMI_NORMAL_QR), "qrne",
-                                     pytest.param("als", marks=SEMI_NORMAL_QR)])
+@pytest.mark.parametrize("variant", ["ne", "qr", "qrne",
+                                     "als"])
 @pytest.mark.parametrize("mode", ["cheap", "exact"])
 def test_rank_deficient_blocks(variant, mode):
     """prod_{j!=n} I_j < R^2: Cholesky fails (NE/QRNE -> gelsy fallback, counted) or R0 is

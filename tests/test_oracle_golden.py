@@ -82,3 +82,95 @@ def test_c1_oracle_matches_reference_run():
     assert np.max(np.abs(np.array(rep.errors) - g["ne_exact_errors"])) < 1e-12
     for j in range(order):
         assert rel(cores[j], g[f"ne_core_{j}"]) < 1e-10
+
+
+# ---------------------------------------------------------------------------
+# the memory-lean oracle (oracle/lean.py, the c5 golden generator) pinned to the reference
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("name", ["nonuni_n4", "n5_i6", "odd_n3", "spec_n3_i30_r3"])
+def test_lean_oracle_small_goldens(name):
+    """The blocked MTTSP / TSQR restatement reproduces the reference's per-sweep exact errors and cores."""
+    from oracle import lean
+    g = load_golden(name)
+    N = len(g["dims"])
+    ranks = tuple(int(r) for r in g["ranks"])
+    init = golden_cores(g, "init", N)
+    for v in ("ne", "qr", "qrne"):
+        if f"{v}_exact_errors" not in g:
+            continue
+        run = lean.solve(g["x"], v, ranks, init, int(g["sweeps"]))
+        assert np.max(np.abs(np.array(run.exact_errors) - g[f"{v}_exact_errors"])) < 1e-12
+        assert np.max(np.abs(np.array(run.cheap_errors) - g[f"{v}_cheap_errors"])) < 1e-9
+        for j in range(N):
+            assert rel(run.cores[j], g[f"{v}_core_{j}"]) < 1e-10
+
+
+def test_lean_oracle_c2_reference_run():
+    """c2 (64^4, R8): lean synth vs the reference's X, lean NE sweeps vs the reference's recorded errors
+    (first 3 sweeps) and one sweep from the reference's sweep-2 state vs its sweep-3 cores."""
+    from oracle import lean
+    g = load_golden("base_c2")
+    order, dim, rt, sd, rf, si, sweeps = (int(v) for v in g["recipe"])
+    x, _ = lean.synth(O.Recipe(order=order, dim=dim, rank=rt, noise=float(g["noise"]), seed=sd))
+    flat = x.ravel()
+    assert abs(np.dot(flat, flat) - g["x_sumsq"]) <= 1e-12 * g["x_sumsq"]
+    assert np.allclose(flat[g["x_sample_idx"]], g["x_samples"], rtol=1e-12, atol=0)
+    init = O.gaussian_ring([dim] * order, [rf] * order, O.philox(si))
+    run = lean.solve(x, "ne", [rf] * order, init, 3, exact=False)
+    assert np.max(np.abs(np.array(run.cheap_errors) - g["ne_exact_errors"][:3])) < 1e-11
+    one = lean.solve(x, "ne", [rf] * order, golden_cores(g, "ne_state2_core", order), 1, exact=False)
+    assert abs(one.cheap_errors[0] - float(g["ne_state3_cheap_error"])) < 1e-12
+    for j in range(order):
+        assert rel(one.cores[j], g[f"ne_state3_core_{j}"]) < 1e-10
+
+
+def test_block_stepper_is_the_oracle_sweep():
+    """bench.py's CPU legs time BlockStepper: N steps from the init cores == one oracle sweep."""
+    g = load_golden("nonuni_n4")
+    N = len(g["dims"])
+    ranks = tuple(int(r) for r in g["ranks"])
+    init = golden_cores(g, "init", N)
+    for v in ("ne", "qr", "qrne"):
+        st = O.BlockStepper(g["x"], v, ranks, init)
+        st.prepare()
+        for k in range(2 * N):
+            st.step(k % N)
+        oc, _ = O.solve(g["x"], v, O.Config(ranks=ranks, max_iters=2, init_cores=init, error_mode="none"))
+        for a, b in zip(st.cores, oc):
+            assert np.array_equal(a, b)
+
+
+# ---------------------------------------------------------------------------
+# R0 without V (TR-ALS-QR / Alg. 1): the merge-and-compress recipe of include/trals.h
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("name", ["spec_n3_i30_r3", "nonuni_n4", "n5_i6", "n2_mat", "odd_n3", "rankdef_n3"])
+@pytest.mark.parametrize("variant", ["qr", "als"])
+def test_r0_merge_recipe_matches_reference(name, variant):
+    """The documented R0 recipe (merge one R-tensor at a time, Householder-compress whenever the
+    lateral exceeds R_a R_c) reproduces the reference's qr_economy(V_[2]) R0 for every mode, in the
+    numpy model of the C-ABI (the GPU kernels are pinned to the same goldens in test_gpu_ops)."""
+    import ctypes
+    import torch
+    from fake_trals import FakeTrals
+    from paper_2210_11362_b200 import _lib as L
+    g = load_golden(name)
+    r0g = load_golden("r0_modes")
+    N = len(g["dims"])
+    dims = [int(d) for d in g["dims"]]
+    ranks = [int(r) for r in g["ranks"]]
+    if variant == "qr":
+        rts = [r0g[f"{name}_rt_{j}"] for j in range(N)]
+    else:
+        rts = [g[f"init_{j}"] for j in range(N)]
+    ks = [t.shape[1] for t in rts]
+    bufs = [torch.from_numpy(np.ascontiguousarray(t)) for t in rts]
+    fake = FakeTrals()
+    for n in range(N):
+        want = r0g[f"{name}_{variant}_r0_{n}"]
+        out = torch.zeros(want.size, dtype=torch.float64)
+        assert fake.trals_r0_merge_f64(N, n, L.i32_array(ranks), L.i32_array(ks),
+                                       L.ptr_array([b.data_ptr() for b in bufs]), ctypes.c_void_p(out.data_ptr()),
+                                       None, 0, None) == 0
+        got = out.numpy().reshape(want.shape)
+        scale = max(1.0, np.abs(want).max())
+        assert np.abs(got - want).max() <= 1e-13 * scale, (n, np.abs(got - want).max())
