@@ -299,7 +299,7 @@ def run_ours(args):
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     from paper_2210_11362_b200 import _lib as L
-    from paper_2210_11362_b200.engine import SweepEngine
+    from paper_2210_11362_b200.engine import OZ64_MAX_RHO, SweepEngine
     from paper_2210_11362_b200.host import make_rng, random_cores
     from paper_2210_11362_b200.solvers import AlsConfig, _slab, decompose
     from paper_2210_11362_b200.synthetic import make_dataset_device
@@ -323,6 +323,11 @@ def run_ours(args):
     cores0 = random_cores(dims, ranks, make_rng(si))
     eng = SweepEngine(x_local, dims, ranks, args.variant, shard_mode=shard if world > 1 else None, lo=lo, hi=hi,
                       world_size=world, fp64_gemm=args.fp64_gemm)
+    # the accuracy guard of fp64_gemm="auto" (include/trals.h), as decompose() applies it
+    rho = eng.x_dynamic_range()
+    if args.fp64_gemm == "auto" and eng.oz64 and rho > OZ64_MAX_RHO:
+        eng = SweepEngine(x_local, dims, ranks, args.variant, shard_mode=shard if world > 1 else None, lo=lo,
+                          hi=hi, world_size=world, fp64_gemm="dmma")
     eng_gemm = eng.fp64_gemm
     p0 = torch.cuda.Event(enable_timing=True)
     p1 = torch.cuda.Event(enable_timing=True)
@@ -525,6 +530,7 @@ def run_ours(args):
                    "step": "one full sweep + per-sweep relative error (cheap identity)",
                    "fp64_gemm": None if fp32 else eng_gemm,
                    "x_digits_ms": prep_ms if (fp32 or oz64) else None,
+                   "x_row_range_rho": rho if not fp32 else None,
                    "launch": launch_note},
         "contraction_tflops": F / sweep_s / 1e12,
         "contraction_roofline_frac": t_roof / sweep_s,

@@ -215,6 +215,20 @@ int64_t trals_spd_fallback_ws_elems(int64_t rows, int m);
 int trals_spd_fallback_f64(const double* d_S, int m, const double* d_M, int64_t rows, double* d_Z, int* d_info,
                            int mode, double rcond, double* d_ws, int64_t ws_elems, void* stream);
 
+/* Accuracy contract of the digit-sliced fp64 products (trals_env_oz64, trals_residual_oz64):
+ * every K-major row a of the sliced operand is held to 2^-56.9 of its own maximum (7 balanced
+ * radix-254 digits), so an output's error is <= 2^-56.9 (max|a| sum|h| + max|h| sum|a|) plus
+ * the dropped pair level (the same order) -- relative to each row's maximum, where a dgemm's
+ * bound is eps sum|a||h|.  The two agree within a small factor when no row has a wide dynamic
+ * range; trals_oz_range_f64 measures it for X: d_out[0] = max over the K-major rows (rows of X
+ * for transpose = 0, columns for transpose = 1) of rho = max|x| K / sum|x|.  The solvers'
+ * fp64_gemm = "auto" takes the int8 engine only when rho <= 2^12 for every X-streaming phase
+ * (Gaussian data: rho ~ 5), i.e. when the product's error stays within 2^-44.9 mean|a| sum|h|;
+ * otherwise they use the DMMA pipe (trals_env_f64). */
+int64_t trals_oz_range_ws_elems(int64_t rows, int64_t cols, int transpose);
+int trals_oz_range_f64(const double* d_x, int64_t rows, int64_t cols, int transpose, double* d_out, double* d_ws,
+                       int64_t ws_elems, void* stream);
+
 /* R0 of the QR-stabilised variants without forming V (tr_als_qr, solvers.py:422-424
  * `q0, r0 = qr_economy(cyclic_unfold(subchain_skip(R-tensors, n), 1))`; for Alg. 1 tr_als,
  * solvers.py:337-339, the same with the cores themselves).  h_rt[j] = the R-tensor of core j

@@ -51,6 +51,8 @@ _SIGNATURES = {
     "trals_spd_fallback_f64": (c_int, [_dp, c_int, _dp, c_int64, _dp, _dp, c_int, c_double, _dp, c_int64, c_void_p]),
     "trals_tri_fallback_f64": (c_int, [_dp, c_int, c_int, _dp, c_int64, _dp, _dp, c_int, c_double, _dp, c_int64,
                                        c_void_p]),
+    "trals_oz_range_ws_elems": (c_int64, [c_int64, c_int64, c_int]),
+    "trals_oz_range_f64": (c_int, [_dp, c_int64, c_int64, c_int, _dp, _dp, c_int64, c_void_p]),
     "trals_r0_merge_ws_elems": (c_int64, [c_int, c_int, POINTER(c_int32), POINTER(c_int32)]),
     "trals_r0_merge_f64": (c_int, [c_int, c_int, POINTER(c_int32), POINTER(c_int32), POINTER(c_void_p), _dp, _dp,
                                    c_int64, c_void_p]),

@@ -93,8 +93,12 @@ std::vector<MergeStep> r0_plan(int N, int n, const int32_t* ranks, const int32_t
 }
 
 struct R0Ws {
-  int64_t mat, tbuf, lwork, gemm, total;
+  int64_t mat, tbuf, lwork, gemm, hh, rbuf, total;
 };
+
+// the own Householder kernels (hh_qr: one CTA / TSQR tree / wide) when the step's matrix is inside
+// their envelope (R_a R_c <= ~115 for tall merges), cuSOLVER dgeqrf otherwise (c5: 400 columns)
+inline bool r0_own_qr(const MergeStep& s) { return s.qr && hh_supported(static_cast<int>(s.rows), static_cast<int>(s.ncol)); }
 
 R0Ws r0_ws(int N, int n, const int32_t* ranks, const int32_t* ks) {
   R0Ws w{};
@@ -105,7 +109,10 @@ R0Ws r0_ws(int N, int n, const int32_t* ranks, const int32_t* ks) {
     const int64_t tnext = static_cast<int64_t>(s.Ra) * (s.qr ? std::min(s.rows, s.ncol) : s.rows) * s.Rc;
     w.tbuf = std::max(w.tbuf, tnext);
     if (s.j >= 0) w.gemm = std::max(w.gemm, gemm_ws(s.Ra, s.m, s.Rb, s.k * s.Rc));
-    if (s.qr && h) {
+    if (r0_own_qr(s)) {
+      w.hh = std::max(w.hh, hh_plan(static_cast<int>(s.rows), static_cast<int>(s.ncol)).ws);
+      w.rbuf = std::max(w.rbuf, std::min(s.rows, s.ncol) * s.ncol);
+    } else if (s.qr && h) {
       int lw = 0;
       if (cusolverDnDgeqrf_bufferSize(h, static_cast<int>(s.rows), static_cast<int>(s.ncol), nullptr,
                                       static_cast<int>(s.rows), &lw) == CUSOLVER_STATUS_SUCCESS)
@@ -113,8 +120,8 @@ R0Ws r0_ws(int N, int n, const int32_t* ranks, const int32_t* ks) {
     }
   }
   const int64_t ncol_max = 4096;
-  // Mat | 2 T buffers | tau | lwork | devInfo (2 doubles) | gemm split-K
-  w.total = w.mat + 2 * w.tbuf + ncol_max + w.lwork + 2 + w.gemm;
+  // Mat | 2 T buffers | tau | lwork | devInfo (2 doubles) | gemm split-K | hh_qr workspace | R buffer
+  w.total = w.mat + 2 * w.tbuf + ncol_max + w.lwork + 2 + w.gemm + w.hh + w.rbuf;
   return w;
 }
 
@@ -141,14 +148,28 @@ __global__ void r0_extract_kernel(const double* __restrict__ mat, int64_t ld, in
   }
 }
 
-// N == 2: mat[(c + Rc a) * m + mu] = T[a][mu][c], T of shape (Ra, m, Rc)
-__global__ void r0_layout_kernel(const double* __restrict__ T, int64_t m, int Ra, int Rc, double* __restrict__ mat) {
-  const int64_t total = m * Ra * Rc;
+// N == 2: the lateral unfolding of T (Ra, m, Rc), column c + Rc a: column-major mat[col * m + mu]
+// (rowmajor = 0) or row-major mat[mu * Ra Rc + col] (rowmajor = 1)
+__global__ void r0_layout_kernel(const double* __restrict__ T, int64_t m, int Ra, int Rc, int rowmajor,
+                                 double* __restrict__ mat) {
+  const int64_t ncol = static_cast<int64_t>(Ra) * Rc, total = m * ncol;
   for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
        t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t col = t / m, mu = t - col * m;
     const int64_t a = col / Rc, c = col - a * Rc;
-    mat[t] = T[(a * m + mu) * Rc + c];
+    mat[rowmajor ? mu * ncol + col : t] = T[(a * m + mu) * Rc + c];
+  }
+}
+
+// T_new[a][r][c] = R[r][c + Rc a] (R row-major kk x Ra Rc, already sign-normalised by hh_qr)
+__global__ void r0_tensor_from_rm_kernel(const double* __restrict__ R, int64_t kk, int Ra, int Rc,
+                                         double* __restrict__ out) {
+  const int64_t ncol = static_cast<int64_t>(Ra) * Rc, total = kk * ncol;
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = t / ncol, col = t - r * ncol;
+    const int64_t a = col / Rc, c = col - a * Rc;
+    out[(a * kk + r) * Rc + c] = R[t];
   }
 }
 
@@ -166,37 +187,54 @@ int r0_merge(int N, int n, const int32_t* ranks, const int32_t* ks, const double
   double* work = tau + 4096;
   int* dinfo = reinterpret_cast<int*>(work + w.lwork);
   double* gws = work + w.lwork + 2;
+  double* hws = gws + w.gemm;
+  double* rbuf = hws + w.hh;
+  constexpr int64_t kBig = int64_t(1) << 40;
   const double* T = rt[(n + 1) % N];  // layout C [a][mu][b]
   for (size_t t = 0; t < plan.size(); ++t) {
     const MergeStep& p = plan[t];
     if (p.ncol > 4096) return TRALS_ERR_UNSUPPORTED;
-    // mat[(c + Rc a) * rows + mu + m i] = sum_b T[a][mu][b] Rj[b][i][c]
-    // GEMM batch a: A(a, mu, b) = T[(a m + mu) Rb + b]; B[b][i Rc + c] = Rj (layout C, ldb = k Rc);
-    // C(a, mu, n = i Rc + c) -> a Rc rows + mu + (n / Rc) m + (n % Rc) rows
+    const bool last = (t + 1 == plan.size());
+    const bool own = r0_own_qr(p);
+    double* out = last ? U : tb[t & 1];
+    // T'[a][mu + m i][c] = sum_b T[a][mu][b] Rj[b][i][c]: a DMMA GEMM batched over a, A(a, mu, b) =
+    // T[(a m + mu) Rb + b], B[b][i Rc + c] = Rj (layout C, ldb = k Rc); C(a, mu, n = i Rc + c) lands
+    //   own QR:    row-major  mat[(mu + m i) ncol + c + Rc a]
+    //   cuSOLVER:  col-major  mat[(c + Rc a) rows + mu + m i]
+    //   no QR:     T_new      out[(a rows + mu + m i) Rc + c]   (layout C, nothing to compress)
     if (p.j >= 0) {
-      const CMap cm{static_cast<int64_t>(p.Rc) * p.rows, int64_t(1) << 40, 0, 1, p.Rc, p.m, p.rows};
-      int st = gemm(T, p.m * p.Rb, p.Rb, 1, p.Ra, p.m, p.Rb, p.k * p.Rc, rt[p.j], p.k * p.Rc, mat, cm, 0, gws,
-                    w.gemm, s);
+      const CMap cm = own ? CMap{p.Rc, kBig, 0, p.ncol, p.Rc, p.m * p.ncol, 1}
+                          : p.qr ? CMap{static_cast<int64_t>(p.Rc) * p.rows, kBig, 0, 1, p.Rc, p.m, p.rows}
+                                 : CMap{p.rows * p.Rc, kBig, 0, p.Rc, p.Rc, p.m * p.Rc, 1};
+      int st = gemm(T, p.m * p.Rb, p.Rb, 1, p.Ra, p.m, p.Rb, p.k * p.Rc, rt[p.j], p.k * p.Rc, p.qr ? mat : out, cm,
+                    0, gws, w.gemm, s);
       if (st) return st;
     } else {
       const int64_t total = p.rows * p.ncol;
       const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 8 * kSMs));
-      r0_layout_kernel<<<blocks, 256, 0, s>>>(T, p.m, p.Ra, p.Rc, mat);
+      r0_layout_kernel<<<blocks, 256, 0, s>>>(T, p.m, p.Ra, p.Rc, own ? 1 : 0, mat);
       if (int e = launch_status()) return e;
     }
-    const bool last = (t + 1 == plan.size());
     if (p.qr) {
-      if (cusolverDnDgeqrf(h, static_cast<int>(p.rows), static_cast<int>(p.ncol), mat, static_cast<int>(p.rows), tau,
-                           work, static_cast<int>(w.lwork), dinfo) != CUSOLVER_STATUS_SUCCESS)
-        return TRALS_ERR_CUDA;
-      ++g_launches;
+      const int64_t kk = std::min(p.rows, p.ncol);
+      const int64_t total = kk * p.ncol;
+      const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 8 * kSMs));
+      if (own) {
+        int st = hh_qr(mat, static_cast<int>(p.rows), static_cast<int>(p.ncol), last ? U : rbuf, hws, w.hh, s);
+        if (st) return st;
+        if (!last) {
+          r0_tensor_from_rm_kernel<<<blocks, 256, 0, s>>>(rbuf, kk, p.Ra, p.Rc, out);
+          if (int e = launch_status()) return e;
+        }
+      } else {
+        if (cusolverDnDgeqrf(h, static_cast<int>(p.rows), static_cast<int>(p.ncol), mat, static_cast<int>(p.rows),
+                             tau, work, static_cast<int>(w.lwork), dinfo) != CUSOLVER_STATUS_SUCCESS)
+          return TRALS_ERR_CUDA;
+        ++g_launches;
+        r0_extract_kernel<<<blocks, 256, 0, s>>>(mat, p.rows, kk, p.ncol, p.Rc, 1, last ? 0 : 1, out);
+        if (int e = launch_status()) return e;
+      }
     }
-    const int64_t kk = p.qr ? std::min(p.rows, p.ncol) : p.rows;
-    double* out = last ? U : tb[t & 1];
-    const int64_t total = kk * p.ncol;
-    const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 8 * kSMs));
-    r0_extract_kernel<<<blocks, 256, 0, s>>>(mat, p.rows, kk, p.ncol, p.Rc, p.qr ? 1 : 0, last ? 0 : 1, out);
-    if (int e = launch_status()) return e;
     T = out;
   }
   return TRALS_OK;
@@ -205,9 +243,9 @@ int r0_merge(int N, int n, const int32_t* ranks, const int32_t* ks, const double
 // Inverse of the upper-triangular diagonal block U[p0.., p0..] (pb x pb) of a row-major m x m
 // factor: W = U_bb^{-1} (upper), WT = W^T, both with pitch ldw.  Row-oriented back substitution,
 // one CTA, the block resident in shared memory; columns of W in parallel.
-__global__ void __launch_bounds__(512) tri_inv_kernel(const double* __restrict__ U, int m, int p0_stride, int nb_blk,
+__global__ void __launch_bounds__(512) tri_inv_kernel(double* __restrict__ U, int m, int p0_stride, int nb_blk,
                                                       double* __restrict__ W0, double* __restrict__ WT0,
-                                                      int64_t wstride, int ldw) {
+                                                      int64_t wstride, int ldw, int zero_lower) {
   extern __shared__ __align__(16) double sm[];
   const int b = blockIdx.x;
   const int p0 = b * p0_stride;
@@ -231,6 +269,11 @@ __global__ void __launch_bounds__(512) tri_inv_kernel(const double* __restrict__
     }
     __syncthreads();
   }
+  if (zero_lower)  // the diagonal block's strict lower triangle (the whole matrix when one block covers it)
+    for (int t = threadIdx.x; t < pb * pb; t += blockDim.x) {
+      const int r = t / pb, c = t - r * pb;
+      if (c < r) U[static_cast<int64_t>(p0 + r) * m + p0 + c] = 0.0;
+    }
   double* W = W0 + b * wstride;
   double* WT = WT0 + b * wstride;
   for (int t = threadIdx.x; t < ldw * ldw; t += blockDim.x) {
@@ -242,22 +285,22 @@ __global__ void __launch_bounds__(512) tri_inv_kernel(const double* __restrict__
 }
 
 int tri_prepare(double* U, int m, double* F, double* aux, int check_degen, int* info, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(tri_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    attr = true;
+  }
   if (m <= kInvMax) {
     // F = U^{-1}, aux = U^{-T} (the m <= 112 layout of trals_cholesky_f64)
     const size_t smem = sizeof(double) * 2 * m * (m + 1);
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(tri_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-      attr = true;
-    }
-    tri_inv_kernel<<<1, 512, smem, s>>>(U, m, m, m, F, aux, 0, m);
+    tri_inv_kernel<<<1, 512, smem, s>>>(U, m, m, m, F, aux, 0, m, 1);
     if (int st = launch_status()) return st;
   } else {
     // F = U^T, aux = per 64-row block W_b, W_b^T (the blocked layout of trals_cholesky_f64)
     const int nblk = (m + kBlkNB - 1) / kBlkNB;
     const size_t smem = sizeof(double) * 2 * kBlkNB * (kBlkNB + 1);
     tri_inv_kernel<<<nblk, 512, smem, s>>>(U, m, kBlkNB, kBlkNB, aux, aux + kBlkNB * kBlkNB,
-                                           2 * kBlkNB * kBlkNB, kBlkNB);
+                                           2 * kBlkNB * kBlkNB, kBlkNB, 0);
     if (int st = launch_status()) return st;
     dim3 grid((m + 31) / 32, (m + 31) / 32);
     chol_finalize_kernel<<<grid, dim3(32, 8), 0, s>>>(U, F, m);

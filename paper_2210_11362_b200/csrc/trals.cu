@@ -588,6 +588,72 @@ int gemm_oz(const int8_t* ad, const int32_t* ea, int64_t M, int64_t K, int64_t N
   return TRALS_OK;
 }
 
+// Accuracy guard of the digit-sliced fp64 products (AlsConfig.fp64_gemm = "auto"): per K-major row
+// of X (its rows for transpose = 0, its columns for transpose = 1) the dynamic-range statistic
+// rho = max|x| * K / sum|x| (0 for an all-zero row); out = max over rows.  The product truncates
+// each row at 2^-56.9 of its maximum, so its error per output is <= 2^-56.9 max|a| sum|h| =
+// 2^-56.9 rho mean|a| sum|h|: rho bounds how far that is from a dgemm's eps sum|a||h| for a
+// spread-out h.  Reductions in a fixed order (deterministic).
+__global__ void __launch_bounds__(256) oz_range_rows_kernel(const double* __restrict__ x, int64_t rows, int64_t cols,
+                                                            double* __restrict__ rho) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t r = w0; r < rows; r += nw) {
+    double m = 0.0, sa = 0.0;
+    for (int64_t c = lane; c < cols; c += 32) {
+      const double v = fabs(x[r * cols + c]);
+      m = fmax(m, v);
+      sa += v;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+      sa += __shfl_xor_sync(0xffffffffu, sa, o);
+    }
+    if (lane == 0) rho[r] = sa > 0.0 ? m * static_cast<double>(cols) / sa : 0.0;
+  }
+}
+
+__global__ void __launch_bounds__(256) oz_range_cols_kernel(const double* __restrict__ x, int64_t rows, int64_t cols,
+                                                            double* __restrict__ rho) {
+  __shared__ double sm[8][32], ss[8][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t c = blockIdx.x * 32 + lane;
+  double m = 0.0, sa = 0.0;
+  if (c < cols)
+    for (int64_t r = warp; r < rows; r += 8) {
+      const double v = fabs(x[r * cols + c]);
+      m = fmax(m, v);
+      sa += v;
+    }
+  sm[warp][lane] = m;
+  ss[warp][lane] = sa;
+  __syncthreads();
+  if (warp == 0 && c < cols) {
+    for (int w = 1; w < 8; ++w) {
+      m = fmax(m, sm[w][lane]);
+      sa += ss[w][lane];
+    }
+    rho[c] = sa > 0.0 ? m * static_cast<double>(rows) / sa : 0.0;
+  }
+}
+
+__global__ void __launch_bounds__(1024) max_reduce_kernel(const double* __restrict__ v, int64_t n,
+                                                          double* __restrict__ out) {
+  __shared__ double red[32];
+  double m = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) m = fmax(m, v[i]);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w) m = fmax(m, red[w]);
+    *out = m;
+  }
+}
+
 // X (fp32 or fp64, row-major [rows][cols]) -> tiled digit planes of its rows (transpose = 0)
 // or columns (transpose = 1) + their exponents; ws = out_rows doubles (row / column maxima)
 template <typename Tin, class SC>
@@ -1929,12 +1995,12 @@ __global__ void __launch_bounds__(kHhThreads, 1) hh_block_kernel(const double* _
   hh_store_r(A, ld, m_all, nc, R + static_cast<int64_t>(b) * rstride, sign != 0, rows_out);
 }
 
-// Wide QR (I < nc) in one launch.  CTA 0 factors the left I x I block (blocked, I <=
+// Wide QR (I < nc) in one launch.  The first CTA to arrive factors the left I x I block (blocked, I <=
 // kHhPanelRows) and publishes every panel (V columns to Vg, T to Tg, then flags[b]);
-// CTAs 1.. each own a chunk of cw of the remaining columns and apply the panels in
+// the later ones each own a chunk of cw of the remaining columns and apply the panels in
 // order as they appear (compact WY: W = V^T A, W' = T^T W, A -= V W' on DMMA), so the
 // application runs behind the factorisation instead of after it.  R gets the rows
-// sign-normalised by diag(R_left).  flags must be zero at launch.
+// sign-normalised by diag(R_left).  flags[0..panels] (panel flags + the role ticket) must be zero at launch.
 __global__ void __launch_bounds__(kHhThreads, 1) hh_wide_kernel(const double* __restrict__ G, int I, int nc,
                                                              double* __restrict__ R, double* __restrict__ Vg,
                                                              double* __restrict__ Tg, int* __restrict__ flags,
@@ -1946,7 +2012,13 @@ __global__ void __launch_bounds__(kHhThreads, 1) hh_wide_kernel(const double* __
   __shared__ double scratch[64 * (kHhThreads / 32)];
   __shared__ double xch[2 * 5 * kHhNB];
   const int tid = threadIdx.x;
-  if (blockIdx.x == 0) {
+  // roles by arrival (atomic ticket), not by blockIdx: the CTA that factors the left block is one that
+  // is already running, so the spinning appliers can never wait on a CTA that has not been scheduled
+  __shared__ int role;
+  const int panels = (I + kHhNB - 1) / kHhNB;
+  if (tid == 0) role = atomicAdd(flags + panels, 1);
+  __syncthreads();
+  if (role == 0) {
     const int ld = I + 1;
     for (int t = tid; t < I * I; t += blockDim.x) {
       const int r = t / I, c = t - r * I;
@@ -1965,7 +2037,7 @@ __global__ void __launch_bounds__(kHhThreads, 1) hh_wide_kernel(const double* __
     return;
   }
   const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
-  const int c0 = I + (blockIdx.x - 1) * cw;
+  const int c0 = I + (role - 1) * cw;
   const int w = min(cw, nc - c0);
   const int ld = cw + 1;
   double* buf = A + static_cast<int64_t>(I) * ld;  // V [I][8] + T [64] of the current panel
@@ -1973,7 +2045,6 @@ __global__ void __launch_bounds__(kHhThreads, 1) hh_wide_kernel(const double* __
     const int r = t / w, c = t - r * w;
     A[r * ld + c] = G[static_cast<int64_t>(r) * nc + c0 + c];
   }
-  const int panels = (I + kHhNB - 1) / kHhNB;
   for (int b = 0; b < panels; ++b) {
     if (tid == 0) {
       volatile int* f = flags + b;
@@ -2082,7 +2153,7 @@ int hh_qr(const double* G, int I, int nc, double* R, double* ws, int64_t ws_elem
   double* Tg = ws + static_cast<int64_t>(I) * I;
   const int panels = (I + kHhNB - 1) / kHhNB;
   int* flags = reinterpret_cast<int*>(Tg + 64 * static_cast<int64_t>(panels));
-  if (cudaMemsetAsync(flags, 0, sizeof(int) * panels, s) != cudaSuccess) return TRALS_ERR_CUDA;
+  if (cudaMemsetAsync(flags, 0, sizeof(int) * (panels + 1), s) != cudaSuccess) return TRALS_ERR_CUDA;  // + ticket
   const int rest = nc - I;
   const int blocks = 1 + (rest > 0 ? (rest + p.chunk - 1) / p.chunk : 0);
   const size_t smem_left = sizeof(double) * static_cast<size_t>(I) * (I + 1);
@@ -2840,6 +2911,25 @@ int trals_tri_fallback_f64(const double* R0, int Lr, int m, const double* Mr, in
   if (ws_elems < trals_spd_fallback_ws_elems(rows, m)) return TRALS_ERR_WORKSPACE;
   pinv_fallback_kernel<<<1, 1024, 0, static_cast<cudaStream_t>(stream)>>>(R0, m, Mr, rows, Z, info, mode, rcond, ws,
                                                                            Lr, 1);
+  return launch_status();
+}
+
+int64_t trals_oz_range_ws_elems(int64_t rows, int64_t cols, int transpose) { return transpose ? cols : rows; }
+
+int trals_oz_range_f64(const double* x, int64_t rows, int64_t cols, int transpose, double* out, double* ws,
+                       int64_t ws_elems, void* stream) {
+  if (!x || !out || !ws || rows < 1 || cols < 1 || (transpose != 0 && transpose != 1)) return TRALS_ERR_ARG;
+  const int64_t out_rows = transpose ? cols : rows;
+  if (ws_elems < out_rows) return TRALS_ERR_WORKSPACE;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (!transpose) {
+    const int blocks = static_cast<int>(std::min<int64_t>((rows + 7) / 8, 16 * kSMs));
+    oz_range_rows_kernel<<<blocks, 256, 0, s>>>(x, rows, cols, ws);
+  } else {
+    oz_range_cols_kernel<<<static_cast<unsigned>((cols + 31) / 32), 256, 0, s>>>(x, rows, cols, ws);
+  }
+  if (int st = launch_status()) return st;
+  max_reduce_kernel<<<1, 1024, 0, s>>>(ws, out_rows, out);
   return launch_status();
 }
 

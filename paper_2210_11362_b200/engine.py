@@ -38,6 +38,7 @@ from . import _lib as L
 
 BUCKETS = ("subchain", "mttsp", "solve", "gramqr", "other")  # solvers.py:57
 OZ64_MIN_FLOPS = 4e9  # fp64_gemm="auto": smallest environment product run on the int8 tensor cores
+OZ64_MAX_RHO = 2.0 ** 12  # fp64_gemm="auto": largest row dynamic range (max|x| K / sum|x|) of X sliced (trals.h)
 
 
 def _prod(v):
@@ -665,6 +666,19 @@ class SweepEngine:
                           ws.numel(), sp), "oz_split")
         if self._x64 is not None:
             self._x64.copy_(self.x)
+
+    def x_dynamic_range(self):
+        """Largest rho = max|x| K / sum|x| over the K-major rows of X in every X-streaming phase of the
+        int8 engine (trals_oz_range_f64): the accuracy guard of fp64_gemm="auto" (include/trals.h)."""
+        if not self.oz64:
+            return 0.0
+        out = self._empty(len(self._xsplit))
+        sp = self._sp()
+        for i, (side, pre, post) in enumerate(self._xsplit):
+            ws = self._empty(max(1, self.lib.trals_oz_range_ws_elems(pre, post, side)))
+            L.check(self.lib.trals_oz_range_f64(self.x.data_ptr(), pre, post, side, out[i:].data_ptr(), ws.data_ptr(),
+                                                ws.numel(), sp), "oz_range")
+        return float(out.max().item())
 
     def ensure_x64(self):
         """fp32 variant with exact errors: the residual kernel reads an fp64 copy of X

@@ -156,7 +156,7 @@ def _run(x, config, variant):
         shard = int(config.shard_mode) % N
         lo, hi = _slab(dims[shard], world, rank)
         src = t.narrow(shard, lo, hi - lo)
-    from .engine import SweepEngine
+    from .engine import OZ64_MAX_RHO, SweepEngine
     try:
         rk = tuple(int(r) for r in config.ranks)
     except (TypeError, ValueError):
@@ -185,11 +185,24 @@ def _run(x, config, variant):
     ranks = check_ranks(config.ranks, N)
     if config.error_mode == "exact":
         check_element_budget(dims, config.element_budget)
+
+    def build(gemm):
+        return SweepEngine(x_local, dims, ranks, variant, shard_mode=shard, lo=lo, hi=hi, group=group,
+                           world_size=world, rank_deficient_fallback=config.rank_deficient_fallback,
+                           svd_rcond=config.svd_rcond, debug_checks=config.debug_checks, fp64_gemm=gemm)
     if eng is None:
-        eng = SweepEngine(x_local, dims, ranks, variant, shard_mode=shard, lo=lo, hi=hi, group=group,
-                          world_size=world, rank_deficient_fallback=config.rank_deficient_fallback,
-                          svd_rcond=config.svd_rcond, debug_checks=config.debug_checks,
-                          fp64_gemm=config.fp64_gemm)
+        eng = build(config.fp64_gemm)
+    if config.fp64_gemm == "auto":
+        # accuracy guard of the int8 engine (include/trals.h): a row of X with a wide dynamic range
+        # is held only to 2^-56.9 of its maximum, so such X runs on the fp64 DMMA pipe
+        if eng.oz64:
+            if _all_ranks_max(eng.x_dynamic_range(), world, group) > OZ64_MAX_RHO:
+                eng = build("dmma")
+                eng.guard_fallback = True
+        elif getattr(eng, "guard_fallback", False):
+            probe = build("auto")
+            if probe.oz64 and _all_ranks_max(probe.x_dynamic_range(), world, group) <= OZ64_MAX_RHO:
+                eng = probe
     eng.stream = torch.cuda.current_stream(dev)
     eng.xnorm2.copy_(xn_dev)
     p0 = torch.cuda.Event(enable_timing=True)
@@ -285,6 +298,17 @@ def _sumsq_device(lib, x, dev):
     L.check(fn(x.data_ptr(), x.numel(), out.data_ptr(), ws.data_ptr(),
                int(torch.cuda.current_stream(dev).cuda_stream)), "sumsq")
     return out
+
+
+def _all_ranks_max(v, world, group):
+    """The same engine choice on every rank: the guard statistic max-reduced over the ranks."""
+    if world <= 1:
+        return v
+    import torch
+    import torch.distributed as tdist
+    t = torch.tensor([v], dtype=torch.float64, device=torch.device("cuda", torch.cuda.current_device()))
+    tdist.all_reduce(t, op=tdist.ReduceOp.MAX, group=group)
+    return float(t.item())
 
 
 def _nccl(group):

@@ -501,3 +501,62 @@ def test_tri_fallback_min_norm(Lr, m, mode):
     assert rel(Z.cpu().numpy(), want) < 1e-9
     inf = info.cpu().numpy()
     assert inf[2] == 0 and inf[3] == (1 if mode == 1 else 0)
+
+
+# ---------------------------------------------------------------------------
+# accuracy guard of the int8 fp64 engine (include/trals.h: trals_oz_range_f64, fp64_gemm="auto")
+# ---------------------------------------------------------------------------
+def _rho_np(x, side):
+    a = np.abs(x if side == 0 else x.T)
+    s = a.sum(axis=1)
+    return float(np.max(np.where(s > 0, a.max(axis=1) * a.shape[1] / np.where(s > 0, s, 1), 0.0)))
+
+
+@pytest.mark.parametrize("rows,cols", [(300, 77), (7, 5000), (2000, 33)])
+@pytest.mark.parametrize("side", [0, 1])
+def test_oz_range_statistic(rows, cols, side):
+    from paper_2210_11362_b200 import _lib as L
+    lib = L.lib()
+    rng = np.random.default_rng(rows + cols + side)
+    x = rng.standard_normal((rows, cols))
+    x[3] = 0.0
+    x[5, 2] = 1e9  # one outlier: rho of that row ~ K
+    out = torch.zeros(1, dtype=torch.float64, device="cuda")
+    ws = torch.empty(lib.trals_oz_range_ws_elems(rows, cols, side), dtype=torch.float64, device="cuda")
+    xd = cuda(x)
+    L.check(lib.trals_oz_range_f64(xd.data_ptr(), rows, cols, side, out.data_ptr(), ws.data_ptr(), ws.numel(),
+                                   int(torch.cuda.current_stream().cuda_stream)), "oz_range")
+    assert abs(out.item() - _rho_np(x, side)) <= 1e-12 * _rho_np(x, side)
+
+
+def test_oz64_guard_adversarial():
+    """Small-X x large-H terms dominate: rows of X with a 1e-12 dynamic range multiplied by an H that
+    is zero where X is large.  The int8 product (exact to 2^-56.9 of each row's maximum) loses those
+    terms; the DMMA product keeps them; the guard statistic flags X, so fp64_gemm="auto" runs it on
+    DMMA (solver-level check in tests/test_gpu_solvers.py::test_auto_engine_guard)."""
+    from paper_2210_11362_b200 import _lib as L
+    lib = L.lib()
+    rng = np.random.default_rng(11)
+    pre, post, r = 256, 8192, 4
+    x = rng.standard_normal((pre, post)) * 1e-12
+    x[:, 0] = 1.0                              # one large entry per row ...
+    h = rng.standard_normal((post, r * r))
+    h[0] = 0.0                                 # ... that H ignores: the output is made of the small terms
+    exact = (x.astype(np.longdouble) @ h.astype(np.longdouble)).astype(np.float64)
+    x64, H = cuda(x), cuda(h)
+    s = int(torch.cuda.current_stream().cuda_stream)
+    got, _, _ = _oz64_env(lib, x64, pre, post, 0, H, r, r, 1, s)
+    ref = torch.empty(pre * r * r, dtype=torch.float64, device="cuda")
+    ws = torch.empty(max(lib.trals_gemm_ws_elems(1, pre, post, r * r), 1 << 20), dtype=torch.float64, device="cuda")
+    L.check(lib.trals_env_f64(x64.data_ptr(), pre, post, 0, H.data_ptr(), r, r, ref.data_ptr(), 1,
+                              ws.data_ptr(), ws.numel(), s), "env_f64")
+    out = torch.zeros(1, dtype=torch.float64, device="cuda")
+    rws = torch.empty(pre, dtype=torch.float64, device="cuda")
+    L.check(lib.trals_oz_range_f64(x64.data_ptr(), pre, post, 0, out.data_ptr(), rws.data_ptr(), rws.numel(), s),
+            "oz_range")
+    torch.cuda.synchronize()
+    e_dmma = rel(ref.cpu().numpy().reshape(pre, -1), exact)
+    e_oz = rel(got.cpu().numpy().reshape(pre, -1), exact)
+    assert e_dmma < 1e-14
+    assert e_oz > 1e3 * e_dmma            # the failure mode the guard exists for
+    assert out.item() > 2.0 ** 12         # ... and the guard sees it

@@ -301,33 +301,27 @@ def test_debug_checks_on_device(variant):
     np.testing.assert_allclose(rep.errors, g[f"{variant}_exact_errors"], rtol=0, atol=1e-9)
 
 
-
-def _mem_available_gb():
-    try:
-        with open("/proc/meminfo") as f:
-            for line in f:
-                if line.startswith("MemAvailable:"):
-                    return int(line.split()[1]) / 2**20
-    except OSError:
-        pass
-    return 0.0
-
-
-@pytest.mark.timeout(1200)
-def test_baseline_c5_head():
-    """BASELINE c5 (160^4, 5.24 GB, R20 -> R20, NE) at full size, the first 2 sweeps against the
-    oracle (pinned to the reference on c1-c4 and the small goldens).  The reference itself cannot
-    run c5 in the build container (its 13 GB subchain plus copies exceed 62 GB), so the oracle runs
-    here on the GPU box's host, when it has the memory.  Errors at 1e-9 absolute, cores at 1e-6
-    relative Frobenius (north_star), on the default engine (int8 Ozaki at c5)."""
-    if _mem_available_gb() < 160:
-        pytest.skip("host memory too small for the c5 oracle (subchain materialisation)")
-    from paper_2210_11362_b200 import AlsConfig, tr_als_ne
-    order, dim, rt, noise, sd, rf, si, sweeps = 4, 160, 20, 1e-3, 8, 20, 9, 2
-    x, _ = O.synth(O.Recipe(order=order, dim=dim, rank=rt, noise=noise, seed=sd), budget=1 << 40)
-    cores, rep = tr_als_ne(x, AlsConfig(ranks=(rf,) * order, max_iters=sweeps, seed=si, error_mode="cheap"))
-    ocores, orep = O.solve(x, "ne", O.Config(ranks=(rf,) * order, max_iters=sweeps, seed=si,
-                                             error_mode="cheap"))
-    np.testing.assert_allclose(rep.errors, orep.errors, rtol=0, atol=1e-9)
-    for j in range(order):
-        assert rel(cores[j], ocores[j]) < 1e-6
+def test_auto_engine_guard():
+    """fp64_gemm="auto" on an X large enough for the int8 engine (80^4, R 8: 5.2 GFLOP per product)
+    whose phase-L rows (6400 long) each carry one entry 1e8 above the rest (rho ~ 6400 > 2^12): the
+    dynamic-range guard moves it to the DMMA pipe, and the run matches the oracle; the same X
+    without the spike stays on the int8 engine."""
+    from paper_2210_11362_b200 import AlsConfig, decompose
+    from paper_2210_11362_b200 import solvers as S
+    dims, ranks = (80, 80, 80, 80), (8, 8, 8, 8)
+    rng = O.philox(5)
+    base = O.noisy(O.dense_from_ring(O.gaussian_ring(dims, (3, 3, 3, 3), rng)), 1e-3, rng)
+    init = O.gaussian_ring(dims, ranks, O.philox(6))
+    for spike, want in ((False, "ozaki"), (True, "dmma")):
+        x = base.copy()
+        if spike:
+            x[:, :, 0, 0] *= 1e8
+        S.clear_plan_cache()
+        cfg = AlsConfig(ranks=ranks, max_iters=2, init_cores=init, error_mode="cheap")
+        cores, rep = decompose(x, "ne", cfg)
+        eng = next(iter(S._PLAN_CACHE.values()))
+        assert eng.fp64_gemm == want
+        ocores, orep = O.solve(x, "ne", O.Config(ranks=ranks, max_iters=2, init_cores=init, error_mode="cheap"))
+        np.testing.assert_allclose(rep.errors, orep.errors, rtol=0, atol=1e-9)
+        for j in range(4):
+            assert rel(cores[j], ocores[j]) < 1e-6
