@@ -48,7 +48,8 @@ enum {
   TRALS_INFO_ASYM = 1,       /* 1 if |S - S^T| > 1e-8 max|S| (linalg.py:70-72) */
   TRALS_INFO_DEGEN = 2,      /* 1-based index of diag <= 1e-13 max|R| (linalg.py:96-99) */
   TRALS_INFO_FALLBACKS = 3,  /* number of fallback solves taken (AlsReport.fallback_count) */
-  TRALS_INFO_SLOTS = 4
+  TRALS_INFO_ILLCOND = 4,    /* QR variants: merged R0's smallest diagonal <= sqrt(m eps) max|R0| */
+  TRALS_INFO_SLOTS = 5
 };
 
 const char* trals_strerror(int code);
@@ -229,19 +230,23 @@ int64_t trals_oz_range_ws_elems(int64_t rows, int64_t cols, int transpose);
 int trals_oz_range_f64(const double* d_x, int64_t rows, int64_t cols, int transpose, double* d_out, double* d_ws,
                        int64_t ws_elems, void* stream);
 
-/* R0 of the QR-stabilised variants without forming V (tr_als_qr, solvers.py:422-424
- * `q0, r0 = qr_economy(cyclic_unfold(subchain_skip(R-tensors, n), 1))`; for Alg. 1 tr_als,
- * solvers.py:337-339, the same with the cores themselves).  h_rt[j] = the R-tensor of core j
- * in layout C, shape (R_j, ks[j], R_{j+1}) (ks[j] = min(I_j, R_j R_{j+1}) for QR, I_j for
- * Alg. 1).  The cores n+1, ..., n-1 are merged one at a time (ring.py:110-131) and every merge
- * whose lateral size exceeds R_a R_c is compressed by a Householder QR (cuSOLVER dgeqrf,
- * deterministic mode): orthogonal transformations of V_[2]'s rows, so the result is the
- * reference's R0 to rounding.  d_R0 (row-major, k0 x m with m = R_n R_{n+1}, k0 =
- * min(prod_{j!=n} ks[j], m)): upper triangular / trapezoidal, nonnegative diagonal
- * (linalg.py:48-51), columns r_n + R_n r_{n+1} (the S_n order). */
-int64_t trals_r0_merge_ws_elems(int N, int n, const int32_t* ranks, const int32_t* ks);
-int trals_r0_merge_f64(int N, int n, const int32_t* ranks, const int32_t* ks, const double* const* h_rt,
-                       double* d_R0, double* d_ws, int64_t ws_elems, void* stream);
+/* R0 of the QR-stabilised variants (tr_als_qr, solvers.py:422-424 `q0, r0 =
+ * qr_economy(cyclic_unfold(V, 1))`; Alg. 1 tr_als, solvers.py:337-339, the same with the cores):
+ * the nonnegative-diagonal factor with R0^T R0 = V_[2]^T V_[2] = S_n, computed without V and without
+ * squaring cond(V) in fp64: the transfer matrices of the R-tensors (of the cores for Alg. 1), their
+ * Gram chain (ring.py:191-214) and the Cholesky factorisation all run in double-double arithmetic
+ * (~2^-104 relative per operation), so R0 is as accurate as the reference's Householder R0 for
+ * cond(V) up to ~2^51 before it is rounded to fp64.  A pivot <= 0 (semidefinite S, rank-deficient V)
+ * leaves a zero row, which the 1e-13 floor of trals_tri_prepare_f64 reports as the reference's
+ * Householder R0 of such a V does (linalg.py:96-99).
+ * trals_dd_transfer_f64: E = sum_i R(i) (x) R(i) of one tensor (layout C, (Ra, k, Rb)) as hi / lo
+ * planes, in the layout of trals_core_gram_f64.
+ * trals_dd_r0_f64: h_Ehi / h_Elo[j] = those of tensor j; writes R0 (m x m row-major, m = R_n
+ * R_{n+1}, columns r_n + R_n r_{n+1}) and, if d_S is not null, the fp64 rounding of S_n. */
+int trals_dd_transfer_f64(const double* d_R, int Ra, int k, int Rb, double* d_Ehi, double* d_Elo, void* stream);
+int64_t trals_dd_r0_ws_elems(int N, const int32_t* ranks);
+int trals_dd_r0_f64(int N, int n, const int32_t* ranks, const double* const* h_Ehi, const double* const* h_Elo,
+                    double* d_S, double* d_R0, double* d_ws, int64_t ws_elems, void* stream);
 
 /* solve_triangular_block's factor step (solvers.py:262-273 with linalg.py:84-101) for a given
  * square R0 (d_U, m x m row-major, upper): the operands of trals_chol_solve_f64 (which then
@@ -255,8 +260,14 @@ int trals_tri_prepare_f64(double* d_U, int m, double* d_F, double* d_aux, int ch
 /* The min-norm fallback of the QR variants taken on R0 itself (linalg.py:104-112 pinv with
  * rcond = AlsConfig.svd_rcond, solvers.py:262-273): one-sided Jacobi SVD of the Lr x m factor
  * (R0 V = U Sigma), Z = M V Sigma^{-2} V^T over the singular values above rcond sigma_max
- * (= W pinv(R0)^T for W = M R0^{-1}).  mode 1: fires on d_info[TRALS_INFO_DEGEN], clears it and
- * counts a fallback; mode 2: non-square R0 (Lr < m, solvers.py:264-266), always, uncounted.
+ * (= W pinv(R0)^T for W = M R0^{-1}).  Because the right-hand side is M = W R0 rather than W, the
+ * cut is max(rcond, sqrt(m eps)) sigma_max: a component with a smaller singular value is divided by
+ * sigma^2 and would only amplify M's rounding.  mode 1: fires on d_info[TRALS_INFO_DEGEN] (counted as
+ * a fallback, flag cleared -- the reference's event) or on d_info[TRALS_INFO_ILLCOND] alone (an
+ * R0 with min|r_ii| <= sqrt(m eps) max|R0| but above the 1e-13 floor, where the two triangular
+ * solves of M would square its condition number: the same min-norm solve, not counted); mode 3
+ * (rank_deficient_fallback off): only the ILLCOND case, so a degenerate R0 still raises;
+ * mode 2: non-square R0 (Lr < m, solvers.py:264-266), always, uncounted.
  * Workspace: trals_spd_fallback_ws_elems(rows, m). */
 int trals_tri_fallback_f64(const double* d_R0, int Lr, int m, const double* d_M, int64_t rows, double* d_Z,
                            int* d_info, int mode, double rcond, double* d_ws, int64_t ws_elems, void* stream);

@@ -15,7 +15,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libtrals.so")
 
 LAYOUT_C, LAYOUT_SLICE, LAYOUT_ZT, LAYOUT_TT = 0, 1, 2, 3
-INFO_CHOL, INFO_ASYM, INFO_DEGEN, INFO_FALLBACKS, INFO_SLOTS = 0, 1, 2, 3, 4
+INFO_CHOL, INFO_ASYM, INFO_DEGEN, INFO_FALLBACKS, INFO_ILLCOND, INFO_SLOTS = 0, 1, 2, 3, 4, 5
 
 _dp = c_void_p  # device pointers travel as void*
 _lib = None
@@ -53,9 +53,10 @@ _SIGNATURES = {
                                        c_void_p]),
     "trals_oz_range_ws_elems": (c_int64, [c_int64, c_int64, c_int]),
     "trals_oz_range_f64": (c_int, [_dp, c_int64, c_int64, c_int, _dp, _dp, c_int64, c_void_p]),
-    "trals_r0_merge_ws_elems": (c_int64, [c_int, c_int, POINTER(c_int32), POINTER(c_int32)]),
-    "trals_r0_merge_f64": (c_int, [c_int, c_int, POINTER(c_int32), POINTER(c_int32), POINTER(c_void_p), _dp, _dp,
-                                   c_int64, c_void_p]),
+    "trals_dd_transfer_f64": (c_int, [_dp, c_int, c_int, c_int, _dp, _dp, c_void_p]),
+    "trals_dd_r0_ws_elems": (c_int64, [c_int, POINTER(c_int32)]),
+    "trals_dd_r0_f64": (c_int, [c_int, c_int, POINTER(c_int32), POINTER(c_void_p), POINTER(c_void_p), _dp, _dp, _dp,
+                                c_int64, c_void_p]),
     "trals_tri_prepare_f64": (c_int, [_dp, c_int, _dp, _dp, c_int, _dp, c_void_p]),
     "trals_reverse_axes_f64": (c_int, [_dp, c_int, POINTER(c_int64), _dp, c_void_p]),
     "trals_sumsq_ws_elems": (c_int64, []),
@@ -132,5 +133,5 @@ def ptr_array(ptrs):
 
 __all__ = ["lib", "load", "check", "TralsError", "EXPORTED", "i64_array", "i32_array", "ptr_array",
            "LAYOUT_C", "LAYOUT_SLICE", "LAYOUT_ZT", "LAYOUT_TT", "INFO_CHOL", "INFO_ASYM", "INFO_DEGEN",
-           "INFO_FALLBACKS", "INFO_SLOTS",
+           "INFO_FALLBACKS", "INFO_ILLCOND", "INFO_SLOTS",
            "c_double"]

@@ -15,7 +15,7 @@ OUT = os.path.join(HERE, "libtrals.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-shared", "-I", os.path.join(ROOT, "include")]
-LIBS = ["-lcusolver"]  # dgeqrf for the QR variants' merged R0 (csrc/qr_r0.cuh)
+LIBS = []
 
 
 def up_to_date() -> bool:

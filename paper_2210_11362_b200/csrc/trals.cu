@@ -1200,7 +1200,11 @@ __global__ void chol_finalize_kernel(double* __restrict__ U, double* __restrict_
   }
 }
 
-__global__ void __launch_bounds__(1024) degen_kernel(const double* __restrict__ U, int m, int* __restrict__ info) {
+// ill_scale > 0 (the QR variants' merged R0): also raise d_info[TRALS_INFO_ILLCOND] when the smallest
+// diagonal is within ill_scale of the largest entry -- the solve then goes through the R0 SVD (see
+// trals_tri_fallback_f64); the reference's 1e-13 floor (TRALS_INFO_DEGEN) is unchanged
+__global__ void __launch_bounds__(1024) degen_kernel(const double* __restrict__ U, int m, int* __restrict__ info,
+                                                     double ill_scale = 0.0) {
   __shared__ double red[32], sd[32];
   __shared__ int si[32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
@@ -1229,6 +1233,7 @@ __global__ void __launch_bounds__(1024) degen_kernel(const double* __restrict__ 
       if (sd[w] < d || (sd[w] == d && si[w] < di)) { d = sd[w]; di = si[w]; }
     }
     if (d <= 1e-13 * a) info[TRALS_INFO_DEGEN] = di + 1;  // linalg.py:96-99
+    if (ill_scale > 0.0 && d <= ill_scale * a) info[TRALS_INFO_ILLCOND] = 1;
   }
 }
 
@@ -1456,9 +1461,16 @@ __global__ void __launch_bounds__(1024) pinv_fallback_kernel(const double* __res
   const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
   const int trig_chol = info[TRALS_INFO_CHOL];
   const int trig_degen = info[TRALS_INFO_DEGEN];
-  // mode 2: non-square R0 in the reference (prod_j k_j < R^2): always the SVD solve, not counted
-  const bool fire = (mode == 0) ? (trig_chol != 0) : (mode == 1 ? (trig_chol != 0 || trig_degen != 0) : true);
+  const int trig_ill = tri ? info[TRALS_INFO_ILLCOND] : 0;
+  // mode 2: non-square R0 in the reference (prod_j k_j < R^2): always the SVD solve, not counted;
+  // mode 3 (tri only, fallback disabled): only the ill-conditioning safety solve
+  bool fire;
+  if (mode == 0) fire = trig_chol != 0;
+  else if (mode == 1) fire = trig_chol != 0 || trig_degen != 0 || trig_ill != 0;
+  else if (mode == 2) fire = true;
+  else fire = trig_ill != 0;
   if (!fire) return;
+  const bool counted = (mode == 0) || (mode == 1 && (trig_chol != 0 || trig_degen != 0));
   const int m2 = (m + 1) & ~1;
   double* A = ws;                          // [m2][m] columns of S (column-major), zero column if padded
   double* V = A + static_cast<int64_t>(m2) * m;   // [m2][m2]
@@ -1539,8 +1551,10 @@ __global__ void __launch_bounds__(1024) pinv_fallback_kernel(const double* __res
   // QR modes, squares of R0's), so the cut never goes below that noise floor: mode 0 (gelsy, cond = eps)
   // uses max(rcond, m eps), modes 1/2 map R0's rcond to max(rcond^2, m eps) on S
   const double floor_noise = m * eps;
-  const double cut = tri ? rcond * smax
-                        : (mode == 0 ? fmax(rcond, floor_noise) : fmax(rcond * rcond, floor_noise)) * smax;
+  // tri: the right-hand side is M = W R0 (not W itself), so components are divided by sigma^2: the
+  // cut never goes below sqrt(m eps) sigma_max (below it the M-based solve only amplifies rounding)
+  const double cut = tri ? fmax(rcond, sqrt(floor_noise)) * smax
+                         : (mode == 0 ? fmax(rcond, floor_noise) : fmax(rcond * rcond, floor_noise)) * smax;
   // S mode:   Z = M pinv(S) = sum_{sig_i > cut} (M a_i / sig_i^2) v_i^T   (a_i = S v_i = sig_i v_i)
   // tri mode: Z = M pinv(R0^T R0) = sum_{sig_i > cut} (M v_i / sig_i^2) v_i^T
   for (int t = tid; t < rows * m2; t += blockDim.x) {
@@ -1564,9 +1578,12 @@ __global__ void __launch_bounds__(1024) pinv_fallback_kernel(const double* __res
   }
   __syncthreads();
   if (tid == 0 && mode != 2) {  // mode 2 replaces the factorisation outright: no flags, not counted
-    info[TRALS_INFO_CHOL] = 0;
-    if (mode == 1) info[TRALS_INFO_DEGEN] = 0;
-    info[TRALS_INFO_FALLBACKS] += 1;
+    if (mode != 3) {
+      info[TRALS_INFO_CHOL] = 0;
+      if (mode == 1) info[TRALS_INFO_DEGEN] = 0;
+    }
+    if (tri) info[TRALS_INFO_ILLCOND] = 0;
+    if (counted) info[TRALS_INFO_FALLBACKS] += 1;
   }
 }
 
@@ -2526,6 +2543,7 @@ int run_mttsp(const double* X, int N, const int64_t* dims, const int32_t* ranks,
 
 }  // namespace
 
+#include "dd_r0.cuh"
 #include "qr_r0.cuh"
 
 // ===========================================================================
@@ -2906,7 +2924,7 @@ int trals_spd_fallback_f64(const double* S, int m, const double* Mr, int64_t row
 
 int trals_tri_fallback_f64(const double* R0, int Lr, int m, const double* Mr, int64_t rows, double* Z, int* info,
                            int mode, double rcond, double* ws, int64_t ws_elems, void* stream) {
-  if (!R0 || !Mr || !Z || !info || !ws || m < 1 || Lr < 1 || Lr > m || rows < 1 || mode < 1 || mode > 2)
+  if (!R0 || !Mr || !Z || !info || !ws || m < 1 || Lr < 1 || Lr > m || rows < 1 || mode < 1 || mode > 3)
     return TRALS_ERR_ARG;
   if (ws_elems < trals_spd_fallback_ws_elems(rows, m)) return TRALS_ERR_WORKSPACE;
   pinv_fallback_kernel<<<1, 1024, 0, static_cast<cudaStream_t>(stream)>>>(R0, m, Mr, rows, Z, info, mode, rcond, ws,
@@ -2933,15 +2951,32 @@ int trals_oz_range_f64(const double* x, int64_t rows, int64_t cols, int transpos
   return launch_status();
 }
 
-int64_t trals_r0_merge_ws_elems(int N, int n, const int32_t* ranks, const int32_t* ks) {
-  if (N < 2 || n < 0 || n >= N || !ranks || !ks) return -1;
-  return r0_ws(N, n, ranks, ks).total;
+int trals_dd_transfer_f64(const double* Rc, int Ra, int k, int Rb, double* Ehi, double* Elo, void* stream) {
+  if (!Rc || !Ehi || !Elo || Ra < 1 || k < 1 || Rb < 1) return TRALS_ERR_ARG;
+  const int64_t total = static_cast<int64_t>(Ra) * Ra * Rb * Rb;
+  const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 8 * kSMs));
+  dd_transfer_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(Rc, Ra, k, Rb, Ehi, Elo);
+  return launch_status();
 }
 
-int trals_r0_merge_f64(int N, int n, const int32_t* ranks, const int32_t* ks, const double* const* rt, double* R0,
-                       double* ws, int64_t ws_elems, void* stream) {
-  if (N < 2 || n < 0 || n >= N || !ranks || !ks || !rt || !R0 || !ws) return TRALS_ERR_ARG;
-  return r0_merge(N, n, ranks, ks, rt, R0, ws, ws_elems, static_cast<cudaStream_t>(stream));
+int64_t trals_dd_r0_ws_elems(int N, const int32_t* ranks) {
+  if (N < 2 || !ranks) return -1;
+  return dd_ws(N, ranks).total;
+}
+
+int trals_dd_r0_f64(int N, int n, const int32_t* ranks, const double* const* Ehi, const double* const* Elo,
+                    double* S, double* R0, double* ws, int64_t ws_elems, void* stream) {
+  if (N < 2 || n < 0 || n >= N || !ranks || !Ehi || !Elo || !R0 || !ws) return TRALS_ERR_ARG;
+  const DdWs w = dd_ws(N, ranks);
+  if (ws_elems < w.total) return TRALS_ERR_WORKSPACE;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int m = ranks[n] * ranks[(n + 1) % N];
+  double* Shi = ws + w.s;
+  double* Slo = Shi + static_cast<int64_t>(m) * m;
+  if (int st = dd_gram_chain(N, n, ranks, Ehi, Elo, Shi, Slo, ws, s)) return st;
+  if (S && cudaMemcpyAsync(S, Shi, sizeof(double) * m * m, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+    return TRALS_ERR_CUDA;
+  return dd_cholesky(Shi, Slo, m, R0, ws, w, s);
 }
 
 int trals_tri_prepare_f64(double* U, int m, double* F, double* aux, int check_degen, int* info, void* stream) {

@@ -174,8 +174,10 @@ class SweepEngine:
             if min(qws) < 0:
                 raise ValueError("per-core QR size outside the kernel envelope")
             self.qr_ws = self._empty(max(1, max(qws)))
-        # QR / ALS: R0 from orthogonal merges of the R-tensors (QR) or of the cores (ALS), never
-        # from chol(S_n) -- the R-tensors are kept per core in layout C
+        # QR / ALS: R0 = chol(S_n) with S_n formed from the R-tensors (QR) or the cores (ALS) and
+        # factored in double-double arithmetic (dd_r0.cuh): the R factor of V_[2] without forming V
+        # and without squaring cond(V) in fp64.  The R-tensors are kept per core in layout C and
+        # their transfer matrices as dd (hi, lo) planes.
         self.use_r0 = self.variant in ("qr", "als")
         if self.use_r0:
             if self.variant == "qr":
@@ -184,10 +186,11 @@ class SweepEngine:
             else:
                 self.r0_ks = list(self.dims)
                 self.RtC = self.Gc
-            ks_a = L.i32_array(self.r0_ks)
-            need = max(self.lib.trals_r0_merge_ws_elems(N, n, L.i32_array(self.ranks), ks_a) for n in range(N))
+            self.Edd = [(self._empty(self.R(j) ** 2 * self.R(j + 1) ** 2), self._empty(self.R(j) ** 2 * self.R(j + 1) ** 2))
+                        for j in range(N)]
+            need = self.lib.trals_dd_r0_ws_elems(N, L.i32_array(self.ranks))
             if need < 0:
-                raise ValueError("R0 merge outside the kernel envelope")
+                raise ValueError("R0 outside the kernel envelope")
             self.r0_ws = self._empty(max(1, need))
         self.fb_ws = self._empty(max(1, max(self.lib.trals_spd_fallback_ws_elems(self.dims[n], self.R(n) * self.R(n + 1))
                                             for n in range(N))))
@@ -428,14 +431,6 @@ class SweepEngine:
             cur, sa, sb = self._absorb_left(cur, sa, sb, leaf)
         self._tree(cur, m + 1, b)
 
-    def _r0_rows(self, n):
-        """Rows of the reference's R0 for mode n: min(prod_{j!=n} k_j, R_n R_{n+1})."""
-        ks = 1
-        for j in range(self.N):
-            if j != n:
-                ks *= self.r0_ks[j]
-        return min(ks, self.R(n) * self.R(n + 1))
-
     def _r0_nonsquare(self, n):
         """QR / ALS: the reference's triangular factor is non-square when it has fewer rows
         than R_n R_{n+1} -- QR: prod_{j!=n} k_j with k_j = min(I_j, R_j R_{j+1})
@@ -460,23 +455,15 @@ class SweepEngine:
         rmax = max(self.ranks)
         self._side_ws(self.lib.trals_gemm_ws_elems(1, rmax ** 2, rmax ** 2, rmax ** 2))
         self.steps.append(Step("other", None, f"fork S{n}", kind="fork"))
-
-        def gram_chain(n=n, S=S, ranks_a=ranks_a):
-            E = L.ptr_array([e.data_ptr() for e in self.E])
-            L.check(self.lib.trals_gram_chain_f64(N, n, ranks_a, E, S.data_ptr(), self.chain_tmp.data_ptr(),
-                                                  self.side_gws.data_ptr(), self.side_gws.numel(), self._sp()),
-                    "gram_chain")
-        self.steps.append(Step("other", gram_chain, f"S{n}", stream="side"))
         if self.use_r0:
-            # QR (solvers.py:422-424) / ALS (:337-339): R0 by merging the R-tensors (the cores) one at
-            # a time with a Householder QR after every merge; then its inverse operands and the 1e-13
+            # QR (solvers.py:422-424) / ALS (:337-339): S_n and R0 = chol(S_n) in double-double from the
+            # transfer matrices of the R-tensors (the cores); then R0's inverse operands and the 1e-13
             # degeneracy test (linalg.py:96-99)
-            ks_a = L.i32_array(self.r0_ks)
-
-            def r0(n=n, ranks_a=ranks_a, ks_a=ks_a):
-                rt = L.ptr_array([t.data_ptr() for t in self.RtC])
-                L.check(self.lib.trals_r0_merge_f64(N, n, ranks_a, ks_a, rt, self.U.data_ptr(), self.r0_ws.data_ptr(),
-                                                    self.r0_ws.numel(), self._sp()), "r0_merge")
+            def r0(n=n, S=S, ranks_a=ranks_a):
+                eh = L.ptr_array([e[0].data_ptr() for e in self.Edd])
+                el = L.ptr_array([e[1].data_ptr() for e in self.Edd])
+                L.check(self.lib.trals_dd_r0_f64(N, n, ranks_a, eh, el, S.data_ptr(), self.U.data_ptr(),
+                                                 self.r0_ws.data_ptr(), self.r0_ws.numel(), self._sp()), "dd_r0")
             self.steps.append(Step("gramqr", r0, f"R0 {n}", stream="side"))
 
             def tri(rr=rr):
@@ -486,6 +473,13 @@ class SweepEngine:
             if not self._r0_nonsquare(n):
                 self.steps.append(Step("solve", tri, f"tri{n}", stream="side"))
             return
+
+        def gram_chain(n=n, S=S, ranks_a=ranks_a):
+            E = L.ptr_array([e.data_ptr() for e in self.E])
+            L.check(self.lib.trals_gram_chain_f64(N, n, ranks_a, E, S.data_ptr(), self.chain_tmp.data_ptr(),
+                                                  self.side_gws.data_ptr(), self.side_gws.numel(), self._sp()),
+                    "gram_chain")
+        self.steps.append(Step("other", gram_chain, f"S{n}", stream="side"))
 
         def factor(S=S, rr=rr):
             L.check(self.lib.trals_cholesky_f64(S.data_ptr(), rr, self.U.data_ptr(), self.Lo.data_ptr(),
@@ -518,15 +512,17 @@ class SweepEngine:
         if self.use_r0:
             # solvers.py:262-273: the min-norm solve on R0 itself -- always for a non-square R0
             # (mode 2, uncounted), on a degenerate diagonal when the fallback is enabled (mode 1)
-            mode = 2 if self._r0_nonsquare(n) else (1 if self.fallback_ok else None)
-            lr = self._r0_rows(n)
-            if mode is not None:
-                def fallback(n=n, M=M, rr=rr, mode=mode, rows=rr_rows, lr=lr):
-                    L.check(self.lib.trals_tri_fallback_f64(self.U.data_ptr(), lr, rr, M.data_ptr(), rows,
-                                                            self.Gt[n].data_ptr(), self.info.data_ptr(), mode,
-                                                            self.svd_rcond, self.fb_ws.data_ptr(), self.fb_ws.numel(),
-                                                            self._sp()), "tri_fallback")
-                self.steps.append(Step("solve", fallback, f"fallback{n}"))
+            # (mode 3 with the fallback disabled: only the ill-conditioning safety solve, a degenerate
+            # R0 still raises DegenerateTriangularError at the end of the run)
+            mode = 2 if self._r0_nonsquare(n) else (1 if self.fallback_ok else 3)
+            lr = rr  # R0 = chol(S_n) is square; rows beyond rank(V) are zero
+
+            def fallback(n=n, M=M, rr=rr, mode=mode, rows=rr_rows, lr=lr):
+                L.check(self.lib.trals_tri_fallback_f64(self.U.data_ptr(), lr, rr, M.data_ptr(), rows,
+                                                        self.Gt[n].data_ptr(), self.info.data_ptr(), mode,
+                                                        self.svd_rcond, self.fb_ws.data_ptr(), self.fb_ws.numel(),
+                                                        self._sp()), "tri_fallback")
+            self.steps.append(Step("solve", fallback, f"fallback{n}"))
         else:
             def fallback(n=n, M=M, rr=rr, rows=rr_rows):
                 L.check(self.lib.trals_spd_fallback_f64(self.S[n].data_ptr(), rr, M.data_ptr(), rows,
@@ -556,6 +552,10 @@ class SweepEngine:
         """Transfer matrix of core n: from the core itself (NE, ring.py:188) or, for QR/QRNE, from the
         R-tensor of its Householder QR (mode2_qr + lateral_gram of the R-tensor, solvers.py:417,468-470)."""
         ra, i, rb = self.R(n), self.dims[n], self.R(n + 1)
+        if self.variant == "als":
+            L.check(self.lib.trals_dd_transfer_f64(self.Gc[n].data_ptr(), ra, i, rb, self.Edd[n][0].data_ptr(),
+                                                   self.Edd[n][1].data_ptr(), sp), "dd_transfer")
+            return
         if not self.use_rqr:
             L.check(self.lib.trals_core_gram_f64(self.Gs[n].data_ptr(), ra, i, rb, self.E[n].data_ptr(),
                                                  self.gws.data_ptr(), self.gws.numel(), sp), "core_gram")
@@ -563,11 +563,15 @@ class SweepEngine:
         k = min(i, ra * rb)
         L.check(self.lib.trals_core_qr_f64(self.Gt[n].data_ptr(), i, ra * rb, self.Rmat.data_ptr(),
                                            self.qr_ws.data_ptr(), self.qr_ws.numel(), sp), "core_qr")
-        L.check(self.lib.trals_core_relayout_f64(self.Rmat.data_ptr(), L.LAYOUT_ZT, ra, k, rb,
-                                                 self.Rslice.data_ptr(), L.LAYOUT_SLICE, sp), "relayout")
+        if not self.use_r0:
+            L.check(self.lib.trals_core_relayout_f64(self.Rmat.data_ptr(), L.LAYOUT_ZT, ra, k, rb,
+                                                     self.Rslice.data_ptr(), L.LAYOUT_SLICE, sp), "relayout")
         if self.use_r0:
             L.check(self.lib.trals_core_relayout_f64(self.Rmat.data_ptr(), L.LAYOUT_ZT, ra, k, rb,
                                                      self.RtC[n].data_ptr(), L.LAYOUT_C, sp), "relayout")
+            L.check(self.lib.trals_dd_transfer_f64(self.RtC[n].data_ptr(), ra, k, rb, self.Edd[n][0].data_ptr(),
+                                                   self.Edd[n][1].data_ptr(), sp), "dd_transfer")
+            return
         L.check(self.lib.trals_core_gram_f64(self.Rslice.data_ptr(), ra, k, rb, self.E[n].data_ptr(),
                                              self.gws.data_ptr(), self.gws.numel(), sp), "core_gram")
 

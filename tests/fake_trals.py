@@ -318,7 +318,7 @@ class FakeTrals:
     def trals_cholesky_f64(self, S, m, U, Lo, aux, check_degen, info, stream):
         self._count("cholesky")
         s = _arr(S, m * m).reshape(m, m)
-        inf = _iarr(info, 4)
+        inf = _iarr(info, 5)
         scale = np.max(np.abs(s))
         if scale > 0 and np.max(np.abs(s - s.T)) > 1e-8 * scale:
             inf[1] = 1
@@ -340,8 +340,11 @@ class FakeTrals:
         self._count("chol_solve")
         u = _arr(U, m * m).reshape(m, m)
         rhs = _arr(M, rows * m).reshape(rows, m)
-        y = sla.solve_triangular(u, rhs.T, trans="T", lower=False)
-        z = sla.solve_triangular(u, y, lower=False).T
+        try:
+            y = sla.solve_triangular(u, rhs.T, trans="T", lower=False)
+            z = sla.solve_triangular(u, y, lower=False).T
+        except np.linalg.LinAlgError:  # singular R0: the device solve writes non-finite values here,
+            z = np.full((rows, m), np.nan)  # which the fallback step that follows overwrites
         _arr(Z, rows * m)[:] = z.ravel()
         return 0
 
@@ -350,7 +353,7 @@ class FakeTrals:
 
     def trals_spd_fallback_f64(self, S, m, M, rows, Z, info, mode, rcond, ws, ws_elems, stream):
         self._count("fallback")
-        inf = _iarr(info, 4)
+        inf = _iarr(info, 5)
         fire = inf[0] != 0 if mode == 0 else (inf[0] != 0 or inf[2] != 0 if mode == 1 else True)
         if not fire:
             return 0
@@ -370,42 +373,45 @@ class FakeTrals:
             inf[3] += 1
         return 0
 
-    def trals_r0_merge_ws_elems(self, N, n, ranks, ks):
+    def trals_dd_transfer_f64(self, Rc, Ra, k, Rb, Ehi, Elo, stream):
+        """Transfer matrix of one tensor in extended precision (the dd planes' semantics)."""
+        self._count("dd_transfer")
+        r = _arr(Rc, Ra * k * Rb).reshape(Ra, k, Rb).astype(np.longdouble)
+        e = np.einsum("aib,cid->acbd", r, r).reshape(Ra * Ra, Rb * Rb)
+        hi = e.astype(np.float64)
+        _arr(Ehi, e.size)[:] = hi.ravel()
+        _arr(Elo, e.size)[:] = (e - hi).astype(np.float64).ravel()
+        return 0
+
+    def trals_dd_r0_ws_elems(self, N, ranks):
         return 1
 
-    def trals_r0_merge_f64(self, N, n, ranks, ks, rt, R0, ws, ws_elems, stream):
-        """R factor of V_[2] (V = subchain of the given tensors, ring.py:138-152) by the documented
-        recipe: merge one tensor at a time, Householder-compress when the lateral exceeds Ra Rc."""
-        self._count("r0_merge")
+    def trals_dd_r0_f64(self, N, n, ranks, Ehi, Elo, S, R0, ws, ws_elems, stream):
+        """S_n from the transfer matrices and its semidefinite Cholesky factor, in extended precision."""
+        self._count("dd_r0")
         r = _vals(ranks, N)
-        k = _vals(ks, N)
-        ps = _ptrs(rt, N)
+        hs, ls = _ptrs(Ehi, N), _ptrs(Elo, N)
         order = list(range(n + 1, N)) + list(range(n))
-
-        def tensor(j):
-            return _arr(ps[j], r[j] * k[j] * r[(j + 1) % N]).reshape(r[j], k[j], r[(j + 1) % N]).copy()
-
-        T = tensor(order[0])
-        steps = order[1:] if len(order) > 1 else [None]
-        for t, j in enumerate(steps):
-            last = t + 1 == len(steps)
-            if j is None:
-                T2 = T
-            else:
-                R = tensor(j)
-                a_, m_, _ = T.shape
-                T2 = np.einsum("amb,bic->aimc", T, R).reshape(a_, -1, R.shape[2])  # lateral mu + m i
-            Ra, rows, Rc = T2.shape
-            mat = T2.transpose(1, 0, 2).reshape(rows, Ra * Rc)  # column c + Rc a
-            if rows > Ra * Rc or last:
-                rr = np.linalg.qr(mat, mode="r")
-                sg = np.sign(np.diagonal(rr)).copy()
-                sg[sg == 0] = 1.0
-                mat = rr * sg[:, None]
-            if last:
-                _arr(R0, mat.size)[:] = mat.ravel()
-                return 0
-            T = mat.reshape(-1, Ra, Rc).transpose(1, 0, 2).copy()
+        F = None
+        for j in order:
+            Rj, Rj1 = r[j], r[(j + 1) % N]
+            sz = Rj * Rj * Rj1 * Rj1
+            e = (_arr(hs[j], sz).astype(np.longdouble) + _arr(ls[j], sz).astype(np.longdouble)).reshape(
+                Rj * Rj, Rj1 * Rj1)
+            F = e.copy() if F is None else F @ e
+        Rn, Rn1 = r[n], r[(n + 1) % N]
+        s = F.reshape(Rn1, Rn1, Rn, Rn).transpose(0, 2, 1, 3).reshape(Rn1 * Rn, Rn1 * Rn)
+        m = s.shape[0]
+        if S:
+            _arr(S, m * m)[:] = s.astype(np.float64).ravel()
+        w = s.copy()
+        u = np.zeros((m, m), dtype=np.longdouble)
+        for j in range(m):
+            d = w[j, j]
+            if d > 0:
+                u[j, j:] = w[j, j:] / np.sqrt(d)
+                w[j + 1:, j + 1:] -= np.outer(u[j, j + 1:], u[j, j + 1:])
+        _arr(R0, m * m)[:] = u.astype(np.float64).ravel()
         return 0
 
     def trals_tri_prepare_f64(self, U, m, F, aux, check_degen, info, stream):
@@ -416,23 +422,28 @@ class FakeTrals:
         if check_degen:
             d = np.abs(np.diagonal(u))
             if d.min() <= 1e-13 * np.max(np.abs(u)):
-                _iarr(info, 4)[2] = int(np.argmin(d)) + 1
+                _iarr(info, 5)[2] = int(np.argmin(d)) + 1
+            if d.min() <= np.sqrt(m * 2.220446049250313e-16) * np.max(np.abs(u)):
+                _iarr(info, 5)[4] = 1
         return 0
 
     def trals_tri_fallback_f64(self, R0, Lr, m, M, rows, Z, info, mode, rcond, ws, ws_elems, stream):
         self._count("fallback")
-        inf = _iarr(info, 4)
-        fire = (inf[2] != 0) if mode == 1 else True
+        inf = _iarr(info, 5)
+        fire = {1: inf[2] != 0 or inf[4] != 0, 2: True, 3: inf[4] != 0}[mode]
         if not fire:
             return 0
+        counted = mode == 1 and inf[2] != 0
         r0 = _arr(R0, Lr * m).reshape(Lr, m)
         rhs = _arr(M, rows * m).reshape(rows, m)
         _, sig, vt = np.linalg.svd(r0, full_matrices=False)
-        keep = sig > rcond * sig[0]
+        keep = sig > max(rcond, np.sqrt(m * 2.220446049250313e-16)) * sig[0]
         v = vt[keep].T
         _arr(Z, rows * m)[:] = (((rhs @ v) / sig[keep] ** 2) @ v.T).ravel()
         if mode == 1:
             inf[2] = 0
+        inf[4] = 0
+        if counted:
             inf[3] += 1
         return 0
 

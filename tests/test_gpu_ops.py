@@ -379,33 +379,43 @@ def test_env_oz64_extreme_rows():
 
 
 # ---------------------------------------------------------------------------
-# R0 without V (TR-ALS-QR solvers.py:422-424, Alg. 1 :337-339): merges + Householder compressions
+# R0 without V (TR-ALS-QR solvers.py:422-424, Alg. 1 :337-339): double-double Gram chain + Cholesky
 # ---------------------------------------------------------------------------
 def _r0_gpu(rts, ranks, n):
     from paper_2210_11362_b200 import _lib as L
     lib = L.lib()
     N = len(rts)
-    ks = [t.shape[1] for t in rts]
+    s = int(torch.cuda.current_stream().cuda_stream)
     bufs = [cuda(np.ascontiguousarray(t)) for t in rts]
-    ra, ka = L.i32_array(ranks), L.i32_array(ks)
+    E = []
+    for j, t in enumerate(rts):
+        ra, k, rb = t.shape
+        eh = torch.empty(ra * ra * rb * rb, dtype=torch.float64, device="cuda")
+        el = torch.empty_like(eh)
+        L.check(lib.trals_dd_transfer_f64(bufs[j].data_ptr(), ra, k, rb, eh.data_ptr(), el.data_ptr(), s), "dd_tr")
+        E.append((eh, el))
+    ra = L.i32_array(ranks)
     m = ranks[n] * ranks[(n + 1) % N]
-    rows = 1
-    for j in range(N):
-        if j != n:
-            rows *= ks[j]
-    k0 = min(rows, m)
-    out = torch.full((k0, m), float("nan"), dtype=torch.float64, device="cuda")
-    ws = torch.empty(max(1, lib.trals_r0_merge_ws_elems(N, n, ra, ka)), dtype=torch.float64, device="cuda")
-    L.check(lib.trals_r0_merge_f64(N, n, ra, ka, L.ptr_array([b.data_ptr() for b in bufs]), out.data_ptr(),
-                                   ws.data_ptr(), ws.numel(), int(torch.cuda.current_stream().cuda_stream)),
-            "r0_merge")
-    return out.cpu().numpy()
+    out = torch.full((m, m), float("nan"), dtype=torch.float64, device="cuda")
+    S = torch.empty((m, m), dtype=torch.float64, device="cuda")
+    ws = torch.empty(max(1, lib.trals_dd_r0_ws_elems(N, ra)), dtype=torch.float64, device="cuda")
+    L.check(lib.trals_dd_r0_f64(N, n, ra, L.ptr_array([e[0].data_ptr() for e in E]),
+                                L.ptr_array([e[1].data_ptr() for e in E]), S.data_ptr(), out.data_ptr(),
+                                ws.data_ptr(), ws.numel(), s), "dd_r0")
+    return out.cpu().numpy(), S.cpu().numpy()
+
+
+def _degenerate(r):
+    d = np.abs(np.diagonal(r))
+    return d.size < r.shape[1] or d.min() <= 1e-13 * np.abs(r).max()
 
 
 @pytest.mark.parametrize("name", ["spec_n3_i30_r3", "nonuni_n4", "n5_i6", "n2_mat", "odd_n3", "rankdef_n3"])
 @pytest.mark.parametrize("variant", ["qr", "als"])
-def test_r0_merge_matches_reference(name, variant):
-    """The reference's per-mode R0 (qr_economy of V_[2], signs included) to 1e-13 of max|R0|."""
+def test_r0_matches_reference(name, variant):
+    """The reference's per-mode R0 (qr_economy of V_[2], signs included): to 1e-13 of max|R0| where it
+    is full rank; for a rank-deficient V (the reference's R0 is then non-square or has a diagonal below
+    the 1e-13 floor, its trailing rows rounding noise) R0^T R0 to 1e-13 and the same degeneracy verdict."""
     g = load_golden(name)
     r0g = load_golden("r0_modes")
     N = len(g["dims"])
@@ -413,23 +423,50 @@ def test_r0_merge_matches_reference(name, variant):
     rts = [r0g[f"{name}_rt_{j}"] if variant == "qr" else g[f"init_{j}"] for j in range(N)]
     for n in range(N):
         want = r0g[f"{name}_{variant}_r0_{n}"]
-        got = _r0_gpu(rts, ranks, n)
-        assert got.shape == want.shape
-        assert np.abs(got - want).max() <= 1e-13 * max(1.0, np.abs(want).max()), n
+        got, S = _r0_gpu(rts, ranks, n)
+        scale = max(1.0, np.abs(want).max())
+        if not _degenerate(want):
+            assert np.abs(got - want).max() <= 1e-13 * scale, n
+        else:
+            gram = want.T @ want
+            assert np.abs(got.T @ got - gram).max() <= 1e-13 * max(1.0, np.abs(gram).max()), n
+            assert _degenerate(got), n
+        assert np.abs(S - want.T @ want).max() <= 1e-13 * max(1.0, np.abs(S).max())
 
 
 @pytest.mark.parametrize("dims,R", [((40, 40, 40, 40), 20), ((30, 30, 30), 12), ((12, 10, 9, 8, 7), 6)])
-def test_r0_merge_large_vs_explicit_qr(dims, R):
-    """A c5-shaped merge (k = 40 < R^2 = 400: 64000 x 400 compressions) against a Householder QR of the
-    explicitly assembled V_[2] (the reference's operation), every mode."""
+def test_r0_large_vs_explicit_qr(dims, R):
+    """A c5-shaped R0 (k = 40 < R^2 = 400) against a Householder QR of the explicitly assembled V_[2]
+    (the reference's operation), every mode."""
     N = len(dims)
     rng = np.random.default_rng(sum(dims) + R)
     cores = [rng.standard_normal((R, d, R)) for d in dims]
     rts = [O.lateral_qr(c).r_tensor for c in cores]
     for n in range(N):
         _, want = O.qr_signed(O.unfold_cyclic(O.chain_without(rts, n), 1))
-        got = _r0_gpu(rts, [R] * N, n)
+        got, _ = _r0_gpu(rts, [R] * N, n)
         assert rel(got, want) < 1e-12, n
+
+
+def test_r0_resolves_ill_conditioned_v():
+    """cond(V) ~ 1e11 (congruent cores): chol(S) in fp64 cannot resolve sigma_min (S squares the
+    condition number past 1/eps); the double-double R0 reproduces V's singular values (from an SVD of
+    the explicit V_[2]) to the accuracy that SVD itself has, eps sigma_max absolute."""
+    rng = np.random.default_rng(9)
+    dims, R = (20, 20, 20), 3
+    cores = []
+    for d in dims:
+        base = rng.standard_normal((d, R * R))
+        base[:, 1] = base[:, 0] + 1e-11 * base[:, 1]  # two nearly collinear columns
+        cores.append(O.fold_classical(base, 1, (R, d, R)))
+    for n in range(3):
+        v = O.unfold_cyclic(O.chain_without(cores, n), 1)
+        sv = np.linalg.svd(v, compute_uv=False)
+        assert sv[-1] / sv[0] < 1e-9  # genuinely ill-conditioned
+        got, _ = _r0_gpu(cores, [R] * 3, n)
+        sg = np.linalg.svd(got, compute_uv=False)
+        assert np.abs(sg - sv).max() <= 1e-14 * sv[0]
+        assert abs(sg[-1] - sv[-1]) <= 1e-3 * sv[-1] + 1e-15 * sv[0]
 
 
 @pytest.mark.parametrize("m,rows", [(25, 100), (64, 64), (100, 500), (400, 160), (113, 40)])
