@@ -122,8 +122,8 @@ int trals_env_oz(const int8_t* d_xdigits, const int32_t* d_xexps, int64_t pre, i
                  void* stream);
 
 /* fp64 environment product on the int8 tensor cores (AlsConfig.fp64_gemm =
- * "ozaki", the default): trals_env_f64 with X given as eight balanced digit
- * planes per K-major row,
+ * "ozaki", the default at c3-c5 under the guard of trals_oz_range_f64): trals_env_f64 with X given as
+ * seven balanced digit planes per K-major row,
  *   x = 2^ex[r] (d_0 + (d_1 + (d_2 + ...) / 254) / 254) / 127,  |d_s| <= 127  (7 digits),
  * (remainder <= 2^-55.9 2^ex[r], |x| < 2^ex[r]; same tiled layout as above with 7 planes,
  * trals_oz64_digits_bytes bytes), the half chain sliced the same way per call,

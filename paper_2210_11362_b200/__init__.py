@@ -11,13 +11,18 @@ package does not need a GPU, calling a solver does.
 from .errors import DegenerateTriangularError, ElementBudgetError, StaleCacheError
 from .estimator import TensorRingALS, exact_relative_error
 from .io import TensorFileError, read_tensor, read_tensor_device, write_tensor
-from .solvers import (BUCKETS, VARIANTS, AlsConfig, AlsReport, decompose, tr_als, tr_als_ne, tr_als_qr,
-                      tr_als_qrne)
-from .synthetic import CORE_KINDS, SynthSpec, make_dataset
+from .ring import (Mode2Qr, gram_chain, gram_chain_order, lateral_gram, mode2_qr, random_cores, reconstruct,
+                   subchain_merge, subchain_skip, tr_inner, tr_norm, validate_cores)
+from .solvers import (BUCKETS, VARIANTS, AlsConfig, AlsReport, SweepCache, cheap_relative_error, decompose, tr_als,
+                      tr_als_ne, tr_als_qr, tr_als_qrne)
+from .synthetic import CORE_KINDS, SynthSpec, add_noise, make_dataset
 
 __version__ = "0.1.0"
 
-__all__ = ["AlsConfig", "AlsReport", "decompose", "tr_als", "tr_als_ne", "tr_als_qr", "tr_als_qrne",
-           "VARIANTS", "BUCKETS", "DegenerateTriangularError", "ElementBudgetError", "StaleCacheError",
-           "TensorRingALS", "exact_relative_error", "SynthSpec", "make_dataset", "CORE_KINDS", "read_tensor",
-           "read_tensor_device", "write_tensor", "TensorFileError", "__version__"]
+# the reference package's names (pkg/src/tenring/__init__.py:9-37) plus this package's extensions
+__all__ = ["TensorRingALS", "Mode2Qr", "gram_chain", "gram_chain_order", "lateral_gram", "mode2_qr", "random_cores",
+           "reconstruct", "subchain_merge", "subchain_skip", "tr_inner", "tr_norm", "validate_cores", "VARIANTS",
+           "AlsConfig", "AlsReport", "cheap_relative_error", "decompose", "exact_relative_error", "tr_als",
+           "tr_als_ne", "tr_als_qr", "tr_als_qrne", "SynthSpec", "add_noise", "make_dataset", "__version__",
+           "SweepCache", "BUCKETS", "DegenerateTriangularError", "ElementBudgetError", "StaleCacheError", "CORE_KINDS",
+           "read_tensor", "read_tensor_device", "write_tensor", "TensorFileError"]

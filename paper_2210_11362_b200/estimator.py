@@ -61,8 +61,7 @@ class TensorRingALS(BaseEstimator):
     """Tensor-ring decomposition fitted by alternating least squares on a B200.
 
     Parameters and attributes are the reference's (estimator.py:16-72):
-    rank, variant ('ne' | 'qr' | 'qrne'; 'als' raises NotImplementedError as
-    `tr_als` does here), max_iter, tol, error_mode, random_state,
+    rank, variant ('als' | 'ne' | 'qr' | 'qrne', all on the GPU), max_iter, tol, error_mode, random_state,
     rank_deficient_fallback, element_budget; fitted `cores_`, `errors_`,
     `n_iter_`, `report_`, `dims_`.  `dtype` (extension, default "float64")
     selects the fp32 variant.

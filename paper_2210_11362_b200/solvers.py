@@ -98,6 +98,64 @@ class AlsReport:
         return self.errors[-1] if self.errors else None
 
 
+@dataclass
+class SweepCache:
+    """End-of-sweep intermediates behind cheap_relative_error (reference solvers.py:140-161): same
+    fields; only those of the variant are set, and `fresh` must be True (end of a full sweep)."""
+
+    variant: str
+    x_norm: float
+    fresh: bool = False
+    core_mat: np.ndarray = None      # updated last core, classical 2-unfolding
+    m_last: np.ndarray = None        # als/ne/qrne: data-times-coefficient product
+    s_last: np.ndarray = None        # ne/qrne: coefficient Gram matrix
+    w_last: np.ndarray = None        # qr: compressed data block
+    r0_last: np.ndarray = None       # qr: triangular factor of the subchain
+    r_core_mat: np.ndarray = None    # qr/qrne: triangular factor of the updated core
+    c_last: np.ndarray = None        # als: q.T @ X_cyc(n).T from the block QR
+    r_a_last: np.ndarray = None      # als: triangular factor of the block QR
+
+
+def cheap_relative_error(cache):
+    """Relative error from sweep intermediates (reference solvers.py:177-212): sqrt(max(0, |X|^2 -
+    2 cross + model)) / |X| with the variant's cross and model terms, evaluated on the GPU.  The solvers
+    compute the same identity on the device every sweep (trals_error_terms_f64); this is the
+    reference's standalone function for a caller-held cache."""
+    import torch
+    if not isinstance(cache, SweepCache):
+        raise TypeError("cheap_relative_error expects a SweepCache")
+    if not cache.fresh:
+        raise StaleCacheError("cheap error is only defined at the end of a full sweep")
+    if cache.x_norm == 0.0:
+        return 0.0
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2210_11362_b200 needs a CUDA device (no CPU fallback)")
+    dev = torch.device("cuda", torch.cuda.current_device())
+
+    def t(a):
+        return torch.as_tensor(np.asarray(a, dtype=np.float64), device=dev)
+
+    def dot(a, b):
+        return float(torch.sum(a * b).item())
+
+    g = t(cache.core_mat)
+    if cache.variant == "ne":
+        cross, model = dot(t(cache.m_last), g), dot(t(cache.s_last), g.T @ g)
+    elif cache.variant == "qr":
+        r0, rz = t(cache.r0_last), t(cache.r_core_mat)
+        cross, model = dot(t(cache.w_last), g @ r0.T), dot(r0.T @ r0, rz.T @ rz)
+    elif cache.variant == "qrne":
+        rz = t(cache.r_core_mat)
+        cross, model = dot(t(cache.m_last), g), dot(t(cache.s_last), rz.T @ rz)
+    elif cache.variant == "als":
+        ra = t(cache.r_a_last)
+        cross, model = dot(t(cache.c_last), ra @ g.T), dot(ra.T @ ra, g.T @ g)
+    else:
+        raise ValueError(f"unknown variant {cache.variant!r}")
+    sq = cache.x_norm ** 2 - 2.0 * cross + model
+    return math.sqrt(max(0.0, sq)) / cache.x_norm
+
+
 def _validate(x, config, variant):
     """solvers.py:224-246 validation order and messages."""
     if variant not in VARIANTS:

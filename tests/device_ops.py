@@ -1,15 +1,16 @@
-"""Tensor-level wrappers over the C-ABI (torch tensors in, torch tensors out).
+"""TEST SUPPORT: tensor-level wrappers over the C-ABI (torch tensors in, torch tensors out).
 
-These are the device operators the sweep engine is built from, exposed one
-by one so the parity tests can check each against the oracle.  All inputs
-must be CUDA float64 tensors; nothing here falls back to the CPU.
+The device operators the sweep engine is built from, exposed one by one so
+the operator-level parity tests (tests/test_gpu_ops.py) can check each
+against the oracle.  All inputs must be CUDA float64 tensors; nothing here
+falls back to the CPU.  Not part of the product package.
 """
 
 from __future__ import annotations
 
 import torch
 
-from . import _lib as L
+from paper_2210_11362_b200 import _lib as L
 
 
 def _stream():

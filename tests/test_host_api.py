@@ -56,3 +56,31 @@ def test_fp64_gemm_auto_policy(dims, ranks, want):
     assert SweepEngine(x, dims, ranks, "ne", fp64_gemm="dmma", _test_lib=FakeTrals()).fp64_gemm == "dmma"
     with pytest.raises(ValueError, match="unknown fp64_gemm"):
         SweepEngine(x, dims, ranks, "ne", fp64_gemm="fast", _test_lib=FakeTrals())
+
+
+def test_reference_names_exported():
+    """Every name of the reference package's surface (pkg/src/tenring/__init__.py:9-37) is importable."""
+    import paper_2210_11362_b200 as P
+    for name in ("TensorRingALS", "Mode2Qr", "gram_chain", "gram_chain_order", "lateral_gram", "mode2_qr",
+                 "random_cores", "reconstruct", "subchain_merge", "subchain_skip", "tr_inner", "tr_norm",
+                 "validate_cores", "VARIANTS", "AlsConfig", "AlsReport", "cheap_relative_error", "decompose",
+                 "exact_relative_error", "tr_als", "tr_als_ne", "tr_als_qr", "tr_als_qrne", "SynthSpec", "add_noise",
+                 "make_dataset", "__version__"):
+        assert hasattr(P, name), name
+        assert name in P.__all__
+    assert P.gram_chain_order(2, 5) == [1, 0, 4, 3]
+
+
+def test_helpers_have_no_cpu_path():
+    """The device helpers fail loudly without a GPU (no silent numpy fallback)."""
+    import torch
+
+    import paper_2210_11362_b200 as P
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    g = np.ones((2, 3, 2))
+    with pytest.raises(RuntimeError, match="CUDA"):
+        P.lateral_gram(g)
+    with pytest.raises(RuntimeError, match="CUDA"):
+        P.cheap_relative_error(P.SweepCache(variant="ne", x_norm=1.0, fresh=True, core_mat=np.ones((3, 4)),
+                                            m_last=np.ones((3, 4)), s_last=np.eye(4)))
