@@ -199,6 +199,15 @@ int64_t trals_chol_solve_ws_elems(int64_t rows, int m);
 int trals_chol_solve_f64(const double* d_U, const double* d_F, const double* d_aux, int m, const double* d_M,
                          int64_t rows, double* d_Z, double* d_ws, int64_t ws_elems, void* stream);
 
+/* trals_chol_solve_f64 with one step of iterative refinement against S (Z0 = solve(M), Z = Z0 +
+ * solve(M - Z0 S)): the solve of the m <= 112 path multiplies by explicit inverses, accurate only to
+ * ~eps cond(S) where S is ill-conditioned (BASELINE c4: cond(S_n) ~ 5e11); the refined Z has the
+ * accuracy of scipy's cho_solve (linalg.py:76).  The engine uses it whenever m <= 112. */
+int64_t trals_chol_solve_refine_ws_elems(int64_t rows, int m);
+int trals_chol_solve_refine_f64(const double* d_U, const double* d_F, const double* d_aux, const double* d_S, int m,
+                                const double* d_M, int64_t rows, double* d_Z, double* d_ws, int64_t ws_elems,
+                                void* stream);
+
 /* Numerical fallback of spd_solve / solve_triangular_block, run right after
  * trals_chol_solve_f64 on the same stream; it returns immediately unless its
  * trigger flag is set.  mode 0 (NE/QRNE, linalg.py:77-81): on a Cholesky

@@ -47,6 +47,8 @@ _SIGNATURES = {
     "trals_cholesky_f64": (c_int, [_dp, c_int, _dp, _dp, _dp, c_int, _dp, c_void_p]),
     "trals_chol_solve_ws_elems": (c_int64, [c_int64, c_int]),
     "trals_chol_solve_f64": (c_int, [_dp, _dp, _dp, c_int, _dp, c_int64, _dp, _dp, c_int64, c_void_p]),
+    "trals_chol_solve_refine_ws_elems": (c_int64, [c_int64, c_int]),
+    "trals_chol_solve_refine_f64": (c_int, [_dp, _dp, _dp, _dp, c_int, _dp, c_int64, _dp, _dp, c_int64, c_void_p]),
     "trals_spd_fallback_ws_elems": (c_int64, [c_int64, c_int]),
     "trals_spd_fallback_f64": (c_int, [_dp, c_int, _dp, c_int64, _dp, _dp, c_int, c_double, _dp, c_int64, c_void_p]),
     "trals_tri_fallback_f64": (c_int, [_dp, c_int, c_int, _dp, c_int64, _dp, _dp, c_int, c_double, _dp, c_int64,

@@ -195,6 +195,8 @@ __global__ void __launch_bounds__(256) dd_chol_diag_kernel(double* __restrict__ 
       R0[o] = c >= r ? a[r][c].hi : 0.0;
     }
   }
+  // the strict lower part of this block's rows of R0
+  for (int t = threadIdx.x; t < pb * p; t += blockDim.x) R0[static_cast<int64_t>(p + t / p) * m + t % p] = 0.0;
 }
 
 // R0 row block p (columns >= p + pb) from the panel rows: rows of R0 = Inv^T W[p.., p+pb..] in dd; the
@@ -212,8 +214,6 @@ __global__ void __launch_bounds__(256) dd_round_rows_kernel(const double* __rest
       Whi[o] = Thi[ot];
       Wlo[o] = Tlo[ot];
       R0[o] = Thi[ot];
-    } else if (c < p) {
-      R0[o] = 0.0;
     }
   }
 }
@@ -224,13 +224,14 @@ struct DdWs {
 
 DdWs dd_ws(int N, const int32_t* ranks) {
   DdWs w{};
-  int64_t emax = 0, smax = 0;
+  int64_t rmax = 0, smax = 0;
   for (int j = 0; j < N; ++j) {
     const int64_t a = ranks[j], b = ranks[(j + 1) % N];
-    emax = std::max(emax, a * a * b * b);
+    rmax = std::max(rmax, a);
     smax = std::max(smax, a * b * a * b);
   }
-  const int64_t chain = std::max(emax, smax);
+  // a chain intermediate is R_{n+1}^2 x R_x^2 for any two ranks: <= rmax^4
+  const int64_t chain = std::max(rmax * rmax * rmax * rmax, smax);
   w.e = 0;                       // 2 planes x 2 ping-pong chain buffers
   w.s = 4 * chain;               // S in dd (2 planes)
   w.w = w.s + 2 * smax;          // Cholesky working matrix (2 planes)

@@ -2541,6 +2541,13 @@ int run_mttsp(const double* X, int N, const int64_t* dims, const int32_t* ranks,
   return TRALS_ERR_ARG;  // unreachable for valid plans
 }
 
+// y += x (fixed order per element: deterministic)
+__global__ void axpy_kernel(const double* __restrict__ x, double* __restrict__ y, int64_t n) {
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < n;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    y[t] += x[t];
+}
+
 }  // namespace
 
 #include "dd_r0.cuh"
@@ -2795,6 +2802,42 @@ int trals_chol_solve_f64(const double* U, const double* F, const double* aux, in
   int st = gemm(Mr, 0, m, 1, 1, rows, m, m, F, m, ws, rm, 0, gws, gws_elems, s);
   if (st) return st;
   return gemm(ws, 0, m, 1, 1, rows, m, m, aux, m, Z, rm, 0, gws, gws_elems, s);
+}
+
+int64_t trals_chol_solve_refine_ws_elems(int64_t rows, int m) {
+  return 3 * rows * m + trals_chol_solve_ws_elems(rows, m);
+}
+
+// One step of iterative refinement around trals_chol_solve_f64: Z0 = solve(M), D = solve(M - Z0 S),
+// Z = Z0 + D.  With the explicit-inverse operands of the m <= 112 path the first solve is accurate
+// only to ~eps cond(S) in S's ill-conditioned directions (BASELINE c4 reaches cond(S_n) ~ 5e11); one
+// refinement step against S brings it to the accuracy of a backward-stable (LAPACK cho_solve) solve.
+int trals_chol_solve_refine_f64(const double* U, const double* F, const double* aux, const double* S, int m,
+                                const double* Mr, int64_t rows, double* Z, double* ws, int64_t ws_elems,
+                                void* stream) {
+  if (!U || !F || !aux || !S || !Mr || !Z || !ws || m < 1) return TRALS_ERR_ARG;
+  if (rows <= 0) return TRALS_OK;
+  if (ws_elems < trals_chol_solve_refine_ws_elems(rows, m)) return TRALS_ERR_WORKSPACE;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t rm_elems = rows * m;
+  double* Rz = ws;               // residual M - Z0 S
+  double* D = ws + rm_elems;     // correction
+  double* Z0 = ws + 2 * rm_elems;
+  double* sws = ws + 3 * rm_elems;
+  const int64_t sws_elems = ws_elems - 3 * rm_elems;
+  if (int st = trals_chol_solve_f64(U, F, aux, m, Mr, rows, Z0, sws, sws_elems, stream)) return st;
+  if (cudaMemcpyAsync(Rz, Mr, sizeof(double) * rm_elems, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+    return TRALS_ERR_CUDA;
+  const CMap rm = rowmajor(m);
+  // Rz -= Z0 S  (A(m = row, k) = Z0[row][k], B = S [k][n])
+  if (int st = gemm(Z0, 0, m, 1, 1, rows, m, m, S, m, Rz, rm, 1, sws, sws_elems, s, -1.0)) return st;
+  if (int st = trals_chol_solve_f64(U, F, aux, m, Rz, rows, D, sws, sws_elems, stream)) return st;
+  // Z = Z0 + D  (as D = D + Z0 I would need an identity; two copies through the GEMM's beta instead)
+  if (cudaMemcpyAsync(Z, Z0, sizeof(double) * rm_elems, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+    return TRALS_ERR_CUDA;
+  const int blocks = static_cast<int>(std::min<int64_t>((rm_elems + 255) / 256, 8 * kSMs));
+  axpy_kernel<<<blocks, 256, 0, s>>>(D, Z, rm_elems);
+  return launch_status();
 }
 
 int64_t trals_sumsq_ws_elems(void) { return 2 * kSumsqBlocks; }

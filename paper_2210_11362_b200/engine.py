@@ -38,6 +38,7 @@ from . import _lib as L
 
 BUCKETS = ("subchain", "mttsp", "solve", "gramqr", "other")  # solvers.py:57
 OZ64_MIN_FLOPS = 4e9  # fp64_gemm="auto": smallest environment product run on the int8 tensor cores
+SMALL_SOLVE_MAX = 112  # m = R_n R_{n+1} <= 112: explicit-inverse solve + one refinement step (trals.h)
 OZ64_MAX_RHO = 2.0 ** 12  # fp64_gemm="auto": largest row dynamic range (max|x| K / sum|x|) of X sliced (trals.h)
 
 
@@ -162,7 +163,8 @@ class SweepEngine:
         self.Lo = self._empty(mmax, mmax)
         self.chol_aux = self._empty(max(1, max(self.lib.trals_cholesky_aux_elems(self.R(n) * self.R(n + 1))
                                               for n in range(N))))
-        self.solve_ws = self._empty(max(1, max(self.lib.trals_chol_solve_ws_elems(self.dims[n], self.R(n) * self.R(n + 1))
+        self.solve_ws = self._empty(max(1, max(self.lib.trals_chol_solve_refine_ws_elems(self.dims[n],
+                                                                                        self.R(n) * self.R(n + 1))
                                               for n in range(N))))
         self.use_rqr = self.variant in ("qr", "qrne")
         if self.use_rqr:
@@ -500,6 +502,14 @@ class SweepEngine:
             self.steps.append(Step("other", lambda n=n: self._debug_check(n), f"debug S{n}"))
 
         def solve(n=n, M=M, rr=rr):
+            if rr <= SMALL_SOLVE_MAX:
+                # explicit-inverse operands: one refinement step against S_n (trals.h)
+                L.check(self.lib.trals_chol_solve_refine_f64(self.U.data_ptr(), self.Lo.data_ptr(),
+                                                             self.chol_aux.data_ptr(), self.S[n].data_ptr(), rr,
+                                                             M.data_ptr(), self.dims[n], self.Gt[n].data_ptr(),
+                                                             self.solve_ws.data_ptr(), self.solve_ws.numel(),
+                                                             self._sp()), "chol_solve_refine")
+                return
             L.check(self.lib.trals_chol_solve_f64(self.U.data_ptr(), self.Lo.data_ptr(), self.chol_aux.data_ptr(), rr,
                                                   M.data_ptr(), self.dims[n], self.Gt[n].data_ptr(),
                                                   self.solve_ws.data_ptr(), self.solve_ws.numel(), self._sp()),

@@ -348,6 +348,13 @@ class FakeTrals:
         _arr(Z, rows * m)[:] = z.ravel()
         return 0
 
+    def trals_chol_solve_refine_ws_elems(self, rows, m):
+        return 1
+
+    def trals_chol_solve_refine_f64(self, U, Lo, aux, S, m, M, rows, Z, ws, ws_elems, stream):
+        self._count("chol_solve")
+        return self.trals_chol_solve_f64(U, Lo, aux, m, M, rows, Z, ws, ws_elems, stream)
+
     def trals_spd_fallback_ws_elems(self, rows, m):
         return 1
 

@@ -457,7 +457,9 @@ def test_r0_resolves_ill_conditioned_v():
     cores = []
     for d in dims:
         base = rng.standard_normal((d, R * R))
-        base[:, 1] = base[:, 0] + 1e-11 * base[:, 1]  # two nearly collinear columns
+        # right-bond columns r_b = 1 nearly equal to r_b = 0 (column r_a + R r_b): the subchain ending in
+        # this core gets two nearly equal columns r_n = 0, 1, whatever mode it skips
+        base[:, R:2 * R] = base[:, :R] + 1e-11 * base[:, R:2 * R]
         cores.append(O.fold_classical(base, 1, (R, d, R)))
     for n in range(3):
         v = O.unfold_cyclic(O.chain_without(cores, n), 1)
