@@ -49,7 +49,8 @@ enum {
   TRALS_INFO_DEGEN = 2,      /* 1-based index of diag <= 1e-13 max|R| (linalg.py:96-99) */
   TRALS_INFO_FALLBACKS = 3,  /* number of fallback solves taken (AlsReport.fallback_count) */
   TRALS_INFO_ILLCOND = 4,    /* QR variants: merged R0's smallest diagonal <= sqrt(m eps) max|R0| */
-  TRALS_INFO_SLOTS = 5
+  TRALS_INFO_REFINE = 5,     /* m <= 112 factor with max|U| > 1e4 min diag(U): refine the solve */
+  TRALS_INFO_SLOTS = 6
 };
 
 const char* trals_strerror(int code);
@@ -199,14 +200,14 @@ int64_t trals_chol_solve_ws_elems(int64_t rows, int m);
 int trals_chol_solve_f64(const double* d_U, const double* d_F, const double* d_aux, int m, const double* d_M,
                          int64_t rows, double* d_Z, double* d_ws, int64_t ws_elems, void* stream);
 
-/* trals_chol_solve_f64 with one step of iterative refinement against S (Z0 = solve(M), Z = Z0 +
- * solve(M - Z0 S)): the solve of the m <= 112 path multiplies by explicit inverses, accurate only to
- * ~eps cond(S) where S is ill-conditioned (BASELINE c4: cond(S_n) ~ 5e11); the refined Z has the
- * accuracy of scipy's cho_solve (linalg.py:76).  The engine uses it whenever m <= 112. */
-int64_t trals_chol_solve_refine_ws_elems(int64_t rows, int m);
-int trals_chol_solve_refine_f64(const double* d_U, const double* d_F, const double* d_aux, const double* d_S, int m,
-                                const double* d_M, int64_t rows, double* d_Z, double* d_ws, int64_t ws_elems,
-                                void* stream);
+/* One step of iterative refinement after trals_chol_solve_f64 on the m <= 112 path (explicit-inverse
+ * operands F = U^{-1}, aux = U^{-T}): R = M - Z S, Z += (R F) aux.  The explicit inverses are accurate
+ * only to ~eps cond(S) where S is ill-conditioned (BASELINE c4: cond(S_n) ~ 5e11); one step brings Z to
+ * the accuracy of scipy's cho_solve (linalg.py:76).  Gated on d_info[TRALS_INFO_REFINE], which the
+ * factorisation (trals_cholesky_f64 / trals_tri_prepare_f64, m <= 112) sets when max|U| > 1e4 min
+ * diag(U); otherwise the kernel returns at once (it stays in the sweep graph). */
+int trals_solve_refine_f64(const double* d_F, const double* d_aux, const double* d_S, int m, const double* d_M,
+                           int64_t rows, double* d_Z, int* d_info, void* stream);
 
 /* Numerical fallback of spd_solve / solve_triangular_block, run right after
  * trals_chol_solve_f64 on the same stream; it returns immediately unless its

@@ -15,7 +15,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libtrals.so")
 
 LAYOUT_C, LAYOUT_SLICE, LAYOUT_ZT, LAYOUT_TT = 0, 1, 2, 3
-INFO_CHOL, INFO_ASYM, INFO_DEGEN, INFO_FALLBACKS, INFO_ILLCOND, INFO_SLOTS = 0, 1, 2, 3, 4, 5
+INFO_CHOL, INFO_ASYM, INFO_DEGEN, INFO_FALLBACKS, INFO_ILLCOND, INFO_REFINE, INFO_SLOTS = 0, 1, 2, 3, 4, 5, 6
 
 _dp = c_void_p  # device pointers travel as void*
 _lib = None
@@ -47,8 +47,7 @@ _SIGNATURES = {
     "trals_cholesky_f64": (c_int, [_dp, c_int, _dp, _dp, _dp, c_int, _dp, c_void_p]),
     "trals_chol_solve_ws_elems": (c_int64, [c_int64, c_int]),
     "trals_chol_solve_f64": (c_int, [_dp, _dp, _dp, c_int, _dp, c_int64, _dp, _dp, c_int64, c_void_p]),
-    "trals_chol_solve_refine_ws_elems": (c_int64, [c_int64, c_int]),
-    "trals_chol_solve_refine_f64": (c_int, [_dp, _dp, _dp, _dp, c_int, _dp, c_int64, _dp, _dp, c_int64, c_void_p]),
+    "trals_solve_refine_f64": (c_int, [_dp, _dp, _dp, c_int, _dp, c_int64, _dp, _dp, c_void_p]),
     "trals_spd_fallback_ws_elems": (c_int64, [c_int64, c_int]),
     "trals_spd_fallback_f64": (c_int, [_dp, c_int, _dp, c_int64, _dp, _dp, c_int, c_double, _dp, c_int64, c_void_p]),
     "trals_tri_fallback_f64": (c_int, [_dp, c_int, c_int, _dp, c_int64, _dp, _dp, c_int, c_double, _dp, c_int64,
@@ -135,5 +134,5 @@ def ptr_array(ptrs):
 
 __all__ = ["lib", "load", "check", "TralsError", "EXPORTED", "i64_array", "i32_array", "ptr_array",
            "LAYOUT_C", "LAYOUT_SLICE", "LAYOUT_ZT", "LAYOUT_TT", "INFO_CHOL", "INFO_ASYM", "INFO_DEGEN",
-           "INFO_FALLBACKS", "INFO_ILLCOND", "INFO_SLOTS",
+           "INFO_FALLBACKS", "INFO_ILLCOND", "INFO_REFINE", "INFO_SLOTS",
            "c_double"]

@@ -1025,6 +1025,8 @@ __device__ int chol8_aug_smem(double* a, int ld, int n, int aug, double* scratch
 
 // Resident factor + inverse for m <= kInvMax: U (upper), W = U^{-1} (upper), V = U^{-T} (lower).
 constexpr int kInvMax = 112;
+// max|U| / min diag(U) above this (cond(S) beyond ~1e8): the explicit-inverse solve is refined once
+constexpr double kRefineRatio = 1e4;
 
 __global__ void __launch_bounds__(512) chol_inv_kernel(const double* __restrict__ S, int m, double* __restrict__ U,
                                                        double* __restrict__ W, double* __restrict__ V,
@@ -1070,7 +1072,6 @@ __global__ void __launch_bounds__(512) chol_inv_kernel(const double* __restrict_
       umax = fmax(umax, fabs(u));
       if (i == j && fabs(u) < dmin) { dmin = fabs(u); didx = i; }
     }
-  if (!check_degen) return;
   for (int o = 16; o > 0; o >>= 1) {
     umax = fmax(umax, __shfl_xor_sync(0xffffffffu, umax, o));
     const double od = __shfl_xor_sync(0xffffffffu, dmin, o);
@@ -1089,7 +1090,9 @@ __global__ void __launch_bounds__(512) chol_inv_kernel(const double* __restrict_
       mx = fmax(mx, red[w]);
       if (sd[w] < dm || (sd[w] == dm && si[w] < di)) { dm = sd[w]; di = si[w]; }
     }
-    if (dm <= 1e-13 * mx) info[TRALS_INFO_DEGEN] = di + 1;  // linalg.py:96-99
+    if (check_degen && dm <= 1e-13 * mx) info[TRALS_INFO_DEGEN] = di + 1;  // linalg.py:96-99
+    // ill-conditioned factor: the explicit-inverse solve gets one refinement step (trals_solve_refine_f64)
+    info[TRALS_INFO_REFINE] = (dm > 0.0 && mx > kRefineRatio * dm) ? 1 : 0;
   }
 }
 
@@ -1234,6 +1237,7 @@ __global__ void __launch_bounds__(1024) degen_kernel(const double* __restrict__ 
     }
     if (d <= 1e-13 * a) info[TRALS_INFO_DEGEN] = di + 1;  // linalg.py:96-99
     if (ill_scale > 0.0 && d <= ill_scale * a) info[TRALS_INFO_ILLCOND] = 1;
+    if (m <= kInvMax) info[TRALS_INFO_REFINE] = (d > 0.0 && a > kRefineRatio * d) ? 1 : 0;
   }
 }
 
@@ -2541,11 +2545,39 @@ int run_mttsp(const double* X, int N, const int64_t* dims, const int32_t* ranks,
   return TRALS_ERR_ARG;  // unreachable for valid plans
 }
 
-// y += x (fixed order per element: deterministic)
-__global__ void axpy_kernel(const double* __restrict__ x, double* __restrict__ y, int64_t n) {
-  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < n;
-       t += static_cast<int64_t>(gridDim.x) * blockDim.x)
-    y[t] += x[t];
+// One step of iterative refinement of Z S = M for the explicit-inverse operands of the m <= 112
+// factor (F = U^{-1}, aux = U^{-T}): R = M - Z S, Z += (R F) aux, one CTA per right-hand-side row,
+// fixed summation order.  Runs only when the factorisation raised d_info[TRALS_INFO_REFINE]
+// (max|U| / min diag(U) > 1e4, i.e. cond(S) beyond ~1e8 -- BASELINE c4's over-specified ranks);
+// otherwise it returns at once, so it sits in the sweep graph unconditionally.
+__global__ void __launch_bounds__(128) refine_kernel(const double* __restrict__ F, const double* __restrict__ aux,
+                                                     const double* __restrict__ S, int m,
+                                                     const double* __restrict__ Mr, int64_t rows,
+                                                     double* __restrict__ Z, const int* __restrict__ info) {
+  if (info[TRALS_INFO_REFINE] == 0) return;
+  __shared__ double z[128], r[128], t[128];
+  for (int64_t row = blockIdx.x; row < rows; row += gridDim.x) {
+    for (int c = threadIdx.x; c < m; c += blockDim.x) z[c] = Z[row * m + c];
+    __syncthreads();
+    for (int c = threadIdx.x; c < m; c += blockDim.x) {
+      double acc = Mr[row * m + c];
+      for (int k = 0; k < m; ++k) acc = fma(-z[k], S[k * m + c], acc);
+      r[c] = acc;
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < m; c += blockDim.x) {
+      double acc = 0.0;
+      for (int k = 0; k < m; ++k) acc = fma(r[k], F[k * m + c], acc);
+      t[c] = acc;
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < m; c += blockDim.x) {
+      double acc = 0.0;
+      for (int k = 0; k < m; ++k) acc = fma(t[k], aux[k * m + c], acc);
+      Z[row * m + c] = z[c] + acc;
+    }
+    __syncthreads();
+  }
 }
 
 }  // namespace
@@ -2804,39 +2836,12 @@ int trals_chol_solve_f64(const double* U, const double* F, const double* aux, in
   return gemm(ws, 0, m, 1, 1, rows, m, m, aux, m, Z, rm, 0, gws, gws_elems, s);
 }
 
-int64_t trals_chol_solve_refine_ws_elems(int64_t rows, int m) {
-  return 3 * rows * m + trals_chol_solve_ws_elems(rows, m);
-}
-
-// One step of iterative refinement around trals_chol_solve_f64: Z0 = solve(M), D = solve(M - Z0 S),
-// Z = Z0 + D.  With the explicit-inverse operands of the m <= 112 path the first solve is accurate
-// only to ~eps cond(S) in S's ill-conditioned directions (BASELINE c4 reaches cond(S_n) ~ 5e11); one
-// refinement step against S brings it to the accuracy of a backward-stable (LAPACK cho_solve) solve.
-int trals_chol_solve_refine_f64(const double* U, const double* F, const double* aux, const double* S, int m,
-                                const double* Mr, int64_t rows, double* Z, double* ws, int64_t ws_elems,
-                                void* stream) {
-  if (!U || !F || !aux || !S || !Mr || !Z || !ws || m < 1) return TRALS_ERR_ARG;
+int trals_solve_refine_f64(const double* F, const double* aux, const double* S, int m, const double* Mr,
+                           int64_t rows, double* Z, int* info, void* stream) {
+  if (!F || !aux || !S || !Mr || !Z || !info || m < 1 || m > kInvMax) return TRALS_ERR_ARG;
   if (rows <= 0) return TRALS_OK;
-  if (ws_elems < trals_chol_solve_refine_ws_elems(rows, m)) return TRALS_ERR_WORKSPACE;
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const int64_t rm_elems = rows * m;
-  double* Rz = ws;               // residual M - Z0 S
-  double* D = ws + rm_elems;     // correction
-  double* Z0 = ws + 2 * rm_elems;
-  double* sws = ws + 3 * rm_elems;
-  const int64_t sws_elems = ws_elems - 3 * rm_elems;
-  if (int st = trals_chol_solve_f64(U, F, aux, m, Mr, rows, Z0, sws, sws_elems, stream)) return st;
-  if (cudaMemcpyAsync(Rz, Mr, sizeof(double) * rm_elems, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
-    return TRALS_ERR_CUDA;
-  const CMap rm = rowmajor(m);
-  // Rz -= Z0 S  (A(m = row, k) = Z0[row][k], B = S [k][n])
-  if (int st = gemm(Z0, 0, m, 1, 1, rows, m, m, S, m, Rz, rm, 1, sws, sws_elems, s, -1.0)) return st;
-  if (int st = trals_chol_solve_f64(U, F, aux, m, Rz, rows, D, sws, sws_elems, stream)) return st;
-  // Z = Z0 + D  (as D = D + Z0 I would need an identity; two copies through the GEMM's beta instead)
-  if (cudaMemcpyAsync(Z, Z0, sizeof(double) * rm_elems, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
-    return TRALS_ERR_CUDA;
-  const int blocks = static_cast<int>(std::min<int64_t>((rm_elems + 255) / 256, 8 * kSMs));
-  axpy_kernel<<<blocks, 256, 0, s>>>(D, Z, rm_elems);
+  refine_kernel<<<static_cast<unsigned>(std::min<int64_t>(rows, 65535)), 128, 0, static_cast<cudaStream_t>(stream)>>>(
+      F, aux, S, m, Mr, rows, Z, info);
   return launch_status();
 }
 

@@ -163,8 +163,7 @@ class SweepEngine:
         self.Lo = self._empty(mmax, mmax)
         self.chol_aux = self._empty(max(1, max(self.lib.trals_cholesky_aux_elems(self.R(n) * self.R(n + 1))
                                               for n in range(N))))
-        self.solve_ws = self._empty(max(1, max(self.lib.trals_chol_solve_refine_ws_elems(self.dims[n],
-                                                                                        self.R(n) * self.R(n + 1))
+        self.solve_ws = self._empty(max(1, max(self.lib.trals_chol_solve_ws_elems(self.dims[n], self.R(n) * self.R(n + 1))
                                               for n in range(N))))
         self.use_rqr = self.variant in ("qr", "qrne")
         if self.use_rqr:
@@ -502,18 +501,17 @@ class SweepEngine:
             self.steps.append(Step("other", lambda n=n: self._debug_check(n), f"debug S{n}"))
 
         def solve(n=n, M=M, rr=rr):
-            if rr <= SMALL_SOLVE_MAX:
-                # explicit-inverse operands: one refinement step against S_n (trals.h)
-                L.check(self.lib.trals_chol_solve_refine_f64(self.U.data_ptr(), self.Lo.data_ptr(),
-                                                             self.chol_aux.data_ptr(), self.S[n].data_ptr(), rr,
-                                                             M.data_ptr(), self.dims[n], self.Gt[n].data_ptr(),
-                                                             self.solve_ws.data_ptr(), self.solve_ws.numel(),
-                                                             self._sp()), "chol_solve_refine")
-                return
             L.check(self.lib.trals_chol_solve_f64(self.U.data_ptr(), self.Lo.data_ptr(), self.chol_aux.data_ptr(), rr,
                                                   M.data_ptr(), self.dims[n], self.Gt[n].data_ptr(),
                                                   self.solve_ws.data_ptr(), self.solve_ws.numel(), self._sp()),
                     "chol_solve")
+            if rr <= SMALL_SOLVE_MAX:
+                # explicit-inverse operands: one refinement step against S_n when the factor is
+                # ill-conditioned (device-side gate, trals.h)
+                L.check(self.lib.trals_solve_refine_f64(self.Lo.data_ptr(), self.chol_aux.data_ptr(),
+                                                        self.S[n].data_ptr(), rr, M.data_ptr(), self.dims[n],
+                                                        self.Gt[n].data_ptr(), self.info.data_ptr(), self._sp()),
+                        "solve_refine")
         if not self._r0_nonsquare(n):
             self.steps.append(Step("solve", solve, f"solve{n}"))
         # numerical fallbacks of the reference (linalg.py:77-81, solvers.py:262-273): the kernel is a

@@ -318,7 +318,7 @@ class FakeTrals:
     def trals_cholesky_f64(self, S, m, U, Lo, aux, check_degen, info, stream):
         self._count("cholesky")
         s = _arr(S, m * m).reshape(m, m)
-        inf = _iarr(info, 5)
+        inf = _iarr(info, 6)
         scale = np.max(np.abs(s))
         if scale > 0 and np.max(np.abs(s - s.T)) > 1e-8 * scale:
             inf[1] = 1
@@ -348,19 +348,16 @@ class FakeTrals:
         _arr(Z, rows * m)[:] = z.ravel()
         return 0
 
-    def trals_chol_solve_refine_ws_elems(self, rows, m):
-        return 1
-
-    def trals_chol_solve_refine_f64(self, U, Lo, aux, S, m, M, rows, Z, ws, ws_elems, stream):
-        self._count("chol_solve")
-        return self.trals_chol_solve_f64(U, Lo, aux, m, M, rows, Z, ws, ws_elems, stream)
+    def trals_solve_refine_f64(self, F, aux, S, m, M, rows, Z, info, stream):
+        self._count("refine")  # the numpy model's solve is already a backward-stable triangular solve
+        return 0
 
     def trals_spd_fallback_ws_elems(self, rows, m):
         return 1
 
     def trals_spd_fallback_f64(self, S, m, M, rows, Z, info, mode, rcond, ws, ws_elems, stream):
         self._count("fallback")
-        inf = _iarr(info, 5)
+        inf = _iarr(info, 6)
         fire = inf[0] != 0 if mode == 0 else (inf[0] != 0 or inf[2] != 0 if mode == 1 else True)
         if not fire:
             return 0
@@ -429,14 +426,14 @@ class FakeTrals:
         if check_degen:
             d = np.abs(np.diagonal(u))
             if d.min() <= 1e-13 * np.max(np.abs(u)):
-                _iarr(info, 5)[2] = int(np.argmin(d)) + 1
+                _iarr(info, 6)[2] = int(np.argmin(d)) + 1
             if d.min() <= np.sqrt(m * 2.220446049250313e-16) * np.max(np.abs(u)):
-                _iarr(info, 5)[4] = 1
+                _iarr(info, 6)[4] = 1
         return 0
 
     def trals_tri_fallback_f64(self, R0, Lr, m, M, rows, Z, info, mode, rcond, ws, ws_elems, stream):
         self._count("fallback")
-        inf = _iarr(info, 5)
+        inf = _iarr(info, 6)
         fire = {1: inf[2] != 0 or inf[4] != 0, 2: True, 3: inf[4] != 0}[mode]
         if not fire:
             return 0

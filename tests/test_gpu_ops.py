@@ -97,7 +97,7 @@ def test_cholesky_solve(m, rows):
     s = a.T @ a
     rhs = rng.standard_normal((rows, m))
     f = ops.cholesky(cuda(s))
-    assert f.info.cpu().numpy().tolist() == [0] * 5
+    assert f.info.cpu().numpy().tolist() == [0] * 6
     ref_u = np.linalg.cholesky(s).T
     assert rel(f.U.cpu().numpy(), ref_u) < 1e-12
     if m <= 112:
@@ -599,3 +599,44 @@ def test_oz64_guard_adversarial():
     assert e_dmma < 1e-14
     assert e_oz > 1e3 * e_dmma            # the failure mode the guard exists for
     assert out.item() > 2.0 ** 12         # ... and the guard sees it
+
+
+def test_solve_refinement_on_ill_conditioned_s():
+    """m <= 112, cond(S) ~ 1e11 (BASELINE c4's regime): the explicit-inverse solve alone is accurate only to
+    ~eps cond(S); the gated refinement step (raised by the factorisation) brings the backward error of
+    Z S = M to the level of scipy's cho_solve.  A well-conditioned S leaves the gate closed."""
+    import scipy.linalg as sla
+
+    import device_ops as ops
+    from paper_2210_11362_b200 import _lib as L
+    lib = L.lib()
+    rng = np.random.default_rng(4)
+    m, rows = 64, 40
+    q, _ = np.linalg.qr(rng.standard_normal((m, m)))
+    s = (q * np.logspace(0, -11, m)) @ q.T
+    s = 0.5 * (s + s.T)
+    rhs = rng.standard_normal((rows, m)) @ s  # a consistent right-hand side
+    f = ops.cholesky(cuda(s))
+    assert int(f.info[L.INFO_REFINE].item()) == 1
+    z0 = ops.chol_solve(f, cuda(rhs))
+    z = z0.clone()
+    L.check(lib.trals_solve_refine_f64(f.L.data_ptr(), f.aux.data_ptr(), cuda(s).data_ptr(), m, cuda(rhs).data_ptr(),
+                                       rows, z.data_ptr(), f.info.data_ptr(),
+                                       int(torch.cuda.current_stream().cuda_stream)), "refine")
+    zr = sla.cho_solve(sla.cho_factor(s), rhs.T).T
+
+    def backward(zz):
+        return np.linalg.norm(zz @ s - rhs) / (np.linalg.norm(s) * np.linalg.norm(zz))
+    assert backward(z.cpu().numpy()) <= 10 * backward(zr) + 1e-16
+    assert backward(z.cpu().numpy()) < backward(z0.cpu().numpy())
+    # well conditioned: gate closed, Z untouched
+    s2 = rng.standard_normal((3 * m, m))
+    s2 = s2.T @ s2
+    f2 = ops.cholesky(cuda(s2))
+    assert int(f2.info[L.INFO_REFINE].item()) == 0
+    z2 = ops.chol_solve(f2, cuda(rhs))
+    before = z2.clone()
+    L.check(lib.trals_solve_refine_f64(f2.L.data_ptr(), f2.aux.data_ptr(), cuda(s2).data_ptr(), m,
+                                       cuda(rhs).data_ptr(), rows, z2.data_ptr(), f2.info.data_ptr(),
+                                       int(torch.cuda.current_stream().cuda_stream)), "refine")
+    assert torch.equal(z2, before)
