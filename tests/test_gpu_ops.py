@@ -616,11 +616,12 @@ def test_solve_refinement_on_ill_conditioned_s():
     s = (q * np.logspace(0, -11, m)) @ q.T
     s = 0.5 * (s + s.T)
     rhs = rng.standard_normal((rows, m)) @ s  # a consistent right-hand side
-    f = ops.cholesky(cuda(s))
+    sd, md = cuda(s), cuda(rhs)  # keep the device copies alive while the kernels use them
+    f = ops.cholesky(sd)
     assert int(f.info[L.INFO_REFINE].item()) == 1
-    z0 = ops.chol_solve(f, cuda(rhs))
+    z0 = ops.chol_solve(f, md)
     z = z0.clone()
-    L.check(lib.trals_solve_refine_f64(f.L.data_ptr(), f.aux.data_ptr(), cuda(s).data_ptr(), m, cuda(rhs).data_ptr(),
+    L.check(lib.trals_solve_refine_f64(f.L.data_ptr(), f.aux.data_ptr(), sd.data_ptr(), m, md.data_ptr(),
                                        rows, z.data_ptr(), f.info.data_ptr(),
                                        int(torch.cuda.current_stream().cuda_stream)), "refine")
     zr = sla.cho_solve(sla.cho_factor(s), rhs.T).T
@@ -632,11 +633,12 @@ def test_solve_refinement_on_ill_conditioned_s():
     # well conditioned: gate closed, Z untouched
     s2 = rng.standard_normal((3 * m, m))
     s2 = s2.T @ s2
-    f2 = ops.cholesky(cuda(s2))
+    s2d = cuda(s2)
+    f2 = ops.cholesky(s2d)
     assert int(f2.info[L.INFO_REFINE].item()) == 0
-    z2 = ops.chol_solve(f2, cuda(rhs))
+    z2 = ops.chol_solve(f2, md)
     before = z2.clone()
-    L.check(lib.trals_solve_refine_f64(f2.L.data_ptr(), f2.aux.data_ptr(), cuda(s2).data_ptr(), m,
-                                       cuda(rhs).data_ptr(), rows, z2.data_ptr(), f2.info.data_ptr(),
+    L.check(lib.trals_solve_refine_f64(f2.L.data_ptr(), f2.aux.data_ptr(), s2d.data_ptr(), m,
+                                       md.data_ptr(), rows, z2.data_ptr(), f2.info.data_ptr(),
                                        int(torch.cuda.current_stream().cuda_stream)), "refine")
     assert torch.equal(z2, before)
