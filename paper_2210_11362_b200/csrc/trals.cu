@@ -15,6 +15,7 @@
 #include "dmma_gemm.cuh"
 #include "dmma_tma_gemm.cuh"
 #include "tc_int8_gemm.cuh"
+#include "crt_int8_gemm.cuh"
 
 using trals::CMap;
 using trals::GemmArgs;
@@ -586,6 +587,238 @@ int gemm_oz(const int8_t* ad, const int32_t* ea, int64_t M, int64_t K, int64_t N
     return launch_status();
   }
   return TRALS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// fp64 environment products by CRT on the int8 tensor cores (crt_int8_gemm.cuh)
+// ---------------------------------------------------------------------------
+// moduli tables: computed once on the host (128-bit integers) and copied to constant memory.
+// TRALS_CRT_MODULI (experiments) = number of moduli, 12..16 (fewer moduli = fewer GEMMs and
+// fewer operand bits: every dropped modulus costs ~4 bits per operand).
+struct CrtHost {
+  trals::CrtTables t{};
+  bool ok = false;
+};
+const CrtHost& crt_host() {
+  static const CrtHost h = [] {
+    CrtHost c;
+    static const uint32_t moduli[trals::kCrtMaxMod] = {
+#define TRALS_CRT_LIST(i, pp) pp,
+        TRALS_CRT_MODULI(TRALS_CRT_LIST)
+#undef TRALS_CRT_LIST
+    };
+    int nm = std::getenv("TRALS_CRT_MODULI") ? std::atoi(std::getenv("TRALS_CRT_MODULI")) : trals::kCrtMaxMod;
+    nm = std::max(12, std::min(nm, trals::kCrtMaxMod));
+    using u128 = unsigned __int128;
+    u128 P = 1;
+    long double lg = 0;
+    for (int i = 0; i < nm; ++i) {
+      P *= moduli[i];
+      lg += std::log2(static_cast<long double>(moduli[i]));
+    }
+    c.t.nm = nm;
+    c.t.P0 = static_cast<uint64_t>(P);
+    c.t.P1 = static_cast<uint64_t>(P >> 64);
+    for (int i = 0; i < trals::kCrtMaxMod; ++i) {
+      const uint32_t p = moduli[i];
+      c.t.p[i] = p;
+      c.t.magic[i] = static_cast<uint32_t>(((1ull << 39) + p - 1) / p);
+      c.t.offs[i] = p * ((1u << 30) / p);
+      c.t.invp[i] = 1.0f / static_cast<float>(p);
+      if (i >= nm) continue;
+      const u128 W = P / p;
+      c.t.w0[i] = static_cast<uint64_t>(W);
+      c.t.w1[i] = static_cast<uint64_t>(W >> 64);
+      const uint32_t wr = static_cast<uint32_t>(W % p);
+      uint32_t q = 0;
+      for (uint32_t z = 1; z < p; ++z)
+        if ((wr * z) % p == 1) { q = z; break; }
+      if (!q) return c;  // (moduli not coprime: cannot happen)
+      c.t.qinv[i] = q;
+    }
+    // ||a'|| ||b'|| <= 2^(ga+gb) < P / 2; rows are int64 -> each <= 62
+    int gtot = static_cast<int>(std::floor(static_cast<double>(lg) - 1.0 - 0.01));
+    gtot = std::min(gtot, 124);
+    c.t.ga = (gtot + 1) / 2;
+    c.t.gb = gtot / 2;
+    if (!((static_cast<u128>(1) << (c.t.ga + c.t.gb + 1)) < P)) return c;
+    if (cudaMemcpyToSymbol(trals::crt_tab, &c.t, sizeof(c.t)) != cudaSuccess) return c;
+    c.ok = true;
+    return c;
+  }();
+  return h;
+}
+
+inline int crt_n16(int64_t N) { return static_cast<int>((N + 15) / 16 * 16); }
+inline bool crt_shape_ok(int64_t M, int64_t K, int64_t N) {
+  return M >= 1 && K >= 1 && N >= 1 && N <= trals::kCrtMaxN && M <= INT32_MAX && K <= INT32_MAX &&
+         (M + trals::kCrtBM - 1) / trals::kCrtBM * trals::kCrtMaxMod * 64 < INT32_MAX;
+}
+inline int64_t crt_kblocks(int64_t K) { return (K + trals::kCrtBK - 1) / trals::kCrtBK; }
+inline int64_t crt_mtiles(int64_t M) { return (M + trals::kCrtBM - 1) / trals::kCrtBM; }
+// bytes of the residue planes of a [rows][K] operand tiled in row tiles of tile_w
+inline int64_t crt_plane_bytes(int64_t rows_pad, int64_t K) { return rows_pad * crt_kblocks(K) * trals::kCrtBK; }
+
+// column statistics slabs: about 4 blocks per SM in total, at least 64 rows per slab
+inline void crt_col_slabs(int64_t rows, int64_t cols, int& slabs, int64_t& rows_per_slab) {
+  const int64_t cblocks = (cols + 31) / 32;
+  const int64_t want = std::max<int64_t>(1, 4 * kSMs / cblocks);
+  rows_per_slab = std::max<int64_t>(64, (rows + want - 1) / want);
+  slabs = static_cast<int>((rows + rows_per_slab - 1) / rows_per_slab);
+}
+
+// K splits: never more than kCrtKmax k per item (int32 sums), more when the items are too few
+// to fill the SMs; cost model in k units (an item's epilogue ~ 1024 k of MMAs)
+inline int crt_splits(int64_t M, int64_t K, int nm) {
+  const int64_t items = crt_mtiles(M) * nm;
+  const int64_t smin = std::max<int64_t>(1, (K + trals::kCrtKmax - 1) / trals::kCrtKmax);
+  const int64_t smax = std::max<int64_t>(smin, std::min<int64_t>(16, K / 2048));
+  int64_t best_s = smin;
+  double best = 1e300;
+  for (int64_t sp = smin; sp <= smax; ++sp) {
+    const int64_t waves = (items * sp + kSMs - 1) / kSMs;
+    const double cost = static_cast<double>(waves) * (static_cast<double>(K) / sp + 1024.0);
+    if (cost < best * (1 - 1e-9)) { best = cost; best_s = sp; }
+  }
+  return static_cast<int>(best_s);
+}
+
+struct CrtWs {
+  int64_t bplanes, sb, part, res, total;  // offsets in doubles
+  int splits;
+  int64_t kb_split;
+};
+CrtWs crt_ws_layout(int64_t M, int64_t K, int64_t N) {
+  const int nm = crt_host().t.nm;
+  const int n16 = crt_n16(N);
+  CrtWs w{};
+  const int64_t kblocks = crt_kblocks(K);
+  int sp = crt_splits(M, K, nm);
+  w.kb_split = (kblocks + sp - 1) / sp;
+  w.splits = static_cast<int>((kblocks + w.kb_split - 1) / w.kb_split);
+  int slabs;
+  int64_t rps;
+  crt_col_slabs(K, N, slabs, rps);
+  w.bplanes = 0;
+  w.sb = w.bplanes + (static_cast<int64_t>(nm) * crt_plane_bytes(n16, K) + 15) / 16 * 2;
+  w.part = w.sb + (N + 3) / 4 * 2;
+  w.res = w.part + static_cast<int64_t>(slabs) * 2 * N;
+  w.total = w.res + (static_cast<int64_t>(w.splits) * nm * M * n16 + 15) / 16 * 2;
+  return w;
+}
+
+// scale exponents of the K-major rows of x (its rows, or its columns when transposed)
+int crt_scales(const double* x, int64_t rows, int64_t cols, int64_t ld, int transpose, int gamma, int32_t* sexp,
+               double* part, cudaStream_t s) {
+  if (!transpose) {
+    const int blocks = static_cast<int>(std::min<int64_t>((rows + 7) / 8, 64 * kSMs));
+    trals::crt_row_scale_kernel<<<blocks, 256, 0, s>>>(x, rows, cols, ld, gamma, sexp);
+    return launch_status();
+  }
+  int slabs;
+  int64_t rps;
+  crt_col_slabs(rows, cols, slabs, rps);
+  dim3 grid(static_cast<unsigned>((cols + 31) / 32), static_cast<unsigned>(slabs));
+  trals::crt_col_stats_kernel<<<grid, 256, 0, s>>>(x, rows, cols, ld, rps, part);
+  if (int st = launch_status()) return st;
+  trals::crt_col_scale_kernel<<<static_cast<unsigned>((cols + 255) / 256), 256, 0, s>>>(part, slabs, cols, rows, gamma,
+                                                                                          sexp);
+  return launch_status();
+}
+
+template <bool FOLD>
+int crt_slice(const double* x, int64_t rows, int64_t cols, int64_t ld, int transpose, const int32_t* sexp,
+              int8_t* planes, int64_t rows_pad, int tile_w, cudaStream_t s) {
+  const int64_t K = transpose ? rows : cols;
+  const int64_t blocks = crt_kblocks(K) * ((rows_pad + 63) / 64);
+  if (blocks > INT32_MAX) return TRALS_ERR_UNSUPPORTED;
+  trals::crt_slice_kernel<FOLD><<<static_cast<unsigned>(blocks), 256, 0, s>>>(
+      x, rows, cols, ld, transpose, sexp, planes, rows_pad, tile_w, crt_host().t.nm, crt_plane_bytes(rows_pad, K));
+  return launch_status();
+}
+
+int64_t crt_split_ws(int64_t rows, int64_t cols, int transpose) {
+  if (!transpose) return 1;
+  int slabs;
+  int64_t rps;
+  crt_col_slabs(rows, cols, slabs, rps);
+  return static_cast<int64_t>(slabs) * 2 * cols;
+}
+
+// X (row-major [rows][cols]) -> residue planes of its rows (transpose = 0) or columns (1) + scale exponents
+int crt_split(const double* x, int64_t rows, int64_t cols, int transpose, int8_t* planes, int32_t* exps, double* ws,
+              int64_t ws_elems, cudaStream_t s) {
+  const int64_t out_rows = transpose ? cols : rows, K = transpose ? rows : cols;
+  if (!x || !planes || !exps || !ws || rows < 1 || cols < 1 || (transpose != 0 && transpose != 1) ||
+      ws_elems < crt_split_ws(rows, cols, transpose) || (reinterpret_cast<uintptr_t>(planes) & 15u))
+    return TRALS_ERR_ARG;
+  if (!crt_host().ok) return TRALS_ERR_CUDA;
+  if (!crt_shape_ok(out_rows, K, 1)) return TRALS_ERR_UNSUPPORTED;
+  if (int st = crt_scales(x, rows, cols, cols, transpose, crt_host().t.ga, exps, ws, s)) return st;
+  return crt_slice<false>(x, rows, cols, cols, transpose, exps, planes, crt_mtiles(out_rows) * trals::kCrtBM,
+                          trals::kCrtBM, s);
+}
+
+// C(m, n) = sum_k A[m][k] B[k][n]: A given as residue planes + row scale exponents, B fp64 [K][ldb]
+// (sliced per call into the workspace), C fp64 through cm
+int gemm_crt(const int8_t* ad, const int32_t* ea, int64_t M, int64_t K, int64_t N, const double* B, int64_t ldb,
+             double* C, const CMap& cm, double* ws, int64_t ws_elems, cudaStream_t s) {
+  if (!crt_host().ok) return TRALS_ERR_CUDA;
+  if (!crt_shape_ok(M, K, N)) return TRALS_ERR_UNSUPPORTED;
+  if (reinterpret_cast<uintptr_t>(ad) & 15u) return TRALS_ERR_ARG;
+  const CrtWs w = crt_ws_layout(M, K, N);
+  if (!ws || w.total > ws_elems) return TRALS_ERR_ARG;
+  const trals::CrtTables& t = crt_host().t;
+  const int n16 = crt_n16(N);
+  int8_t* bd = reinterpret_cast<int8_t*>(ws + w.bplanes);
+  int32_t* sb = reinterpret_cast<int32_t*>(ws + w.sb);
+  uint8_t* res = reinterpret_cast<uint8_t*>(ws + w.res);
+  if (int st = crt_scales(B, K, N, ldb, 1, t.gb, sb, ws + w.part, s)) return st;
+  if (int st = crt_slice<true>(B, K, N, ldb, 1, sb, bd, n16, n16, s)) return st;
+  trals::CrtArgs g{};
+  g.M = M; g.K = K; g.n16 = n16; g.nm = t.nm;
+  if (n16 <= 256) { g.nc0 = n16; g.nc1 = 0; }
+  else { g.nc0 = (n16 / 2 + 15) / 16 * 16; g.nc1 = n16 - g.nc0; }
+  g.mtiles = static_cast<int>(crt_mtiles(M));
+  g.splits = w.splits;
+  g.kblocks = crt_kblocks(K);
+  g.kb_split = w.kb_split;
+  g.a_plane = crt_plane_bytes(static_cast<int64_t>(g.mtiles) * trals::kCrtBM, K);
+  g.b_plane = crt_plane_bytes(n16, K);
+  g.ad = ad; g.bd = bd; g.out = res;
+  const int stage = trals::kCrtBM * trals::kCrtBK + n16 * trals::kCrtBK;
+  g.stages = std::min(8, (212 * 1024) / stage);
+  if (g.stages < 2) return TRALS_ERR_UNSUPPORTED;
+  const size_t smem = static_cast<size_t>(g.stages) * stage + (2 * g.stages + 2) * 8 + 16 + 1024;
+  static size_t smem_set = 0;
+  if (smem > smem_set) {
+    if (cudaFuncSetAttribute(trals::crt8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem)) != cudaSuccess)
+      return TRALS_ERR_CUDA;
+    smem_set = smem;
+  }
+  const int64_t items = static_cast<int64_t>(g.mtiles) * g.nm * g.splits;
+  const int grid = static_cast<int>(std::min<int64_t>(items, kSMs));
+  trals::crt8_kernel<<<grid, 192, smem, s>>>(g);
+  if (int st = launch_status()) return st;
+  trals::CrtOutArgs o{};
+  o.res = res; o.M = M; o.n16 = n16; o.N = static_cast<int>(N); o.nm = t.nm; o.splits = g.splits;
+  o.sa = ea; o.sb = sb; o.C = C; o.cmap = cm;
+  o.perm = (cm.N2 > 0 && cm.N2 < N && N % cm.N2 == 0 && cm.sn1 < cm.sn2) ? static_cast<int>(N / cm.N2) : 0;
+  const int64_t cblocks = (M + trals::kCrtRB - 1) / trals::kCrtRB;
+  if (cblocks > INT32_MAX) return TRALS_ERR_UNSUPPORTED;
+  trals::crt_combine_kernel<<<static_cast<unsigned>(cblocks), 256, trals::kCrtRB * (n16 + 1) * sizeof(double), s>>>(o);
+  return launch_status();
+}
+
+// env() on the CRT engine: X given as residue planes + scale exponents, K-major for this side
+int env_crt(const int8_t* xd, const int32_t* xe, int64_t pre, int64_t post, int side, const double* H, int r_lo,
+            int r_hi, double* E, int leaf, double* ws, int64_t ws_elems, cudaStream_t s) {
+  const int64_t RR = static_cast<int64_t>(r_lo) * r_hi;
+  const int64_t rows = side == 0 ? pre : post, K = side == 0 ? post : pre;
+  CMap cm{0, rows, 0, r_lo, r_hi, 1, rows * r_lo};
+  if (leaf) cm = CMap{0, rows, 0, RR, r_hi, r_hi, 1};
+  return gemm_crt(xd, xe, rows, K, RR, H, RR, E, cm, ws, ws_elems, s);
 }
 
 // Accuracy guard of the digit-sliced fp64 products (AlsConfig.fp64_gemm = "auto"): per K-major row
@@ -2718,6 +2951,40 @@ int trals_env_oz64(const int8_t* xd, const int32_t* xe, int64_t pre, int64_t pos
                               static_cast<cudaStream_t>(stream));
 }
 
+
+int trals_crt_supported(int64_t rows, int64_t k, int64_t n) {
+  return crt_host().ok && crt_shape_ok(rows, k, n) ? 1 : 0;
+}
+
+int trals_crt_moduli(void) { return crt_host().ok ? crt_host().t.nm : 0; }
+
+int64_t trals_crt_planes_bytes(int64_t rows, int64_t k) {
+  if (rows < 1 || k < 1 || !crt_host().ok) return 0;
+  return static_cast<int64_t>(crt_host().t.nm) * crt_plane_bytes(crt_mtiles(rows) * trals::kCrtBM, k);
+}
+
+int64_t trals_crt_split_ws_elems(int64_t rows, int64_t cols, int transpose) {
+  return rows < 1 || cols < 1 ? 0 : crt_split_ws(rows, cols, transpose);
+}
+
+int trals_crt_split_f64(const double* x, int64_t rows, int64_t cols, int transpose, int8_t* planes, int32_t* exps,
+                        double* ws, int64_t ws_elems, void* stream) {
+  return crt_split(x, rows, cols, transpose, planes, exps, ws, ws_elems, static_cast<cudaStream_t>(stream));
+}
+
+int64_t trals_env_crt_ws_elems(int64_t pre, int64_t post, int side, int r_lo, int r_hi) {
+  const int64_t RR = static_cast<int64_t>(r_lo) * r_hi;
+  const int64_t rows = side == 0 ? pre : post, K = side == 0 ? post : pre;
+  if (!crt_host().ok || !crt_shape_ok(rows, K, RR)) return 0;
+  return crt_ws_layout(rows, K, RR).total;
+}
+
+int trals_env_crt(const int8_t* xd, const int32_t* xe, int64_t pre, int64_t post, int side, const double* H,
+                  int r_lo, int r_hi, double* E, int leaf, double* ws, int64_t ws_elems, void* stream) {
+  if (!xd || !xe || !H || !E || !ws || pre < 1 || post < 1 || r_lo < 1 || r_hi < 1 || (side != 0 && side != 1))
+    return TRALS_ERR_ARG;
+  return env_crt(xd, xe, pre, post, side, H, r_lo, r_hi, E, leaf, ws, ws_elems, static_cast<cudaStream_t>(stream));
+}
 
 int trals_absorb_right_f64(const double* E, int Ra, int64_t pre, int64_t Ib, int Rb, int Rb1, const double* core_zt,
                            double* out, int leaf, double* ws, int64_t ws_elems, void* stream) {

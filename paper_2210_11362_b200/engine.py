@@ -38,6 +38,7 @@ from . import _lib as L
 
 BUCKETS = ("subchain", "mttsp", "solve", "gramqr", "other")  # solvers.py:57
 OZ64_MIN_FLOPS = 4e9  # fp64_gemm="auto": smallest environment product run on the int8 tensor cores
+CRT_MIN_K = 4096      # fp64_gemm="auto": shortest contraction run by the CRT form of the int8 engine
 SMALL_SOLVE_MAX = 112  # m = R_n R_{n+1} <= 112: explicit-inverse solve + one refinement step (trals.h)
 OZ64_MAX_RHO = 2.0 ** 12  # fp64_gemm="auto": largest row dynamic range (max|x| K / sum|x|) of X sliced (trals.h)
 
@@ -100,8 +101,14 @@ class SweepEngine:
         # digit-pair products combined in fp64 -- the DMMA product's accuracy at ~3x its rate).
         # "auto": ozaki once an environment product is large enough to amortise the per-call
         # slicing of the half chain (measured crossover: BASELINE c2, 2.1 GFLOP, is a tie)
-        if fp64_gemm not in ("auto", "dmma", "ozaki"):
-            raise ValueError(f"unknown fp64_gemm {fp64_gemm!r}; expected 'auto', 'dmma' or 'ozaki'")
+        # The int8 engine has two forms, chosen per environment product: the digit-pair one above and,
+        # for long contractions (K >= CRT_MIN_K, R^2 <= 512: BASELINE c5), the CRT one -- 16 modular
+        # int8 GEMMs + an exact 128-bit reconstruction (csrc/crt_int8_gemm.cuh), whose per-output
+        # cost only pays off when K is long.  "crt" forces the CRT form wherever it is supported,
+        # "ozaki" the digit-pair form everywhere.
+        if fp64_gemm not in ("auto", "dmma", "ozaki", "crt"):
+            raise ValueError(f"unknown fp64_gemm {fp64_gemm!r}; expected 'auto', 'dmma', 'ozaki' or 'crt'")
+        self.crt_min_k = {"auto": CRT_MIN_K, "crt": 1}.get(fp64_gemm)
         if fp64_gemm == "auto":
             env_flops = 2.0 * _prod(x_local.shape) * max(int(r) for r in ranks) ** 2
             fp64_gemm = "ozaki" if env_flops >= OZ64_MIN_FLOPS else "dmma"
@@ -112,7 +119,8 @@ class SweepEngine:
                 if 2 * 8 * x_local.numel() * 1.05 > free:
                     fp64_gemm = "dmma"
         self.fp64_gemm = fp64_gemm
-        self.oz64 = (not self.fp32) and fp64_gemm == "ozaki" and _test_lib is None
+        self.oz64 = (not self.fp32) and fp64_gemm in ("ozaki", "crt") and _test_lib is None
+        self.env_kinds = set()  # forms of the int8 engine in use: "oz64" (digit pairs), "crt"
         self.sliced = self.fp32 or self.oz64
         self.lib = _test_lib if _test_lib is not None else L.lib()
         self.dev = x_local.device
@@ -131,7 +139,9 @@ class SweepEngine:
         if tuple(x_local.shape) != tuple(self.dl):
             raise ValueError(f"local slab shape {tuple(x_local.shape)} != expected {tuple(self.dl)}")
         self.x = x_local
-        self._xsplit = {}   # fp32 / oz64: (side, pre, post) -> (digits, exps): X sliced, K-major for that side
+        # fp32 / oz64: (kind, side, pre, post) -> (planes, exps): X sliced, K-major for that side
+        # (kind "oz32" / "oz64": digit planes, "crt": residue planes)
+        self._xsplit = {}
         self._x64 = None    # fp32 + exact errors: fp64 copy of X for the residual kernel
         self.fallback_ok = bool(rank_deficient_fallback)
         # AlsConfig.debug_checks (solvers.py:376-377, 432-438, 485-487): assert the coefficient
@@ -328,12 +338,11 @@ class SweepEngine:
             target = lambda E0=E0: E0.data_ptr()
 
         if self.sliced:
-            key = (side, pre, post)
-            nbytes = self.lib.trals_oz_digits_bytes if self.fp32 else self.lib.trals_oz64_digits_bytes
-            wsf = self.lib.trals_env_oz_ws_elems if self.fp32 else self.lib.trals_env_oz64_ws_elems
-            envf = self.lib.trals_env_oz if self.fp32 else self.lib.trals_env_oz64
+            rows, k = (pre, post) if side == 0 else (post, pre)
+            kind = "oz32" if self.fp32 else self._env_kind(rows, k, r_lo * r_hi)
+            key = (kind, side, pre, post)
+            nbytes, _, wsf, envf = self._sliced_api(kind)
             if key not in self._xsplit:
-                rows, k = (pre, post) if side == 0 else (post, pre)
                 self._xsplit[key] = (torch.empty(int(nbytes(rows, k)), dtype=torch.int8, device=self.dev),
                                      torch.empty(rows, dtype=torch.int32, device=self.dev))
             self._ws(wsf(pre, post, side, r_lo, r_hi))
@@ -662,6 +671,29 @@ class SweepEngine:
                                                      sp), "relayout")
         self._gram(j, sp)
 
+    def _env_kind(self, rows, k, rr):
+        """Form of the int8 engine for one fp64 environment product (rows x k) . (k x rr)."""
+        kind = "oz64"
+        if (self.crt_min_k is not None and k >= self.crt_min_k and self.lib.trals_crt_supported(rows, k, rr)):
+            # 16 residue bytes per element of this phase's copy of X must fit beside everything else
+            free, _ = torch.cuda.mem_get_info(self.dev)
+            if self.lib.trals_crt_planes_bytes(rows, k) * 1.05 < free:
+                kind = "crt"
+        self.env_kinds.add(kind)
+        return kind
+
+    def _sliced_api(self, kind):
+        """(plane bytes, (split, split workspace), env workspace, env) of one sliced form."""
+        lib = self.lib
+        if kind == "oz32":
+            return (lib.trals_oz_digits_bytes, (lib.trals_oz_split_f32, lib.trals_oz_split_ws_elems),
+                    lib.trals_env_oz_ws_elems, lib.trals_env_oz)
+        if kind == "crt":
+            return (lib.trals_crt_planes_bytes, (lib.trals_crt_split_f64, lib.trals_crt_split_ws_elems),
+                    lib.trals_env_crt_ws_elems, lib.trals_env_crt)
+        return (lib.trals_oz64_digits_bytes, (lib.trals_oz64_split_f64, lib.trals_oz_split_ws_elems),
+                lib.trals_env_oz64_ws_elems, lib.trals_env_oz64)
+
     def prepare_x(self):
         """Derive the per-X state after X (self.x) was (re)loaded: for the sliced
         environment products (fp32 variant, fp64 "ozaki"), X's int8 digit planes
@@ -670,9 +702,9 @@ class SweepEngine:
         if not self.sliced:
             return
         sp = self._sp()
-        split = self.lib.trals_oz_split_f32 if self.fp32 else self.lib.trals_oz64_split_f64
-        for (side, pre, post), (xd, xe) in self._xsplit.items():
-            need = self.lib.trals_oz_split_ws_elems(pre, post, side)
+        for (kind, side, pre, post), (xd, xe) in self._xsplit.items():
+            _, (split, split_ws), _, _ = self._sliced_api(kind)
+            need = split_ws(pre, post, side)
             ws = torch.empty(max(1, need), dtype=torch.float64, device=self.dev)
             L.check(split(self.x.data_ptr(), pre, post, side, xd.data_ptr(), xe.data_ptr(), ws.data_ptr(),
                           ws.numel(), sp), "oz_split")
@@ -686,7 +718,7 @@ class SweepEngine:
             return 0.0
         out = self._empty(len(self._xsplit))
         sp = self._sp()
-        for i, (side, pre, post) in enumerate(self._xsplit):
+        for i, (_, side, pre, post) in enumerate(self._xsplit):
             ws = self._empty(max(1, self.lib.trals_oz_range_ws_elems(pre, post, side)))
             L.check(self.lib.trals_oz_range_f64(self.x.data_ptr(), pre, post, side, out[i:].data_ptr(), ws.data_ptr(),
                                                 ws.numel(), sp), "oz_range")

@@ -29,7 +29,7 @@ ERROR_MODES = ("exact", "cheap", "none")         # solvers.py:56
 BUCKETS = ("subchain", "mttsp", "solve", "gramqr", "other")  # solvers.py:57
 SVD_RCOND_DEFAULT = 1e-12                        # linalg.py:20
 DTYPES = ("float64", "float32")                  # AlsConfig.dtype (extension)
-FP64_GEMMS = ("auto", "ozaki", "dmma")            # AlsConfig.fp64_gemm (extension)
+FP64_GEMMS = ("auto", "ozaki", "crt", "dmma")            # AlsConfig.fp64_gemm (extension)
 
 
 @dataclass
