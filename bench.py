@@ -395,14 +395,19 @@ def run_ours(args):
     final_err = float(eng.err_cur[0].item()) if use_graph else float(errs[args.warmup + args.steps - 1, 0].item())
 
     # dominant kernel: the X-streaming environment GEMM (one per phase)
-    oz64 = (not fp32) and eng_gemm == "ozaki"
+    oz64 = (not fp32) and eng_gemm in ("ozaki", "crt")
+    # form of the int8 engine behind the environment products: CRT (one int8 GEMM per modulus) for
+    # long contractions, else the 28 digit-pair products
+    crt = oz64 and eng.env_kinds == {"crt"}
+    i8_products = L.lib().trals_crt_moduli() if crt else OZ64_PAIRS
+    i8_forms = sorted(eng.env_kinds) if oz64 else None
     env_flops = eng.env_flops()
     per_launch = [env_flops[i % len(env_flops)] / (env_ms[i] * 1e-3) / 1e12 for i in range(len(env_ms))]
     env_avg_ms = float(np.mean(env_ms))
     env_tf = float(np.mean(per_launch))
     env_share = env_avg_ms * len(env_flops) / ms
     traffic = None
-    tag = "_fp32" if fp32 else ("_oz64" if oz64 else "")
+    tag = "_fp32" if fp32 else ("_crt" if crt else "_oz64" if oz64 else "")
     tpath = os.path.join(ROOT, "profiles", f"{args.config}{tag}_env_traffic.json")
     if os.path.exists(tpath) and world == 1:
         try:
@@ -416,7 +421,7 @@ def run_ours(args):
     ebytes = 4 if fp32 else 8
     # P = the peak of the pipe actually used (fp64 on int8: the int8 rate / 28 pairs)
     peak_tf = (INT8_FP32_EQ_TFLOPS if fp32 else
-               INT8_PEAK_TOPS / OZ64_PAIRS if oz64 else FP64_PEAK_TFLOPS)
+               INT8_PEAK_TOPS / i8_products if oz64 else FP64_PEAK_TFLOPS)
     t_roof = roofline_sweep_time(dims, ranks, peak_tf, bw, world, ebytes)
     t_roof_dmma = roofline_sweep_time(dims, ranks, FP64_PEAK_TFLOPS, bw, world, ebytes)
     sweep_s = ms_max * 1e-3
@@ -497,14 +502,22 @@ def run_ours(args):
                 "flops_per_launch": env_flops, "tflops_fp32_equiv": env_tf,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth)"}
     elif oz64:
-        # fp64 on the int8 tensor cores: the algorithmic work of one launch is the 28 digit-pair
-        # products over the real (unpadded) M x N x K
-        i8_tops = env_tf * OZ64_PAIRS
+        # fp64 on the int8 tensor cores: the algorithmic work of one launch is the int8 products
+        # (28 digit pairs, or one per CRT modulus) over the real (unpadded) M x N x K
+        i8_tops = env_tf * i8_products
+        if crt:
+            kern = ("crt8_kernel<pair> (fp64 X x half-chain environment product on the int8 tcgen05 tensor cores "
+                    f"by the Chinese remainder theorem: {i8_products} u8 x u8 GEMMs modulo pairwise coprime p_i <= 256, "
+                    "cta_group::2 MMAs 256 x {208,192} x 32, exact int32 sums reduced mod p_i in the epilogue; "
+                    "the timed env step also holds the half chain's residue slicing and the exact 128-bit "
+                    "CRT reconstruction kernel)")
+        else:
+            kern = ("oz8_kernel<64, OzF64> (fp64 X x half-chain environment product on the int8 tcgen05 "
+                    "tensor cores: 7 balanced radix-254 digits per operand, 28 exact int32 digit-pair products)")
         roof = {"bound": "tensor", "achieved": i8_tops, "peak": INT8_PEAK_TOPS, "unit": "TFLOP/s",
                 "frac": i8_tops / INT8_PEAK_TOPS, "traffic": traffic,
-                "kernel": "oz8_kernel<64, OzF64> (fp64 X x half-chain environment product on the int8 tcgen05 "
-                          "tensor cores: 7 balanced radix-254 digits per operand, 28 exact int32 digit-pair products)",
-                "ops": "int8 tensor ops = 28 x 2 M N K per launch", "flops_per_launch": env_flops,
+                "kernel": kern,
+                "ops": f"int8 tensor ops = {i8_products} x 2 M N K per launch", "flops_per_launch": env_flops,
                 "fp64_equiv_tflops": env_tf, "fp64_equiv_frac_of_dmma_peak": env_tf / FP64_PEAK_TFLOPS,
                 "avg_launch_ms": env_avg_ms, "share_of_step": env_share,
                 "frac_of_burst_peak": i8_tops / INT8_PEAK_BURST_TOPS,
@@ -529,6 +542,7 @@ def run_ours(args):
                    "l2": "X (%.2f GB) larger than the 126 MB L2, no flush needed" % (np.prod(dims) * ebytes / 1e9),
                    "step": "one full sweep + per-sweep relative error (cheap identity)",
                    "fp64_gemm": None if fp32 else eng_gemm,
+                   "int8_engine_forms": i8_forms,
                    "x_digits_ms": prep_ms if (fp32 or oz64) else None,
                    "x_row_range_rho": rho if not fp32 else None,
                    "launch": launch_note},
@@ -566,7 +580,7 @@ def main():
     ap.add_argument("--variant", choices=["ne", "qr", "qrne"], default="ne")
     ap.add_argument("--dtype", choices=["float64", "float32"], default="float64",
                     help="float32 = the fp32 variant (BASELINE config 4): int8 tensor-core environment products")
-    ap.add_argument("--fp64-gemm", choices=["auto", "ozaki", "dmma"], default="auto",
+    ap.add_argument("--fp64-gemm", choices=["auto", "ozaki", "crt", "dmma"], default="auto",
                     help="fp64 environment products: int8 tensor-core digit slicing, the DMMA pipe, or "
                          "auto (ozaki for products >= 4 GFLOP: c3-c5)")
     ap.add_argument("--no-e2e", action="store_true")

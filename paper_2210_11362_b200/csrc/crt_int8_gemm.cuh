@@ -11,14 +11,14 @@
 //    integer product C' = a'.b' then lies in (-P/2, P/2)).  With 16 moduli P = 2^125.38,
 //    ga = gb = 62: a Gaussian row of 25600 entries keeps 2^-55 of its rms (entries above
 //    2^53 of the scaled row are not rounded at all).
-// 2. Residues.  For each modulus p_i (pairwise coprime, <= 256) the symmetric residues
-//    a' mod p_i, (b' q_i) mod p_i fit int8 (q_i = (P/p_i)^-1 mod p_i folded into B).
-//    X's residues are made once per X (16 planes in the MMA's shared-memory image), the
-//    half chain's per call.
-// 3. One int8 GEMM per modulus (exact int32 accumulation, K <= 65472 per split), whose
-//    epilogue reduces the sums mod p_i to one byte per output: t_i = (C' q_i) mod p_i.
-// 4. CRT.  C' = sum_i t_i (P/p_i) - P rint(sum_i t_i / p_i), evaluated exactly in 128-bit
-//    integer arithmetic, rounded once to fp64 and scaled by 2^-(sa+sb).
+// 2. Residues.  For each modulus p_i (pairwise coprime, <= 256) the residues a' mod p_i,
+//    b' mod p_i in [0, p_i) are unsigned bytes.  X's residues are made once per X (16 planes
+//    in the MMA's shared-memory image), the half chain's per call.
+// 3. One u8 x u8 GEMM per modulus (exact int32 accumulation, 255^2 K < 2^31: K <= 33024 per
+//    split), whose epilogue reduces the sums mod p_i to one byte per output: t_i = C' mod p_i.
+// 4. CRT.  C' = sum_i t_i W_i - P rint(sum_i t_i q_i / p_i) with W_i = (P/p_i) q_i mod P,
+//    q_i = (P/p_i)^-1 mod p_i, evaluated exactly in 128-bit integer arithmetic (modulo 2^128:
+//    the result is below 2^125), rounded once to fp64 and scaled by 2^-(sa+sb).
 // So the result is the correctly rounded exact product of the rounded operands: the only
 // error is the rint() of step 1.
 //
@@ -36,7 +36,7 @@ namespace trals {
 constexpr int kCrtMaxMod = 16;
 constexpr int kCrtBK = 64;            // int8 k per stage row (SWIZZLE_64B)
 constexpr int kCrtBM = 128;
-constexpr int64_t kCrtKmax = 65472;   // 128^2 K < 2^30 - 256 (31-bit unsigned epilogue operand), multiple of 64
+constexpr int64_t kCrtKmax = 33024;   // 255^2 K < 2^31 (int32 sums of u8 x u8 products), multiple of 64
 constexpr int kCrtMaxN = 512;         // TMEM columns
 
 // the 16 largest pairwise coprime integers <= 256 (255 = 3 5 17, 253 = 11 23, 247 = 13 19, 217 = 7 31, primes)
@@ -47,11 +47,9 @@ constexpr int kCrtMaxN = 512;         // TMEM columns
 struct CrtTables {
   uint32_t p[kCrtMaxMod];
   uint32_t magic[kCrtMaxMod];  // ceil(2^39 / p): floor(n / p) = umulhi(magic, n) >> 7 for n < 2^31
-  uint32_t offs[kCrtMaxMod];   // p floor(2^30 / p): makes the int32 sums non-negative
-  uint32_t qinv[kCrtMaxMod];   // (P / p)^-1 mod p
-  float invp[kCrtMaxMod];
-  uint64_t w0[kCrtMaxMod], w1[kCrtMaxMod];  // P / p_i = w1 2^64 + w0
-  uint64_t P0, P1;                          // P = P1 2^64 + P0
+  uint32_t fq[kCrtMaxMod];     // rint(2^19 q_i / p_i), q_i = (P / p_i)^-1 mod p_i
+  uint32_t w[kCrtMaxMod][4];   // W_i = (P / p_i) q_i mod P, 32-bit limbs (little endian)
+  uint32_t P[4];               // P, 32-bit limbs
   int nm, ga, gb;
 };
 __constant__ CrtTables crt_tab;
@@ -107,12 +105,22 @@ __global__ void __launch_bounds__(256) crt_col_stats_kernel(const double* __rest
   const int64_t r0 = blockIdx.y * rows_per_slab;
   const int64_t r1 = (r0 + rows_per_slab < rows) ? r0 + rows_per_slab : rows;
   double m = 0.0, ss = 0.0;
-  if (c < cols)
-    for (int64_t r = r0 + warp; r < r1; r += 8) {
+  if (c < cols) {
+    int64_t r = r0 + warp;
+    for (; r + 24 < r1; r += 32) {  // four loads in flight
+      const double v0 = x[r * ld + c], v1 = x[(r + 8) * ld + c], v2 = x[(r + 16) * ld + c], v3 = x[(r + 24) * ld + c];
+      m = fmax(fmax(m, fabs(v0)), fmax(fabs(v1), fmax(fabs(v2), fabs(v3))));
+      ss = fma(v0, v0, ss);
+      ss = fma(v1, v1, ss);
+      ss = fma(v2, v2, ss);
+      ss = fma(v3, v3, ss);
+    }
+    for (; r < r1; r += 8) {
       const double v = x[r * ld + c];
       m = fmax(m, fabs(v));
       ss = fma(v, v, ss);
     }
+  }
   sm[warp][lane] = m;
   sq[warp][lane] = ss;
   __syncthreads();
@@ -126,38 +134,41 @@ __global__ void __launch_bounds__(256) crt_col_stats_kernel(const double* __rest
   }
 }
 
+// one warp per column: lanes over the slabs, fixed-order tree
 __global__ void __launch_bounds__(256) crt_col_scale_kernel(const double* __restrict__ part, int slabs, int64_t cols,
                                                             int64_t K, int gamma, int32_t* __restrict__ sexp) {
-  const int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int64_t c = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
   if (c >= cols) return;
   double m = 0.0, ss = 0.0;
-  for (int s = 0; s < slabs; ++s) {
+  for (int s = lane; s < slabs; s += 32) {
     m = fmax(m, part[(static_cast<int64_t>(s) * 2 + 0) * cols + c]);
     ss += part[(static_cast<int64_t>(s) * 2 + 1) * cols + c];
   }
-  sexp[c] = crt_scale_exp(m, ss, K, gamma);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  }
+  if (lane == 0) sexp[c] = crt_scale_exp(m, ss, K, gamma);
 }
 
 // ---------------------------------------------------------------------------
 // residues
 // ---------------------------------------------------------------------------
-// symmetric int8 residues of the integer a (|a| <= 2^62, already rounded) modulo the 16 moduli;
-// FOLD: of a q_i.  |a| is split into three 21-bit limbs, so each residue is a 32-bit
-// remainder by a compile-time constant.
-template <bool FOLD>
-__device__ __forceinline__ void crt_residues(double a, int8_t (&r)[kCrtMaxMod]) {
-  const long long v = __double2ll_rn(a);
-  const bool neg = v < 0;
-  const unsigned long long u = neg ? static_cast<unsigned long long>(-v) : static_cast<unsigned long long>(v);
+// residues in [0, p_i) of the integer v (|v| <= 2^62) modulo the 16 moduli, packed one byte each
+// into 4 words per ... (see crt_slice_kernel).  v is taken in two's complement: three 21-bit limbs
+// plus the sign bit of weight -2^63, so each residue is one 32-bit remainder by a compile-time
+// constant (x0 + x1 c1 + x2 c2 + x3 c3 < 2^31).
+__device__ __forceinline__ void crt_residues(long long v, uint32_t (&r)[kCrtMaxMod]) {
+  const unsigned long long u = static_cast<unsigned long long>(v);
   const uint32_t x0 = static_cast<uint32_t>(u) & 0x1FFFFFu, x1 = static_cast<uint32_t>(u >> 21) & 0x1FFFFFu,
-                 x2 = static_cast<uint32_t>(u >> 42);
-#define TRALS_CRT_RES(i, pp)                                                                  \
-  {                                                                                           \
-    constexpr uint32_t c1 = (1u << 21) % pp, c2 = static_cast<uint32_t>((1ull << 42) % pp);   \
-    uint32_t t = (x2 * c2 + x1 * c1 + x0) % pp;                                               \
-    if (FOLD) t = (t * crt_tab.qinv[i]) % pp;                                                 \
-    int s = t > (pp - 1) / 2 ? static_cast<int>(t) - pp : static_cast<int>(t);                \
-    r[i] = static_cast<int8_t>(neg ? -s : s);                                                 \
+                 x2 = static_cast<uint32_t>(u >> 42) & 0x1FFFFFu, x3 = static_cast<uint32_t>(u >> 63);
+#define TRALS_CRT_RES(i, pp)                                                                       \
+  {                                                                                                \
+    constexpr uint32_t c1 = (1u << 21) % pp, c2 = static_cast<uint32_t>((1ull << 42) % pp),        \
+                       c3 = (pp - static_cast<uint32_t>((1ull << 63) % pp)) % pp;                  \
+    r[i] = (x2 * c2 + x1 * c1 + x3 * c3 + x0) % pp;                                                \
   }
   TRALS_CRT_MODULI(TRALS_CRT_RES)
 #undef TRALS_CRT_RES
@@ -167,11 +178,11 @@ __device__ __forceinline__ void crt_residues(double a, int8_t (&r)[kCrtMaxMod]) 
 // transposed), plane i = modulus i, each plane tiled [row tile of tile_w][64-k block][tile_w x 64 B]
 // in the UMMA K-major SWIZZLE_64B pattern, zero padded to rows_pad x ceil(K / 64) 64.
 // A CTA owns a 64-row x 64-k block (read coalesced along the contiguous axis into shared
-// memory); each group of 4 threads writes one row's 64 residue bytes per plane.
-template <bool FOLD>
+// memory); a thread turns 4 consecutive k of one row into one 4-byte word per plane (16 threads
+// write a row's 64 bytes of a plane), four row groups per thread.
 __global__ void __launch_bounds__(256) crt_slice_kernel(const double* __restrict__ x, int64_t rows, int64_t cols,
                                                         int64_t ld, int transpose,
-                                                        const int32_t* __restrict__ sexp, int8_t* __restrict__ out,
+                                                        const int32_t* __restrict__ sexp, uint8_t* __restrict__ out,
                                                         int64_t rows_pad, int tile_w, int nm, int64_t plane_bytes) {
   __shared__ double tile[64][65];
   const int64_t out_rows = transpose ? cols : rows, K = transpose ? rows : cols;
@@ -194,30 +205,30 @@ __global__ void __launch_bounds__(256) crt_slice_kernel(const double* __restrict
     tile[kk][rr] = v;
   }
   __syncthreads();
-  const int rl = tid >> 2, ch = tid & 3;
-  const int64_t orow = r0 + rl;
-  if (orow >= rows_pad) return;
-  const int s = orow < out_rows ? sexp[orow] : 0;
-  uint32_t w[kCrtMaxMod][4];
+  const int kg = tid & 15;  // 4-k group of the 64-k block
+#pragma unroll 1
+  for (int rl = tid >> 4; rl < 64; rl += 16) {
+    const int64_t orow = r0 + rl;
+    if (orow >= rows_pad) break;
+    const int s = orow < out_rows ? sexp[orow] : 0;
+    uint32_t w[kCrtMaxMod];
 #pragma unroll
-  for (int i = 0; i < kCrtMaxMod; ++i)
+    for (int i = 0; i < kCrtMaxMod; ++i) w[i] = 0;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) w[i][q] = 0;
+    for (int j = 0; j < 4; ++j) {
+      uint32_t rs[kCrtMaxMod];
+      crt_residues(__double2ll_rn(scalbn(tile[kg * 4 + j][rl], s)), rs);
 #pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    int8_t rs[kCrtMaxMod];
-    crt_residues<FOLD>(scalbn(tile[ch * 16 + j][rl], s), rs);
+      for (int i = 0; i < kCrtMaxMod; ++i) w[i] |= rs[i] << (8 * j);
+    }
+    const int64_t t = orow / tile_w;
+    const int rr = static_cast<int>(orow - t * tile_w);
+    const int64_t off = (t * kblocks + kb) * (static_cast<int64_t>(tile_w) * kCrtBK) + rr * kCrtBK +
+                        ((((kg >> 2) ^ ((rr >> 1) & 3)) << 4) | ((kg & 3) << 2));
 #pragma unroll
     for (int i = 0; i < kCrtMaxMod; ++i)
-      w[i][j >> 2] |= static_cast<uint32_t>(static_cast<uint8_t>(rs[i])) << (8 * (j & 3));
+      if (i < nm) *reinterpret_cast<uint32_t*>(out + i * plane_bytes + off) = w[i];
   }
-  const int64_t t = orow / tile_w;
-  const int rr = static_cast<int>(orow - t * tile_w);
-  const int64_t off = (t * kblocks + kb) * (static_cast<int64_t>(tile_w) * kCrtBK) + rr * kCrtBK +
-                      ((ch ^ ((rr >> 1) & 3)) << 4);
-#pragma unroll
-  for (int i = 0; i < kCrtMaxMod; ++i)
-    if (i < nm) *reinterpret_cast<uint4*>(out + i * plane_bytes + off) = make_uint4(w[i][0], w[i][1], w[i][2], w[i][3]);
 }
 
 // ---------------------------------------------------------------------------
@@ -229,33 +240,88 @@ struct CrtArgs {
   int mtiles, splits, stages;
   int64_t kblocks, kb_split;  // 64-k blocks in total / per K split
   int64_t a_plane, b_plane;   // bytes per residue plane
-  const int8_t* ad;           // [nm][mtiles][kblocks][128 x 64 B]
-  const int8_t* bd;           // [nm][kblocks][n16 x 64 B]
-  uint8_t* out;               // [splits][nm][M][n16]: (C' q_i) mod p_i
+  const uint8_t* ad;          // [nm][mtiles (even)][kblocks][128 x 64 B]
+  const uint8_t* bd;          // [nm][kblocks][n16 x 64 B]
+  uint8_t* out;               // [splits][nm][M][n16]: C' mod p_i
 };
 
-// instruction descriptor: D s32, A/B signed int8, K-major, M = 128
-__device__ __forceinline__ uint32_t crt_idesc(int n) { return i8_idesc(n); }
+// instruction descriptor: D s32, A/B unsigned int8 (type fields 0), K-major, N = n, M = 128 (one CTA)
+// or 256 (CTA pair)
+__device__ __forceinline__ uint32_t crt_idesc(int n, int m) {
+  uint32_t d = 0;
+  d |= 2u << 4;
+  d |= static_cast<uint32_t>(n >> 3) << 17;
+  d |= static_cast<uint32_t>(m >> 4) << 24;
+  return d;
+}
 
-template <class F>
+__device__ __forceinline__ void umma_i8_pair_warp(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
+                                                  uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+
+// commit of the pair's MMAs: arrives on the mbarrier at this offset in both CTAs
+__device__ __forceinline__ void crt_commit_pair_warp(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}\n" ::"r"(
+          smem_u32(bar)),
+      "h"(static_cast<uint16_t>(3))
+      : "memory");
+}
+
+// arrive on the mbarrier at the same offset in CTA `rank` of the cluster (plain arrive / plain
+// try_wait on the other side, as for a barrier signalled by a peer's bulk copy: cluster-scope
+// release / acquire qualifiers cost a memory barrier per stage -- 2200 instead of ~400 cycles)
+__device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, uint32_t rank) {
+  asm volatile(
+      "{\n\t.reg .b32 ra;\n\t"
+      "mapa.shared::cluster.u32 ra, %0, %1;\n\t"
+      "mbarrier.arrive.shared::cluster.b64 _, [ra];\n\t}\n" ::"r"(smem_u32(bar)),
+      "r"(rank)
+      : "memory");
+}
+
+// Work items.  One CTA: (split, modulus, m-tile), CTA b takes items b, b + grid, ...  CTA pair: the
+// pair takes (split, modulus, pair of m-tiles) and CTA rank r the m-tile 2 j + r of it.
+template <bool PAIR, class F>
 __device__ __forceinline__ void crt_for_items(const CrtArgs& g, F&& body) {
-  const int per_split = g.nm * g.mtiles, total = per_split * g.splits;
-  for (int u = blockIdx.x; u < total; u += gridDim.x) {
+  const int mu = PAIR ? (g.mtiles + 1) / 2 : g.mtiles;
+  const int per_split = g.nm * mu, total = per_split * g.splits;
+  const int first = PAIR ? blockIdx.x / 2 : blockIdx.x, step = PAIR ? gridDim.x / 2 : gridDim.x;
+  for (int u = first; u < total; u += step) {
     const int rem = u % per_split;
-    body(u / per_split, rem / g.mtiles, rem % g.mtiles);
+    body(u / per_split, rem / mu, rem % mu);
   }
 }
 
+// PAIR: clusters of two CTAs (one TPC) run tcgen05.mma.cta_group::2 -- M = 256, each CTA holding its
+// own 128 rows of A and half of the B rows of every MMA -- so a CTA fills (128 + N / 2) x 64 bytes
+// of shared memory per 64 k instead of (128 + N) x 64: at N = 400 the one-CTA form needs ~84 B/clk
+// per SM to feed the tensor pipe, more than L2 delivers.  The leader (rank 0) issues the MMAs; its
+// MMA warp waits for its own stage and for the peer's (relayed by the peer's MMA warp, which has
+// nothing else to do); commits are multicast to both CTAs' barriers.
+template <bool PAIR>
 __global__ void __launch_bounds__(192, 1) crt8_kernel(const __grid_constant__ CrtArgs g) {
   extern __shared__ uint8_t smraw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
   const int S = g.stages;
-  const uint32_t bstage = static_cast<uint32_t>(g.n16) * kCrtBK;
+  const uint32_t crank = PAIR ? cluster_ctarank() : 0u;
+  const uint32_t b0bytes = static_cast<uint32_t>(g.nc0) * kCrtBK / (PAIR ? 2 : 1);
+  const uint32_t b1bytes = static_cast<uint32_t>(g.nc1) * kCrtBK / (PAIR ? 2 : 1);
+  const uint32_t bstage_g = static_cast<uint32_t>(g.n16) * kCrtBK;  // one 64-k block of a B plane in HBM
   const uint32_t astage = kCrtBM * kCrtBK;
-  const uint32_t stage = astage + bstage;
+  const uint32_t stage = astage + b0bytes + b1bytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + static_cast<size_t>(S) * stage);
   uint64_t* empty = full + S;
-  uint64_t* acc_full = empty + S;
+  uint64_t* peer_full = empty + S;       // (leader) the peer's stage has landed
+  uint64_t* acc_full = peer_full + S;
   uint64_t* acc_empty = acc_full + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
 
@@ -265,17 +331,24 @@ __global__ void __launch_bounds__(192, 1) crt8_kernel(const __grid_constant__ Cr
     for (int s = 0; s < S; ++s) {
       mbar_init(full + s, 1);
       mbar_init(empty + s, 1);
+      mbar_init(peer_full + s, 1);
     }
     mbar_init(acc_full, 1);
-    mbar_init(acc_empty, 4);
+    mbar_init(acc_empty, PAIR ? 8 : 4);  // one arrive per epilogue warp (of both CTAs)
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(smem_u32(tmem_slot)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    if constexpr (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(smem_u32(tmem_slot)));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(smem_u32(tmem_slot)));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
+  if constexpr (PAIR) cluster_sync_all();  // both CTAs' barriers initialised before any remote arrive
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const uint32_t tmem = *tmem_slot;
 
@@ -289,50 +362,81 @@ __global__ void __launch_bounds__(192, 1) crt8_kernel(const __grid_constant__ Cr
     // ------------------------------ bulk-copy producer ------------------------------
     if (lane == 0) {
       uint32_t gk = 0;
-      crt_for_items(g, [&](int split, int mod, int mt) {
+      crt_for_items<PAIR>(g, [&](int split, int mod, int mu) {
         int64_t kb0;
         int nkb;
         item_k(split, kb0, nkb);
-        const int8_t* asrc = g.ad + mod * g.a_plane + (static_cast<int64_t>(mt) * g.kblocks + kb0) * astage;
-        const int8_t* bsrc = g.bd + mod * g.b_plane + kb0 * bstage;
+        const int mt = PAIR ? 2 * mu + static_cast<int>(crank) : mu;
+        const uint8_t* asrc = g.ad + mod * g.a_plane + (static_cast<int64_t>(mt) * g.kblocks + kb0) * astage;
+        const uint8_t* bsrc = g.bd + mod * g.b_plane + kb0 * bstage_g;
+        const uint8_t* b0src = bsrc + crank * b0bytes;
+        const uint8_t* b1src = bsrc + static_cast<uint32_t>(g.nc0) * kCrtBK + crank * b1bytes;
         for (int kt = 0; kt < nkb; ++kt, ++gk) {
           const uint32_t s = gk % S;
           if (gk >= static_cast<uint32_t>(S)) mbar_wait(empty + s, ((gk / S) - 1) & 1);
           uint8_t* st = sm + static_cast<size_t>(s) * stage;
           mbar_expect_tx(full + s, stage);
           bulk_load(st, asrc + static_cast<int64_t>(kt) * astage, astage, full + s);
-          bulk_load(st + astage, bsrc + static_cast<int64_t>(kt) * bstage, bstage, full + s);
+          bulk_load(st + astage, b0src + static_cast<int64_t>(kt) * bstage_g, b0bytes, full + s);
+          if (b1bytes) bulk_load(st + astage + b0bytes, b1src + static_cast<int64_t>(kt) * bstage_g, b1bytes, full + s);
+        }
+      });
+    }
+  } else if (warp == 1 && crank != 0) {
+    // ------------------------------ peer relay: this CTA's stage has landed -> leader ------------------------------
+    if (lane == 0) {
+      uint32_t gk = 0;
+      crt_for_items<PAIR>(g, [&](int split, int, int) {
+        int64_t kb0;
+        int nkb;
+        item_k(split, kb0, nkb);
+        for (int kt = 0; kt < nkb; ++kt, ++gk) {
+          const uint32_t s = gk % S;
+          mbar_wait(full + s, (gk / S) & 1);
+          mbar_arrive_remote(peer_full + s, 0);
         }
       });
     }
   } else if (warp == 1) {
     // ------------------------------ MMA issuer (whole warp, one elected lane) ------------------------------
     const uint64_t dA0 = oz_desc<kCrtBK>(smem_u32(sm)), dB0 = oz_desc<kCrtBK>(smem_u32(sm) + astage);
-    const uint32_t id0 = crt_idesc(g.nc0), id1 = crt_idesc(g.nc1 > 0 ? g.nc1 : 16);
-    const uint32_t b1off = (static_cast<uint32_t>(g.nc0) * kCrtBK) >> 4;
+    const uint32_t id0 = crt_idesc(g.nc0, PAIR ? 256 : 128), id1 = crt_idesc(g.nc1 > 0 ? g.nc1 : 16, PAIR ? 256 : 128);
+    const uint32_t b1off = b0bytes >> 4;
     uint32_t gk = 0, it = 0;
-    crt_for_items(g, [&](int split, int, int) {
+    crt_for_items<PAIR>(g, [&](int split, int, int) {
       int64_t kb0;
       int nkb;
       item_k(split, kb0, nkb);
-      mbar_wait(acc_empty, it & 1);  // drained by the epilogue
+      mbar_wait(acc_empty, it & 1);  // drained by the epilogue (of both CTAs)
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
       for (int kt = 0; kt < nkb; ++kt, ++gk) {
         const uint32_t s = gk % S;
         mbar_wait(full + s, (gk / S) & 1);
+        if constexpr (PAIR) mbar_wait(peer_full + s, (gk / S) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         const uint64_t da = dA0 + ((s * stage) >> 4), db = dB0 + ((s * stage) >> 4);
 #pragma unroll
         for (int k = 0; k < kCrtBK / 32; ++k) {
           const uint32_t acc = (kt > 0 || k > 0) ? 1u : 0u;
-          umma_i8_warp(tmem, da + ((k * 32) >> 4), db + ((k * 32) >> 4), id0, acc);
-          if (g.nc1 > 0) umma_i8_warp(tmem + g.nc0, da + ((k * 32) >> 4), db + b1off + ((k * 32) >> 4), id1, acc);
+          if constexpr (PAIR) {
+            umma_i8_pair_warp(tmem, da + ((k * 32) >> 4), db + ((k * 32) >> 4), id0, acc);
+            if (g.nc1 > 0) umma_i8_pair_warp(tmem + g.nc0, da + ((k * 32) >> 4), db + b1off + ((k * 32) >> 4), id1, acc);
+          } else {
+            umma_i8_warp(tmem, da + ((k * 32) >> 4), db + ((k * 32) >> 4), id0, acc);
+            if (g.nc1 > 0) umma_i8_warp(tmem + g.nc0, da + ((k * 32) >> 4), db + b1off + ((k * 32) >> 4), id1, acc);
+          }
         }
-        oz_commit_warp(empty + s);
+        if constexpr (PAIR) crt_commit_pair_warp(empty + s);
+        else oz_commit_warp(empty + s);
         __syncwarp();
       }
-      if (nkb > 0) oz_commit_warp(acc_full);
-      else if (lane == 0) mbar_arrive(acc_full);
+      if (nkb > 0) {
+        if constexpr (PAIR) crt_commit_pair_warp(acc_full);
+        else oz_commit_warp(acc_full);
+      } else if (lane == 0) {
+        mbar_arrive(acc_full);
+        if constexpr (PAIR) mbar_arrive_remote(acc_full, 1);
+      }
       __syncwarp();
       ++it;
     });
@@ -340,13 +444,20 @@ __global__ void __launch_bounds__(192, 1) crt8_kernel(const __grid_constant__ Cr
     // ------------------------------ epilogue: int32 sums -> residues mod p (one byte each) ------------------------------
     const int quad = warp & 3;
     const uint32_t tlane = tmem + (static_cast<uint32_t>(quad * 32) << 16);
-    if (lane == 0) mbar_arrive(acc_empty);
+    auto release = [&]() {
+      if (lane == 0) {
+        if (PAIR && crank != 0) mbar_arrive_remote(acc_empty, 0);
+        else mbar_arrive(acc_empty);
+      }
+    };
+    release();
     uint32_t it = 0;
-    crt_for_items(g, [&](int split, int mod, int mt) {
+    crt_for_items<PAIR>(g, [&](int split, int mod, int mu) {
       int64_t kb0;
       int nkb;
       item_k(split, kb0, nkb);
-      const uint32_t p = crt_tab.p[mod], magic = crt_tab.magic[mod], offs = crt_tab.offs[mod];
+      const int mt = PAIR ? 2 * mu + static_cast<int>(crank) : mu;
+      const uint32_t p = crt_tab.p[mod], magic = crt_tab.magic[mod];
       const int64_t m = static_cast<int64_t>(mt) * kCrtBM + quad * 32 + lane;
       uint8_t* orow = g.out + ((static_cast<int64_t>(split) * g.nm + mod) * g.M + m) * g.n16;
       mbar_wait(acc_full, it & 1);
@@ -363,7 +474,7 @@ __global__ void __launch_bounds__(192, 1) crt8_kernel(const __grid_constant__ Cr
           uint32_t w[4] = {0, 0, 0, 0};
 #pragma unroll
           for (int q = 0; q < 16; ++q) {
-            const uint32_t n = nkb > 0 ? v[h][q] + offs : 0u;  // in (0, 2^31)
+            const uint32_t n = nkb > 0 ? v[h][q] : 0u;  // in [0, 2^31)
             const uint32_t t = n - (__umulhi(magic, n) >> 7) * p;
             w[q >> 2] |= t << (8 * (q & 3));
           }
@@ -372,45 +483,55 @@ __global__ void __launch_bounds__(192, 1) crt8_kernel(const __grid_constant__ Cr
       }
       asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
       __syncwarp();
-      if (lane == 0) mbar_arrive(acc_empty);
+      release();
       ++it;
     });
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
+  if constexpr (PAIR) cluster_sync_all();  // no CTA leaves while the pair's MMAs or signals may still touch it
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
+    if constexpr (PAIR) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
+    else asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
   }
 }
 
 // ---------------------------------------------------------------------------
 // CRT reconstruction
 // ---------------------------------------------------------------------------
-// C' from its residues t_i = (C' q_i) mod p_i (|C'| < 0.39 P): exact 128-bit arithmetic
-// modulo 2^128, one rounding to fp64; returns C' 2^e2
-__device__ __forceinline__ double crt_value(const uint32_t (&t)[kCrtMaxMod], int nm, int e2) {
-  uint64_t a0 = 0, a1 = 0;
-  float f = 0.f;
+// C' from its residues t_i = C' mod p_i (|C'| < 0.39 P), exactly, modulo 2^128: the four 32-bit
+// limbs of sum_i t_i W_i accumulate without carries in 64-bit registers (t_i < 2^8, 16 terms:
+// < 2^44 each), q P is subtracted limb by limb, one signed carry pass, one rounding to fp64;
+// returns C' 2^e2.  (Tables are zero beyond the moduli in use.)
+__device__ __forceinline__ double crt_value(const uint32_t (&t)[kCrtMaxMod], int e2) {
+  uint64_t s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+  uint32_t fq = 0;
 #pragma unroll
-  for (int i = 0; i < kCrtMaxMod; ++i)
-    if (i < nm) {
-      const uint64_t ti = t[i];
-      const uint64_t lo = ti * crt_tab.w0[i], hi = __umul64hi(ti, crt_tab.w0[i]);
-      a0 += lo;
-      a1 += hi + (a0 < lo ? 1u : 0u) + ti * crt_tab.w1[i];
-      f = fmaf(static_cast<float>(t[i]), crt_tab.invp[i], f);
-    }
-  // sum = C' + q P with q = rint(sum / P) = rint(sum_i t_i / p_i): |C' / P| < 0.39, float error ~1e-5
-  const uint64_t q = static_cast<uint64_t>(__float2uint_rn(f));
-  const uint64_t qp0 = q * crt_tab.P0;
-  const uint64_t r0 = a0 - qp0;
-  const uint64_t r1 = a1 - __umul64hi(q, crt_tab.P0) - q * crt_tab.P1 - (a0 < qp0 ? 1u : 0u);
-  const bool neg = static_cast<int64_t>(r1) < 0;
-  uint64_t m0 = r0, m1 = r1;
+  for (int i = 0; i < kCrtMaxMod; ++i) {
+    s0 += static_cast<uint64_t>(t[i]) * crt_tab.w[i][0];
+    s1 += static_cast<uint64_t>(t[i]) * crt_tab.w[i][1];
+    s2 += static_cast<uint64_t>(t[i]) * crt_tab.w[i][2];
+    s3 += static_cast<uint64_t>(t[i]) * crt_tab.w[i][3];
+    fq += t[i] * crt_tab.fq[i];
+  }
+  // sum = C' + q P with q = rint(sum / P) = rint(sum_i t_i q_i / p_i) <= 4080: |C' / P| < 0.39,
+  // and the 2^-19 fixed-point sum is good to 0.004
+  const uint32_t q = (fq + (1u << 18)) >> 19;
+  int64_t d0 = static_cast<int64_t>(s0) - static_cast<int64_t>(static_cast<uint64_t>(q) * crt_tab.P[0]);
+  int64_t d1 = static_cast<int64_t>(s1) - static_cast<int64_t>(static_cast<uint64_t>(q) * crt_tab.P[1]);
+  int64_t d2 = static_cast<int64_t>(s2) - static_cast<int64_t>(static_cast<uint64_t>(q) * crt_tab.P[2]);
+  int64_t d3 = static_cast<int64_t>(s3) - static_cast<int64_t>(static_cast<uint64_t>(q) * crt_tab.P[3]);
+  d1 += d0 >> 32;
+  d2 += d1 >> 32;
+  d3 += d2 >> 32;
+  const uint32_t r0 = static_cast<uint32_t>(d0), r1 = static_cast<uint32_t>(d1), r2 = static_cast<uint32_t>(d2),
+                 r3 = static_cast<uint32_t>(d3);
+  const bool neg = static_cast<int32_t>(r3) < 0;
+  uint64_t m0 = (static_cast<uint64_t>(r1) << 32) | r0, m1 = (static_cast<uint64_t>(r3) << 32) | r2;
   if (neg) {
-    m0 = ~r0 + 1;
-    m1 = ~r1 + (m0 == 0 ? 1u : 0u);
+    m0 = ~m0 + 1;
+    m1 = ~m1 + (m0 == 0 ? 1u : 0u);
   }
   double d;
   int sh = 0;
@@ -442,63 +563,86 @@ struct CrtOutArgs {
 
 constexpr int kCrtRB = 8;  // rows per block of the reconstruction
 
-__global__ void __launch_bounds__(256) crt_combine_kernel(const CrtOutArgs g) {
+__global__ void __launch_bounds__(256, 3) crt_combine_kernel(const CrtOutArgs g) {
   extern __shared__ double vals[];  // [kCrtRB][n16 + 1]
   const int ldv = g.n16 + 1;
   const int64_t m0 = static_cast<int64_t>(blockIdx.x) * kCrtRB;
   const int groups = g.n16 / 4;
   const int64_t plane = g.M * g.n16;
-  for (int e = threadIdx.x; e < kCrtRB * groups; e += blockDim.x) {
-    const int rl = e / groups, gq = e % groups;
+  // a thread reconstructs 4 consecutive columns of one row: one 4-byte word per modulus plane,
+  // all 16 loads in flight together
+  int rl = threadIdx.x / groups, gq = threadIdx.x % groups;
+  const int drl = blockDim.x / groups, dgq = blockDim.x % groups;
+  while (rl < kCrtRB && m0 + rl < g.M) {
     const int64_t m = m0 + rl;
-    if (m >= g.M) continue;
-    uint32_t t[4][kCrtMaxMod];
+    const uint8_t* src = g.res + m * g.n16 + 4 * gq;
+    uint32_t wv[kCrtMaxMod];
 #pragma unroll
-    for (int i = 0; i < kCrtMaxMod; ++i) {
-      uint32_t b[4] = {0, 0, 0, 0};
-      if (i < g.nm) {
-        for (int sp = 0; sp < g.splits; ++sp) {
-          const uint32_t w = __ldcs(reinterpret_cast<const uint32_t*>(
-              g.res + (static_cast<int64_t>(sp) * g.nm + i) * plane + m * g.n16 + 4 * gq));
+    for (int i = 0; i < kCrtMaxMod; ++i)
+      wv[i] = __ldcs(reinterpret_cast<const uint32_t*>(src + (i < g.nm ? i : 0) * plane));
+    if (g.splits > 1) {
+      // residues of the K splits add modulo p_i (their sum is C' mod p_i of the whole product)
+#pragma unroll 1
+      for (int sp = 1; sp < g.splits; ++sp) {
 #pragma unroll
-          for (int q = 0; q < 4; ++q) b[q] += (w >> (8 * q)) & 0xFFu;
-        }
-        if (g.splits > 1) {
+        for (int i = 0; i < kCrtMaxMod; ++i) {
+          const uint32_t w2 = __ldcs(reinterpret_cast<const uint32_t*>(
+              src + (static_cast<int64_t>(sp) * g.nm + (i < g.nm ? i : 0)) * plane));
+          uint32_t o = 0;
 #pragma unroll
-          for (int q = 0; q < 4; ++q) b[q] %= crt_tab.p[i];
+          for (int q = 0; q < 4; ++q) {
+            uint32_t b = ((wv[i] >> (8 * q)) & 0xFFu) + ((w2 >> (8 * q)) & 0xFFu);
+            b -= b >= crt_tab.p[i] ? crt_tab.p[i] : 0u;
+            o |= b << (8 * q);
+          }
+          wv[i] = o;
         }
       }
-#pragma unroll
-      for (int q = 0; q < 4; ++q) t[q][i] = b[q];
     }
     const int sa = g.sa[m];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int n = 4 * gq + q;
-      vals[rl * ldv + n] = n < g.N ? crt_value(t[q], g.nm, -(sa + g.sb[n])) : 0.0;
+      uint32_t t[kCrtMaxMod];
+#pragma unroll
+      for (int i = 0; i < kCrtMaxMod; ++i) t[i] = (wv[i] >> (8 * q)) & 0xFFu;
+      vals[rl * ldv + n] = n < g.N ? crt_value(t, -(sa + g.sb[n])) : 0.0;
+    }
+    gq += dgq;
+    rl += drl;
+    if (gq >= groups) {
+      gq -= groups;
+      ++rl;
     }
   }
   __syncthreads();
   const int rows = static_cast<int>((g.M - m0) < kCrtRB ? (g.M - m0) : kCrtRB);
   const uint32_t M2 = static_cast<uint32_t>(g.cmap.M2), N2 = static_cast<uint32_t>(g.cmap.N2);
-  if (g.perm > 0) {
-    // j -> (n2, row, n1): for Env[r_hi][m][r_lo] each n2 plane gets one contiguous rows x r_lo block
-    const int q1 = g.perm, total = rows * g.N;
-    for (int e = threadIdx.x; e < total; e += blockDim.x) {
-      const int n1 = e % q1, rl = (e / q1) % rows, n2 = e / (q1 * rows);
-      const uint32_t mm = static_cast<uint32_t>(m0 + rl);
-      const int64_t off = static_cast<int64_t>(mm / M2) * g.cmap.sm1 + static_cast<int64_t>(mm % M2) * g.cmap.sm2 +
-                          static_cast<int64_t>(n1) * g.cmap.sn1 + static_cast<int64_t>(n2) * g.cmap.sn2;
-      g.C[off] = vals[rl * ldv + n1 * static_cast<int>(N2) + n2];
+  // stores in the order of C's addresses; e -> (outer, row, inner) advanced incrementally (no
+  // per-element divisions).  perm: for Env[r_hi][m][r_lo] each n2 plane gets one contiguous
+  // rows x r_lo block (inner = n1 of perm values, outer = n2); else inner = n, outer unused.
+  const int inner = g.perm > 0 ? g.perm : g.N, outer = g.perm > 0 ? g.N / g.perm : 1;
+  int i1 = threadIdx.x % inner, tq = threadIdx.x / inner;
+  int o2 = tq / rows;
+  rl = tq % rows;
+  const int d1 = blockDim.x % inner, dq = blockDim.x / inner;
+  while (o2 < outer) {
+    const int n = g.perm > 0 ? i1 * static_cast<int>(N2) + o2 : i1;
+    const uint32_t mm = static_cast<uint32_t>(m0 + rl), un = static_cast<uint32_t>(n);
+    const uint32_t nq = g.perm > 0 ? static_cast<uint32_t>(i1) : un / N2, nr = g.perm > 0 ? static_cast<uint32_t>(o2) : un % N2;
+    const int64_t off = static_cast<int64_t>(mm / M2) * g.cmap.sm1 + static_cast<int64_t>(mm % M2) * g.cmap.sm2 +
+                        static_cast<int64_t>(nq) * g.cmap.sn1 + static_cast<int64_t>(nr) * g.cmap.sn2;
+    g.C[off] = vals[rl * ldv + n];
+    i1 += d1;
+    int carry = dq;
+    if (i1 >= inner) {
+      i1 -= inner;
+      ++carry;
     }
-  } else {
-    const int total = rows * g.N;
-    for (int e = threadIdx.x; e < total; e += blockDim.x) {
-      const int n = e % g.N, rl = e / g.N;
-      const uint32_t mm = static_cast<uint32_t>(m0 + rl), un = static_cast<uint32_t>(n);
-      const int64_t off = static_cast<int64_t>(mm / M2) * g.cmap.sm1 + static_cast<int64_t>(mm % M2) * g.cmap.sm2 +
-                          static_cast<int64_t>(un / N2) * g.cmap.sn1 + static_cast<int64_t>(un % N2) * g.cmap.sn2;
-      g.C[off] = vals[rl * ldv + n];
+    rl += carry;
+    while (rl >= rows) {
+      rl -= rows;
+      ++o2;
     }
   }
 }

@@ -9,6 +9,7 @@
 
 #include <cudaTypedefs.h>
 
+#include <cstdio>
 #include <cstdlib>
 
 #include "../../include/trals.h"
@@ -617,24 +618,21 @@ const CrtHost& crt_host() {
       lg += std::log2(static_cast<long double>(moduli[i]));
     }
     c.t.nm = nm;
-    c.t.P0 = static_cast<uint64_t>(P);
-    c.t.P1 = static_cast<uint64_t>(P >> 64);
+    for (int j = 0; j < 4; ++j) c.t.P[j] = static_cast<uint32_t>(P >> (32 * j));
     for (int i = 0; i < trals::kCrtMaxMod; ++i) {
       const uint32_t p = moduli[i];
       c.t.p[i] = p;
       c.t.magic[i] = static_cast<uint32_t>(((1ull << 39) + p - 1) / p);
-      c.t.offs[i] = p * ((1u << 30) / p);
-      c.t.invp[i] = 1.0f / static_cast<float>(p);
       if (i >= nm) continue;
       const u128 W = P / p;
-      c.t.w0[i] = static_cast<uint64_t>(W);
-      c.t.w1[i] = static_cast<uint64_t>(W >> 64);
       const uint32_t wr = static_cast<uint32_t>(W % p);
       uint32_t q = 0;
       for (uint32_t z = 1; z < p; ++z)
         if ((wr * z) % p == 1) { q = z; break; }
       if (!q) return c;  // (moduli not coprime: cannot happen)
-      c.t.qinv[i] = q;
+      const u128 Wq = W * q;  // = (P / p) q < P: already reduced mod P
+      for (int j = 0; j < 4; ++j) c.t.w[i][j] = static_cast<uint32_t>(Wq >> (32 * j));
+      c.t.fq[i] = static_cast<uint32_t>(std::llround(std::ldexp(static_cast<double>(q) / p, 19)));
     }
     // ||a'|| ||b'|| <= 2^(ga+gb) < P / 2; rows are int64 -> each <= 62
     int gtot = static_cast<int>(std::floor(static_cast<double>(lg) - 1.0 - 0.01));
@@ -656,6 +654,14 @@ inline bool crt_shape_ok(int64_t M, int64_t K, int64_t N) {
 }
 inline int64_t crt_kblocks(int64_t K) { return (K + trals::kCrtBK - 1) / trals::kCrtBK; }
 inline int64_t crt_mtiles(int64_t M) { return (M + trals::kCrtBM - 1) / trals::kCrtBM; }
+// rows of an A residue plane: whole pairs of m-tiles (the CTA-pair kernel loads both tiles of a pair)
+inline int64_t crt_a_rows_pad(int64_t M) { return (M + 2 * trals::kCrtBM - 1) / (2 * trals::kCrtBM) * (2 * trals::kCrtBM); }
+// TRALS_CRT_PAIR=0 (experiments): one-CTA MMAs (cta_group::1) instead of CTA pairs
+inline bool crt_pair() {
+  static int v = -1;
+  if (v < 0) v = (std::getenv("TRALS_CRT_PAIR") && std::atoi(std::getenv("TRALS_CRT_PAIR")) == 0) ? 0 : 1;
+  return v == 1;
+}
 // bytes of the residue planes of a [rows][K] operand tiled in row tiles of tile_w
 inline int64_t crt_plane_bytes(int64_t rows_pad, int64_t K) { return rows_pad * crt_kblocks(K) * trals::kCrtBK; }
 
@@ -721,18 +727,17 @@ int crt_scales(const double* x, int64_t rows, int64_t cols, int64_t ld, int tran
   dim3 grid(static_cast<unsigned>((cols + 31) / 32), static_cast<unsigned>(slabs));
   trals::crt_col_stats_kernel<<<grid, 256, 0, s>>>(x, rows, cols, ld, rps, part);
   if (int st = launch_status()) return st;
-  trals::crt_col_scale_kernel<<<static_cast<unsigned>((cols + 255) / 256), 256, 0, s>>>(part, slabs, cols, rows, gamma,
-                                                                                          sexp);
+  trals::crt_col_scale_kernel<<<static_cast<unsigned>((cols + 7) / 8), 256, 0, s>>>(part, slabs, cols, rows, gamma,
+                                                                                      sexp);
   return launch_status();
 }
 
-template <bool FOLD>
 int crt_slice(const double* x, int64_t rows, int64_t cols, int64_t ld, int transpose, const int32_t* sexp,
-              int8_t* planes, int64_t rows_pad, int tile_w, cudaStream_t s) {
+              uint8_t* planes, int64_t rows_pad, int tile_w, cudaStream_t s) {
   const int64_t K = transpose ? rows : cols;
   const int64_t blocks = crt_kblocks(K) * ((rows_pad + 63) / 64);
   if (blocks > INT32_MAX) return TRALS_ERR_UNSUPPORTED;
-  trals::crt_slice_kernel<FOLD><<<static_cast<unsigned>(blocks), 256, 0, s>>>(
+  trals::crt_slice_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(
       x, rows, cols, ld, transpose, sexp, planes, rows_pad, tile_w, crt_host().t.nm, crt_plane_bytes(rows_pad, K));
   return launch_status();
 }
@@ -755,8 +760,8 @@ int crt_split(const double* x, int64_t rows, int64_t cols, int transpose, int8_t
   if (!crt_host().ok) return TRALS_ERR_CUDA;
   if (!crt_shape_ok(out_rows, K, 1)) return TRALS_ERR_UNSUPPORTED;
   if (int st = crt_scales(x, rows, cols, cols, transpose, crt_host().t.ga, exps, ws, s)) return st;
-  return crt_slice<false>(x, rows, cols, cols, transpose, exps, planes, crt_mtiles(out_rows) * trals::kCrtBM,
-                          trals::kCrtBM, s);
+  return crt_slice(x, rows, cols, cols, transpose, exps, reinterpret_cast<uint8_t*>(planes), crt_a_rows_pad(out_rows),
+                   trals::kCrtBM, s);
 }
 
 // C(m, n) = sum_k A[m][k] B[k][n]: A given as residue planes + row scale exponents, B fp64 [K][ldb]
@@ -770,11 +775,11 @@ int gemm_crt(const int8_t* ad, const int32_t* ea, int64_t M, int64_t K, int64_t 
   if (!ws || w.total > ws_elems) return TRALS_ERR_ARG;
   const trals::CrtTables& t = crt_host().t;
   const int n16 = crt_n16(N);
-  int8_t* bd = reinterpret_cast<int8_t*>(ws + w.bplanes);
+  uint8_t* bd = reinterpret_cast<uint8_t*>(ws + w.bplanes);
   int32_t* sb = reinterpret_cast<int32_t*>(ws + w.sb);
   uint8_t* res = reinterpret_cast<uint8_t*>(ws + w.res);
   if (int st = crt_scales(B, K, N, ldb, 1, t.gb, sb, ws + w.part, s)) return st;
-  if (int st = crt_slice<true>(B, K, N, ldb, 1, sb, bd, n16, n16, s)) return st;
+  if (int st = crt_slice(B, K, N, ldb, 1, sb, bd, n16, n16, s)) return st;
   trals::CrtArgs g{};
   g.M = M; g.K = K; g.n16 = n16; g.nm = t.nm;
   if (n16 <= 256) { g.nc0 = n16; g.nc1 = 0; }
@@ -783,23 +788,53 @@ int gemm_crt(const int8_t* ad, const int32_t* ea, int64_t M, int64_t K, int64_t 
   g.splits = w.splits;
   g.kblocks = crt_kblocks(K);
   g.kb_split = w.kb_split;
-  g.a_plane = crt_plane_bytes(static_cast<int64_t>(g.mtiles) * trals::kCrtBM, K);
+  g.a_plane = crt_plane_bytes(crt_a_rows_pad(M), K);
   g.b_plane = crt_plane_bytes(n16, K);
-  g.ad = ad; g.bd = bd; g.out = res;
-  const int stage = trals::kCrtBM * trals::kCrtBK + n16 * trals::kCrtBK;
+  g.ad = reinterpret_cast<const uint8_t*>(ad); g.bd = bd; g.out = res;
+  const bool pair = crt_pair();
+  const int stage = trals::kCrtBM * trals::kCrtBK + n16 * trals::kCrtBK / (pair ? 2 : 1);
   g.stages = std::min(8, (212 * 1024) / stage);
   if (g.stages < 2) return TRALS_ERR_UNSUPPORTED;
-  const size_t smem = static_cast<size_t>(g.stages) * stage + (2 * g.stages + 2) * 8 + 16 + 1024;
-  static size_t smem_set = 0;
-  if (smem > smem_set) {
-    if (cudaFuncSetAttribute(trals::crt8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(smem)) != cudaSuccess)
+  const size_t smem = static_cast<size_t>(g.stages) * stage + (3 * g.stages + 2) * 8 + 16 + 1024;
+  auto kern = pair ? trals::crt8_kernel<true> : trals::crt8_kernel<false>;
+  static size_t smem_set[2] = {0, 0};
+  if (smem > smem_set[pair]) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) !=
+        cudaSuccess)
       return TRALS_ERR_CUDA;
-    smem_set = smem;
+    smem_set[pair] = smem;
   }
-  const int64_t items = static_cast<int64_t>(g.mtiles) * g.nm * g.splits;
-  const int grid = static_cast<int>(std::min<int64_t>(items, kSMs));
-  trals::crt8_kernel<<<grid, 192, smem, s>>>(g);
+  if (pair) {
+    const int64_t units = (static_cast<int64_t>(g.mtiles) + 1) / 2 * g.nm * g.splits;
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.blockDim = dim3(192);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    static int max_clusters = 0;  // CTA pairs resident at once (persistent kernel)
+    if (!max_clusters) {
+      cfg.gridDim = dim3(kSMs / 2 * 2);
+      if (cudaOccupancyMaxActiveClusters(&max_clusters, kern, &cfg) != cudaSuccess || max_clusters < 1)
+        max_clusters = kSMs / 2;
+      if (std::getenv("TRALS_CRT_DEBUG")) std::fprintf(stderr, "crt pair: max active clusters %d\n", max_clusters);
+      max_clusters = std::min(max_clusters, kSMs / 2);
+    }
+    static int force = -1;  // TRALS_CRT_CLUSTERS (experiments): number of CTA pairs launched
+    if (force < 0) force = std::getenv("TRALS_CRT_CLUSTERS") ? std::atoi(std::getenv("TRALS_CRT_CLUSTERS")) : 0;
+    const int ncl = force > 0 ? force : max_clusters;
+    cfg.gridDim = dim3(static_cast<unsigned>(std::min<int64_t>(units, ncl) * 2));
+    if (cudaLaunchKernelEx(&cfg, kern, g) != cudaSuccess) return TRALS_ERR_CUDA;
+  } else {
+    const int64_t items = static_cast<int64_t>(g.mtiles) * g.nm * g.splits;
+    const int grid = static_cast<int>(std::min<int64_t>(items, kSMs));
+    kern<<<grid, 192, smem, s>>>(g);
+  }
   if (int st = launch_status()) return st;
   trals::CrtOutArgs o{};
   o.res = res; o.M = M; o.n16 = n16; o.N = static_cast<int>(N); o.nm = t.nm; o.splits = g.splits;
@@ -2960,7 +2995,7 @@ int trals_crt_moduli(void) { return crt_host().ok ? crt_host().t.nm : 0; }
 
 int64_t trals_crt_planes_bytes(int64_t rows, int64_t k) {
   if (rows < 1 || k < 1 || !crt_host().ok) return 0;
-  return static_cast<int64_t>(crt_host().t.nm) * crt_plane_bytes(crt_mtiles(rows) * trals::kCrtBM, k);
+  return static_cast<int64_t>(crt_host().t.nm) * crt_plane_bytes(crt_a_rows_pad(rows), k);
 }
 
 int64_t trals_crt_split_ws_elems(int64_t rows, int64_t cols, int transpose) {

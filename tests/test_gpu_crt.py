@@ -66,7 +66,7 @@ def _plane_offsets(rows, k):
 
 
 def _crt_rebuild(res):
-    """Exact integers from their symmetric residues res[i] (object arrays of Python ints)."""
+    """Exact integers from their residues res[i] in [0, p_i) (object arrays of Python ints)."""
     nm = len(res)
     P = 1
     for p in MODULI[:nm]:
@@ -89,7 +89,7 @@ def _crt_rebuild(res):
 def test_env_crt_matches_f64(pre, post, side, r_lo, r_hi, leaf):
     """CRT environment product against the DMMA one on the same X: tails in every dimension, one and
     two MMA column chunks (R^2 <= 256 / > 256, up to 512 columns), K splits (incl. the forced one for
-    K > 65472), both sides, both CMaps.  The residue planes rebuild rint(2^s x) exactly, with the
+    K > 33024), both sides, both CMaps.  The residue planes rebuild rint(2^s x) exactly, with the
     scaled rows inside the 2^62 norm bound; the products agree to the fp64 rounding level."""
     from paper_2210_11362_b200 import _lib as L
     lib = L.lib()
@@ -106,12 +106,12 @@ def test_env_crt_matches_f64(pre, post, side, r_lo, r_hi, leaf):
     got, planes, exps = _crt_env(lib, x64, pre, post, side, H, r_lo, r_hi, leaf)
     torch.cuda.synchronize()
     if rows * K <= 400_000:
-        buf = planes.cpu().numpy()
+        buf = planes.cpu().numpy().view(np.uint8)
         psize = buf.size // nm
         off = _plane_offsets(rows, K)
         res = [buf[i * psize:(i + 1) * psize][off].astype(np.int64).astype(object) for i in range(nm)]
         for i, p in enumerate(MODULI[:nm]):
-            assert max(abs(int(v)) for v in res[i].ravel()) <= p // 2
+            assert max(int(v) for v in res[i].ravel()) < p
         val, _ = _crt_rebuild(res)
         xs = x if side == 0 else x.T
         s = exps.cpu().numpy().astype(np.int64)
@@ -179,9 +179,9 @@ def test_env_crt_deterministic():
     assert torch.equal(a, b)
 
 
-@pytest.mark.parametrize("K", [65472, 65473])
+@pytest.mark.parametrize("K", [33024, 33025])
 def test_env_crt_kmax_boundaries(K):
-    """Contraction lengths at the int32 bound of one K split (128^2 x 65472 < 2^30) and one past
+    """Contraction lengths at the int32 bound of one K split (255^2 x 33024 < 2^31) and one past
     it (two splits, residues added mod p before the reconstruction), on rows of +-(1 - tiny): the
     product stays at the fp64 rounding level of the DMMA one, so no int32 sum wrapped around."""
     from paper_2210_11362_b200 import _lib as L
