@@ -162,6 +162,12 @@ int64_t trals_env_crt_ws_elems(int64_t pre, int64_t post, int side, int r_lo, in
 int trals_env_crt(const int8_t* d_xplanes, const int32_t* d_xexps, int64_t pre, int64_t post, int side,
                   const double* d_H, int r_lo, int r_hi, double* d_env, int leaf, double* d_ws, int64_t ws_elems,
                   void* stream);
+/* The same product stage by stage on the same workspace (stages: bit mask, run in this order):
+ * 1 = scales + residue planes of the half chain, 2 = the modular int8 GEMMs, 4 = CRT reconstruction
+ * into d_env.  trals_env_crt == stages 7.  Lets the caller time or schedule the stages apart. */
+int trals_env_crt_stage(const int8_t* d_xplanes, const int32_t* d_xexps, int64_t pre, int64_t post, int side,
+                        const double* d_H, int r_lo, int r_hi, double* d_env, int leaf, double* d_ws,
+                        int64_t ws_elems, int stages, void* stream);
 /* Absorb the rightmost / leftmost core of an environment segment.
  * Env layout [r_a][i_a .. i_b][r_{b+1}].
  *   right: Out[r_a][pre][r_b]       = sum E[r_a][pre][i_b][r_{b+1}] G_b[r_b,i_b,r_{b+1}]

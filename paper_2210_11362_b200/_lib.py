@@ -86,6 +86,8 @@ _SIGNATURES = {
     "trals_env_crt_ws_elems": (c_int64, [c_int64, c_int64, c_int, c_int, c_int]),
     "trals_env_crt": (c_int, [_dp, _dp, c_int64, c_int64, c_int, _dp, c_int, c_int, _dp, c_int, _dp, c_int64,
                               c_void_p]),
+    "trals_env_crt_stage": (c_int, [_dp, _dp, c_int64, c_int64, c_int, _dp, c_int, c_int, _dp, c_int, _dp, c_int64,
+                                    c_int, c_void_p]),
     "trals_residual_oz64_ws_elems": (c_int64, [c_int64, c_int64, c_int64]),
     "trals_residual_oz64": (c_int, [_dp, c_int64, c_int64, _dp, _dp, c_int64, _dp, _dp, _dp, c_int64, c_void_p]),
     "trals_mttsp_ws_elems": (c_int64, [c_int, POINTER(c_int64), POINTER(c_int32), c_int]),

@@ -766,8 +766,10 @@ int crt_split(const double* x, int64_t rows, int64_t cols, int transpose, int8_t
 
 // C(m, n) = sum_k A[m][k] B[k][n]: A given as residue planes + row scale exponents, B fp64 [K][ldb]
 // (sliced per call into the workspace), C fp64 through cm
+// stages: 1 = slice B (scales + residue planes into ws), 2 = the modular GEMMs, 4 = CRT reconstruction;
+// the three run in this order on ws, in one call or in separate ones
 int gemm_crt(const int8_t* ad, const int32_t* ea, int64_t M, int64_t K, int64_t N, const double* B, int64_t ldb,
-             double* C, const CMap& cm, double* ws, int64_t ws_elems, cudaStream_t s) {
+             double* C, const CMap& cm, double* ws, int64_t ws_elems, int stages, cudaStream_t s) {
   if (!crt_host().ok) return TRALS_ERR_CUDA;
   if (!crt_shape_ok(M, K, N)) return TRALS_ERR_UNSUPPORTED;
   if (reinterpret_cast<uintptr_t>(ad) & 15u) return TRALS_ERR_ARG;
@@ -778,8 +780,10 @@ int gemm_crt(const int8_t* ad, const int32_t* ea, int64_t M, int64_t K, int64_t 
   uint8_t* bd = reinterpret_cast<uint8_t*>(ws + w.bplanes);
   int32_t* sb = reinterpret_cast<int32_t*>(ws + w.sb);
   uint8_t* res = reinterpret_cast<uint8_t*>(ws + w.res);
-  if (int st = crt_scales(B, K, N, ldb, 1, t.gb, sb, ws + w.part, s)) return st;
-  if (int st = crt_slice(B, K, N, ldb, 1, sb, bd, n16, n16, s)) return st;
+  if (stages & 1) {
+    if (int st = crt_scales(B, K, N, ldb, 1, t.gb, sb, ws + w.part, s)) return st;
+    if (int st = crt_slice(B, K, N, ldb, 1, sb, bd, n16, n16, s)) return st;
+  }
   trals::CrtArgs g{};
   g.M = M; g.K = K; g.n16 = n16; g.nm = t.nm;
   if (n16 <= 256) { g.nc0 = n16; g.nc1 = 0; }
@@ -791,6 +795,7 @@ int gemm_crt(const int8_t* ad, const int32_t* ea, int64_t M, int64_t K, int64_t 
   g.a_plane = crt_plane_bytes(crt_a_rows_pad(M), K);
   g.b_plane = crt_plane_bytes(n16, K);
   g.ad = reinterpret_cast<const uint8_t*>(ad); g.bd = bd; g.out = res;
+  if (stages & 2) {
   const bool pair = crt_pair();
   const int stage = trals::kCrtBM * trals::kCrtBK + n16 * trals::kCrtBK / (pair ? 2 : 1);
   g.stages = std::min(8, (212 * 1024) / stage);
@@ -836,6 +841,8 @@ int gemm_crt(const int8_t* ad, const int32_t* ea, int64_t M, int64_t K, int64_t 
     kern<<<grid, 192, smem, s>>>(g);
   }
   if (int st = launch_status()) return st;
+  }
+  if (!(stages & 4)) return TRALS_OK;
   trals::CrtOutArgs o{};
   o.res = res; o.M = M; o.n16 = n16; o.N = static_cast<int>(N); o.nm = t.nm; o.splits = g.splits;
   o.sa = ea; o.sb = sb; o.C = C; o.cmap = cm;
@@ -848,12 +855,12 @@ int gemm_crt(const int8_t* ad, const int32_t* ea, int64_t M, int64_t K, int64_t 
 
 // env() on the CRT engine: X given as residue planes + scale exponents, K-major for this side
 int env_crt(const int8_t* xd, const int32_t* xe, int64_t pre, int64_t post, int side, const double* H, int r_lo,
-            int r_hi, double* E, int leaf, double* ws, int64_t ws_elems, cudaStream_t s) {
+            int r_hi, double* E, int leaf, double* ws, int64_t ws_elems, int stages, cudaStream_t s) {
   const int64_t RR = static_cast<int64_t>(r_lo) * r_hi;
   const int64_t rows = side == 0 ? pre : post, K = side == 0 ? post : pre;
   CMap cm{0, rows, 0, r_lo, r_hi, 1, rows * r_lo};
   if (leaf) cm = CMap{0, rows, 0, RR, r_hi, r_hi, 1};
-  return gemm_crt(xd, xe, rows, K, RR, H, RR, E, cm, ws, ws_elems, s);
+  return gemm_crt(xd, xe, rows, K, RR, H, RR, E, cm, ws, ws_elems, stages, s);
 }
 
 // Accuracy guard of the digit-sliced fp64 products (AlsConfig.fp64_gemm = "auto"): per K-major row
@@ -3018,7 +3025,17 @@ int trals_env_crt(const int8_t* xd, const int32_t* xe, int64_t pre, int64_t post
                   int r_lo, int r_hi, double* E, int leaf, double* ws, int64_t ws_elems, void* stream) {
   if (!xd || !xe || !H || !E || !ws || pre < 1 || post < 1 || r_lo < 1 || r_hi < 1 || (side != 0 && side != 1))
     return TRALS_ERR_ARG;
-  return env_crt(xd, xe, pre, post, side, H, r_lo, r_hi, E, leaf, ws, ws_elems, static_cast<cudaStream_t>(stream));
+  return env_crt(xd, xe, pre, post, side, H, r_lo, r_hi, E, leaf, ws, ws_elems, 7, static_cast<cudaStream_t>(stream));
+}
+
+int trals_env_crt_stage(const int8_t* xd, const int32_t* xe, int64_t pre, int64_t post, int side, const double* H,
+                        int r_lo, int r_hi, double* E, int leaf, double* ws, int64_t ws_elems, int stages,
+                        void* stream) {
+  if (!xd || !xe || !H || !E || !ws || pre < 1 || post < 1 || r_lo < 1 || r_hi < 1 || (side != 0 && side != 1) ||
+      stages < 1 || stages > 7)
+    return TRALS_ERR_ARG;
+  return env_crt(xd, xe, pre, post, side, H, r_lo, r_hi, E, leaf, ws, ws_elems, stages,
+                 static_cast<cudaStream_t>(stream));
 }
 
 int trals_absorb_right_f64(const double* E, int Ra, int64_t pre, int64_t Ib, int Rb, int Rb1, const double* core_zt,

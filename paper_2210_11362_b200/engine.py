@@ -337,6 +337,7 @@ class SweepEngine:
             self._bufs.append(E0)
             target = lambda E0=E0: E0.data_ptr()
 
+        env_name = f"env[{seg_a}..{seg_b}]"
         if self.sliced:
             rows, k = (pre, post) if side == 0 else (post, pre)
             kind = "oz32" if self.fp32 else self._env_kind(rows, k, r_lo * r_hi)
@@ -348,17 +349,28 @@ class SweepEngine:
             self._ws(wsf(pre, post, side, r_lo, r_hi))
 
             def env_step(pre=pre, post=post, side=side, H=H, r_lo=r_lo, r_hi=r_hi, target=target,
-                         leaf=int(root_leaf), key=key, envf=envf):
+                         leaf=int(root_leaf), key=key, envf=envf, stages=None):
                 xd, xe = self._xsplit[key]
+                extra = () if stages is None else (stages,)
                 L.check(envf(xd.data_ptr(), xe.data_ptr(), pre, post, side, H.data_ptr(), r_lo, r_hi, target(),
-                             leaf, self.gws.data_ptr(), self.gws.numel(), self._sp()), "env_oz")
+                             leaf, self.gws.data_ptr(), self.gws.numel(), *extra, self._sp()), "env_oz")
+            if kind == "crt":
+                # three steps on the shared workspace: the half chain's residue planes, the modular
+                # GEMMs (the dominant kernel: the step named env[...]), the CRT reconstruction
+                staged = self.lib.trals_env_crt_stage
+                self.steps.append(Step("mttsp", lambda f=env_step, g=staged: f(envf=g, stages=1),
+                                       f"bslice[{seg_a}..{seg_b}]"))
+                self.steps.append(Step("mttsp", lambda f=env_step, g=staged: f(envf=g, stages=2),
+                                       f"env[{seg_a}..{seg_b}]"))
+                env_step = lambda f=env_step, g=staged: f(envf=g, stages=4)  # noqa: E731
+                env_name = f"crt[{seg_a}..{seg_b}]"
         else:
             def env_step(pre=pre, post=post, side=side, H=H, r_lo=r_lo, r_hi=r_hi, target=target,
                          leaf=int(root_leaf)):
                 L.check(self.lib.trals_env_f64(self.x.data_ptr(), pre, post, side, H.data_ptr(), r_lo, r_hi,
                                                target(), leaf, self.gws.data_ptr(), self.gws.numel(), self._sp()),
                         "env")
-        self.steps.append(Step("mttsp", env_step, f"env[{seg_a}..{seg_b}]"))
+        self.steps.append(Step("mttsp", env_step, env_name))
         self.stats.x_passes_per_sweep += 1
         self._env_flops.append(2.0 * pre * post * RR)
         if root_leaf:
@@ -744,12 +756,13 @@ class SweepEngine:
         """Flops of each X-streaming environment product (2*M*K*N), in step order."""
         return list(self._env_flops)
 
-    def run_sweep(self, events=None, env_events=None):
+    def run_sweep(self, events=None, env_events=None, aux_events=None):
         """Launch one full sweep.
 
         events: list -> (bucket, event) pairs appended at bucket changes.
         env_events: list -> (start, end) event pairs around every X-streaming
         environment product (the dominant kernel, for the roofline).
+        aux_events: dict -> the same for the CRT form's other stages ("bslice", "crt").
         """
         prev = None
         cuda = self.dev.type == "cuda"
@@ -770,13 +783,18 @@ class SweepEngine:
                 ev.record(self.stream)
                 events.append((st.bucket, ev))
                 prev = st.bucket
+            timed = None
             if env_events is not None and st.name.startswith("env"):
+                timed = env_events
+            elif aux_events is not None and st.name.startswith(("bslice", "crt[")):
+                timed = aux_events.setdefault(st.name.split("[")[0], [])
+            if timed is not None:
                 e0 = torch.cuda.Event(enable_timing=True)
                 e1 = torch.cuda.Event(enable_timing=True)
                 e0.record(self.stream)
                 st.fn()
                 e1.record(self.stream)
-                env_events.append((e0, e1))
+                timed.append((e0, e1))
             else:
                 st.fn()
         self._cur = None
