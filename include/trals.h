@@ -143,17 +143,20 @@ int trals_env_oz64(const int8_t* d_xdigits, const int32_t* d_xexps, int64_t pre,
  * (AlsConfig.fp64_gemm = "crt"; the default for long contractions, K >= 4096 and R^2 <= 512,
  * i.e. BASELINE c5): trals_env_f64 with X given as residue planes.  Every K-major row r of X is
  * scaled by 2^sx[r] (from its 2-norm) and rounded to integers x' = rint(2^sx x) with
- * ||x'||_2 <= 2^62; plane i holds the symmetric int8 residues x' mod p_i for the
- * trals_crt_moduli() (16) pairwise coprime moduli p_i <= 256, each plane tiled
+ * ||x'||_2 <= 2^trals_crt_row_bits(0) (58; 62 with 16 moduli); plane i holds the residues
+ * x' mod p_i in [0, p_i) (unsigned bytes) for the trals_crt_moduli() (15; TRALS_CRT_MODULI=12..16)
+ * largest pairwise coprime moduli p_i <= 256, each plane tiled
  * [128-row tile][64-k block][128 x 64 B] in the UMMA K-major SWIZZLE_64B pattern
  * (trals_crt_planes_bytes bytes in total).  The half chain is sliced the same way per call;
  * one exact int8 GEMM per modulus, reduced mod p_i in its epilogue, and an exact 128-bit CRT
  * reconstruction: the result is the correctly rounded exact product of the rounded operands.
- * Accuracy contract: as trals_env_oz64 (below), with each row rounded at 2^-62 of its 2-norm
- * instead of 2^-56.9 of its maximum.  Replaces the same reference call as trals_env_f64
+ * Accuracy contract: as trals_env_oz64 (below), with each row rounded at 2^-58 of its 2-norm
+ * instead of 2^-56.9 of its maximum (measured at K = 25600 on Gaussian operands: 3.8e-16 relative
+ * against an extended-precision product, fp64 DMMA 9.2e-16).  Replaces the same reference call as trals_env_f64
  * (solvers.py:379).  trals_crt_supported: 1 when the shape (rows x k) . (k x n) is covered. */
 int trals_crt_supported(int64_t rows, int64_t k, int64_t n);
 int trals_crt_moduli(void);
+int trals_crt_row_bits(int operand); /* log2 of the 2-norm bound of the scaled rows of X (0) / the half chain (1) */
 int64_t trals_crt_planes_bytes(int64_t rows, int64_t k);
 int64_t trals_crt_split_ws_elems(int64_t rows, int64_t cols, int transpose);
 int trals_crt_split_f64(const double* d_x, int64_t rows, int64_t cols, int transpose, int8_t* d_planes,

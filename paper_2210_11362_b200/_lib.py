@@ -80,6 +80,7 @@ _SIGNATURES = {
     "trals_residual_f64": (c_int, [_dp, c_int64, c_int64, _dp, _dp, c_int64, _dp, _dp, _dp, c_int64, c_void_p]),
     "trals_crt_supported": (c_int, [c_int64, c_int64, c_int64]),
     "trals_crt_moduli": (c_int, []),
+    "trals_crt_row_bits": (c_int, [c_int]),
     "trals_crt_planes_bytes": (c_int64, [c_int64, c_int64]),
     "trals_crt_split_ws_elems": (c_int64, [c_int64, c_int64, c_int]),
     "trals_crt_split_f64": (c_int, [_dp, c_int64, c_int64, c_int, _dp, _dp, _dp, c_int64, c_void_p]),

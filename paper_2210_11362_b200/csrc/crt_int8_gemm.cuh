@@ -1,5 +1,5 @@
 // fp64 environment products on the int8 tcgen05 tensor cores by the Chinese remainder
-// theorem (integer modular emulation, "Ozaki scheme II"): 16 int8 GEMMs per fp64 GEMM
+// theorem (integer modular emulation, "Ozaki scheme II"): 15 (or 16) int8 GEMMs per fp64 GEMM
 // instead of the 28 digit-pair products of the radix-254 slicing (tc_int8_gemm.cuh).
 //
 //   C(m, n) = sum_k A[m][k] B[k][n]        A = X (K-major rows), B = the fp64 half chain
@@ -8,9 +8,10 @@
 //    (2^sb[n]) from its 2-norm such that the integer rows a' = rint(2^sa a),
 //    b' = rint(2^sb b) satisfy ||a'||_2 <= 2^ga, ||b'||_2 <= 2^gb with
 //    2^(ga+gb) < P / 2, P the product of the moduli below (Cauchy-Schwarz: the exact
-//    integer product C' = a'.b' then lies in (-P/2, P/2)).  With 16 moduli P = 2^125.38,
-//    ga = gb = 62: a Gaussian row of 25600 entries keeps 2^-55 of its rms (entries above
-//    2^53 of the scaled row are not rounded at all).
+//    integer product C' = a'.b' then lies in (-P/2, P/2)).  With the default 15 moduli
+//    P = 2^117.78, ga = gb = 58: a Gaussian row of 25600 entries keeps 2^-51 of its rms, and
+//    the rounding errors are zero-mean: the product is 2.5x more accurate than fp64 DMMA at
+//    K = 25600.  (16 moduli: P = 2^125.38, ga = gb = 62.)
 // 2. Residues.  For each modulus p_i (pairwise coprime, <= 256) the residues a' mod p_i,
 //    b' mod p_i in [0, p_i) are unsigned bytes.  X's residues are made once per X (16 planes
 //    in the MMA's shared-memory image), the half chain's per call.
@@ -34,6 +35,11 @@
 namespace trals {
 
 constexpr int kCrtMaxMod = 16;
+// Moduli in use by default.  15: P = 2^117.8, rows rounded at 2^-58 of their 2-norm -- measured
+// against an extended-precision product at the c5 shape (K = 25600) 3.8e-16 relative, 2.5x more
+// accurate than the fp64 DMMA product (9.2e-16) and than the digit-pair form (6e-16).  16 moduli
+// (2^-62, 4.8e-17: the final rounding alone) cost one more GEMM in 15 (TRALS_CRT_MODULI=16).
+constexpr int kCrtDefaultMod = 15;
 constexpr int kCrtBK = 64;            // int8 k per stage row (SWIZZLE_64B)
 constexpr int kCrtBM = 128;
 constexpr int64_t kCrtKmax = 33024;   // 255^2 K < 2^31 (int32 sums of u8 x u8 products), multiple of 64

@@ -594,8 +594,8 @@ int gemm_oz(const int8_t* ad, const int32_t* ea, int64_t M, int64_t K, int64_t N
 // fp64 environment products by CRT on the int8 tensor cores (crt_int8_gemm.cuh)
 // ---------------------------------------------------------------------------
 // moduli tables: computed once on the host (128-bit integers) and copied to constant memory.
-// TRALS_CRT_MODULI (experiments) = number of moduli, 12..16 (fewer moduli = fewer GEMMs and
-// fewer operand bits: every dropped modulus costs ~4 bits per operand).
+// TRALS_CRT_MODULI = number of moduli, 12..16 (default kCrtDefaultMod = 15; every modulus is one
+// more int8 GEMM and ~4 more bits per operand row).
 struct CrtHost {
   trals::CrtTables t{};
   bool ok = false;
@@ -608,7 +608,7 @@ const CrtHost& crt_host() {
         TRALS_CRT_MODULI(TRALS_CRT_LIST)
 #undef TRALS_CRT_LIST
     };
-    int nm = std::getenv("TRALS_CRT_MODULI") ? std::atoi(std::getenv("TRALS_CRT_MODULI")) : trals::kCrtMaxMod;
+    int nm = std::getenv("TRALS_CRT_MODULI") ? std::atoi(std::getenv("TRALS_CRT_MODULI")) : trals::kCrtDefaultMod;
     nm = std::max(12, std::min(nm, trals::kCrtMaxMod));
     using u128 = unsigned __int128;
     u128 P = 1;
@@ -2999,6 +2999,11 @@ int trals_crt_supported(int64_t rows, int64_t k, int64_t n) {
 }
 
 int trals_crt_moduli(void) { return crt_host().ok ? crt_host().t.nm : 0; }
+
+int trals_crt_row_bits(int operand) {
+  if (!crt_host().ok) return 0;
+  return operand == 0 ? crt_host().t.ga : crt_host().t.gb;
+}
 
 int64_t trals_crt_planes_bytes(int64_t rows, int64_t k) {
   if (rows < 1 || k < 1 || !crt_host().ok) return 0;
