@@ -249,6 +249,13 @@ struct CrtArgs {
   const uint8_t* ad;          // [nm][mtiles (even)][kblocks][128 x 64 B]
   const uint8_t* bd;          // [nm][kblocks][n16 x 64 B]
   uint8_t* out;               // [splits][nm][M][n16]: C' mod p_i
+  // Tail split (splits == 1): the units beyond the last full wave (unit index >= tail_start) are cut
+  // into tail_splits K pieces of tail_kb 64-k blocks, so the last wave takes 1 / tail_splits of a
+  // unit's time.  Piece 0 writes the unit's rows of `out`, piece s >= 1 writes
+  // tail_out[s - 1][unit - tail_start][rows of the unit][n16]; the reconstruction adds them mod p_i.
+  int tail_start, tail_splits;
+  int64_t tail_kb;
+  uint8_t* tail_out;
 };
 
 // instruction descriptor: D s32, A/B unsigned int8 (type fields 0), K-major, N = n, M = 128 (one CTA)
@@ -298,12 +305,30 @@ __device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, uint32_t rank)
 // pair takes (split, modulus, pair of m-tiles) and CTA rank r the m-tile 2 j + r of it.
 template <bool PAIR, class F>
 __device__ __forceinline__ void crt_for_items(const CrtArgs& g, F&& body) {
+  // body(split, modulus, unit row index, first 64-k block, number of blocks, tail piece or -1, unit)
   const int mu = PAIR ? (g.mtiles + 1) / 2 : g.mtiles;
-  const int per_split = g.nm * mu, total = per_split * g.splits;
+  const int per_split = g.nm * mu, units = per_split * g.splits;
+  const int total = g.tail_start + (units - g.tail_start) * g.tail_splits;
   const int first = PAIR ? blockIdx.x / 2 : blockIdx.x, step = PAIR ? gridDim.x / 2 : gridDim.x;
-  for (int u = first; u < total; u += step) {
-    const int rem = u % per_split;
-    body(u / per_split, rem / mu, rem % mu);
+  for (int it = first; it < total; it += step) {
+    int u = it, piece = -1;
+    if (it >= g.tail_start) {
+      const int j = it - g.tail_start;
+      u = g.tail_start + j / g.tail_splits;
+      piece = j % g.tail_splits;
+    }
+    const int split = u / per_split, rem = u % per_split;
+    int64_t kb0, kbn;
+    if (piece < 0) {
+      kb0 = static_cast<int64_t>(split) * g.kb_split;
+      kbn = g.kb_split;
+    } else {
+      kb0 = static_cast<int64_t>(piece) * g.tail_kb;
+      kbn = g.tail_kb;
+    }
+    const int64_t rest = g.kblocks - kb0;
+    const int nkb = static_cast<int>(rest < kbn ? (rest > 0 ? rest : 0) : kbn);
+    body(split, rem / mu, rem % mu, kb0, nkb, piece, u);
   }
 }
 
@@ -358,20 +383,11 @@ __global__ void __launch_bounds__(192, 1) crt8_kernel(const __grid_constant__ Cr
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const uint32_t tmem = *tmem_slot;
 
-  auto item_k = [&](int split, int64_t& kb0, int& nkb) {
-    kb0 = static_cast<int64_t>(split) * g.kb_split;
-    const int64_t rest = g.kblocks - kb0;
-    nkb = static_cast<int>(rest < g.kb_split ? (rest > 0 ? rest : 0) : g.kb_split);
-  };
-
   if (warp == 0) {
     // ------------------------------ bulk-copy producer ------------------------------
     if (lane == 0) {
       uint32_t gk = 0;
-      crt_for_items<PAIR>(g, [&](int split, int mod, int mu) {
-        int64_t kb0;
-        int nkb;
-        item_k(split, kb0, nkb);
+      crt_for_items<PAIR>(g, [&](int, int mod, int mu, int64_t kb0, int nkb, int, int) {
         const int mt = PAIR ? 2 * mu + static_cast<int>(crank) : mu;
         const uint8_t* asrc = g.ad + mod * g.a_plane + (static_cast<int64_t>(mt) * g.kblocks + kb0) * astage;
         const uint8_t* bsrc = g.bd + mod * g.b_plane + kb0 * bstage_g;
@@ -392,10 +408,7 @@ __global__ void __launch_bounds__(192, 1) crt8_kernel(const __grid_constant__ Cr
     // ------------------------------ peer relay: this CTA's stage has landed -> leader ------------------------------
     if (lane == 0) {
       uint32_t gk = 0;
-      crt_for_items<PAIR>(g, [&](int split, int, int) {
-        int64_t kb0;
-        int nkb;
-        item_k(split, kb0, nkb);
+      crt_for_items<PAIR>(g, [&](int, int, int, int64_t, int nkb, int, int) {
         for (int kt = 0; kt < nkb; ++kt, ++gk) {
           const uint32_t s = gk % S;
           mbar_wait(full + s, (gk / S) & 1);
@@ -409,10 +422,7 @@ __global__ void __launch_bounds__(192, 1) crt8_kernel(const __grid_constant__ Cr
     const uint32_t id0 = crt_idesc(g.nc0, PAIR ? 256 : 128), id1 = crt_idesc(g.nc1 > 0 ? g.nc1 : 16, PAIR ? 256 : 128);
     const uint32_t b1off = b0bytes >> 4;
     uint32_t gk = 0, it = 0;
-    crt_for_items<PAIR>(g, [&](int split, int, int) {
-      int64_t kb0;
-      int nkb;
-      item_k(split, kb0, nkb);
+    crt_for_items<PAIR>(g, [&](int, int, int, int64_t, int nkb, int, int) {
       mbar_wait(acc_empty, it & 1);  // drained by the epilogue (of both CTAs)
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
       for (int kt = 0; kt < nkb; ++kt, ++gk) {
@@ -458,14 +468,17 @@ __global__ void __launch_bounds__(192, 1) crt8_kernel(const __grid_constant__ Cr
     };
     release();
     uint32_t it = 0;
-    crt_for_items<PAIR>(g, [&](int split, int mod, int mu) {
-      int64_t kb0;
-      int nkb;
-      item_k(split, kb0, nkb);
+    crt_for_items<PAIR>(g, [&](int split, int mod, int mu, int64_t, int nkb, int piece, int u) {
       const int mt = PAIR ? 2 * mu + static_cast<int>(crank) : mu;
       const uint32_t p = crt_tab.p[mod], magic = crt_tab.magic[mod];
+      const int urow = (PAIR ? static_cast<int>(crank) * kCrtBM : 0) + quad * 32 + lane;  // row inside the unit
       const int64_t m = static_cast<int64_t>(mt) * kCrtBM + quad * 32 + lane;
       uint8_t* orow = g.out + ((static_cast<int64_t>(split) * g.nm + mod) * g.M + m) * g.n16;
+      if (piece > 0) {
+        const int64_t tunits = static_cast<int64_t>(g.nm) * (PAIR ? (g.mtiles + 1) / 2 : g.mtiles) - g.tail_start;
+        orow = g.tail_out + ((static_cast<int64_t>(piece - 1) * tunits + (u - g.tail_start)) *
+                                 (PAIR ? 2 * kCrtBM : kCrtBM) + urow) * g.n16;
+      }
       mbar_wait(acc_full, it & 1);
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
 #pragma unroll 1
@@ -565,6 +578,9 @@ struct CrtOutArgs {
   double* C;
   CMap cmap;
   int perm;            // > 0: store order n = (j % perm) N2 + j / perm (N = perm N2): contiguous runs of C
+  // tail split of the GEMMs (CrtArgs): residues of the K pieces s >= 1 of the units >= tail_start
+  int tail_start, tail_splits, unit_rows, units_per_mod;
+  const uint8_t* tail_res;  // [tail_splits - 1][units - tail_start][unit_rows][n16]
 };
 
 constexpr int kCrtRB = 8;  // rows per block of the reconstruction
@@ -602,6 +618,30 @@ __global__ void __launch_bounds__(256, 3) crt_combine_kernel(const CrtOutArgs g)
             o |= b << (8 * q);
           }
           wv[i] = o;
+        }
+      }
+    }
+    if (g.tail_splits > 1) {
+      // the K pieces of the tail units (the last moduli of the last unit rows) add modulo p_i
+      const int64_t ur = m / g.unit_rows;
+      const int64_t tunits = static_cast<int64_t>(g.nm) * g.units_per_mod - g.tail_start;
+#pragma unroll
+      for (int i = 0; i < kCrtMaxMod; ++i) {
+        const int64_t u = static_cast<int64_t>(i) * g.units_per_mod + ur;
+        if (i < g.nm && u >= g.tail_start) {
+          for (int sp = 1; sp < g.tail_splits; ++sp) {
+            const uint32_t w2 = __ldcs(reinterpret_cast<const uint32_t*>(
+                g.tail_res + ((static_cast<int64_t>(sp - 1) * tunits + (u - g.tail_start)) * g.unit_rows +
+                              (m - ur * g.unit_rows)) * g.n16 + 4 * gq));
+            uint32_t o = 0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              uint32_t b = ((wv[i] >> (8 * q)) & 0xFFu) + ((w2 >> (8 * q)) & 0xFFu);
+              b -= b >= crt_tab.p[i] ? crt_tab.p[i] : 0u;
+              o |= b << (8 * q);
+            }
+            wv[i] = o;
+          }
         }
       }
     }

@@ -690,9 +690,11 @@ inline int crt_splits(int64_t M, int64_t K, int nm) {
 }
 
 struct CrtWs {
-  int64_t bplanes, sb, part, res, total;  // offsets in doubles
+  int64_t bplanes, sb, part, res, tail, total;  // offsets in doubles
   int splits;
   int64_t kb_split;
+  int tail_start, tail_splits, unit_rows, units_per_mod;  // tail split of the last partial wave (CrtArgs)
+  int64_t tail_kb;
 };
 CrtWs crt_ws_layout(int64_t M, int64_t K, int64_t N) {
   const int nm = crt_host().t.nm;
@@ -702,6 +704,27 @@ CrtWs crt_ws_layout(int64_t M, int64_t K, int64_t N) {
   int sp = crt_splits(M, K, nm);
   w.kb_split = (kblocks + sp - 1) / sp;
   w.splits = static_cast<int>((kblocks + w.kb_split - 1) / w.kb_split);
+  // tail split: with one K split and at least one full wave, the units of the last partial wave
+  // are cut into K pieces that fill the wave (TRALS_CRT_TAIL=0 disables)
+  static int tail_on = -1;
+  if (tail_on < 0) tail_on = (std::getenv("TRALS_CRT_TAIL") && std::atoi(std::getenv("TRALS_CRT_TAIL")) == 0) ? 0 : 1;
+  const bool pair = crt_pair();
+  const int slots = pair ? kSMs / 2 : kSMs;
+  w.unit_rows = pair ? 2 * trals::kCrtBM : trals::kCrtBM;
+  w.units_per_mod = static_cast<int>(pair ? (crt_mtiles(M) + 1) / 2 : crt_mtiles(M));
+  const int64_t units = static_cast<int64_t>(nm) * w.units_per_mod * w.splits;
+  w.tail_start = static_cast<int>(units);
+  w.tail_splits = 1;
+  w.tail_kb = kblocks;
+  if (tail_on && w.splits == 1 && units > slots && units % slots != 0) {
+    const int64_t tail = units % slots;
+    int64_t st = std::min<int64_t>({slots / tail, 8, kblocks / 32});
+    if (st >= 2) {
+      w.tail_kb = (kblocks + st - 1) / st;
+      w.tail_splits = static_cast<int>((kblocks + w.tail_kb - 1) / w.tail_kb);
+      w.tail_start = static_cast<int>(units - tail);
+    }
+  }
   int slabs;
   int64_t rps;
   crt_col_slabs(K, N, slabs, rps);
@@ -709,7 +732,9 @@ CrtWs crt_ws_layout(int64_t M, int64_t K, int64_t N) {
   w.sb = w.bplanes + (static_cast<int64_t>(nm) * crt_plane_bytes(n16, K) + 15) / 16 * 2;
   w.part = w.sb + (N + 3) / 4 * 2;
   w.res = w.part + static_cast<int64_t>(slabs) * 2 * N;
-  w.total = w.res + (static_cast<int64_t>(w.splits) * nm * M * n16 + 15) / 16 * 2;
+  w.tail = w.res + (static_cast<int64_t>(w.splits) * nm * M * n16 + 15) / 16 * 2;
+  const int64_t tail_bytes = static_cast<int64_t>(w.tail_splits - 1) * (units - w.tail_start) * w.unit_rows * n16;
+  w.total = w.tail + (tail_bytes + 15) / 16 * 2;
   return w;
 }
 
@@ -795,6 +820,8 @@ int gemm_crt(const int8_t* ad, const int32_t* ea, int64_t M, int64_t K, int64_t 
   g.a_plane = crt_plane_bytes(crt_a_rows_pad(M), K);
   g.b_plane = crt_plane_bytes(n16, K);
   g.ad = reinterpret_cast<const uint8_t*>(ad); g.bd = bd; g.out = res;
+  g.tail_start = w.tail_start; g.tail_splits = w.tail_splits; g.tail_kb = w.tail_kb;
+  g.tail_out = reinterpret_cast<uint8_t*>(ws + w.tail);
   if (stages & 2) {
   const bool pair = crt_pair();
   const int stage = trals::kCrtBM * trals::kCrtBK + n16 * trals::kCrtBK / (pair ? 2 : 1);
@@ -810,7 +837,9 @@ int gemm_crt(const int8_t* ad, const int32_t* ea, int64_t M, int64_t K, int64_t 
     smem_set[pair] = smem;
   }
   if (pair) {
-    const int64_t units = (static_cast<int64_t>(g.mtiles) + 1) / 2 * g.nm * g.splits;
+    const int64_t units = (static_cast<int64_t>(g.mtiles) + 1) / 2 * g.nm * g.splits +
+                          static_cast<int64_t>(w.tail_splits - 1) * ((static_cast<int64_t>(g.mtiles) + 1) / 2 * g.nm -
+                                                                    w.tail_start);
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -847,6 +876,9 @@ int gemm_crt(const int8_t* ad, const int32_t* ea, int64_t M, int64_t K, int64_t 
   o.res = res; o.M = M; o.n16 = n16; o.N = static_cast<int>(N); o.nm = t.nm; o.splits = g.splits;
   o.sa = ea; o.sb = sb; o.C = C; o.cmap = cm;
   o.perm = (cm.N2 > 0 && cm.N2 < N && N % cm.N2 == 0 && cm.sn1 < cm.sn2) ? static_cast<int>(N / cm.N2) : 0;
+  o.tail_start = w.tail_start; o.tail_splits = w.tail_splits; o.unit_rows = w.unit_rows;
+  o.units_per_mod = w.units_per_mod;
+  o.tail_res = reinterpret_cast<const uint8_t*>(ws + w.tail);
   const int64_t cblocks = (M + trals::kCrtRB - 1) / trals::kCrtRB;
   if (cblocks > INT32_MAX) return TRALS_ERR_UNSUPPORTED;
   trals::crt_combine_kernel<<<static_cast<unsigned>(cblocks), 256, trals::kCrtRB * (n16 + 1) * sizeof(double), s>>>(o);

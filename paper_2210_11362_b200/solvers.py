@@ -50,14 +50,16 @@ class AlsConfig:
     reference is ~1e-4 instead of 1e-9.
 
     `fp64_gemm` (extension) selects the engine of the fp64 environment
-    products (the X-streaming MTTSP, solvers.py:379): "ozaki" runs
-    them on the int8 tcgen05 tensor cores over 7 balanced digit slices of X
-    and of the half chain -- 28 exact int32 digit-pair products combined in
-    fp64, with the accuracy of an fp64 product (measured against an
-    extended-precision one) -- "dmma" on the fp64 DMMA pipe, and "auto"
-    (default) picks ozaki when 2 |X| R^2 >= 4 GFLOP (BASELINE c3-c5) and the
-    digit planes fit in free device memory.  X's digit
-    planes (2 x |X| bytes) are made once per call, timed as
+    products (the X-streaming MTTSP, solvers.py:379): "dmma" runs them on the
+    fp64 DMMA pipe; the int8 tcgen05 engine runs them with the accuracy of
+    an fp64 product (measured against an extended-precision one) either as
+    15 modular int8 GEMMs + an exact CRT reconstruction ("crt": contractions
+    of K >= 4096 with R^2 <= 512) or as 28 exact digit-pair products over 7
+    balanced digit slices ("ozaki").  "auto" (default) picks the int8 engine
+    when 2 |X| R^2 >= 4 GFLOP (BASELINE c3-c5), per product the CRT form
+    where it applies, provided the planes fit in free device memory and X
+    passes the dynamic-range guard (include/trals.h).  X's
+    planes (7 or 15 bytes per element and phase) are made once per call, timed as
     upfront_seconds["mttsp"].
     """
 

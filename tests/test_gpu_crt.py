@@ -85,11 +85,12 @@ def _crt_rebuild(res):
     (129, 1000, 1, 20, 20, 0), (1000, 129, 0, 11, 9, 0), (1600, 4000, 0, 8, 8, 0), (4000, 1600, 1, 8, 8, 1),
     (200, 70000, 0, 8, 8, 0), (70000, 150, 1, 6, 8, 0), (640, 640, 0, 20, 20, 1), (260, 5000, 0, 16, 32, 0),
     (131, 4100, 0, 17, 16, 1),
+    (2560, 8192, 0, 20, 20, 0), (6000, 2600, 1, 8, 8, 1),  # more than one wave of work units: tail K split
 ])
 def test_env_crt_matches_f64(pre, post, side, r_lo, r_hi, leaf):
     """CRT environment product against the DMMA one on the same X: tails in every dimension, one and
     two MMA column chunks (R^2 <= 256 / > 256, up to 512 columns), K splits (incl. the forced one for
-    K > 33024), both sides, both CMaps.  The residue planes rebuild rint(2^s x) exactly, with the
+    K > 33024) and the tail K split of the last partial wave, both sides, both CMaps.  The residue planes rebuild rint(2^s x) exactly, with the
     scaled rows inside the 2^58 norm bound (15 moduli); the products agree to the fp64 rounding level."""
     from paper_2210_11362_b200 import _lib as L
     lib = L.lib()
