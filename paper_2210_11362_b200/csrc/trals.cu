@@ -1002,9 +1002,15 @@ inline CMap rowmajor(int64_t ldc) { return CMap{0, 1 << 30, 0, ldc, 1 << 30, 0, 
 struct ResOzWs {
   int64_t adig, aexp, amx, bdig, bexp, bmx, part, total;  // offsets in doubles
 };
-// 32-wide double-buffered n-tiles (c5, K = 400): 14.2 ms against 20 ms for the DMMA residual; the
-// launch streams ~90 GB of digit tiles through L2 (7.5 TB/s), so 64-wide tiles or a grouped
-// tile order that keeps HL's digits L2-resident measured the same
+// 32-wide double-buffered n-tiles (c5, K = 400): 9.9 ms against 20 ms for the DMMA residual.  The
+// launch is bound by what one SM can take in from L2: 465 KB of digit tiles per 128 x 32 output
+// tile, 80 GB per launch = 8.4 TB/s = ~57 GB/s per SM (the env kernels top out at the same
+// 9-10 TB/s).  Measured (round 2): with the level combine stubbed out 9.0 ms (so not the
+// epilogue); a stage-free epilogue with the X loads issued before the accumulator wait 10.2 ms;
+// A stages multicast over clusters of 2 / 4 n-tiles (2.5x fewer L2 reads, same bytes into each
+// SM) 10.9 / 11.6 ms; 64-wide tiles or a grouped tile order: the same.  Fewer bytes per output
+// need wider tiles per A pass -- CTA pairs with 64-wide tiles (TMEM: 7 levels x 64 columns,
+// single-buffered, so 8 epilogue warps) -- not built.
 constexpr int kResBN = 32;
 ResOzWs residual_oz64_layout(int64_t pre, int64_t post, int64_t K) {
   using SC = trals::OzF64;
