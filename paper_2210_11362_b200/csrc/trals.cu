@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <mutex>
 #include <vector>
 
 #include <cudaTypedefs.h>
@@ -600,51 +601,64 @@ struct CrtHost {
   trals::CrtTables t{};
   bool ok = false;
 };
-const CrtHost& crt_host() {
-  static const CrtHost h = [] {
-    CrtHost c;
-    static const uint32_t moduli[trals::kCrtMaxMod] = {
+CrtHost crt_host_build() {
+  CrtHost c;
+  static const uint32_t moduli[trals::kCrtMaxMod] = {
 #define TRALS_CRT_LIST(i, pp) pp,
-        TRALS_CRT_MODULI(TRALS_CRT_LIST)
+      TRALS_CRT_MODULI(TRALS_CRT_LIST)
 #undef TRALS_CRT_LIST
-    };
-    int nm = std::getenv("TRALS_CRT_MODULI") ? std::atoi(std::getenv("TRALS_CRT_MODULI")) : trals::kCrtDefaultMod;
-    nm = std::max(12, std::min(nm, trals::kCrtMaxMod));
-    using u128 = unsigned __int128;
-    u128 P = 1;
-    long double lg = 0;
-    for (int i = 0; i < nm; ++i) {
-      P *= moduli[i];
-      lg += std::log2(static_cast<long double>(moduli[i]));
-    }
-    c.t.nm = nm;
-    for (int j = 0; j < 4; ++j) c.t.P[j] = static_cast<uint32_t>(P >> (32 * j));
-    for (int i = 0; i < trals::kCrtMaxMod; ++i) {
-      const uint32_t p = moduli[i];
-      c.t.p[i] = p;
-      c.t.magic[i] = static_cast<uint32_t>(((1ull << 39) + p - 1) / p);
-      if (i >= nm) continue;
-      const u128 W = P / p;
-      const uint32_t wr = static_cast<uint32_t>(W % p);
-      uint32_t q = 0;
-      for (uint32_t z = 1; z < p; ++z)
-        if ((wr * z) % p == 1) { q = z; break; }
-      if (!q) return c;  // (moduli not coprime: cannot happen)
-      const u128 Wq = W * q;  // = (P / p) q < P: already reduced mod P
-      for (int j = 0; j < 4; ++j) c.t.w[i][j] = static_cast<uint32_t>(Wq >> (32 * j));
-      c.t.fq[i] = static_cast<uint32_t>(std::llround(std::ldexp(static_cast<double>(q) / p, 19)));
-    }
-    // ||a'|| ||b'|| <= 2^(ga+gb) < P / 2; rows are int64 -> each <= 62
-    int gtot = static_cast<int>(std::floor(static_cast<double>(lg) - 1.0 - 0.01));
-    gtot = std::min(gtot, 124);
-    c.t.ga = (gtot + 1) / 2;
-    c.t.gb = gtot / 2;
-    if (!((static_cast<u128>(1) << (c.t.ga + c.t.gb + 1)) < P)) return c;
-    if (cudaMemcpyToSymbol(trals::crt_tab, &c.t, sizeof(c.t)) != cudaSuccess) return c;
-    c.ok = true;
-    return c;
-  }();
-  return h;
+  };
+  int nm = std::getenv("TRALS_CRT_MODULI") ? std::atoi(std::getenv("TRALS_CRT_MODULI")) : trals::kCrtDefaultMod;
+  nm = std::max(12, std::min(nm, trals::kCrtMaxMod));
+  using u128 = unsigned __int128;
+  u128 P = 1;
+  long double lg = 0;
+  for (int i = 0; i < nm; ++i) {
+    P *= moduli[i];
+    lg += std::log2(static_cast<long double>(moduli[i]));
+  }
+  c.t.nm = nm;
+  for (int j = 0; j < 4; ++j) c.t.P[j] = static_cast<uint32_t>(P >> (32 * j));
+  for (int i = 0; i < trals::kCrtMaxMod; ++i) {
+    const uint32_t p = moduli[i];
+    c.t.p[i] = p;
+    c.t.magic[i] = static_cast<uint32_t>(((1ull << 39) + p - 1) / p);
+    if (i >= nm) continue;
+    const u128 W = P / p;
+    const uint32_t wr = static_cast<uint32_t>(W % p);
+    uint32_t q = 0;
+    for (uint32_t z = 1; z < p; ++z)
+      if ((wr * z) % p == 1) { q = z; break; }
+    if (!q) return c;  // (moduli not coprime: cannot happen)
+    const u128 Wq = W * q;  // = (P / p) q < P: already reduced mod P
+    for (int j = 0; j < 4; ++j) c.t.w[i][j] = static_cast<uint32_t>(Wq >> (32 * j));
+    c.t.fq[i] = static_cast<uint32_t>(std::llround(std::ldexp(static_cast<double>(q) / p, 19)));
+  }
+  // ||a'|| ||b'|| <= 2^(ga+gb) < P / 2; rows are int64 -> each <= 62
+  int gtot = static_cast<int>(std::floor(static_cast<double>(lg) - 1.0 - 0.01));
+  gtot = std::min(gtot, 124);
+  c.t.ga = (gtot + 1) / 2;
+  c.t.gb = gtot / 2;
+  if (!((static_cast<u128>(1) << (c.t.ga + c.t.gb + 1)) < P)) return c;
+  if (cudaMemcpyToSymbol(trals::crt_tab, &c.t, sizeof(c.t)) != cudaSuccess) return c;
+  c.ok = true;
+  return c;
+}
+
+// one table set per device (constant memory is per device): built and uploaded on first use
+const CrtHost& crt_host() {
+  constexpr int kMaxDev = 64;
+  static CrtHost tabs[kMaxDev];
+  static bool done[kMaxDev] = {};
+  static std::mutex mu;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDev) dev = 0;
+  std::lock_guard<std::mutex> lock(mu);
+  if (!done[dev]) {
+    tabs[dev] = crt_host_build();
+    done[dev] = true;
+  }
+  return tabs[dev];
 }
 
 inline int crt_n16(int64_t N) { return static_cast<int>((N + 15) / 16 * 16); }
