@@ -428,8 +428,13 @@ __device__ __forceinline__ void oz_for_tiles(const OzArgs& g, F&& body) {
 // CN > 1: launched in clusters of CN along the n-tiles; every CTA loads D / CN of each A stage
 // and multicasts it to the cluster, its own B stage locally; a stage is free once all CN
 // CTAs' MMAs have read it (empty barriers count CN commits).
+// Residual mode runs 8 epilogue warps (two per TMEM lane quarter, alternating 16-column chunks)
+// without the staging buffer: every thread owns one output row.
+template <bool RES>
+constexpr int oz_threads() { return (RES ? 10 : 6) * 32; }
+
 template <int BN, class SC, bool RES = false, int CN = 1>
-__global__ void __launch_bounds__(OzTile<BN, SC>::THREADS, 1)
+__global__ void __launch_bounds__(oz_threads<RES>(), 1)
 oz8_kernel(const __grid_constant__ OzArgs g) {
   // Persistent: CTA b takes tiles b, b + gridDim.x, ...; the smem ring runs across
   // tile boundaries, so the producer prefetches the next tile while the
@@ -457,7 +462,7 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
     }
     for (int b = 0; b < T::ACC; ++b) {
       mbar_init(acc_full + b, 1);
-      mbar_init(acc_empty + b, 4);  // one arrive per epilogue warp
+      mbar_init(acc_empty + b, RES ? 8 : 4);  // one arrive per epilogue warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -565,9 +570,12 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
     // engine uses).  Whole-tile staging releases TMEM before the global stores;
     // chunked staging (large digit stages) stores 16 columns at a time.
     const int quad = warp & 3;
+    constexpr int EH = RES ? 2 : 1;              // epilogue warps per TMEM lane quarter
+    const int half = RES ? (warp - 2) >> 2 : 0;  // residual mode: this warp's 16-column chunks are ci % EH == half
     const uint32_t tlane0 = tmem + (static_cast<uint32_t>(quad * 32) << 16);
     __shared__ int64_t roff_s[kOzBM];  // chunked path: C offsets of the current tile's rows
-    for (int b = 0; b < T::ACC; ++b) tmem_zero<LV * BN>(tlane0 + b * T::ACC_COLS);  // MMAs always accumulate
+    if (half == 0)
+      for (int b = 0; b < T::ACC; ++b) tmem_zero<LV * BN>(tlane0 + b * T::ACC_COLS);  // MMAs always accumulate
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
     __syncwarp();
     if (lane == 0)
@@ -583,10 +591,85 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
       const int64_t nend = (n0 + bw < g.N) ? n0 + bw : g.N;
       const int ab = static_cast<int>(it % T::ACC);
       const uint32_t tlane = tlane0 + ab * T::ACC_COLS;
-      mbar_wait(acc_full + ab, (it / T::ACC) & 1);
-      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
       const int r = quad * 32 + lane;
       const int64_t m = m0 + r;
+      if constexpr (RES) {
+        // Residual mode: every thread owns one output row of the tile, so it reads its own X
+        // entries (whole 128-byte lines per 16-column chunk) -- issued before the wait for the
+        // accumulators, so the DRAM latency overlaps the tile's MMAs -- and needs neither the
+        // staging buffer nor a CTA barrier.  Chunk ci of the tile belongs to the warp with
+        // ci % EH == half of this lane quarter.
+        constexpr int CWR = 16, NCH = BN / CWR / EH;  // chunk width, chunks per warp
+        const bool rok = m < g.M;
+        const double* xrow = g.X + (rok ? m : 0) * g.ldx + n0;
+        const bool vec = ((g.ldx & 1) == 0) && ((reinterpret_cast<uintptr_t>(g.X) & 15u) == 0);
+        double xres[NCH * CWR];
+#pragma unroll
+        for (int j = 0; j < NCH; ++j) {
+          const int c0 = (j * EH + half) * CWR;
+#pragma unroll
+          for (int q = 0; q < CWR; q += 2) {
+            const bool ok0 = rok && c0 + q < bw && n0 + c0 + q < nend;
+            const bool ok1 = rok && c0 + q + 1 < bw && n0 + c0 + q + 1 < nend;
+            if (vec && ok1) {
+              const double2 t = __ldcs(reinterpret_cast<const double2*>(xrow + c0 + q));
+              xres[j * CWR + q] = t.x;
+              xres[j * CWR + q + 1] = t.y;
+            } else {
+              xres[j * CWR + q] = ok0 ? __ldcs(xrow + c0 + q) : 0.0;
+              xres[j * CWR + q + 1] = ok1 ? __ldcs(xrow + c0 + q + 1) : 0.0;
+            }
+          }
+        }
+        mbar_wait(acc_full + ab, (it / T::ACC) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        const double sa = (rok && ktiles > 0) ? ldexp(1.0, g.ea[m]) : 0.0;
+#pragma unroll
+        for (int j = 0; j < NCH; ++j) {
+          const int c0 = (j * EH + half) * CWR;
+          if (c0 < bw) {
+            uint32_t v[LV][CWR];
+#pragma unroll
+            for (int L = 0; L < LV; ++L) tmem_ld16(tlane + L * bw + c0, v[L]);
+            asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+            for (int q = 0; q < CWR; ++q) {
+              constexpr int H = (LV + 1) / 2;
+              int64_t hi = static_cast<int32_t>(v[0][q]), lo = static_cast<int32_t>(v[H][q]);
+#pragma unroll
+              for (int L = 1; L < H; ++L) hi = hi * static_cast<int64_t>(SC::RAD) + static_cast<int32_t>(v[L][q]);
+#pragma unroll
+              for (int L = H + 1; L < LV; ++L) lo = lo * static_cast<int64_t>(SC::RAD) + static_cast<int32_t>(v[L][q]);
+              constexpr double CHI = SC::W0 * oz_rad_pow<SC>(H - 1), CLO = CHI * oz_rad_pow<SC>(LV - H);
+              const double val = fma(static_cast<double>(lo), CLO, static_cast<double>(hi) * CHI);
+              const int64_t n = n0 + c0 + q;
+              if (rok && n < nend) {
+                const int e = g.eb[n];  // (warp-uniform address: one broadcast load)
+                const double sb = static_cast<unsigned>(e + 1022) <= 2045u ? __hiloint2double((e + 1023) << 20, 0)
+                                                                            : ldexp(1.0, e);
+                const double d = xres[j * CWR + q] - (val * sa) * sb;
+                rsum = fma(d, d, rsum);
+              }
+            }
+            // zero this chunk's level accumulators for the next tile (MMAs always accumulate)
+#pragma unroll
+            for (int L = 0; L < LV; ++L)
+              asm volatile(
+                  "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};\n" ::"r"(
+                      tlane + L * bw + c0),
+                  "r"(0u)
+                  : "memory");
+          }
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+        asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(acc_empty + ab);
+        ++it;
+        return;
+      }
+      mbar_wait(acc_full + ab, (it / T::ACC) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
       const double sa = (m < g.M && ktiles > 0) ? ldexp(1.0, g.ea[m]) : 0.0;
       bool part = g.splits > 1;
       bool second = false;  // fix-up: this CTA finishes the tile (adds the other half's partial)
@@ -720,13 +803,16 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
       }
       ++it;
     });
-    if constexpr (RES) {  // fixed-order CTA partial: warp shuffles, then the 4 warps in order
+    if constexpr (RES) {  // fixed-order CTA partial: warp shuffles, then the 8 warps in order
       for (int o = 16; o > 0; o >>= 1) rsum += __shfl_xor_sync(0xffffffffu, rsum, o);
-      double* red = otile;  // free now
-      asm volatile("bar.sync 1, 128;\n" ::: "memory");
-      if (lane == 0) red[quad] = rsum;
-      asm volatile("bar.sync 1, 128;\n" ::: "memory");
-      if (quad == 0 && lane == 0) g.rpart[blockIdx.x] = ((red[0] + red[1]) + red[2]) + red[3];
+      double* red = otile;  // (unused in residual mode)
+      if (lane == 0) red[warp - 2] = rsum;
+      asm volatile("bar.sync 1, 256;\n" ::: "memory");
+      if (warp == 2 && lane == 0) {
+        double t = red[0];
+        for (int w = 1; w < 8; ++w) t += red[w];
+        g.rpart[blockIdx.x] = t;
+      }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");

@@ -496,7 +496,7 @@ int launch_oz(const trals::OzArgs& g, int grid, cudaStream_t s) {
     attr = true;
   }
   if constexpr (CN == 1) {
-    kern<<<grid, T::THREADS, T::SMEM, s>>>(g);
+    kern<<<grid, trals::oz_threads<RES>(), T::SMEM, s>>>(g);
     return launch_status();
   } else {
     cudaLaunchConfig_t cfg = {};
@@ -505,7 +505,7 @@ int launch_oz(const trals::OzArgs& g, int grid, cudaStream_t s) {
     at[0].val.clusterDim.x = CN;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
-    cfg.blockDim = dim3(T::THREADS);
+    cfg.blockDim = dim3(trals::oz_threads<RES>());
     cfg.dynamicSmemBytes = T::SMEM;
     cfg.stream = s;
     cfg.attrs = at;
@@ -1016,15 +1016,15 @@ inline CMap rowmajor(int64_t ldc) { return CMap{0, 1 << 30, 0, ldc, 1 << 30, 0, 
 struct ResOzWs {
   int64_t adig, aexp, amx, bdig, bexp, bmx, part, total;  // offsets in doubles
 };
-// 32-wide double-buffered n-tiles (c5, K = 400): 9.9 ms against 20 ms for the DMMA residual.  The
-// launch is bound by what one SM can take in from L2: 465 KB of digit tiles per 128 x 32 output
-// tile, 80 GB per launch = 8.4 TB/s = ~57 GB/s per SM (the env kernels top out at the same
-// 9-10 TB/s).  Measured (round 2): with the level combine stubbed out 9.0 ms (so not the
-// epilogue); a stage-free epilogue with the X loads issued before the accumulator wait 10.2 ms;
-// A stages multicast over clusters of 2 / 4 n-tiles (2.5x fewer L2 reads, same bytes into each
-// SM) 10.9 / 11.6 ms; 64-wide tiles or a grouped tile order: the same.  Fewer bytes per output
-// need wider tiles per A pass -- CTA pairs with 64-wide tiles (TMEM: 7 levels x 64 columns,
-// single-buffered, so 8 epilogue warps) -- not built.
+// 32-wide double-buffered n-tiles, 8 epilogue warps (c5, K = 400): 7.7 ms against 20 ms for the
+// DMMA residual.  The launch is bound by what one SM can take in from L2: 465 KB of digit tiles
+// per 128 x 32 output tile (7.3 us at ~64 GB/s per SM; 80 GB per launch -- the env kernels top out
+// at the same 9-10 TB/s).  Round-2 measurements on the way: the staged 4-warp epilogue 9.9 ms
+// (9.0 with its level combine stubbed out); the same epilogue without staging or barriers, X
+// loads issued before the accumulator wait, 10.2; with 8 epilogue warps 7.7; 64-wide
+// single-buffered tiles (less to take in, but the epilogue no longer overlaps the MMAs) 7.8; A
+// stages multicast over clusters of 2 / 4 n-tiles (2.5x fewer L2 reads, the same bytes into each
+// SM) 10.9 / 11.6 on the 4-warp form.
 constexpr int kResBN = 32;
 ResOzWs residual_oz64_layout(int64_t pre, int64_t post, int64_t K) {
   using SC = trals::OzF64;
