@@ -433,8 +433,11 @@ __device__ __forceinline__ void oz_for_tiles(const OzArgs& g, F&& body) {
 template <bool RES>
 constexpr int oz_threads() { return (RES ? 10 : 6) * 32; }
 
-template <int BN, class SC, bool RES = false, int CN = 1>
-__global__ void __launch_bounds__(oz_threads<RES>(), 1)
+// W8 (chunked storing epilogue): 8 epilogue warps as well -- the two warps of a lane quarter take
+// alternate 16-column chunks, each half with its own staging buffer and named barrier.  For the
+// short-K shapes (c3, c4), whose tiles spend longer in the epilogue than in their MMAs.
+template <int BN, class SC, bool RES = false, int CN = 1, bool W8 = false>
+__global__ void __launch_bounds__(oz_threads<RES || W8>(), 1)
 oz8_kernel(const __grid_constant__ OzArgs g) {
   // Persistent: CTA b takes tiles b, b + gridDim.x, ...; the smem ring runs across
   // tile boundaries, so the producer prefetches the next tile while the
@@ -444,8 +447,10 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
   constexpr int D = SC::D, LV = SC::LV;
   extern __shared__ uint8_t smraw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+  static_assert(!W8 || (T::CHUNKED && !RES), "W8 is the chunked storing epilogue on 8 warps");
+  constexpr int OUTB = (W8 ? 2 : 1) * T::OUT_BYTES;            // one staging buffer per epilogue half
   double* otile = reinterpret_cast<double*>(sm + S * T::STAGE);  // [kOzBM][OUT_LD] epilogue staging
-  uint64_t* full = reinterpret_cast<uint64_t*>(sm + S * T::STAGE + T::OUT_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + S * T::STAGE + OUTB);
   uint64_t* empty = full + S;
   uint64_t* acc_full = empty + S;          // [ACC]
   uint64_t* acc_empty = acc_full + T::ACC;  // [ACC]
@@ -462,7 +467,7 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
     }
     for (int b = 0; b < T::ACC; ++b) {
       mbar_init(acc_full + b, 1);
-      mbar_init(acc_empty + b, RES ? 8 : 4);  // one arrive per epilogue warp
+      mbar_init(acc_empty + b, (RES || W8) ? 8 : 4);  // one arrive per epilogue warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -570,10 +575,21 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
     // engine uses).  Whole-tile staging releases TMEM before the global stores;
     // chunked staging (large digit stages) stores 16 columns at a time.
     const int quad = warp & 3;
-    constexpr int EH = RES ? 2 : 1;              // epilogue warps per TMEM lane quarter
-    const int half = RES ? (warp - 2) >> 2 : 0;  // residual mode: this warp's 16-column chunks are ci % EH == half
+    constexpr int EH = (RES || W8) ? 2 : 1;              // epilogue warps per TMEM lane quarter
+    const int half = (RES || W8) ? (warp - 2) >> 2 : 0;  // this warp's 16-column chunks are ci % EH == half
     const uint32_t tlane0 = tmem + (static_cast<uint32_t>(quad * 32) << 16);
-    __shared__ int64_t roff_s[kOzBM];  // chunked path: C offsets of the current tile's rows
+    __shared__ int64_t roff_all[W8 ? 2 : 1][kOzBM];  // chunked path: C offsets of the current tile's rows
+    int64_t* roff_s = roff_all[W8 ? half : 0];
+    double* otile_h = otile + (W8 ? half : 0) * (T::OUT_BYTES / 8);  // this half's staging buffer
+    // named barriers: one per epilogue half (128 threads), one across both halves (fix-up ticket)
+    auto bar_half = [&]() {
+      if (W8 && half == 1) asm volatile("bar.sync 2, 128;\n" ::: "memory");
+      else asm volatile("bar.sync 1, 128;\n" ::: "memory");
+    };
+    auto bar_all = [&]() {
+      if constexpr (W8) asm volatile("bar.sync 3, 256;\n" ::: "memory");
+      else asm volatile("bar.sync 1, 128;\n" ::: "memory");
+    };
     if (half == 0)
       for (int b = 0; b < T::ACC; ++b) tmem_zero<LV * BN>(tlane0 + b * T::ACC_COLS);  // MMAs always accumulate
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
@@ -676,7 +692,7 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
       const int tile = mt * g.ntiles + nt;
       if (T::CHUNKED && g.fixup) {
         __shared__ int ticket_s;
-        if (quad == 0 && lane == 0) {
+        if (half == 0 && quad == 0 && lane == 0) {
           const int tk = atomicAdd(g.tickets + tile, 1);
           if (tk == 1) {
             while (atomicAdd(g.ready + tile, 0) == 0) __nanosleep(200);
@@ -684,7 +700,7 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
           }
           ticket_s = tk;
         }
-        asm volatile("bar.sync 1, 128;\n" ::: "memory");
+        bar_all();
         second = ticket_s == 1;
         part = !second;
       }
@@ -706,7 +722,7 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
       constexpr int NIT = kOzBM / (4 * RPW);    // store iterations per chunk
       const int cl = lane % CW, rsub = lane / CW;
 #pragma unroll 1
-      for (int c0 = 0; c0 < bw; c0 += CW) {
+      for (int c0 = half * CW; c0 < bw; c0 += EH * CW) {
         uint32_t v[LV][CW];
 #pragma unroll
         for (int L = 0; L < LV; ++L) tmem_ldc<CW>(tlane + L * bw + c0, v[L]);
@@ -727,11 +743,11 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
           // range do not lose bits to a subnormal scale factor
           constexpr double CHI = SC::W0 * oz_rad_pow<SC>(H - 1), CLO = CHI * oz_rad_pow<SC>(LV - H);
           const double val = fma(static_cast<double>(lo), CLO, static_cast<double>(hi) * CHI);
-          otile[r * T::OUT_LD + oc + q] = val * sa;
+          otile_h[r * T::OUT_LD + oc + q] = val * sa;
         }
         if constexpr (T::CHUNKED) {
           // store this CW-column chunk: lane -> (row rsub, column cl), warp -> rows quad*RPW + ...
-          asm volatile("bar.sync 1, 128;\n" ::: "memory");
+          bar_half();
           const int64_t n = n0 + c0 + cl;
           const bool nok = n < nend;
           const uint32_t un = static_cast<uint32_t>(n);
@@ -756,7 +772,7 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
             const int rr = quad * RPW + rsub + 4 * RPW * k;
             if (rr >= rows) break;
             const int64_t roff = roff_s[rr];
-            const double o = otile[rr * T::OUT_LD + cl] * sb + pv[k];
+            const double o = otile_h[rr * T::OUT_LD + cl] * sb + pv[k];
             if constexpr (RES) {
               if (nok) {
                 const double d = xv[k] - o;
@@ -766,15 +782,29 @@ oz8_kernel(const __grid_constant__ OzArgs g) {
               if (nok) base[roff + coff] = o;
             }
           }
-          asm volatile("bar.sync 1, 128;\n" ::: "memory");
+          bar_half();
         }
       }
       if (T::CHUNKED && g.fixup && part) {  // publish this half's partial
         __threadfence();
-        asm volatile("bar.sync 1, 128;\n" ::: "memory");
-        if (quad == 0 && lane == 0) atomicExch(g.ready + tile, 1);
+        bar_all();
+        if (half == 0 && quad == 0 && lane == 0) atomicExch(g.ready + tile, 1);
       }
-      tmem_zero<LV * BN>(tlane);
+      if constexpr (W8) {
+        // each half zeroes the level accumulators of its own chunks
+        for (int c0 = half * CW; c0 < bw; c0 += EH * CW) {
+#pragma unroll
+          for (int L = 0; L < LV; ++L)
+            asm volatile(
+                "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};\n" ::"r"(
+                    tlane + L * bw + c0),
+                "r"(0u)
+                : "memory");
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+      } else {
+        tmem_zero<LV * BN>(tlane);
+      }
       asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(acc_empty + ab);  // the MMA warp may reuse this buffer

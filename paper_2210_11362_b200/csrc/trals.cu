@@ -486,17 +486,19 @@ int launch_colmax(const T* x, int64_t rows, int64_t cols, int64_t ld, double* ou
   return launch_status();
 }
 
-template <int BN, class SC, bool RES = false, int CN = 1>
+template <int BN, class SC, bool RES = false, int CN = 1, bool W8 = false>
 int launch_oz(const trals::OzArgs& g, int grid, cudaStream_t s) {
   using T = trals::OzTile<BN, SC>;
-  auto kern = trals::oz8_kernel<BN, SC, RES, CN>;
+  auto kern = trals::oz8_kernel<BN, SC, RES, CN, W8>;
+  constexpr size_t kSmem = T::SMEM + (W8 ? T::OUT_BYTES : 0);  // W8: a staging buffer per epilogue half
+  static_assert(kSmem <= 227 * 1024, "shared memory of the int8 kernel");
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(T::SMEM));
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmem));
     attr = true;
   }
   if constexpr (CN == 1) {
-    kern<<<grid, trals::oz_threads<RES>(), T::SMEM, s>>>(g);
+    kern<<<grid, trals::oz_threads<RES || W8>(), kSmem, s>>>(g);
     return launch_status();
   } else {
     cudaLaunchConfig_t cfg = {};
@@ -505,8 +507,8 @@ int launch_oz(const trals::OzArgs& g, int grid, cudaStream_t s) {
     at[0].val.clusterDim.x = CN;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
-    cfg.blockDim = dim3(trals::oz_threads<RES>());
-    cfg.dynamicSmemBytes = T::SMEM;
+    cfg.blockDim = dim3(trals::oz_threads<RES || W8>());
+    cfg.dynamicSmemBytes = kSmem;
     cfg.stream = s;
     cfg.attrs = at;
     cfg.numAttrs = 1;
@@ -577,7 +579,18 @@ int gemm_oz(const int8_t* ad, const int32_t* ea, int64_t M, int64_t K, int64_t N
   int st = TRALS_ERR_UNSUPPORTED;
   if (cn == 4) st = bn == 32 ? launch_oz<32, SC, false, 4>(g, grid, s) : launch_oz<kOzBN, SC, false, 4>(g, grid, s);
   if (cn == 2) st = bn == 32 ? launch_oz<32, SC, false, 2>(g, grid, s) : launch_oz<kOzBN, SC, false, 2>(g, grid, s);
-  if (cn == 1) st = bn == 32 ? launch_oz<32, SC>(g, grid, s) : launch_oz<kOzBN, SC>(g, grid, s);
+  // short K (c3, c4): the tiles spend longer in the epilogue than in their MMAs -> 8 epilogue warps
+  // (TRALS_OZ_W8=0, experiments: the 4-warp form everywhere)
+  static int w8 = -1;
+  if (w8 < 0) w8 = (std::getenv("TRALS_OZ_W8") && std::atoi(std::getenv("TRALS_OZ_W8")) == 0) ? 0 : 1;
+  bool done = false;
+  if constexpr (SC::BAL) {
+    if (cn == 1 && w8 && K < kOzShortK) {
+      st = bn == 32 ? launch_oz<32, SC, false, 1, true>(g, grid, s) : launch_oz<kOzBN, SC, false, 1, true>(g, grid, s);
+      done = true;
+    }
+  }
+  if (cn == 1 && !done) st = bn == 32 ? launch_oz<32, SC>(g, grid, s) : launch_oz<kOzBN, SC>(g, grid, s);
   if (st) return st;
   if (sp.splits > 1 && !g.fixup) {
     GemmArgs r{};
