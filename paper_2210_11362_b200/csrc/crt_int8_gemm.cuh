@@ -578,10 +578,50 @@ struct CrtOutArgs {
   double* C;
   CMap cmap;
   int perm;            // > 0: store order n = (j % perm) N2 + j / perm (N = perm N2): contiguous runs of C
-  // tail split of the GEMMs (CrtArgs): residues of the K pieces s >= 1 of the units >= tail_start
-  int tail_start, tail_splits, unit_rows, units_per_mod;
-  const uint8_t* tail_res;  // [tail_splits - 1][units - tail_start][unit_rows][n16]
 };
+
+// Tail split of the GEMMs (CrtArgs): adds the residues of the K pieces s >= 1 of the units
+// >= tail_start into the units' rows of the main residue planes, modulo p_i (a few MB; runs before
+// the reconstruction).  One thread per (tail unit, row of the unit, 4 columns).
+struct CrtTailArgs {
+  uint8_t* res;             // [nm][M][n16] (one K split)
+  const uint8_t* tail_res;  // [tail_splits - 1][tail units][unit_rows][n16]
+  int64_t M;
+  int n16, nm, tail_start, tail_splits, unit_rows, units_per_mod;
+};
+
+__global__ void __launch_bounds__(256) crt_tail_merge_kernel(const CrtTailArgs g) {
+  const int groups = g.n16 / 4;
+  const int64_t tunits = static_cast<int64_t>(g.nm) * g.units_per_mod - g.tail_start;
+  const int64_t total = tunits * g.unit_rows * groups;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int gq = static_cast<int>(e % groups);
+    const int64_t ur = e / groups;
+    const int row = static_cast<int>(ur % g.unit_rows);
+    const int64_t tu = ur / g.unit_rows;
+    const int64_t u = g.tail_start + tu;
+    const int mod = static_cast<int>(u / g.units_per_mod);
+    const int64_t m = (u % g.units_per_mod) * g.unit_rows + row;
+    if (m >= g.M) continue;
+    uint32_t* dst = reinterpret_cast<uint32_t*>(g.res + (static_cast<int64_t>(mod) * g.M + m) * g.n16 + 4 * gq);
+    uint32_t w = *dst;
+    const uint32_t p = crt_tab.p[mod];
+    for (int sp = 1; sp < g.tail_splits; ++sp) {
+      const uint32_t w2 = __ldcs(reinterpret_cast<const uint32_t*>(
+          g.tail_res + ((static_cast<int64_t>(sp - 1) * tunits + tu) * g.unit_rows + row) * g.n16 + 4 * gq));
+      uint32_t o = 0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint32_t b = ((w >> (8 * q)) & 0xFFu) + ((w2 >> (8 * q)) & 0xFFu);
+        b -= b >= p ? p : 0u;
+        o |= b << (8 * q);
+      }
+      w = o;
+    }
+    *dst = w;
+  }
+}
 
 constexpr int kCrtRB = 8;  // rows per block of the reconstruction
 
@@ -618,30 +658,6 @@ __global__ void __launch_bounds__(256, 3) crt_combine_kernel(const CrtOutArgs g)
             o |= b << (8 * q);
           }
           wv[i] = o;
-        }
-      }
-    }
-    if (g.tail_splits > 1) {
-      // the K pieces of the tail units (the last moduli of the last unit rows) add modulo p_i
-      const int64_t ur = m / g.unit_rows;
-      const int64_t tunits = static_cast<int64_t>(g.nm) * g.units_per_mod - g.tail_start;
-#pragma unroll
-      for (int i = 0; i < kCrtMaxMod; ++i) {
-        const int64_t u = static_cast<int64_t>(i) * g.units_per_mod + ur;
-        if (i < g.nm && u >= g.tail_start) {
-          for (int sp = 1; sp < g.tail_splits; ++sp) {
-            const uint32_t w2 = __ldcs(reinterpret_cast<const uint32_t*>(
-                g.tail_res + ((static_cast<int64_t>(sp - 1) * tunits + (u - g.tail_start)) * g.unit_rows +
-                              (m - ur * g.unit_rows)) * g.n16 + 4 * gq));
-            uint32_t o = 0;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              uint32_t b = ((wv[i] >> (8 * q)) & 0xFFu) + ((w2 >> (8 * q)) & 0xFFu);
-              b -= b >= crt_tab.p[i] ? crt_tab.p[i] : 0u;
-              o |= b << (8 * q);
-            }
-            wv[i] = o;
-          }
         }
       }
     }

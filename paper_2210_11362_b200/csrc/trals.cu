@@ -899,13 +899,20 @@ int gemm_crt(const int8_t* ad, const int32_t* ea, int64_t M, int64_t K, int64_t 
   if (int st = launch_status()) return st;
   }
   if (!(stages & 4)) return TRALS_OK;
+  if (w.tail_splits > 1) {  // fold the tail units' K pieces into the main residue planes
+    trals::CrtTailArgs ta{};
+    ta.res = res; ta.tail_res = reinterpret_cast<const uint8_t*>(ws + w.tail); ta.M = M; ta.n16 = n16; ta.nm = t.nm;
+    ta.tail_start = w.tail_start; ta.tail_splits = w.tail_splits; ta.unit_rows = w.unit_rows;
+    ta.units_per_mod = w.units_per_mod;
+    const int64_t work = (static_cast<int64_t>(t.nm) * w.units_per_mod - w.tail_start) * w.unit_rows * (n16 / 4);
+    const int blocks = static_cast<int>(std::min<int64_t>((work + 255) / 256, 8 * kSMs));
+    trals::crt_tail_merge_kernel<<<blocks, 256, 0, s>>>(ta);
+    if (int st = launch_status()) return st;
+  }
   trals::CrtOutArgs o{};
   o.res = res; o.M = M; o.n16 = n16; o.N = static_cast<int>(N); o.nm = t.nm; o.splits = g.splits;
   o.sa = ea; o.sb = sb; o.C = C; o.cmap = cm;
   o.perm = (cm.N2 > 0 && cm.N2 < N && N % cm.N2 == 0 && cm.sn1 < cm.sn2) ? static_cast<int>(N / cm.N2) : 0;
-  o.tail_start = w.tail_start; o.tail_splits = w.tail_splits; o.unit_rows = w.unit_rows;
-  o.units_per_mod = w.units_per_mod;
-  o.tail_res = reinterpret_cast<const uint8_t*>(ws + w.tail);
   const int64_t cblocks = (M + trals::kCrtRB - 1) / trals::kCrtRB;
   if (cblocks > INT32_MAX) return TRALS_ERR_UNSUPPORTED;
   trals::crt_combine_kernel<<<static_cast<unsigned>(cblocks), 256, trals::kCrtRB * (n16 + 1) * sizeof(double), s>>>(o);
