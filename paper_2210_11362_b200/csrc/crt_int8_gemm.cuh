@@ -23,8 +23,8 @@
 // So the result is the correctly rounded exact product of the rounded operands: the only
 // error is the rint() of step 1.
 //
-// Kernel (crt8_kernel): persistent, one CTA per SM; a work item is (K split, modulus,
-// 128-row m-tile) x all N <= 512 columns: the whole N lives in TMEM (N int32 columns), so
+// Kernel (crt8_kernel): persistent, one CTA per SM (in CTA pairs, below); a work item is (K split,
+// modulus, 128-row m-tile) x all N <= 512 columns: the whole N lives in TMEM (N int32 columns), so
 // every A byte is read from HBM once per launch and the MMAs are 128 x {<= 256} x 32
 // (two per 32 k for N = 400: 208 + 192).  Items are ordered modulus-major, so the CTAs
 // share one B plane (K x N bytes, L2 resident) at a time.  Roles as in oz8_kernel: bulk-copy
