@@ -141,7 +141,7 @@ __global__ void __launch_bounds__(256) dd_chol_diag_kernel(double* __restrict__ 
                                                            int p, double* __restrict__ R0, double* __restrict__ Ihi,
                                                            double* __restrict__ Ilo) {
   __shared__ ddv a[kDdNB][kDdNB + 1], x[kDdNB][kDdNB + 1];
-  __shared__ int zero_row[kDdNB];
+  __shared__ ddv rinv[kDdNB];  // 1 / r_jj (0 for a zero row)
   const int pb = min(kDdNB, m - p);
   for (int t = threadIdx.x; t < kDdNB * kDdNB; t += blockDim.x) {
     const int r = t / kDdNB, c = t % kDdNB;
@@ -150,38 +150,65 @@ __global__ void __launch_bounds__(256) dd_chol_diag_kernel(double* __restrict__ 
     x[r][c] = {0.0, 0.0};
   }
   __syncthreads();
-  // right-looking within the block: column j's pivot, row j scaled, trailing rows updated
+  // Right-looking within the block, one barrier per pivot: every thread derives the pivot's root and
+  // its dd reciprocal from a[j][j] itself (no broadcast round trip), then updates its share of the
+  // trailing elements from the unscaled row: a[r][c] -= (a[j][r] / d_j) a[j][c]; the threads of row j
+  // leave the scaled row r_jc = a[j][c] / r_jj behind.  (Multiplying by the dd reciprocal instead of
+  // dividing costs ~2^-104 per element, the level of every other operation here.)
   for (int j = 0; j < pb; ++j) {
-    __shared__ ddv piv;
-    if (threadIdx.x == 0) {
-      const ddv d = a[j][j];
-      const bool z = !(d.hi > 0.0);
-      zero_row[j] = z;
-      piv = z ? ddv{0.0, 0.0} : dd_sqrt(d);
+    const ddv d = a[j][j];
+    const bool z = !(d.hi > 0.0);
+    ddv rjj{0.0, 0.0}, ri{0.0, 0.0}, di{0.0, 0.0};
+    if (!z) {
+      // sqrt(d) and 1 / sqrt(d) in dd from one fp64 rsqrt and one Newton step each (no fp64
+      // division or sqrt on the pivot chain: ~200 instead of ~800 cycles)
+      const double y = rsqrt(d.hi);  // 1 / sqrt(d) to ~2^-52
+      const double r0 = d.hi * y;    // sqrt(d) to ~2^-52
+      const double r0sq = r0 * r0;
+      const ddv e = dd_add(d, ddv{-r0sq, -fma(r0, r0, -r0sq)});  // d - r0^2, exact product
+      rjj = dd_quick(r0, e.hi * (0.5 * y));                        // r0 + (d - r0^2) / (2 r0)
+      const ddv t = dd_mul(rjj, ddv{y, 0.0});                      // r y = 1 + O(2^-52)
+      const ddv e2 = dd_add(ddv{1.0, 0.0}, dd_neg(t));
+      ri = dd_quick(y, e2.hi * y);                                 // y (2 - r y)
+      di = dd_mul(ri, ri);                                         // 1 / d_j
     }
-    __syncthreads();
-    const ddv rjj = piv;
-    const bool z = zero_row[j];
-    for (int c = j + threadIdx.x; c < pb; c += blockDim.x) a[j][c] = z ? ddv{0.0, 0.0} : (c == j ? rjj : dd_div(a[j][c], rjj));
-    __syncthreads();
     const int rem = pb - j - 1;
-    for (int t = threadIdx.x; t < rem * rem; t += blockDim.x) {
+    // trailing update first (reads row j unscaled), in registers; written after the barrier below
+    ddv upd[4];
+    int nupd = 0;
+    for (int t = threadIdx.x; t < rem * rem; t += blockDim.x, ++nupd) {
       const int r = j + 1 + t / rem, c = j + 1 + t % rem;
-      if (c >= r) a[r][c] = dd_add(a[r][c], dd_neg(dd_mul(a[j][r], a[j][c])));
+      upd[nupd] = (c >= r && !z) ? dd_add(a[r][c], dd_neg(dd_mul(dd_mul(a[j][r], di), a[j][c]))) : a[r][c];
     }
+    ddv rowv{0.0, 0.0};
+    const int cj = j + threadIdx.x;
+    if (cj < pb) rowv = z ? ddv{0.0, 0.0} : (cj == j ? rjj : dd_mul(a[j][cj], ri));
+    __syncthreads();
+    nupd = 0;
+    for (int t = threadIdx.x; t < rem * rem; t += blockDim.x, ++nupd) {
+      const int r = j + 1 + t / rem, c = j + 1 + t % rem;
+      if (c >= r) a[r][c] = upd[nupd];
+    }
+    if (cj < pb) a[j][cj] = rowv;
+    if (threadIdx.x == 0) rinv[j] = ri;
     __syncthreads();
   }
-  // inverse of the upper block (zero rows stay zero: their inverse rows are not used by the panel
-  // update since the corresponding R0 rows are zero too)
+  // inverse of the upper block, rows bottom-up; 8 threads per column split the inner sum (fixed
+  // order: partial sums by l mod 8, then a shuffle tree).  Zero rows stay zero: their inverse rows
+  // are not used by the panel update since the corresponding R0 rows are zero too.
+  const int col = threadIdx.x >> 3, part = threadIdx.x & 7;  // 32 columns x 8 parts
   for (int i = pb - 1; i >= 0; --i) {
-    for (int c = i + threadIdx.x; c < pb; c += blockDim.x) {
-      if (zero_row[i]) {
-        x[i][c] = {0.0, 0.0};
-        continue;
-      }
-      ddv acc = (c == i) ? ddv{1.0, 0.0} : ddv{0.0, 0.0};
-      for (int l = i + 1; l <= c; ++l) acc = dd_add(acc, dd_neg(dd_mul(a[i][l], x[l][c])));
-      x[i][c] = dd_div(acc, a[i][i]);
+    ddv acc{0.0, 0.0};
+    if (col < pb && col >= i)
+      for (int l = i + 1 + part; l <= col; l += 8) acc = dd_add(acc, dd_neg(dd_mul(a[i][l], x[l][col])));
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) {
+      const ddv other{__shfl_xor_sync(0xffffffffu, acc.hi, o), __shfl_xor_sync(0xffffffffu, acc.lo, o)};
+      acc = dd_add(acc, other);
+    }
+    if (part == 0 && col < pb && col >= i) {
+      if (col == i) acc = dd_add(acc, {1.0, 0.0});
+      x[i][col] = dd_mul(acc, rinv[i]);  // (rinv = 0 for a zero row)
     }
     __syncthreads();
   }
