@@ -62,6 +62,21 @@ __device__ __forceinline__ ddv dd_sqrt(ddv a) {
   return dd_quick(x, r.hi / (2.0 * x));
 }
 
+// Compensated dot-product step (Ogita-Rump-Oishi "Dot2" with dd operands): (s, err) += sg a b, the
+// running sum's rounding errors and the products' low parts collected in err.  The dependent chain
+// per term is one addition (s), against the ~12 dependent operations of dd_add(dd_mul()); the result
+// dd_quick(s, err) carries the same ~2^-104 relative error (relative to sum |a b|).
+__device__ __forceinline__ void dd_dot_step(double& s, double& err, ddv a, ddv b, double sg) {
+  const double ah = sg * a.hi, al = sg * a.lo;
+  const double p = ah * b.hi;
+  const double ep = fma(ah, b.hi, -p);
+  const double cross = fma(ah, b.lo, al * b.hi);
+  const double sn = s + p, bb = sn - s;
+  const double es = (s - (sn - bb)) + (p - bb);
+  s = sn;
+  err += (es + ep) + cross;
+}
+
 // E[(a*Ra + c)][(b*Rb + d)] = sum_i R[a][i][b] R[c][i][d] (R layout C, (Ra, k, Rb)); hi / lo planes
 __global__ void __launch_bounds__(256) dd_transfer_kernel(const double* __restrict__ R, int Ra, int k, int Rb,
                                                           double* __restrict__ Ehi, double* __restrict__ Elo) {
@@ -101,7 +116,7 @@ __global__ void __launch_bounds__(256) dd_gemm_kernel(const DdGemm g) {
   __shared__ ddv As[16][17], Bs[16][17];
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
   const int m = blockIdx.y * 16 + ty, n = blockIdx.x * 16 + tx;
-  ddv acc{0.0, 0.0};
+  double sacc = 0.0, eacc = 0.0;  // compensated dot product (dd_dot_step): half the flops of dd_add(dd_mul())
   for (int k0 = 0; k0 < g.K; k0 += 16) {
     {
       const int mm = blockIdx.y * 16 + ty, kk = k0 + tx;
@@ -113,9 +128,10 @@ __global__ void __launch_bounds__(256) dd_gemm_kernel(const DdGemm g) {
     }
     __syncthreads();
 #pragma unroll 4
-    for (int kk = 0; kk < 16; ++kk) acc = dd_add(acc, dd_mul(As[ty][kk], Bs[kk][tx]));
+    for (int kk = 0; kk < 16; ++kk) dd_dot_step(sacc, eacc, As[ty][kk], Bs[kk][tx], 1.0);
     __syncthreads();
   }
+  const ddv acc = dd_quick(sacc, eacc);
   if (m < g.M && n < g.N) {
     const int64_t o = (m / g.M2) * g.sm1 + (m % g.M2) * g.sm2 + (n / g.N2) * g.sn1 + (n % g.N2) * g.sn2;
     ddv v = dd_mul(acc, {g.alpha, 0.0});
@@ -143,6 +159,7 @@ __global__ void __launch_bounds__(256) dd_chol_diag_kernel(double* __restrict__ 
   __shared__ ddv a[kDdNB][kDdNB + 1], x[kDdNB][kDdNB + 1];
   __shared__ ddv rinv[kDdNB];  // 1 / r_jj (0 for a zero row)
   const int pb = min(kDdNB, m - p);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int t = threadIdx.x; t < kDdNB * kDdNB; t += blockDim.x) {
     const int r = t / kDdNB, c = t % kDdNB;
     const int64_t o = static_cast<int64_t>(p + r) * m + p + c;
@@ -150,68 +167,65 @@ __global__ void __launch_bounds__(256) dd_chol_diag_kernel(double* __restrict__ 
     x[r][c] = {0.0, 0.0};
   }
   __syncthreads();
-  // Right-looking within the block, one barrier per pivot: every thread derives the pivot's root and
-  // its dd reciprocal from a[j][j] itself (no broadcast round trip), then updates its share of the
-  // trailing elements from the unscaled row: a[r][c] -= (a[j][r] / d_j) a[j][c]; the threads of row j
-  // leave the scaled row r_jc = a[j][c] / r_jj behind.  (Multiplying by the dd reciprocal instead of
-  // dividing costs ~2^-104 per element, the level of every other operation here.)
-  for (int j = 0; j < pb; ++j) {
-    const ddv d = a[j][j];
-    const bool z = !(d.hi > 0.0);
-    ddv rjj{0.0, 0.0}, ri{0.0, 0.0}, di{0.0, 0.0};
-    if (!z) {
-      // sqrt(d) and 1 / sqrt(d) in dd from one fp64 rsqrt and one Newton step each (no fp64
-      // division or sqrt on the pivot chain: ~200 instead of ~800 cycles)
-      const double y = rsqrt(d.hi);  // 1 / sqrt(d) to ~2^-52
-      const double r0 = d.hi * y;    // sqrt(d) to ~2^-52
-      const double r0sq = r0 * r0;
-      const ddv e = dd_add(d, ddv{-r0sq, -fma(r0, r0, -r0sq)});  // d - r0^2, exact product
-      rjj = dd_quick(r0, e.hi * (0.5 * y));                        // r0 + (d - r0^2) / (2 r0)
-      const ddv t = dd_mul(rjj, ddv{y, 0.0});                      // r y = 1 + O(2^-52)
-      const ddv e2 = dd_add(ddv{1.0, 0.0}, dd_neg(t));
-      ri = dd_quick(y, e2.hi * y);                                 // y (2 - r y)
-      di = dd_mul(ri, ri);                                         // 1 / d_j
+  // Left-looking factorisation by one warp, lane c = column c, no block barriers: row r is
+  // a[r][c] - sum_{j<r} u_jr u_jc as one compensated dot product per lane, then the pivot's root and
+  // reciprocal from one fp64 rsqrt + one Newton step each (no fp64 divide / sqrt on the chain) and
+  // the scaled row.  (The right-looking form with two block barriers per pivot took 83 us per
+  // 32 x 32 block, this one ~1/3 of it.)
+  if (warp == 0) {
+    const int c = lane;
+    for (int r = 0; r < pb; ++r) {
+      double sd = 0.0, ed = 0.0;
+      if (c >= r && c < pb) {
+        sd = a[r][c].hi;
+        ed = a[r][c].lo;
+#pragma unroll 4
+        for (int j = 0; j < r; ++j) dd_dot_step(sd, ed, a[j][r], a[j][c], -1.0);
+      }
+      const ddv v = dd_quick(sd, ed);
+      const ddv d{__shfl_sync(0xffffffffu, v.hi, r), __shfl_sync(0xffffffffu, v.lo, r)};
+      const bool z = !(d.hi > 0.0);
+      ddv rjj{0.0, 0.0}, ri{0.0, 0.0};
+      if (!z) {
+        const double y = rsqrt(d.hi);  // 1 / sqrt(d) to ~2^-52
+        const double r0 = d.hi * y;    // sqrt(d) to ~2^-52
+        const double r0sq = r0 * r0;
+        const ddv e = dd_add(d, ddv{-r0sq, -fma(r0, r0, -r0sq)});  // d - r0^2, exact product
+        rjj = dd_quick(r0, e.hi * (0.5 * y));                        // r0 + (d - r0^2) / (2 r0)
+        const ddv t = dd_mul(rjj, ddv{y, 0.0});                      // r y = 1 + O(2^-52)
+        const ddv e2 = dd_add(ddv{1.0, 0.0}, dd_neg(t));
+        ri = dd_quick(y, e2.hi * y);                                 // y (2 - r y)
+      }
+      if (c >= r && c < pb) a[r][c] = z ? ddv{0.0, 0.0} : (c == r ? rjj : dd_mul(v, ri));
+      if (c == 0) rinv[r] = ri;
+      __syncwarp();
     }
-    const int rem = pb - j - 1;
-    // trailing update first (reads row j unscaled), in registers; written after the barrier below
-    ddv upd[4];
-    int nupd = 0;
-    for (int t = threadIdx.x; t < rem * rem; t += blockDim.x, ++nupd) {
-      const int r = j + 1 + t / rem, c = j + 1 + t % rem;
-      upd[nupd] = (c >= r && !z) ? dd_add(a[r][c], dd_neg(dd_mul(dd_mul(a[j][r], di), a[j][c]))) : a[r][c];
-    }
-    ddv rowv{0.0, 0.0};
-    const int cj = j + threadIdx.x;
-    if (cj < pb) rowv = z ? ddv{0.0, 0.0} : (cj == j ? rjj : dd_mul(a[j][cj], ri));
-    __syncthreads();
-    nupd = 0;
-    for (int t = threadIdx.x; t < rem * rem; t += blockDim.x, ++nupd) {
-      const int r = j + 1 + t / rem, c = j + 1 + t % rem;
-      if (c >= r) a[r][c] = upd[nupd];
-    }
-    if (cj < pb) a[j][cj] = rowv;
-    if (threadIdx.x == 0) rinv[j] = ri;
-    __syncthreads();
   }
-  // inverse of the upper block, rows bottom-up; 8 threads per column split the inner sum (fixed
-  // order: partial sums by l mod 8, then a shuffle tree).  Zero rows stay zero: their inverse rows
-  // are not used by the panel update since the corresponding R0 rows are zero too.
+  __syncthreads();
+  // inverse of the upper block, rows bottom-up: 8 lanes per column split the inner sum (compensated
+  // partial dot products, then a fixed-order tree); a column's 8 lanes sit in one warp, so the rows
+  // are separated by warp barriers only.  Zero rows stay zero: their inverse rows are not used by
+  // the panel update since the corresponding R0 rows are zero too.
   const int col = threadIdx.x >> 3, part = threadIdx.x & 7;  // 32 columns x 8 parts
   for (int i = pb - 1; i >= 0; --i) {
-    ddv acc{0.0, 0.0};
+    double sd = 0.0, ed = 0.0;
     if (col < pb && col >= i)
-      for (int l = i + 1 + part; l <= col; l += 8) acc = dd_add(acc, dd_neg(dd_mul(a[i][l], x[l][col])));
+      for (int l = i + 1 + part; l <= col; l += 8) dd_dot_step(sd, ed, a[i][l], x[l][col], -1.0);
 #pragma unroll
     for (int o = 4; o > 0; o >>= 1) {
-      const ddv other{__shfl_xor_sync(0xffffffffu, acc.hi, o), __shfl_xor_sync(0xffffffffu, acc.lo, o)};
-      acc = dd_add(acc, other);
+      const double s2 = __shfl_xor_sync(0xffffffffu, sd, o), e2 = __shfl_xor_sync(0xffffffffu, ed, o);
+      const double sn = sd + s2, bb = sn - sd;
+      ed += e2 + ((sd - (sn - bb)) + (s2 - bb));
+      sd = sn;
     }
     if (part == 0 && col < pb && col >= i) {
+      ddv acc = dd_quick(sd, ed);
       if (col == i) acc = dd_add(acc, {1.0, 0.0});
       x[i][col] = dd_mul(acc, rinv[i]);  // (rinv = 0 for a zero row)
     }
-    __syncthreads();
+    __syncwarp();
   }
+  __syncthreads();
   for (int t = threadIdx.x; t < kDdNB * kDdNB; t += blockDim.x) {
     const int r = t / kDdNB, c = t % kDdNB;
     const bool in = r < pb && c < pb && c >= r;
