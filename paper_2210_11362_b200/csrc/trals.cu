@@ -1037,14 +1037,14 @@ struct ResOzWs {
   int64_t adig, aexp, amx, bdig, bexp, bmx, part, total;  // offsets in doubles
 };
 // 32-wide double-buffered n-tiles, 8 epilogue warps (c5, K = 400): 7.7 ms against 20 ms for the
-// DMMA residual.  The launch is bound by what one SM can take in from L2: 465 KB of digit tiles
-// per 128 x 32 output tile (7.3 us at ~64 GB/s per SM; 80 GB per launch -- the env kernels top out
-// at the same 9-10 TB/s).  Round-2 measurements on the way: the staged 4-warp epilogue 9.9 ms
+// DMMA residual.  Per 128 x 32 output tile it moves 465 KB of digit tiles (80 GB per launch,
+// 8.4 TB/s: less than half of what the L2 -> SM bulk-copy path delivers, tools/micro/l2_ingest.cu)
+// and issues 7 MMAs per 32 k, 224 down to 32 columns wide; the tensor pipe is 34 % active (narrow
+// MMAs + epilogue, not bandwidth).  Round-2 measurements on the way: the staged 4-warp epilogue 9.9 ms
 // (9.0 with its level combine stubbed out); the same epilogue without staging or barriers, X
 // loads issued before the accumulator wait, 10.2; with 8 epilogue warps 7.7; 64-wide
 // single-buffered tiles (less to take in, but the epilogue no longer overlaps the MMAs) 7.8; A
-// stages multicast over clusters of 2 / 4 n-tiles (2.5x fewer L2 reads, the same bytes into each
-// SM) 10.9 / 11.6 on the 4-warp form.
+// stages multicast over clusters of 2 / 4 n-tiles (2.5x fewer L2 reads) 10.9 / 11.6 on the 4-warp form.
 constexpr int kResBN = 32;
 ResOzWs residual_oz64_layout(int64_t pre, int64_t post, int64_t K) {
   using SC = trals::OzF64;
