@@ -467,9 +467,10 @@ class SweepEngine:
                 ks *= self.dims[j] if self.variant == "als" else min(self.dims[j], self.R(j) * self.R(j + 1))
         return ks < self.R(n) * self.R(n + 1)
 
-    def _factor(self, n):
+    def _factor(self, n, first=None):
         """S_n from the Gram chain and its Cholesky factor -- depends on cores only, so it runs on
-        the side stream as soon as core n-1 is final, overlapping the right-hand side of mode n."""
+        the side stream as soon as core n-1 is final, overlapping the right-hand side of mode n.
+        `first`: a side-stream step to run right after the fork (the Gram / per-core QR of core n-1)."""
         N = self.N
         rr = self.R(n) * self.R(n + 1)
         S = self.S[n]
@@ -477,6 +478,8 @@ class SweepEngine:
         rmax = max(self.ranks)
         self._side_ws(self.lib.trals_gemm_ws_elems(1, rmax ** 2, rmax ** 2, rmax ** 2))
         self.steps.append(Step("other", None, f"fork S{n}", kind="fork"))
+        if first is not None:
+            self.steps.append(first)
         if self.use_r0:
             # QR (solvers.py:422-424) / ALS (:337-339): S_n and R0 = chol(S_n) in double-double from the
             # transfer matrices of the R-tensors (the cores); then R0's inverse operands and the 1e-13
@@ -571,23 +574,33 @@ class SweepEngine:
                 L.check(self.lib.trals_core_relayout_f64(self.core_zt(n).data_ptr(), L.LAYOUT_ZT, ra,
                                                          self.hi - self.lo, rb, self.Gc_loc.data_ptr(),
                                                          L.LAYOUT_C, sp), "relayout")
-            self._gram(n, sp)
-        self._ws(self.lib.trals_gemm_ws_elems(1, rr, self.dims[n], rr))
         self.steps.append(Step("gramqr", refresh, f"refresh{n}"))
+        # The transfer matrix of the new core (NE: its Gram; QR / QRNE: the per-core Householder QR
+        # first) only feeds the Gram chains, so it runs on the side stream ahead of S_{n+1} and its
+        # factor, off the main stream's path to the next right-hand side (c5 QRNE: the 0.33 ms QR of
+        # every core was on the critical path).
+        self._side_ws(self.lib.trals_gemm_ws_elems(1, rr, self.dims[n], rr))
+        gram = Step("gramqr", lambda n=n: self._gram(n, self._sp(), side=True), f"gram{n}", stream="side")
         if n + 1 < N:
-            self._factor(n + 1)
+            self._factor(n + 1, first=gram)
+        else:
+            self.steps.append(Step("other", None, f"fork gram{n}", kind="fork"))
+            self.steps.append(gram)
+            self.steps.append(Step("gramqr", None, f"join gram{n}", kind="join"))
 
-    def _gram(self, n, sp):
+    def _gram(self, n, sp, side=False):
         """Transfer matrix of core n: from the core itself (NE, ring.py:188) or, for QR/QRNE, from the
-        R-tensor of its Householder QR (mode2_qr + lateral_gram of the R-tensor, solvers.py:417,468-470)."""
+        R-tensor of its Householder QR (mode2_qr + lateral_gram of the R-tensor, solvers.py:417,468-470).
+        side: called from a side-stream step (uses that stream's GEMM workspace)."""
         ra, i, rb = self.R(n), self.dims[n], self.R(n + 1)
+        gws = self.side_gws if side else self.gws
         if self.variant == "als":
             L.check(self.lib.trals_dd_transfer_f64(self.Gc[n].data_ptr(), ra, i, rb, self.Edd[n][0].data_ptr(),
                                                    self.Edd[n][1].data_ptr(), sp), "dd_transfer")
             return
         if not self.use_rqr:
             L.check(self.lib.trals_core_gram_f64(self.Gs[n].data_ptr(), ra, i, rb, self.E[n].data_ptr(),
-                                                 self.gws.data_ptr(), self.gws.numel(), sp), "core_gram")
+                                                 gws.data_ptr(), gws.numel(), sp), "core_gram")
             return
         k = min(i, ra * rb)
         L.check(self.lib.trals_core_qr_f64(self.Gt[n].data_ptr(), i, ra * rb, self.Rmat.data_ptr(),
@@ -602,7 +615,7 @@ class SweepEngine:
                                                    self.Edd[n][1].data_ptr(), sp), "dd_transfer")
             return
         L.check(self.lib.trals_core_gram_f64(self.Rslice.data_ptr(), ra, k, rb, self.E[n].data_ptr(),
-                                             self.gws.data_ptr(), self.gws.numel(), sp), "core_gram")
+                                             gws.data_ptr(), gws.numel(), sp), "core_gram")
 
     def _debug_check(self, n):
         """The reference's debug identities for block n (solvers.py:376-377 NE, 485-487 QRNE,

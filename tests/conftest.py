@@ -30,3 +30,21 @@ def rel(a, b):
     b = np.asarray(b, dtype=np.float64)
     nb = np.linalg.norm(b.ravel())
     return float(np.linalg.norm((a - b).ravel()) / (nb if nb > 0 else 1.0))
+
+
+@pytest.fixture(autouse=True, scope="module")
+def _release_plans():
+    """Drop the cached engines after every test module: the BASELINE-size plans keep tens of GB of
+    device buffers (operand planes, workspaces) alive otherwise."""
+    yield
+    try:
+        import gc
+
+        import torch
+        if torch.cuda.is_available():
+            from paper_2210_11362_b200.solvers import clear_plan_cache
+            clear_plan_cache()
+            gc.collect()
+            torch.cuda.empty_cache()
+    except Exception:
+        pass

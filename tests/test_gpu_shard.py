@@ -66,6 +66,15 @@ def _worker(rank, world, port, case, out_dir):
 @pytest.mark.timeout(900)
 @pytest.mark.parametrize("case", sorted(CASES))
 def test_two_rank_shard_on_gpu(case, tmp_path):
+    # the two ranks share this GPU with the parent: release the parent's cached plans first (the c5
+    # engines of the other test modules hold ~20 GB of operand planes each)
+    import gc
+
+    import torch
+    from paper_2210_11362_b200.solvers import clear_plan_cache
+    clear_plan_cache()
+    gc.collect()
+    torch.cuda.empty_cache()
     ctx = mp.get_context("spawn")
     port = 29700 + (abs(hash(case)) % 200)
     procs = [ctx.Process(target=_worker, args=(r, 2, port, case, str(tmp_path))) for r in range(2)]
