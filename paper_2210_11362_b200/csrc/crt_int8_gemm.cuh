@@ -565,7 +565,13 @@ __device__ __forceinline__ double crt_value(const uint32_t (&t)[kCrtMaxMod], int
     d = __ull2double_rn(top);
     sh = 64 - z;
   }
-  d = scalbn(d, sh + e2);
+  // d 2^(sh + e2) by two exact power-of-two factors (each exponent inside the normal range for
+  // |sh + e2| <= 2044; beyond that scalbn)
+  const int e = sh + e2, e1 = e >> 1, eh = e - e1;
+  if (static_cast<unsigned>(e1 + 1022) <= 2045u && static_cast<unsigned>(eh + 1022) <= 2045u)
+    d = (d * __hiloint2double((1023 + e1) << 20, 0)) * __hiloint2double((1023 + eh) << 20, 0);
+  else
+    d = scalbn(d, e);
   return neg ? -d : d;
 }
 
@@ -667,7 +673,7 @@ __global__ void __launch_bounds__(256, 3) crt_combine_kernel(const CrtOutArgs g)
       const int n = 4 * gq + q;
       uint32_t t[kCrtMaxMod];
 #pragma unroll
-      for (int i = 0; i < kCrtMaxMod; ++i) t[i] = (wv[i] >> (8 * q)) & 0xFFu;
+      for (int i = 0; i < kCrtMaxMod; ++i) t[i] = __byte_perm(wv[i], 0, 0x4440 + q);  // byte q of the word
       vals[rl * ldv + n] = n < g.N ? crt_value(t, -(sa + g.sb[n])) : 0.0;
     }
     gq += dgq;
@@ -677,9 +683,14 @@ __global__ void __launch_bounds__(256, 3) crt_combine_kernel(const CrtOutArgs g)
       ++rl;
     }
   }
+  __shared__ int64_t roff[kCrtRB];  // C offsets of the block's rows
+  const uint32_t M2 = static_cast<uint32_t>(g.cmap.M2), N2 = static_cast<uint32_t>(g.cmap.N2);
+  if (threadIdx.x < kCrtRB) {
+    const uint32_t mm = static_cast<uint32_t>(m0 + threadIdx.x);
+    roff[threadIdx.x] = static_cast<int64_t>(mm / M2) * g.cmap.sm1 + static_cast<int64_t>(mm % M2) * g.cmap.sm2;
+  }
   __syncthreads();
   const int rows = static_cast<int>((g.M - m0) < kCrtRB ? (g.M - m0) : kCrtRB);
-  const uint32_t M2 = static_cast<uint32_t>(g.cmap.M2), N2 = static_cast<uint32_t>(g.cmap.N2);
   // stores in the order of C's addresses; e -> (outer, row, inner) advanced incrementally (no
   // per-element divisions).  perm: for Env[r_hi][m][r_lo] each n2 plane gets one contiguous
   // rows x r_lo block (inner = n1 of perm values, outer = n2); else inner = n, outer unused.
@@ -690,10 +701,9 @@ __global__ void __launch_bounds__(256, 3) crt_combine_kernel(const CrtOutArgs g)
   const int d1 = blockDim.x % inner, dq = blockDim.x / inner;
   while (o2 < outer) {
     const int n = g.perm > 0 ? i1 * static_cast<int>(N2) + o2 : i1;
-    const uint32_t mm = static_cast<uint32_t>(m0 + rl), un = static_cast<uint32_t>(n);
+    const uint32_t un = static_cast<uint32_t>(n);
     const uint32_t nq = g.perm > 0 ? static_cast<uint32_t>(i1) : un / N2, nr = g.perm > 0 ? static_cast<uint32_t>(o2) : un % N2;
-    const int64_t off = static_cast<int64_t>(mm / M2) * g.cmap.sm1 + static_cast<int64_t>(mm % M2) * g.cmap.sm2 +
-                        static_cast<int64_t>(nq) * g.cmap.sn1 + static_cast<int64_t>(nr) * g.cmap.sn2;
+    const int64_t off = roff[rl] + static_cast<int64_t>(nq) * g.cmap.sn1 + static_cast<int64_t>(nr) * g.cmap.sn2;
     g.C[off] = vals[rl * ldv + n];
     i1 += d1;
     int carry = dq;
