@@ -260,7 +260,15 @@ class SweepEngine:
         self._bufs = []  # keep env buffers alive
         self._env_flops = []
         self.stats.x_passes_per_sweep = 0
-        self._factor(0)
+        # The sweep opens with the transfer matrix of the LAST core (solved at the end of the previous
+        # sweep; before the first sweep this recomputes what set_cores left): like every other core's
+        # it runs on the side stream ahead of the Gram chain that needs it (S_0), here under the first
+        # environment product instead of at the end of the previous sweep.
+        last = N - 1
+        rr_last = self.R(last) * self.R(last + 1)
+        self._side_ws(self.lib.trals_gemm_ws_elems(1, rr_last, self.dims[last], rr_last))
+        self._factor(0, first=Step("gramqr", lambda n=last: self._gram(n, self._sp(), side=True), f"gram{last}",
+                                   stream="side"))
         if N == 2:
             phases = [(0, 0), (1, 1)]
         else:
@@ -580,13 +588,10 @@ class SweepEngine:
         # factor, off the main stream's path to the next right-hand side (c5 QRNE: the 0.33 ms QR of
         # every core was on the critical path).
         self._side_ws(self.lib.trals_gemm_ws_elems(1, rr, self.dims[n], rr))
-        gram = Step("gramqr", lambda n=n: self._gram(n, self._sp(), side=True), f"gram{n}", stream="side")
         if n + 1 < N:
+            gram = Step("gramqr", lambda n=n: self._gram(n, self._sp(), side=True), f"gram{n}", stream="side")
             self._factor(n + 1, first=gram)
-        else:
-            self.steps.append(Step("other", None, f"fork gram{n}", kind="fork"))
-            self.steps.append(gram)
-            self.steps.append(Step("gramqr", None, f"join gram{n}", kind="join"))
+        # (the last core's transfer matrix is formed at the start of the next sweep, see _compile)
 
     def _gram(self, n, sp, side=False):
         """Transfer matrix of core n: from the core itself (NE, ring.py:188) or, for QR/QRNE, from the
