@@ -206,6 +206,11 @@ int trals_core_qr_f64(const double* d_Gzt, int I, int RR, double* d_R, double* d
  * matrix of core j; d_tmp holds two R^2 x R^2 buffers. */
 int trals_gram_chain_f64(int N, int n, const int32_t* ranks, const double* const* h_E,
                          double* d_S, double* d_tmp, double* d_ws, int64_t ws_elems, void* stream);
+/* The same chain in two parts (R = the largest rank in d_tmp's size): part 1 forms every product but
+ * the last and leaves the prefix in d_tmp, part 2 multiplies it by the last factor -- the transfer
+ * matrix of core n-1, the core solved just before block n -- into d_S; part 0 = both. */
+int trals_gram_chain_part_f64(int N, int n, const int32_t* ranks, const double* const* h_E,
+                              double* d_S, double* d_tmp, double* d_ws, int64_t ws_elems, int part, void* stream);
 
 /* spd_solve (linalg.py:55-81), factor step: symmetry check (1e-8 relative,
  * -> d_info[TRALS_INFO_ASYM]), symmetrise, upper Cholesky S = U^T U

@@ -43,6 +43,8 @@ _SIGNATURES = {
     "trals_core_qr_f64": (c_int, [_dp, c_int, c_int, _dp, _dp, c_int64, c_void_p]),
     "trals_gram_chain_f64": (c_int, [c_int, c_int, POINTER(c_int32), POINTER(c_void_p), _dp, _dp, _dp,
                                      c_int64, c_void_p]),
+    "trals_gram_chain_part_f64": (c_int, [c_int, c_int, POINTER(c_int32), POINTER(c_void_p), _dp, _dp, _dp,
+                                     c_int64, c_int, c_void_p]),
     "trals_cholesky_aux_elems": (c_int64, [c_int]),
     "trals_cholesky_f64": (c_int, [_dp, c_int, _dp, _dp, _dp, c_int, _dp, c_void_p]),
     "trals_chol_solve_ws_elems": (c_int64, [c_int64, c_int]),

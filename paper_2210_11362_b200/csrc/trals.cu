@@ -3136,10 +3136,12 @@ int trals_core_gram_f64(const double* Gs, int Ra, int64_t I, int Rb, double* E, 
   return gemm(Gs, 0, 1, RR, 1, RR, I, RR, Gs, RR, E, cm, 0, ws, ws_elems, static_cast<cudaStream_t>(stream));
 }
 
-int trals_gram_chain_f64(int N, int n, const int32_t* ranks, const double* const* E, double* S, double* tmp,
-                         double* ws, int64_t ws_elems, void* stream) {
-  if (N < 2 || n < 0 || n >= N || !ranks || !E || !S) return TRALS_ERR_ARG;
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
+// part: 0 = the whole chain; 1 = every product but the last (the prefix stays in tmp); 2 = the last
+// product from the prefix of an earlier part-1 call with the same arguments.  The last factor is the
+// transfer matrix of core n-1 -- the core solved just before block n -- so the prefix can be formed
+// while that core is still being solved.
+static int gram_chain_part(int N, int n, const int32_t* ranks, const double* const* E, double* S, double* tmp,
+                           double* ws, int64_t ws_elems, int part, cudaStream_t s) {
   // ring order n+1, ..., N-1, 0, ..., n-1 ; F = E_{n+1} E_{n+2} ... E_{n-1}
   std::vector<int> order;
   for (int j = n + 1; j < N; ++j) order.push_back(j);
@@ -3151,12 +3153,16 @@ int trals_gram_chain_f64(int N, int n, const int32_t* ranks, const double* const
   const int64_t rows = Rn1 * Rn1;  // F rows
   if (order.size() == 1) {
     // N == 2: S is a reshuffle of the single transfer matrix
+    if (part == 1) return TRALS_OK;
     const int64_t total = RR * RR;
     const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 4 * kSMs));
     reshuffle_kernel<<<blocks, 256, 0, s>>>(E[order[0]], rows, Rn * Rn, to_s, S);
     return launch_status();
   }
-  double* bufs[2] = {tmp, tmp + RR * RR};
+  // intermediate products: sized for the largest one, alternating halves of tmp
+  int64_t maxc = 0;
+  for (int j : order) maxc = std::max<int64_t>(maxc, static_cast<int64_t>(ranks[(j + 1) % N]) * ranks[(j + 1) % N]);
+  double* bufs[2] = {tmp, tmp + rows * maxc};
   const double* cur = E[order[0]];
   int64_t cols = static_cast<int64_t>(ranks[(order[0] + 1) % N]) * ranks[(order[0] + 1) % N];
   for (size_t t = 1; t < order.size(); ++t) {
@@ -3166,12 +3172,27 @@ int trals_gram_chain_f64(int N, int n, const int32_t* ranks, const double* const
     const bool last = (t + 1 == order.size());
     double* dst = last ? S : bufs[t & 1];
     const CMap cm = last ? to_s : rowmajor(ncols);
-    int st = gemm(cur, 0, cols, 1, 1, rows, cols, ncols, E[j], ncols, dst, cm, 0, ws, ws_elems, s);
-    if (st) return st;
+    const bool run = part == 0 || (part == 1 && !last) || (part == 2 && last);
+    if (run) {
+      int st = gemm(cur, 0, cols, 1, 1, rows, cols, ncols, E[j], ncols, dst, cm, 0, ws, ws_elems, s);
+      if (st) return st;
+    }
     cur = dst;
     cols = ncols;
   }
   return TRALS_OK;
+}
+
+int trals_gram_chain_f64(int N, int n, const int32_t* ranks, const double* const* E, double* S, double* tmp,
+                         double* ws, int64_t ws_elems, void* stream) {
+  if (N < 2 || n < 0 || n >= N || !ranks || !E || !S) return TRALS_ERR_ARG;
+  return gram_chain_part(N, n, ranks, E, S, tmp, ws, ws_elems, 0, static_cast<cudaStream_t>(stream));
+}
+
+int trals_gram_chain_part_f64(int N, int n, const int32_t* ranks, const double* const* E, double* S, double* tmp,
+                              double* ws, int64_t ws_elems, int part, void* stream) {
+  if (N < 2 || n < 0 || n >= N || !ranks || !E || !S || part < 0 || part > 2) return TRALS_ERR_ARG;
+  return gram_chain_part(N, n, ranks, E, S, tmp, ws, ws_elems, part, static_cast<cudaStream_t>(stream));
 }
 
 int64_t trals_cholesky_aux_elems(int m) {

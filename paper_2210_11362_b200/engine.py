@@ -257,6 +257,7 @@ class SweepEngine:
     def _compile(self):
         N = self.N
         self.steps: list[Step] = []
+        self._chain_prefix = set()  # blocks whose Gram-chain prefix is formed ahead (see _factor)
         self._bufs = []  # keep env buffers alive
         self._env_flops = []
         self.stats.x_passes_per_sweep = 0
@@ -264,16 +265,17 @@ class SweepEngine:
         # sweep; before the first sweep this recomputes what set_cores left): like every other core's
         # it runs on the side stream ahead of the Gram chain that needs it (S_0), here under the first
         # environment product instead of at the end of the previous sweep.
-        last = N - 1
-        rr_last = self.R(last) * self.R(last + 1)
-        self._side_ws(self.lib.trals_gemm_ws_elems(1, rr_last, self.dims[last], rr_last))
-        self._factor(0, first=Step("gramqr", lambda n=last: self._gram(n, self._sp(), side=True), f"gram{last}",
-                                   stream="side"))
         if N == 2:
             phases = [(0, 0), (1, 1)]
         else:
             h = (N + 1) // 2
             phases = [(0, h - 1), (h, N - 1)]
+        self._phase_first = {a for a, _ in phases}
+        last = N - 1
+        rr_last = self.R(last) * self.R(last + 1)
+        self._side_ws(self.lib.trals_gemm_ws_elems(1, rr_last, self.dims[last], rr_last))
+        self._factor(0, first=Step("gramqr", lambda n=last: self._gram(n, self._sp(), side=True), f"gram{last}",
+                                   stream="side"))
         for a, b in phases:
             self._phase(a, b)
         # error terms need the last mode's quantities (solvers.py:385-389)
@@ -507,18 +509,30 @@ class SweepEngine:
                 self.steps.append(Step("solve", tri, f"tri{n}", stream="side"))
             return
 
-        def gram_chain(n=n, S=S, ranks_a=ranks_a):
+        def gram_chain(n=n, S=S, ranks_a=ranks_a, part=0):
             E = L.ptr_array([e.data_ptr() for e in self.E])
-            L.check(self.lib.trals_gram_chain_f64(N, n, ranks_a, E, S.data_ptr(), self.chain_tmp.data_ptr(),
-                                                  self.side_gws.data_ptr(), self.side_gws.numel(), self._sp()),
-                    "gram_chain")
-        self.steps.append(Step("other", gram_chain, f"S{n}", stream="side"))
+            L.check(self.lib.trals_gram_chain_part_f64(N, n, ranks_a, E, S.data_ptr(), self.chain_tmp.data_ptr(),
+                                                       self.side_gws.data_ptr(), self.side_gws.numel(), part,
+                                                       self._sp()), "gram_chain")
+        # every factor of S_n but the last (core n-1's) was ready before core n-1 was solved: when the
+        # previous block's factorisation left the prefix behind (below), only the last product remains
+        hoisted = n in self._chain_prefix
+        self.steps.append(Step("other", lambda f=gram_chain, p=2 if hoisted else 0: f(part=p), f"S{n}", stream="side"))
 
         def factor(S=S, rr=rr):
             L.check(self.lib.trals_cholesky_f64(S.data_ptr(), rr, self.U.data_ptr(), self.Lo.data_ptr(),
                                                 self.chol_aux.data_ptr(), 0, self.info.data_ptr(),
                                                 self._sp()), "cholesky")
         self.steps.append(Step("solve", factor, f"chol{n}", stream="side"))
+        if N >= 4 and n + 1 < N and n in self._phase_first and (n + 1) not in self._phase_first:
+            # prefix of the next block's Gram chain (cores n+2, ..., n-1: none of them core n), on the
+            # side stream behind this factorisation and ahead of core n's solve.  Only behind the first
+            # block of a phase: its factorisation hides under the environment product, so the main
+            # stream's join does not wait for the prefix, and the next block's chain is the exposed one
+            nxt = n + 1
+            self.steps.append(Step("other", lambda f=gram_chain, nn=nxt, SS=self.S[nxt]: f(n=nn, S=SS, part=1),
+                                   f"S{nxt} prefix", stream="side"))
+            self._chain_prefix.add(nxt)
 
     def _solve(self, n):
         """Steps for one block update once M_n is complete (local rows)."""

@@ -292,6 +292,13 @@ class FakeTrals:
         _arr(R, r.size)[:] = r.ravel()
         return 0
 
+    def trals_gram_chain_part_f64(self, N, n, ranks, E, S, tmp, ws, ws_elems, part, stream):
+        """part 1 (prefix) is a no-op in this model; part 2 / 0 form the whole chain."""
+        if part == 1:
+            self._count("gram_chain_prefix")
+            return 0
+        return self.trals_gram_chain_f64(N, n, ranks, E, S, tmp, ws, ws_elems, stream)
+
     def trals_gram_chain_f64(self, N, n, ranks, E, S, tmp, ws, ws_elems, stream):
         self._count("gram_chain")
         r = _vals(ranks, N)
